@@ -1,0 +1,231 @@
+"""Encrypted circuits of the frozen layers, oracle side (TEST INFRASTRUCTURE ONLY).
+
+Follows, in the paper's order and notation:
+  * Dense layer, BSGS diagonal method, Eq. 1:
+        M x = sum_{k<t2} rot_{k t1}( sum_{j<t1} diag'_{k t1 + j}(M) o rot_j(x) ),
+        diag'_i(M) = rot_{-floor(i/t1) t1}(diag_i(M)),  t = t1 t2,  zero-padded to t x t.
+    Input packed duplicated [x || x] ("twice the number of neurons").  Readings R4-R8.
+  * Square activation (BASELINE.json cfg4) and the cubic ReLU approximation, Eq. 2:
+        ReLU_approx(z) = -0.0061728 z^3 + 0.092593 z^2 + 0.59259 z + 0.49383   (schedule R23).
+  * Replicate y + rot_{-t}(y) restoring the duplicated layout (R-replicate).
+  * The float64 plaintext reference forward these must match after decryption (north_star, 1e-3).
+Ring arithmetic is the C oracle's (`Context`); nothing here touches residues except through it.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import encoding
+
+RELU_APPROX = (-0.0061728, 0.092593, 0.59259, 0.49383)   # c3, c2, c1, c0  (Eq. 2)
+
+
+@dataclass
+class Ct:
+    data: np.ndarray      # [2 (or 3)][level+1][N] NTT-domain residues
+    scale: float
+
+    @property
+    def level(self):
+        return self.data.shape[1] - 1
+
+
+def bsgs_split(rows: int, cols: int):
+    """t = max(rows, cols) (P:L96 zero padding); t1 = 2^ceil(ceil(log2 t)/2); t padded to t1 | t (R5)."""
+    t = max(rows, cols)
+    lg = max(0, math.ceil(math.log2(t)))
+    t1 = 1 << math.ceil(lg / 2)
+    t = -(-t // t1) * t1
+    return t, t1, t // t1
+
+
+def diagonals(W: np.ndarray):
+    """diag_i(M)[s] = Mpad[s][(s + i) mod t]  for i < t."""
+    rows, cols = W.shape
+    t, t1, t2 = bsgs_split(rows, cols)
+    Mp = np.zeros((t, t))
+    Mp[:rows, :cols] = W
+    s = np.arange(t)
+    return np.stack([Mp[s, (s + i) % t] for i in range(t)]), (t, t1, t2)
+
+
+def diag_prime_slots(W: np.ndarray, n_slots: int):
+    """diag'_{k t1 + j} = rot_{-k t1}(diag_{k t1 + j}) as full slot vectors (zero-filled, R4)."""
+    D, (t, t1, t2) = diagonals(W)
+    if 2 * t > n_slots:
+        raise ValueError("2t exceeds the slot count")
+    out = np.zeros((t, n_slots))
+    for i in range(t):
+        k = i // t1
+        out[i, k * t1: k * t1 + t] = D[i]
+    return out, (t, t1, t2)
+
+
+@dataclass
+class EncodedLayer:
+    """Shared encoded plaintexts of one dense layer (integer coefficients, R8)."""
+    rows: int
+    cols: int
+    t: int
+    t1: int
+    t2: int
+    level: int                  # level of the input ciphertext
+    pt_scale: float             # Delta_w = q_level (R8)
+    bias_scale: float           # = input scale (exact after rescale)
+    diag_coeffs: np.ndarray     # [t][N] int64
+    bias_coeffs: np.ndarray     # [N] int64
+
+
+def encode_layer(ctx, W, b, level: int, in_scale: float) -> EncodedLayer:
+    W = np.asarray(W, dtype=np.float64)
+    rows, cols = W.shape
+    slots, (t, t1, t2) = diag_prime_slots(W, ctx.n // 2)
+    q_l = float(ctx.primes[level])
+    coeffs = np.stack([encoding.encode(slots[i], q_l, ctx.n) for i in range(t)])
+    bias = np.zeros(ctx.n // 2)
+    if b is not None:
+        bias[:rows] = b
+    bcoef = encoding.encode(bias, in_scale, ctx.n)
+    return EncodedLayer(rows, cols, t, t1, t2, level, q_l, in_scale, coeffs, bcoef)
+
+
+def rotation_steps_for(layers_shapes):
+    """Every Galois step the forward needs: baby 1..t1-1, giant k t1, replicate -t (R5)."""
+    steps = set()
+    for li, (rows, cols) in enumerate(layers_shapes):
+        t, t1, t2 = bsgs_split(rows, cols)
+        steps.update(range(1, t1))
+        steps.update(k * t1 for k in range(1, t2))
+        if li > 0:
+            steps.add(-t)
+    return sorted(steps)
+
+
+class OpCount:
+    def __init__(self):
+        self.rot = 0
+        self.mul_plain = 0
+        self.add = 0
+
+
+def matvec(ctx, ct: Ct, layer: EncodedLayer, ops: OpCount | None = None) -> Ct:
+    """Eq. 1 then one rescale (R7) then + bias (R-bias).  t1+t2-2 rotations, t pt-ct mults."""
+    l = ct.level
+    assert layer.level == l, "layer encoded for another level"
+    pts = [ctx.plain(layer.diag_coeffs[i], l) for i in range(layer.t)]
+    baby = [ct.data] + [ctx.rotate(ct.data, j) for j in range(1, layer.t1)]
+    if ops:
+        ops.rot += layer.t1 - 1
+    y = None
+    for k in range(layer.t2):
+        w = None
+        for j in range(layer.t1):
+            term = ctx.mul_plain(baby[j], pts[k * layer.t1 + j])
+            w = term if w is None else ctx.add(w, term)
+            if ops:
+                ops.mul_plain += 1
+        if k > 0:
+            w = ctx.rotate(w, k * layer.t1)
+            if ops:
+                ops.rot += 1
+        y = w if y is None else ctx.add(y, w)
+    y = ctx.rescale(y)
+    out_scale = ct.scale * layer.pt_scale / float(ctx.primes[l])
+    y = ctx.add_plain(y, ctx.plain(layer.bias_coeffs, l - 1))
+    return Ct(y, out_scale)
+
+
+def square(ctx, z: Ct) -> Ct:
+    """rescale(relin(z (x) z)): depth 1 (BASELINE cfg4 activation)."""
+    l = z.level
+    y = ctx.rescale(ctx.relinearize(ctx.tensor(z.data, z.data)))
+    return Ct(y, z.scale * z.scale / float(ctx.primes[l]))
+
+
+def cubic(ctx, z: Ct, coeffs=RELU_APPROX) -> Ct:
+    """Eq. 2 at depth 2, schedule R23:
+       z2 = rescale(relin(z (x) z));  a = rescale(z o [c3]_{q_l}) + [c2]_S;
+       h = rescale(relin(z2 (x) a));  g = drop(rescale(z o [c1]_{S3 q_l / S})) + [c0]_{S3};  out = h + g."""
+    c3, c2, c1, c0 = coeffs
+    l = z.level
+    S = z.scale
+    ql, ql1 = float(ctx.primes[l]), float(ctx.primes[l - 1])
+    n = ctx.n
+    z2 = ctx.rescale(ctx.relinearize(ctx.tensor(z.data, z.data)))               # l-1, S^2/ql
+    a = ctx.rescale(ctx.mul_plain(z.data, ctx.plain(encoding.encode_const(c3, ql, n), l)))
+    a = ctx.add_plain(a, ctx.plain(encoding.encode_const(c2, S, n), l - 1))     # l-1, S
+    h = ctx.rescale(ctx.relinearize(ctx.tensor(z2, a)))                         # l-2, S3
+    S3 = (S * S / ql) * S / ql1
+    g = ctx.rescale(ctx.mul_plain(z.data, ctx.plain(encoding.encode_const(c1, S3 * ql / S, n), l)))
+    g = ctx.drop_level(g, l - 2)
+    g = ctx.add_plain(g, ctx.plain(encoding.encode_const(c0, S3, n), l - 2))
+    return Ct(ctx.add(h, g), S3)
+
+
+def replicate(ctx, y: Ct, t: int) -> Ct:
+    """y + rot_{-t}(y): [y | 0] -> [y | y] on slots [0, 2t) (P:L116 duplicated layout)."""
+    return Ct(ctx.add(y.data, ctx.rotate(y.data, -t)), y.scale)
+
+
+def forward(ctx, ct: Ct, layers, activation: str = "square", ops: OpCount | None = None) -> Ct:
+    """dense_1 -> act -> replicate -> dense_2 -> ... (P:L118 frozen stack, BASELINE cfg4)."""
+    for li, layer in enumerate(layers):
+        if li > 0:
+            ct = replicate(ctx, ct, layer.t)
+            if ops:
+                ops.rot += 1
+        ct = matvec(ctx, ct, layer, ops)
+        if li < len(layers) - 1:
+            if activation == "square":
+                ct = square(ctx, ct)
+            elif activation == "cubic":
+                ct = cubic(ctx, ct)
+            elif activation != "none":
+                raise ValueError(activation)
+    return ct
+
+
+def encode_model(ctx, Ws, bs, level: int, scale: float, activation: str):
+    """Encode every layer at the level/scale its input will have (R8 scale bookkeeping)."""
+    layers = []
+    s = scale
+    l = level
+    for li, (W, b) in enumerate(zip(Ws, bs)):
+        lay = encode_layer(ctx, W, b, l, s)
+        layers.append(lay)
+        l -= 1                                   # one rescale in the dense layer; scale unchanged
+        if li < len(Ws) - 1:
+            if activation == "square":
+                s = s * s / float(ctx.primes[l])
+                l -= 1
+            elif activation == "cubic":
+                ql, ql1 = float(ctx.primes[l]), float(ctx.primes[l - 1])
+                s = (s * s / ql) * s / ql1
+                l -= 2
+    return layers
+
+
+def plain_forward(x, Ws, bs, activation: str = "square"):
+    """float64 reference (north_star): y1 = W1 x + b1; z = act(y1); y = W2 z + b2 ..."""
+    y = np.asarray(x, dtype=np.float64)
+    for li, (W, b) in enumerate(zip(Ws, bs)):
+        y = W @ y + b
+        if li < len(Ws) - 1:
+            if activation == "square":
+                y = y * y
+            elif activation == "cubic":
+                c3, c2, c1, c0 = RELU_APPROX
+                y = ((c3 * y + c2) * y + c1) * y + c0
+    return y
+
+
+def pack_input(x, t: int, n_slots: int) -> np.ndarray:
+    """[x || x] on slots [0, 2t), zeros elsewhere."""
+    v = np.zeros(n_slots)
+    x = np.asarray(x, dtype=np.float64)
+    v[: x.size] = x
+    v[t: t + x.size] = x
+    return v
