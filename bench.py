@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 CKKS encrypted-forward hot path (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" = one pass of the whole hot path (all SURVEY 8(a) rows) over one batch: BASELINE cfg5,
+1024 independent 512-d inputs, each in its own N=16384 ciphertext (8 limbs + special prime),
+through dense 512->256, square, replicate, dense 256->128, as one batched launch sequence.
+Inputs are resident in HBM (2 GiB of ciphertexts, larger than the 126 MB L2, so no L2 flush is
+needed between steps).  N>1 (torchrun): independent replicas, one batch per rank ("weak").
+
+Prints ONE JSON line (rank 0).  See DESIGN.md section 7 for every definition used here.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "encrypted forward passes/sec; NTT & key-switch HBM GB/s vs 8 TB/s peak"
+UNIT = "forwards/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--batch", type=int, default=None, help="ciphertexts per step (default cfg5: 1024)")
+    p.add_argument("--max-batch", type=int, default=256, help="ciphertexts per internal launch sequence")
+    p.add_argument("--no-extras", action="store_true", help="skip the cfg2/cfg3 sub-benchmarks")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------------------------ distributed
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def dist_init(backend):
+    import torch.distributed as dist
+    rank, local, world = dist_env()
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend)
+    return rank, local, world
+
+
+def barrier():
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+
+
+def max_over_ranks(x, device):
+    import torch
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+    return float(x)
+
+
+# ------------------------------------------------------------------------------------ clocks
+class Clocks:
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) == 6 and parts[0].isdigit():
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [int(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------------ helpers
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def profiled_traffic(kernel):
+    """dram bytes per launch of `kernel` from the committed ncu summary (profiles/), else None."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+def build_forward(G, cfg, B, max_batch, device):
+    """Product path only: library encoder, device keygen/encryption."""
+    import synthetic as S
+    shapes = list(cfg.layers)
+    steps = G.model_steps(shapes)
+    ctx = G.Context(cfg.log_n, cfg.data_bits, cfg.special_bits, key_seed=cfg.key_seed, rot_steps=steps,
+                    max_batch=max_batch, device=device)
+    Delta = 2.0 ** cfg.log2_scale
+    levels, scales, _ = ctx.model_plan(shapes, G.ACT_SQUARE, ctx.top_level, Delta)
+    prob = S.dense_problem(cfg, batch=B)
+    layers = [G.Layer(ctx, r, c, levels[i], W=prob["W"][i], bias=prob["b"][i], in_scale=scales[i])
+              for i, (r, c) in enumerate(shapes)]
+    model = G.Model(ctx, layers, G.ACT_SQUARE)
+    t0 = G.bsgs_plan(*shapes[0])[0]
+    slots = ctx.n // 2
+    ms = np.empty((B, ctx.n), dtype=np.int64)
+    v = np.zeros(slots)
+    for b in range(B):
+        v[:] = 0
+        x = prob["x"][b]
+        v[: x.size] = x
+        v[t0: t0 + x.size] = x                      # duplicated layout [x || x]
+        ms[b] = ctx.encode(v, Delta)
+    ct = ctx.encrypt(ms, cfg.enc_seed, 0, Delta)
+    return ctx, model, ct, prob
+
+
+# ------------------------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    from paper_2205_11935_b200 import ckks as G
+    import synthetic as S
+
+    rank, local, world = dist_init("nccl")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    cfg = S.CFG5
+    B = args.batch or cfg.batch
+    ctx, model, ct, prob = build_forward(G, cfg, B, args.max_batch, device)
+    out = ctx.empty_ct(B, model.final_level)
+    work = torch.empty(model.work_bytes(B), dtype=torch.uint8, device=device)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(max(3, args.warmup)):
+        model.forward(ct, out, work)
+    torch.cuda.synchronize()
+
+    ctx.probe(G.PROBE_MODUP)
+    clocks = Clocks(local)
+    clocks.start()
+    l0 = ctx.launches()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        model.forward(ct, out, work)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_local = e0.elapsed_time(e1)
+    launches = ctx.launches() - l0
+    clk = clocks.stop()
+    mod_ms, mod_n, mod_bytes = ctx.probe_read()
+    ctx.probe(G.PROBE_OFF)
+    ms = max_over_ranks(ms_local, device)
+    value = B * world * args.steps / (ms / 1e3)
+
+    peak, peak_src = measured_peaks()
+    achieved = mod_bytes / (mod_ms / 1e3) / 1e9 if mod_ms > 0 else 0.0
+    trafic = profiled_traffic("k_ks_modup")
+    roofline = {"bound": "hbm", "kernel": "k_ks_modup (key-switch ModUp NTT)", "achieved": round(achieved, 1),
+                "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": trafic, "launches_probed": mod_n, "kernel_ms_total": round(mod_ms, 3),
+                "share_of_step": round(mod_ms / ms_local, 4) if ms_local else None,
+                "vs_8TBs": round(achieved / 8000.0, 4)}
+
+    result = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+              "warmup": max(3, args.warmup), "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+              "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded; shapes of BASELINE cfg5)",
+              "config": {"workload": cfg.name, "batch_per_gpu": B, "N": ctx.n, "limbs": ctx.n_data,
+                         "special_primes": ctx.n_special, "dnum": ctx.n_data, "layers": [list(s) for s in cfg.layers],
+                         "activation": "square", "max_batch": args.max_batch,
+                         "l2": "inputs (2 GiB of ciphertexts) larger than L2; no flush",
+                         "parallelism": f"replicas x{world}"},
+              "gpu_launches": launches, "roofline": roofline}
+    if clk:
+        result["clocks"] = clk
+
+    # ---- e2e through the C-ABI with host buffers (H2D + D2H inside the timed region)
+    if not args.no_e2e:
+        nl_in = ct.level + 1
+        h_in = torch.empty((B, 2, nl_in, ctx.n), dtype=torch.int64, pin_memory=True)
+        h_in.copy_(ct.data)
+        h_out = torch.empty((B, 2, model.final_level + 1, ctx.n), dtype=torch.int64, pin_memory=True)
+        ework = work                                                     # sized for the host path too
+        model.forward_host(h_in, ct.level, ct.scale, h_out, ework)       # warm
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            model.forward_host(h_in, ct.level, ct.scale, h_out, ework)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = max_over_ranks(f0.elapsed_time(f1), device)
+        # same bits as the device-resident run
+        assert torch.equal(h_out, out.data.cpu()), "e2e output differs from the device-resident run"
+        result["e2e"] = {"value": round(B * world * args.steps / (ems / 1e3), 3), "unit": UNIT,
+                         "h2d_bytes_per_step": int(h_in.numel() * 8), "d2h_bytes_per_step": int(h_out.numel() * 8),
+                         "wall_s": round(time.perf_counter() - t0, 3)}
+        del h_in, h_out
+
+    del work, out, ct, model
+    torch.cuda.empty_cache()
+
+    # ---- sub-benchmarks: cfg2 batched NTT, cfg3 rotation/key-switch batch (same kernels)
+    if not args.no_extras:
+        result["ntt_microbench"] = bench_ntt(G, S, device, args)
+        result["keyswitch"] = bench_keyswitch(G, S, device, args)
+        for k in ("ntt_microbench", "keyswitch"):
+            result[k]["frac_of_measured_hbm"] = round(result[k]["GBps"] / peak, 4)
+            result[k]["frac_of_8TBs"] = round(result[k]["GBps"] / 8000.0, 4)
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(S)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    barrier()
+
+
+def bench_ntt(G, S, device, args):
+    import torch
+    cfg = S.CFG2
+    ctx = G.Context(cfg.log_n, cfg.data_bits, (), key_seed=cfg.key_seed, want_relin=False, max_batch=1, device=device)
+    gen = torch.Generator(device=device).manual_seed(cfg.data_seed)
+    x = torch.empty((cfg.batch, len(cfg.data_bits), ctx.n), dtype=torch.int64, device=device)
+    for i, q in enumerate(ctx.primes):
+        x[:, i].random_(0, q, generator=gen)
+    for _ in range(3):
+        ctx.ntt_fwd(x)
+        ctx.ntt_inv(x)
+    torch.cuda.synchronize()
+    res = {}
+    for name, fn in (("fwd", ctx.ntt_fwd), ("inv", ctx.ntt_inv)):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(3, args.steps)
+        e0.record()
+        for _ in range(reps):
+            fn(x)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        byts = 2.0 * x.numel() * 8
+        res[name] = {"ms": round(ms, 4), "GBps": round(byts / (ms / 1e3) / 1e9, 1),
+                     "limb_transforms_per_s": round(x.shape[0] * x.shape[1] / (ms / 1e3), 1)}
+    gbps = 2 * res["fwd"]["GBps"] * res["inv"]["GBps"] / (res["fwd"]["GBps"] + res["inv"]["GBps"])
+    return {"workload": cfg.name, "shape": list(x.shape), "GBps": round(gbps, 1), **res,
+            "bytes_def": "2 * 8 * N * limbs * batch per direction (read + write once)"}
+
+
+def bench_keyswitch(G, S, device, args):
+    import torch
+    cfg = S.CFG3
+    ctx = G.Context(cfg.log_n, cfg.data_bits, cfg.special_bits, key_seed=cfg.key_seed, rot_steps=cfg.rot_steps,
+                    want_relin=False, max_batch=cfg.batch, device=device)
+    gen = torch.Generator(device=device).manual_seed(cfg.data_seed)
+    x = torch.empty((cfg.batch, 2, ctx.n_data, ctx.n), dtype=torch.int64, device=device)
+    for i in range(ctx.n_data):
+        x[:, :, i].random_(0, ctx.primes[i], generator=gen)
+    ct = G.Ciphertext(x, ctx.top_level, 2.0 ** 40)
+    out = ctx.empty_ct(cfg.batch, ctx.top_level)
+    for st in cfg.rot_steps[:3]:
+        ctx.rotate(ct, st, out)
+    torch.cuda.synchronize()
+    reps = max(2, args.steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        for st in cfg.rot_steps:
+            ctx.rotate(ct, st, out)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    L, n = ctx.n_data, ctx.n
+    nrot = cfg.batch * len(cfg.rot_steps)
+    evk = L * 2 * (L + 1) * n * 8
+    byts = nrot * (4 * L * n * 8) + len(cfg.rot_steps) * evk
+    return {"workload": cfg.name, "rotations_per_s": round(nrot / (ms / 1e3), 1), "ms_per_batch_of_9_steps": round(ms, 3),
+            "GBps": round(byts / (ms / 1e3) / 1e9, 1),
+            "bytes_def": "2304 * (4 L N 8) + 9 * evk_bytes per batch (ct in+out, keys once)"}
+
+
+# ------------------------------------------------------------------------------------ oracle arms
+def oracle_forward_setup(S):
+    import oracle
+    from oracle import circuits as OC
+    from oracle import encoding as OE
+    cfg = S.CFG5
+    o = oracle.Context(cfg.log_n, cfg.data_bits, cfg.special_bits)
+    o.keygen(cfg.key_seed, OC.rotation_steps_for(cfg.layers))
+    prob = S.dense_problem(cfg, batch=4)
+    Delta = 2.0 ** cfg.log2_scale
+    layers = OC.encode_model(o, prob["W"], prob["b"], o.top_level, Delta, "square")
+
+    def one(i):
+        m = OE.encode(OC.pack_input(prob["x"][i % 4], layers[0].t, o.n // 2), Delta, o.n)
+        ct = OC.Ct(o.encrypt(m, cfg.enc_seed, i), Delta)
+        t0 = time.perf_counter()
+        OC.forward(o, ct, layers, "square")
+        return time.perf_counter() - t0
+
+    return one
+
+
+def cpu_baseline(S):
+    one = oracle_forward_setup(S)
+    dt = one(0)
+    return {"value": round(1.0 / dt, 5), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": "1 ciphertext of the cfg5 workload (cfg4 network) through the single-threaded C oracle "
+                      f"({dt:.1f} s); keygen/encode/encrypt untimed",
+            "host_cores_available": os.cpu_count()}
+
+
+def run_reference(args):
+    rank, local, world = dist_env()
+    if world > 1:
+        try:
+            dist_init("gloo")
+        except Exception:
+            pass
+        if rank != 0:
+            barrier()
+            return
+    import synthetic as S
+    one = oracle_forward_setup(S)
+    for i in range(max(1, min(args.warmup, 1))):
+        one(i)
+    times = [one(100 + i) for i in range(args.steps)]
+    tot = sum(times)
+    value = args.steps / tot
+    res = {"impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 1),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+           "data": "synthetic (seeded; shapes of BASELINE cfg5)",
+           "config": {"workload": S.CFG5.name, "batch_per_step": 1, "N": S.CFG5.n, "limbs": len(S.CFG5.data_bits),
+                      "note": "each step = 1 ciphertext of the cfg5 batch (bounded sample) through the CPU oracle"},
+           "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": f"{args.steps} ciphertexts of cfg5, single-threaded C oracle"},
+           "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "gpu_launches": 0}
+    print(json.dumps(res), flush=True)
+    if world > 1:
+        barrier()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,198 @@
+/*
+ * ckks.h -- C-ABI of the B200 CKKS encrypted-dense-layer library (libckks_b200.so).
+ *
+ * What it computes: the server side of CryptoTL (arXiv 2205.11935): dense layers with plaintext
+ * weights applied to a CKKS ciphertext by the baby-step/giant-step diagonal method (PAPER.md L92-96,
+ * Eq. 1), the polynomial activation (square, or Eq. 2 at PAPER.md L112) and rescaling (PAPER.md
+ * L85), over an RNS ring Z_Q[X]/(X^N + 1).  CKKS internals the paper leaves to SEAL
+ * follow the readings R1-R24 of DESIGN.md section 3.
+ *
+ * Conventions shared by every call
+ *   - All device memory is owned by the caller (e.g. torch tensors).  The context BORROWS the
+ *     tables/keys/workspace buffers passed to ckks_ctx_create; layers and models borrow theirs.
+ *     Nothing is allocated on the device by the library after creation.
+ *   - Ciphertext layout: `data` = device pointer to [batch][n_comp][level+1][N] uint64 words,
+ *     NTT (evaluation) domain, residue of limb i modulo q_i in canonical range [0, q_i).
+ *     n_comp is 2 (or 3 between ckks_mul and ckks_relinearize).
+ *   - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *     Preconditions (level, scale, key presence, shapes) are checked on the host before launch.
+ *   - Return value: CKKS_OK (0) or a negative ckks_status; ckks_last_error() gives a message
+ *     (thread-local).  On error nothing has been launched.
+ *   - There is no CPU fallback: without a CUDA device every compute call returns CKKS_E_CUDA.
+ */
+#ifndef CKKS_B200_H
+#define CKKS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CKKS_OK = 0,
+    CKKS_E_PARAM = -1,  /* bad N / chain / scale / argument            */
+    CKKS_E_LEVEL = -2,  /* depth exhausted: rescale at level 0          */
+    CKKS_E_NOKEY = -3,  /* rotation step without a Galois key, or no relin key       */
+    CKKS_E_SCALE = -4,  /* scales of an addition differ by more than 2^-40 relative   */
+    CKKS_E_DOMAIN = -5, /* representation misuse                                              */
+    CKKS_E_SHAPE = -6,  /* level / batch / component mismatch, aliasing not allowed            */
+    CKKS_E_CUDA = -7,   /* CUDA error or no device                                             */
+    CKKS_E_SIZE = -8    /* caller buffer too small / batch above the context's max_batch       */
+} ckks_status;
+
+typedef struct ckks_ctx ckks_ctx;
+typedef struct ckks_layer ckks_layer;
+typedef struct ckks_model ckks_model;
+
+/* Scheme parameters (R1, R13-R15).  Primes: for each entry of prime_bits in order, the largest
+ * unused prime q < 2^bits with q = 1 mod 2N; the first n_data are q_0..q_{L-1}, then the special
+ * prime P (n_special = 1) used by key switching.  Keys are generated on the device from key_seed. */
+typedef struct {
+    uint32_t log_n;             /* 10..14 (N = 1024 .. 16384; one limb must fit shared memory)     */
+    uint32_t n_data;            /* L >= 1 data primes                                              */
+    uint32_t n_special;         /* 0 (NTT-only context) or 1                                       */
+    const uint32_t* prime_bits; /* n_data + n_special entries, each in [log_n + 2, 61]             */
+    double sigma;               /* discrete Gaussian error parameter, 3.2 (R13)                    */
+    uint64_t key_seed;          /* seed of the counter-based PRNG for s, pk, relin and Galois keys */
+    const int32_t* rot_steps;   /* rotation steps needing Galois keys (left rotation by step)      */
+    uint32_t n_rot_steps;
+    int32_t want_relin;         /* generate the relinearisation key (s^2 -> s)                     */
+    uint32_t max_batch;         /* ciphertexts per internal launch sequence (workspace sizing)     */
+} ckks_params;
+
+/* Host-readable context description. */
+typedef struct {
+    uint32_t log_n, n, n_data, n_special, n_keys;
+    uint64_t primes[16];        /* q_0..q_{L-1}, then P                                            */
+    uint64_t psi[16];           /* minimal primitive 2N-th root used by the NTT (R2)               */
+} ckks_info;
+
+typedef struct {
+    uint64_t* data;  /* device [batch][n_comp][level+1][N]                                         */
+    uint32_t batch;
+    uint32_t n_comp;
+    uint32_t level;  /* limbs = level + 1                                                          */
+    double scale;    /* tracked scale (real)                                                       */
+} ckks_ct;
+
+const char* ckks_last_error(void);
+
+/* ---- context (setup; not on the hot path) -------------------------------------------------- */
+/* Byte sizes of the three device buffers ckks_ctx_create needs (each 256-byte aligned). */
+ckks_status ckks_ctx_sizes(const ckks_params* p, size_t* table_bytes, size_t* key_bytes, size_t* work_bytes);
+/* Builds primes/tables on the host, uploads them, and generates s, pk, relin key and the Galois
+ * keys on the device (seeded; synchronises `stream` before returning).  Borrows the buffers. */
+ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, void* d_work, void* stream,
+                            ckks_ctx** out);
+void ckks_ctx_destroy(ckks_ctx* ctx);
+ckks_status ckks_ctx_info(const ckks_ctx* ctx, ckks_info* out);
+/* Number of kernels this context has launched so far (bench accounting). */
+uint64_t ckks_launch_count(const ckks_ctx* ctx);
+/* Measurement probe: from now on record a CUDA event pair, on the launching stream, around every
+ * launch of one kernel class: kind 1 = key-switch ModUp NTT kernel, 2 = a whole key switch
+ * (5 kernels), 3 = batched NTT (ckks_ntt_fwd/inv); 0 = off.  Resets the accumulated record.
+ * ckks_probe_read synchronises on the last event and returns the summed device time (ms) and the
+ * number of probed launches, and (alg_bytes, may be NULL) the algorithmic HBM bytes of those launches
+ * as defined in DESIGN.md section 7.  Costs two event records per probed launch; off by default. */
+ckks_status ckks_probe_enable(ckks_ctx* ctx, int32_t kind);
+ckks_status ckks_probe_read(ckks_ctx* ctx, double* total_ms, uint64_t* launches, double* alg_bytes);
+
+/* ---- ring: batched negacyclic NTT ---------------------------------------- */
+/* In place over d = device [batch][limbs][N]; limb i is reduced modulo prime i.  Forward maps
+ * coefficients (any residues in [0, q_i)) to NTT(a)[k] = sum_j a_j psi^{(2 brev(k)+1) j}
+ * (bit-reversed order, R2); inverse is its exact inverse.  limbs <= n_data + n_special. */
+ckks_status ckks_ntt_fwd(ckks_ctx* ctx, uint64_t* d, uint32_t batch, uint32_t limbs, void* stream);
+ckks_status ckks_ntt_inv(ckks_ctx* ctx, uint64_t* d, uint32_t batch, uint32_t limbs, void* stream);
+
+/* ---- CKKS evaluator (rows a3-a5, a8, a10) --------------------------------------------------- */
+/* Left rotation of every slot vector by `step`: (sigma_g(c0), 0) +
+ * KS(sigma_g(c1); gk_g), g = 5^(step mod N/2) mod 2N, non-hoisted (R11).  out must not alias in;
+ * out->data is written, its level/scale/batch/n_comp are set.  CKKS_E_NOKEY if no key for g. */
+ckks_status ckks_rotate(ckks_ctx* ctx, const ckks_ct* in, int32_t step, ckks_ct* out, void* stream);
+/* Tensor product (a0 b0, a0 b1 + a1 b0, a1 b1); equal level and batch; out3 has 3 components. */
+ckks_status ckks_mul(ckks_ctx* ctx, const ckks_ct* a, const ckks_ct* b, ckks_ct* out3, void* stream);
+/* (c0, c1, c2) -> (c0, c1) + KS(c2; rlk).  in3 has 3 components; out must not alias in3. */
+ckks_status ckks_relinearize(ckks_ctx* ctx, const ckks_ct* in3, ckks_ct* out, void* stream);
+/* Divide by q_l with rounding and drop limb l (R10); scale /= q_l.
+ * CKKS_E_LEVEL at level 0.  Works for 2 or 3 components.  out must not alias in. */
+ckks_status ckks_rescale(ckks_ctx* ctx, const ckks_ct* in, ckks_ct* out, void* stream);
+/* Slot-wise sum; equal level, batch, n_comp and scale (CKKS_E_SCALE beyond 2^-40 relative). */
+ckks_status ckks_add(ckks_ctx* ctx, const ckks_ct* a, const ckks_ct* b, ckks_ct* out, void* stream);
+
+/* ---- dense layer (Eq. 1, rows a6, a7, a9) ---------------------------------------------------- */
+/* Device bytes of an encoded rows x cols layer whose input ciphertext is at `level`. */
+ckks_status ckks_layer_sizes(const ckks_ctx* ctx, uint32_t rows, uint32_t cols, uint32_t level, size_t* dev_bytes);
+/* Encode W (host, row-major rows x cols, float64) and bias (host, rows, may be NULL) with the
+ * library's own encoder: diag'_i zero-padded to t x t, t1 = 2^ceil(ceil(log2 t)/2)
+ * (R5), plaintext scale q_level (R8), bias at scale in_scale and level-1.  Borrows dev_buf. */
+ckks_status ckks_layer_create(ckks_ctx* ctx, const double* W, uint32_t rows, uint32_t cols, const double* bias,
+                              uint32_t level, double in_scale, void* dev_buf, void* stream, ckks_layer** out);
+/* Same layer from already-encoded integer coefficients: diag_coeffs host [t][N] int64 (diag'_i
+ * encodings, i < t), bias_coeffs host [N] int64 (may be NULL).  Used to feed both the oracle and
+ * the library the same plaintexts (SURVEY 7 hard part 2). */
+ckks_status ckks_layer_import(ckks_ctx* ctx, const int64_t* diag_coeffs, const int64_t* bias_coeffs, uint32_t rows,
+                              uint32_t cols, uint32_t level, double pt_scale, double bias_scale, void* dev_buf,
+                              void* stream, ckks_layer** out);
+void ckks_layer_destroy(ckks_layer* layer);
+/* Workspace (device bytes) ckks_matvec_diag / ckks_encrypted_forward need for `batch` cts. */
+ckks_status ckks_layer_work_sizes(const ckks_ctx* ctx, const ckks_layer* layer, uint32_t batch, size_t* bytes);
+/* y = sum_k rot_{k t1}(sum_j diag'_{k t1+j} o rot_j(x)) (Eq. 1), one rescale (R7), + bias.
+ * in at the layer's level; out at level-1, scale = in scale.  work: ckks_layer_work_sizes bytes. */
+ckks_status ckks_matvec_diag(ckks_ctx* ctx, const ckks_layer* layer, const ckks_ct* in, ckks_ct* out, void* work,
+                             void* stream);
+
+/* ---- model / forward (rows a10-a12) --------------------------------------------------------- */
+/* activation: 0 none, 1 square (BASELINE cfg4), 2 cubic ReLU approximation (Eq. 2).
+ * Layers must be encoded for the levels/scales the forward produces (R8). */
+ckks_status ckks_model_create(ckks_ctx* ctx, const ckks_layer* const* layers, uint32_t n_layers, int32_t activation,
+                              ckks_model** out);
+void ckks_model_destroy(ckks_model* model);
+/* BSGS split of a rows x cols layer: t = max(rows, cols) padded to a multiple of
+ * t1 = 2^ceil(ceil(log2 t)/2), t2 = t / t1 (R5). */
+ckks_status ckks_bsgs_plan(uint32_t rows, uint32_t cols, uint32_t* t, uint32_t* t1, uint32_t* t2);
+/* Level/scale schedule of a forward (R8): for each layer the level and scale its input has, and
+ * the sorted set of rotation steps the forward needs (baby 1..t1-1, giant k t1, replicate -t).
+ * steps may be NULL to query the count; *n_steps is its capacity on input, the count on output. */
+ckks_status ckks_model_plan(const ckks_ctx* ctx, uint32_t n_layers, const uint32_t* rows, const uint32_t* cols,
+                            int32_t activation, uint32_t in_level, double in_scale, uint32_t* layer_level,
+                            double* layer_in_scale, int32_t* steps, uint32_t* n_steps);
+/* Device workspace bytes for a forward over `batch` ciphertexts (chunked at max_batch). */
+ckks_status ckks_model_work_sizes(const ckks_ctx* ctx, const ckks_model* model, uint32_t batch, size_t* bytes);
+/* dense_1 -> act -> replicate -> dense_2 -> ... on a batch of independent
+ * ciphertexts; out is written at the final level (sets out->level/scale). */
+ckks_status ckks_encrypted_forward(ckks_ctx* ctx, const ckks_model* model, const ckks_ct* in, ckks_ct* out,
+                                   void* work, void* stream);
+/* Same, end to end from HOST buffers: h_in [batch][2][in_level+1][N] (pinned recommended) is
+ * copied to the device chunk by chunk, evaluated, and copied back to h_out [batch][2][out_level+1][N].
+ * Synchronises the stream before returning. */
+ckks_status ckks_encrypted_forward_host(ckks_ctx* ctx, const ckks_model* model, const uint64_t* h_in,
+                                        uint32_t batch, uint32_t in_level, double in_scale, uint64_t* h_out,
+                                        uint32_t* out_level, double* out_scale, void* work, void* stream);
+
+/* ---- client-side helpers (off the hot path) ------------------------------------------------ */
+/* values (count <= N/2 reals) -> int64 coefficients m[N] = round(scale * inverse embedding) (R4). */
+ckks_status ckks_encode(const ckks_ctx* ctx, const double* values, uint32_t count, double scale, int64_t* coeffs);
+/* Public-key encryption at the top level of host coefficients [batch][N] (R6, R17); the randomness
+ * of ciphertext i comes from (enc_seed, first_index + i).  out->data device [batch][2][L][N]. */
+ckks_status ckks_encrypt(ckks_ctx* ctx, const int64_t* h_coeffs, uint32_t batch, uint64_t enc_seed,
+                         uint64_t first_index, double scale, ckks_ct* out, void* stream);
+/* c0 + c1 s, inverse NTT: d_out device [batch][level+1][N] coefficient residues. */
+ckks_status ckks_decrypt(ckks_ctx* ctx, const ckks_ct* in, uint64_t* d_out, void* stream);
+/* Host decode of one decrypted [level+1][N] residue block: centered CRT lift, canonical
+ * embedding, / scale -> values[count]. */
+ckks_status ckks_decode(const ckks_ctx* ctx, const uint64_t* h_residues, uint32_t level, double scale, double* values,
+                        uint32_t count);
+/* Export key material to host memory (synchronises `stream`):
+ *   key_id 0 = relinearisation key, key_id = g (odd) = Galois key: [L][2][L+1][N] NTT form;
+ *   key_id -1 = secret s in NTT form over all primes [L + n_special][N];
+ *   key_id -2 = public key [2][L][N] NTT form.  (Test/parity use only.) */
+ckks_status ckks_export_key(ckks_ctx* ctx, int64_t key_id, uint64_t* h_out, void* stream);
+/* Galois element of a left rotation by step (R3). */
+uint64_t ckks_galois_elt(const ckks_ctx* ctx, int32_t step);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CKKS_B200_H */

@@ -1,0 +1,1257 @@
+// api.cpp -- host side of libckks_b200: the C-ABI of include/ckks.h.
+//
+// The host only (a) builds constants once per context (prime chain, psi, twiddle tables, CRT
+// constants) and (b) sequences kernel launches with level/scale bookkeeping.  Every step of the
+// hot path runs in the sm_100a kernels of kernels.cu.  There is no CPU fallback: without a CUDA
+// device, compute calls fail with CKKS_E_CUDA.
+#include "../../include/ckks.h"
+#include "common.cuh"
+#include "kernels.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+typedef unsigned __int128 u128;
+
+namespace {
+
+thread_local std::string g_err;
+
+ckks_status fail(ckks_status s, const std::string& msg)
+{
+    g_err = msg;
+    return s;
+}
+
+struct CkksError : std::runtime_error {
+    ckks_status st;
+    CkksError(ckks_status s, const std::string& m) : std::runtime_error(m), st(s) {}
+};
+
+#define CK_TRY(...)                                                                             \
+    try {                                                                                         \
+        __VA_ARGS__                                                                               \
+    } catch (const CkksError& e) {                                                                \
+        return fail(e.st, e.what());                                                              \
+    } catch (const std::exception& e) {                                                           \
+        return fail(CKKS_E_CUDA, e.what());                                                       \
+    }
+
+void cuda_ok(cudaError_t e, const char* what)
+{
+    if (e != cudaSuccess) throw CkksError(CKKS_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------------------ host number theory
+u64 h_mulmod(u64 a, u64 b, u64 m) { return (u64)((u128)a * b % m); }
+u64 h_pow(u64 a, u64 e, u64 m)
+{
+    u64 r = 1 % m;
+    a %= m;
+    for (; e; e >>= 1) {
+        if (e & 1) r = h_mulmod(r, a, m);
+        a = h_mulmod(a, a, m);
+    }
+    return r;
+}
+bool h_is_prime(u64 n)
+{
+    if (n < 4) return n >= 2;
+    for (u64 p : {2ULL, 3ULL, 5ULL, 7ULL, 11ULL, 13ULL, 17ULL, 19ULL, 23ULL, 29ULL, 31ULL, 37ULL})
+        if (n % p == 0) return n == p;
+    u64 d = n - 1;
+    int s = 0;
+    while (!(d & 1)) d >>= 1, ++s;
+    for (u64 a : {2ULL, 3ULL, 5ULL, 7ULL, 11ULL, 13ULL, 17ULL, 19ULL, 23ULL, 29ULL, 31ULL, 37ULL}) {
+        u64 x = h_pow(a, d, n);
+        if (x == 1 || x == n - 1) continue;
+        bool witness = true;
+        for (int r = 1; r < s && witness; ++r) {
+            x = h_mulmod(x, x, n);
+            if (x == n - 1) witness = false;
+        }
+        if (witness) return false;
+    }
+    return true;
+}
+u64 h_shoup(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
+u32 h_brev(u32 x, int bits)
+{
+    u32 r = 0;
+    for (int i = 0; i < bits; ++i) r = (r << 1) | ((x >> i) & 1);
+    return r;
+}
+
+// R1: largest unused prime below 2^bits congruent to 1 mod 2N, in list order.
+std::vector<u64> prime_chain(int log_n, const std::vector<u32>& bits)
+{
+    const u64 m = 2ULL << log_n;
+    std::vector<u64> out;
+    for (u32 b : bits) {
+        if ((int)b < log_n + 2 || b > 61) throw CkksError(CKKS_E_PARAM, "prime bit size out of range [log_n+2, 61]");
+        u64 c = (1ULL << b) + 1 - m;
+        while (!(h_is_prime(c) && std::find(out.begin(), out.end(), c) == out.end())) {
+            if (c <= m + 1) throw CkksError(CKKS_E_PARAM, "ran out of primes");
+            c -= m;
+        }
+        out.push_back(c);
+    }
+    return out;
+}
+// R2: smallest primitive 2N-th root of unity mod q.
+u64 min_root(u64 q, int log_n)
+{
+    const u64 m = 2ULL << log_n, n = 1ULL << log_n;
+    u64 g = 0;
+    for (u64 x = 2;; ++x) {
+        u64 c = h_pow(x, (q - 1) / m, q);
+        if (h_pow(c, n, q) == q - 1) {
+            g = c;
+            break;
+        }
+    }
+    const u64 g2 = h_mulmod(g, g, q);
+    u64 best = g, cur = g;
+    for (u64 k = 1; k < m; k += 2) {
+        best = std::min(best, cur);
+        cur = h_mulmod(cur, g2, q);
+    }
+    return best;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// ------------------------------------------------------------------------------ FFT (encode/decode)
+void fft(std::vector<std::complex<double>>& a, int sign)
+{
+    const size_t n = a.size();
+    for (size_t i = 1, j = 0; i < n; ++i) {
+        size_t bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) std::swap(a[i], a[j]);
+    }
+    for (size_t len = 2; len <= n; len <<= 1) {
+        const double ang = sign * 2.0 * M_PI / (double)len;
+        for (size_t i = 0; i < n; i += len)
+            for (size_t k = 0; k < len / 2; ++k) {
+                const std::complex<double> w(std::cos(ang * (double)k), std::sin(ang * (double)k));
+                const std::complex<double> u = a[i + k], v = a[i + k + len / 2] * w;
+                a[i + k] = u + v;
+                a[i + k + len / 2] = u - v;
+            }
+    }
+}
+
+std::vector<u64> slot_exps(int n)
+{
+    std::vector<u64> e(n / 2);
+    u64 v = 1;
+    for (int i = 0; i < n / 2; ++i) {
+        e[i] = v;
+        v = (v * 5) % (2ULL * n);
+    }
+    return e;
+}
+
+// R4: m_k = round_half_away(Re FFT_2N(Z)[k] / N), Z[5^i] = scale z_i, Z[-5^i] = conj.
+void encode_host(int n, const double* values, size_t count, double scale, int64_t* out)
+{
+    if (count > (size_t)n / 2) throw CkksError(CKKS_E_PARAM, "more values than slots");
+    std::vector<std::complex<double>> Z(2 * (size_t)n, 0.0);
+    const auto e = slot_exps(n);
+    for (size_t i = 0; i < count; ++i) {
+        Z[e[i]] = scale * values[i];
+        Z[(2 * n - e[i]) % (2 * n)] = scale * values[i];
+    }
+    fft(Z, -1);
+    for (int k = 0; k < n; ++k) {
+        const double x = Z[k].real() / n;
+        const double r = (x < 0 ? -1.0 : 1.0) * std::floor(std::fabs(x) + 0.5);
+        if (std::fabs(r) >= 4.6e18) throw CkksError(CKKS_E_PARAM, "encoded coefficient overflows int64");
+        out[k] = (int64_t)r;
+    }
+}
+
+}  // namespace
+
+// ================================================================================== structures
+struct ckks_ctx {
+    int log_n = 0, n = 0, L = 0, ns = 0, np = 0;
+    double sigma = 3.2;
+    uint32_t max_batch = 1;
+    std::vector<u64> primes, psi;
+    DCtx host_dc{};
+    DCtx* d_dc = nullptr;
+    u64* d_tw = nullptr;
+    u64* d_s = nullptr;      // [np][N] secret, NTT form
+    u64* d_pk = nullptr;     // [2][L][N]
+    u64* d_keys = nullptr;   // [nkeys][L][2][L+1][N]
+    size_t key_words = 0;    // per switching key
+    std::vector<int64_t> key_ids;
+    std::map<int64_t, int> key_slot;
+    u64* d_work = nullptr;
+    size_t work_bytes = 0;
+    unsigned long long launches = 0;
+    ck::Probe probe;
+
+    ck::Launch launch(void* st)
+    {
+        ck::Launch l;
+        l.dc = d_dc;
+        l.log_n = log_n;
+        l.n_data = L;
+        l.n_special = ns;
+        l.st = (cudaStream_t)st;
+        l.counter = &launches;
+        l.probe = &probe;
+        return l;
+    }
+    size_t ct_words(int nl, int ncomp = 2) const { return (size_t)ncomp * nl * n; }
+    const u64* key(int64_t id) const
+    {
+        auto it = key_slot.find(id);
+        if (it == key_slot.end()) return nullptr;
+        return d_keys + (size_t)it->second * key_words;
+    }
+    uint32_t galois(int64_t step) const
+    {
+        const int64_t slots = n / 2;
+        const int64_t r = ((step % slots) + slots) % slots;
+        return (uint32_t)h_pow(5, (u64)r, 2ULL * n);
+    }
+    // KS workspace views for `B` ciphertexts (sized for the top level)
+    ck::KsWork ks_work(int B) const
+    {
+        ck::KsWork w;
+        u64* p = d_work;
+        w.digits = p;
+        p += (size_t)B * L * n;
+        w.modup = p;
+        p += (size_t)B * L * (L + 1) * n;
+        w.acc = p;
+        p += (size_t)B * 2 * (L + 1) * n;
+        w.rem = p;
+        return w;
+    }
+};
+
+struct ckks_layer {
+    uint32_t rows, cols, t, t1, t2, level;
+    double pt_scale, bias_scale;
+    u64* d_pts;     // [t][level+1][N]
+    u64* d_bias;    // [level][N] or null
+};
+
+struct ckks_model {
+    std::vector<const ckks_layer*> layers;
+    int activation;
+};
+
+namespace {
+
+size_t ks_work_words(int L, int n, int B) { return (size_t)B * n * ((size_t)L + (size_t)L * (L + 1) + 2 * (L + 1) + 3); }
+size_t enc_work_words(int L, int n, int B) { return (size_t)B * n * (4 * (size_t)L + 1); }
+
+void check_ct(const ckks_ctx* c, const ckks_ct* x, int ncomp_expect = 2)
+{
+    if (!x || !x->data) throw CkksError(CKKS_E_PARAM, "null ciphertext");
+    if (ncomp_expect && (int)x->n_comp != ncomp_expect) throw CkksError(CKKS_E_SHAPE, "wrong number of components");
+    if ((int)x->level >= c->L) throw CkksError(CKKS_E_SHAPE, "level above the chain");
+    if (x->batch == 0) throw CkksError(CKKS_E_SHAPE, "empty batch");
+}
+
+void bsgs_split(uint32_t rows, uint32_t cols, uint32_t& t, uint32_t& t1, uint32_t& t2)
+{
+    t = std::max(rows, cols);
+    int lg = 0;
+    while ((1u << lg) < t) ++lg;
+    t1 = 1u << ((lg + 1) / 2);
+    t = (t + t1 - 1) / t1 * t1;
+    t2 = t / t1;
+}
+
+// rotate a batch (chunked by max_batch): out = rot_step(in)  [+ out if accumulate]
+void rotate_impl(ckks_ctx* c, const u64* in, size_t in_stride, int nl, int batch, int64_t step, u64* out,
+                 size_t out_stride, bool accumulate, void* stream)
+{
+    const uint32_t g = c->galois(step);
+    auto L = c->launch(stream);
+    if (g == 1) {
+        for (int b = 0; b < batch; ++b) {
+            if (accumulate)
+                ck::add(L, in + b * in_stride, 0, out + b * out_stride, 0, out + b * out_stride, 0, 1, 2, nl);
+            else
+                cuda_ok(cudaMemcpyAsync(out + b * out_stride, in + b * in_stride, c->ct_words(nl) * 8,
+                                        cudaMemcpyDeviceToDevice, (cudaStream_t)stream), "copy");
+        }
+        return;
+    }
+    const u64* key = c->key((int64_t)g);
+    if (!key) throw CkksError(CKKS_E_NOKEY, "no Galois key for step " + std::to_string(step));
+    for (int b0 = 0; b0 < batch; b0 += (int)c->max_batch) {
+        const int B = std::min((int)c->max_batch, batch - b0);
+        ck::KsIn ki{in + (size_t)b0 * in_stride, in_stride, (size_t)nl * c->n, g};
+        ck::KsOut ko{out + (size_t)b0 * out_stride, out_stride, in + (size_t)b0 * in_stride, in_stride, g, 0,
+                     accumulate ? 1 : 0};
+        ck::keyswitch(L, ki, key, B, nl, c->ks_work(B), ko);
+    }
+}
+
+void relin_impl(ckks_ctx* c, const u64* in3, size_t in_stride, int nl, int batch, u64* out, size_t out_stride,
+                void* stream)
+{
+    const u64* key = c->key(0);
+    if (!key) throw CkksError(CKKS_E_NOKEY, "no relinearisation key");
+    auto L = c->launch(stream);
+    for (int b0 = 0; b0 < batch; b0 += (int)c->max_batch) {
+        const int B = std::min((int)c->max_batch, batch - b0);
+        ck::KsIn ki{in3 + (size_t)b0 * in_stride, in_stride, (size_t)2 * nl * c->n, 0};
+        ck::KsOut ko{out + (size_t)b0 * out_stride, out_stride, in3 + (size_t)b0 * in_stride, in_stride, 0, 1, 0};
+        ck::keyswitch(L, ki, key, B, nl, c->ks_work(B), ko);
+    }
+}
+
+void rescale_impl(ckks_ctx* c, const u64* in, size_t in_stride, int ncomp, int nl, int batch, u64* out,
+                  size_t out_stride, const u64* bias, void* stream)
+{
+    if (nl < 2) throw CkksError(CKKS_E_LEVEL, "rescale at level 0 (depth exhausted)");
+    auto L = c->launch(stream);
+    u64* rem = c->ks_work(c->max_batch).rem;   // [B][<=3][N]
+    for (int b0 = 0; b0 < batch; b0 += (int)c->max_batch) {
+        const int B = std::min((int)c->max_batch, batch - b0);
+        ck::rescale(L, in + (size_t)b0 * in_stride, in_stride, out + (size_t)b0 * out_stride, out_stride, B, ncomp,
+                    nl, rem, bias);
+    }
+}
+
+// Device scalar constant helpers for the cubic activation (R23): constant plaintext m0 at
+// coefficient 0 has NTT value m0 mod q_i in every slot.
+}  // namespace
+
+namespace ck {
+void mul_scalar(const Launch&, const uint64_t* in, size_t sin, uint64_t* out, size_t sout, const uint64_t* res,
+                int batch, int ncomp, int nl);
+void add_scalar(const Launch&, uint64_t* ct, size_t stride, const uint64_t* res, int batch, int nl);
+}  // namespace ck
+
+// ================================================================================== C-ABI
+extern "C" {
+
+const char* ckks_last_error(void) { return g_err.c_str(); }
+
+static void sizes_impl(const ckks_params* p, size_t* tb, size_t* kb, size_t* wb, std::vector<u64>* primes_out)
+{
+    if (!p || !p->prime_bits) throw CkksError(CKKS_E_PARAM, "null params");
+    if (p->log_n < 10 || p->log_n > 14) throw CkksError(CKKS_E_PARAM, "log_n must be in [10, 14]");
+    if (p->n_data < 1 || p->n_special > 1 || p->n_data + p->n_special > CKKS_MAXP)
+        throw CkksError(CKKS_E_PARAM, "need 1 <= n_data, n_special <= 1, n_data + n_special <= 16");
+    if (p->n_special == 0 && (p->n_rot_steps || p->want_relin))
+        throw CkksError(CKKS_E_PARAM, "key switching needs a special prime");
+    if (p->max_batch < 1) throw CkksError(CKKS_E_PARAM, "max_batch >= 1");
+    const int n = 1 << p->log_n, L = (int)p->n_data, np = L + (int)p->n_special;
+    std::vector<u32> bits(p->prime_bits, p->prime_bits + np);
+    auto primes = prime_chain((int)p->log_n, bits);
+    if (primes_out) *primes_out = primes;
+    // number of distinct switching keys
+    std::vector<int64_t> ids;
+    if (p->want_relin) ids.push_back(0);
+    for (uint32_t i = 0; i < p->n_rot_steps; ++i) {
+        const int64_t slots = n / 2;
+        const int64_t r = (((int64_t)p->rot_steps[i] % slots) + slots) % slots;
+        const int64_t g = (int64_t)h_pow(5, (u64)r, 2ULL * n);
+        if (g != 1 && std::find(ids.begin(), ids.end(), g) == ids.end()) ids.push_back(g);
+    }
+    const size_t key_words = p->n_special ? (size_t)L * 2 * (L + 1) * n : 0;
+    *tb = align256(sizeof(DCtx)) + align256((size_t)np * 4 * n * 8);
+    *kb = align256((size_t)np * n * 8) + align256((size_t)2 * L * n * 8) + ids.size() * key_words * 8;
+    const int B = (int)p->max_batch;
+    size_t w = std::max(enc_work_words(L, n, B), p->n_special ? ks_work_words(L, n, B) : (size_t)0);
+    // keygen scratch: e_ntt [L][L+1][N] + s' [np][N]
+    w = std::max(w, (size_t)L * (L + 1) * n + (size_t)np * n);
+    *wb = align256(w * 8);
+}
+
+ckks_status ckks_ctx_sizes(const ckks_params* p, size_t* table_bytes, size_t* key_bytes, size_t* work_bytes)
+{
+    CK_TRY({
+        sizes_impl(p, table_bytes, key_bytes, work_bytes, nullptr);
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, void* d_work, void* stream,
+                            ckks_ctx** out)
+{
+    CK_TRY({
+        if (!out) throw CkksError(CKKS_E_PARAM, "null out");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw CkksError(CKKS_E_CUDA, "no CUDA device");
+        size_t tb, kb, wb;
+        std::vector<u64> primes;
+        sizes_impl(p, &tb, &kb, &wb, &primes);
+        if (!d_tables || !d_keys || !d_work) throw CkksError(CKKS_E_PARAM, "null device buffer");
+        auto* c = new ckks_ctx();
+        c->log_n = (int)p->log_n;
+        c->n = 1 << c->log_n;
+        c->L = (int)p->n_data;
+        c->ns = (int)p->n_special;
+        c->np = c->L + c->ns;
+        c->sigma = p->sigma > 0 ? p->sigma : 3.2;
+        c->max_batch = p->max_batch;
+        c->primes = primes;
+        const int n = c->n, np = c->np, L = c->L;
+        // ---- constants
+        DCtx& h = c->host_dc;
+        std::memset(&h, 0, sizeof(DCtx));
+        h.log_n = c->log_n;
+        h.n = n;
+        h.n_data = L;
+        h.n_special = c->ns;
+        h.n_primes = np;
+        std::vector<u64> tw((size_t)np * 4 * n);
+        for (int i = 0; i < np; ++i) {
+            const u64 q = primes[i];
+            const u64 psi = min_root(q, c->log_n), ipsi = h_pow(psi, q - 2, q);
+            c->psi.push_back(psi);
+            DPrime& P = h.p[i];
+            P.q = q;
+            P.q2 = 2 * q;
+            P.ninv = h_pow((u64)n % q, q - 2, q);
+            P.ninv_sh = h_shoup(P.ninv, q);
+            P.one_sh = (u64)(((u128)1 << 64) / q);
+            P.r64 = (u64)(((u128)1 << 64) % q);
+            P.r64_sh = h_shoup(P.r64, q);
+            u64* W = tw.data() + (size_t)i * 4 * n;
+            u64 pw = 1, ipw = 1;
+            for (int m = 0; m < n; ++m) {
+                const u32 r = h_brev((u32)m, c->log_n);
+                W[r] = pw;
+                W[n + r] = h_shoup(pw, q);
+                W[2 * n + r] = ipw;
+                W[3 * n + r] = h_shoup(ipw, q);
+                pw = h_mulmod(pw, psi, q);
+                ipw = h_mulmod(ipw, ipsi, q);
+            }
+            for (int b = 0; b < np; ++b) {
+                h.qmod[i][b] = q % primes[b];
+                if (b != i) {
+                    h.qinv[i][b] = h_pow(q % primes[b], primes[b] - 2, primes[b]);
+                    h.qinv_sh[i][b] = h_shoup(h.qinv[i][b], primes[b]);
+                }
+            }
+        }
+        // R13 CDT, same definition as DESIGN.md (computed here independently)
+        {
+            const int B = (int)std::floor(6.0 * c->sigma);
+            if (2 * B > 40) throw CkksError(CKKS_E_PARAM, "sigma too large");
+            std::vector<double> rho(2 * B + 1);
+            double total = 0.0;
+            for (int x = -B; x <= B; ++x) {
+                rho[x + B] = std::exp(-(double)(x * x) / (2.0 * c->sigma * c->sigma));
+                total += rho[x + B];
+            }
+            double cum = 0.0;
+            for (int x = -B; x < B; ++x) {
+                cum += rho[x + B];
+                h.cdt[x + B] = (u64)std::ldexp(cum / total, 64);
+            }
+            h.cdt_bound = B;
+        }
+        char* tbase = (char*)d_tables;
+        c->d_dc = (DCtx*)tbase;
+        c->d_tw = (u64*)(tbase + align256(sizeof(DCtx)));
+        h.tw = c->d_tw;
+        cudaStream_t st = (cudaStream_t)stream;
+        cuda_ok(cudaMemcpyAsync(c->d_tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice, st), "upload tables");
+        cuda_ok(cudaMemcpyAsync(c->d_dc, &h, sizeof(DCtx), cudaMemcpyHostToDevice, st), "upload consts");
+        // ---- key buffers
+        char* kbase = (char*)d_keys;
+        c->d_s = (u64*)kbase;
+        c->d_pk = (u64*)(kbase + align256((size_t)np * n * 8));
+        c->d_keys = (u64*)(kbase + align256((size_t)np * n * 8) + align256((size_t)2 * L * n * 8));
+        c->key_words = c->ns ? (size_t)L * 2 * (L + 1) * n : 0;
+        c->d_work = (u64*)d_work;
+        c->work_bytes = wb;
+        if (p->want_relin) c->key_ids.push_back(0);
+        for (uint32_t i = 0; i < p->n_rot_steps; ++i) {
+            const int64_t g = c->galois(p->rot_steps[i]);
+            if (g != 1 && std::find(c->key_ids.begin(), c->key_ids.end(), g) == c->key_ids.end())
+                c->key_ids.push_back(g);
+        }
+        for (size_t i = 0; i < c->key_ids.size(); ++i) c->key_slot[c->key_ids[i]] = (int)i;
+        // ---- keygen on the device (R5, R13-R15; stream tags of DESIGN.md)
+        auto Lc = c->launch(stream);
+        const u64 seed = p->key_seed;
+        ck::sample_ntt(Lc, c->d_s, 1, np, L, 0, seed, 1, 0, 0, 0, 0);                 // s (TAG 1)
+        u64* scratch = c->d_work;
+        for (int i = 0; i < L; ++i) ck::sample_uniform(Lc, c->d_pk + (size_t)(L + i) * n, i, seed, 2, 0, 0);
+        ck::sample_ntt(Lc, scratch, 1, L, L, 1, seed, 3, 0, 0, 0, 0);                 // pk e (TAG 3)
+        ck::pk_combine(Lc, c->d_pk, scratch, c->d_s, L);
+        if (c->ns) {
+            u64* e_ntt = scratch;                               // [L][L+1][N]
+            u64* sp = scratch + (size_t)L * (L + 1) * n;        // [np][N]
+            for (size_t ki = 0; ki < c->key_ids.size(); ++ki) {
+                const int64_t id = c->key_ids[ki];
+                u64* key = c->d_keys + ki * c->key_words;
+                if (id == 0) ck::square_ntt(Lc, c->d_s, sp, np);
+                else ck::galois_ntt(Lc, c->d_s, sp, np, (uint32_t)id);
+                for (int j = 0; j < L; ++j)
+                    for (int pi = 0; pi <= L; ++pi)
+                        ck::sample_uniform(Lc, key + (((size_t)j * 2 + 1) * (L + 1) + pi) * n, pi, seed, 4, (u64)id,
+                                           (u64)j);
+                ck::sample_ntt(Lc, e_ntt, L, L + 1, L, 1, seed, 5, (u64)id, 0, 0, 1);   // e_j (TAG 5)
+                ck::keyswitch_key_combine(Lc, key, e_ntt, c->d_s, sp, L);
+            }
+        }
+        cuda_ok(cudaStreamSynchronize(st), "keygen");
+        *out = c;
+        return CKKS_OK;
+    })
+}
+
+void ckks_ctx_destroy(ckks_ctx* ctx)
+{
+    if (ctx)
+        for (auto e : ctx->probe.ev) cudaEventDestroy(e);
+    delete ctx;
+}
+
+ckks_status ckks_probe_enable(ckks_ctx* c, int32_t kind)
+{
+    CK_TRY({
+        if (!c || kind < 0 || kind > 3) throw CkksError(CKKS_E_PARAM, "probe kind 0..3");
+        c->probe.kind = kind;
+        c->probe.used = 0;
+        c->probe.alg_bytes = 0;
+        while (kind && c->probe.ev.size() < 4096) {
+            cudaEvent_t e;
+            cuda_ok(cudaEventCreate(&e), "event");
+            c->probe.ev.push_back(e);
+        }
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_probe_read(ckks_ctx* c, double* total_ms, uint64_t* launches, double* alg_bytes)
+{
+    CK_TRY({
+        if (!c || !total_ms || !launches) throw CkksError(CKKS_E_PARAM, "null");
+        double tot = 0;
+        const size_t pairs = c->probe.used / 2;
+        if (pairs) cuda_ok(cudaEventSynchronize(c->probe.ev[2 * pairs - 1]), "probe sync");
+        for (size_t i = 0; i < pairs; ++i) {
+            float ms = 0;
+            cuda_ok(cudaEventElapsedTime(&ms, c->probe.ev[2 * i], c->probe.ev[2 * i + 1]), "elapsed");
+            tot += ms;
+        }
+        *total_ms = tot;
+        *launches = pairs;
+        if (alg_bytes) *alg_bytes = c->probe.alg_bytes;
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_ctx_info(const ckks_ctx* c, ckks_info* o)
+{
+    if (!c || !o) return fail(CKKS_E_PARAM, "null");
+    std::memset(o, 0, sizeof(*o));
+    o->log_n = (uint32_t)c->log_n;
+    o->n = (uint32_t)c->n;
+    o->n_data = (uint32_t)c->L;
+    o->n_special = (uint32_t)c->ns;
+    o->n_keys = (uint32_t)c->key_ids.size();
+    for (int i = 0; i < c->np; ++i) {
+        o->primes[i] = c->primes[i];
+        o->psi[i] = c->psi[i];
+    }
+    return CKKS_OK;
+}
+
+uint64_t ckks_launch_count(const ckks_ctx* c) { return c ? c->launches : 0; }
+
+uint64_t ckks_galois_elt(const ckks_ctx* c, int32_t step) { return c ? c->galois(step) : 0; }
+
+static ckks_status ntt_impl(ckks_ctx* c, uint64_t* d, uint32_t batch, uint32_t limbs, void* stream, bool inv)
+{
+    CK_TRY({
+        if (!c || !d) throw CkksError(CKKS_E_PARAM, "null");
+        if (limbs == 0 || (int)limbs > c->np) throw CkksError(CKKS_E_SHAPE, "limbs > number of primes");
+        if (batch == 0) return CKKS_OK;
+        auto L = c->launch(stream);
+        // grid.y is limited to 65535 CTAs: chunk the batch
+        for (uint32_t b0 = 0; b0 < batch; b0 += 65535) {
+            const uint32_t B = std::min<uint32_t>(65535, batch - b0);
+            ck::ntt_batch(L, d + (size_t)b0 * limbs * c->n, (int)B, (int)limbs, 0, inv);
+        }
+        return CKKS_OK;
+    })
+}
+ckks_status ckks_ntt_fwd(ckks_ctx* c, uint64_t* d, uint32_t batch, uint32_t limbs, void* stream)
+{
+    return ntt_impl(c, d, batch, limbs, stream, false);
+}
+ckks_status ckks_ntt_inv(ckks_ctx* c, uint64_t* d, uint32_t batch, uint32_t limbs, void* stream)
+{
+    return ntt_impl(c, d, batch, limbs, stream, true);
+}
+
+ckks_status ckks_rotate(ckks_ctx* c, const ckks_ct* in, int32_t step, ckks_ct* out, void* stream)
+{
+    CK_TRY({
+        if (!c || !out || !out->data) throw CkksError(CKKS_E_PARAM, "null");
+        check_ct(c, in);
+        if (in->data == out->data) throw CkksError(CKKS_E_SHAPE, "rotate: out aliases in");
+        const int nl = (int)in->level + 1;
+        rotate_impl(c, in->data, c->ct_words(nl), nl, (int)in->batch, step, out->data, c->ct_words(nl), false, stream);
+        out->batch = in->batch;
+        out->n_comp = 2;
+        out->level = in->level;
+        out->scale = in->scale;
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_mul(ckks_ctx* c, const ckks_ct* a, const ckks_ct* b, ckks_ct* out3, void* stream)
+{
+    CK_TRY({
+        if (!c || !out3 || !out3->data) throw CkksError(CKKS_E_PARAM, "null");
+        check_ct(c, a);
+        check_ct(c, b);
+        if (a->level != b->level || a->batch != b->batch) throw CkksError(CKKS_E_SHAPE, "mul: level/batch mismatch");
+        const int nl = (int)a->level + 1;
+        auto L = c->launch(stream);
+        for (uint32_t b0 = 0; b0 < a->batch; b0 += 65535) {
+            const int B = (int)std::min<uint32_t>(65535, a->batch - b0);
+            ck::tensor(L, a->data + b0 * c->ct_words(nl), b->data + b0 * c->ct_words(nl), c->ct_words(nl),
+                       out3->data + b0 * c->ct_words(nl, 3), c->ct_words(nl, 3), B, nl);
+        }
+        out3->batch = a->batch;
+        out3->n_comp = 3;
+        out3->level = a->level;
+        out3->scale = a->scale * b->scale;
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_relinearize(ckks_ctx* c, const ckks_ct* in3, ckks_ct* out, void* stream)
+{
+    CK_TRY({
+        if (!c || !out || !out->data) throw CkksError(CKKS_E_PARAM, "null");
+        check_ct(c, in3, 3);
+        if (in3->data == out->data) throw CkksError(CKKS_E_SHAPE, "relinearize: out aliases in");
+        const int nl = (int)in3->level + 1;
+        relin_impl(c, in3->data, c->ct_words(nl, 3), nl, (int)in3->batch, out->data, c->ct_words(nl), stream);
+        out->batch = in3->batch;
+        out->n_comp = 2;
+        out->level = in3->level;
+        out->scale = in3->scale;
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_rescale(ckks_ctx* c, const ckks_ct* in, ckks_ct* out, void* stream)
+{
+    CK_TRY({
+        if (!c || !out || !out->data) throw CkksError(CKKS_E_PARAM, "null");
+        check_ct(c, in, 0);
+        if (in->n_comp < 2 || in->n_comp > 3) throw CkksError(CKKS_E_SHAPE, "rescale: 2 or 3 components");
+        if (in->data == out->data) throw CkksError(CKKS_E_SHAPE, "rescale: out aliases in");
+        const int nl = (int)in->level + 1, nc = (int)in->n_comp;
+        rescale_impl(c, in->data, c->ct_words(nl, nc), nc, nl, (int)in->batch, out->data, c->ct_words(nl - 1, nc),
+                     nullptr, stream);
+        out->batch = in->batch;
+        out->n_comp = in->n_comp;
+        out->level = in->level - 1;
+        out->scale = in->scale / (double)c->primes[in->level];
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_add(ckks_ctx* c, const ckks_ct* a, const ckks_ct* b, ckks_ct* out, void* stream)
+{
+    CK_TRY({
+        if (!c || !out || !out->data) throw CkksError(CKKS_E_PARAM, "null");
+        check_ct(c, a, 0);
+        check_ct(c, b, 0);
+        if (a->level != b->level || a->batch != b->batch || a->n_comp != b->n_comp)
+            throw CkksError(CKKS_E_SHAPE, "add: shape mismatch");
+        if (std::fabs(a->scale - b->scale) > std::ldexp(std::max(a->scale, b->scale), -40))
+            throw CkksError(CKKS_E_SCALE, "add: scale mismatch beyond 2^-40 relative");
+        const int nl = (int)a->level + 1, nc = (int)a->n_comp;
+        const size_t w = c->ct_words(nl, nc);
+        auto L = c->launch(stream);
+        for (uint32_t b0 = 0; b0 < a->batch; b0 += 65535) {
+            const int B = (int)std::min<uint32_t>(65535, a->batch - b0);
+            ck::add(L, a->data + b0 * w, w, b->data + b0 * w, w, out->data + b0 * w, w, B, nc, nl);
+        }
+        out->batch = a->batch;
+        out->n_comp = a->n_comp;
+        out->level = a->level;
+        out->scale = a->scale;
+        return CKKS_OK;
+    })
+}
+
+// ------------------------------------------------------------------------------------ layers
+ckks_status ckks_layer_sizes(const ckks_ctx* c, uint32_t rows, uint32_t cols, uint32_t level, size_t* bytes)
+{
+    CK_TRY({
+        if (!c || !bytes || rows == 0 || cols == 0) throw CkksError(CKKS_E_PARAM, "bad layer shape");
+        if (level < 1 || (int)level >= c->L) throw CkksError(CKKS_E_LEVEL, "layer level must be in [1, L-1]");
+        uint32_t t, t1, t2;
+        bsgs_split(rows, cols, t, t1, t2);
+        *bytes = align256((size_t)t * (level + 1) * c->n * 8) + align256((size_t)level * c->n * 8) +
+                 align256((size_t)(t > 1 ? t : 1) * c->n * 8);   // staging for the int64 coefficients
+        return CKKS_OK;
+    })
+}
+
+static ckks_status layer_from_coeffs(ckks_ctx* c, const int64_t* diag, const int64_t* bias, uint32_t rows,
+                                     uint32_t cols, uint32_t level, double pt_scale, double bias_scale, void* dev_buf,
+                                     void* stream, ckks_layer** out)
+{
+    uint32_t t, t1, t2;
+    bsgs_split(rows, cols, t, t1, t2);
+    if (2 * t > (uint32_t)c->n / 2) throw CkksError(CKKS_E_PARAM, "2t exceeds the slot count");
+    if (t1 > 32 || t2 > 32) throw CkksError(CKKS_E_PARAM, "t1, t2 <= 32 supported (t <= 1024)");
+    auto* ly = new ckks_layer();
+    ly->rows = rows;
+    ly->cols = cols;
+    ly->t = t;
+    ly->t1 = t1;
+    ly->t2 = t2;
+    ly->level = level;
+    ly->pt_scale = pt_scale;
+    ly->bias_scale = bias_scale;
+    char* base = (char*)dev_buf;
+    ly->d_pts = (u64*)base;
+    ly->d_bias = bias ? (u64*)(base + align256((size_t)t * (level + 1) * c->n * 8)) : nullptr;
+    int64_t* stage = (int64_t*)(base + align256((size_t)t * (level + 1) * c->n * 8) + align256((size_t)level * c->n * 8));
+    cudaStream_t st = (cudaStream_t)stream;
+    auto L = c->launch(stream);
+    cuda_ok(cudaMemcpyAsync(stage, diag, (size_t)t * c->n * 8, cudaMemcpyHostToDevice, st), "upload diag");
+    ck::signed_to_ntt(L, stage, ly->d_pts, (int)t, (int)level + 1);
+    if (bias) {
+        cuda_ok(cudaStreamSynchronize(st), "sync");
+        cuda_ok(cudaMemcpyAsync(stage, bias, (size_t)c->n * 8, cudaMemcpyHostToDevice, st), "upload bias");
+        ck::signed_to_ntt(L, stage, ly->d_bias, 1, (int)level);
+    }
+    cuda_ok(cudaStreamSynchronize(st), "layer upload");
+    *out = ly;
+    return CKKS_OK;
+}
+
+ckks_status ckks_layer_import(ckks_ctx* c, const int64_t* diag_coeffs, const int64_t* bias_coeffs, uint32_t rows,
+                              uint32_t cols, uint32_t level, double pt_scale, double bias_scale, void* dev_buf,
+                              void* stream, ckks_layer** out)
+{
+    CK_TRY({
+        if (!c || !diag_coeffs || !dev_buf || !out) throw CkksError(CKKS_E_PARAM, "null");
+        if (level < 1 || (int)level >= c->L) throw CkksError(CKKS_E_LEVEL, "layer level must be in [1, L-1]");
+        return layer_from_coeffs(c, diag_coeffs, bias_coeffs, rows, cols, level, pt_scale, bias_scale, dev_buf,
+                                 stream, out);
+    })
+}
+
+ckks_status ckks_layer_create(ckks_ctx* c, const double* W, uint32_t rows, uint32_t cols, const double* bias,
+                              uint32_t level, double in_scale, void* dev_buf, void* stream, ckks_layer** out)
+{
+    CK_TRY({
+        if (!c || !W || !dev_buf || !out) throw CkksError(CKKS_E_PARAM, "null");
+        if (level < 1 || (int)level >= c->L) throw CkksError(CKKS_E_LEVEL, "layer level must be in [1, L-1]");
+        uint32_t t, t1, t2;
+        bsgs_split(rows, cols, t, t1, t2);
+        const int n = c->n, slots = n / 2;
+        if (2 * t > (uint32_t)slots) throw CkksError(CKKS_E_PARAM, "2t exceeds the slot count");
+        const double ptscale = (double)c->primes[level];
+        std::vector<int64_t> coeffs((size_t)t * n);
+        std::vector<double> v(slots);
+        for (uint32_t i = 0; i < t; ++i) {
+            // diag'_i = rot_{-floor(i/t1) t1}(diag_i): slots [k t1, k t1 + t) (R4)
+            std::fill(v.begin(), v.end(), 0.0);
+            const uint32_t k = i / t1;
+            for (uint32_t s = 0; s < t; ++s) {
+                const uint32_t col = (s + i) % t;
+                v[k * t1 + s] = (s < rows && col < cols) ? W[(size_t)s * cols + col] : 0.0;
+            }
+            encode_host(n, v.data(), slots, ptscale, coeffs.data() + (size_t)i * n);
+        }
+        std::vector<int64_t> bcoef;
+        if (bias) {
+            std::fill(v.begin(), v.end(), 0.0);
+            for (uint32_t s = 0; s < rows; ++s) v[s] = bias[s];
+            bcoef.resize(n);
+            encode_host(n, v.data(), slots, in_scale, bcoef.data());
+        }
+        return layer_from_coeffs(c, coeffs.data(), bias ? bcoef.data() : nullptr, rows, cols, level, ptscale,
+                                 in_scale, dev_buf, stream, out);
+    })
+}
+
+void ckks_layer_destroy(ckks_layer* l) { delete l; }
+
+static size_t layer_work_words(const ckks_ctx* c, const ckks_layer* l, int B)
+{
+    const size_t ctw = c->ct_words((int)l->level + 1);
+    return ((size_t)(l->t1 - 1) + l->t2) * B * ctw;
+}
+
+ckks_status ckks_layer_work_sizes(const ckks_ctx* c, const ckks_layer* l, uint32_t batch, size_t* bytes)
+{
+    if (!c || !l || !bytes) return fail(CKKS_E_PARAM, "null");
+    const int B = (int)std::min<uint32_t>(batch ? batch : 1, c->max_batch);
+    *bytes = align256(layer_work_words(c, l, B) * 8);
+    return CKKS_OK;
+}
+
+// matvec on B ciphertexts (B <= max_batch): in -> out (level-1), work holds baby + W.
+static void matvec_chunk(ckks_ctx* c, const ckks_layer* ly, const u64* in, size_t in_stride, int B, u64* out,
+                         size_t out_stride, u64* work, void* stream)
+{
+    const int nl = (int)ly->level + 1;
+    const size_t ctw = c->ct_words(nl);
+    auto L = c->launch(stream);
+    u64* baby = work;                                   // [t1-1][B][2][nl][N]
+    u64* Wk = work + (size_t)(ly->t1 - 1) * B * ctw;    // [t2][B][2][nl][N]
+    for (uint32_t j = 1; j < ly->t1; ++j)
+        rotate_impl(c, in, in_stride, nl, B, (int64_t)j, baby + (size_t)(j - 1) * B * ctw, ctw, false, stream);
+    ck::bsgs_mac(L, ly->d_pts, in, in_stride, baby, Wk, (int)ly->t1, (int)ly->t2, B, nl);
+    for (uint32_t k = 1; k < ly->t2; ++k)
+        rotate_impl(c, Wk + (size_t)k * B * ctw, ctw, nl, B, (int64_t)k * ly->t1, Wk, ctw, true, stream);
+    rescale_impl(c, Wk, ctw, 2, nl, B, out, out_stride, ly->d_bias, stream);
+}
+
+ckks_status ckks_matvec_diag(ckks_ctx* c, const ckks_layer* ly, const ckks_ct* in, ckks_ct* out, void* work,
+                             void* stream)
+{
+    CK_TRY({
+        if (!c || !ly || !out || !out->data || !work) throw CkksError(CKKS_E_PARAM, "null");
+        check_ct(c, in);
+        if (in->level != ly->level) throw CkksError(CKKS_E_SHAPE, "input level != layer level");
+        const int nl = (int)in->level + 1;
+        for (uint32_t b0 = 0; b0 < in->batch; b0 += c->max_batch) {
+            const int B = (int)std::min<uint32_t>(c->max_batch, in->batch - b0);
+            matvec_chunk(c, ly, in->data + (size_t)b0 * c->ct_words(nl), c->ct_words(nl), B,
+                         out->data + (size_t)b0 * c->ct_words(nl - 1), c->ct_words(nl - 1), (u64*)work, stream);
+        }
+        out->batch = in->batch;
+        out->n_comp = 2;
+        out->level = in->level - 1;
+        out->scale = in->scale * ly->pt_scale / (double)c->primes[in->level];
+        return CKKS_OK;
+    })
+}
+
+// ------------------------------------------------------------------------------------ model
+ckks_status ckks_model_create(ckks_ctx* c, const ckks_layer* const* layers, uint32_t n_layers, int32_t activation,
+                              ckks_model** out)
+{
+    CK_TRY({
+        if (!c || !layers || !out || n_layers == 0) throw CkksError(CKKS_E_PARAM, "null/empty model");
+        if (activation < 0 || activation > 2) throw CkksError(CKKS_E_PARAM, "activation 0|1|2");
+        auto* m = new ckks_model();
+        m->activation = activation;
+        int lvl = (int)layers[0]->level;
+        for (uint32_t i = 0; i < n_layers; ++i) {
+            if ((int)layers[i]->level != lvl) {
+                delete m;
+                throw CkksError(CKKS_E_LEVEL, "layer " + std::to_string(i) + " encoded for the wrong level");
+            }
+            m->layers.push_back(layers[i]);
+            lvl -= 1;
+            if (i + 1 < n_layers) lvl -= (activation == 1 ? 1 : activation == 2 ? 2 : 0);
+        }
+        if (lvl < 0) {
+            delete m;
+            throw CkksError(CKKS_E_LEVEL, "model deeper than the chain");
+        }
+        *out = m;
+        return CKKS_OK;
+    })
+}
+
+void ckks_model_destroy(ckks_model* m) { delete m; }
+
+ckks_status ckks_bsgs_plan(uint32_t rows, uint32_t cols, uint32_t* t, uint32_t* t1, uint32_t* t2)
+{
+    if (!rows || !cols || !t || !t1 || !t2) return fail(CKKS_E_PARAM, "bad shape");
+    bsgs_split(rows, cols, *t, *t1, *t2);
+    return CKKS_OK;
+}
+
+ckks_status ckks_model_plan(const ckks_ctx* c, uint32_t n_layers, const uint32_t* rows, const uint32_t* cols,
+                            int32_t activation, uint32_t in_level, double in_scale, uint32_t* layer_level,
+                            double* layer_in_scale, int32_t* steps, uint32_t* n_steps)
+{
+    CK_TRY({
+        if (!c || !rows || !cols || !layer_level || !layer_in_scale || !n_steps || n_layers == 0)
+            throw CkksError(CKKS_E_PARAM, "null");
+        std::vector<int32_t> st;
+        int lvl = (int)in_level;
+        double s = in_scale;
+        for (uint32_t i = 0; i < n_layers; ++i) {
+            uint32_t t, t1, t2;
+            bsgs_split(rows[i], cols[i], t, t1, t2);
+            if (lvl < 1) throw CkksError(CKKS_E_LEVEL, "model deeper than the chain");
+            layer_level[i] = (uint32_t)lvl;
+            layer_in_scale[i] = s;
+            for (uint32_t j = 1; j < t1; ++j) st.push_back((int32_t)j);
+            for (uint32_t k = 1; k < t2; ++k) st.push_back((int32_t)(k * t1));
+            if (i > 0) st.push_back(-(int32_t)t);
+            lvl -= 1;                       // dense: pt scale q_l, one rescale -> scale unchanged (R8)
+            if (i + 1 < n_layers) {
+                if (activation == 1) {
+                    s = s * s / (double)c->primes[lvl];
+                    lvl -= 1;
+                } else if (activation == 2) {
+                    const double ql = (double)c->primes[lvl], ql1 = (double)c->primes[lvl - 1];
+                    s = (s * s / ql) * s / ql1;
+                    lvl -= 2;
+                }
+            }
+        }
+        if (lvl < 0) throw CkksError(CKKS_E_LEVEL, "model deeper than the chain");
+        std::sort(st.begin(), st.end());
+        st.erase(std::unique(st.begin(), st.end()), st.end());
+        if (steps) {
+            if (st.size() > *n_steps) throw CkksError(CKKS_E_SIZE, "steps buffer too small");
+            std::copy(st.begin(), st.end(), steps);
+        }
+        *n_steps = (uint32_t)st.size();
+        return CKKS_OK;
+    })
+}
+
+static size_t model_work_words(const ckks_ctx* c, const ckks_model* m, int B)
+{
+    size_t lw = 0;
+    for (auto* l : m->layers) lw = std::max(lw, layer_work_words(c, l, B));
+    const size_t big = (size_t)B * c->ct_words(c->L, 3);
+    return lw + 4 * big;
+}
+// + host-path staging: one chunk of input and one of output ciphertexts
+static size_t host_stage_words(const ckks_ctx* c, int B) { return (size_t)B * 2 * c->ct_words(c->L); }
+
+ckks_status ckks_model_work_sizes(const ckks_ctx* c, const ckks_model* m, uint32_t batch, size_t* bytes)
+{
+    if (!c || !m || !bytes) return fail(CKKS_E_PARAM, "null");
+    const int B = (int)std::min<uint32_t>(batch ? batch : 1, c->max_batch);
+    *bytes = align256((model_work_words(c, m, B) + host_stage_words(c, B)) * 8);
+    return CKKS_OK;
+}
+
+// residues of a signed integer constant (host) -> device array [nl] in `dst` (small upload)
+static void const_residues(ckks_ctx* c, int64_t m0, int nl, std::vector<u64>& out)
+{
+    out.resize(nl);
+    for (int i = 0; i < nl; ++i) {
+        const u64 q = c->primes[i];
+        out[i] = m0 >= 0 ? (u64)m0 % q : (q - ((u64)(-(m0 + 1)) + 1) % q) % q;
+    }
+}
+
+static int64_t round_away(double x) { return (int64_t)((x < 0 ? -1.0 : 1.0) * std::floor(std::fabs(x) + 0.5)); }
+
+// One chunk of B ciphertexts through the model.  in: [B][2][l0+1][N]; out: final level.
+static void forward_chunk(ckks_ctx* c, const ckks_model* m, const u64* in, size_t in_stride, int B, double in_scale,
+                          u64* out, size_t out_stride, u64* work, void* stream, int* out_level, double* out_scale)
+{
+    const size_t big = (size_t)B * c->ct_words(c->L, 3);
+    size_t lw = 0;
+    for (auto* l : m->layers) lw = std::max(lw, layer_work_words(c, l, B));
+    u64* lwork = work;
+    u64* bufA = work + lw;
+    u64* bufB = bufA + big;
+    u64* bufC = bufB + big;
+    u64* bufD = bufC + big;
+    auto L = c->launch(stream);
+    const u64* cur = in;
+    size_t cur_stride = in_stride;
+    double scale = in_scale;
+    int level = (int)m->layers[0]->level;
+    const int nlay = (int)m->layers.size();
+    for (int li = 0; li < nlay; ++li) {
+        const ckks_layer* ly = m->layers[li];
+        int nl = level + 1;
+        if (li > 0) {
+            // replicate: y + rot_{-t}(y)  (P:L116 duplicated layout)
+            const size_t ctw = c->ct_words(nl);
+            u64* rep = (cur == bufA) ? bufB : bufA;
+            cuda_ok(cudaMemcpy2DAsync(rep, ctw * 8, cur, cur_stride * 8, ctw * 8, B, cudaMemcpyDeviceToDevice,
+                                      (cudaStream_t)stream), "replicate copy");
+            rotate_impl(c, cur, cur_stride, nl, B, -(int64_t)ly->t, rep, ctw, true, stream);
+            cur = rep;
+            cur_stride = ctw;
+        }
+        const bool last = (li == nlay - 1);
+        u64* dst = last ? out : ((cur == bufA) ? bufB : bufA);
+        const size_t dst_stride = last ? out_stride : c->ct_words(nl - 1);
+        matvec_chunk(c, ly, cur, cur_stride, B, dst, dst_stride, lwork, stream);
+        scale = scale * ly->pt_scale / (double)c->primes[level];
+        level -= 1;
+        nl -= 1;
+        cur = dst;
+        cur_stride = dst_stride;
+        if (last) break;
+        if (m->activation == 1) {
+            // square: rescale(relin(z (x) z))
+            const size_t w3 = c->ct_words(nl, 3), w2 = c->ct_words(nl);
+            ck::tensor(L, cur, cur, cur_stride, bufC, w3, B, nl);
+            relin_impl(c, bufC, w3, nl, B, bufD, w2, stream);
+            u64* nxt = (cur == bufA) ? bufB : bufA;
+            rescale_impl(c, bufD, w2, 2, nl, B, nxt, c->ct_words(nl - 1), nullptr, stream);
+            scale = scale * scale / (double)c->primes[level];
+            level -= 1;
+            cur = nxt;
+            cur_stride = c->ct_words(nl - 1);
+        } else if (m->activation == 2) {
+            // Eq. 2 cubic, schedule R23
+            const double c3 = -0.0061728, c2 = 0.092593, c1 = 0.59259, c0 = 0.49383;
+            const double S = scale, ql = (double)c->primes[level], ql1 = (double)c->primes[level - 1];
+            const size_t w3 = c->ct_words(nl, 3), w2 = c->ct_words(nl), w2m = c->ct_words(nl - 1),
+                         w2mm = c->ct_words(nl - 2);
+            u64* z = (u64*)cur;   // level l, in bufA or bufB
+            u64* other = (cur == bufA) ? bufB : bufA;
+            // z2 = rescale(relin(z (x) z)) -> other  (level l-1)
+            ck::tensor(L, z, z, cur_stride, bufC, w3, B, nl);
+            relin_impl(c, bufC, w3, nl, B, bufD, w2, stream);
+            rescale_impl(c, bufD, w2, 2, nl, B, other, w2m, nullptr, stream);
+            u64* z2 = other;
+            // a = rescale(z o [c3]_{ql}) + [c2]_S  -> bufD (level l-1)
+            std::vector<u64> res;
+            u64* dres = bufD + (size_t)B * w2m;   // small scratch after a
+            const_residues(c, round_away(c3 * ql), nl, res);
+            cuda_ok(cudaMemcpyAsync(dres, res.data(), nl * 8, cudaMemcpyHostToDevice, (cudaStream_t)stream), "c3");
+            ck::mul_scalar(L, z, cur_stride, bufC, w2, dres, B, 2, nl);
+            rescale_impl(c, bufC, w2, 2, nl, B, bufD, w2m, nullptr, stream);
+            const_residues(c, round_away(c2 * S), nl - 1, res);
+            cuda_ok(cudaMemcpyAsync(dres, res.data(), (nl - 1) * 8, cudaMemcpyHostToDevice, (cudaStream_t)stream), "c2");
+            ck::add_scalar(L, bufD, w2m, dres, B, nl - 1);
+            // h = rescale(relin(z2 (x) a)) -> bufC region reused: tensor into bufC, relin into
+            // a scratch after the tensor, rescale into `h` (level l-2)
+            ck::tensor(L, z2, bufD, w2m, bufC, c->ct_words(nl - 1, 3), B, nl - 1);
+            u64* rl = other;   // z2 is dead after the tensor
+            relin_impl(c, bufC, c->ct_words(nl - 1, 3), nl - 1, B, rl, w2m, stream);
+            u64* h = bufD;   // a no longer needed
+            rescale_impl(c, rl, w2m, 2, nl - 1, B, h, w2mm, nullptr, stream);
+            const double S3 = (S * S / ql) * S / ql1;
+            // g = drop(rescale(z o [c1]_{S3 ql / S})) + [c0]_{S3} -> accumulate into h
+            const_residues(c, round_away(c1 * (S3 * ql / S)), nl, res);
+            cuda_ok(cudaMemcpyAsync(dres + 64, res.data(), nl * 8, cudaMemcpyHostToDevice, (cudaStream_t)stream), "c1");
+            ck::mul_scalar(L, z, cur_stride, bufC, w2, dres + 64, B, 2, nl);
+            u64* g = other;   // z2 no longer needed
+            rescale_impl(c, bufC, w2, 2, nl, B, g, w2m, nullptr, stream);
+            const_residues(c, round_away(c0 * S3), nl - 2, res);
+            cuda_ok(cudaMemcpyAsync(dres + 128, res.data(), (nl - 2) * 8, cudaMemcpyHostToDevice, (cudaStream_t)stream),
+                    "c0");
+            // h += drop(g): add the first nl-2 limbs of each component of g
+            ck::add(L, h, w2mm, g, w2m, h, w2mm, B, 1, nl - 2);
+            ck::add(L, h + (size_t)(nl - 2) * c->n, w2mm, g + (size_t)(nl - 1) * c->n, w2m, h + (size_t)(nl - 2) * c->n,
+                    w2mm, B, 1, nl - 2);
+            ck::add_scalar(L, h, w2mm, dres + 128, B, nl - 2);
+            // move h to bufA/bufB for the next layer
+            u64* nxt = (cur == bufA) ? bufB : bufA;
+            cuda_ok(cudaMemcpyAsync(nxt, h, (size_t)B * w2mm * 8, cudaMemcpyDeviceToDevice, (cudaStream_t)stream), "mv");
+            scale = S3;
+            level -= 2;
+            cur = nxt;
+            cur_stride = w2mm;
+        }
+    }
+    *out_level = level;
+    *out_scale = scale;
+}
+
+static int model_out_level(const ckks_model* m)
+{
+    int lvl = (int)m->layers[0]->level;
+    for (size_t i = 0; i < m->layers.size(); ++i) {
+        lvl -= 1;
+        if (i + 1 < m->layers.size()) lvl -= (m->activation == 1 ? 1 : m->activation == 2 ? 2 : 0);
+    }
+    return lvl;
+}
+
+ckks_status ckks_encrypted_forward(ckks_ctx* c, const ckks_model* m, const ckks_ct* in, ckks_ct* out, void* work,
+                                   void* stream)
+{
+    CK_TRY({
+        if (!c || !m || !out || !out->data || !work) throw CkksError(CKKS_E_PARAM, "null");
+        check_ct(c, in);
+        if (in->level != m->layers[0]->level) throw CkksError(CKKS_E_SHAPE, "input level != first layer level");
+        const int nl_in = (int)in->level + 1, ol = model_out_level(m);
+        int lvl = 0;
+        double sc = 0;
+        for (uint32_t b0 = 0; b0 < in->batch; b0 += c->max_batch) {
+            const int B = (int)std::min<uint32_t>(c->max_batch, in->batch - b0);
+            forward_chunk(c, m, in->data + (size_t)b0 * c->ct_words(nl_in), c->ct_words(nl_in), B, in->scale,
+                          out->data + (size_t)b0 * c->ct_words(ol + 1), c->ct_words(ol + 1), (u64*)work, stream, &lvl,
+                          &sc);
+        }
+        out->batch = in->batch;
+        out->n_comp = 2;
+        out->level = (uint32_t)lvl;
+        out->scale = sc;
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_encrypted_forward_host(ckks_ctx* c, const ckks_model* m, const uint64_t* h_in, uint32_t batch,
+                                        uint32_t in_level, double in_scale, uint64_t* h_out, uint32_t* out_level,
+                                        double* out_scale, void* work, void* stream)
+{
+    CK_TRY({
+        if (!c || !m || !h_in || !h_out || !work) throw CkksError(CKKS_E_PARAM, "null");
+        if (in_level != m->layers[0]->level) throw CkksError(CKKS_E_SHAPE, "input level != first layer level");
+        const int nl_in = (int)in_level + 1, ol = model_out_level(m);
+        const int Bmax = (int)c->max_batch;
+        // device staging after the model workspace: [Bmax] input cts + [Bmax] output cts
+        const size_t mw = model_work_words(c, m, Bmax);
+        u64* d_in = (u64*)work + mw;
+        u64* d_out = d_in + (size_t)Bmax * c->ct_words(nl_in);
+        cudaStream_t st = (cudaStream_t)stream;
+        int lvl = 0;
+        double sc = 0;
+        for (uint32_t b0 = 0; b0 < batch; b0 += Bmax) {
+            const int B = (int)std::min<uint32_t>(Bmax, batch - b0);
+            cuda_ok(cudaMemcpyAsync(d_in, h_in + (size_t)b0 * c->ct_words(nl_in), (size_t)B * c->ct_words(nl_in) * 8,
+                                    cudaMemcpyHostToDevice, st), "h2d");
+            forward_chunk(c, m, d_in, c->ct_words(nl_in), B, in_scale, d_out, c->ct_words(ol + 1), (u64*)work, stream,
+                          &lvl, &sc);
+            cuda_ok(cudaMemcpyAsync(h_out + (size_t)b0 * c->ct_words(ol + 1), d_out, (size_t)B * c->ct_words(ol + 1) * 8,
+                                    cudaMemcpyDeviceToHost, st), "d2h");
+        }
+        cuda_ok(cudaStreamSynchronize(st), "forward_host");
+        if (out_level) *out_level = (uint32_t)lvl;
+        if (out_scale) *out_scale = sc;
+        return CKKS_OK;
+    })
+}
+
+// ------------------------------------------------------------------------------------ client side
+ckks_status ckks_encode(const ckks_ctx* c, const double* values, uint32_t count, double scale, int64_t* coeffs)
+{
+    CK_TRY({
+        if (!c || (!values && count) || !coeffs) throw CkksError(CKKS_E_PARAM, "null");
+        encode_host(c->n, values, count, scale, coeffs);
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_encrypt(ckks_ctx* c, const int64_t* h_coeffs, uint32_t batch, uint64_t enc_seed,
+                         uint64_t first_index, double scale, ckks_ct* out, void* stream)
+{
+    CK_TRY({
+        if (!c || !h_coeffs || !out || !out->data) throw CkksError(CKKS_E_PARAM, "null");
+        const int L = c->L, n = c->n;
+        auto Lc = c->launch(stream);
+        cudaStream_t st = (cudaStream_t)stream;
+        for (uint32_t b0 = 0; b0 < batch; b0 += c->max_batch) {
+            const int B = (int)std::min<uint32_t>(c->max_batch, batch - b0);
+            u64* u = c->d_work;
+            u64* e0 = u + (size_t)B * L * n;
+            u64* e1 = e0 + (size_t)B * L * n;
+            u64* mm = e1 + (size_t)B * L * n;
+            int64_t* stage = (int64_t*)(mm + (size_t)B * L * n);
+            cuda_ok(cudaMemcpyAsync(stage, h_coeffs + (size_t)b0 * n, (size_t)B * n * 8, cudaMemcpyHostToDevice, st),
+                    "upload m");
+            ck::signed_to_ntt(Lc, stage, mm, B, L);
+            ck::sample_ntt(Lc, u, B, L, L, 0, enc_seed, 6, first_index + b0, 1, 0, 0);
+            ck::sample_ntt(Lc, e0, B, L, L, 1, enc_seed, 7, first_index + b0, 1, 0, 0);
+            ck::sample_ntt(Lc, e1, B, L, L, 1, enc_seed, 8, first_index + b0, 1, 0, 0);
+            ck::encrypt_combine(Lc, c->d_pk, u, e0, e1, mm, out->data + (size_t)b0 * c->ct_words(L), B, L);
+            cuda_ok(cudaStreamSynchronize(st), "encrypt");   // staging reused by the next chunk
+        }
+        out->batch = batch;
+        out->n_comp = 2;
+        out->level = (uint32_t)(L - 1);
+        out->scale = scale;
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_decrypt(ckks_ctx* c, const ckks_ct* in, uint64_t* d_out, void* stream)
+{
+    CK_TRY({
+        if (!c || !d_out) throw CkksError(CKKS_E_PARAM, "null");
+        check_ct(c, in);
+        const int nl = (int)in->level + 1;
+        auto L = c->launch(stream);
+        for (uint32_t b0 = 0; b0 < in->batch; b0 += 65535) {
+            const int B = (int)std::min<uint32_t>(65535, in->batch - b0);
+            ck::decrypt(L, in->data + (size_t)b0 * c->ct_words(nl), c->ct_words(nl), c->d_s,
+                        d_out + (size_t)b0 * nl * c->n, B, nl);
+        }
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_decode(const ckks_ctx* c, const uint64_t* res, uint32_t level, double scale, double* values,
+                        uint32_t count)
+{
+    CK_TRY({
+        if (!c || !res || !values) throw CkksError(CKKS_E_PARAM, "null");
+        if ((int)level >= c->L) throw CkksError(CKKS_E_SHAPE, "level");
+        const int n = c->n, nl = (int)level + 1;
+        if (count > (uint32_t)n / 2) throw CkksError(CKKS_E_PARAM, "count > slots");
+        // balanced mixed-radix (Garner) lift: x = sum_i v_i M_i, v_i in (-q_i/2, q_i/2], M_i = q_0..q_{i-1}
+        std::vector<std::vector<u64>> inv(nl, std::vector<u64>(nl));
+        for (int i = 0; i < nl; ++i)
+            for (int k = 0; k < i; ++k) inv[k][i] = h_pow(c->primes[k] % c->primes[i], c->primes[i] - 2, c->primes[i]);
+        std::vector<std::complex<double>> M(2 * (size_t)n, 0.0);
+        std::vector<int64_t> v(nl);
+        for (int k = 0; k < n; ++k) {
+            for (int i = 0; i < nl; ++i) {
+                const u64 q = c->primes[i];
+                // t = (x - sum_{j<i} v_j M_j) / M_i mod q, evaluated incrementally
+                u64 t = res[(size_t)i * n + k] % q;
+                for (int j = 0; j < i; ++j) {
+                    const u64 vj = v[j] >= 0 ? (u64)v[j] % q : (q - ((u64)(-v[j]) % q)) % q;
+                    t = (t + q - vj) % q;
+                    t = h_mulmod(t, inv[j][i], q);
+                }
+                v[i] = t > q / 2 ? (int64_t)t - (int64_t)q : (int64_t)t;
+            }
+            long double x = 0, Mi = 1;
+            for (int i = 0; i < nl; ++i) {
+                x += (long double)v[i] * Mi;
+                Mi *= (long double)c->primes[i];
+            }
+            M[k] = (double)x;
+        }
+        fft(M, +1);   // M[e] = sum_k m_k exp(+2 pi i e k / 2N)
+        const auto e = slot_exps(n);
+        for (uint32_t i = 0; i < count; ++i) values[i] = M[e[i]].real() / scale;
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_export_key(ckks_ctx* c, int64_t key_id, uint64_t* h_out, void* stream)
+{
+    CK_TRY({
+        if (!c || !h_out) throw CkksError(CKKS_E_PARAM, "null");
+        cudaStream_t st = (cudaStream_t)stream;
+        if (key_id == -1) {
+            cuda_ok(cudaMemcpyAsync(h_out, c->d_s, (size_t)c->np * c->n * 8, cudaMemcpyDeviceToHost, st), "export s");
+        } else if (key_id == -2) {
+            cuda_ok(cudaMemcpyAsync(h_out, c->d_pk, (size_t)2 * c->L * c->n * 8, cudaMemcpyDeviceToHost, st), "export pk");
+        } else {
+            const u64* k = c->key(key_id);
+            if (!k) throw CkksError(CKKS_E_NOKEY, "no such key");
+            cuda_ok(cudaMemcpyAsync(h_out, k, c->key_words * 8, cudaMemcpyDeviceToHost, st), "export key");
+        }
+        cuda_ok(cudaStreamSynchronize(st), "export");
+        return CKKS_OK;
+    })
+}
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// common.cuh -- device-side types and modular arithmetic for the B200 CKKS path.
+//
+// Residues are 64-bit words modulo primes q < 2^61 (R1).  Products use the integer pipes:
+//   * Shoup multiplication by a precomputed constant w (w' = floor(w 2^64 / q)):
+//         shoup(a, w) = a w - floor(a w' / 2^64) q  in [0, 2q)   for any a < 2^64.
+//   * 128-bit reduction  x = hi 2^64 + lo  ->  shoup(hi, 2^64 mod q) + shoup(lo, 1)  in [0, 4q).
+// Lazy ranges are stated at every use.
+#pragma once
+#include <cstdint>
+
+typedef uint64_t u64;
+typedef uint32_t u32;
+
+#define CKKS_MAXP 16
+
+struct DPrime {
+    u64 q, q2;
+    u64 ninv, ninv_sh;   // N^{-1} mod q and its Shoup companion
+    u64 one_sh;          // floor(2^64 / q): Shoup companion of 1
+    u64 r64, r64_sh;     // 2^64 mod q and companion
+};
+
+// Per-context constants, resident in device memory (tables buffer).
+struct DCtx {
+    int log_n, n, n_data, n_special, n_primes;
+    int pad_;
+    DPrime p[CKKS_MAXP];
+    u64 qmod[CKKS_MAXP][CKKS_MAXP];     // q_a mod q_b
+    u64 qinv[CKKS_MAXP][CKKS_MAXP];     // q_a^{-1} mod q_b   (a != b)
+    u64 qinv_sh[CKKS_MAXP][CKKS_MAXP];
+    const u64* tw;                      // [n_primes][4][N]: W, W', IW, IW'  (bit-reversed psi powers)
+    u64 cdt[40];                        // discrete Gaussian CDT thresholds (R13)
+    int cdt_bound;
+};
+
+__device__ __forceinline__ u64 csub(u64 a, u64 m) { return a >= m ? a - m : a; }
+
+__device__ __forceinline__ u64 shoup_mul(u64 a, u64 w, u64 wsh, u64 q)
+{
+    u64 h = __umul64hi(a, wsh);
+    return a * w - h * q;   // [0, 2q)
+}
+
+// any 64-bit a -> [0, 2q)
+__device__ __forceinline__ u64 reduce64_lazy(u64 a, const DPrime& P)
+{
+    return a - __umul64hi(a, P.one_sh) * P.q;
+}
+__device__ __forceinline__ u64 reduce64(u64 a, const DPrime& P) { return csub(reduce64_lazy(a, P), P.q); }
+
+// (hi, lo) 128-bit -> [0, q)
+__device__ __forceinline__ u64 reduce128(u64 hi, u64 lo, const DPrime& P)
+{
+    u64 a = shoup_mul(hi, P.r64, P.r64_sh, P.q);   // [0, 2q)
+    u64 b = reduce64_lazy(lo, P);                  // [0, 2q)
+    u64 s = a + b;                                 // [0, 4q) < 2^63
+    s = csub(s, P.q2);
+    return csub(s, P.q);
+}
+
+__device__ __forceinline__ u64 mulmod(u64 a, u64 b, const DPrime& P)
+{
+    return reduce128(__umul64hi(a, b), a * b, P);
+}
+
+// 128-bit accumulator
+struct Acc128 {
+    u64 lo, hi;
+    __device__ __forceinline__ void zero() { lo = 0; hi = 0; }
+    __device__ __forceinline__ void mac(u64 a, u64 b)
+    {
+        u64 plo = a * b, phi = __umul64hi(a, b);
+        lo += plo;
+        hi += phi + (lo < plo ? 1 : 0);
+    }
+    __device__ __forceinline__ u64 reduce(const DPrime& P) const { return reduce128(hi, lo, P); }
+};
+
+__device__ __forceinline__ u64 addmod(u64 a, u64 b, u64 q) { return csub(a + b, q); }
+__device__ __forceinline__ u64 submod(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
+
+// centered residue r in [0, m) (m odd) reduced mod prime b: r if r <= (m-1)/2 else r - m  (R10)
+__device__ __forceinline__ u64 centered_to(u64 r, u64 m, u64 m_mod_b, const DPrime& B)
+{
+    if (r <= (m >> 1)) return reduce64(r, B);
+    // r - m  ==  r mod b  - (m mod b)
+    u64 rb = reduce64(r, B);
+    return submod(rb, m_mod_b, B.q);
+}
+
+__device__ __forceinline__ u32 brev32(u32 x, int bits) { return __brev(x) >> (32 - bits); }

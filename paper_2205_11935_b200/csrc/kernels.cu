@@ -1,0 +1,691 @@
+// kernels.cu -- sm_100a kernels of the CKKS encrypted-dense-layer hot path.
+//
+// Every operation of SURVEY 8(a) rows a2-a12 is one of these kernels; the host side (api.cpp)
+// only sequences launches and tracks level/scale.  Integer pipes only (no tensor cores: nothing
+// here is a floating-point contraction).  Layouts:
+//   ciphertext  [batch][comp][limb][N]  u64, NTT domain, canonical residues in [0, q)
+//   key         [digit j][comp][prime 0..L][N]  (prime L = special P)
+//   plaintexts  [t][limb][N]
+#include "common.cuh"
+#include "ntt.cuh"
+#include "kernels.h"
+
+#include <stdexcept>
+#include <string>
+
+namespace ck {
+
+// ------------------------------------------------------------------------------------ helpers
+__device__ __forceinline__ const u64* twp(const DCtx* dc, int p) { return dc->tw + (size_t)p * 4 * dc->n; }
+
+// NTT-domain automorphism (R3): out[k] = in[src(k)] with 2 brev(src)+1 = g (2 brev(k)+1) mod 2N
+__device__ __forceinline__ int galois_src(int k, u32 g, int logn)
+{
+    const u32 e = 2u * brev32((u32)k, logn) + 1u;
+    const u32 eg = (e * g) & ((2u << logn) - 1u);
+    return (int)brev32((eg - 1u) >> 1, logn);
+}
+
+static void check_launch(const char* what)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class K>
+static void allow_smem(K kernel, size_t bytes)
+{
+    if (bytes > 48 * 1024) {
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    }
+}
+
+#define NTT_DISPATCH(LOGN_VAR, ...)                                                     \
+    switch (LOGN_VAR) {                                                                  \
+    case 10: { constexpr int LG = 10; __VA_ARGS__; } break;                                     \
+    case 11: { constexpr int LG = 11; __VA_ARGS__; } break;                                     \
+    case 12: { constexpr int LG = 12; __VA_ARGS__; } break;                                     \
+    case 13: { constexpr int LG = 13; __VA_ARGS__; } break;                                     \
+    case 14: { constexpr int LG = 14; __VA_ARGS__; } break;                                     \
+    default: throw std::runtime_error("unsupported log_n");                              \
+    }
+
+// ------------------------------------------------------------------------------------ PRNG (R15)
+__device__ __forceinline__ u64 mix64(u64 z)
+{
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ u64 prng(u64 seed, u64 stream, u64 i)
+{
+    const u64 k = mix64(seed ^ mix64(stream));
+    return mix64(k + (i + 1) * 0x9E3779B97F4A7C15ULL);
+}
+__device__ __forceinline__ u64 stream_tag(u64 purpose, u64 id, u64 digit, u64 prime)
+{
+    return (purpose << 56) | ((id & 0xFFFFFFFFFULL) << 20) | ((digit & 0x3FF) << 10) | (prime & 0x3FF);
+}
+__device__ __forceinline__ long long sample_small(const DCtx* dc, int kind, u64 seed, u64 stream, u64 i)
+{
+    const u64 r = prng(seed, stream, i);
+    if (kind == 0) return (long long)(((r >> 32) * 3ULL) >> 32) - 1;   // ternary (R14)
+    const int B = dc->cdt_bound;                                         // CDT Gaussian (R13)
+    long long v = -B;
+    for (int k = 0; k < 2 * B; ++k) v += (r >= dc->cdt[k]) ? 1 : 0;
+    return v;
+}
+__device__ __forceinline__ u64 signed_to_res(long long x, const DPrime& P)
+{
+    if (x >= 0) return reduce64((u64)x, P);
+    const u64 m = reduce64((u64)(-(x + 1)) + 1ULL, P);
+    return m ? P.q - m : 0;
+}
+
+// ------------------------------------------------------------------------------------ NTT batch
+template <int LOGN, bool INV>
+__global__ void __launch_bounds__(NttThreads<LOGN>::value)
+k_ntt_batch(const DCtx* __restrict__ dc, u64* __restrict__ data, int limbs, int prime0)
+{
+    extern __shared__ u64 sm[];
+    using T = NttCta<LOGN, NttThreads<LOGN>::value>;
+    const int l = blockIdx.x, b = blockIdx.y, p = prime0 + l;
+    u64* a = data + ((size_t)b * limbs + l) * T::N;
+    const DPrime Pr = dc->p[p];
+    auto ld = [&](int i) { return a[i]; };
+    auto st = [&](int i, u64 v) { a[i] = v; };
+    if constexpr (INV) T::inverse(sm, Pr, twp(dc, p), ld, st);
+    else T::forward(sm, Pr, twp(dc, p), ld, st);
+}
+
+void ntt_batch(const Launch& L, uint64_t* data, int batch, int limbs, int prime0, bool inverse)
+{
+    if (batch <= 0 || limbs <= 0) return;
+    const size_t smem = sizeof(u64) << L.log_n;
+    NTT_DISPATCH(L.log_n, {
+        constexpr int NT = NttThreads<LG>::value;
+        auto k = inverse ? k_ntt_batch<LG, true> : k_ntt_batch<LG, false>;
+        allow_smem(k, smem);
+        const bool pr = L.probe && L.probe->on(PROBE_NTT);
+        if (pr) {
+            L.probe->mark(L.st);
+            L.probe->alg_bytes += 2.0 * batch * limbs * (double)(8 << L.log_n);   // read + write each limb once
+        }
+        k<<<dim3(limbs, batch), NT, smem, L.st>>>(L.dc, data, limbs, prime0);
+        if (pr) L.probe->mark(L.st);
+    });
+    check_launch("ntt_batch");
+    if (L.counter) ++*L.counter;
+}
+
+// ------------------------------------------------------------------------------------ key switch
+// (1) digits: d_j = iNTT_{q_j}(sigma_g(d)[j])  -> [B][nl][N] in [0, q_j)                  (R9)
+template <int LOGN>
+__global__ void __launch_bounds__(NttThreads<LOGN>::value)
+k_ks_digits(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t ct_stride, size_t comp_off,
+            u32 galois, u64* __restrict__ digits, int nl)
+{
+    extern __shared__ u64 sm[];
+    using T = NttCta<LOGN, NttThreads<LOGN>::value>;
+    const int j = blockIdx.x, b = blockIdx.y;
+    const u64* src = in + (size_t)b * ct_stride + comp_off + (size_t)j * T::N;
+    u64* dst = digits + ((size_t)b * nl + j) * T::N;
+    const DPrime Pr = dc->p[j];
+    auto ld = [&](int i) { return galois ? src[galois_src(i, galois, LOGN)] : src[i]; };
+    auto st = [&](int i, u64 v) { dst[i] = v; };
+    T::inverse(sm, Pr, twp(dc, j), ld, st);
+}
+
+// (2) ModUp: D_{j,e} = NTT_{p_e}(d_j mod p_e) for e != j, e in [0, nl] (nl = special)
+template <int LOGN>
+__global__ void __launch_bounds__(NttThreads<LOGN>::value)
+k_ks_modup(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* __restrict__ modup, int nl, int special)
+{
+    extern __shared__ u64 sm[];
+    using T = NttCta<LOGN, NttThreads<LOGN>::value>;
+    const int j = blockIdx.x / nl;
+    int e = blockIdx.x % nl;
+    if (e >= j) ++e;
+    const int b = blockIdx.y;
+    const int p = (e == nl) ? special : e;
+    const DPrime Pr = dc->p[p];
+    const u64* src = digits + ((size_t)b * nl + j) * T::N;
+    u64* dst = modup + (((size_t)b * nl + j) * (nl + 1) + e) * T::N;
+    auto ld = [&](int i) { return reduce64_lazy(src[i], Pr); };
+    auto st = [&](int i, u64 v) { dst[i] = v; };
+    T::forward(sm, Pr, twp(dc, p), ld, st);
+}
+
+// (3) inner product u_c[e] = sum_j D_{j,e} key_j.c[p_e]  (128-bit accumulation, one reduction)
+__global__ void __launch_bounds__(256)
+k_ks_ip(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ in, size_t ct_stride,
+        size_t comp_off, u32 galois, const u64* __restrict__ key, int L, int nl, int special, u64* __restrict__ acc)
+{
+    const int n = dc->n, logn = dc->log_n;
+    const int k = blockIdx.x * 256 + threadIdx.x;
+    const int e = blockIdx.y, b = blockIdx.z;
+    const int p = (e == nl) ? special : e;
+    const int pk = (e == nl) ? L : e;
+    const DPrime Pr = dc->p[p];
+    Acc128 a0, a1;
+    a0.zero();
+    a1.zero();
+    for (int j = 0; j < nl; ++j) {
+        u64 dv;
+        if (j == e) {
+            const u64* src = in + (size_t)b * ct_stride + comp_off + (size_t)j * n;
+            dv = galois ? src[galois_src(k, galois, logn)] : src[k];
+        } else {
+            dv = modup[(((size_t)b * nl + j) * (nl + 1) + e) * n + k];
+        }
+        const u64 k0 = key[(((size_t)j * 2 + 0) * (L + 1) + pk) * n + k];
+        const u64 k1 = key[(((size_t)j * 2 + 1) * (L + 1) + pk) * n + k];
+        a0.mac(dv, k0);
+        a1.mac(dv, k1);
+    }
+    acc[(((size_t)b * 2 + 0) * (nl + 1) + e) * n + k] = a0.reduce(Pr);
+    acc[(((size_t)b * 2 + 1) * (nl + 1) + e) * n + k] = a1.reduce(Pr);
+}
+
+// (4) ModDown part 1: r_c = iNTT_P(u_c[P])
+template <int LOGN>
+__global__ void __launch_bounds__(NttThreads<LOGN>::value)
+k_ks_moddown_intt(const DCtx* __restrict__ dc, const u64* __restrict__ acc, u64* __restrict__ rem, int nl, int special)
+{
+    extern __shared__ u64 sm[];
+    using T = NttCta<LOGN, NttThreads<LOGN>::value>;
+    const int c = blockIdx.x, b = blockIdx.y;
+    const u64* src = acc + (((size_t)b * 2 + c) * (nl + 1) + nl) * T::N;
+    u64* dst = rem + ((size_t)b * 2 + c) * T::N;
+    const DPrime Pr = dc->p[special];
+    auto ld = [&](int i) { return src[i]; };
+    auto st = [&](int i, u64 v) { dst[i] = v; };
+    T::inverse(sm, Pr, twp(dc, special), ld, st);
+}
+
+// (5) ModDown part 2: out_c[i] = (u_c[i] - NTT_{q_i}(centered(r_c) mod q_i)) P^{-1}  (+ addend)
+template <int LOGN>
+__global__ void __launch_bounds__(NttThreads<LOGN>::value)
+k_ks_moddown_out(const DCtx* __restrict__ dc, const u64* __restrict__ acc, const u64* __restrict__ rem, int nl,
+                 int special, u64* __restrict__ out, size_t out_stride, const u64* __restrict__ add,
+                 size_t add_stride, u32 add_galois, int add_comp1, int accumulate)
+{
+    extern __shared__ u64 sm[];
+    using T = NttCta<LOGN, NttThreads<LOGN>::value>;
+    const int i = blockIdx.x, c = blockIdx.y, b = blockIdx.z;
+    const DPrime Pr = dc->p[i];
+    const u64 Pmod = dc->qmod[special][i];
+    const u64 Pinv = dc->qinv[special][i], Pinv_sh = dc->qinv_sh[special][i];
+    const u64 Pbig = dc->p[special].q;
+    const u64* r = rem + ((size_t)b * 2 + c) * T::N;
+    const u64* u = acc + (((size_t)b * 2 + c) * (nl + 1) + i) * T::N;
+    u64* o = out + (size_t)b * out_stride + ((size_t)c * nl + i) * T::N;
+    const u64* ad = nullptr;
+    if (add && (c == 0 || add_comp1)) ad = add + (size_t)b * add_stride + ((size_t)c * nl + i) * T::N;
+    auto ld = [&](int k) { return centered_to(r[k], Pbig, Pmod, Pr); };
+    auto st = [&](int k, u64 v) {
+        u64 x = shoup_mul(u[k] + Pr.q - v, Pinv, Pinv_sh, Pr.q);   // [0, 2q)
+        x = csub(x, Pr.q);
+        if (ad) x = addmod(x, add_galois ? ad[galois_src(k, add_galois, LOGN)] : ad[k], Pr.q);
+        if (accumulate) x = addmod(x, o[k], Pr.q);
+        o[k] = x;
+    };
+    T::forward(sm, Pr, twp(dc, i), ld, st);
+}
+
+void keyswitch(const Launch& L, const KsIn& in, const uint64_t* key, int batch, int nl, const KsWork& w,
+               const KsOut& out)
+{
+    if (batch <= 0) return;
+    const int special = L.n_data;   // special prime is stored after the data primes
+    const size_t smem = sizeof(u64) << L.log_n;
+    const int n = 1 << L.log_n;
+    NTT_DISPATCH(L.log_n, {
+        constexpr int NT = NttThreads<LG>::value;
+        allow_smem(k_ks_digits<LG>, smem);
+        allow_smem(k_ks_modup<LG>, smem);
+        allow_smem(k_ks_moddown_intt<LG>, smem);
+        allow_smem(k_ks_moddown_out<LG>, smem);
+        const bool pk = L.probe && L.probe->on(PROBE_KEYSWITCH), pm = L.probe && L.probe->on(PROBE_MODUP);
+        if (pk) {
+            L.probe->mark(L.st);
+            // switched component + addend in, 2 components out, key rows used once per launch
+            L.probe->alg_bytes += (4.0 * batch * nl + 2.0 * nl * (nl + 1)) * (double)(8 << L.log_n);
+        }
+        k_ks_digits<LG><<<dim3(nl, batch), NT, smem, L.st>>>(L.dc, in.base, in.ct_stride, in.comp_off, in.galois,
+                                                              w.digits, nl);
+        if (pm) {
+            L.probe->mark(L.st);
+            // digits read once, nl x nl ModUp limbs written
+            L.probe->alg_bytes += ((double)batch * nl + (double)batch * nl * nl) * (double)(8 << L.log_n);
+        }
+        k_ks_modup<LG><<<dim3(nl * nl, batch), NT, smem, L.st>>>(L.dc, w.digits, w.modup, nl, special);
+        if (pm) L.probe->mark(L.st);
+        k_ks_ip<<<dim3(n / 256, nl + 1, batch), 256, 0, L.st>>>(L.dc, w.modup, in.base, in.ct_stride, in.comp_off,
+                                                               in.galois, key, L.n_data, nl, special, w.acc);
+        k_ks_moddown_intt<LG><<<dim3(2, batch), NT, smem, L.st>>>(L.dc, w.acc, w.rem, nl, special);
+        k_ks_moddown_out<LG><<<dim3(nl, 2, batch), NT, smem, L.st>>>(L.dc, w.acc, w.rem, nl, special, out.base,
+                                                                     out.ct_stride, out.add, out.add_stride,
+                                                                     out.add_galois, out.add_comp1, out.accumulate);
+        if (pk) L.probe->mark(L.st);
+    });
+    check_launch("keyswitch");
+    if (L.counter) *L.counter += 5;
+}
+
+// ------------------------------------------------------------------------------------ rescale
+template <int LOGN>
+__global__ void __launch_bounds__(NttThreads<LOGN>::value)
+k_rescale_intt(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t in_stride, int ncomp, int nl,
+               u64* __restrict__ rem)
+{
+    extern __shared__ u64 sm[];
+    using T = NttCta<LOGN, NttThreads<LOGN>::value>;
+    const int c = blockIdx.x, b = blockIdx.y, l = nl - 1;
+    const u64* src = in + (size_t)b * in_stride + ((size_t)c * nl + l) * T::N;
+    u64* dst = rem + ((size_t)b * ncomp + c) * T::N;
+    const DPrime Pr = dc->p[l];
+    auto ld = [&](int i) { return src[i]; };
+    auto st = [&](int i, u64 v) { dst[i] = v; };
+    T::inverse(sm, Pr, twp(dc, l), ld, st);
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttThreads<LOGN>::value)
+k_rescale_out(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t in_stride, int ncomp, int nl,
+              const u64* __restrict__ rem, u64* __restrict__ out, size_t out_stride, const u64* __restrict__ bias)
+{
+    extern __shared__ u64 sm[];
+    using T = NttCta<LOGN, NttThreads<LOGN>::value>;
+    const int i = blockIdx.x, c = blockIdx.y, b = blockIdx.z, l = nl - 1;
+    const DPrime Pr = dc->p[i];
+    const u64 qlmod = dc->qmod[l][i];
+    const u64 qlinv = dc->qinv[l][i], qlinv_sh = dc->qinv_sh[l][i];
+    const u64 ql = dc->p[l].q;
+    const u64* r = rem + ((size_t)b * ncomp + c) * T::N;
+    const u64* a = in + (size_t)b * in_stride + ((size_t)c * nl + i) * T::N;
+    u64* o = out + (size_t)b * out_stride + ((size_t)c * (nl - 1) + i) * T::N;
+    const u64* bi = (bias && c == 0) ? bias + (size_t)i * T::N : nullptr;
+    auto ld = [&](int k) { return centered_to(r[k], ql, qlmod, Pr); };
+    auto st = [&](int k, u64 v) {
+        u64 x = csub(shoup_mul(a[k] + Pr.q - v, qlinv, qlinv_sh, Pr.q), Pr.q);
+        if (bi) x = addmod(x, bi[k], Pr.q);
+        o[k] = x;
+    };
+    T::forward(sm, Pr, twp(dc, i), ld, st);
+}
+
+void rescale(const Launch& L, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, int batch,
+             int ncomp, int nl, uint64_t* rem, const uint64_t* bias)
+{
+    if (batch <= 0) return;
+    const size_t smem = sizeof(u64) << L.log_n;
+    NTT_DISPATCH(L.log_n, {
+        constexpr int NT = NttThreads<LG>::value;
+        allow_smem(k_rescale_intt<LG>, smem);
+        allow_smem(k_rescale_out<LG>, smem);
+        k_rescale_intt<LG><<<dim3(ncomp, batch), NT, smem, L.st>>>(L.dc, in, in_stride, ncomp, nl, rem);
+        k_rescale_out<LG><<<dim3(nl - 1, ncomp, batch), NT, smem, L.st>>>(L.dc, in, in_stride, ncomp, nl, rem, out,
+                                                                         out_stride, bias);
+    });
+    check_launch("rescale");
+    if (L.counter) *L.counter += 2;
+}
+
+// ------------------------------------------------------------------------------------ elementwise
+__global__ void __launch_bounds__(256)
+k_tensor(const DCtx* __restrict__ dc, const u64* __restrict__ a, const u64* __restrict__ bb, size_t stride,
+         u64* __restrict__ out, size_t out_stride, int nl)
+{
+    const int n = dc->n;
+    const int k = blockIdx.x * 256 + threadIdx.x, l = blockIdx.y, b = blockIdx.z;
+    const DPrime Pr = dc->p[l];
+    const u64* A = a + (size_t)b * stride;
+    const u64* B = bb + (size_t)b * stride;
+    const size_t i0 = (size_t)l * n + k, i1 = ((size_t)nl + l) * n + k;
+    const u64 a0 = A[i0], a1 = A[i1], b0 = B[i0], b1 = B[i1];
+    u64* O = out + (size_t)b * out_stride;
+    O[i0] = mulmod(a0, b0, Pr);
+    Acc128 m;
+    m.zero();
+    m.mac(a0, b1);
+    m.mac(a1, b0);
+    O[i1] = m.reduce(Pr);
+    O[((size_t)2 * nl + l) * n + k] = mulmod(a1, b1, Pr);
+}
+
+void tensor(const Launch& L, const uint64_t* a, const uint64_t* b, size_t stride, uint64_t* out3, size_t out_stride,
+            int batch, int nl)
+{
+    if (batch <= 0) return;
+    const int n = 1 << L.log_n;
+    k_tensor<<<dim3(n / 256, nl, batch), 256, 0, L.st>>>(L.dc, a, b, stride, out3, out_stride, nl);
+    check_launch("tensor");
+    if (L.counter) ++*L.counter;
+}
+
+__global__ void __launch_bounds__(256)
+k_add(const DCtx* __restrict__ dc, const u64* __restrict__ a, size_t sa, const u64* __restrict__ bb, size_t sb,
+      u64* __restrict__ out, size_t so, int nl)
+{
+    const int n = dc->n;
+    const int k = blockIdx.x * 256 + threadIdx.x, cl = blockIdx.y, b = blockIdx.z;
+    const int l = cl % nl;
+    const u64 q = dc->p[l].q;
+    const size_t off = (size_t)cl * n + k;
+    out[(size_t)b * so + off] = addmod(a[(size_t)b * sa + off], bb[(size_t)b * sb + off], q);
+}
+
+void add(const Launch& L, const uint64_t* a, size_t sa, const uint64_t* b, size_t sb, uint64_t* out, size_t so,
+         int batch, int ncomp, int nl)
+{
+    if (batch <= 0) return;
+    const int n = 1 << L.log_n;
+    k_add<<<dim3(n / 256, ncomp * nl, batch), 256, 0, L.st>>>(L.dc, a, sa, b, sb, out, so, nl);
+    check_launch("add");
+    if (L.counter) ++*L.counter;
+}
+
+// BSGS inner sums (Eq. 1 inner parenthesis), weights-stationary:
+//   w_k[b] = sum_{j<t1} pt_{k t1 + j} o v_j[b],   v_0 = input ct, v_j = rot_j(input).
+// Thread (coefficient x, giant index k) keeps its t1 plaintext words in registers and loops over the
+// batch, so every plaintext word is read once per launch; v words are shared through L1 by the t2
+// threads of the same coefficient.
+template <int T1MAX>
+__global__ void __launch_bounds__(256)
+k_bsgs_mac(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u64* __restrict__ v0,
+           size_t v0_stride, const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl)
+{
+    const int n = dc->n;
+    const int x = blockIdx.x * 32 + threadIdx.x, l = blockIdx.y, k = blockIdx.z * blockDim.y + threadIdx.y;
+    if (k >= t2) return;
+    const DPrime Pr = dc->p[l];
+    const size_t ctw = (size_t)2 * nl * n;
+    u64 pv[T1MAX];
+#pragma unroll
+    for (int j = 0; j < T1MAX; ++j)
+        pv[j] = (j < t1) ? pts[((size_t)(k * t1 + j) * nl + l) * n + x] : 0;
+    for (int b = 0; b < batch; ++b) {
+        Acc128 a0, a1;
+        a0.zero();
+        a1.zero();
+#pragma unroll
+        for (int j = 0; j < T1MAX; ++j) {
+            if (j < t1) {
+                const u64* v = (j == 0) ? v0 + (size_t)b * v0_stride : vb + ((size_t)(j - 1) * batch + b) * ctw;
+                a0.mac(pv[j], v[(size_t)l * n + x]);
+                a1.mac(pv[j], v[((size_t)nl + l) * n + x]);
+            }
+        }
+        u64* w = wout + ((size_t)k * batch + b) * ctw;
+        w[(size_t)l * n + x] = a0.reduce(Pr);
+        w[((size_t)nl + l) * n + x] = a1.reduce(Pr);
+    }
+}
+
+void bsgs_mac(const Launch& L, const uint64_t* pts, const uint64_t* v0, size_t v0_stride, const uint64_t* vbaby,
+              uint64_t* wout, int t1, int t2, int batch, int nl)
+{
+    if (batch <= 0) return;
+    const int n = 1 << L.log_n;
+    if (t1 > 32) throw std::runtime_error("bsgs_mac: t1 <= 32");
+    const int ky = 8;
+    dim3 grid(n / 32, nl, (t2 + ky - 1) / ky), block(32, ky);
+    if (t1 <= 8) k_bsgs_mac<8><<<grid, block, 0, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl);
+    else if (t1 <= 16) k_bsgs_mac<16><<<grid, block, 0, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl);
+    else k_bsgs_mac<32><<<grid, block, 0, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl);
+    check_launch("bsgs_mac");
+    if (L.counter) ++*L.counter;
+}
+
+// ------------------------------------------------------------------------------------ decrypt
+template <int LOGN>
+__global__ void __launch_bounds__(NttThreads<LOGN>::value)
+k_decrypt(const DCtx* __restrict__ dc, const u64* __restrict__ ct, size_t ct_stride, const u64* __restrict__ s_ntt,
+          u64* __restrict__ out, int nl)
+{
+    extern __shared__ u64 sm[];
+    using T = NttCta<LOGN, NttThreads<LOGN>::value>;
+    const int l = blockIdx.x, b = blockIdx.y;
+    const DPrime Pr = dc->p[l];
+    const u64* c0 = ct + (size_t)b * ct_stride + (size_t)l * T::N;
+    const u64* c1 = ct + (size_t)b * ct_stride + ((size_t)nl + l) * T::N;
+    const u64* s = s_ntt + (size_t)l * T::N;
+    u64* o = out + ((size_t)b * nl + l) * T::N;
+    auto ld = [&](int i) { return addmod(c0[i], mulmod(c1[i], s[i], Pr), Pr.q); };
+    auto st = [&](int i, u64 v) { o[i] = v; };
+    T::inverse(sm, Pr, twp(dc, l), ld, st);
+}
+
+void decrypt(const Launch& L, const uint64_t* ct, size_t ct_stride, const uint64_t* s_ntt, uint64_t* out, int batch,
+             int nl)
+{
+    if (batch <= 0) return;
+    const size_t smem = sizeof(u64) << L.log_n;
+    NTT_DISPATCH(L.log_n, {
+        constexpr int NT = NttThreads<LG>::value;
+        allow_smem(k_decrypt<LG>, smem);
+        k_decrypt<LG><<<dim3(nl, batch), NT, smem, L.st>>>(L.dc, ct, ct_stride, s_ntt, out, nl);
+    });
+    check_launch("decrypt");
+    if (L.counter) ++*L.counter;
+}
+
+// ------------------------------------------------------------------------------------ signed -> NTT
+template <int LOGN>
+__global__ void __launch_bounds__(NttThreads<LOGN>::value)
+k_signed_to_ntt(const DCtx* __restrict__ dc, const long long* __restrict__ coeffs, u64* __restrict__ out, int nl)
+{
+    extern __shared__ u64 sm[];
+    using T = NttCta<LOGN, NttThreads<LOGN>::value>;
+    const int l = blockIdx.x, y = blockIdx.y;
+    const DPrime Pr = dc->p[l];
+    const long long* src = coeffs + (size_t)y * T::N;
+    u64* o = out + ((size_t)y * nl + l) * T::N;
+    auto ld = [&](int i) { return signed_to_res(src[i], Pr); };
+    auto st = [&](int i, u64 v) { o[i] = v; };
+    T::forward(sm, Pr, twp(dc, l), ld, st);
+}
+
+void signed_to_ntt(const Launch& L, const int64_t* coeffs, uint64_t* out, int count, int nl)
+{
+    if (count <= 0) return;
+    const size_t smem = sizeof(u64) << L.log_n;
+    NTT_DISPATCH(L.log_n, {
+        constexpr int NT = NttThreads<LG>::value;
+        allow_smem(k_signed_to_ntt<LG>, smem);
+        k_signed_to_ntt<LG><<<dim3(nl, count), NT, smem, L.st>>>(L.dc, (const long long*)coeffs, out, nl);
+    });
+    check_launch("signed_to_ntt");
+    if (L.counter) ++*L.counter;
+}
+
+// ------------------------------------------------------------------------------------ samplers / keygen
+template <int LOGN>
+__global__ void __launch_bounds__(NttThreads<LOGN>::value)
+k_sample_ntt(const DCtx* __restrict__ dc, u64* __restrict__ out, int nlimbs, int nl_data, int kind, u64 seed,
+             u64 purpose, u64 id0, u64 id_step, u64 digit0, u64 digit_step)
+{
+    extern __shared__ u64 sm[];
+    using T = NttCta<LOGN, NttThreads<LOGN>::value>;
+    const int limb = blockIdx.x, y = blockIdx.y;
+    const int p = (limb < nl_data) ? limb : dc->n_data;
+    const DPrime Pr = dc->p[p];
+    const u64 stream = stream_tag(purpose, id0 + (u64)y * id_step, digit0 + (u64)y * digit_step, 0);
+    u64* o = out + ((size_t)y * nlimbs + limb) * T::N;
+    auto ld = [&](int i) { return signed_to_res(sample_small(dc, kind, seed, stream, (u64)i), Pr); };
+    auto st = [&](int i, u64 v) { o[i] = v; };
+    T::forward(sm, Pr, twp(dc, p), ld, st);
+}
+
+void sample_ntt(const Launch& L, uint64_t* out, int ny, int nlimbs, int nl_data, int kind, uint64_t seed,
+                uint64_t purpose, uint64_t id0, uint64_t id_step, uint64_t digit0, uint64_t digit_step)
+{
+    const size_t smem = sizeof(u64) << L.log_n;
+    NTT_DISPATCH(L.log_n, {
+        constexpr int NT = NttThreads<LG>::value;
+        allow_smem(k_sample_ntt<LG>, smem);
+        k_sample_ntt<LG><<<dim3(nlimbs, ny), NT, smem, L.st>>>(L.dc, out, nlimbs, nl_data, kind, seed, purpose, id0,
+                                                               id_step, digit0, digit_step);
+    });
+    check_launch("sample_ntt");
+    if (L.counter) ++*L.counter;
+}
+
+__global__ void k_sample_uniform(const DCtx* __restrict__ dc, u64* __restrict__ out, int prime, u64 seed, u64 stream)
+{
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    const DPrime Pr = dc->p[prime];
+    const u64 hi = prng(seed, stream, 2 * (u64)i), lo = prng(seed, stream, 2 * (u64)i + 1);
+    out[i] = reduce128(hi, lo, Pr);   // (hi 2^64 + lo) mod q, exactly (R15)
+}
+
+void sample_uniform(const Launch& L, uint64_t* out, int prime, uint64_t seed, uint64_t purpose, uint64_t id,
+                    uint64_t digit)
+{
+    const int n = 1 << L.log_n;
+    // stream tag computed on the host side identically
+    const uint64_t stream = (purpose << 56) | ((id & 0xFFFFFFFFFULL) << 20) | ((digit & 0x3FF) << 10) |
+                            ((uint64_t)prime & 0x3FF);
+    k_sample_uniform<<<n / 256, 256, 0, L.st>>>(L.dc, out, prime, seed, stream);
+    check_launch("sample_uniform");
+    if (L.counter) ++*L.counter;
+}
+
+// key[j][1][p] already holds a_j[p]; e_ntt[j][p][N]; s_ntt[p][N]; sprime[p][N]:
+//   key[j][0][p] = -a s + e + [p == j] (P mod q_j) s'      (R5)
+__global__ void k_ks_key_combine(const DCtx* __restrict__ dc, u64* __restrict__ key, const u64* __restrict__ e_ntt,
+                                 const u64* __restrict__ s_ntt, const u64* __restrict__ sprime, int L)
+{
+    const int n = dc->n;
+    const int k = blockIdx.x * 256 + threadIdx.x, p = blockIdx.y, j = blockIdx.z;
+    const DPrime Pr = dc->p[p];
+    const size_t row1 = (((size_t)j * 2 + 1) * (L + 1) + p) * n + k;
+    const size_t row0 = (((size_t)j * 2 + 0) * (L + 1) + p) * n + k;
+    const u64 a = key[row1];
+    const u64 s = s_ntt[(size_t)p * n + k];
+    u64 v = submod(e_ntt[((size_t)j * (L + 1) + p) * n + k], mulmod(a, s, Pr), Pr.q);
+    if (p == j) {
+        const u64 gadget = dc->qmod[L][p];   // P mod q_j
+        v = addmod(v, mulmod(gadget, sprime[(size_t)p * n + k], Pr), Pr.q);
+    }
+    key[row0] = v;
+}
+
+void keyswitch_key_combine(const Launch& L, uint64_t* key, const uint64_t* e_ntt, const uint64_t* s_ntt,
+                           const uint64_t* sprime, int Ld)
+{
+    const int n = 1 << L.log_n;
+    k_ks_key_combine<<<dim3(n / 256, Ld + 1, Ld), 256, 0, L.st>>>(L.dc, key, e_ntt, s_ntt, sprime, Ld);
+    check_launch("ks_key_combine");
+    if (L.counter) ++*L.counter;
+}
+
+// pk[0][p] = -a s + e ; pk[1][p] = a (already written)
+__global__ void k_pk_combine(const DCtx* __restrict__ dc, u64* __restrict__ pk, const u64* __restrict__ e_ntt,
+                             const u64* __restrict__ s_ntt, int L)
+{
+    const int n = dc->n;
+    const int k = blockIdx.x * 256 + threadIdx.x, p = blockIdx.y;
+    const DPrime Pr = dc->p[p];
+    const u64 a = pk[((size_t)L + p) * n + k];
+    pk[(size_t)p * n + k] = submod(e_ntt[(size_t)p * n + k], mulmod(a, s_ntt[(size_t)p * n + k], Pr), Pr.q);
+}
+
+void pk_combine(const Launch& L, uint64_t* pk, const uint64_t* e_ntt, const uint64_t* s_ntt, int Ld)
+{
+    const int n = 1 << L.log_n;
+    k_pk_combine<<<dim3(n / 256, Ld), 256, 0, L.st>>>(L.dc, pk, e_ntt, s_ntt, Ld);
+    check_launch("pk_combine");
+    if (L.counter) ++*L.counter;
+}
+
+__global__ void k_square_ntt(const DCtx* __restrict__ dc, const u64* __restrict__ s, u64* __restrict__ out)
+{
+    const int n = dc->n;
+    const int k = blockIdx.x * 256 + threadIdx.x, p = blockIdx.y;
+    const u64 v = s[(size_t)p * n + k];
+    out[(size_t)p * n + k] = mulmod(v, v, dc->p[p]);
+}
+void square_ntt(const Launch& L, const uint64_t* s, uint64_t* out, int np)
+{
+    const int n = 1 << L.log_n;
+    k_square_ntt<<<dim3(n / 256, np), 256, 0, L.st>>>(L.dc, s, out);
+    check_launch("square_ntt");
+    if (L.counter) ++*L.counter;
+}
+
+__global__ void k_galois_ntt(const DCtx* __restrict__ dc, const u64* __restrict__ s, u64* __restrict__ out, u32 g)
+{
+    const int n = dc->n;
+    const int k = blockIdx.x * 256 + threadIdx.x, p = blockIdx.y;
+    out[(size_t)p * n + k] = s[(size_t)p * n + galois_src(k, g, dc->log_n)];
+}
+void galois_ntt(const Launch& L, const uint64_t* s, uint64_t* out, int np, uint32_t g)
+{
+    const int n = 1 << L.log_n;
+    k_galois_ntt<<<dim3(n / 256, np), 256, 0, L.st>>>(L.dc, s, out, g);
+    check_launch("galois_ntt");
+    if (L.counter) ++*L.counter;
+}
+
+// c0 = pk0 u + e0 + m ; c1 = pk1 u + e1   (R6, R17), all NTT form over the L data primes
+__global__ void k_encrypt_combine(const DCtx* __restrict__ dc, const u64* __restrict__ pk, const u64* __restrict__ u,
+                                  const u64* __restrict__ e0, const u64* __restrict__ e1, const u64* __restrict__ m,
+                                  u64* __restrict__ ct, int L)
+{
+    const int n = dc->n;
+    const int k = blockIdx.x * 256 + threadIdx.x, p = blockIdx.y, b = blockIdx.z;
+    const DPrime Pr = dc->p[p];
+    const size_t off = ((size_t)b * L + p) * n + k;
+    const u64 uu = u[off];
+    const u64 c0 = addmod(addmod(mulmod(pk[(size_t)p * n + k], uu, Pr), e0[off], Pr.q), m[off], Pr.q);
+    const u64 c1 = addmod(mulmod(pk[((size_t)L + p) * n + k], uu, Pr), e1[off], Pr.q);
+    ct[((size_t)b * 2 * L + p) * n + k] = c0;
+    ct[((size_t)b * 2 * L + L + p) * n + k] = c1;
+}
+
+void encrypt_combine(const Launch& L, const uint64_t* pk, const uint64_t* u, const uint64_t* e0, const uint64_t* e1,
+                     const uint64_t* m, uint64_t* ct, int batch, int Ld)
+{
+    const int n = 1 << L.log_n;
+    k_encrypt_combine<<<dim3(n / 256, Ld, batch), 256, 0, L.st>>>(L.dc, pk, u, e0, e1, m, ct, Ld);
+    check_launch("encrypt_combine");
+    if (L.counter) ++*L.counter;
+}
+
+// constant plaintexts (cubic activation, R23): NTT of an integer constant m0 is m0 mod q in every slot
+__global__ void __launch_bounds__(256)
+k_mul_scalar(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t sin, u64* __restrict__ out, size_t sout,
+             const u64* __restrict__ res, int nl)
+{
+    const int n = dc->n;
+    const int k = blockIdx.x * 256 + threadIdx.x, cl = blockIdx.y, b = blockIdx.z;
+    const int l = cl % nl;
+    out[(size_t)b * sout + (size_t)cl * n + k] = mulmod(in[(size_t)b * sin + (size_t)cl * n + k], res[l], dc->p[l]);
+}
+void mul_scalar(const Launch& L, const uint64_t* in, size_t sin, uint64_t* out, size_t sout, const uint64_t* res,
+                int batch, int ncomp, int nl)
+{
+    const int n = 1 << L.log_n;
+    k_mul_scalar<<<dim3(n / 256, ncomp * nl, batch), 256, 0, L.st>>>(L.dc, in, sin, out, sout, res, nl);
+    check_launch("mul_scalar");
+    if (L.counter) ++*L.counter;
+}
+__global__ void __launch_bounds__(256)
+k_add_scalar(const DCtx* __restrict__ dc, u64* __restrict__ ct, size_t stride, const u64* __restrict__ res)
+{
+    const int n = dc->n;
+    const int k = blockIdx.x * 256 + threadIdx.x, l = blockIdx.y, b = blockIdx.z;
+    u64& v = ct[(size_t)b * stride + (size_t)l * n + k];
+    v = addmod(v, res[l], dc->p[l].q);
+}
+void add_scalar(const Launch& L, uint64_t* ct, size_t stride, const uint64_t* res, int batch, int nl)
+{
+    const int n = 1 << L.log_n;
+    k_add_scalar<<<dim3(n / 256, nl, batch), 256, 0, L.st>>>(L.dc, ct, stride, res);
+    check_launch("add_scalar");
+    if (L.counter) ++*L.counter;
+}
+
+}  // namespace ck

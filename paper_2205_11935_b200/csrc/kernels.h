@@ -1,0 +1,101 @@
+// kernels.h -- host-side launchers of the sm_100a kernels (internal to the library, not the C-ABI).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <vector>
+
+struct DCtx;
+
+namespace ck {
+
+// CUDA-event probe around every launch of one kernel class (bench roofline, measured live).
+enum ProbeKind { PROBE_OFF = 0, PROBE_MODUP = 1, PROBE_KEYSWITCH = 2, PROBE_NTT = 3 };
+struct Probe {
+    int kind = PROBE_OFF;
+    std::vector<cudaEvent_t> ev;
+    size_t used = 0;
+    double alg_bytes = 0;   // algorithmic bytes of the probed launches
+    void mark(cudaStream_t s)
+    {
+        if (used == ev.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            ev.push_back(e);
+        }
+        cudaEventRecord(ev[used++], s);
+    }
+    bool on(int k) const { return kind == k; }
+};
+
+struct Launch {
+    const DCtx* dc;       // device constants
+    int log_n;
+    int n_data, n_special;
+    cudaStream_t st;
+    unsigned long long* counter;   // launches issued (for bench gpu_launches)
+    Probe* probe;
+};
+
+// batched in-place NTT over [batch][limbs][N]; limb l uses prime (prime0 + l)
+void ntt_batch(const Launch&, uint64_t* data, int batch, int limbs, int prime0, bool inverse);
+
+// ---- key switching, see ks.cu / DESIGN.md section 5
+struct KsIn {
+    const uint64_t* base;     // first ciphertext
+    size_t ct_stride;         // words between consecutive ciphertexts
+    size_t comp_off;          // words from a ciphertext to the component being switched
+    uint32_t galois;          // 0: no automorphism; else apply sigma_g on load (NTT domain)
+};
+struct KsOut {
+    uint64_t* base;           // [b] at base + b*ct_stride, layout [2][nl][N]
+    size_t ct_stride;
+    const uint64_t* add;      // optional addend ciphertexts (same layout rules as input)
+    size_t add_stride;
+    uint32_t add_galois;      // apply sigma_g to the addend on load
+    int add_comp1;            // add component 1 of the addend as well (relinearize)
+    int accumulate;           // out += result (giant-step accumulation)
+};
+struct KsWork {
+    uint64_t* digits;         // [B][nl][N]
+    uint64_t* modup;          // [B][nl][nl+1][N]
+    uint64_t* acc;            // [B][2][nl+1][N]
+    uint64_t* rem;            // [B][2][N]
+};
+void keyswitch(const Launch&, const KsIn& in, const uint64_t* key, int batch, int nl, const KsWork& w,
+               const KsOut& out);
+
+// rescale: in [B][ncomp][nl][N] (stride in_stride words) -> out [B][ncomp][nl-1][N]; optional
+// bias plaintext [nl-1][N] added to component 0.
+void rescale(const Launch&, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, int batch,
+             int ncomp, int nl, uint64_t* rem /*[B][ncomp][N]*/, const uint64_t* bias);
+
+void tensor(const Launch&, const uint64_t* a, const uint64_t* b, size_t stride, uint64_t* out3, size_t out_stride,
+            int batch, int nl);
+void add(const Launch&, const uint64_t* a, size_t sa, const uint64_t* b, size_t sb, uint64_t* out, size_t so,
+         int batch, int ncomp, int nl);
+void bsgs_mac(const Launch&, const uint64_t* pts, const uint64_t* v0, size_t v0_stride, const uint64_t* vbaby,
+              uint64_t* wout, int t1, int t2, int batch, int nl);
+void decrypt(const Launch&, const uint64_t* ct, size_t ct_stride, const uint64_t* s_ntt, uint64_t* out, int batch, int nl);
+
+// signed int64 coefficients [count][N] -> NTT residues out[count][nl][N] over primes 0..nl-1
+void signed_to_ntt(const Launch&, const int64_t* coeffs, uint64_t* out, int count, int nl);
+
+// ---- keygen / encryption samplers (R13-R15; streams as in DESIGN.md)
+// out[y][limb][N] = NTT_{p(limb)}(sample_kind(seed, stream(purpose, id0 + y*id_step, digit0 + y*digit_step, 0), i))
+// p(limb) = limb < nl_data ? limb : special index.  kind 0 ternary, 1 gaussian.
+void sample_ntt(const Launch&, uint64_t* out, int ny, int nlimbs, int nl_data, int kind, uint64_t seed,
+                uint64_t purpose, uint64_t id0, uint64_t id_step, uint64_t digit0, uint64_t digit_step);
+// out[N] uniform mod prime p with stream (purpose, id, digit, p)
+void sample_uniform(const Launch&, uint64_t* out, int prime, uint64_t seed, uint64_t purpose, uint64_t id,
+                    uint64_t digit);
+// key material combine, see keygen in api.cpp
+void keyswitch_key_combine(const Launch&, uint64_t* key, const uint64_t* e_ntt, const uint64_t* s_ntt,
+                           const uint64_t* sprime, int L);
+void pk_combine(const Launch&, uint64_t* pk, const uint64_t* e_ntt, const uint64_t* s_ntt, int L);
+void square_ntt(const Launch&, const uint64_t* s, uint64_t* out, int np);
+void galois_ntt(const Launch&, const uint64_t* s, uint64_t* out, int np, uint32_t g);
+void encrypt_combine(const Launch&, const uint64_t* pk, const uint64_t* u, const uint64_t* e0, const uint64_t* e1,
+                     const uint64_t* m, uint64_t* ct, int batch, int L);
+
+}  // namespace ck

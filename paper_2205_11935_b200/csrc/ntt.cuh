@@ -1,0 +1,200 @@
+// ntt.cuh -- CTA-level negacyclic NTT / iNTT over one limb, radix-2^LOGE register passes.
+//
+// Definition (R2):  NTT(a)[k] = sum_i a_i psi^{(2 brev(k) + 1) i}  mod q,
+// bit-reversed output order.  Stage s (0..LOGN-1) of the forward transform pairs indices that
+// differ in bit LOGN-1-s with twiddle W[2^s + block] = psi^{brev(2^s + block)} (Cooley-Tukey);
+// the inverse runs the stages backwards with IW = psi^{-brev(.)} (Gentleman-Sande) and N^{-1}.
+//
+// B200 mapping.  One CTA owns one limb (N <= 16384 words = 128 KiB of shared memory).  Each of
+// NT threads holds E = N/NT residues in registers; a "pass" performs K = LOGE consecutive stages
+// entirely in registers on groups of 2^K elements (radix-2^K), so the limb crosses shared memory
+// only between passes (3 round trips for N=16384, NT=512).  The first forward pass loads straight
+// from the caller's loader (HBM, coalesced: lane <-> consecutive index), the last pass stores
+// straight through the caller's storer (each thread owns E contiguous words).  The inverse mirrors
+// this.  Shared memory is XOR-swizzled  a ^ ((a >> LOGE) & 15)  -- conflict-free (2 wavefronts per
+// 64-bit warp access) for every pass of every supported (LOGN, NT), checked by
+// tests/test_ntt_layout.py.  Butterflies are Harvey-lazy: forward values live in [0, 4q), inverse
+// values in [0, 2q); loaders must supply values < 2q; storers receive canonical values in [0, q).
+#pragma once
+#include "common.cuh"
+#include <type_traits>
+
+template <int I, int END, class F>
+__device__ __forceinline__ void static_for(F&& f)
+{
+    if constexpr (I < END) {
+        f(std::integral_constant<int, I>{});
+        static_for<I + 1, END>(f);
+    }
+}
+
+constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x >> 1); }
+
+template <int LOGN_, int NT_>
+struct NttCta {
+    static constexpr int LOGN = LOGN_;
+    static constexpr int NT = NT_;
+    static constexpr int N = 1 << LOGN;
+    static constexpr int E = N / NT;
+    static constexpr int LOGE = ilog2c(E);
+    static constexpr int NPASS = (LOGN + LOGE - 1) / LOGE;
+    static_assert((1 << LOGE) == E, "E must be a power of two");
+    static_assert(LOGE >= 2 && LOGE <= 5, "2..5 stages per pass");
+
+    template <int P>
+    struct Pass {
+        static constexpr int S0 = P * LOGE;
+        static constexpr int K = (LOGN - S0 < LOGE) ? (LOGN - S0) : LOGE;
+        static constexpr int G = E >> K;          // groups per thread
+        static constexpr int SH = LOGN - S0 - K;  // log2(stride between group elements)
+    };
+
+    __device__ __forceinline__ static int swz(int a) { return a ^ ((a >> LOGE) & 15); }
+
+    // index of element i of the thread's group g in pass P
+    template <int P>
+    __device__ __forceinline__ static int index(int tid, int g, int i)
+    {
+        using G_ = Pass<P>;
+        const int gid = tid * G_::G + g;
+        const int b0 = gid >> G_::SH;
+        const int o = gid & ((1 << G_::SH) - 1);
+        return (b0 << (LOGN - G_::S0)) + (i << G_::SH) + o;
+    }
+
+    template <int P>
+    __device__ __forceinline__ static void fwd_compute(u64 (&x)[E], int tid, const u64* __restrict__ W,
+                                                       const u64* __restrict__ Wsh, u64 q, u64 q2)
+    {
+        using G_ = Pass<P>;
+        constexpr int K = G_::K;
+#pragma unroll
+        for (int g = 0; g < G_::G; ++g) {
+            const int gid = tid * G_::G + g;
+            const int b0 = gid >> G_::SH;
+#pragma unroll
+            for (int r = 0; r < K; ++r) {
+                const int half = 1 << (K - 1 - r);
+#pragma unroll
+                for (int i = 0; i < (1 << K); ++i) {
+                    if (i & half) continue;
+                    const int m = (1 << (G_::S0 + r)) + (b0 << r) + (i >> (K - r));
+                    const u64 w = __ldg(W + m), ws = __ldg(Wsh + m);
+                    u64& X = x[g * (1 << K) + i];
+                    u64& Y = x[g * (1 << K) + i + half];
+                    const u64 xx = csub(X, q2);
+                    const u64 t = shoup_mul(Y, w, ws, q);
+                    X = xx + t;
+                    Y = xx - t + q2;
+                }
+            }
+        }
+    }
+
+    template <int P>
+    __device__ __forceinline__ static void inv_compute(u64 (&x)[E], int tid, const u64* __restrict__ IW,
+                                                       const u64* __restrict__ IWsh, u64 q, u64 q2)
+    {
+        using G_ = Pass<P>;
+        constexpr int K = G_::K;
+#pragma unroll
+        for (int g = 0; g < G_::G; ++g) {
+            const int gid = tid * G_::G + g;
+            const int b0 = gid >> G_::SH;
+#pragma unroll
+            for (int r = K - 1; r >= 0; --r) {
+                const int half = 1 << (K - 1 - r);
+#pragma unroll
+                for (int i = 0; i < (1 << K); ++i) {
+                    if (i & half) continue;
+                    const int m = (1 << (G_::S0 + r)) + (b0 << r) + (i >> (K - r));
+                    const u64 w = __ldg(IW + m), ws = __ldg(IWsh + m);
+                    u64& X = x[g * (1 << K) + i];
+                    u64& Y = x[g * (1 << K) + i + half];
+                    const u64 u = X, v = Y;
+                    X = csub(u + v, q2);
+                    Y = shoup_mul(u - v + q2, w, ws, q);
+                }
+            }
+        }
+    }
+
+    // Forward NTT of one limb.  ld(idx) -> value in [0, 2q); st(idx, v) receives v in [0, q).
+    // `tw` points at this prime's [4][N] table block.  `sm` holds N words (+ nothing else).
+    template <class Load, class Store>
+    __device__ __forceinline__ static void forward(u64* sm, const DPrime& Pr, const u64* __restrict__ tw,
+                                                   Load&& ld, Store&& st)
+    {
+        const int tid = threadIdx.x;
+        const u64 q = Pr.q, q2 = Pr.q2;
+        const u64* W = tw;
+        const u64* Wsh = tw + N;
+        u64 x[E];
+        static_for<0, NPASS>([&](auto pc) {
+            constexpr int P = decltype(pc)::value;
+            using G_ = Pass<P>;
+            constexpr int K = G_::K;
+#pragma unroll
+            for (int g = 0; g < G_::G; ++g)
+#pragma unroll
+                for (int i = 0; i < (1 << K); ++i) {
+                    const int idx = index<P>(tid, g, i);
+                    if constexpr (P == 0) x[g * (1 << K) + i] = ld(idx);
+                    else x[g * (1 << K) + i] = sm[swz(idx)];
+                }
+            fwd_compute<P>(x, tid, W, Wsh, q, q2);
+#pragma unroll
+            for (int g = 0; g < G_::G; ++g)
+#pragma unroll
+                for (int i = 0; i < (1 << K); ++i) {
+                    const int idx = index<P>(tid, g, i);
+                    u64 v = x[g * (1 << K) + i];
+                    if constexpr (P == NPASS - 1) st(idx, csub(csub(v, q2), q));
+                    else sm[swz(idx)] = v;
+                }
+            if constexpr (P < NPASS - 1) __syncthreads();
+        });
+        __syncthreads();   // shared memory free again on return
+    }
+
+    // Inverse NTT of one limb (includes N^{-1}).  ld(idx) -> value in [0, 2q); st gets [0, q).
+    template <class Load, class Store>
+    __device__ __forceinline__ static void inverse(u64* sm, const DPrime& Pr, const u64* __restrict__ tw,
+                                                   Load&& ld, Store&& st)
+    {
+        const int tid = threadIdx.x;
+        const u64 q = Pr.q, q2 = Pr.q2;
+        const u64* IW = tw + 2 * N;
+        const u64* IWsh = tw + 3 * N;
+        const u64 ninv = Pr.ninv, ninv_sh = Pr.ninv_sh;
+        u64 x[E];
+        static_for<0, NPASS>([&](auto pc) {
+            constexpr int P = NPASS - 1 - decltype(pc)::value;
+            using G_ = Pass<P>;
+            constexpr int K = G_::K;
+#pragma unroll
+            for (int g = 0; g < G_::G; ++g)
+#pragma unroll
+                for (int i = 0; i < (1 << K); ++i) {
+                    const int idx = index<P>(tid, g, i);
+                    if constexpr (P == NPASS - 1) x[g * (1 << K) + i] = ld(idx);
+                    else x[g * (1 << K) + i] = sm[swz(idx)];
+                }
+            inv_compute<P>(x, tid, IW, IWsh, q, q2);
+#pragma unroll
+            for (int g = 0; g < G_::G; ++g)
+#pragma unroll
+                for (int i = 0; i < (1 << K); ++i) {
+                    const int idx = index<P>(tid, g, i);
+                    u64 v = x[g * (1 << K) + i];
+                    if constexpr (P == 0) st(idx, csub(shoup_mul(v, ninv, ninv_sh, q), q));
+                    else sm[swz(idx)] = v;
+                }
+            if constexpr (P > 0) __syncthreads();
+        });
+        __syncthreads();
+    }
+};
+
+// Threads per CTA for each supported ring dimension (E = 32 for N >= 8192, 16 below).
+template <int LOGN> struct NttThreads { static constexpr int value = (LOGN >= 13) ? (1 << (LOGN - 5)) : (1 << (LOGN - 4)); };
