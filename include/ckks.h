@@ -145,9 +145,13 @@ ckks_status ckks_matvec_diag(ckks_ctx* ctx, const ckks_layer* layer, const ckks_
 
 /* ---- model / forward (rows a10-a12) --------------------------------------------------------- */
 /* activation: 0 none, 1 square (BASELINE cfg4), 2 cubic ReLU approximation (Eq. 2).
- * Layers must be encoded for the levels/scales the forward produces (R8). */
+ * Layers must be encoded for the levels/scales the forward produces (see ckks_model_plan, R8).
+ * The cubic's constant term c0 is added on the previous layer's valid slots [0, rows) only (R23),
+ * from a plaintext the model keeps in dev_buf (ckks_model_sizes bytes; NULL/0 for none/square):
+ * act_coeffs = host [n_layers-1][N] int64 encodings of those plaintexts, or NULL to encode here. */
+ckks_status ckks_model_sizes(const ckks_ctx* ctx, uint32_t n_layers, int32_t activation, size_t* dev_bytes);
 ckks_status ckks_model_create(ckks_ctx* ctx, const ckks_layer* const* layers, uint32_t n_layers, int32_t activation,
-                              ckks_model** out);
+                              const int64_t* act_coeffs, void* dev_buf, void* stream, ckks_model** out);
 void ckks_model_destroy(ckks_model* model);
 /* BSGS split of a rows x cols layer: t = max(rows, cols) padded to a multiple of
  * t1 = 2^ceil(ceil(log2 t)/2), t2 = t / t1 (R5). */

@@ -145,10 +145,19 @@ def square(ctx, z: Ct) -> Ct:
     return Ct(y, z.scale * z.scale / float(ctx.primes[l]))
 
 
-def cubic(ctx, z: Ct, coeffs=RELU_APPROX) -> Ct:
+def cubic_c0_coeffs(c0: float, valid: int, scale: float, n: int) -> np.ndarray:
+    """The constant term restricted to the valid slots [0, valid) (R23: keeps the zero padding the
+    following replicate relies on), encoded at the activation output scale."""
+    v = np.zeros(n // 2)
+    v[:valid] = c0
+    return encoding.encode(v, scale, n)
+
+
+def cubic(ctx, z: Ct, coeffs=RELU_APPROX, valid: int | None = None, c0_coeffs=None) -> Ct:
     """Eq. 2 at depth 2, schedule R23:
        z2 = rescale(relin(z (x) z));  a = rescale(z o [c3]_{q_l}) + [c2]_S;
-       h = rescale(relin(z2 (x) a));  g = drop(rescale(z o [c1]_{S3 q_l / S})) + [c0]_{S3};  out = h + g."""
+       h = rescale(relin(z2 (x) a));  g = drop(rescale(z o [c1]_{S3 q_l / S})) + [c0]_{S3};  out = h + g.
+    [c0]_{S3} is the constant in every slot (valid=None) or c0 on slots [0, valid) only."""
     c3, c2, c1, c0 = coeffs
     l = z.level
     S = z.scale
@@ -161,13 +170,29 @@ def cubic(ctx, z: Ct, coeffs=RELU_APPROX) -> Ct:
     S3 = (S * S / ql) * S / ql1
     g = ctx.rescale(ctx.mul_plain(z.data, ctx.plain(encoding.encode_const(c1, S3 * ql / S, n), l)))
     g = ctx.drop_level(g, l - 2)
-    g = ctx.add_plain(g, ctx.plain(encoding.encode_const(c0, S3, n), l - 2))
+    if c0_coeffs is None:
+        c0_coeffs = encoding.encode_const(c0, S3, n) if valid is None else cubic_c0_coeffs(c0, valid, S3, n)
+    g = ctx.add_plain(g, ctx.plain(c0_coeffs, l - 2))
     return Ct(ctx.add(h, g), S3)
 
 
 def replicate(ctx, y: Ct, t: int) -> Ct:
     """y + rot_{-t}(y): [y | 0] -> [y | y] on slots [0, 2t) (P:L116 duplicated layout)."""
     return Ct(ctx.add(y.data, ctx.rotate(y.data, -t)), y.scale)
+
+
+def activation_plaintexts(ctx, layers, activation: str):
+    """Masked constant-term plaintexts of the cubic activations (one per non-final layer), R23."""
+    if activation != "cubic":
+        return None
+    out = []
+    for lay in layers[:-1]:
+        S = lay.bias_scale                          # dense output scale = its input scale (R8)
+        l = lay.level - 1
+        ql, ql1 = float(ctx.primes[l]), float(ctx.primes[l - 1])
+        S3 = (S * S / ql) * S / ql1
+        out.append(cubic_c0_coeffs(RELU_APPROX[3], lay.rows, S3, ctx.n))
+    return np.stack(out)
 
 
 def forward(ctx, ct: Ct, layers, activation: str = "square", ops: OpCount | None = None) -> Ct:
@@ -182,7 +207,7 @@ def forward(ctx, ct: Ct, layers, activation: str = "square", ops: OpCount | None
             if activation == "square":
                 ct = square(ctx, ct)
             elif activation == "cubic":
-                ct = cubic(ctx, ct)
+                ct = cubic(ctx, ct, valid=layer.rows)
             elif activation != "none":
                 raise ValueError(activation)
     return ct

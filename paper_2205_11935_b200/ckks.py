@@ -69,7 +69,8 @@ SIGNATURES = {
     "ckks_layer_destroy": (None, [_VP]),
     "ckks_layer_work_sizes": (_I, [_VP, _VP, _U32, _PSZ]),
     "ckks_matvec_diag": (_I, [_VP, _VP, _PCT, _PCT, _VP, _VP]),
-    "ckks_model_create": (_I, [_VP, ctypes.POINTER(_VP), _U32, _I, ctypes.POINTER(_VP)]),
+    "ckks_model_sizes": (_I, [_VP, _U32, _I, _PSZ]),
+    "ckks_model_create": (_I, [_VP, ctypes.POINTER(_VP), _U32, _I, _VP, _VP, _VP, ctypes.POINTER(_VP)]),
     "ckks_model_destroy": (None, [_VP]),
     "ckks_model_work_sizes": (_I, [_VP, _VP, _U32, _PSZ]),
     "ckks_encrypted_forward": (_I, [_VP, _VP, _PCT, _PCT, _VP, _VP]),
@@ -376,12 +377,19 @@ class Layer:
 
 
 class Model:
-    def __init__(self, ctx: Context, layers, activation=ACT_SQUARE):
+    def __init__(self, ctx: Context, layers, activation=ACT_SQUARE, act_coeffs=None, stream=None):
         self.ctx = ctx
         self.layers = list(layers)
         arr = (ctypes.c_void_p * len(layers))(*[l.h.value for l in layers])
+        nb = ctypes.c_size_t()
+        _check(lib().ckks_model_sizes(ctx.h, len(layers), int(activation), ctypes.byref(nb)), "ckks_model_sizes")
+        self.buf = ctx.torch.empty(max(1, nb.value), dtype=ctx.torch.uint8, device=ctx.device)
+        ac = None if act_coeffs is None else np.ascontiguousarray(act_coeffs, dtype=np.int64)
+        self._keep = ac
         h = ctypes.c_void_p()
-        _check(lib().ckks_model_create(ctx.h, arr, len(layers), int(activation), ctypes.byref(h)), "ckks_model_create")
+        _check(lib().ckks_model_create(ctx.h, arr, len(layers), int(activation),
+                                       None if ac is None else ac.ctypes.data_as(ctypes.c_void_p), _ptr(self.buf),
+                                       _stream(stream), ctypes.byref(h)), "ckks_model_create")
         self.h = h
         depth = {ACT_NONE: 0, ACT_SQUARE: 1, ACT_CUBIC: 2}[int(activation)]
         self.in_level = self.layers[0].level

@@ -7,6 +7,7 @@
 #include "../../include/ckks.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "ntt.cuh"
 
 #include <cuda_runtime.h>
 
@@ -254,6 +255,7 @@ struct ckks_layer {
 struct ckks_model {
     std::vector<const ckks_layer*> layers;
     int activation;
+    u64* d_act = nullptr;   // cubic: masked constant-term plaintexts [n_layers-1][L][N] (R23)
 };
 
 namespace {
@@ -430,16 +432,30 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
             P.one_sh = (u64)(((u128)1 << 64) / q);
             P.r64 = (u64)(((u128)1 << 64) % q);
             P.r64_sh = h_shoup(P.r64, q);
+            // W[idx] = psi^{brev(idx)} (stage s = floor(log2 idx), block idx - 2^s), stored at the
+            // pass-ordered position ntt_tw_position (ntt.cuh); same for psi^{-1}.
             u64* W = tw.data() + (size_t)i * 4 * n;
+            std::vector<u64> fw(n), iw(n);
             u64 pw = 1, ipw = 1;
             for (int m = 0; m < n; ++m) {
                 const u32 r = h_brev((u32)m, c->log_n);
-                W[r] = pw;
-                W[n + r] = h_shoup(pw, q);
-                W[2 * n + r] = ipw;
-                W[3 * n + r] = h_shoup(ipw, q);
+                fw[r] = pw;
+                iw[r] = ipw;
                 pw = h_mulmod(pw, psi, q);
                 ipw = h_mulmod(ipw, ipsi, q);
+            }
+            W[0] = fw[0];
+            W[n] = h_shoup(fw[0], q);
+            W[2 * n] = iw[0];
+            W[3 * n] = h_shoup(iw[0], q);
+            for (int idx = 1; idx < n; ++idx) {
+                int s = 0;
+                while ((2 << s) <= idx) ++s;
+                const int pos = ntt_tw_position(c->log_n, s, idx - (1 << s));
+                W[pos] = fw[idx];
+                W[n + pos] = h_shoup(fw[idx], q);
+                W[2 * n + pos] = iw[idx];
+                W[3 * n + pos] = h_shoup(iw[idx], q);
             }
             for (int b = 0; b < np; ++b) {
                 h.qmod[i][b] = q % primes[b];
@@ -852,27 +868,62 @@ ckks_status ckks_matvec_diag(ckks_ctx* c, const ckks_layer* ly, const ckks_ct* i
 }
 
 // ------------------------------------------------------------------------------------ model
+static size_t model_dev_words(const ckks_ctx* c, uint32_t n_layers, int32_t activation)
+{
+    return activation == 2 && n_layers > 1 ? (size_t)(n_layers - 1) * c->L * c->n + c->n : 0;
+}
+
+ckks_status ckks_model_sizes(const ckks_ctx* c, uint32_t n_layers, int32_t activation, size_t* bytes)
+{
+    if (!c || !bytes) return fail(CKKS_E_PARAM, "null");
+    *bytes = align256(model_dev_words(c, n_layers, activation) * 8);
+    return CKKS_OK;
+}
+
 ckks_status ckks_model_create(ckks_ctx* c, const ckks_layer* const* layers, uint32_t n_layers, int32_t activation,
-                              ckks_model** out)
+                              const int64_t* act_coeffs, void* dev_buf, void* stream, ckks_model** out)
 {
     CK_TRY({
         if (!c || !layers || !out || n_layers == 0) throw CkksError(CKKS_E_PARAM, "null/empty model");
         if (activation < 0 || activation > 2) throw CkksError(CKKS_E_PARAM, "activation 0|1|2");
-        auto* m = new ckks_model();
-        m->activation = activation;
         int lvl = (int)layers[0]->level;
         for (uint32_t i = 0; i < n_layers; ++i) {
-            if ((int)layers[i]->level != lvl) {
-                delete m;
+            if ((int)layers[i]->level != lvl)
                 throw CkksError(CKKS_E_LEVEL, "layer " + std::to_string(i) + " encoded for the wrong level");
-            }
-            m->layers.push_back(layers[i]);
             lvl -= 1;
             if (i + 1 < n_layers) lvl -= (activation == 1 ? 1 : activation == 2 ? 2 : 0);
         }
-        if (lvl < 0) {
-            delete m;
-            throw CkksError(CKKS_E_LEVEL, "model deeper than the chain");
+        if (lvl < 0) throw CkksError(CKKS_E_LEVEL, "model deeper than the chain");
+        auto* m = new ckks_model();
+        m->activation = activation;
+        for (uint32_t i = 0; i < n_layers; ++i) m->layers.push_back(layers[i]);
+        if (model_dev_words(c, n_layers, activation)) {
+            if (!dev_buf) {
+                delete m;
+                throw CkksError(CKKS_E_PARAM, "cubic activation needs the model device buffer");
+            }
+            m->d_act = (u64*)dev_buf;
+            int64_t* stage = (int64_t*)(m->d_act + (size_t)(n_layers - 1) * c->L * c->n);
+            auto L = c->launch(stream);
+            cudaStream_t st = (cudaStream_t)stream;
+            std::vector<int64_t> coef(c->n);
+            std::vector<double> v(c->n / 2);
+            for (uint32_t i = 0; i + 1 < n_layers; ++i) {
+                const ckks_layer* ly = layers[i];
+                const int l = (int)ly->level - 1;   // activation input level
+                const double S = ly->bias_scale, ql = (double)c->primes[l], ql1 = (double)c->primes[l - 1];
+                const double S3 = (S * S / ql) * S / ql1;
+                const int64_t* src = act_coeffs ? act_coeffs + (size_t)i * c->n : nullptr;
+                if (!src) {
+                    std::fill(v.begin(), v.end(), 0.0);
+                    for (uint32_t r = 0; r < ly->rows; ++r) v[r] = 0.49383;   // c0 of Eq. 2 on valid slots
+                    encode_host(c->n, v.data(), v.size(), S3, coef.data());
+                    src = coef.data();
+                }
+                cuda_ok(cudaMemcpyAsync(stage, src, (size_t)c->n * 8, cudaMemcpyHostToDevice, st), "act upload");
+                ck::signed_to_ntt(L, stage, m->d_act + (size_t)i * c->L * c->n, 1, l - 1);
+                cuda_ok(cudaStreamSynchronize(st), "act upload");
+            }
         }
         *out = m;
         return CKKS_OK;
@@ -1050,14 +1101,13 @@ static void forward_chunk(ckks_ctx* c, const ckks_model* m, const u64* in, size_
             ck::mul_scalar(L, z, cur_stride, bufC, w2, dres + 64, B, 2, nl);
             u64* g = other;   // z2 no longer needed
             rescale_impl(c, bufC, w2, 2, nl, B, g, w2m, nullptr, stream);
-            const_residues(c, round_away(c0 * S3), nl - 2, res);
-            cuda_ok(cudaMemcpyAsync(dres + 128, res.data(), (nl - 2) * 8, cudaMemcpyHostToDevice, (cudaStream_t)stream),
-                    "c0");
+            (void)c0;
             // h += drop(g): add the first nl-2 limbs of each component of g
             ck::add(L, h, w2mm, g, w2m, h, w2mm, B, 1, nl - 2);
             ck::add(L, h + (size_t)(nl - 2) * c->n, w2mm, g + (size_t)(nl - 1) * c->n, w2m, h + (size_t)(nl - 2) * c->n,
                     w2mm, B, 1, nl - 2);
-            ck::add_scalar(L, h, w2mm, dres + 128, B, nl - 2);
+            // + c0 on the valid slots (model plaintext, R23)
+            ck::add(L, h, w2mm, m->d_act + (size_t)li * c->L * c->n, 0, h, w2mm, B, 1, nl - 2);
             // move h to bufA/bufB for the next layer
             u64* nxt = (cur == bufA) ? bufB : bufA;
             cuda_ok(cudaMemcpyAsync(nxt, h, (size_t)B * w2mm * 8, cudaMemcpyDeviceToDevice, (cudaStream_t)stream), "mv");

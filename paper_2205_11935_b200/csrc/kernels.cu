@@ -396,30 +396,45 @@ __global__ void __launch_bounds__(256)
 k_bsgs_mac(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u64* __restrict__ v0,
            size_t v0_stride, const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl)
 {
+    // CTA = 16 coefficients x one limb; its plaintext tile A[t][16] is staged in shared memory once
+    // and reused for every ciphertext; thread (x, b-lane) keeps v_j[b] (all j, both components) in
+    // registers and produces w_k[b] for every k.
+    extern __shared__ u64 A[];
     const int n = dc->n;
-    const int x = blockIdx.x * 32 + threadIdx.x, l = blockIdx.y, k = blockIdx.z * blockDim.y + threadIdx.y;
-    if (k >= t2) return;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int x0 = blockIdx.x * 16, x = x0 + tx, l = blockIdx.y;
+    const int t = t1 * t2;
+    for (int i = threadIdx.x; i < t * 16; i += blockDim.x)
+        A[i] = pts[((size_t)(i >> 4) * nl + l) * n + x0 + (i & 15)];
+    __syncthreads();
     const DPrime Pr = dc->p[l];
     const size_t ctw = (size_t)2 * nl * n;
-    u64 pv[T1MAX];
-#pragma unroll
-    for (int j = 0; j < T1MAX; ++j)
-        pv[j] = (j < t1) ? pts[((size_t)(k * t1 + j) * nl + l) * n + x] : 0;
-    for (int b = 0; b < batch; ++b) {
-        Acc128 a0, a1;
-        a0.zero();
-        a1.zero();
+    for (int b = ty; b < batch; b += 16) {
+        u64 va[T1MAX], vc[T1MAX];
 #pragma unroll
         for (int j = 0; j < T1MAX; ++j) {
             if (j < t1) {
                 const u64* v = (j == 0) ? v0 + (size_t)b * v0_stride : vb + ((size_t)(j - 1) * batch + b) * ctw;
-                a0.mac(pv[j], v[(size_t)l * n + x]);
-                a1.mac(pv[j], v[((size_t)nl + l) * n + x]);
+                va[j] = v[(size_t)l * n + x];
+                vc[j] = v[((size_t)nl + l) * n + x];
             }
         }
-        u64* w = wout + ((size_t)k * batch + b) * ctw;
-        w[(size_t)l * n + x] = a0.reduce(Pr);
-        w[((size_t)nl + l) * n + x] = a1.reduce(Pr);
+        for (int k = 0; k < t2; ++k) {
+            Acc128 a0, a1;
+            a0.zero();
+            a1.zero();
+#pragma unroll
+            for (int j = 0; j < T1MAX; ++j) {
+                if (j < t1) {
+                    const u64 a = A[(k * t1 + j) * 16 + tx];
+                    a0.mac(a, va[j]);
+                    a1.mac(a, vc[j]);
+                }
+            }
+            u64* w = wout + ((size_t)k * batch + b) * ctw;
+            w[(size_t)l * n + x] = a0.reduce(Pr);
+            w[((size_t)nl + l) * n + x] = a1.reduce(Pr);
+        }
     }
 }
 
@@ -429,11 +444,18 @@ void bsgs_mac(const Launch& L, const uint64_t* pts, const uint64_t* v0, size_t v
     if (batch <= 0) return;
     const int n = 1 << L.log_n;
     if (t1 > 32) throw std::runtime_error("bsgs_mac: t1 <= 32");
-    const int ky = 8;
-    dim3 grid(n / 32, nl, (t2 + ky - 1) / ky), block(32, ky);
-    if (t1 <= 8) k_bsgs_mac<8><<<grid, block, 0, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl);
-    else if (t1 <= 16) k_bsgs_mac<16><<<grid, block, 0, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl);
-    else k_bsgs_mac<32><<<grid, block, 0, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl);
+    const size_t smem = (size_t)t1 * t2 * 16 * 8;
+    dim3 grid(n / 16, nl);
+    if (t1 <= 8) {
+        allow_smem(k_bsgs_mac<8>, smem);
+        k_bsgs_mac<8><<<grid, 256, smem, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl);
+    } else if (t1 <= 16) {
+        allow_smem(k_bsgs_mac<16>, smem);
+        k_bsgs_mac<16><<<grid, 256, smem, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl);
+    } else {
+        allow_smem(k_bsgs_mac<32>, smem);
+        k_bsgs_mac<32><<<grid, 256, smem, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl);
+    }
     check_launch("bsgs_mac");
     if (L.counter) ++*L.counter;
 }

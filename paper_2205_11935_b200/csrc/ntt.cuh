@@ -49,18 +49,22 @@ struct NttCta {
         static constexpr int SH = LOGN - S0 - K;  // log2(stride between group elements)
     };
 
-    __device__ __forceinline__ static int swz(int a) { return a ^ ((a >> LOGE) & 15); }
+    __device__ __forceinline__ static int swz(int a) { return a ^ (((a >> 4) ^ (a >> 5)) & 15); }
 
     // index of element i of the thread's group g in pass P
     template <int P>
     __device__ __forceinline__ static int index(int tid, int g, int i)
     {
         using G_ = Pass<P>;
-        const int gid = tid * G_::G + g;
+        const int gid = g * NT + tid;
         const int b0 = gid >> G_::SH;
         const int o = gid & ((1 << G_::SH) - 1);
         return (b0 << (LOGN - G_::S0)) + (i << G_::SH) + o;
     }
+
+    // Twiddle table position of stage s = S0 + r, block b0 * 2^r + j (tables are stored
+    // "pass-ordered", see ntt_tw_position, so lanes with consecutive b0 read consecutive words).
+    __device__ __forceinline__ static int tw_index(int S0, int r, int b0, int j) { return (1 << (S0 + r)) + (j << S0) + b0; }
 
     template <int P>
     __device__ __forceinline__ static void fwd_compute(u64 (&x)[E], int tid, const u64* __restrict__ W,
@@ -70,7 +74,7 @@ struct NttCta {
         constexpr int K = G_::K;
 #pragma unroll
         for (int g = 0; g < G_::G; ++g) {
-            const int gid = tid * G_::G + g;
+            const int gid = g * NT + tid;
             const int b0 = gid >> G_::SH;
 #pragma unroll
             for (int r = 0; r < K; ++r) {
@@ -78,7 +82,7 @@ struct NttCta {
 #pragma unroll
                 for (int i = 0; i < (1 << K); ++i) {
                     if (i & half) continue;
-                    const int m = (1 << (G_::S0 + r)) + (b0 << r) + (i >> (K - r));
+                    const int m = tw_index(G_::S0, r, b0, i >> (K - r));
                     const u64 w = __ldg(W + m), ws = __ldg(Wsh + m);
                     u64& X = x[g * (1 << K) + i];
                     u64& Y = x[g * (1 << K) + i + half];
@@ -99,7 +103,7 @@ struct NttCta {
         constexpr int K = G_::K;
 #pragma unroll
         for (int g = 0; g < G_::G; ++g) {
-            const int gid = tid * G_::G + g;
+            const int gid = g * NT + tid;
             const int b0 = gid >> G_::SH;
 #pragma unroll
             for (int r = K - 1; r >= 0; --r) {
@@ -107,7 +111,7 @@ struct NttCta {
 #pragma unroll
                 for (int i = 0; i < (1 << K); ++i) {
                     if (i & half) continue;
-                    const int m = (1 << (G_::S0 + r)) + (b0 << r) + (i >> (K - r));
+                    const int m = tw_index(G_::S0, r, b0, i >> (K - r));
                     const u64 w = __ldg(IW + m), ws = __ldg(IWsh + m);
                     u64& X = x[g * (1 << K) + i];
                     u64& Y = x[g * (1 << K) + i + half];
@@ -121,7 +125,7 @@ struct NttCta {
 
     // Forward NTT of one limb.  ld(idx) -> value in [0, 2q); st(idx, v) receives v in [0, q).
     // `tw` points at this prime's [4][N] table block.  `sm` holds N words (+ nothing else).
-    template <class Load, class Store>
+    template <bool STAGED = true, class Load, class Store>
     __device__ __forceinline__ static void forward(u64* sm, const DPrime& Pr, const u64* __restrict__ tw,
                                                    Load&& ld, Store&& st)
     {
@@ -149,16 +153,28 @@ struct NttCta {
                 for (int i = 0; i < (1 << K); ++i) {
                     const int idx = index<P>(tid, g, i);
                     u64 v = x[g * (1 << K) + i];
-                    if constexpr (P == NPASS - 1) st(idx, csub(csub(v, q2), q));
-                    else sm[swz(idx)] = v;
+                    if constexpr (P == NPASS - 1) {
+                        if constexpr (STAGED) sm[swz(idx)] = v;
+                        else st(idx, csub(csub(v, q2), q));
+                    } else {
+                        sm[swz(idx)] = v;
+                    }
                 }
-            if constexpr (P < NPASS - 1) __syncthreads();
+            __syncthreads();
         });
-        __syncthreads();   // shared memory free again on return
+        if constexpr (STAGED) {
+            // coalesced epilogue: lane <-> consecutive index
+#pragma unroll 4
+            for (int c = 0; c < E; ++c) {
+                const int idx = c * NT + tid;
+                st(idx, csub(csub(sm[swz(idx)], q2), q));
+            }
+            __syncthreads();   // shared memory free again on return
+        }
     }
 
     // Inverse NTT of one limb (includes N^{-1}).  ld(idx) -> value in [0, 2q); st gets [0, q).
-    template <class Load, class Store>
+    template <bool STAGED = true, class Load, class Store>
     __device__ __forceinline__ static void inverse(u64* sm, const DPrime& Pr, const u64* __restrict__ tw,
                                                    Load&& ld, Store&& st)
     {
@@ -168,6 +184,15 @@ struct NttCta {
         const u64* IWsh = tw + 3 * N;
         const u64 ninv = Pr.ninv, ninv_sh = Pr.ninv_sh;
         u64 x[E];
+        if constexpr (STAGED) {
+            // coalesced prologue: lane <-> consecutive index, through shared memory
+#pragma unroll 4
+            for (int c = 0; c < E; ++c) {
+                const int idx = c * NT + tid;
+                sm[swz(idx)] = ld(idx);
+            }
+            __syncthreads();
+        }
         static_for<0, NPASS>([&](auto pc) {
             constexpr int P = NPASS - 1 - decltype(pc)::value;
             using G_ = Pass<P>;
@@ -177,7 +202,7 @@ struct NttCta {
 #pragma unroll
                 for (int i = 0; i < (1 << K); ++i) {
                     const int idx = index<P>(tid, g, i);
-                    if constexpr (P == NPASS - 1) x[g * (1 << K) + i] = ld(idx);
+                    if constexpr (P == NPASS - 1 && !STAGED) x[g * (1 << K) + i] = ld(idx);
                     else x[g * (1 << K) + i] = sm[swz(idx)];
                 }
             inv_compute<P>(x, tid, IW, IWsh, q, q2);
@@ -190,11 +215,21 @@ struct NttCta {
                     if constexpr (P == 0) st(idx, csub(shoup_mul(v, ninv, ninv_sh, q), q));
                     else sm[swz(idx)] = v;
                 }
-            if constexpr (P > 0) __syncthreads();
+            __syncthreads();
         });
-        __syncthreads();
     }
 };
 
 // Threads per CTA for each supported ring dimension (E = 32 for N >= 8192, 16 below).
-template <int LOGN> struct NttThreads { static constexpr int value = (LOGN >= 13) ? (1 << (LOGN - 5)) : (1 << (LOGN - 4)); };
+__host__ __device__ constexpr int ntt_loge(int logn) { return logn >= 13 ? 5 : 4; }
+template <int LOGN> struct NttThreads { static constexpr int value = 1 << (LOGN - ntt_loge(LOGN)); };
+
+// Host: position of the forward/inverse twiddle of stage s, block m (= b0 2^r + j with
+// r = s - S0(s), S0(s) = floor(s / LOGE) LOGE) in the pass-ordered table:  2^s + j 2^S0 + b0.
+inline int ntt_tw_position(int logn, int s, int m)
+{
+    const int loge = ntt_loge(logn);
+    const int S0 = (s / loge) * loge, r = s - S0;
+    const int b0 = m >> r, j = m & ((1 << r) - 1);
+    return (1 << s) + (j << S0) + b0;
+}

@@ -221,7 +221,8 @@ def _model_case(cfg, activation, B, max_batch, data_bits=None, log_n=None, seed_
     layers = OC.encode_model(o, prob["W"], prob["b"], o.top_level, Delta, activation)
     glayers = [G.Layer(g, l.rows, l.cols, l.level, diag_coeffs=l.diag_coeffs, bias_coeffs=l.bias_coeffs,
                        pt_scale=l.pt_scale, bias_scale=l.bias_scale) for l in layers]
-    model = G.Model(g, glayers, {"none": 0, "square": 1, "cubic": 2}[activation])
+    model = G.Model(g, glayers, {"none": 0, "square": 1, "cubic": 2}[activation],
+                    act_coeffs=OC.activation_plaintexts(o, layers, activation))
     ms = np.stack([OE.encode(OC.pack_input(prob["x"][b], layers[0].t, o.n // 2), Delta, o.n) for b in range(B)])
     ct = g.encrypt(ms, cfg.enc_seed, 0, Delta)
     out = model.forward(ct)

@@ -325,3 +325,13 @@ def test_forward_cfg4_vs_float64():
     y, ref, out = _forward_case(S.CFG4, "square")
     assert np.max(np.abs(y[: ref.size] - ref)) < 1e-5
     assert out.level == 4 and out.data.shape[1] == 5
+
+
+def test_forward_cubic_small_ring_vs_float64():
+    """Two dense layers with the Eq. 2 activation between them (R23 masked constant term) on N=4096."""
+    cfg = S.Config(name="small", log_n=12, data_bits=(60,) + (40,) * 5, special_bits=(60,), log2_scale=40,
+                   layers=((64, 128), (32, 64)), activation="cubic", in_dim=128,
+                   weight_std=(1 / np.sqrt(128), 1 / np.sqrt(64)))
+    y, ref, out = _forward_case(cfg, "cubic")
+    assert np.max(np.abs(y[: ref.size] - ref)) < 1e-5
+    assert out.level == 1

@@ -1,0 +1,6 @@
+(timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -30) > gpurun_out/pytest_gpu.log 2>&1
+timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1
+P="python tools/profile_forward.py"
+$P --mode forward --batch 256 > gpurun_out/pf_plain.log 2>&1 && \
+ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_forward_b256.csv $P --mode forward --batch 256 > gpurun_out/ncu1.log 2>&1
+tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/bench.log | tail -3
