@@ -94,8 +94,8 @@ k_ntt_batch(const DCtx* __restrict__ dc, u64* __restrict__ data, int limbs, int 
     const DPrime Pr = dc->p[p];
     auto ld = [&](int i) { return a[i]; };
     auto st = [&](int i, u64 v) { a[i] = v; };
-    if constexpr (INV) T::inverse(sm, Pr, twp(dc, p), ld, st);
-    else T::forward(sm, Pr, twp(dc, p), ld, st);
+    if constexpr (INV) ntt_inverse<T>(sm, Pr, twp(dc, p), ld, st);
+    else ntt_forward<T>(sm, Pr, twp(dc, p), ld, st);
 }
 
 void ntt_batch(const Launch& L, uint64_t* data, int batch, int limbs, int prime0, bool inverse)
@@ -133,7 +133,7 @@ k_ks_digits(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t ct_s
     const DPrime Pr = dc->p[j];
     auto ld = [&](int i) { return galois ? src[galois_src(i, galois, LOGN)] : src[i]; };
     auto st = [&](int i, u64 v) { dst[i] = v; };
-    T::inverse(sm, Pr, twp(dc, j), ld, st);
+    ntt_inverse<T>(sm, Pr, twp(dc, j), ld, st);
 }
 
 // (2) ModUp: D_{j,e} = NTT_{p_e}(d_j mod p_e) for e != j, e in [0, nl] (nl = special)
@@ -153,7 +153,7 @@ k_ks_modup(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* __r
     u64* dst = modup + (((size_t)b * nl + j) * (nl + 1) + e) * T::N;
     auto ld = [&](int i) { return reduce64_lazy(src[i], Pr); };
     auto st = [&](int i, u64 v) { dst[i] = v; };
-    T::forward(sm, Pr, twp(dc, p), ld, st);
+    ntt_forward<T>(sm, Pr, twp(dc, p), ld, st);
 }
 
 // (3) inner product u_c[e] = sum_j D_{j,e} key_j.c[p_e]  (128-bit accumulation, one reduction)
@@ -200,7 +200,7 @@ k_ks_moddown_intt(const DCtx* __restrict__ dc, const u64* __restrict__ acc, u64*
     const DPrime Pr = dc->p[special];
     auto ld = [&](int i) { return src[i]; };
     auto st = [&](int i, u64 v) { dst[i] = v; };
-    T::inverse(sm, Pr, twp(dc, special), ld, st);
+    ntt_inverse<T>(sm, Pr, twp(dc, special), ld, st);
 }
 
 // (5) ModDown part 2: out_c[i] = (u_c[i] - NTT_{q_i}(centered(r_c) mod q_i)) P^{-1}  (+ addend)
@@ -230,7 +230,7 @@ k_ks_moddown_out(const DCtx* __restrict__ dc, const u64* __restrict__ acc, const
         if (accumulate) x = addmod(x, o[k], Pr.q);
         o[k] = x;
     };
-    T::forward(sm, Pr, twp(dc, i), ld, st);
+    ntt_forward<T>(sm, Pr, twp(dc, i), ld, st);
 }
 
 void keyswitch(const Launch& L, const KsIn& in, const uint64_t* key, int batch, int nl, const KsWork& w,
@@ -287,7 +287,7 @@ k_rescale_intt(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t i
     const DPrime Pr = dc->p[l];
     auto ld = [&](int i) { return src[i]; };
     auto st = [&](int i, u64 v) { dst[i] = v; };
-    T::inverse(sm, Pr, twp(dc, l), ld, st);
+    ntt_inverse<T>(sm, Pr, twp(dc, l), ld, st);
 }
 
 template <int LOGN>
@@ -312,7 +312,7 @@ k_rescale_out(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t in
         if (bi) x = addmod(x, bi[k], Pr.q);
         o[k] = x;
     };
-    T::forward(sm, Pr, twp(dc, i), ld, st);
+    ntt_forward<T>(sm, Pr, twp(dc, i), ld, st);
 }
 
 void rescale(const Launch& L, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, int batch,
@@ -476,7 +476,7 @@ k_decrypt(const DCtx* __restrict__ dc, const u64* __restrict__ ct, size_t ct_str
     u64* o = out + ((size_t)b * nl + l) * T::N;
     auto ld = [&](int i) { return addmod(c0[i], mulmod(c1[i], s[i], Pr), Pr.q); };
     auto st = [&](int i, u64 v) { o[i] = v; };
-    T::inverse(sm, Pr, twp(dc, l), ld, st);
+    ntt_inverse<T>(sm, Pr, twp(dc, l), ld, st);
 }
 
 void decrypt(const Launch& L, const uint64_t* ct, size_t ct_stride, const uint64_t* s_ntt, uint64_t* out, int batch,
@@ -506,7 +506,7 @@ k_signed_to_ntt(const DCtx* __restrict__ dc, const long long* __restrict__ coeff
     u64* o = out + ((size_t)y * nl + l) * T::N;
     auto ld = [&](int i) { return signed_to_res(src[i], Pr); };
     auto st = [&](int i, u64 v) { o[i] = v; };
-    T::forward(sm, Pr, twp(dc, l), ld, st);
+    ntt_forward<T>(sm, Pr, twp(dc, l), ld, st);
 }
 
 void signed_to_ntt(const Launch& L, const int64_t* coeffs, uint64_t* out, int count, int nl)
@@ -537,7 +537,7 @@ k_sample_ntt(const DCtx* __restrict__ dc, u64* __restrict__ out, int nlimbs, int
     u64* o = out + ((size_t)y * nlimbs + limb) * T::N;
     auto ld = [&](int i) { return signed_to_res(sample_small(dc, kind, seed, stream, (u64)i), Pr); };
     auto st = [&](int i, u64 v) { o[i] = v; };
-    T::forward(sm, Pr, twp(dc, p), ld, st);
+    ntt_forward<T>(sm, Pr, twp(dc, p), ld, st);
 }
 
 void sample_ntt(const Launch& L, uint64_t* out, int ny, int nlimbs, int nl_data, int kind, uint64_t seed,

@@ -30,6 +30,18 @@ __device__ __forceinline__ void static_for(F&& f)
 
 constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x >> 1); }
 
+// Prime classes: the lazy-reduction schedule is chosen from the headroom 2^64 / q (bounds tracked
+// per stage at compile time).
+//   PC_SMALL  q < 2^44: no reductions inside the transform (forward grows by <= 2q per stage,
+//                       inverse doubles per stage; both stay < 2^60 for 14 stages)
+//   PC_MID    q < 2^52: forward without reductions, inverse Harvey-lazy
+//   PC_BIG    q < 2^61: Harvey-lazy both ways ([0,4q) forward, [0,2q) inverse)
+enum { PC_SMALL = 0, PC_MID = 1, PC_BIG = 2 };
+__host__ __device__ __forceinline__ int prime_class(u64 q)
+{
+    return q < (1ULL << 44) ? PC_SMALL : (q < (1ULL << 52) ? PC_MID : PC_BIG);
+}
+
 template <int LOGN_, int NT_>
 struct NttCta {
     static constexpr int LOGN = LOGN_;
@@ -66,7 +78,7 @@ struct NttCta {
     // "pass-ordered", see ntt_tw_position, so lanes with consecutive b0 read consecutive words).
     __device__ __forceinline__ static int tw_index(int S0, int r, int b0, int j) { return (1 << (S0 + r)) + (j << S0) + b0; }
 
-    template <int P>
+    template <int P, int PC>
     __device__ __forceinline__ static void fwd_compute(u64 (&x)[E], int tid, const u64* __restrict__ W,
                                                        const u64* __restrict__ Wsh, u64 q, u64 q2)
     {
@@ -86,7 +98,7 @@ struct NttCta {
                     const u64 w = __ldg(W + m), ws = __ldg(Wsh + m);
                     u64& X = x[g * (1 << K) + i];
                     u64& Y = x[g * (1 << K) + i + half];
-                    const u64 xx = csub(X, q2);
+                    const u64 xx = (PC == PC_BIG) ? csub(X, q2) : X;
                     const u64 t = shoup_mul(Y, w, ws, q);
                     X = xx + t;
                     Y = xx - t + q2;
@@ -95,7 +107,7 @@ struct NttCta {
         }
     }
 
-    template <int P>
+    template <int P, int PC>
     __device__ __forceinline__ static void inv_compute(u64 (&x)[E], int tid, const u64* __restrict__ IW,
                                                        const u64* __restrict__ IWsh, u64 q, u64 q2)
     {
@@ -116,16 +128,30 @@ struct NttCta {
                     u64& X = x[g * (1 << K) + i];
                     u64& Y = x[g * (1 << K) + i + half];
                     const u64 u = X, v = Y;
-                    X = csub(u + v, q2);
-                    Y = shoup_mul(u - v + q2, w, ws, q);
+                    if constexpr (PC == PC_SMALL) {
+                        // both inputs < 2^(c+1) q after c = LOGN - S0 - 1 - r stages: no reduction
+                        X = u + v;
+                        Y = shoup_mul(u - v + (q << (LOGN - G_::S0 - r)), w, ws, q);
+                    } else {
+                        X = csub(u + v, q2);
+                        Y = shoup_mul(u - v + q2, w, ws, q);
+                    }
                 }
             }
         }
     }
 
+    // forward outputs: [0, 4q) (BIG) or [0, 30q) (SMALL/MID) -> [0, q)
+    template <int PC>
+    __device__ __forceinline__ static u64 fwd_final(u64 v, const DPrime& Pr)
+    {
+        if constexpr (PC == PC_BIG) return csub(csub(v, Pr.q2), Pr.q);
+        else return reduce64(v, Pr);
+    }
+
     // Forward NTT of one limb.  ld(idx) -> value in [0, 2q); st(idx, v) receives v in [0, q).
     // `tw` points at this prime's [4][N] table block.  `sm` holds N words (+ nothing else).
-    template <bool STAGED = true, class Load, class Store>
+    template <int PC = PC_BIG, bool STAGED = true, class Load, class Store>
     __device__ __forceinline__ static void forward(u64* sm, const DPrime& Pr, const u64* __restrict__ tw,
                                                    Load&& ld, Store&& st)
     {
@@ -146,7 +172,7 @@ struct NttCta {
                     if constexpr (P == 0) x[g * (1 << K) + i] = ld(idx);
                     else x[g * (1 << K) + i] = sm[swz(idx)];
                 }
-            fwd_compute<P>(x, tid, W, Wsh, q, q2);
+            fwd_compute<P, PC>(x, tid, W, Wsh, q, q2);
 #pragma unroll
             for (int g = 0; g < G_::G; ++g)
 #pragma unroll
@@ -155,7 +181,7 @@ struct NttCta {
                     u64 v = x[g * (1 << K) + i];
                     if constexpr (P == NPASS - 1) {
                         if constexpr (STAGED) sm[swz(idx)] = v;
-                        else st(idx, csub(csub(v, q2), q));
+                        else st(idx, fwd_final<PC>(v, Pr));
                     } else {
                         sm[swz(idx)] = v;
                     }
@@ -167,14 +193,14 @@ struct NttCta {
 #pragma unroll 4
             for (int c = 0; c < E; ++c) {
                 const int idx = c * NT + tid;
-                st(idx, csub(csub(sm[swz(idx)], q2), q));
+                st(idx, fwd_final<PC>(sm[swz(idx)], Pr));
             }
             __syncthreads();   // shared memory free again on return
         }
     }
 
     // Inverse NTT of one limb (includes N^{-1}).  ld(idx) -> value in [0, 2q); st gets [0, q).
-    template <bool STAGED = true, class Load, class Store>
+    template <int PC = PC_BIG, bool STAGED = true, class Load, class Store>
     __device__ __forceinline__ static void inverse(u64* sm, const DPrime& Pr, const u64* __restrict__ tw,
                                                    Load&& ld, Store&& st)
     {
@@ -205,7 +231,7 @@ struct NttCta {
                     if constexpr (P == NPASS - 1 && !STAGED) x[g * (1 << K) + i] = ld(idx);
                     else x[g * (1 << K) + i] = sm[swz(idx)];
                 }
-            inv_compute<P>(x, tid, IW, IWsh, q, q2);
+            inv_compute<P, PC>(x, tid, IW, IWsh, q, q2);
 #pragma unroll
             for (int g = 0; g < G_::G; ++g)
 #pragma unroll
@@ -219,6 +245,23 @@ struct NttCta {
         });
     }
 };
+
+// Runtime dispatch on the prime class (uniform per CTA).
+template <class T, class Load, class Store>
+__device__ __forceinline__ void ntt_forward(u64* sm, const DPrime& Pr, const u64* tw, Load&& ld, Store&& st)
+{
+    switch (prime_class(Pr.q)) {
+    case PC_SMALL: T::template forward<PC_SMALL>(sm, Pr, tw, ld, st); break;
+    case PC_MID: T::template forward<PC_MID>(sm, Pr, tw, ld, st); break;
+    default: T::template forward<PC_BIG>(sm, Pr, tw, ld, st); break;
+    }
+}
+template <class T, class Load, class Store>
+__device__ __forceinline__ void ntt_inverse(u64* sm, const DPrime& Pr, const u64* tw, Load&& ld, Store&& st)
+{
+    if (prime_class(Pr.q) == PC_SMALL) T::template inverse<PC_SMALL>(sm, Pr, tw, ld, st);
+    else T::template inverse<PC_BIG>(sm, Pr, tw, ld, st);
+}
 
 // Threads per CTA for each supported ring dimension (E = 32 for N >= 8192, 16 below).
 __host__ __device__ constexpr int ntt_loge(int logn) { return logn >= 13 ? 5 : 4; }
