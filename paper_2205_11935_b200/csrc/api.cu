@@ -373,7 +373,7 @@ static void sizes_impl(const ckks_params* p, size_t* tb, size_t* kb, size_t* wb,
         if (g != 1 && std::find(ids.begin(), ids.end(), g) == ids.end()) ids.push_back(g);
     }
     const size_t key_words = p->n_special ? (size_t)L * 2 * (L + 1) * n : 0;
-    *tb = align256(sizeof(DCtx)) + align256((size_t)np * 4 * n * 8);
+    *tb = align256(sizeof(DCtx)) + align256((size_t)np * 8 * n * 8);
     *kb = align256((size_t)np * n * 8) + align256((size_t)2 * L * n * 8) + ids.size() * key_words * 8;
     const int B = (int)p->max_batch;
     size_t w = std::max(enc_work_words(L, n, B), p->n_special ? ks_work_words(L, n, B) : (size_t)0);
@@ -419,7 +419,7 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
         h.n_data = L;
         h.n_special = c->ns;
         h.n_primes = np;
-        std::vector<u64> tw((size_t)np * 4 * n);
+        std::vector<u64> tw((size_t)np * 8 * n);
         for (int i = 0; i < np; ++i) {
             const u64 q = primes[i];
             const u64 psi = min_root(q, c->log_n), ipsi = h_pow(psi, q - 2, q);
@@ -434,7 +434,7 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
             P.r64_sh = h_shoup(P.r64, q);
             // W[idx] = psi^{brev(idx)} (stage s = floor(log2 idx), block idx - 2^s), stored at the
             // pass-ordered position ntt_tw_position (ntt.cuh); same for psi^{-1}.
-            u64* W = tw.data() + (size_t)i * 4 * n;
+            u64* W = tw.data() + (size_t)i * 8 * n;
             std::vector<u64> fw(n), iw(n);
             u64 pw = 1, ipw = 1;
             for (int m = 0; m < n; ++m) {
@@ -456,6 +456,15 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
                 W[n + pos] = h_shoup(fw[idx], q);
                 W[2 * n + pos] = iw[idx];
                 W[3 * n + pos] = h_shoup(iw[idx], q);
+            }
+            // FP64 copies for PC_FP primes: w and fl(w / q), as raw double bits
+            for (int pos = 0; pos < n; ++pos) {
+                const double wd = (double)W[pos], iwd = (double)W[2 * n + pos];
+                const double wq = wd / (double)q, iwq = iwd / (double)q;
+                std::memcpy(&W[4 * n + pos], &wd, 8);
+                std::memcpy(&W[5 * n + pos], &wq, 8);
+                std::memcpy(&W[6 * n + pos], &iwd, 8);
+                std::memcpy(&W[7 * n + pos], &iwq, 8);
             }
             for (int b = 0; b < np; ++b) {
                 h.qmod[i][b] = q % primes[b];

@@ -16,7 +16,7 @@
 namespace ck {
 
 // ------------------------------------------------------------------------------------ helpers
-__device__ __forceinline__ const u64* twp(const DCtx* dc, int p) { return dc->tw + (size_t)p * 4 * dc->n; }
+__device__ __forceinline__ const u64* twp(const DCtx* dc, int p) { return dc->tw + (size_t)p * 8 * dc->n; }
 
 // NTT-domain automorphism (R3): out[k] = in[src(k)] with 2 brev(src)+1 = g (2 brev(k)+1) mod 2N
 __device__ __forceinline__ int galois_src(int k, u32 g, int logn)

@@ -30,16 +30,45 @@ __device__ __forceinline__ void static_for(F&& f)
 
 constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x >> 1); }
 
-// Prime classes: the lazy-reduction schedule is chosen from the headroom 2^64 / q (bounds tracked
-// per stage at compile time).
-//   PC_SMALL  q < 2^44: no reductions inside the transform (forward grows by <= 2q per stage,
-//                       inverse doubles per stage; both stay < 2^60 for 14 stages)
-//   PC_MID    q < 2^52: forward without reductions, inverse Harvey-lazy
-//   PC_BIG    q < 2^61: Harvey-lazy both ways ([0,4q) forward, [0,2q) inverse)
-enum { PC_SMALL = 0, PC_MID = 1, PC_BIG = 2 };
+// Prime classes: the arithmetic and the lazy-reduction schedule are chosen from q (bounds tracked
+// per stage).
+//   PC_FP     q < 2^45: residues held as exact integers in FP64 registers; butterflies on the
+//                       FP64 pipe (8 DFMA-class ops: error-free product + rint quotient), signed
+//                       representatives; forward needs no reduction, inverse reduces per pass
+//   PC_MID    q < 2^52: 64-bit integer Shoup, forward without reductions, inverse Harvey-lazy
+//   PC_BIG    q < 2^61: 64-bit integer Shoup, Harvey-lazy both ways ([0,4q) fwd, [0,2q) inv)
+enum { PC_FP = 0, PC_MID = 1, PC_BIG = 2, PC_SMALL = 3 };
 __host__ __device__ __forceinline__ int prime_class(u64 q)
 {
-    return q < (1ULL << 44) ? PC_SMALL : (q < (1ULL << 52) ? PC_MID : PC_BIG);
+    return q < (1ULL << 45) ? PC_FP : (q < (1ULL << 52) ? PC_MID : PC_BIG);
+}
+
+// ---- FP64 modular arithmetic on exact integers (|values| < 2^51)
+#define CK_RND_MAGIC 6755399441055744.0   /* 1.5 * 2^52: x + M - M = rint(x) for |x| < 2^51 */
+#define CK_TWO52 4503599627370496.0
+// y * w mod q as a signed representative in (-0.51 q, 0.51 q); wq = fl(w / q)
+__device__ __forceinline__ double fmodmul(double y, double w, double wq, double q)
+{
+    const double ph = y * w;
+    const double pl = __fma_rn(y, w, -ph);                        // exact low part of y*w
+    const double k = __fma_rn(y, wq, CK_RND_MAGIC) - CK_RND_MAGIC; // rint(y w / q)
+    return __fma_rn(-k, q, ph) + pl;                               // exact integer
+}
+// v mod q, signed representative in [-q/2, q/2]; qinv = fl(1/q)
+__device__ __forceinline__ double freduce(double v, double q, double qinv)
+{
+    const double k = __fma_rn(v, qinv, CK_RND_MAGIC) - CK_RND_MAGIC;
+    return __fma_rn(-k, q, v);
+}
+__device__ __forceinline__ double u2d(u64 a) { return __longlong_as_double((long long)(a | 0x4330000000000000ULL)) - CK_TWO52; }
+// v in [0, 2^52) exact integer -> u64
+__device__ __forceinline__ u64 d2u(double v) { return (u64)__double_as_longlong(v + CK_TWO52) & 0xFFFFFFFFFFFFFULL; }
+// signed representative with |v| < 2^51 -> canonical [0, q)
+__device__ __forceinline__ u64 fcanon(double v, double q, double qinv)
+{
+    double r = freduce(v, q, qinv);   // [-q/2, q/2]
+    r = r < 0.0 ? r + q : r;
+    return d2u(r);
 }
 
 template <int LOGN_, int NT_>
@@ -139,6 +168,148 @@ struct NttCta {
                 }
             }
         }
+    }
+
+    // ---- FP64 variants (PC_FP): x holds exact signed integers
+    template <int P>
+    __device__ __forceinline__ static void fwd_compute_fp(double (&x)[E], int tid, const double* __restrict__ Wd,
+                                                          const double* __restrict__ Wq, double q)
+    {
+        using G_ = Pass<P>;
+        constexpr int K = G_::K;
+#pragma unroll
+        for (int g = 0; g < G_::G; ++g) {
+            const int b0 = (g * NT + tid) >> G_::SH;
+#pragma unroll
+            for (int r = 0; r < K; ++r) {
+                const int half = 1 << (K - 1 - r);
+#pragma unroll
+                for (int i = 0; i < (1 << K); ++i) {
+                    if (i & half) continue;
+                    const int m = tw_index(G_::S0, r, b0, i >> (K - r));
+                    const double w = __ldg(Wd + m), wq = __ldg(Wq + m);
+                    double& X = x[g * (1 << K) + i];
+                    double& Y = x[g * (1 << K) + i + half];
+                    const double t = fmodmul(Y, w, wq, q);   // |t| < 0.51 q
+                    const double xx = X;
+                    X = xx + t;                              // |.| grows by < 0.51 q per stage
+                    Y = xx - t;
+                }
+            }
+        }
+    }
+
+    template <int P>
+    __device__ __forceinline__ static void inv_compute_fp(double (&x)[E], int tid, const double* __restrict__ IWd,
+                                                          const double* __restrict__ IWq, double q, double qinv)
+    {
+        using G_ = Pass<P>;
+        constexpr int K = G_::K;
+        // pass entry: bring every value back to [-q/2, q/2] (the X lineage doubles per stage)
+        if constexpr (P != NPASS - 1) {
+#pragma unroll
+            for (int i = 0; i < E; ++i) x[i] = freduce(x[i], q, qinv);
+        }
+#pragma unroll
+        for (int g = 0; g < G_::G; ++g) {
+            const int b0 = (g * NT + tid) >> G_::SH;
+#pragma unroll
+            for (int r = K - 1; r >= 0; --r) {
+                const int half = 1 << (K - 1 - r);
+#pragma unroll
+                for (int i = 0; i < (1 << K); ++i) {
+                    if (i & half) continue;
+                    const int m = tw_index(G_::S0, r, b0, i >> (K - r));
+                    const double w = __ldg(IWd + m), wq = __ldg(IWq + m);
+                    double& X = x[g * (1 << K) + i];
+                    double& Y = x[g * (1 << K) + i + half];
+                    const double u = X, v = Y;
+                    X = u + v;
+                    Y = fmodmul(u - v, w, wq, q);
+                }
+            }
+        }
+    }
+
+    template <class Load, class Store>
+    __device__ __forceinline__ static void forward_fp(u64* sm, const DPrime& Pr, const u64* __restrict__ tw,
+                                                      Load&& ld, Store&& st)
+    {
+        const int tid = threadIdx.x;
+        const double q = (double)Pr.q, qinv = 1.0 / q;
+        const double* Wd = reinterpret_cast<const double*>(tw + 4 * N);
+        const double* Wq = reinterpret_cast<const double*>(tw + 5 * N);
+        double* smd = reinterpret_cast<double*>(sm);
+        double x[E];
+        static_for<0, NPASS>([&](auto pc) {
+            constexpr int P = decltype(pc)::value;
+            using G_ = Pass<P>;
+            constexpr int K = G_::K;
+#pragma unroll
+            for (int g = 0; g < G_::G; ++g)
+#pragma unroll
+                for (int i = 0; i < (1 << K); ++i) {
+                    const int idx = index<P>(tid, g, i);
+                    if constexpr (P == 0) x[g * (1 << K) + i] = u2d(ld(idx));
+                    else x[g * (1 << K) + i] = smd[swz(idx)];
+                }
+            fwd_compute_fp<P>(x, tid, Wd, Wq, q);
+#pragma unroll
+            for (int g = 0; g < G_::G; ++g)
+#pragma unroll
+                for (int i = 0; i < (1 << K); ++i) smd[swz(index<P>(tid, g, i))] = x[g * (1 << K) + i];
+            __syncthreads();
+        });
+#pragma unroll 4
+        for (int c = 0; c < E; ++c) {
+            const int idx = c * NT + tid;
+            st(idx, fcanon(smd[swz(idx)], q, qinv));
+        }
+        __syncthreads();
+    }
+
+    template <class Load, class Store>
+    __device__ __forceinline__ static void inverse_fp(u64* sm, const DPrime& Pr, const u64* __restrict__ tw,
+                                                      Load&& ld, Store&& st)
+    {
+        const int tid = threadIdx.x;
+        const double q = (double)Pr.q, qinv = 1.0 / q;
+        const double* IWd = reinterpret_cast<const double*>(tw + 6 * N);
+        const double* IWq = reinterpret_cast<const double*>(tw + 7 * N);
+        const double ninv = (double)Pr.ninv, ninvq = ninv / q;
+        double* smd = reinterpret_cast<double*>(sm);
+        double x[E];
+#pragma unroll 4
+        for (int c = 0; c < E; ++c) {
+            const int idx = c * NT + tid;
+            smd[swz(idx)] = u2d(ld(idx));
+        }
+        __syncthreads();
+        static_for<0, NPASS>([&](auto pc) {
+            constexpr int P = NPASS - 1 - decltype(pc)::value;
+            using G_ = Pass<P>;
+            constexpr int K = G_::K;
+#pragma unroll
+            for (int g = 0; g < G_::G; ++g)
+#pragma unroll
+                for (int i = 0; i < (1 << K); ++i) x[g * (1 << K) + i] = smd[swz(index<P>(tid, g, i))];
+            inv_compute_fp<P>(x, tid, IWd, IWq, q, qinv);
+#pragma unroll
+            for (int g = 0; g < G_::G; ++g)
+#pragma unroll
+                for (int i = 0; i < (1 << K); ++i) {
+                    const int idx = index<P>(tid, g, i);
+                    const double v = x[g * (1 << K) + i];
+                    if constexpr (P == 0) {
+                        double r = fmodmul(v, ninv, ninvq, q);   // (-0.51 q, 0.51 q)
+                        r = r < 0.0 ? r + q : r;
+                        st(idx, d2u(r));
+                    } else {
+                        smd[swz(idx)] = v;
+                    }
+                }
+            __syncthreads();
+        });
     }
 
     // forward outputs: [0, 4q) (BIG) or [0, 30q) (SMALL/MID) -> [0, q)
@@ -251,7 +422,7 @@ template <class T, class Load, class Store>
 __device__ __forceinline__ void ntt_forward(u64* sm, const DPrime& Pr, const u64* tw, Load&& ld, Store&& st)
 {
     switch (prime_class(Pr.q)) {
-    case PC_SMALL: T::template forward<PC_SMALL>(sm, Pr, tw, ld, st); break;
+    case PC_FP: T::forward_fp(sm, Pr, tw, ld, st); break;
     case PC_MID: T::template forward<PC_MID>(sm, Pr, tw, ld, st); break;
     default: T::template forward<PC_BIG>(sm, Pr, tw, ld, st); break;
     }
@@ -259,7 +430,7 @@ __device__ __forceinline__ void ntt_forward(u64* sm, const DPrime& Pr, const u64
 template <class T, class Load, class Store>
 __device__ __forceinline__ void ntt_inverse(u64* sm, const DPrime& Pr, const u64* tw, Load&& ld, Store&& st)
 {
-    if (prime_class(Pr.q) == PC_SMALL) T::template inverse<PC_SMALL>(sm, Pr, tw, ld, st);
+    if (prime_class(Pr.q) == PC_FP) T::inverse_fp(sm, Pr, tw, ld, st);
     else T::template inverse<PC_BIG>(sm, Pr, tw, ld, st);
 }
 
