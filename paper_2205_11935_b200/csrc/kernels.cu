@@ -156,81 +156,87 @@ k_ks_modup(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* __r
     ntt_forward<T>(sm, Pr, twp(dc, p), ld, st);
 }
 
-// (3) inner product u_c[e] = sum_j D_{j,e} key_j.c[p_e]  (128-bit accumulation, one reduction)
-__global__ void __launch_bounds__(256)
-k_ks_ip(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ in, size_t ct_stride,
-        size_t comp_off, u32 galois, const u64* __restrict__ key, int L, int nl, int special, u64* __restrict__ acc)
-{
-    const int n = dc->n, logn = dc->log_n;
-    const int k = blockIdx.x * 256 + threadIdx.x;
-    const int e = blockIdx.y, b = blockIdx.z;
-    const int p = (e == nl) ? special : e;
-    const int pk = (e == nl) ? L : e;
-    const DPrime Pr = dc->p[p];
-    Acc128 a0, a1;
-    a0.zero();
-    a1.zero();
-    for (int j = 0; j < nl; ++j) {
-        u64 dv;
-        if (j == e) {
-            const u64* src = in + (size_t)b * ct_stride + comp_off + (size_t)j * n;
-            dv = galois ? src[galois_src(k, galois, logn)] : src[k];
-        } else {
-            dv = modup[(((size_t)b * nl + j) * (nl + 1) + e) * n + k];
-        }
-        const u64 k0 = key[(((size_t)j * 2 + 0) * (L + 1) + pk) * n + k];
-        const u64 k1 = key[(((size_t)j * 2 + 1) * (L + 1) + pk) * n + k];
-        a0.mac(dv, k0);
-        a1.mac(dv, k1);
-    }
-    acc[(((size_t)b * 2 + 0) * (nl + 1) + e) * n + k] = a0.reduce(Pr);
-    acc[(((size_t)b * 2 + 1) * (nl + 1) + e) * n + k] = a1.reduce(Pr);
-}
-
-// (4) ModDown part 1: r_c = iNTT_P(u_c[P])
+// (3) ModDown, special-prime row: r_c = iNTT_P( sum_j D_{j,P} key_j.c[P] )  -- the inner product for
+//     the special prime is computed in the (coalesced, staged) loader of the inverse NTT.
 template <int LOGN>
 __global__ void __launch_bounds__(NttThreads<LOGN>::value)
-k_ks_moddown_intt(const DCtx* __restrict__ dc, const u64* __restrict__ acc, u64* __restrict__ rem, int nl, int special)
+k_ks_moddown_intt(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ key, int L,
+                  int nl, int special, u64* __restrict__ rem)
 {
     extern __shared__ u64 sm[];
     using T = NttCta<LOGN, NttThreads<LOGN>::value>;
     const int c = blockIdx.x, b = blockIdx.y;
-    const u64* src = acc + (((size_t)b * 2 + c) * (nl + 1) + nl) * T::N;
-    u64* dst = rem + ((size_t)b * 2 + c) * T::N;
     const DPrime Pr = dc->p[special];
-    auto ld = [&](int i) { return src[i]; };
+    u64* dst = rem + ((size_t)b * 2 + c) * T::N;
+    auto ld = [&](int k) {
+        Acc128 a;
+        a.zero();
+        for (int j = 0; j < nl; ++j)
+            a.mac(modup[(((size_t)b * nl + j) * (nl + 1) + nl) * T::N + k],
+                  key[(((size_t)j * 2 + c) * (L + 1) + L) * T::N + k]);
+        return a.reduce(Pr);
+    };
     auto st = [&](int i, u64 v) { dst[i] = v; };
     ntt_inverse<T>(sm, Pr, twp(dc, special), ld, st);
 }
 
-// (5) ModDown part 2: out_c[i] = (u_c[i] - NTT_{q_i}(centered(r_c) mod q_i)) P^{-1}  (+ addend)
+// (4) ModDown, data rows: x_c[i] = NTT_{q_i}(centered(r_c) mod q_i)   (written into acc[b][c][i])
 template <int LOGN>
 __global__ void __launch_bounds__(NttThreads<LOGN>::value)
-k_ks_moddown_out(const DCtx* __restrict__ dc, const u64* __restrict__ acc, const u64* __restrict__ rem, int nl,
-                 int special, u64* __restrict__ out, size_t out_stride, const u64* __restrict__ add,
-                 size_t add_stride, u32 add_galois, int add_comp1, int accumulate)
+k_ks_moddown_ntt(const DCtx* __restrict__ dc, const u64* __restrict__ rem, int nl, int special, u64* __restrict__ xo)
 {
     extern __shared__ u64 sm[];
     using T = NttCta<LOGN, NttThreads<LOGN>::value>;
     const int i = blockIdx.x, c = blockIdx.y, b = blockIdx.z;
     const DPrime Pr = dc->p[i];
     const u64 Pmod = dc->qmod[special][i];
-    const u64 Pinv = dc->qinv[special][i], Pinv_sh = dc->qinv_sh[special][i];
     const u64 Pbig = dc->p[special].q;
     const u64* r = rem + ((size_t)b * 2 + c) * T::N;
-    const u64* u = acc + (((size_t)b * 2 + c) * (nl + 1) + i) * T::N;
-    u64* o = out + (size_t)b * out_stride + ((size_t)c * nl + i) * T::N;
-    const u64* ad = nullptr;
-    if (add && (c == 0 || add_comp1)) ad = add + (size_t)b * add_stride + ((size_t)c * nl + i) * T::N;
+    u64* o = xo + (((size_t)b * 2 + c) * (nl + 1) + i) * T::N;
     auto ld = [&](int k) { return centered_to(r[k], Pbig, Pmod, Pr); };
-    auto st = [&](int k, u64 v) {
-        u64 x = shoup_mul(u[k] + Pr.q - v, Pinv, Pinv_sh, Pr.q);   // [0, 2q)
-        x = csub(x, Pr.q);
-        if (ad) x = addmod(x, add_galois ? ad[galois_src(k, add_galois, LOGN)] : ad[k], Pr.q);
-        if (accumulate) x = addmod(x, o[k], Pr.q);
-        o[k] = x;
-    };
+    auto st = [&](int k, u64 v) { o[k] = v; };
     ntt_forward<T>(sm, Pr, twp(dc, i), ld, st);
+}
+
+// (5) inner product over the data primes fused with the ModDown combine and the output epilogue:
+//     out_c[i] = (sum_j D_{j,i} key_j.c[i] - x_c[i]) P^{-1}  (+ addend, + out)     D_{i,i} = input limb
+__global__ void __launch_bounds__(256)
+k_ks_ip_combine(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ in,
+                size_t ct_stride, size_t comp_off, u32 galois, const u64* __restrict__ key, int L, int nl, int special,
+                const u64* __restrict__ xo, u64* __restrict__ out, size_t out_stride, const u64* __restrict__ add,
+                size_t add_stride, u32 add_galois, int add_comp1, int accumulate)
+{
+    const int n = dc->n, logn = dc->log_n;
+    const int k = blockIdx.x * 256 + threadIdx.x, i = blockIdx.y, b = blockIdx.z;
+    const DPrime Pr = dc->p[i];
+    Acc128 a0, a1;
+    a0.zero();
+    a1.zero();
+    for (int j = 0; j < nl; ++j) {
+        u64 dv;
+        if (j == i) {
+            const u64* src = in + (size_t)b * ct_stride + comp_off + (size_t)j * n;
+            dv = galois ? src[galois_src(k, galois, logn)] : src[k];
+        } else {
+            dv = modup[(((size_t)b * nl + j) * (nl + 1) + i) * n + k];
+        }
+        a0.mac(dv, key[(((size_t)j * 2 + 0) * (L + 1) + i) * n + k]);
+        a1.mac(dv, key[(((size_t)j * 2 + 1) * (L + 1) + i) * n + k]);
+    }
+    const u64 Pinv = dc->qinv[special][i], Pinv_sh = dc->qinv_sh[special][i];
+    const u64 u[2] = {a0.reduce(Pr), a1.reduce(Pr)};
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const u64 x = xo[(((size_t)b * 2 + c) * (nl + 1) + i) * n + k];
+        u64 v = csub(shoup_mul(u[c] + Pr.q - x, Pinv, Pinv_sh, Pr.q), Pr.q);
+        if (add && (c == 0 || add_comp1)) {
+            const u64* ad = add + (size_t)b * add_stride + ((size_t)c * nl + i) * n;
+            v = addmod(v, add_galois ? ad[galois_src(k, add_galois, logn)] : ad[k], Pr.q);
+        }
+        u64& o = out[(size_t)b * out_stride + ((size_t)c * nl + i) * n + k];
+        if (accumulate) v = addmod(v, o, Pr.q);
+        o = v;
+    }
 }
 
 void keyswitch(const Launch& L, const KsIn& in, const uint64_t* key, int batch, int nl, const KsWork& w,
@@ -245,7 +251,7 @@ void keyswitch(const Launch& L, const KsIn& in, const uint64_t* key, int batch, 
         allow_smem(k_ks_digits<LG>, smem);
         allow_smem(k_ks_modup<LG>, smem);
         allow_smem(k_ks_moddown_intt<LG>, smem);
-        allow_smem(k_ks_moddown_out<LG>, smem);
+        allow_smem(k_ks_moddown_ntt<LG>, smem);
         const bool pk = L.probe && L.probe->on(PROBE_KEYSWITCH), pm = L.probe && L.probe->on(PROBE_MODUP);
         if (pk) {
             L.probe->mark(L.st);
@@ -261,12 +267,11 @@ void keyswitch(const Launch& L, const KsIn& in, const uint64_t* key, int batch, 
         }
         k_ks_modup<LG><<<dim3(nl * nl, batch), NT, smem, L.st>>>(L.dc, w.digits, w.modup, nl, special);
         if (pm) L.probe->mark(L.st);
-        k_ks_ip<<<dim3(n / 256, nl + 1, batch), 256, 0, L.st>>>(L.dc, w.modup, in.base, in.ct_stride, in.comp_off,
-                                                               in.galois, key, L.n_data, nl, special, w.acc);
-        k_ks_moddown_intt<LG><<<dim3(2, batch), NT, smem, L.st>>>(L.dc, w.acc, w.rem, nl, special);
-        k_ks_moddown_out<LG><<<dim3(nl, 2, batch), NT, smem, L.st>>>(L.dc, w.acc, w.rem, nl, special, out.base,
-                                                                     out.ct_stride, out.add, out.add_stride,
-                                                                     out.add_galois, out.add_comp1, out.accumulate);
+        k_ks_moddown_intt<LG><<<dim3(2, batch), NT, smem, L.st>>>(L.dc, w.modup, key, L.n_data, nl, special, w.rem);
+        k_ks_moddown_ntt<LG><<<dim3(nl, 2, batch), NT, smem, L.st>>>(L.dc, w.rem, nl, special, w.acc);
+        k_ks_ip_combine<<<dim3(n / 256, nl, batch), 256, 0, L.st>>>(
+            L.dc, w.modup, in.base, in.ct_stride, in.comp_off, in.galois, key, L.n_data, nl, special, w.acc, out.base,
+            out.ct_stride, out.add, out.add_stride, out.add_galois, out.add_comp1, out.accumulate);
         if (pk) L.probe->mark(L.st);
     });
     check_launch("keyswitch");
@@ -391,51 +396,86 @@ void add(const Launch& L, const uint64_t* a, size_t sa, const uint64_t* b, size_
 // Thread (coefficient x, giant index k) keeps its t1 plaintext words in registers and loops over the
 // batch, so every plaintext word is read once per launch; v words are shared through L1 by the t2
 // threads of the same coefficient.
-template <int T1MAX>
-__global__ void __launch_bounds__(256)
-k_bsgs_mac(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u64* __restrict__ v0,
-           size_t v0_stride, const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl)
+// One (coefficient x, ciphertext b) per thread; for each component and each half of the giant
+// indices it keeps 16 accumulators and streams j: v_j[b] is loaded once per (c, k-half) and used
+// for 16 products, plaintext words come from the shared tile A[t][16] (broadcast across b-lanes).
+// FP64 path for primes < 2^45: product y*w exact as ph+pl, quotient rint(ph/q), signed remainder,
+// sum of t1 remainders |.| < 17 q stays exact.  Integer path: 128-bit lazy accumulation.
+template <bool FP>
+__device__ __forceinline__ void bsgs_mac_body(const DCtx* __restrict__ dc, const u64* __restrict__ A,
+                                              const u64* __restrict__ v0, size_t v0_stride, const u64* __restrict__ vb,
+                                              u64* __restrict__ wout, int t1, int t2, int batch, int nl, int l, int x,
+                                              int tx, int ty)
 {
-    // CTA = 16 coefficients x one limb; its plaintext tile A[t][16] is staged in shared memory once
-    // and reused for every ciphertext; thread (x, b-lane) keeps v_j[b] (all j, both components) in
-    // registers and produces w_k[b] for every k.
+    const int n = dc->n;
+    const DPrime Pr = dc->p[l];
+    const size_t ctw = (size_t)2 * nl * n;
+    const double q = (double)Pr.q, qinv = 1.0 / q;
+    for (int b = ty; b < batch; b += 16) {
+        for (int c = 0; c < 2; ++c) {
+            const size_t off = ((size_t)c * nl + l) * n + x;
+            for (int k0 = 0; k0 < t2; k0 += 16) {
+                const int nk = (t2 - k0) < 16 ? (t2 - k0) : 16;
+                if constexpr (FP) {
+                    double acc[16];
+#pragma unroll
+                    for (int z = 0; z < 16; ++z) acc[z] = 0.0;
+#pragma unroll 2
+                    for (int j = 0; j < t1; ++j) {
+                        const u64* v = (j == 0) ? v0 + (size_t)b * v0_stride : vb + ((size_t)(j - 1) * batch + b) * ctw;
+                        const double y = u2d(v[off]);
+#pragma unroll
+                        for (int z = 0; z < 16; ++z) {
+                            if (z < nk) {
+                                const double w = __longlong_as_double((long long)A[((k0 + z) * t1 + j) * 16 + tx]);
+                                const double ph = y * w;
+                                const double pl = __fma_rn(y, w, -ph);
+                                const double kq = __fma_rn(ph, qinv, CK_RND_MAGIC) - CK_RND_MAGIC;
+                                acc[z] += __fma_rn(-kq, q, ph) + pl;
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int z = 0; z < 16; ++z)
+                        if (z < nk) wout[((size_t)(k0 + z) * batch + b) * ctw + off] = fcanon(acc[z], q, qinv);
+                } else {
+                    Acc128 acc[16];
+#pragma unroll
+                    for (int z = 0; z < 16; ++z) acc[z].zero();
+#pragma unroll 2
+                    for (int j = 0; j < t1; ++j) {
+                        const u64* v = (j == 0) ? v0 + (size_t)b * v0_stride : vb + ((size_t)(j - 1) * batch + b) * ctw;
+                        const u64 y = v[off];
+#pragma unroll
+                        for (int z = 0; z < 16; ++z)
+                            if (z < nk) acc[z].mac(A[((k0 + z) * t1 + j) * 16 + tx], y);
+                    }
+#pragma unroll
+                    for (int z = 0; z < 16; ++z)
+                        if (z < nk) wout[((size_t)(k0 + z) * batch + b) * ctw + off] = acc[z].reduce(Pr);
+                }
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256, 2)
+k_bsgs_mac(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u64* __restrict__ v0, size_t v0_stride,
+           const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl)
+{
     extern __shared__ u64 A[];
     const int n = dc->n;
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int x0 = blockIdx.x * 16, x = x0 + tx, l = blockIdx.y;
     const int t = t1 * t2;
-    for (int i = threadIdx.x; i < t * 16; i += blockDim.x)
-        A[i] = pts[((size_t)(i >> 4) * nl + l) * n + x0 + (i & 15)];
-    __syncthreads();
-    const DPrime Pr = dc->p[l];
-    const size_t ctw = (size_t)2 * nl * n;
-    for (int b = ty; b < batch; b += 16) {
-        u64 va[T1MAX], vc[T1MAX];
-#pragma unroll
-        for (int j = 0; j < T1MAX; ++j) {
-            if (j < t1) {
-                const u64* v = (j == 0) ? v0 + (size_t)b * v0_stride : vb + ((size_t)(j - 1) * batch + b) * ctw;
-                va[j] = v[(size_t)l * n + x];
-                vc[j] = v[((size_t)nl + l) * n + x];
-            }
-        }
-        for (int k = 0; k < t2; ++k) {
-            Acc128 a0, a1;
-            a0.zero();
-            a1.zero();
-#pragma unroll
-            for (int j = 0; j < T1MAX; ++j) {
-                if (j < t1) {
-                    const u64 a = A[(k * t1 + j) * 16 + tx];
-                    a0.mac(a, va[j]);
-                    a1.mac(a, vc[j]);
-                }
-            }
-            u64* w = wout + ((size_t)k * batch + b) * ctw;
-            w[(size_t)l * n + x] = a0.reduce(Pr);
-            w[((size_t)nl + l) * n + x] = a1.reduce(Pr);
-        }
+    const bool fp = prime_class(dc->p[l].q) == PC_FP;
+    for (int i = threadIdx.x; i < t * 16; i += blockDim.x) {
+        const u64 a = pts[((size_t)(i >> 4) * nl + l) * n + x0 + (i & 15)];
+        A[i] = fp ? (u64)__double_as_longlong(u2d(a)) : a;
     }
+    __syncthreads();
+    if (fp) bsgs_mac_body<true>(dc, A, v0, v0_stride, vb, wout, t1, t2, batch, nl, l, x, tx, ty);
+    else bsgs_mac_body<false>(dc, A, v0, v0_stride, vb, wout, t1, t2, batch, nl, l, x, tx, ty);
 }
 
 void bsgs_mac(const Launch& L, const uint64_t* pts, const uint64_t* v0, size_t v0_stride, const uint64_t* vbaby,
@@ -443,19 +483,10 @@ void bsgs_mac(const Launch& L, const uint64_t* pts, const uint64_t* v0, size_t v
 {
     if (batch <= 0) return;
     const int n = 1 << L.log_n;
-    if (t1 > 32) throw std::runtime_error("bsgs_mac: t1 <= 32");
     const size_t smem = (size_t)t1 * t2 * 16 * 8;
-    dim3 grid(n / 16, nl);
-    if (t1 <= 8) {
-        allow_smem(k_bsgs_mac<8>, smem);
-        k_bsgs_mac<8><<<grid, 256, smem, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl);
-    } else if (t1 <= 16) {
-        allow_smem(k_bsgs_mac<16>, smem);
-        k_bsgs_mac<16><<<grid, 256, smem, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl);
-    } else {
-        allow_smem(k_bsgs_mac<32>, smem);
-        k_bsgs_mac<32><<<grid, 256, smem, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl);
-    }
+    if (smem > 200 * 1024) throw std::runtime_error("bsgs_mac: plaintext tile too large (t <= 1600)");
+    allow_smem(k_bsgs_mac, smem);
+    k_bsgs_mac<<<dim3(n / 16, nl), 256, smem, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl);
     check_launch("bsgs_mac");
     if (L.counter) ++*L.counter;
 }
