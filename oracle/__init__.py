@@ -90,6 +90,7 @@ def _declare(L):
         "or_keyswitch": (INT, [vp, u64p, INT, I64, u64p]),
         "or_relinearize": (INT, [vp, u64p, INT, u64p]),
         "or_rotate": (INT, [vp, u64p, INT, I64, u64p]),
+        "or_rotate_hoisted": (INT, [vp, u64p, INT, I64, u64p]),
         "or_rescale": (INT, [vp, u64p, INT, INT, u64p]),
         "or_drop_level": (None, [vp, u64p, INT, INT, INT, u64p]),
     }
@@ -287,6 +288,13 @@ class Context:
         ct = np.ascontiguousarray(ct, dtype=np.uint64)
         out = np.empty_like(ct)
         _check(lib().or_rotate(self._c, _p(ct), ct.shape[1] - 1, step, _p(out)), f"rotate({step})")
+        return out
+
+    def rotate_hoisted(self, ct, step):
+        """Hoisted rotation (NEXT f-1): digits of the unrotated c1, automorphism on the signed digits."""
+        ct = np.ascontiguousarray(ct, dtype=np.uint64)
+        out = np.empty_like(ct)
+        _check(lib().or_rotate_hoisted(self._c, _p(ct), ct.shape[1] - 1, step, _p(out)), f"rotate_hoisted({step})")
         return out
 
     def rescale(self, ct):

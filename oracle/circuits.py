@@ -111,12 +111,14 @@ class OpCount:
         self.add = 0
 
 
-def matvec(ctx, ct: Ct, layer: EncodedLayer, ops: OpCount | None = None) -> Ct:
-    """Eq. 1 then one rescale (R7) then + bias (R-bias).  t1+t2-2 rotations, t pt-ct mults."""
+def matvec(ctx, ct: Ct, layer: EncodedLayer, ops: OpCount | None = None, hoisted: bool = False) -> Ct:
+    """Eq. 1 then one rescale (R7) then + bias (R-bias).  t1+t2-2 rotations, t pt-ct mults.
+    hoisted=True: the t1-1 baby-step rotations are hoisted (NEXT f-1, R11b)."""
     l = ct.level
     assert layer.level == l, "layer encoded for another level"
     pts = [ctx.plain(layer.diag_coeffs[i], l) for i in range(layer.t)]
-    baby = [ct.data] + [ctx.rotate(ct.data, j) for j in range(1, layer.t1)]
+    rot = ctx.rotate_hoisted if hoisted else ctx.rotate
+    baby = [ct.data] + [rot(ct.data, j) for j in range(1, layer.t1)]
     if ops:
         ops.rot += layer.t1 - 1
     y = None
@@ -195,14 +197,15 @@ def activation_plaintexts(ctx, layers, activation: str):
     return np.stack(out)
 
 
-def forward(ctx, ct: Ct, layers, activation: str = "square", ops: OpCount | None = None) -> Ct:
+def forward(ctx, ct: Ct, layers, activation: str = "square", ops: OpCount | None = None,
+            hoisted: bool = False) -> Ct:
     """dense_1 -> act -> replicate -> dense_2 -> ... (P:L118 frozen stack, BASELINE cfg4)."""
     for li, layer in enumerate(layers):
         if li > 0:
             ct = replicate(ctx, ct, layer.t)
             if ops:
                 ops.rot += 1
-        ct = matvec(ctx, ct, layer, ops)
+        ct = matvec(ctx, ct, layer, ops, hoisted=hoisted)
         if li < len(layers) - 1:
             if activation == "square":
                 ct = square(ctx, ct)

@@ -640,39 +640,29 @@ static u64 centered_mod(u64 r, u64 m, u64 q)
 
 /* ------------------------------------------------------------------ key switching (R5, R9-R12) */
 /*
- * KS(d; key) at level l, d in NTT form over q_0..q_l.  Output (u0, u1) in NTT form over q_0..q_l,
- * with  u0 + u1 s  ~=  d s'  (the key's s').  Steps, in the order of DESIGN.md R-KS:
- *   1. digits d_j = iNTT_{q_j}(d[j]) as integers in [0, q_j)                      (unsigned lift, R9)
- *   2. ModUp: D_{j,p} = NTT_p(d_j mod p) for every p in {q_0..q_l, P}
+ * Key switch from explicit digit polynomials (signed integer coefficients, one digit per data
+ * prime j <= l), R-KS steps 2-4:
+ *   2. ModUp: D_{j,p} = NTT_p(digit_j mod p) for every p in {q_0..q_l, P}
  *   3. inner product  u~_c[p] = sum_{j<=l} D_{j,p} key_j.c[p]   mod p
  *   4. ModDown: r = centered(iNTT_P(u~_c[P])),  u_c[i] = (u~_c[i] - NTT_{q_i}(r mod q_i)) P^{-1} mod q_i
  */
-int or_keyswitch(const or_ctx* c, const u64* d, int level, int64_t key_id, u64* out)
+static int ks_from_digits(const or_ctx* c, const int64_t* digit, int level, int64_t key_id, u64* out)
 {
     int kidx = find_key(c, key_id);
     if (kidx < 0) return -3;
-    if (level < 0 || level >= c->n_data) return -2;
     int n = c->n, L = c->n_data, nl = level + 1, np_key = L + 1;
     const u64* key = c->key[kidx];
-    /* extended prime list: data primes 0..l then the special prime (index L) */
     int ext[OR_MAXP];
     for (int i = 0; i < nl; i++) ext[i] = i;
     ext[nl] = L;
     int ne = nl + 1;
-    /* 1. digits */
-    u64* digit = (u64*)malloc(sizeof(u64) * (size_t)nl * n);
-    for (int j = 0; j < nl; j++) {
-        memcpy(digit + (size_t)j * n, d + (size_t)j * n, sizeof(u64) * n);
-        or_intt(c, j, digit + (size_t)j * n);
-    }
-    /* 2+3. ModUp and inner product */
     u64* acc = (u64*)calloc((size_t)2 * ne * n, sizeof(u64));
     u64* D = (u64*)malloc(sizeof(u64) * n);
     for (int j = 0; j < nl; j++) {
         for (int e = 0; e < ne; e++) {
             int p = ext[e];
             u64 q = c->q[p];
-            for (int k = 0; k < n; k++) D[k] = digit[(size_t)j * n + k] % q;
+            for (int k = 0; k < n; k++) D[k] = from_signed(digit[(size_t)j * n + k], q);
             or_ntt(c, p, D);
             for (int comp = 0; comp < 2; comp++) {
                 const u64* kv = key + (((size_t)j * 2 + comp) * np_key + p) * n;
@@ -681,7 +671,6 @@ int or_keyswitch(const or_ctx* c, const u64* d, int level, int64_t key_id, u64* 
             }
         }
     }
-    /* 4. ModDown */
     u64 P = c->q[L];
     u64* r = (u64*)malloc(sizeof(u64) * n);
     u64* t = (u64*)malloc(sizeof(u64) * n);
@@ -698,8 +687,34 @@ int or_keyswitch(const or_ctx* c, const u64* d, int level, int64_t key_id, u64* 
             for (int k = 0; k < n; k++) o[k] = mulmod(submod(a[k], t[k], q), pinv, q);
         }
     }
-    free(digit); free(acc); free(D); free(r); free(t);
+    free(acc); free(D); free(r); free(t);
     return 0;
+}
+
+/* digits of d (NTT form): d_j = iNTT_{q_j}(d[j]) as integers in [0, q_j)  (R9, unsigned lift) */
+static int64_t* digits_of(const or_ctx* c, const u64* d, int level)
+{
+    int n = c->n, nl = level + 1;
+    int64_t* digit = (int64_t*)malloc(sizeof(int64_t) * (size_t)nl * n);
+    u64* tmp = (u64*)malloc(sizeof(u64) * n);
+    for (int j = 0; j < nl; j++) {
+        memcpy(tmp, d + (size_t)j * n, sizeof(u64) * n);
+        or_intt(c, j, tmp);
+        for (int k = 0; k < n; k++) digit[(size_t)j * n + k] = (int64_t)tmp[k];
+    }
+    free(tmp);
+    return digit;
+}
+
+/* KS(d; key) at level l with the unsigned digits of d (R-KS step 1 + ks_from_digits). */
+int or_keyswitch(const or_ctx* c, const u64* d, int level, int64_t key_id, u64* out)
+{
+    if (find_key(c, key_id) < 0) return -3;
+    if (level < 0 || level >= c->n_data) return -2;
+    int64_t* digit = digits_of(c, d, level);
+    int st = ks_from_digits(c, digit, level, key_id, out);
+    free(digit);
+    return st;
 }
 
 /* Relinearize (R-composite): (c0, c1, c2) -> (c0, c1) + KS(c2; rlk).  in3: [3][l+1][N]. */
@@ -740,6 +755,50 @@ int or_rotate(const or_ctx* c, const u64* ct, int level, int64_t step, u64* out)
     }
     free(rc);
     free(u);
+    return st;
+}
+
+/*
+ * Hoisted rotation (NEXT f-1; reading R11b): the digits are taken from the UNROTATED c1 and the
+ * automorphism is applied to them as signed integer polynomials,
+ *     d_j = iNTT_{q_j}(c1[j]) in [0, q_j),   d'_j = sigma_g(d_j)  (coefficient i -> i g mod 2N, negated
+ *     if >= N, as a signed integer: -d, not q_j - d),
+ *     (sigma_g(c0), 0) + ModDown(sum_j ModUp(d'_j) key_j).
+ * All rotations of one ciphertext can then share ModUp(d_j) (sigma_g commutes with NTT_p).  The
+ * result differs from the non-hoisted one by an encryption of a small value (different rounding
+ * of the digit lift), so it has its own pins.
+ */
+int or_rotate_hoisted(const or_ctx* c, const u64* ct, int level, int64_t step, u64* out)
+{
+    int n = c->n, nl = level + 1;
+    size_t h = (size_t)nl * n;
+    u64 g = or_galois_elt(c, step);
+    if (g == 1) { memcpy(out, ct, sizeof(u64) * 2 * h); return 0; }
+    if (find_key(c, (int64_t)g) < 0) return -3;
+    int64_t* digit = digits_of(c, ct + h, level);
+    int64_t* sd = (int64_t*)malloc(sizeof(int64_t) * (size_t)nl * n);
+    u64 two_n = 2ULL * (u64)n;
+    for (int j = 0; j < nl; j++)
+        for (u64 i = 0; i < (u64)n; i++) {
+            u64 e = (i * g) % two_n;
+            int64_t v = digit[(size_t)j * n + i];
+            if (e < (u64)n) sd[(size_t)j * n + e] = v;
+            else sd[(size_t)j * n + (e - n)] = -v;
+        }
+    u64* u = (u64*)malloc(sizeof(u64) * 2 * h);
+    int st = ks_from_digits(c, sd, level, (int64_t)g, u);
+    if (st == 0) {
+        u64* rc0 = (u64*)malloc(sizeof(u64) * h);
+        for (int p = 0; p < nl; p++) or_automorphism_ntt(c, p, ct + (size_t)p * n, g, rc0 + (size_t)p * n);
+        for (int p = 0; p < nl; p++)
+            for (int k = 0; k < n; k++) {
+                size_t i = (size_t)p * n + k;
+                out[i] = addmod(rc0[i], u[i], c->q[p]);
+                out[h + i] = u[h + i];
+            }
+        free(rc0);
+    }
+    free(digit); free(sd); free(u);
     return st;
 }
 

@@ -335,3 +335,86 @@ def test_forward_cubic_small_ring_vs_float64():
     y, ref, out = _forward_case(cfg, "cubic")
     assert np.max(np.abs(y[: ref.size] - ref)) < 1e-5
     assert out.level == 1
+
+
+# ------------------------------------------------------------------------------- hoisted rotation (f-1)
+def _hoisted_ks_by_bigint(ctx, c1_ntt, key, level, g):
+    """Definition: digits of the unrotated c1, sigma_g applied as SIGNED integer polynomials, then
+    U = sum_j sigma_g(d_j) * key_j over Q_l P (schoolbook), out = round(U / P)."""
+    n, L = ctx.n, ctx.n_data
+    nl = level + 1
+    ext = list(range(nl)) + [L]
+    P = ctx.primes[L]
+    digits = []
+    for j in range(nl):
+        d = [int(v) for v in ctx.intt(c1_ntt[j], j)]
+        sd = [0] * n
+        for i, v in enumerate(d):
+            e = (i * g) % (2 * n)
+            if e < n:
+                sd[e] = v
+            else:
+                sd[e - n] = -v
+        digits.append(sd)
+    outs = []
+    for comp in range(2):
+        per_prime = []
+        for p in ext:
+            q = ctx.primes[p]
+            acc = [0] * n
+            for j in range(nl):
+                kc = [int(v) for v in ctx.intt(key[j, comp, p], p)]
+                prod = schoolbook_negacyclic([x % q for x in digits[j]], kc, q)
+                acc = [(a + b) % q for a, b in zip(acc, prod)]
+            per_prime.append(acc)
+        U, QP = crt(per_prime, [ctx.primes[p] for p in ext])
+        Ql = QP // P
+        outs.append([((x - centered(x, P)) // P) % Ql for x in U])
+    return outs
+
+
+@pytest.mark.parametrize("level", [2, 1])
+def test_hoisted_rotation_exact_bigint(level):
+    ctx = small_ctx(steps=(1, 3))
+    n = ctx.n
+    rng = np.random.default_rng(21 + level)
+    ct = np.stack([np.stack([rng.integers(0, ctx.primes[i], n, dtype=np.uint64) for i in range(level + 1)])
+                   for _ in range(2)])
+    for step in (1, 3):
+        g = ctx.galois_elt(step)
+        out = ctx.rotate_hoisted(ct, step)
+        ref = _hoisted_ks_by_bigint(ctx, ct[1], ctx.export_key(g), level, g)
+        got1, _ = crt([ctx.intt(out[1, i], i) for i in range(level + 1)], ctx.primes[: level + 1])
+        assert got1 == ref[1]
+        # component 0 = sigma_g(c0) + u0
+        c0r = np.stack([ctx.automorphism_ntt(ct[0, i], i, g) for i in range(level + 1)])
+        u0 = np.stack([(out[0, i].astype(object) - c0r[i].astype(object)) % ctx.primes[i] for i in range(level + 1)])
+        got0, _ = crt([ctx.intt(u0[i].astype(np.uint64), i) for i in range(level + 1)], ctx.primes[: level + 1])
+        assert got0 == ref[0]
+
+
+def test_hoisted_rotation_decrypts_and_differs():
+    ctx = small_ctx(log_n=10, steps=(1, 5, -3))
+    v = np.random.default_rng(5).uniform(-1, 1, ctx.n // 2)
+    ct = enc_vec(ctx, v, 2.0 ** 40)
+    for step in (1, 5, -3):
+        h = ctx.rotate_hoisted(ct.data, step)
+        nh = ctx.rotate(ct.data, step)
+        assert not np.array_equal(h, nh)                        # different digit lift -> different residues
+        dec = dec_vec(ctx, C.Ct(h, ct.scale))
+        assert np.max(np.abs(dec - np.roll(v, -step))) < 1e-6
+
+
+def test_forward_cfg1_hoisted_vs_float64():
+    cfg = S.CFG1
+    ctx = oracle.Context(cfg.log_n, cfg.data_bits, cfg.special_bits)
+    ctx.keygen(cfg.key_seed, C.rotation_steps_for(cfg.layers))
+    prob = S.dense_problem(cfg)
+    Delta = 2.0 ** 40
+    layers = C.encode_model(ctx, prob["W"], prob["b"], ctx.top_level, Delta, "none")
+    ct = enc_vec(ctx, C.pack_input(prob["x"][0], layers[0].t, ctx.n // 2), Delta)
+    ops = C.OpCount()
+    out = C.forward(ctx, ct, layers, "none", ops, hoisted=True)
+    y = dec_vec(ctx, out)
+    assert np.max(np.abs(y[:16] - (prob["W"][0] @ prob["x"][0] + prob["b"][0]))) < 1e-6
+    assert ops.rot == 14
