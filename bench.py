@@ -42,6 +42,7 @@ def parse():
     p.add_argument("--no-extras", action="store_true", help="skip the cfg2/cfg3 sub-benchmarks")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-hoist", action="store_true", help="non-hoisted baby steps (SEAL semantics, R11)")
     return p.parse_args()
 
 
@@ -139,7 +140,7 @@ def profiled_traffic(kernel):
         return None
 
 
-def build_forward(G, cfg, B, max_batch, device):
+def build_forward(G, cfg, B, max_batch, device, hoisted=True):
     """Product path only: library encoder, device keygen/encryption."""
     import synthetic as S
     shapes = list(cfg.layers)
@@ -152,6 +153,7 @@ def build_forward(G, cfg, B, max_batch, device):
     layers = [G.Layer(ctx, r, c, levels[i], W=prob["W"][i], bias=prob["b"][i], in_scale=scales[i])
               for i, (r, c) in enumerate(shapes)]
     model = G.Model(ctx, layers, G.ACT_SQUARE)
+    model.set_hoisting(hoisted)
     t0 = G.bsgs_plan(*shapes[0])[0]
     slots = ctx.n // 2
     ms = np.empty((B, ctx.n), dtype=np.int64)
@@ -177,7 +179,7 @@ def run_ours(args):
     device = torch.device("cuda", local)
     cfg = S.CFG5
     B = args.batch or cfg.batch
-    ctx, model, ct, prob = build_forward(G, cfg, B, args.max_batch, device)
+    ctx, model, ct, prob = build_forward(G, cfg, B, args.max_batch, device, hoisted=not args.no_hoist)
     out = ctx.empty_ct(B, model.final_level)
     work = torch.empty(model.work_bytes(B), dtype=torch.uint8, device=device)
     stream = torch.cuda.current_stream()
@@ -222,6 +224,7 @@ def run_ours(args):
               "config": {"workload": cfg.name, "batch_per_gpu": B, "N": ctx.n, "limbs": ctx.n_data,
                          "special_primes": ctx.n_special, "dnum": ctx.n_data, "layers": [list(s) for s in cfg.layers],
                          "activation": "square", "max_batch": args.max_batch,
+                         "baby_steps": "non-hoisted (R11)" if args.no_hoist else "hoisted (NEXT f-1, R11b)",
                          "l2": "inputs (2 GiB of ciphertexts) larger than L2; no flush",
                          "parallelism": f"replicas x{world}"},
               "gpu_launches": launches, "roofline": roofline}

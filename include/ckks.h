@@ -111,6 +111,13 @@ ckks_status ckks_ntt_inv(ckks_ctx* ctx, uint64_t* d, uint32_t batch, uint32_t li
  * KS(sigma_g(c1); gk_g), g = 5^(step mod N/2) mod 2N, non-hoisted (R11).  out must not alias in;
  * out->data is written, its level/scale/batch/n_comp are set.  CKKS_E_NOKEY if no key for g. */
 ckks_status ckks_rotate(ckks_ctx* ctx, const ckks_ct* in, int32_t step, ckks_ct* out, void* stream);
+/* Hoisted rotations (R11b): n_steps rotations of the same input
+ * sharing one ModUp of the unrotated c1: out_s = (sigma_g(c0), 0) + ModDown(sum_j sigma_g(D_j) gk_j)
+ * with D_j = ModUp of the unsigned digits of c1 -- computed as sigma_g(c0 + ModDown(sum_j D_j key'_j))
+ * with pre-permuted keys.  Residues differ from ckks_rotate (different digit lift); both decrypt
+ * to the rotated slots.  outs: array of n_steps ciphertext descriptors (device data preallocated). */
+ckks_status ckks_rotate_hoisted(ckks_ctx* ctx, const ckks_ct* in, const int32_t* steps, uint32_t n_steps,
+                                ckks_ct* outs, void* stream);
 /* Tensor product (a0 b0, a0 b1 + a1 b0, a1 b1); equal level and batch; out3 has 3 components. */
 ckks_status ckks_mul(ckks_ctx* ctx, const ckks_ct* a, const ckks_ct* b, ckks_ct* out3, void* stream);
 /* (c0, c1, c2) -> (c0, c1) + KS(c2; rlk).  in3 has 3 components; out must not alias in3. */
@@ -153,6 +160,8 @@ ckks_status ckks_model_sizes(const ckks_ctx* ctx, uint32_t n_layers, int32_t act
 ckks_status ckks_model_create(ckks_ctx* ctx, const ckks_layer* const* layers, uint32_t n_layers, int32_t activation,
                               const int64_t* act_coeffs, void* dev_buf, void* stream, ckks_model** out);
 void ckks_model_destroy(ckks_model* model);
+/* on != 0: the baby-step rotations of every dense layer are hoisted (ckks_rotate_hoisted semantics). */
+ckks_status ckks_model_set_hoisting(ckks_model* model, int32_t on);
 /* BSGS split of a rows x cols layer: t = max(rows, cols) padded to a multiple of
  * t1 = 2^ceil(ceil(log2 t)/2), t2 = t / t1 (R5). */
 ckks_status ckks_bsgs_plan(uint32_t rows, uint32_t cols, uint32_t* t, uint32_t* t1, uint32_t* t2);

@@ -60,6 +60,8 @@ SIGNATURES = {
     "ckks_ntt_inv": (_I, [_VP, _VP, _U32, _U32, _VP]),
     "ckks_rotate": (_I, [_VP, _PCT, _I, _PCT, _VP]),
     "ckks_mul": (_I, [_VP, _PCT, _PCT, _PCT, _VP]),
+    "ckks_rotate_hoisted": (_I, [_VP, _PCT, ctypes.POINTER(_I), _U32, _PCT, _VP]),
+    "ckks_model_set_hoisting": (_I, [_VP, _I]),
     "ckks_relinearize": (_I, [_VP, _PCT, _PCT, _VP]),
     "ckks_rescale": (_I, [_VP, _PCT, _PCT, _VP]),
     "ckks_add": (_I, [_VP, _PCT, _PCT, _PCT, _VP]),
@@ -259,6 +261,18 @@ class Context:
         out = out or self.empty_ct(ct.batch, ct.level)
         return self._op("ckks_rotate", ct, out=out, stream=stream, extra=(int(step),))
 
+    def rotate_hoisted(self, ct, steps, outs=None, stream=None):
+        steps = [int(s) for s in steps]
+        outs = outs or [self.empty_ct(ct.batch, ct.level) for _ in steps]
+        arr = (ckks_ct * len(steps))(*[o.c() for o in outs])
+        st = (_I * len(steps))(*steps)
+        i = ct.c()
+        _check(lib().ckks_rotate_hoisted(self.h, ctypes.byref(i), st, len(steps), arr, _stream(stream)),
+               "ckks_rotate_hoisted")
+        for o, a in zip(outs, arr):
+            o.level, o.scale = a.level, a.scale
+        return outs
+
     def mul(self, a, b, out=None, stream=None):
         out = out or self.empty_ct(a.batch, a.level, 3)
         return self._op("ckks_mul", a, b, out=out, stream=stream)
@@ -402,6 +416,10 @@ class Model:
             except Exception:
                 pass
             self.h = None
+
+    def set_hoisting(self, on=True):
+        _check(lib().ckks_model_set_hoisting(self.h, 1 if on else 0), "ckks_model_set_hoisting")
+        self.hoisted = bool(on)
 
     def work_bytes(self, batch):
         nb = ctypes.c_size_t()

@@ -196,6 +196,7 @@ struct ckks_ctx {
     u64* d_s = nullptr;      // [np][N] secret, NTT form
     u64* d_pk = nullptr;     // [2][L][N]
     u64* d_keys = nullptr;   // [nkeys][L][2][L+1][N]
+    u64* d_keys_perm = nullptr;   // Galois keys pre-permuted by sigma_{g^-1} (hoisted rotations)
     size_t key_words = 0;    // per switching key
     std::vector<int64_t> key_ids;
     std::map<int64_t, int> key_slot;
@@ -223,6 +224,13 @@ struct ckks_ctx {
         if (it == key_slot.end()) return nullptr;
         return d_keys + (size_t)it->second * key_words;
     }
+    const u64* key_perm(int64_t id) const
+    {
+        auto it = key_slot.find(id);
+        if (it == key_slot.end() || id == 0) return nullptr;
+        return d_keys_perm + (size_t)it->second * key_words;
+    }
+    uint32_t galois_inv(uint32_t g) const { return (uint32_t)h_pow(g, (u64)n - 1, 2ULL * n); }
     uint32_t galois(int64_t step) const
     {
         const int64_t slots = n / 2;
@@ -255,6 +263,7 @@ struct ckks_layer {
 struct ckks_model {
     std::vector<const ckks_layer*> layers;
     int activation;
+    int hoisted = 0;        // baby-step rotations hoisted (NEXT f-1)
     u64* d_act = nullptr;   // cubic: masked constant-term plaintexts [n_layers-1][L][N] (R23)
 };
 
@@ -305,6 +314,41 @@ void rotate_impl(ckks_ctx* c, const u64* in, size_t in_stride, int nl, int batch
         ck::KsOut ko{out + (size_t)b0 * out_stride, out_stride, in + (size_t)b0 * in_stride, in_stride, g, 0,
                      accumulate ? 1 : 0};
         ck::keyswitch(L, ki, key, B, nl, c->ks_work(B), ko);
+    }
+}
+
+// Hoisted rotations (NEXT f-1, R11b): one ModUp of the unrotated c1 shared by every step;
+// out_s = sigma_g(c0 + ModDown(sum_j D_j key'_j)),  key' = sigma_{g^-1}(gk_g).
+void rotate_hoisted_impl(ckks_ctx* c, const u64* in, size_t in_stride, int nl, int batch, const int64_t* steps,
+                         int n_steps, u64* const* outs, size_t out_stride, void* stream)
+{
+    auto L = c->launch(stream);
+    for (int s = 0; s < n_steps; ++s) {
+        const uint32_t g = c->galois(steps[s]);
+        if (g != 1 && !c->key_perm((int64_t)g))
+            throw CkksError(CKKS_E_NOKEY, "no Galois key for step " + std::to_string(steps[s]));
+    }
+    for (int b0 = 0; b0 < batch; b0 += (int)c->max_batch) {
+        const int B = std::min((int)c->max_batch, batch - b0);
+        const u64* inb = in + (size_t)b0 * in_stride;
+        ck::KsIn ki{inb, in_stride, (size_t)nl * c->n, 0};
+        auto w = c->ks_work(B);
+        bool have_modup = false;
+        for (int s = 0; s < n_steps; ++s) {
+            const uint32_t g = c->galois(steps[s]);
+            u64* ob = outs[s] + (size_t)b0 * out_stride;
+            if (g == 1) {
+                cuda_ok(cudaMemcpy2DAsync(ob, out_stride * 8, inb, in_stride * 8, c->ct_words(nl) * 8, B,
+                                          cudaMemcpyDeviceToDevice, (cudaStream_t)stream), "copy");
+                continue;
+            }
+            if (!have_modup) {
+                ck::keyswitch_modup(L, ki, B, nl, w);
+                have_modup = true;
+            }
+            ck::KsOut ko{ob, out_stride, inb, in_stride, 0, 0, 0};
+            ck::keyswitch_finish(L, ki, c->key_perm((int64_t)g), B, nl, w, ko, c->galois_inv(g));
+        }
     }
 }
 
@@ -374,7 +418,8 @@ static void sizes_impl(const ckks_params* p, size_t* tb, size_t* kb, size_t* wb,
     }
     const size_t key_words = p->n_special ? (size_t)L * 2 * (L + 1) * n : 0;
     *tb = align256(sizeof(DCtx)) + align256((size_t)np * 8 * n * 8);
-    *kb = align256((size_t)np * n * 8) + align256((size_t)2 * L * n * 8) + ids.size() * key_words * 8;
+    // every switching key, plus a sigma_{g^-1}-permuted copy per key slot (used by hoisted rotations)
+    *kb = align256((size_t)np * n * 8) + align256((size_t)2 * L * n * 8) + 2 * ids.size() * key_words * 8;
     const int B = (int)p->max_batch;
     size_t w = std::max(enc_work_words(L, n, B), p->n_special ? ks_work_words(L, n, B) : (size_t)0);
     // keygen scratch: e_ntt [L][L+1][N] + s' [np][N]
@@ -513,6 +558,7 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
                 c->key_ids.push_back(g);
         }
         for (size_t i = 0; i < c->key_ids.size(); ++i) c->key_slot[c->key_ids[i]] = (int)i;
+        c->d_keys_perm = c->d_keys + c->key_ids.size() * c->key_words;
         // ---- keygen on the device (R5, R13-R15; stream tags of DESIGN.md)
         auto Lc = c->launch(stream);
         const u64 seed = p->key_seed;
@@ -535,6 +581,9 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
                                            (u64)j);
                 ck::sample_ntt(Lc, e_ntt, L, L + 1, L, 1, seed, 5, (u64)id, 0, 0, 1);   // e_j (TAG 5)
                 ck::keyswitch_key_combine(Lc, key, e_ntt, c->d_s, sp, L);
+                if (id != 0)   // key'_j = sigma_{g^-1}(gk_j): sum_j sigma_g(D_j) gk_j = sigma_g(sum_j D_j key'_j)
+                    ck::galois_limbs(Lc, key, c->d_keys_perm + ki * c->key_words, (size_t)L * 2 * (L + 1),
+                                     c->galois_inv((uint32_t)id));
             }
         }
         cuda_ok(cudaStreamSynchronize(st), "keygen");
@@ -643,6 +692,38 @@ ckks_status ckks_rotate(ckks_ctx* c, const ckks_ct* in, int32_t step, ckks_ct* o
         out->scale = in->scale;
         return CKKS_OK;
     })
+}
+
+ckks_status ckks_rotate_hoisted(ckks_ctx* c, const ckks_ct* in, const int32_t* steps, uint32_t n_steps, ckks_ct* outs,
+                                void* stream)
+{
+    CK_TRY({
+        if (!c || !steps || !outs || n_steps == 0) throw CkksError(CKKS_E_PARAM, "null");
+        check_ct(c, in);
+        const int nl = (int)in->level + 1;
+        std::vector<int64_t> st(steps, steps + n_steps);
+        std::vector<u64*> o(n_steps);
+        for (uint32_t s = 0; s < n_steps; ++s) {
+            if (!outs[s].data || outs[s].data == in->data) throw CkksError(CKKS_E_SHAPE, "rotate_hoisted: bad out");
+            o[s] = outs[s].data;
+        }
+        rotate_hoisted_impl(c, in->data, c->ct_words(nl), nl, (int)in->batch, st.data(), (int)n_steps, o.data(),
+                            c->ct_words(nl), stream);
+        for (uint32_t s = 0; s < n_steps; ++s) {
+            outs[s].batch = in->batch;
+            outs[s].n_comp = 2;
+            outs[s].level = in->level;
+            outs[s].scale = in->scale;
+        }
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_model_set_hoisting(ckks_model* m, int32_t on)
+{
+    if (!m) return fail(CKKS_E_PARAM, "null");
+    m->hoisted = on ? 1 : 0;
+    return CKKS_OK;
 }
 
 ckks_status ckks_mul(ckks_ctx* c, const ckks_ct* a, const ckks_ct* b, ckks_ct* out3, void* stream)
@@ -840,15 +921,25 @@ ckks_status ckks_layer_work_sizes(const ckks_ctx* c, const ckks_layer* l, uint32
 
 // matvec on B ciphertexts (B <= max_batch): in -> out (level-1), work holds baby + W.
 static void matvec_chunk(ckks_ctx* c, const ckks_layer* ly, const u64* in, size_t in_stride, int B, u64* out,
-                         size_t out_stride, u64* work, void* stream)
+                         size_t out_stride, u64* work, void* stream, bool hoisted = false)
 {
     const int nl = (int)ly->level + 1;
     const size_t ctw = c->ct_words(nl);
     auto L = c->launch(stream);
     u64* baby = work;                                   // [t1-1][B][2][nl][N]
     u64* Wk = work + (size_t)(ly->t1 - 1) * B * ctw;    // [t2][B][2][nl][N]
-    for (uint32_t j = 1; j < ly->t1; ++j)
-        rotate_impl(c, in, in_stride, nl, B, (int64_t)j, baby + (size_t)(j - 1) * B * ctw, ctw, false, stream);
+    if (hoisted) {
+        std::vector<int64_t> steps;
+        std::vector<u64*> outs;
+        for (uint32_t j = 1; j < ly->t1; ++j) {
+            steps.push_back((int64_t)j);
+            outs.push_back(baby + (size_t)(j - 1) * B * ctw);
+        }
+        rotate_hoisted_impl(c, in, in_stride, nl, B, steps.data(), (int)steps.size(), outs.data(), ctw, stream);
+    } else {
+        for (uint32_t j = 1; j < ly->t1; ++j)
+            rotate_impl(c, in, in_stride, nl, B, (int64_t)j, baby + (size_t)(j - 1) * B * ctw, ctw, false, stream);
+    }
     ck::bsgs_mac(L, ly->d_pts, in, in_stride, baby, Wk, (int)ly->t1, (int)ly->t2, B, nl);
     for (uint32_t k = 1; k < ly->t2; ++k)
         rotate_impl(c, Wk + (size_t)k * B * ctw, ctw, nl, B, (int64_t)k * ly->t1, Wk, ctw, true, stream);
@@ -1055,7 +1146,7 @@ static void forward_chunk(ckks_ctx* c, const ckks_model* m, const u64* in, size_
         const bool last = (li == nlay - 1);
         u64* dst = last ? out : ((cur == bufA) ? bufB : bufA);
         const size_t dst_stride = last ? out_stride : c->ct_words(nl - 1);
-        matvec_chunk(c, ly, cur, cur_stride, B, dst, dst_stride, lwork, stream);
+        matvec_chunk(c, ly, cur, cur_stride, B, dst, dst_stride, lwork, stream, m->hoisted != 0);
         scale = scale * ly->pt_scale / (double)c->primes[level];
         level -= 1;
         nl -= 1;

@@ -10,6 +10,7 @@
 #include "ntt.cuh"
 #include "kernels.h"
 
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(256)
 k_ks_ip_combine(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ in,
                 size_t ct_stride, size_t comp_off, u32 galois, const u64* __restrict__ key, int L, int nl, int special,
                 const u64* __restrict__ xo, u64* __restrict__ out, size_t out_stride, const u64* __restrict__ add,
-                size_t add_stride, u32 add_galois, int add_comp1, int accumulate)
+                size_t add_stride, u32 add_galois, int add_comp1, int accumulate, u32 scatter_g)
 {
     const int n = dc->n, logn = dc->log_n;
     const int k = blockIdx.x * 256 + threadIdx.x, i = blockIdx.y, b = blockIdx.z;
@@ -233,31 +234,23 @@ k_ks_ip_combine(const DCtx* __restrict__ dc, const u64* __restrict__ modup, cons
             const u64* ad = add + (size_t)b * add_stride + ((size_t)c * nl + i) * n;
             v = addmod(v, add_galois ? ad[galois_src(k, add_galois, logn)] : ad[k], Pr.q);
         }
-        u64& o = out[(size_t)b * out_stride + ((size_t)c * nl + i) * n + k];
+        const int kd = scatter_g ? galois_src(k, scatter_g, logn) : k;
+        u64& o = out[(size_t)b * out_stride + ((size_t)c * nl + i) * n + kd];
         if (accumulate) v = addmod(v, o, Pr.q);
         o = v;
     }
 }
 
-void keyswitch(const Launch& L, const KsIn& in, const uint64_t* key, int batch, int nl, const KsWork& w,
-               const KsOut& out)
+void keyswitch_modup(const Launch& L, const KsIn& in, int batch, int nl, const KsWork& w)
 {
     if (batch <= 0) return;
     const int special = L.n_data;   // special prime is stored after the data primes
     const size_t smem = sizeof(u64) << L.log_n;
-    const int n = 1 << L.log_n;
     NTT_DISPATCH(L.log_n, {
         constexpr int NT = NttThreads<LG>::value;
         allow_smem(k_ks_digits<LG>, smem);
         allow_smem(k_ks_modup<LG>, smem);
-        allow_smem(k_ks_moddown_intt<LG>, smem);
-        allow_smem(k_ks_moddown_ntt<LG>, smem);
-        const bool pk = L.probe && L.probe->on(PROBE_KEYSWITCH), pm = L.probe && L.probe->on(PROBE_MODUP);
-        if (pk) {
-            L.probe->mark(L.st);
-            // switched component + addend in, 2 components out, key rows used once per launch
-            L.probe->alg_bytes += (4.0 * batch * nl + 2.0 * nl * (nl + 1)) * (double)(8 << L.log_n);
-        }
+        const bool pm = L.probe && L.probe->on(PROBE_MODUP);
         k_ks_digits<LG><<<dim3(nl, batch), NT, smem, L.st>>>(L.dc, in.base, in.ct_stride, in.comp_off, in.galois,
                                                               w.digits, nl);
         if (pm) {
@@ -267,15 +260,63 @@ void keyswitch(const Launch& L, const KsIn& in, const uint64_t* key, int batch, 
         }
         k_ks_modup<LG><<<dim3(nl * nl, batch), NT, smem, L.st>>>(L.dc, w.digits, w.modup, nl, special);
         if (pm) L.probe->mark(L.st);
+    });
+    check_launch("keyswitch_modup");
+    if (L.counter) *L.counter += 2;
+}
+
+void keyswitch_finish(const Launch& L, const KsIn& in, const uint64_t* key, int batch, int nl, const KsWork& w,
+                      const KsOut& out, uint32_t scatter_g)
+{
+    if (batch <= 0) return;
+    const int special = L.n_data;
+    const size_t smem = sizeof(u64) << L.log_n;
+    const int n = 1 << L.log_n;
+    NTT_DISPATCH(L.log_n, {
+        constexpr int NT = NttThreads<LG>::value;
+        allow_smem(k_ks_moddown_intt<LG>, smem);
+        allow_smem(k_ks_moddown_ntt<LG>, smem);
         k_ks_moddown_intt<LG><<<dim3(2, batch), NT, smem, L.st>>>(L.dc, w.modup, key, L.n_data, nl, special, w.rem);
         k_ks_moddown_ntt<LG><<<dim3(nl, 2, batch), NT, smem, L.st>>>(L.dc, w.rem, nl, special, w.acc);
         k_ks_ip_combine<<<dim3(n / 256, nl, batch), 256, 0, L.st>>>(
             L.dc, w.modup, in.base, in.ct_stride, in.comp_off, in.galois, key, L.n_data, nl, special, w.acc, out.base,
-            out.ct_stride, out.add, out.add_stride, out.add_galois, out.add_comp1, out.accumulate);
-        if (pk) L.probe->mark(L.st);
+            out.ct_stride, out.add, out.add_stride, out.add_galois, out.add_comp1, out.accumulate, scatter_g);
     });
-    check_launch("keyswitch");
-    if (L.counter) *L.counter += 5;
+    check_launch("keyswitch_finish");
+    if (L.counter) *L.counter += 3;
+}
+
+void keyswitch(const Launch& L, const KsIn& in, const uint64_t* key, int batch, int nl, const KsWork& w,
+               const KsOut& out)
+{
+    const bool pk = L.probe && L.probe->on(PROBE_KEYSWITCH);
+    if (pk) {
+        L.probe->mark(L.st);
+        // switched component + addend in, 2 components out, key rows used once per launch
+        L.probe->alg_bytes += (4.0 * batch * nl + 2.0 * nl * (nl + 1)) * (double)(8 << L.log_n);
+    }
+    keyswitch_modup(L, in, batch, nl, w);
+    keyswitch_finish(L, in, key, batch, nl, w, out, 0);
+    if (pk) L.probe->mark(L.st);
+}
+
+__global__ void k_galois_limbs(const DCtx* __restrict__ dc, const u64* __restrict__ in, u64* __restrict__ out, u32 g)
+{
+    const int n = dc->n;
+    const int k = blockIdx.x * 256 + threadIdx.x;
+    const size_t limb = blockIdx.y + (size_t)blockIdx.z * gridDim.y;
+    out[limb * n + k] = in[limb * n + galois_src(k, g, dc->log_n)];
+}
+
+void galois_limbs(const Launch& L, const uint64_t* in, uint64_t* out, size_t limbs, uint32_t g)
+{
+    const int n = 1 << L.log_n;
+    for (size_t done = 0; done < limbs; done += 65535) {
+        const unsigned cnt = (unsigned)std::min<size_t>(limbs - done, 65535);
+        k_galois_limbs<<<dim3(n / 256, cnt, 1), 256, 0, L.st>>>(L.dc, in + done * n, out + done * n, g);
+    }
+    check_launch("galois_limbs");
+    if (L.counter) ++*L.counter;
 }
 
 // ------------------------------------------------------------------------------------ rescale

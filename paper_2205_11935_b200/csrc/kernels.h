@@ -64,6 +64,14 @@ struct KsWork {
 };
 void keyswitch(const Launch&, const KsIn& in, const uint64_t* key, int batch, int nl, const KsWork& w,
                const KsOut& out);
+// the two halves of a key switch: ModUp of `in` into w (digits, modup), and the inner product +
+// ModDown from w.modup.  scatter_g != 0 writes the result permuted by sigma_{g} where the caller
+// passes g^{-1} (hoisted rotation: out = sigma_g(c0 + ModDown(sum_j D_j key'_j))).
+void keyswitch_modup(const Launch&, const KsIn& in, int batch, int nl, const KsWork& w);
+void keyswitch_finish(const Launch&, const KsIn& in, const uint64_t* key, int batch, int nl, const KsWork& w,
+                      const KsOut& out, uint32_t scatter_g);
+// out limbs[c][N] = in limbs[c][galois_src(k, g)] for `limbs` consecutive limbs (key pre-permutation)
+void galois_limbs(const Launch&, const uint64_t* in, uint64_t* out, size_t limbs, uint32_t g);
 
 // rescale: in [B][ncomp][nl][N] (stride in_stride words) -> out [B][ncomp][nl-1][N]; optional
 // bias plaintext [nl-1][N] added to component 0.

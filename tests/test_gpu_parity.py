@@ -132,6 +132,22 @@ def test_rotate_parity_ragged_batch(c1, step):
         assert np.array_equal(got[b], o.rotate(cts[b], step)), b
 
 
+def test_rotate_hoisted_parity(c1):
+    """NEXT f-1: hoisted rotations (one ModUp shared by all steps) vs the oracle's hoisted definition."""
+    cfg, g, o = c1
+    ms, cts = _enc_batch(cfg, o, 3, seed=31)
+    ct = g.from_numpy(cts, scale=2.0 ** 40)
+    steps = [1, 3, 0, 5, -7, 56]
+    outs = g.rotate_hoisted(ct, steps)
+    for st, out in zip(steps, outs):
+        got = u64(out.data)
+        for b in range(3):
+            assert np.array_equal(got[b], o.rotate_hoisted(cts[b], st)), (st, b)
+    low = o.drop_level(cts[0], 1)
+    outs = g.rotate_hoisted(g.from_numpy(low[None], scale=2.0 ** 40), [3])
+    assert np.array_equal(u64(outs[0].data)[0], o.rotate_hoisted(low, 3))
+
+
 def test_rotate_lower_level_and_errors(c1):
     cfg, g, o = c1
     ms, cts = _enc_batch(cfg, o, 1, seed=7)
@@ -209,7 +225,7 @@ def test_library_encoder_vs_oracle_encoder(c1):
 
 
 # ------------------------------------------------------------------------------------------ forward
-def _model_case(cfg, activation, B, max_batch, data_bits=None, log_n=None, seed_batch=None):
+def _model_case(cfg, activation, B, max_batch, data_bits=None, log_n=None, seed_batch=None, hoisted=False):
     log_n = log_n or cfg.log_n
     data_bits = data_bits or cfg.data_bits
     steps = OC.rotation_steps_for(cfg.layers)
@@ -223,6 +239,8 @@ def _model_case(cfg, activation, B, max_batch, data_bits=None, log_n=None, seed_
                        pt_scale=l.pt_scale, bias_scale=l.bias_scale) for l in layers]
     model = G.Model(g, glayers, {"none": 0, "square": 1, "cubic": 2}[activation],
                     act_coeffs=OC.activation_plaintexts(o, layers, activation))
+    if hoisted:
+        model.set_hoisting(True)
     ms = np.stack([OE.encode(OC.pack_input(prob["x"][b], layers[0].t, o.n // 2), Delta, o.n) for b in range(B)])
     ct = g.encrypt(ms, cfg.enc_seed, 0, Delta)
     out = model.forward(ct)
@@ -262,6 +280,31 @@ def test_forward_cfg4_parity_and_accuracy():
     # the library's own decryption and decoding agree
     gy = g.decode(u64(g.decrypt(out))[0], out.level, out.scale, 128)
     assert np.max(np.abs(gy - y)) < 1e-3
+
+
+@pytest.mark.parametrize("activation", ["square", "cubic"])
+def test_forward_small_ring_hoisted_parity(activation):
+    o, g, prob, layers, ms, ct, out = _model_case(
+        S.Config(name="small", log_n=12, data_bits=(60,) + (40,) * 5, special_bits=(60,), log2_scale=40,
+                 layers=((64, 128), (32, 64)), activation=activation, in_dim=128,
+                 weight_std=(1 / np.sqrt(128), 1 / np.sqrt(64))), activation, B=3, max_batch=2, hoisted=True)
+    got = u64(out.data)
+    for b in range(3):
+        ref = OC.forward(o, OC.Ct(o.encrypt(ms[b], S.CFG4.enc_seed, b), 2.0 ** 40), layers, activation, hoisted=True)
+        assert np.array_equal(got[b], ref.data), b
+        y = OC.plain_forward(prob["x"][b], prob["W"], prob["b"], activation)
+        dec = OE.decode(o.decrypt(ref.data), o.primes, ref.scale, o.n)
+        assert np.max(np.abs(dec[: y.size] - y)) < 1e-3
+
+
+def test_forward_cfg4_hoisted_parity_and_accuracy():
+    cfg = S.CFG4
+    o, g, prob, layers, ms, ct, out = _model_case(cfg, "square", B=2, max_batch=2, hoisted=True)
+    for b in range(2):
+        ref = OC.forward(o, OC.Ct(o.encrypt(ms[b], cfg.enc_seed, b), 2.0 ** 40), layers, "square", hoisted=True)
+        assert np.array_equal(u64(out.data)[b], ref.data)
+        y = OC.plain_forward(prob["x"][b], prob["W"], prob["b"], "square")
+        assert np.max(np.abs(OE.decode(o.decrypt(ref.data), o.primes, ref.scale, o.n)[:128] - y)) < 1e-3
 
 
 def test_rotation_batch_cfg3_sampled():

@@ -52,8 +52,8 @@ def test_ctx_sizes_host_side(L):
     assert L.lib().ckks_ctx_sizes(ctypes.byref(p), ctypes.byref(tb), ctypes.byref(kb), ctypes.byref(wb)) == 0
     n, Ld = 1 << 14, 8
     key = Ld * 2 * (Ld + 1) * n * 8
-    # s + pk + (relin + 2 Galois keys)
-    assert kb.value >= 3 * key and kb.value < 3 * key + 10 * 2 * Ld * n * 8
+    # s + pk + (relin + 2 Galois keys) + their sigma_{g^-1}-permuted copies (hoisted rotations)
+    assert kb.value >= 6 * key and kb.value < 6 * key + 10 * 2 * Ld * n * 8
     assert tb.value >= 9 * 4 * n * 8
     bad, keep2 = _params(L, log_n=15)
     assert L.lib().ckks_ctx_sizes(ctypes.byref(bad), ctypes.byref(tb), ctypes.byref(kb), ctypes.byref(wb)) == L.E_PARAM

@@ -24,10 +24,11 @@ def main():
     p.add_argument("--mode", default="forward", choices=["forward", "ntt", "ks"])
     p.add_argument("--batch", type=int, default=256)
     p.add_argument("--max-batch", type=int, default=256)
+    p.add_argument("--no-hoist", action="store_true")
     a = p.parse_args()
     dev = torch.device("cuda", 0)
     if a.mode == "forward":
-        ctx, model, ct, _ = bench.build_forward(G, S.CFG5, a.batch, a.max_batch, dev)
+        ctx, model, ct, _ = bench.build_forward(G, S.CFG5, a.batch, a.max_batch, dev, hoisted=not a.no_hoist)
         out = ctx.empty_ct(a.batch, model.final_level)
         work = torch.empty(model.work_bytes(a.batch), dtype=torch.uint8, device=dev)
         model.forward(ct, out, work)
