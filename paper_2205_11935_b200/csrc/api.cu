@@ -247,7 +247,7 @@ struct ckks_ctx {
         w.modup = p;
         p += (size_t)B * L * (L + 1) * n;
         w.acc = p;
-        p += (size_t)B * 2 * (L + 1) * n;
+        p += (size_t)KS_GMAX * B * 2 * (L + 1) * n;
         w.rem = p;
         return w;
     }
@@ -269,7 +269,11 @@ struct ckks_model {
 
 namespace {
 
-size_t ks_work_words(int L, int n, int B) { return (size_t)B * n * ((size_t)L + (size_t)L * (L + 1) + 2 * (L + 1) + 3); }
+// digits + modup + KS_GMAX x (ModDown outputs x + remainders)
+size_t ks_work_words(int L, int n, int B)
+{
+    return (size_t)B * n * ((size_t)L + (size_t)L * (L + 1) + (size_t)KS_GMAX * (2 * (L + 1) + 3));
+}
 size_t enc_work_words(int L, int n, int B) { return (size_t)B * n * (4 * (size_t)L + 1); }
 
 void check_ct(const ckks_ctx* c, const ckks_ct* x, int ncomp_expect = 2)
@@ -334,6 +338,14 @@ void rotate_hoisted_impl(ckks_ctx* c, const u64* in, size_t in_stride, int nl, i
         ck::KsIn ki{inb, in_stride, (size_t)nl * c->n, 0};
         auto w = c->ks_work(B);
         bool have_modup = false;
+        ck::KsGroup grp{};
+        grp.G = 0;
+        auto flush = [&]() {
+            if (!grp.G) return;
+            ck::KsOut ko{nullptr, out_stride, inb, in_stride, 0, 0, 0};
+            ck::keyswitch_finish(L, ki, grp, B, nl, w, ko);
+            grp.G = 0;
+        };
         for (int s = 0; s < n_steps; ++s) {
             const uint32_t g = c->galois(steps[s]);
             u64* ob = outs[s] + (size_t)b0 * out_stride;
@@ -346,9 +358,13 @@ void rotate_hoisted_impl(ckks_ctx* c, const u64* in, size_t in_stride, int nl, i
                 ck::keyswitch_modup(L, ki, B, nl, w);
                 have_modup = true;
             }
-            ck::KsOut ko{ob, out_stride, inb, in_stride, 0, 0, 0};
-            ck::keyswitch_finish(L, ki, c->key_perm((int64_t)g), B, nl, w, ko, c->galois_inv(g));
+            grp.key[grp.G] = c->key_perm((int64_t)g);
+            grp.out[grp.G] = ob;
+            grp.scatter[grp.G] = g;
+            grp.ginv[grp.G] = c->galois_inv(g);
+            if (++grp.G == KS_GMAX) flush();
         }
+        flush();
     }
 }
 

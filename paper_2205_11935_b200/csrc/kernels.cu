@@ -159,16 +159,18 @@ k_ks_modup(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* __r
 
 // (3) ModDown, special-prime row: r_c = iNTT_P( sum_j D_{j,P} key_j.c[P] )  -- the inner product for
 //     the special prime is computed in the (coalesced, staged) loader of the inverse NTT.
+//     grid (2, B, G): one CTA per (component, ciphertext, rotation of the group).
 template <int LOGN>
 __global__ void __launch_bounds__(NttThreads<LOGN>::value)
-k_ks_moddown_intt(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ key, int L,
-                  int nl, int special, u64* __restrict__ rem)
+k_ks_moddown_intt(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const KsGroup grp, int L, int nl,
+                  int special, u64* __restrict__ rem)
 {
     extern __shared__ u64 sm[];
     using T = NttCta<LOGN, NttThreads<LOGN>::value>;
-    const int c = blockIdx.x, b = blockIdx.y;
+    const int c = blockIdx.x, b = blockIdx.y, g = blockIdx.z, B = gridDim.y;
+    const u64* __restrict__ key = grp.key[g];
     const DPrime Pr = dc->p[special];
-    u64* dst = rem + ((size_t)b * 2 + c) * T::N;
+    u64* dst = rem + (((size_t)g * B + b) * 2 + c) * T::N;
     auto ld = [&](int k) {
         Acc128 a;
         a.zero();
@@ -181,63 +183,102 @@ k_ks_moddown_intt(const DCtx* __restrict__ dc, const u64* __restrict__ modup, co
     ntt_inverse<T>(sm, Pr, twp(dc, special), ld, st);
 }
 
-// (4) ModDown, data rows: x_c[i] = NTT_{q_i}(centered(r_c) mod q_i)   (written into acc[b][c][i])
+// (4) ModDown, data rows: x_g,c[i] = NTT_{q_i}(centered(r_g,c) mod q_i).  grid (nl, 2, B*G)
 template <int LOGN>
 __global__ void __launch_bounds__(NttThreads<LOGN>::value)
 k_ks_moddown_ntt(const DCtx* __restrict__ dc, const u64* __restrict__ rem, int nl, int special, u64* __restrict__ xo)
 {
     extern __shared__ u64 sm[];
     using T = NttCta<LOGN, NttThreads<LOGN>::value>;
-    const int i = blockIdx.x, c = blockIdx.y, b = blockIdx.z;
+    const int i = blockIdx.x, c = blockIdx.y, gb = blockIdx.z;   // gb = g * B + b
     const DPrime Pr = dc->p[i];
     const u64 Pmod = dc->qmod[special][i];
     const u64 Pbig = dc->p[special].q;
-    const u64* r = rem + ((size_t)b * 2 + c) * T::N;
-    u64* o = xo + (((size_t)b * 2 + c) * (nl + 1) + i) * T::N;
+    const u64* r = rem + ((size_t)gb * 2 + c) * T::N;
+    u64* o = xo + (((size_t)gb * 2 + c) * (nl + 1) + i) * T::N;
     auto ld = [&](int k) { return centered_to(r[k], Pbig, Pmod, Pr); };
     auto st = [&](int k, u64 v) { o[k] = v; };
     ntt_forward<T>(sm, Pr, twp(dc, i), ld, st);
 }
 
-// (5) inner product over the data primes fused with the ModDown combine and the output epilogue:
-//     out_c[i] = (sum_j D_{j,i} key_j.c[i] - x_c[i]) P^{-1}  (+ addend, + out)     D_{i,i} = input limb
-__global__ void __launch_bounds__(256)
-k_ks_ip_combine(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ in,
-                size_t ct_stride, size_t comp_off, u32 galois, const u64* __restrict__ key, int L, int nl, int special,
-                const u64* __restrict__ xo, u64* __restrict__ out, size_t out_stride, const u64* __restrict__ add,
-                size_t add_stride, u32 add_galois, int add_comp1, int accumulate, u32 scatter_g)
+// (5) inner product over the data primes + ModDown combine + output permutation, for every rotation
+//     g of the group, one CTA per (ciphertext, limb i, SOURCE block of 1024 NTT-domain indices):
+//       u_g,c[k] = sum_j D_{j,i}[k] key_g,j.c[i][k]            (D_{j,i}[k] loaded once for all g)
+//       y_g,c[k] = (u_g,c[k] - x_g,c[i][k]) P^{-1} + addend_c[k]
+//       out_g,c[i][k'] (+)= y_g,c[src_g(k')]                  (hoisted: out = sigma_g(y))
+//     sigma_g maps the block of indices sharing their top log2(N/1024) bits onto one block (those bits
+//     are the low bits of brev(k), on which sigma_g acts as an affine map), so the permutation is done
+//     through 16 KiB of shared memory and every global access is coalesced.
+#define IPO_BLK 1024
+template <int NL>
+__global__ void __launch_bounds__(IPO_BLK)
+k_ks_ip_out(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ in, size_t ct_stride,
+            size_t comp_off, u32 galois, const KsGroup grp, int L, int special, const u64* __restrict__ xo,
+            size_t out_stride, const u64* __restrict__ add, size_t add_stride, u32 add_galois, int add_comp1,
+            int accumulate, int B)
 {
+    __shared__ u64 ys[2][IPO_BLK];
+    constexpr int nl = NL;
     const int n = dc->n, logn = dc->log_n;
-    const int k = blockIdx.x * 256 + threadIdx.x, i = blockIdx.y, b = blockIdx.z;
+    // grid (B, nl, N/1024): the ciphertext index runs fastest so the key rows of (g, i, block) are
+    // read from DRAM once and then hit L2 for every ciphertext
+    const int b = blockIdx.x, i = blockIdx.y, blk = blockIdx.z;
+    const int t = threadIdx.x;
+    const int k = blk * IPO_BLK + t;   // source index
     const DPrime Pr = dc->p[i];
-    Acc128 a0, a1;
-    a0.zero();
-    a1.zero();
-    for (int j = 0; j < nl; ++j) {
-        u64 dv;
+    u64 dv[NL];
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
         if (j == i) {
             const u64* src = in + (size_t)b * ct_stride + comp_off + (size_t)j * n;
-            dv = galois ? src[galois_src(k, galois, logn)] : src[k];
+            dv[j] = galois ? src[galois_src(k, galois, logn)] : src[k];
         } else {
-            dv = modup[(((size_t)b * nl + j) * (nl + 1) + i) * n + k];
+            dv[j] = modup[(((size_t)b * nl + j) * (nl + 1) + i) * n + k];
         }
-        a0.mac(dv, key[(((size_t)j * 2 + 0) * (L + 1) + i) * n + k]);
-        a1.mac(dv, key[(((size_t)j * 2 + 1) * (L + 1) + i) * n + k]);
+    }
+    u64 ad[2] = {0, 0};
+    if (add) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+            if (c == 0 || add_comp1) {
+                const u64* a = add + (size_t)b * add_stride + ((size_t)c * nl + i) * n;
+                ad[c] = add_galois ? a[galois_src(k, add_galois, logn)] : a[k];
+            }
     }
     const u64 Pinv = dc->qinv[special][i], Pinv_sh = dc->qinv_sh[special][i];
-    const u64 u[2] = {a0.reduce(Pr), a1.reduce(Pr)};
+    for (int g = 0; g < grp.G; ++g) {
+        const u64* __restrict__ key = grp.key[g] + (size_t)i * n + k;
+        const size_t kstride = (size_t)(L + 1) * n;
+        Acc128 a0, a1;
+        a0.zero();
+        a1.zero();
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-        const u64 x = xo[(((size_t)b * 2 + c) * (nl + 1) + i) * n + k];
-        u64 v = csub(shoup_mul(u[c] + Pr.q - x, Pinv, Pinv_sh, Pr.q), Pr.q);
-        if (add && (c == 0 || add_comp1)) {
-            const u64* ad = add + (size_t)b * add_stride + ((size_t)c * nl + i) * n;
-            v = addmod(v, add_galois ? ad[galois_src(k, add_galois, logn)] : ad[k], Pr.q);
+        for (int j = 0; j < NL; ++j) {
+            a0.mac(dv[j], key[(size_t)(2 * j + 0) * kstride]);
+            a1.mac(dv[j], key[(size_t)(2 * j + 1) * kstride]);
         }
-        const int kd = scatter_g ? galois_src(k, scatter_g, logn) : k;
-        u64& o = out[(size_t)b * out_stride + ((size_t)c * nl + i) * n + kd];
-        if (accumulate) v = addmod(v, o, Pr.q);
-        o = v;
+        const u64 u[2] = {a0.reduce(Pr), a1.reduce(Pr)};
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const u64 x = xo[((((size_t)g * B + b) * 2 + c) * (nl + 1) + i) * n + k];
+            ys[c][t] = addmod(csub(shoup_mul(u[c] + Pr.q - x, Pinv, Pinv_sh, Pr.q), Pr.q), ad[c], Pr.q);
+        }
+        __syncthreads();
+        // destination block of this source block under sigma_g, and the source of each destination
+        const u32 gp = grp.scatter[g];
+        int dblk = blk, sidx = t;
+        if (gp) {
+            dblk = galois_src(blk * IPO_BLK, grp.ginv[g], logn) / IPO_BLK;
+            sidx = galois_src(dblk * IPO_BLK + t, gp, logn) - blk * IPO_BLK;
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            u64& o = grp.out[g][(size_t)b * out_stride + ((size_t)c * nl + i) * n + (size_t)dblk * IPO_BLK + t];
+            u64 v = ys[c][sidx];
+            if (accumulate) v = addmod(v, o, Pr.q);
+            o = v;
+        }
+        __syncthreads();
     }
 }
 
@@ -265,10 +306,30 @@ void keyswitch_modup(const Launch& L, const KsIn& in, int batch, int nl, const K
     if (L.counter) *L.counter += 2;
 }
 
-void keyswitch_finish(const Launch& L, const KsIn& in, const uint64_t* key, int batch, int nl, const KsWork& w,
-                      const KsOut& out, uint32_t scatter_g)
+static void launch_ks_ip_out(const Launch& L, const KsWork& w, const KsIn& in, const KsGroup& grp, int batch, int nl,
+                             const KsOut& out)
 {
-    if (batch <= 0) return;
+    const int n = 1 << L.log_n;
+    const dim3 grid(batch, nl, n / IPO_BLK);
+#define IP_CASE(V)                                                                                                   \
+    case V:                                                                                                           \
+        k_ks_ip_out<V><<<grid, IPO_BLK, 0, L.st>>>(L.dc, w.modup, in.base, in.ct_stride, in.comp_off, in.galois, grp,  \
+                                                   L.n_data, L.n_data, w.acc, out.ct_stride, out.add, out.add_stride, \
+                                                   out.add_galois, out.add_comp1, out.accumulate, batch);             \
+        break;
+    switch (nl) {
+        IP_CASE(1) IP_CASE(2) IP_CASE(3) IP_CASE(4) IP_CASE(5) IP_CASE(6) IP_CASE(7) IP_CASE(8)
+        IP_CASE(9) IP_CASE(10) IP_CASE(11) IP_CASE(12) IP_CASE(13) IP_CASE(14) IP_CASE(15) IP_CASE(16)
+    default: throw std::runtime_error("nl > 16");
+    }
+#undef IP_CASE
+}
+
+void keyswitch_finish(const Launch& L, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
+                      const KsOut& out)
+{
+    if (batch <= 0 || grp.G <= 0) return;
+    if (grp.G > KS_GMAX || nl > KS_LMAX) throw std::runtime_error("keyswitch_finish: group/limb limits");
     const int special = L.n_data;
     const size_t smem = sizeof(u64) << L.log_n;
     const int n = 1 << L.log_n;
@@ -276,12 +337,12 @@ void keyswitch_finish(const Launch& L, const KsIn& in, const uint64_t* key, int 
         constexpr int NT = NttThreads<LG>::value;
         allow_smem(k_ks_moddown_intt<LG>, smem);
         allow_smem(k_ks_moddown_ntt<LG>, smem);
-        k_ks_moddown_intt<LG><<<dim3(2, batch), NT, smem, L.st>>>(L.dc, w.modup, key, L.n_data, nl, special, w.rem);
-        k_ks_moddown_ntt<LG><<<dim3(nl, 2, batch), NT, smem, L.st>>>(L.dc, w.rem, nl, special, w.acc);
-        k_ks_ip_combine<<<dim3(n / 256, nl, batch), 256, 0, L.st>>>(
-            L.dc, w.modup, in.base, in.ct_stride, in.comp_off, in.galois, key, L.n_data, nl, special, w.acc, out.base,
-            out.ct_stride, out.add, out.add_stride, out.add_galois, out.add_comp1, out.accumulate, scatter_g);
+        k_ks_moddown_intt<LG><<<dim3(2, batch, grp.G), NT, smem, L.st>>>(L.dc, w.modup, grp, L.n_data, nl, special,
+                                                                         w.rem);
+        k_ks_moddown_ntt<LG><<<dim3(nl, 2, batch * grp.G), NT, smem, L.st>>>(L.dc, w.rem, nl, special, w.acc);
     });
+    if (n < IPO_BLK) throw std::runtime_error("N >= 1024 required");
+    launch_ks_ip_out(L, w, in, grp, batch, nl, out);
     check_launch("keyswitch_finish");
     if (L.counter) *L.counter += 3;
 }
@@ -296,7 +357,12 @@ void keyswitch(const Launch& L, const KsIn& in, const uint64_t* key, int batch, 
         L.probe->alg_bytes += (4.0 * batch * nl + 2.0 * nl * (nl + 1)) * (double)(8 << L.log_n);
     }
     keyswitch_modup(L, in, batch, nl, w);
-    keyswitch_finish(L, in, key, batch, nl, w, out, 0);
+    KsGroup grp{};
+    grp.key[0] = key;
+    grp.out[0] = out.base;
+    grp.scatter[0] = 0;
+    grp.G = 1;
+    keyswitch_finish(L, in, grp, batch, nl, w, out);
     if (pk) L.probe->mark(L.st);
 }
 

@@ -59,8 +59,18 @@ struct KsOut {
 struct KsWork {
     uint64_t* digits;         // [B][nl][N]
     uint64_t* modup;          // [B][nl][nl+1][N]
-    uint64_t* acc;            // [B][2][nl+1][N]
-    uint64_t* rem;            // [B][2][N]
+    uint64_t* acc;            // [G][B][2][nl+1][N]   (ModDown NTT outputs x, one block per rotation)
+    uint64_t* rem;            // [G][B][3][N]
+};
+#define KS_GMAX 8
+#define KS_LMAX 16
+// up to KS_GMAX key switches of the SAME ModUp output (hoisted rotations), finished together
+struct KsGroup {
+    const uint64_t* key[KS_GMAX];
+    uint64_t* out[KS_GMAX];
+    uint32_t scatter[KS_GMAX];   // 0, or g: write the result permuted by sigma_g (out[k] = y[src_g(k)])
+    uint32_t ginv[KS_GMAX];      // g^{-1} mod 2N (when scatter != 0)
+    int G;
 };
 void keyswitch(const Launch&, const KsIn& in, const uint64_t* key, int batch, int nl, const KsWork& w,
                const KsOut& out);
@@ -68,8 +78,8 @@ void keyswitch(const Launch&, const KsIn& in, const uint64_t* key, int batch, in
 // ModDown from w.modup.  scatter_g != 0 writes the result permuted by sigma_{g} where the caller
 // passes g^{-1} (hoisted rotation: out = sigma_g(c0 + ModDown(sum_j D_j key'_j))).
 void keyswitch_modup(const Launch&, const KsIn& in, int batch, int nl, const KsWork& w);
-void keyswitch_finish(const Launch&, const KsIn& in, const uint64_t* key, int batch, int nl, const KsWork& w,
-                      const KsOut& out, uint32_t scatter_g);
+void keyswitch_finish(const Launch&, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
+                      const KsOut& out);
 // out limbs[c][N] = in limbs[c][galois_src(k, g)] for `limbs` consecutive limbs (key pre-permutation)
 void galois_limbs(const Launch&, const uint64_t* in, uint64_t* out, size_t limbs, uint32_t g);
 
