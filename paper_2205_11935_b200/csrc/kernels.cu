@@ -527,18 +527,34 @@ __device__ __forceinline__ void bsgs_mac_body(const DCtx* __restrict__ dc, const
                     double acc[16];
 #pragma unroll
                     for (int z = 0; z < 16; ++z) acc[z] = 0.0;
-#pragma unroll 2
-                    for (int j = 0; j < t1; ++j) {
-                        const u64* v = (j == 0) ? v0 + (size_t)b * v0_stride : vb + ((size_t)(j - 1) * batch + b) * ctw;
-                        const double y = u2d(v[off]);
+                    // 8 baby-step words in flight per thread before they are consumed
+                    for (int j0 = 0; j0 < t1; j0 += 8) {
+                        double y[8];
 #pragma unroll
-                        for (int z = 0; z < 16; ++z) {
-                            if (z < nk) {
-                                const double w = __longlong_as_double((long long)A[((k0 + z) * t1 + j) * 16 + tx]);
-                                const double ph = y * w;
-                                const double pl = __fma_rn(y, w, -ph);
-                                const double kq = __fma_rn(ph, qinv, CK_RND_MAGIC) - CK_RND_MAGIC;
-                                acc[z] += __fma_rn(-kq, q, ph) + pl;
+                        for (int u = 0; u < 8; ++u) {
+                            const int j = j0 + u;
+                            y[u] = 0.0;
+                            if (j < t1) {
+                                const u64* v = (j == 0) ? v0 + (size_t)b * v0_stride
+                                                        : vb + ((size_t)(j - 1) * batch + b) * ctw;
+                                y[u] = u2d(v[off]);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int j = j0 + u;
+                            if (j < t1) {
+#pragma unroll
+                                for (int z = 0; z < 16; ++z) {
+                                    if (z < nk) {
+                                        const double w =
+                                            __longlong_as_double((long long)A[((k0 + z) * t1 + j) * 16 + tx]);
+                                        const double ph = y[u] * w;
+                                        const double pl = __fma_rn(y[u], w, -ph);
+                                        const double kq = __fma_rn(ph, qinv, CK_RND_MAGIC) - CK_RND_MAGIC;
+                                        acc[z] += __fma_rn(-kq, q, ph) + pl;
+                                    }
+                                }
                             }
                         }
                     }
