@@ -139,11 +139,11 @@ k_ks_digits(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t ct_s
 
 // (2) ModUp: D_{j,e} = NTT_{p_e}(d_j mod p_e) for e != j, e in [0, nl] (nl = special)
 template <int LOGN>
-__global__ void __launch_bounds__(NttThreads<LOGN>::value)
+__global__ void __launch_bounds__(NttThreadsWide<LOGN>::value)
 k_ks_modup(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* __restrict__ modup, int nl, int special)
 {
     extern __shared__ u64 sm[];
-    using T = NttCta<LOGN, NttThreads<LOGN>::value>;
+    using T = NttCta<LOGN, NttThreadsWide<LOGN>::value>;
     const int j = blockIdx.x / nl;
     int e = blockIdx.x % nl;
     if (e >= j) ++e;
@@ -299,7 +299,8 @@ void keyswitch_modup(const Launch& L, const KsIn& in, int batch, int nl, const K
             // digits read once, nl x nl ModUp limbs written
             L.probe->alg_bytes += ((double)batch * nl + (double)batch * nl * nl) * (double)(8 << L.log_n);
         }
-        k_ks_modup<LG><<<dim3(nl * nl, batch), NT, smem, L.st>>>(L.dc, w.digits, w.modup, nl, special);
+        k_ks_modup<LG><<<dim3(nl * nl, batch), NttThreadsWide<LG>::value, smem, L.st>>>(L.dc, w.digits, w.modup, nl,
+                                                                                        special);
         if (pm) L.probe->mark(L.st);
     });
     check_launch("keyswitch_modup");

@@ -78,14 +78,16 @@ struct NttCta {
     static constexpr int N = 1 << LOGN;
     static constexpr int E = N / NT;
     static constexpr int LOGE = ilog2c(E);
-    static constexpr int NPASS = (LOGN + LOGE - 1) / LOGE;
+    static constexpr int LOGK = 4;                          // stages per pass (radix 16), fixed:
+                                                            // the twiddle tables are ordered for it
+    static constexpr int NPASS = (LOGN + LOGK - 1) / LOGK;
     static_assert((1 << LOGE) == E, "E must be a power of two");
-    static_assert(LOGE >= 2 && LOGE <= 5, "2..5 stages per pass");
+    static_assert(LOGE >= LOGK && LOGE <= 5, "16 or 32 residues per thread");
 
     template <int P>
     struct Pass {
-        static constexpr int S0 = P * LOGE;
-        static constexpr int K = (LOGN - S0 < LOGE) ? (LOGN - S0) : LOGE;
+        static constexpr int S0 = P * LOGK;
+        static constexpr int K = (LOGN - S0 < LOGK) ? (LOGN - S0) : LOGK;
         static constexpr int G = E >> K;          // groups per thread
         static constexpr int SH = LOGN - S0 - K;  // log2(stride between group elements)
     };
@@ -434,16 +436,19 @@ __device__ __forceinline__ void ntt_inverse(u64* sm, const DPrime& Pr, const u64
     else T::template inverse<PC_BIG>(sm, Pr, tw, ld, st);
 }
 
-// Threads per CTA for each supported ring dimension (E = 32 for N >= 8192, 16 below).
-__host__ __device__ constexpr int ntt_loge(int logn) { return logn >= 13 ? 5 : 4; }
-template <int LOGN> struct NttThreads { static constexpr int value = 1 << (LOGN - ntt_loge(LOGN)); };
+// Threads per CTA: 16 residues per thread by default (more warps to hide the load latency of
+// prologue/epilogue-heavy kernels); NttThreadsWide = 32 residues per thread (more ILP, for the
+// compute-bound ModUp).  Passes are radix-16 in both cases (ntt_logk).
+__host__ __device__ constexpr int ntt_logk(int logn) { return (void)logn, 4; }
+template <int LOGN> struct NttThreads { static constexpr int value = 1 << (LOGN - 4); };
+template <int LOGN> struct NttThreadsWide { static constexpr int value = 1 << (LOGN - 5); };
 
 // Host: position of the forward/inverse twiddle of stage s, block m (= b0 2^r + j with
-// r = s - S0(s), S0(s) = floor(s / LOGE) LOGE) in the pass-ordered table:  2^s + j 2^S0 + b0.
+// r = s - S0(s), S0(s) = floor(s / LOGK) LOGK) in the pass-ordered table:  2^s + j 2^S0 + b0.
 inline int ntt_tw_position(int logn, int s, int m)
 {
-    const int loge = ntt_loge(logn);
-    const int S0 = (s / loge) * loge, r = s - S0;
+    const int logk = ntt_logk(logn);
+    const int S0 = (s / logk) * logk, r = s - S0;
     const int b0 = m >> r, j = m & ((1 << r) - 1);
     return (1 << s) + (j << S0) + b0;
 }

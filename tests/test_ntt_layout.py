@@ -7,13 +7,14 @@ import pytest
 
 
 def ntt_threads(logn):
-    return (1 << (logn - 5)) if logn >= 13 else (1 << (logn - 4))
+    return 1 << (logn - 4)        # default 16 residues per thread (ntt.cuh NttThreads)
 
 
 def passes(logn, loge):
+    """radix-16 passes (ntt.cuh LOGK = 4) regardless of the residues per thread"""
     out, s0 = [], 0
     while s0 < logn:
-        k = min(loge, logn - s0)
+        k = min(4, logn - s0)
         out.append((s0, k))
         s0 += k
     return out
@@ -36,9 +37,10 @@ def wavefronts(addrs):
     return tot
 
 
+@pytest.mark.parametrize("per_thread", [16, 32])
 @pytest.mark.parametrize("logn", [10, 11, 12, 13, 14])
-def test_ntt_layout(logn):
-    nt = ntt_threads(logn)
+def test_ntt_layout(logn, per_thread):
+    nt = (1 << logn) // per_thread
     E = (1 << logn) // nt
     loge = E.bit_length() - 1
     swz = lambda a: a ^ (((a >> 4) ^ (a >> 5)) & 15)
@@ -61,8 +63,8 @@ def test_ntt_layout(logn):
 
 
 def tw_position(logn, s, m):
-    loge = 5 if logn >= 13 else 4
-    S0 = (s // loge) * loge
+    logk = 4
+    S0 = (s // logk) * logk
     r = s - S0
     return (1 << s) + ((m & ((1 << r) - 1)) << S0) + (m >> r)
 
