@@ -202,14 +202,14 @@ k_ks_moddown_ntt(const DCtx* __restrict__ dc, const u64* __restrict__ rem, int n
 }
 
 // (5) inner product over the data primes + ModDown combine + output permutation, for every rotation
-//     g of the group, one CTA per (ciphertext, limb i, SOURCE block of 1024 NTT-domain indices):
+//     g of the group, one CTA per (ciphertext, limb i, SOURCE block of IPO_BLK NTT-domain indices):
 //       u_g,c[k] = sum_j D_{j,i}[k] key_g,j.c[i][k]            (D_{j,i}[k] loaded once for all g)
 //       y_g,c[k] = (u_g,c[k] - x_g,c[i][k]) P^{-1} + addend_c[k]
 //       out_g,c[i][k'] (+)= y_g,c[src_g(k')]                  (hoisted: out = sigma_g(y))
-//     sigma_g maps the block of indices sharing their top log2(N/1024) bits onto one block (those bits
-//     are the low bits of brev(k), on which sigma_g acts as an affine map), so the permutation is done
-//     through 16 KiB of shared memory and every global access is coalesced.
-#define IPO_BLK 1024
+//     sigma_g maps the block of indices sharing their top log2(N/IPO_BLK) bits onto one block (those bits
+//     are the low bits of brev(k), on which sigma_g acts as an affine map) so the permutation is done
+//     through 2 x IPO_BLK words of shared memory and every global access is coalesced.
+#define IPO_BLK 256
 template <int NL>
 __global__ void __launch_bounds__(IPO_BLK)
 k_ks_ip_out(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ in, size_t ct_stride,
