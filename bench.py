@@ -188,7 +188,7 @@ def run_ours(args):
         model.forward(ct, out, work)
     torch.cuda.synchronize()
 
-    ctx.probe(G.PROBE_MODUP)
+    ctx.probe(G.PROBE_ALL)
     clocks = Clocks(local)
     clocks.start()
     l0 = ctx.launches()
@@ -204,8 +204,14 @@ def run_ours(args):
     ms_local = e0.elapsed_time(e1)
     launches = ctx.launches() - l0
     clk = clocks.stop()
-    mod_ms, mod_n, mod_bytes = ctx.probe_read()
+    per_kernel = ctx.probe_read_all()
     ctx.probe(G.PROBE_OFF)
+    mod = per_kernel.get("k_ks_modup", {"ms": 0.0, "launches": 0, "alg_bytes": 0.0})
+    mod_ms, mod_n, mod_bytes = mod["ms"], mod["launches"], mod["alg_bytes"]
+    probed_ms = sum(v["ms"] for v in per_kernel.values())
+    kernel_shares = {k: {"share": round(v["ms"] / probed_ms, 4), "ms_per_step": round(v["ms"] / args.steps, 3),
+                         "launches_per_step": v["launches"] // args.steps}
+                     for k, v in sorted(per_kernel.items(), key=lambda kv: -kv[1]["ms"])}
     ms = max_over_ranks(ms_local, device)
     value = B * world * args.steps / (ms / 1e3)
 
@@ -227,7 +233,8 @@ def run_ours(args):
                          "baby_steps": "non-hoisted (R11)" if args.no_hoist else "hoisted (NEXT f-1, R11b)",
                          "l2": "inputs (2 GiB of ciphertexts) larger than L2; no flush",
                          "parallelism": f"replicas x{world}"},
-              "gpu_launches": launches, "roofline": roofline}
+              "gpu_launches": launches, "roofline": roofline,
+              "kernel_shares": kernel_shares}
     if clk:
         result["clocks"] = clk
 

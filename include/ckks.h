@@ -98,6 +98,9 @@ uint64_t ckks_launch_count(const ckks_ctx* ctx);
  * as defined in DESIGN.md section 7.  Costs two event records per probed launch; off by default. */
 ckks_status ckks_probe_enable(ckks_ctx* ctx, int32_t kind);
 ckks_status ckks_probe_read(ckks_ctx* ctx, double* total_ms, uint64_t* launches, double* alg_bytes);
+/* kind 4 = every hot-path kernel launch (tagged by kernel name).  Writes a JSON object
+ * {"<kernel>": {"ms": total, "launches": n, "alg_bytes": b}, ...} into json (capacity cap). */
+ckks_status ckks_probe_read_all(ckks_ctx* ctx, char* json, size_t cap);
 
 /* ---- ring: batched negacyclic NTT ---------------------------------------- */
 /* In place over d = device [batch][limbs][N]; limb i is reduced modulo prime i.  Forward maps

@@ -86,11 +86,12 @@ SIGNATURES = {
     "ckks_galois_elt": (_U64, [_VP, _I]),
     "ckks_probe_enable": (_I, [_VP, _I]),
     "ckks_probe_read": (_I, [_VP, ctypes.POINTER(_D), ctypes.POINTER(_U64), ctypes.POINTER(_D)]),
+    "ckks_probe_read_all": (_I, [_VP, ctypes.c_char_p, _SZ]),
     "ckks_bsgs_plan": (_I, [_U32, _U32, ctypes.POINTER(_U32), ctypes.POINTER(_U32), ctypes.POINTER(_U32)]),
     "ckks_model_plan": (_I, [_VP, _U32, ctypes.POINTER(_U32), ctypes.POINTER(_U32), _I, _U32, _D,
                              ctypes.POINTER(_U32), ctypes.POINTER(_D), ctypes.POINTER(_I), ctypes.POINTER(_U32)]),
 }
-PROBE_OFF, PROBE_MODUP, PROBE_KEYSWITCH, PROBE_NTT = 0, 1, 2, 3
+PROBE_OFF, PROBE_MODUP, PROBE_KEYSWITCH, PROBE_NTT, PROBE_ALL = 0, 1, 2, 3, 4
 
 
 def lib_path() -> str:
@@ -209,6 +210,12 @@ class Context:
         ms, n, b = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_double()
         _check(lib().ckks_probe_read(self.h, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(b)), "ckks_probe_read")
         return ms.value, n.value, b.value
+
+    def probe_read_all(self):
+        import json
+        buf = ctypes.create_string_buffer(1 << 16)
+        _check(lib().ckks_probe_read_all(self.h, buf, len(buf)), "ckks_probe_read_all")
+        return json.loads(buf.value.decode())
 
     def model_plan(self, shapes, activation, in_level, in_scale):
         """-> ([layer input level], [layer input scale], [rotation steps]) from the library's planner."""

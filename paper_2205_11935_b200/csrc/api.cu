@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -618,15 +619,48 @@ void ckks_ctx_destroy(ckks_ctx* ctx)
 ckks_status ckks_probe_enable(ckks_ctx* c, int32_t kind)
 {
     CK_TRY({
-        if (!c || kind < 0 || kind > 3) throw CkksError(CKKS_E_PARAM, "probe kind 0..3");
+        if (!c || kind < 0 || kind > 4) throw CkksError(CKKS_E_PARAM, "probe kind 0..4");
         c->probe.kind = kind;
         c->probe.used = 0;
         c->probe.alg_bytes = 0;
+        c->probe.names.clear();
+        c->probe.bytes_by_kernel.clear();
         while (kind && c->probe.ev.size() < 4096) {
             cudaEvent_t e;
             cuda_ok(cudaEventCreate(&e), "event");
             c->probe.ev.push_back(e);
         }
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_probe_read_all(ckks_ctx* c, char* json, size_t cap)
+{
+    CK_TRY({
+        if (!c || !json || cap == 0) throw CkksError(CKKS_E_PARAM, "null");
+        const size_t pairs = c->probe.used / 2;
+        if (pairs) cuda_ok(cudaEventSynchronize(c->probe.ev[2 * pairs - 1]), "probe sync");
+        std::map<std::string, std::pair<double, uint64_t>> per;
+        for (size_t i = 0; i < pairs && i < c->probe.names.size(); ++i) {
+            float ms = 0;
+            cuda_ok(cudaEventElapsedTime(&ms, c->probe.ev[2 * i], c->probe.ev[2 * i + 1]), "elapsed");
+            auto& e = per[c->probe.names[i]];
+            e.first += ms;
+            e.second += 1;
+        }
+        std::string s = "{";
+        for (auto& kv : per) {
+            if (s.size() > 1) s += ", ";
+            char buf[256];
+            const auto it = c->probe.bytes_by_kernel.find(kv.first);
+            std::snprintf(buf, sizeof(buf), "\"%s\": {\"ms\": %.6f, \"launches\": %llu, \"alg_bytes\": %.1f}",
+                          kv.first.c_str(), kv.second.first, (unsigned long long)kv.second.second,
+                          it == c->probe.bytes_by_kernel.end() ? 0.0 : it->second);
+            s += buf;
+        }
+        s += "}";
+        if (s.size() + 1 > cap) throw CkksError(CKKS_E_SIZE, "json buffer too small");
+        std::memcpy(json, s.c_str(), s.size() + 1);
         return CKKS_OK;
     })
 }

@@ -108,11 +108,13 @@ void ntt_batch(const Launch& L, uint64_t* data, int batch, int limbs, int prime0
         auto k = inverse ? k_ntt_batch<LG, true> : k_ntt_batch<LG, false>;
         allow_smem(k, smem);
         const bool pr = L.probe && L.probe->on(PROBE_NTT);
+        if (L.probe && L.probe->on(PROBE_ALL))
+            L.probe->bytes_by_kernel["k_ntt_batch"] += 2.0 * batch * limbs * (double)(8 << L.log_n);
         if (pr) {
             L.probe->mark(L.st);
             L.probe->alg_bytes += 2.0 * batch * limbs * (double)(8 << L.log_n);   // read + write each limb once
         }
-        k<<<dim3(limbs, batch), NT, smem, L.st>>>(L.dc, data, limbs, prime0);
+        { ProbeScope ps_(L.probe, L.st, "k_ntt_batch"); k<<<dim3(limbs, batch), NT, smem, L.st>>>(L.dc, data, limbs, prime0); }
         if (pr) L.probe->mark(L.st);
     });
     check_launch("ntt_batch");
@@ -292,15 +294,18 @@ void keyswitch_modup(const Launch& L, const KsIn& in, int batch, int nl, const K
         allow_smem(k_ks_digits<LG>, smem);
         allow_smem(k_ks_modup<LG>, smem);
         const bool pm = L.probe && L.probe->on(PROBE_MODUP);
-        k_ks_digits<LG><<<dim3(nl, batch), NT, smem, L.st>>>(L.dc, in.base, in.ct_stride, in.comp_off, in.galois,
-                                                              w.digits, nl);
+        if (L.probe && L.probe->on(PROBE_ALL))
+            L.probe->bytes_by_kernel["k_ks_modup"] +=
+                ((double)batch * nl + (double)batch * nl * nl) * (double)(8 << L.log_n);
+        { ProbeScope ps_(L.probe, L.st, "k_ks_digits"); k_ks_digits<LG><<<dim3(nl, batch), NT, smem, L.st>>>(L.dc, in.base, in.ct_stride, in.comp_off, in.galois,
+                                                              w.digits, nl); }
         if (pm) {
             L.probe->mark(L.st);
             // digits read once, nl x nl ModUp limbs written
             L.probe->alg_bytes += ((double)batch * nl + (double)batch * nl * nl) * (double)(8 << L.log_n);
         }
-        k_ks_modup<LG><<<dim3(nl * nl, batch), NttThreadsWide<LG>::value, smem, L.st>>>(L.dc, w.digits, w.modup, nl,
-                                                                                        special);
+        { ProbeScope ps_(L.probe, L.st, "k_ks_modup"); k_ks_modup<LG><<<dim3(nl * nl, batch), NttThreadsWide<LG>::value, smem, L.st>>>(L.dc, w.digits, w.modup, nl,
+                                                                                        special); }
         if (pm) L.probe->mark(L.st);
     });
     check_launch("keyswitch_modup");
@@ -314,9 +319,9 @@ static void launch_ks_ip_out(const Launch& L, const KsWork& w, const KsIn& in, c
     const dim3 grid(batch, nl, n / IPO_BLK);
 #define IP_CASE(V)                                                                                                   \
     case V:                                                                                                           \
-        k_ks_ip_out<V><<<grid, IPO_BLK, 0, L.st>>>(L.dc, w.modup, in.base, in.ct_stride, in.comp_off, in.galois, grp,  \
+        { ProbeScope ps_(L.probe, L.st, "k_ks_ip_out"); k_ks_ip_out<V><<<grid, IPO_BLK, 0, L.st>>>(L.dc, w.modup, in.base, in.ct_stride, in.comp_off, in.galois, grp,  \
                                                    L.n_data, L.n_data, w.acc, out.ct_stride, out.add, out.add_stride, \
-                                                   out.add_galois, out.add_comp1, out.accumulate, batch);             \
+                                                   out.add_galois, out.add_comp1, out.accumulate, batch); }             \
         break;
     switch (nl) {
         IP_CASE(1) IP_CASE(2) IP_CASE(3) IP_CASE(4) IP_CASE(5) IP_CASE(6) IP_CASE(7) IP_CASE(8)
@@ -338,9 +343,9 @@ void keyswitch_finish(const Launch& L, const KsIn& in, const KsGroup& grp, int b
         constexpr int NT = NttThreads<LG>::value;
         allow_smem(k_ks_moddown_intt<LG>, smem);
         allow_smem(k_ks_moddown_ntt<LG>, smem);
-        k_ks_moddown_intt<LG><<<dim3(2, batch, grp.G), NT, smem, L.st>>>(L.dc, w.modup, grp, L.n_data, nl, special,
-                                                                         w.rem);
-        k_ks_moddown_ntt<LG><<<dim3(nl, 2, batch * grp.G), NT, smem, L.st>>>(L.dc, w.rem, nl, special, w.acc);
+        { ProbeScope ps_(L.probe, L.st, "k_ks_moddown_intt"); k_ks_moddown_intt<LG><<<dim3(2, batch, grp.G), NT, smem, L.st>>>(L.dc, w.modup, grp, L.n_data, nl, special,
+                                                                         w.rem); }
+        { ProbeScope ps_(L.probe, L.st, "k_ks_moddown_ntt"); k_ks_moddown_ntt<LG><<<dim3(nl, 2, batch * grp.G), NT, smem, L.st>>>(L.dc, w.rem, nl, special, w.acc); }
     });
     if (n < IPO_BLK) throw std::runtime_error("N >= 1024 required");
     launch_ks_ip_out(L, w, in, grp, batch, nl, out);
@@ -437,9 +442,9 @@ void rescale(const Launch& L, const uint64_t* in, size_t in_stride, uint64_t* ou
         constexpr int NT = NttThreads<LG>::value;
         allow_smem(k_rescale_intt<LG>, smem);
         allow_smem(k_rescale_out<LG>, smem);
-        k_rescale_intt<LG><<<dim3(ncomp, batch), NT, smem, L.st>>>(L.dc, in, in_stride, ncomp, nl, rem);
-        k_rescale_out<LG><<<dim3(nl - 1, ncomp, batch), NT, smem, L.st>>>(L.dc, in, in_stride, ncomp, nl, rem, out,
-                                                                         out_stride, bias);
+        { ProbeScope ps_(L.probe, L.st, "k_rescale_intt"); k_rescale_intt<LG><<<dim3(ncomp, batch), NT, smem, L.st>>>(L.dc, in, in_stride, ncomp, nl, rem); }
+        { ProbeScope ps_(L.probe, L.st, "k_rescale_out"); k_rescale_out<LG><<<dim3(nl - 1, ncomp, batch), NT, smem, L.st>>>(L.dc, in, in_stride, ncomp, nl, rem, out,
+                                                                         out_stride, bias); }
     });
     check_launch("rescale");
     if (L.counter) *L.counter += 2;
@@ -472,7 +477,7 @@ void tensor(const Launch& L, const uint64_t* a, const uint64_t* b, size_t stride
 {
     if (batch <= 0) return;
     const int n = 1 << L.log_n;
-    k_tensor<<<dim3(n / 256, nl, batch), 256, 0, L.st>>>(L.dc, a, b, stride, out3, out_stride, nl);
+    { ProbeScope ps_(L.probe, L.st, "k_tensor"); k_tensor<<<dim3(n / 256, nl, batch), 256, 0, L.st>>>(L.dc, a, b, stride, out3, out_stride, nl); }
     check_launch("tensor");
     if (L.counter) ++*L.counter;
 }
@@ -494,7 +499,7 @@ void add(const Launch& L, const uint64_t* a, size_t sa, const uint64_t* b, size_
 {
     if (batch <= 0) return;
     const int n = 1 << L.log_n;
-    k_add<<<dim3(n / 256, ncomp * nl, batch), 256, 0, L.st>>>(L.dc, a, sa, b, sb, out, so, nl);
+    { ProbeScope ps_(L.probe, L.st, "k_add"); k_add<<<dim3(n / 256, ncomp * nl, batch), 256, 0, L.st>>>(L.dc, a, sa, b, sb, out, so, nl); }
     check_launch("add");
     if (L.counter) ++*L.counter;
 }
@@ -610,7 +615,7 @@ void bsgs_mac(const Launch& L, const uint64_t* pts, const uint64_t* v0, size_t v
     const size_t smem = (size_t)t1 * t2 * 16 * 8;
     if (smem > 200 * 1024) throw std::runtime_error("bsgs_mac: plaintext tile too large (t <= 1600)");
     allow_smem(k_bsgs_mac, smem);
-    k_bsgs_mac<<<dim3(n / 16, nl), 256, smem, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl);
+    { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac"); k_bsgs_mac<<<dim3(n / 16, nl), 256, smem, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl); }
     check_launch("bsgs_mac");
     if (L.counter) ++*L.counter;
 }

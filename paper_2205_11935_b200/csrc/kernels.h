@@ -3,6 +3,8 @@
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <map>
+#include <string>
 #include <vector>
 
 struct DCtx;
@@ -10,12 +12,14 @@ struct DCtx;
 namespace ck {
 
 // CUDA-event probe around every launch of one kernel class (bench roofline, measured live).
-enum ProbeKind { PROBE_OFF = 0, PROBE_MODUP = 1, PROBE_KEYSWITCH = 2, PROBE_NTT = 3 };
+enum ProbeKind { PROBE_OFF = 0, PROBE_MODUP = 1, PROBE_KEYSWITCH = 2, PROBE_NTT = 3, PROBE_ALL = 4 };
 struct Probe {
     int kind = PROBE_OFF;
     std::vector<cudaEvent_t> ev;
+    std::vector<const char*> names;   // PROBE_ALL: kernel name of each event pair
     size_t used = 0;
     double alg_bytes = 0;   // algorithmic bytes of the probed launches
+    std::map<std::string, double> bytes_by_kernel;   // PROBE_ALL: algorithmic bytes per kernel name
     void mark(cudaStream_t s)
     {
         if (used == ev.size()) {
@@ -26,6 +30,24 @@ struct Probe {
         cudaEventRecord(ev[used++], s);
     }
     bool on(int k) const { return kind == k; }
+};
+
+struct Launch;
+// PROBE_ALL: event pair around one launch site, tagged with the kernel name
+struct ProbeScope {
+    Probe* p;
+    cudaStream_t st;
+    ProbeScope(Probe* probe, cudaStream_t s, const char* name) : p(probe && probe->kind == PROBE_ALL ? probe : nullptr), st(s)
+    {
+        if (p) {
+            p->names.push_back(name);
+            p->mark(st);
+        }
+    }
+    ~ProbeScope()
+    {
+        if (p) p->mark(st);
+    }
 };
 
 struct Launch {
