@@ -66,6 +66,15 @@ def barrier():
         dist.barrier()
 
 
+def replica_throughput(units_per_rank, local_ms, device):
+    """Replicas: every rank processes its own batch; the job time is the max
+    over ranks and the value is all units processed / that time.  Returns (value_per_s, max_ms)."""
+    import torch.distributed as dist
+    world = dist.get_world_size() if (dist.is_available() and dist.is_initialized()) else 1
+    ms = max_over_ranks(local_ms, device)
+    return units_per_rank * world / (ms / 1e3), ms
+
+
 def max_over_ranks(x, device):
     import torch
     import torch.distributed as dist
@@ -212,8 +221,7 @@ def run_ours(args):
     kernel_shares = {k: {"share": round(v["ms"] / probed_ms, 4), "ms_per_step": round(v["ms"] / args.steps, 3),
                          "launches_per_step": v["launches"] // args.steps}
                      for k, v in sorted(per_kernel.items(), key=lambda kv: -kv[1]["ms"])}
-    ms = max_over_ranks(ms_local, device)
-    value = B * world * args.steps / (ms / 1e3)
+    value, ms = replica_throughput(B * args.steps, ms_local, device)
 
     peak, peak_src = measured_peaks()
     achieved = mod_bytes / (mod_ms / 1e3) / 1e9 if mod_ms > 0 else 0.0
