@@ -11,6 +11,7 @@
 #include "kernels.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -39,6 +40,18 @@ static void allow_smem(K kernel, size_t bytes)
     if (bytes > 48 * 1024) {
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     }
+}
+
+// Threads per CTA of the key-switch NTT kernels: bit set = 32 residues per thread (N/32 threads),
+// clear = 16 (N/16 threads).  bits: 1 digits, 2 ModUp, 4 ModDown iNTT, 8 ModDown NTT.  Default 2;
+// CKKS_NTT_WIDE overrides it (tuning experiments only).
+static int ntt_wide_mask()
+{
+    static int mask = [] {
+        const char* e = getenv("CKKS_NTT_WIDE");
+        return e ? atoi(e) : 2;
+    }();
+    return mask;
 }
 
 #define NTT_DISPATCH(LOGN_VAR, ...)                                                     \
@@ -123,13 +136,13 @@ void ntt_batch(const Launch& L, uint64_t* data, int batch, int limbs, int prime0
 
 // ------------------------------------------------------------------------------------ key switch
 // (1) digits: d_j = iNTT_{q_j}(sigma_g(d)[j])  -> [B][nl][N] in [0, q_j)                  (R9)
-template <int LOGN>
-__global__ void __launch_bounds__(NttThreads<LOGN>::value)
+template <int LOGN, int NTH>
+__global__ void __launch_bounds__(NTH)
 k_ks_digits(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t ct_stride, size_t comp_off,
             u32 galois, u64* __restrict__ digits, int nl)
 {
     extern __shared__ u64 sm[];
-    using T = NttCta<LOGN, NttThreads<LOGN>::value>;
+    using T = NttCta<LOGN, NTH>;
     const int j = blockIdx.x, b = blockIdx.y;
     const u64* src = in + (size_t)b * ct_stride + comp_off + (size_t)j * T::N;
     u64* dst = digits + ((size_t)b * nl + j) * T::N;
@@ -140,12 +153,12 @@ k_ks_digits(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t ct_s
 }
 
 // (2) ModUp: D_{j,e} = NTT_{p_e}(d_j mod p_e) for e != j, e in [0, nl] (nl = special)
-template <int LOGN>
-__global__ void __launch_bounds__(NttThreadsWide<LOGN>::value)
+template <int LOGN, int NTH>
+__global__ void __launch_bounds__(NTH)
 k_ks_modup(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* __restrict__ modup, int nl, int special)
 {
     extern __shared__ u64 sm[];
-    using T = NttCta<LOGN, NttThreadsWide<LOGN>::value>;
+    using T = NttCta<LOGN, NTH>;
     const int j = blockIdx.x / nl;
     int e = blockIdx.x % nl;
     if (e >= j) ++e;
@@ -162,13 +175,13 @@ k_ks_modup(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* __r
 // (3) ModDown, special-prime row: r_c = iNTT_P( sum_j D_{j,P} key_j.c[P] )  -- the inner product for
 //     the special prime is computed in the (coalesced, staged) loader of the inverse NTT.
 //     grid (2, B, G): one CTA per (component, ciphertext, rotation of the group).
-template <int LOGN>
-__global__ void __launch_bounds__(NttThreads<LOGN>::value)
+template <int LOGN, int NTH>
+__global__ void __launch_bounds__(NTH)
 k_ks_moddown_intt(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const KsGroup grp, int L, int nl,
                   int special, u64* __restrict__ rem)
 {
     extern __shared__ u64 sm[];
-    using T = NttCta<LOGN, NttThreads<LOGN>::value>;
+    using T = NttCta<LOGN, NTH>;
     const int c = blockIdx.x, b = blockIdx.y, g = blockIdx.z, B = gridDim.y;
     const u64* __restrict__ key = grp.key[g];
     const DPrime Pr = dc->p[special];
@@ -186,12 +199,12 @@ k_ks_moddown_intt(const DCtx* __restrict__ dc, const u64* __restrict__ modup, co
 }
 
 // (4) ModDown, data rows: x_g,c[i] = NTT_{q_i}(centered(r_g,c) mod q_i).  grid (nl, 2, B*G)
-template <int LOGN>
-__global__ void __launch_bounds__(NttThreads<LOGN>::value)
+template <int LOGN, int NTH>
+__global__ void __launch_bounds__(NTH)
 k_ks_moddown_ntt(const DCtx* __restrict__ dc, const u64* __restrict__ rem, int nl, int special, u64* __restrict__ xo)
 {
     extern __shared__ u64 sm[];
-    using T = NttCta<LOGN, NttThreads<LOGN>::value>;
+    using T = NttCta<LOGN, NTH>;
     const int i = blockIdx.x, c = blockIdx.y, gb = blockIdx.z;   // gb = g * B + b
     const DPrime Pr = dc->p[i];
     const u64 Pmod = dc->qmod[special][i];
@@ -291,20 +304,24 @@ void keyswitch_modup(const Launch& L, const KsIn& in, int batch, int nl, const K
     const size_t smem = sizeof(u64) << L.log_n;
     NTT_DISPATCH(L.log_n, {
         constexpr int NT = NttThreads<LG>::value;
-        allow_smem(k_ks_digits<LG>, smem);
-        allow_smem(k_ks_modup<LG>, smem);
+        constexpr int NW = NttThreadsWide<LG>::value;
+        const int wm = ntt_wide_mask();
+        auto kd = (wm & 1) ? k_ks_digits<LG, NW> : k_ks_digits<LG, NT>;
+        auto km = (wm & 2) ? k_ks_modup<LG, NW> : k_ks_modup<LG, NT>;
+        allow_smem(kd, smem);
+        allow_smem(km, smem);
         const bool pm = L.probe && L.probe->on(PROBE_MODUP);
         if (L.probe && L.probe->on(PROBE_ALL))
             L.probe->bytes_by_kernel["k_ks_modup"] +=
                 ((double)batch * nl + (double)batch * nl * nl) * (double)(8 << L.log_n);
-        { ProbeScope ps_(L.probe, L.st, "k_ks_digits"); k_ks_digits<LG><<<dim3(nl, batch), NT, smem, L.st>>>(L.dc, in.base, in.ct_stride, in.comp_off, in.galois,
+        { ProbeScope ps_(L.probe, L.st, "k_ks_digits"); kd<<<dim3(nl, batch), (wm & 1) ? NW : NT, smem, L.st>>>(L.dc, in.base, in.ct_stride, in.comp_off, in.galois,
                                                               w.digits, nl); }
         if (pm) {
             L.probe->mark(L.st);
             // digits read once, nl x nl ModUp limbs written
             L.probe->alg_bytes += ((double)batch * nl + (double)batch * nl * nl) * (double)(8 << L.log_n);
         }
-        { ProbeScope ps_(L.probe, L.st, "k_ks_modup"); k_ks_modup<LG><<<dim3(nl * nl, batch), NttThreadsWide<LG>::value, smem, L.st>>>(L.dc, w.digits, w.modup, nl,
+        { ProbeScope ps_(L.probe, L.st, "k_ks_modup"); km<<<dim3(nl * nl, batch), (wm & 2) ? NW : NT, smem, L.st>>>(L.dc, w.digits, w.modup, nl,
                                                                                         special); }
         if (pm) L.probe->mark(L.st);
     });
@@ -341,11 +358,15 @@ void keyswitch_finish(const Launch& L, const KsIn& in, const KsGroup& grp, int b
     const int n = 1 << L.log_n;
     NTT_DISPATCH(L.log_n, {
         constexpr int NT = NttThreads<LG>::value;
-        allow_smem(k_ks_moddown_intt<LG>, smem);
-        allow_smem(k_ks_moddown_ntt<LG>, smem);
-        { ProbeScope ps_(L.probe, L.st, "k_ks_moddown_intt"); k_ks_moddown_intt<LG><<<dim3(2, batch, grp.G), NT, smem, L.st>>>(L.dc, w.modup, grp, L.n_data, nl, special,
+        constexpr int NW = NttThreadsWide<LG>::value;
+        const int wm = ntt_wide_mask();
+        auto ki = (wm & 4) ? k_ks_moddown_intt<LG, NW> : k_ks_moddown_intt<LG, NT>;
+        auto kn = (wm & 8) ? k_ks_moddown_ntt<LG, NW> : k_ks_moddown_ntt<LG, NT>;
+        allow_smem(ki, smem);
+        allow_smem(kn, smem);
+        { ProbeScope ps_(L.probe, L.st, "k_ks_moddown_intt"); ki<<<dim3(2, batch, grp.G), (wm & 4) ? NW : NT, smem, L.st>>>(L.dc, w.modup, grp, L.n_data, nl, special,
                                                                          w.rem); }
-        { ProbeScope ps_(L.probe, L.st, "k_ks_moddown_ntt"); k_ks_moddown_ntt<LG><<<dim3(nl, 2, batch * grp.G), NT, smem, L.st>>>(L.dc, w.rem, nl, special, w.acc); }
+        { ProbeScope ps_(L.probe, L.st, "k_ks_moddown_ntt"); kn<<<dim3(nl, 2, batch * grp.G), (wm & 8) ? NW : NT, smem, L.st>>>(L.dc, w.rem, nl, special, w.acc); }
     });
     if (n < IPO_BLK) throw std::runtime_error("N >= 1024 required");
     launch_ks_ip_out(L, w, in, grp, batch, nl, out);
