@@ -619,6 +619,7 @@ k_bsgs_mac(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u64* 
     const int x0 = blockIdx.x * 16, x = x0 + tx, l = blockIdx.y;
     const int t = t1 * t2;
     const bool fp = prime_class(dc->p[l].q) == PC_FP;
+    if (fp) return;   // FP-class limbs are handled by k_bsgs_mac_fp
     for (int i = threadIdx.x; i < t * 16; i += blockDim.x) {
         const u64 a = pts[((size_t)(i >> 4) * nl + l) * n + x0 + (i & 15)];
         A[i] = fp ? (u64)__double_as_longlong(u2d(a)) : a;
@@ -626,6 +627,88 @@ k_bsgs_mac(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u64* 
     __syncthreads();
     if (fp) bsgs_mac_body<true>(dc, A, v0, v0_stride, vb, wout, t1, t2, batch, nl, l, x, tx, ty);
     else bsgs_mac_body<false>(dc, A, v0, v0_stride, vb, wout, t1, t2, batch, nl, l, x, tx, ty);
+}
+
+// FP-class limbs (q < 2^45): split-operand FP64 MAC.  Plaintext words a and ciphertext words y are
+// split at 2^23 (a = a1 2^23 + a0, y = y1 2^23 + y0, all parts < 2^23), so every partial product
+// is < 2^46 and the three sums  A = sum a1 y1,  B = sum (a1 y0 + a0 y1),  C = sum a0 y0  over t1 <= 32
+// terms stay below 2^51: exact in FP64 with one DFMA per partial product (4 per MAC, no per-term
+// reduction, accumulator-only dependency chains).  w_k = A 2^46 + B 2^23 + C  mod q at the end.
+// CTA = 8 coefficients x 32 ciphertext lanes; the split plaintext tile [t][8] (double2) is staged once.
+#define MACF_XT 8
+#define MACF_BL 32
+#define MACF_KH 8
+__global__ void __launch_bounds__(MACF_XT * MACF_BL, 2)
+k_bsgs_mac_fp(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u64* __restrict__ v0, size_t v0_stride,
+              const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl)
+{
+    extern __shared__ double2 A2[];
+    const int n = dc->n;
+    const int l = blockIdx.y;
+    const DPrime Pr = dc->p[l];
+    if (prime_class(Pr.q) != PC_FP) return;
+    const int tx = threadIdx.x % MACF_XT, ty = threadIdx.x / MACF_XT;
+    const int x0 = blockIdx.x * MACF_XT, x = x0 + tx;
+    const int t = t1 * t2;
+    const u64 mask23 = (1ULL << 23) - 1;
+    for (int i = threadIdx.x; i < t * MACF_XT; i += blockDim.x) {
+        const u64 a = pts[((size_t)(i / MACF_XT) * nl + l) * n + x0 + (i % MACF_XT)];
+        A2[i] = make_double2(u2d(a >> 23), u2d(a & mask23));
+    }
+    __syncthreads();
+    const double q = (double)Pr.q, qinv = 1.0 / q;
+    const double two23 = 8388608.0, two46 = 70368744177664.0;
+    const double w46 = two46 - floor(two46 * qinv) * q;                        // 2^46 mod q (exact)
+    const double w46q = w46 / q, w23q = two23 / q;
+    const size_t ctw = (size_t)2 * nl * n;
+    for (int b = ty; b < batch; b += MACF_BL) {
+        for (int c = 0; c < 2; ++c) {
+            const size_t off = ((size_t)c * nl + l) * n + x;
+            for (int k0 = 0; k0 < t2; k0 += MACF_KH) {
+                double sA[MACF_KH], sB[MACF_KH], sC[MACF_KH];
+#pragma unroll
+                for (int z = 0; z < MACF_KH; ++z) sA[z] = sB[z] = sC[z] = 0.0;
+                for (int j0 = 0; j0 < t1; j0 += 8) {
+                    double y1[8], y0[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int j = j0 + u;
+                        u64 y = 0;
+                        if (j < t1) {
+                            const u64* v = (j == 0) ? v0 + (size_t)b * v0_stride : vb + ((size_t)(j - 1) * batch + b) * ctw;
+                            y = v[off];
+                        }
+                        y1[u] = u2d(y >> 23);
+                        y0[u] = u2d(y & mask23);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int j = j0 + u;
+                        if (j < t1) {
+#pragma unroll
+                            for (int z = 0; z < MACF_KH; ++z) {
+                                if (k0 + z < t2) {
+                                    const double2 a = A2[((k0 + z) * t1 + j) * MACF_XT + tx];
+                                    sA[z] = __fma_rn(a.x, y1[u], sA[z]);
+                                    sB[z] = __fma_rn(a.x, y0[u], sB[z]);
+                                    sB[z] = __fma_rn(a.y, y1[u], sB[z]);
+                                    sC[z] = __fma_rn(a.y, y0[u], sC[z]);
+                                }
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int z = 0; z < MACF_KH; ++z) {
+                    if (k0 + z < t2) {
+                        const double r = fmodmul(freduce(sA[z], q, qinv), w46, w46q, q) +
+                                         fmodmul(freduce(sB[z], q, qinv), two23, w23q, q) + freduce(sC[z], q, qinv);
+                        wout[((size_t)(k0 + z) * batch + b) * ctw + off] = fcanon(r, q, qinv);
+                    }
+                }
+            }
+        }
+    }
 }
 
 void bsgs_mac(const Launch& L, const uint64_t* pts, const uint64_t* v0, size_t v0_stride, const uint64_t* vbaby,
@@ -637,8 +720,11 @@ void bsgs_mac(const Launch& L, const uint64_t* pts, const uint64_t* v0, size_t v
     if (smem > 200 * 1024) throw std::runtime_error("bsgs_mac: plaintext tile too large (t <= 1600)");
     allow_smem(k_bsgs_mac, smem);
     { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac"); k_bsgs_mac<<<dim3(n / 16, nl), 256, smem, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl); }
+    const size_t smem_fp = (size_t)t1 * t2 * MACF_XT * sizeof(double2);
+    allow_smem(k_bsgs_mac_fp, smem_fp);
+    { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_fp"); k_bsgs_mac_fp<<<dim3(n / MACF_XT, nl), MACF_XT * MACF_BL, smem_fp, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl); }
     check_launch("bsgs_mac");
-    if (L.counter) ++*L.counter;
+    if (L.counter) *L.counter += 2;
 }
 
 // ------------------------------------------------------------------------------------ decrypt
