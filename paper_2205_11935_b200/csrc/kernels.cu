@@ -530,105 +530,6 @@ void add(const Launch& L, const uint64_t* a, size_t sa, const uint64_t* b, size_
 // Thread (coefficient x, giant index k) keeps its t1 plaintext words in registers and loops over the
 // batch, so every plaintext word is read once per launch; v words are shared through L1 by the t2
 // threads of the same coefficient.
-// One (coefficient x, ciphertext b) per thread; for each component and each half of the giant
-// indices it keeps 16 accumulators and streams j: v_j[b] is loaded once per (c, k-half) and used
-// for 16 products, plaintext words come from the shared tile A[t][16] (broadcast across b-lanes).
-// FP64 path for primes < 2^45: product y*w exact as ph+pl, quotient rint(ph/q), signed remainder,
-// sum of t1 remainders |.| < 17 q stays exact.  Integer path: 128-bit lazy accumulation.
-template <bool FP>
-__device__ __forceinline__ void bsgs_mac_body(const DCtx* __restrict__ dc, const u64* __restrict__ A,
-                                              const u64* __restrict__ v0, size_t v0_stride, const u64* __restrict__ vb,
-                                              u64* __restrict__ wout, int t1, int t2, int batch, int nl, int l, int x,
-                                              int tx, int ty)
-{
-    const int n = dc->n;
-    const DPrime Pr = dc->p[l];
-    const size_t ctw = (size_t)2 * nl * n;
-    const double q = (double)Pr.q, qinv = 1.0 / q;
-    for (int b = ty; b < batch; b += 16) {
-        for (int c = 0; c < 2; ++c) {
-            const size_t off = ((size_t)c * nl + l) * n + x;
-            for (int k0 = 0; k0 < t2; k0 += 16) {
-                const int nk = (t2 - k0) < 16 ? (t2 - k0) : 16;
-                if constexpr (FP) {
-                    double acc[16];
-#pragma unroll
-                    for (int z = 0; z < 16; ++z) acc[z] = 0.0;
-                    // 8 baby-step words in flight per thread before they are consumed
-                    for (int j0 = 0; j0 < t1; j0 += 8) {
-                        double y[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const int j = j0 + u;
-                            y[u] = 0.0;
-                            if (j < t1) {
-                                const u64* v = (j == 0) ? v0 + (size_t)b * v0_stride
-                                                        : vb + ((size_t)(j - 1) * batch + b) * ctw;
-                                y[u] = u2d(v[off]);
-                            }
-                        }
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const int j = j0 + u;
-                            if (j < t1) {
-#pragma unroll
-                                for (int z = 0; z < 16; ++z) {
-                                    if (z < nk) {
-                                        const double w =
-                                            __longlong_as_double((long long)A[((k0 + z) * t1 + j) * 16 + tx]);
-                                        const double ph = y[u] * w;
-                                        const double pl = __fma_rn(y[u], w, -ph);
-                                        const double kq = __fma_rn(ph, qinv, CK_RND_MAGIC) - CK_RND_MAGIC;
-                                        acc[z] += __fma_rn(-kq, q, ph) + pl;
-                                    }
-                                }
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int z = 0; z < 16; ++z)
-                        if (z < nk) wout[((size_t)(k0 + z) * batch + b) * ctw + off] = fcanon(acc[z], q, qinv);
-                } else {
-                    Acc128 acc[16];
-#pragma unroll
-                    for (int z = 0; z < 16; ++z) acc[z].zero();
-#pragma unroll 2
-                    for (int j = 0; j < t1; ++j) {
-                        const u64* v = (j == 0) ? v0 + (size_t)b * v0_stride : vb + ((size_t)(j - 1) * batch + b) * ctw;
-                        const u64 y = v[off];
-#pragma unroll
-                        for (int z = 0; z < 16; ++z)
-                            if (z < nk) acc[z].mac(A[((k0 + z) * t1 + j) * 16 + tx], y);
-                    }
-#pragma unroll
-                    for (int z = 0; z < 16; ++z)
-                        if (z < nk) wout[((size_t)(k0 + z) * batch + b) * ctw + off] = acc[z].reduce(Pr);
-                }
-            }
-        }
-    }
-}
-
-__global__ void __launch_bounds__(256, 2)
-k_bsgs_mac(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u64* __restrict__ v0, size_t v0_stride,
-           const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl)
-{
-    extern __shared__ u64 A[];
-    const int n = dc->n;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int x0 = blockIdx.x * 16, x = x0 + tx, l = blockIdx.y;
-    const int t = t1 * t2;
-    const bool fp = prime_class(dc->p[l].q) == PC_FP;
-    if (fp) return;   // FP-class limbs are handled by k_bsgs_mac_fp
-    for (int i = threadIdx.x; i < t * 16; i += blockDim.x) {
-        const u64 a = pts[((size_t)(i >> 4) * nl + l) * n + x0 + (i & 15)];
-        A[i] = fp ? (u64)__double_as_longlong(u2d(a)) : a;
-    }
-    __syncthreads();
-    if (fp) bsgs_mac_body<true>(dc, A, v0, v0_stride, vb, wout, t1, t2, batch, nl, l, x, tx, ty);
-    else bsgs_mac_body<false>(dc, A, v0, v0_stride, vb, wout, t1, t2, batch, nl, l, x, tx, ty);
-}
-
 // FP-class limbs (q < 2^45): split-operand FP64 MAC.  Plaintext words a and ciphertext words y are
 // split at 2^23 (a = a1 2^23 + a0, y = y1 2^23 + y0, all parts < 2^23), so every partial product
 // is < 2^46 and the three sums  A = sum a1 y1,  B = sum (a1 y0 + a0 y1),  C = sum a0 y0  over t1 <= 32
@@ -711,15 +612,68 @@ k_bsgs_mac_fp(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u6
     }
 }
 
+// BIG-class limbs (60-bit primes): same tiling as k_bsgs_mac_fp with 128-bit integer accumulators.
+__global__ void __launch_bounds__(MACF_XT * MACF_BL, 2)
+k_bsgs_mac_int(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u64* __restrict__ v0, size_t v0_stride,
+               const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl)
+{
+    extern __shared__ u64 Ai[];
+    const int n = dc->n;
+    const int l = blockIdx.y;
+    const DPrime Pr = dc->p[l];
+    if (prime_class(Pr.q) == PC_FP) return;
+    const int tx = threadIdx.x % MACF_XT, ty = threadIdx.x / MACF_XT;
+    const int x0 = blockIdx.x * MACF_XT, x = x0 + tx;
+    const int t = t1 * t2;
+    for (int i = threadIdx.x; i < t * MACF_XT; i += blockDim.x)
+        Ai[i] = pts[((size_t)(i / MACF_XT) * nl + l) * n + x0 + (i % MACF_XT)];
+    __syncthreads();
+    const size_t ctw = (size_t)2 * nl * n;
+    for (int b = ty; b < batch; b += MACF_BL) {
+        for (int c = 0; c < 2; ++c) {
+            const size_t off = ((size_t)c * nl + l) * n + x;
+            for (int k0 = 0; k0 < t2; k0 += MACF_KH) {
+                Acc128 s[MACF_KH];
+#pragma unroll
+                for (int z = 0; z < MACF_KH; ++z) s[z].zero();
+                for (int j0 = 0; j0 < t1; j0 += 8) {
+                    u64 y[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int j = j0 + u;
+                        y[u] = 0;
+                        if (j < t1) {
+                            const u64* v = (j == 0) ? v0 + (size_t)b * v0_stride : vb + ((size_t)(j - 1) * batch + b) * ctw;
+                            y[u] = v[off];
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        if (j0 + u < t1) {
+#pragma unroll
+                            for (int z = 0; z < MACF_KH; ++z)
+                                if (k0 + z < t2) s[z].mac(Ai[((k0 + z) * t1 + j0 + u) * MACF_XT + tx], y[u]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int z = 0; z < MACF_KH; ++z)
+                    if (k0 + z < t2) wout[((size_t)(k0 + z) * batch + b) * ctw + off] = s[z].reduce(Pr);
+            }
+        }
+    }
+}
+
 void bsgs_mac(const Launch& L, const uint64_t* pts, const uint64_t* v0, size_t v0_stride, const uint64_t* vbaby,
               uint64_t* wout, int t1, int t2, int batch, int nl)
 {
     if (batch <= 0) return;
     const int n = 1 << L.log_n;
-    const size_t smem = (size_t)t1 * t2 * 16 * 8;
-    if (smem > 200 * 1024) throw std::runtime_error("bsgs_mac: plaintext tile too large (t <= 1600)");
-    allow_smem(k_bsgs_mac, smem);
-    { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac"); k_bsgs_mac<<<dim3(n / 16, nl), 256, smem, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl); }
+    if ((size_t)t1 * t2 * MACF_XT * sizeof(double2) > 200 * 1024)
+        throw std::runtime_error("bsgs_mac: plaintext tile too large (t <= 1600)");
+    const size_t smem_int = (size_t)t1 * t2 * MACF_XT * sizeof(u64);
+    allow_smem(k_bsgs_mac_int, smem_int);
+    { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_int"); k_bsgs_mac_int<<<dim3(n / MACF_XT, nl), MACF_XT * MACF_BL, smem_int, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl); }
     const size_t smem_fp = (size_t)t1 * t2 * MACF_XT * sizeof(double2);
     allow_smem(k_bsgs_mac_fp, smem_fp);
     { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_fp"); k_bsgs_mac_fp<<<dim3(n / MACF_XT, nl), MACF_XT * MACF_BL, smem_fp, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl); }
