@@ -205,6 +205,7 @@ struct ckks_ctx {
     size_t work_bytes = 0;
     unsigned long long launches = 0;
     ck::Probe probe;
+    std::vector<int> pclass;   // prime class per prime (host copy)
 
     ck::Launch launch(void* st)
     {
@@ -216,6 +217,7 @@ struct ckks_ctx {
         l.st = (cudaStream_t)st;
         l.counter = &launches;
         l.probe = &probe;
+        l.pclass = pclass.data();
         return l;
     }
     size_t ct_words(int nl, int ncomp = 2) const { return (size_t)ncomp * nl * n; }
@@ -472,6 +474,7 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
         c->sigma = p->sigma > 0 ? p->sigma : 3.2;
         c->max_batch = p->max_batch;
         c->primes = primes;
+        for (u64 q : primes) c->pclass.push_back(prime_class(q));
         const int n = c->n, np = c->np, L = c->L;
         // ---- constants
         DCtx& h = c->host_dc;
@@ -625,6 +628,7 @@ ckks_status ckks_probe_enable(ckks_ctx* c, int32_t kind)
         c->probe.alg_bytes = 0;
         c->probe.names.clear();
         c->probe.bytes_by_kernel.clear();
+        c->probe.bfly_fp = c->probe.bfly_int = 0;
         while (kind && c->probe.ev.size() < 4096) {
             cudaEvent_t e;
             cuda_ok(cudaEventCreate(&e), "event");
@@ -656,6 +660,12 @@ ckks_status ckks_probe_read_all(ckks_ctx* c, char* json, size_t cap)
             std::snprintf(buf, sizeof(buf), "\"%s\": {\"ms\": %.6f, \"launches\": %llu, \"alg_bytes\": %.1f}",
                           kv.first.c_str(), kv.second.first, (unsigned long long)kv.second.second,
                           it == c->probe.bytes_by_kernel.end() ? 0.0 : it->second);
+            s += buf;
+        }
+        {
+            char buf[160];
+            std::snprintf(buf, sizeof(buf), "%s\"_modup_butterflies\": {\"fp64\": %.1f, \"int\": %.1f}",
+                          s.size() > 1 ? ", " : "", c->probe.bfly_fp, c->probe.bfly_int);
             s += buf;
         }
         s += "}";

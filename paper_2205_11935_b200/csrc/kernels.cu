@@ -311,9 +311,19 @@ void keyswitch_modup(const Launch& L, const KsIn& in, int batch, int nl, const K
         allow_smem(kd, smem);
         allow_smem(km, smem);
         const bool pm = L.probe && L.probe->on(PROBE_MODUP);
-        if (L.probe && L.probe->on(PROBE_ALL))
+        if (L.probe && L.probe->on(PROBE_ALL)) {
             L.probe->bytes_by_kernel["k_ks_modup"] +=
                 ((double)batch * nl + (double)batch * nl * nl) * (double)(8 << L.log_n);
+            // butterflies per limb NTT: (N/2) log2 N; targets of digit j: every prime but q_j
+            const double bf = (double)(1 << (L.log_n - 1)) * L.log_n * batch;
+            for (int j = 0; j < nl; ++j)
+                for (int e = 0; e <= nl; ++e) {
+                    if (e == j) continue;
+                    const int p = (e == nl) ? L.n_data : e;
+                    if (L.pclass && L.pclass[p] == PC_FP) L.probe->bfly_fp += bf;
+                    else L.probe->bfly_int += bf;
+                }
+        }
         { ProbeScope ps_(L.probe, L.st, "k_ks_digits"); kd<<<dim3(nl, batch), (wm & 1) ? NW : NT, smem, L.st>>>(L.dc, in.base, in.ct_stride, in.comp_off, in.galois,
                                                               w.digits, nl); }
         if (pm) {

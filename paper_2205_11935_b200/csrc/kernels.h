@@ -20,6 +20,7 @@ struct Probe {
     size_t used = 0;
     double alg_bytes = 0;   // algorithmic bytes of the probed launches
     std::map<std::string, double> bytes_by_kernel;   // PROBE_ALL: algorithmic bytes per kernel name
+    double bfly_fp = 0, bfly_int = 0;                // ModUp butterflies on FP64-class / integer-class primes
     void mark(cudaStream_t s)
     {
         if (used == ev.size()) {
@@ -57,6 +58,7 @@ struct Launch {
     cudaStream_t st;
     unsigned long long* counter;   // launches issued (for bench gpu_launches)
     Probe* probe;
+    const int* pclass;             // host: prime class (ntt.cuh PC_*) of every prime, for probe accounting
 };
 
 // batched in-place NTT over [batch][limbs][N]; limb l uses prime (prime0 + l)
