@@ -257,3 +257,221 @@ def pack_input(x, t: int, n_slots: int) -> np.ndarray:
     v[: x.size] = x
     v[t: t + x.size] = x
     return v
+
+
+# =============================================================================== NEXT f-2: frozen stack
+# The paper's frozen server stack: Conv1D (f=9) -> Dense 768 + ReLU_approx (Eq. 2)
+# -> AvgPool (f=3) -> [Dropout = identity at inference] -> Dense 766, depth 6, with p items per
+# ciphertext.  Readings R25-R28:
+#   R25 packing: p = floor(n / (2t + c)) items (c = conv half-width, 0 without conv; = the paper's
+#       floor(#slots / 2 #neurons) when c is small enough), region size R = floor(n / p); item r at
+#       slots [rR, rR + t), zeros in [rR + t, (r+1)R) until a replicate duplicates it.
+#   R26 conv1d ('same', zero padded, P:L98 packed SISO): out[k] = sum_{i<f} w_i x[k + i - c] + b,
+#       = sum_i m_i o rot_{i-c}(x), m_i = w_i on every item's [rR, rR + t); f mults, f-1 rotations.
+#   R27 avgpool (x_o = (1/f) sum_i rot_{-i}(x)): out[k] = (1/f) sum_{i<f} x[k - i],
+#       valid on [f-1, t) of each item (the 1/f plaintext is the validity mask); f-1 rotations, 1 mult.
+#   R28 the dense after the pool reads its input from slots [f-1, t): cols = t, columns < f-1 zero.
+
+def packing(n_slots: int, t: int, conv_half: int = 0):
+    """(p, R): items per ciphertext and region size (R25)."""
+    p = n_slots // (2 * t + conv_half)
+    if p < 1:
+        raise ValueError("item does not fit")
+    return p, n_slots // p
+
+
+def region_mask(values, t: int, region: int, items: int, n_slots: int, offset: int = 0) -> np.ndarray:
+    """Per-slot vector holding `values` (length <= t, or a scalar) at [rR + offset, ...) for every item."""
+    out = np.zeros(n_slots)
+    v = np.broadcast_to(np.asarray(values, dtype=np.float64), (t - offset,)) if np.ndim(values) == 0 \
+        else np.asarray(values, dtype=np.float64)
+    for r in range(items):
+        out[r * region + offset: r * region + offset + v.size] = v
+    return out
+
+
+@dataclass
+class HoistedLayer:
+    """A linear layer evaluated as  y = sum_k rot_{k g}( sum_j pt_{k,j} o rot_{s_j}(x) )  (+ bias), with
+    baby steps s_0 = 0, s_1.. and (for the BSGS dense) giant step g = t1.  Shared encodings (R8)."""
+    kind: str                   # "dense" | "conv" | "pool"
+    t: int
+    t2: int
+    baby_steps: list
+    giant: int
+    level: int
+    pt_scale: float
+    bias_scale: float
+    pt_coeffs: np.ndarray       # [t2 * t1][N] int64
+    bias_coeffs: np.ndarray     # [N] int64 or None
+    rows: int = 0
+    cols: int = 0
+
+    @property
+    def t1(self):
+        return len(self.baby_steps)
+
+
+def encode_dense_packed(ctx, W, b, level, in_scale, region, items) -> HoistedLayer:
+    """BSGS dense (Eq. 1) with diag' replicated in every item region."""
+    W = np.asarray(W, dtype=np.float64)
+    rows, cols = W.shape
+    D, (t, t1, t2) = diagonals(W)
+    n = ctx.n // 2
+    q_l = float(ctx.primes[level])
+    pts = []
+    for i in range(t):
+        k = i // t1
+        v = np.zeros(n)
+        for r in range(items):
+            v[r * region + k * t1: r * region + k * t1 + t] = D[i]
+        pts.append(encoding.encode(v, q_l, ctx.n))
+    bias = None
+    if b is not None:
+        bias = encoding.encode(region_mask(np.asarray(b), t, region, items, n), in_scale, ctx.n)
+    return HoistedLayer("dense", t, t2, list(range(t1)), t1, level, q_l, in_scale, np.stack(pts), bias, rows, cols)
+
+
+def encode_conv(ctx, w, bias, t, level, in_scale, region, items) -> HoistedLayer:
+    """R26: taps ordered so that step 0 (the centre tap) comes first."""
+    w = np.asarray(w, dtype=np.float64)
+    f = w.size
+    c = (f - 1) // 2
+    order = [c] + [i for i in range(f) if i != c]
+    n = ctx.n // 2
+    q_l = float(ctx.primes[level])
+    pts = np.stack([encoding.encode(region_mask(w[i], t, region, items, n), q_l, ctx.n) for i in order])
+    bc = None
+    if bias is not None:
+        bc = encoding.encode(region_mask(float(bias), t, region, items, n), in_scale, ctx.n)
+    return HoistedLayer("conv", t, 1, [i - c for i in order], 0, level, q_l, in_scale, pts, bc, t, t)
+
+
+def encode_pool(ctx, f, t, level, region, items) -> HoistedLayer:
+    """R27: f copies of the 1/f validity mask on [f-1, t); steps 0, -1, .., -(f-1)."""
+    n = ctx.n // 2
+    q_l = float(ctx.primes[level])
+    m = encoding.encode(region_mask(1.0 / f, t, region, items, n, offset=f - 1), q_l, ctx.n)
+    return HoistedLayer("pool", t, 1, [-i for i in range(f)], 0, level, q_l, 0.0, np.stack([m] * f), None, t, t)
+
+
+def apply_layer(ctx, ct: Ct, lay: HoistedLayer, hoisted: bool = True, ops: OpCount | None = None) -> Ct:
+    """y = sum_k rot_{k g}(sum_j pt_{k,j} o rot_{s_j}(x)), one rescale, + bias (Eq. 1 / R26 / R27)."""
+    l = ct.level
+    assert lay.level == l
+    rot = ctx.rotate_hoisted if hoisted else ctx.rotate
+    baby = [ct.data if s == 0 else rot(ct.data, s) for s in lay.baby_steps]
+    if ops:
+        ops.rot += sum(1 for s in lay.baby_steps if s != 0)
+    y = None
+    for k in range(lay.t2):
+        w = None
+        for j in range(lay.t1):
+            term = ctx.mul_plain(baby[j], ctx.plain(lay.pt_coeffs[k * lay.t1 + j], l))
+            w = term if w is None else ctx.add(w, term)
+            if ops:
+                ops.mul_plain += 1
+        if k > 0:
+            w = ctx.rotate(w, k * lay.giant)
+            if ops:
+                ops.rot += 1
+        y = w if y is None else ctx.add(y, w)
+    y = ctx.rescale(y)
+    if lay.bias_coeffs is not None:
+        y = ctx.add_plain(y, ctx.plain(lay.bias_coeffs, l - 1))
+    return Ct(y, ct.scale * lay.pt_scale / float(ctx.primes[l]))
+
+
+def frozen_stack_params(t: int = 768, f_conv: int = 9, f_pool: int = 3):
+    return {"t": t, "f_conv": f_conv, "f_pool": f_pool}
+
+
+def frozen_stack_steps(t, t_dense_shapes, f_conv, f_pool):
+    c = (f_conv - 1) // 2
+    steps = set(d for d in range(-c, c + 1) if d != 0)
+    steps.update(-i for i in range(1, f_pool))
+    for rows, cols in t_dense_shapes:
+        tt, t1, t2 = bsgs_split(rows, cols)
+        steps.update(range(1, t1))
+        steps.update(k * t1 for k in range(1, t2))
+        steps.add(-tt)
+    return sorted(steps)
+
+
+def encode_frozen_stack(ctx, weights, level, scale, region, items):
+    """weights: dict conv_w (f), conv_b, W1 (t x t), b1 (t), W2 (t-fp+1 x t-fp+1), b2; returns the
+    stage list [(layer, activation, replicate_t)] with levels/scales of the depth-6 schedule."""
+    t = weights["W1"].shape[1]
+    fp = weights["f_pool"]
+    stages = []
+    l, s = level, scale
+    conv = encode_conv(ctx, weights["conv_w"], weights["conv_b"], t, l, s, region, items)
+    stages.append((conv, "none", 0))
+    l -= 1
+    d1 = encode_dense_packed(ctx, weights["W1"], weights["b1"], l, s, region, items)
+    stages.append((d1, "cubic", t))
+    l -= 1
+    ql, ql1 = float(ctx.primes[l]), float(ctx.primes[l - 1])
+    s = (s * s / ql) * s / ql1
+    l -= 2
+    pool = encode_pool(ctx, fp, t, l, region, items)
+    stages.append((pool, "none", 0))
+    l -= 1
+    W2 = np.zeros((weights["W2"].shape[0], t))
+    W2[:, fp - 1:] = weights["W2"]                     # R28: input slots [f-1, t)
+    d2 = encode_dense_packed(ctx, W2, weights["b2"], l, s, region, items)
+    stages.append((d2, "none", t))
+    return stages
+
+
+def cubic_masked_coeffs(ctx, rows, t, region, items, scale):
+    v = region_mask(RELU_APPROX[3], t, region, items, ctx.n // 2)
+    v = np.where(np.arange(ctx.n // 2) % region < rows, v, 0.0) if items else v
+    return encoding.encode(v, scale, ctx.n)
+
+
+def forward_stages(ctx, ct: Ct, stages, region, items, hoisted=True, ops=None) -> Ct:
+    for lay, act, rep_t in stages:
+        if rep_t:
+            ct = replicate(ctx, ct, rep_t)
+            if ops:
+                ops.rot += 1
+        ct = apply_layer(ctx, ct, lay, hoisted, ops)
+        if act == "cubic":
+            l = ct.level
+            S = ct.scale
+            ql, ql1 = float(ctx.primes[l]), float(ctx.primes[l - 1])
+            S3 = (S * S / ql) * S / ql1
+            c0 = cubic_masked_coeffs(ctx, lay.rows, lay.t, region, items, S3)
+            ct = cubic(ctx, ct, c0_coeffs=c0)
+        elif act == "square":
+            ct = square(ctx, ct)
+    return ct
+
+
+def conv_same(x, w, b):
+    f = len(w)
+    c = (f - 1) // 2
+    xp = np.concatenate([np.zeros(c), x, np.zeros(c)])
+    return np.array([np.dot(w, xp[k:k + f]) for k in range(len(x))]) + b
+
+
+def pool_valid_right(x, f):
+    return np.array([np.mean(x[k - f + 1:k + 1]) for k in range(f - 1, len(x))])
+
+
+def plain_frozen_forward(x, weights):
+    """float64 twin of the frozen stack (dropout = identity at inference)."""
+    y = conv_same(np.asarray(x, dtype=np.float64), weights["conv_w"], weights["conv_b"])
+    y = weights["W1"] @ y + weights["b1"]
+    c3, c2, c1, c0 = RELU_APPROX
+    y = ((c3 * y + c2) * y + c1) * y + c0
+    y = pool_valid_right(y, weights["f_pool"])
+    return weights["W2"] @ y + weights["b2"]
+
+
+def pack_items(xs, t, region, n_slots):
+    v = np.zeros(n_slots)
+    for r, x in enumerate(xs):
+        v[r * region: r * region + len(x)] = x
+    return v
