@@ -43,7 +43,6 @@ typedef enum {
 } ckks_status;
 
 typedef struct ckks_ctx ckks_ctx;
-typedef struct ckks_layer ckks_layer;
 typedef struct ckks_model ckks_model;
 
 /* Scheme parameters (R1, R13-R15).  Primes: for each entry of prime_bits in order, the largest
@@ -68,6 +67,33 @@ typedef struct {
     uint64_t primes[16];        /* q_0..q_{L-1}, then P                                            */
     uint64_t psi[16];           /* minimal primitive 2N-th root used by the NTT (R2)               */
 } ckks_info;
+
+/* Layer kinds (the paper's frozen stack).  Every layer is evaluated as
+ *   y = sum_{k<t2} rot_{k giant}( sum_{j<t1} pt_{k t1 + j} o rot_{baby_steps[j]}(x) )  (+ bias)
+ * with one rescale: the BSGS dense (Eq. 1), the packed-SISO conv1d (L98, R26) and the
+ * average pool (L100-103, R27).  Multi-item packing (L115-116, R25): item r of p lives in slots
+ * [r R, r R + t) (R = region size); layer plaintexts hold one copy per item. */
+enum { CKKS_LAYER_DENSE = 0, CKKS_LAYER_CONV1D = 1, CKKS_LAYER_AVGPOOL = 2 };
+typedef struct {
+    int32_t kind;
+    uint32_t rows, cols;        /* dense shape; conv/pool: t, t                                    */
+    uint32_t t;                 /* item width (distance of a replicate before the next layer)      */
+    uint32_t t2;                /* giant steps (1 for conv/pool)                                   */
+    uint32_t n_baby;            /* t1 <= 32                                                        */
+    const int32_t* baby_steps;  /* n_baby rotation steps, baby_steps[0] == 0                       */
+    int32_t giant;              /* giant step (t1 for the dense)                                   */
+    uint32_t region, items;     /* R, p (items 1 and region 0 = single item)                       */
+    uint32_t level;             /* level of the input ciphertext                                   */
+    double pt_scale, bias_scale;
+} ckks_layer_desc;
+
+/* One stage of a model: optional replicate y + rot_{-t}(y) before the layer, activation after it. */
+typedef struct ckks_layer ckks_layer;
+typedef struct {
+    const ckks_layer* layer;
+    int32_t activation;         /* 0 none, 1 square, 2 cubic (Eq. 2)                               */
+    uint32_t replicate_t;       /* 0 = no replicate                                                */
+} ckks_stage;
 
 typedef struct {
     uint64_t* data;  /* device [batch][n_comp][level+1][N]                                         */
@@ -146,6 +172,23 @@ ckks_status ckks_layer_import(ckks_ctx* ctx, const int64_t* diag_coeffs, const i
                               uint32_t cols, uint32_t level, double pt_scale, double bias_scale, void* dev_buf,
                               void* stream, ckks_layer** out);
 void ckks_layer_destroy(ckks_layer* layer);
+/* f-2 constructors (library encoder).  dense with p items in regions of R slots (R >= 2t); conv1d
+ * with f taps ('same', zero padded, centre tap first), scalar bias on [rR, rR + t); avgpool of size f
+ * (right-aligned window, 1/f mask on [rR + f - 1, rR + t)).  dev_buf: ckks_layer_general_sizes bytes
+ * for t (dense), f (conv, pool) plaintexts. */
+ckks_status ckks_dense_create_packed(ckks_ctx* ctx, const double* W, uint32_t rows, uint32_t cols, const double* bias,
+                                     uint32_t region, uint32_t items, uint32_t level, double in_scale, void* dev_buf,
+                                     void* stream, ckks_layer** out);
+ckks_status ckks_conv1d_create(ckks_ctx* ctx, const double* w, uint32_t f, double bias, uint32_t t, uint32_t region,
+                               uint32_t items, uint32_t level, double in_scale, void* dev_buf, void* stream,
+                               ckks_layer** out);
+ckks_status ckks_avgpool_create(ckks_ctx* ctx, uint32_t f, uint32_t t, uint32_t region, uint32_t items, uint32_t level,
+                                void* dev_buf, void* stream, ckks_layer** out);
+ckks_status ckks_layer_general_sizes(const ckks_ctx* ctx, uint32_t n_plaintexts, uint32_t level, size_t* dev_bytes);
+/* Any layer from already-encoded plaintexts: pt_coeffs host [t2 * n_baby][N] int64 in (k, j) order,
+ * bias_coeffs host [N] or NULL (parity path: the oracle's encodings). */
+ckks_status ckks_layer_import_general(ckks_ctx* ctx, const ckks_layer_desc* desc, const int64_t* pt_coeffs,
+                                      const int64_t* bias_coeffs, void* dev_buf, void* stream, ckks_layer** out);
 /* Workspace (device bytes) ckks_matvec_diag / ckks_encrypted_forward need for `batch` cts. */
 ckks_status ckks_layer_work_sizes(const ckks_ctx* ctx, const ckks_layer* layer, uint32_t batch, size_t* bytes);
 /* y = sum_k rot_{k t1}(sum_j diag'_{k t1+j} o rot_j(x)) (Eq. 1), one rescale (R7), + bias.
@@ -162,6 +205,12 @@ ckks_status ckks_matvec_diag(ckks_ctx* ctx, const ckks_layer* layer, const ckks_
 ckks_status ckks_model_sizes(const ckks_ctx* ctx, uint32_t n_layers, int32_t activation, size_t* dev_bytes);
 ckks_status ckks_model_create(ckks_ctx* ctx, const ckks_layer* const* layers, uint32_t n_layers, int32_t activation,
                               const int64_t* act_coeffs, void* dev_buf, void* stream, ckks_model** out);
+/* General stage list (e.g. the paper's depth-6 frozen stack: conv -> [rep] dense+cubic -> pool ->
+ * [rep] dense).  act_coeffs: host [n][N], row i = the masked c0 plaintext of stage i when its
+ * activation is cubic (NULL: encoded here on the layer's rows of every item). */
+ckks_status ckks_model_stages_sizes(const ckks_ctx* ctx, const ckks_stage* stages, uint32_t n, size_t* dev_bytes);
+ckks_status ckks_model_create_stages(ckks_ctx* ctx, const ckks_stage* stages, uint32_t n, const int64_t* act_coeffs,
+                                     void* dev_buf, void* stream, ckks_model** out);
 void ckks_model_destroy(ckks_model* model);
 /* on != 0: the baby-step rotations of every dense layer are hoisted (ckks_rotate_hoisted semantics). */
 ckks_status ckks_model_set_hoisting(ckks_model* model, int32_t on);

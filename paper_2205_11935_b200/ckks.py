@@ -44,6 +44,20 @@ class ckks_ct(ctypes.Structure):
                 ("level", ctypes.c_uint32), ("scale", ctypes.c_double)]
 
 
+class ckks_layer_desc(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("rows", ctypes.c_uint32), ("cols", ctypes.c_uint32),
+                ("t", ctypes.c_uint32), ("t2", ctypes.c_uint32), ("n_baby", ctypes.c_uint32),
+                ("baby_steps", ctypes.POINTER(ctypes.c_int32)), ("giant", ctypes.c_int32),
+                ("region", ctypes.c_uint32), ("items", ctypes.c_uint32), ("level", ctypes.c_uint32),
+                ("pt_scale", ctypes.c_double), ("bias_scale", ctypes.c_double)]
+
+
+class ckks_stage(ctypes.Structure):
+    _fields_ = [("layer", ctypes.c_void_p), ("activation", ctypes.c_int32), ("replicate_t", ctypes.c_uint32)]
+
+
+LAYER_DENSE, LAYER_CONV1D, LAYER_AVGPOOL = 0, 1, 2
+
 _VP, _SZ = ctypes.c_void_p, ctypes.c_size_t
 _PSZ = ctypes.POINTER(ctypes.c_size_t)
 _PCT = ctypes.POINTER(ckks_ct)
@@ -61,6 +75,13 @@ SIGNATURES = {
     "ckks_rotate": (_I, [_VP, _PCT, _I, _PCT, _VP]),
     "ckks_mul": (_I, [_VP, _PCT, _PCT, _PCT, _VP]),
     "ckks_rotate_hoisted": (_I, [_VP, _PCT, ctypes.POINTER(_I), _U32, _PCT, _VP]),
+    "ckks_dense_create_packed": (_I, [_VP, _VP, _U32, _U32, _VP, _U32, _U32, _U32, _D, _VP, _VP, ctypes.POINTER(_VP)]),
+    "ckks_conv1d_create": (_I, [_VP, _VP, _U32, _D, _U32, _U32, _U32, _U32, _D, _VP, _VP, ctypes.POINTER(_VP)]),
+    "ckks_avgpool_create": (_I, [_VP, _U32, _U32, _U32, _U32, _U32, _VP, _VP, ctypes.POINTER(_VP)]),
+    "ckks_layer_general_sizes": (_I, [_VP, _U32, _U32, _PSZ]),
+    "ckks_layer_import_general": (_I, [_VP, ctypes.POINTER(ckks_layer_desc), _VP, _VP, _VP, _VP, ctypes.POINTER(_VP)]),
+    "ckks_model_stages_sizes": (_I, [_VP, ctypes.POINTER(ckks_stage), _U32, _PSZ]),
+    "ckks_model_create_stages": (_I, [_VP, ctypes.POINTER(ckks_stage), _U32, _VP, _VP, _VP, ctypes.POINTER(_VP)]),
     "ckks_model_set_hoisting": (_I, [_VP, _I]),
     "ckks_relinearize": (_I, [_VP, _PCT, _PCT, _VP]),
     "ckks_rescale": (_I, [_VP, _PCT, _PCT, _VP]),
@@ -397,6 +418,74 @@ class Layer:
         return out
 
 
+class GeneralLayer(Layer):
+    """Any f-2 layer (dense with item regions, conv1d, avgpool); built through the library encoder
+    (`dense`, `conv1d`, `avgpool`) or imported from encoded coefficients (`imported`)."""
+
+    def __init__(self, ctx, n_plaintexts, level, t, rows, build):
+        torch = ctx.torch
+        self.ctx = ctx
+        nb = ctypes.c_size_t()
+        _check(lib().ckks_layer_general_sizes(ctx.h, n_plaintexts, level, ctypes.byref(nb)), "ckks_layer_general_sizes")
+        self.buf = torch.empty(nb.value, dtype=torch.uint8, device=ctx.device)
+        h = ctypes.c_void_p()
+        build(self, h)
+        self.h = h
+        self.level = level
+        self.t = t
+        self.rows = rows
+
+    @classmethod
+    def dense(cls, ctx, W, bias, region, items, level, in_scale, stream=None):
+        Wn = np.ascontiguousarray(W, dtype=np.float64)
+        rows, cols = Wn.shape
+        t = bsgs_plan(rows, cols)[0]
+        bn = None if bias is None else np.ascontiguousarray(bias, dtype=np.float64)
+
+        def build(self, h):
+            self._keep = (Wn, bn)
+            _check(lib().ckks_dense_create_packed(ctx.h, Wn.ctypes.data_as(ctypes.c_void_p), rows, cols,
+                                                  None if bn is None else bn.ctypes.data_as(ctypes.c_void_p), region,
+                                                  items, level, float(in_scale), _ptr(self.buf), _stream(stream),
+                                                  ctypes.byref(h)), "ckks_dense_create_packed")
+        return cls(ctx, t, level, t, rows, build)
+
+    @classmethod
+    def conv1d(cls, ctx, w, bias, t, region, items, level, in_scale, stream=None):
+        wn = np.ascontiguousarray(w, dtype=np.float64)
+
+        def build(self, h):
+            self._keep = wn
+            _check(lib().ckks_conv1d_create(ctx.h, wn.ctypes.data_as(ctypes.c_void_p), wn.size, float(bias), t, region,
+                                            items, level, float(in_scale), _ptr(self.buf), _stream(stream),
+                                            ctypes.byref(h)), "ckks_conv1d_create")
+        return cls(ctx, wn.size, level, t, t, build)
+
+    @classmethod
+    def avgpool(cls, ctx, f, t, region, items, level, stream=None):
+        def build(self, h):
+            _check(lib().ckks_avgpool_create(ctx.h, f, t, region, items, level, _ptr(self.buf), _stream(stream),
+                                             ctypes.byref(h)), "ckks_avgpool_create")
+        return cls(ctx, f, level, t, t, build)
+
+    @classmethod
+    def imported(cls, ctx, kind, rows, cols, t, t2, baby_steps, giant, region, items, level, pt_scale, bias_scale,
+                 pt_coeffs, bias_coeffs=None, stream=None):
+        steps = (ctypes.c_int32 * len(baby_steps))(*[int(s) for s in baby_steps])
+        pts = np.ascontiguousarray(pt_coeffs, dtype=np.int64)
+        bc = None if bias_coeffs is None else np.ascontiguousarray(bias_coeffs, dtype=np.int64)
+        d = ckks_layer_desc(kind, rows, cols, t, t2, len(baby_steps), steps, giant, region, items, level,
+                            float(pt_scale), float(bias_scale))
+
+        def build(self, h):
+            self._keep = (steps, pts, bc, d)
+            _check(lib().ckks_layer_import_general(ctx.h, ctypes.byref(d), pts.ctypes.data_as(ctypes.c_void_p),
+                                                   None if bc is None else bc.ctypes.data_as(ctypes.c_void_p),
+                                                   _ptr(self.buf), _stream(stream), ctypes.byref(h)),
+                   "ckks_layer_import_general")
+        return cls(ctx, pts.shape[0], level, t, rows, build)
+
+
 class Model:
     def __init__(self, ctx: Context, layers, activation=ACT_SQUARE, act_coeffs=None, stream=None):
         self.ctx = ctx
@@ -423,6 +512,29 @@ class Model:
             except Exception:
                 pass
             self.h = None
+
+    @classmethod
+    def from_stages(cls, ctx, stages, act_coeffs=None, stream=None):
+        """stages: [(layer, activation, replicate_t)]."""
+        self = cls.__new__(cls)
+        self.ctx = ctx
+        self.layers = [s[0] for s in stages]
+        arr = (ckks_stage * len(stages))(*[ckks_stage(l.h.value, int(a), int(r)) for l, a, r in stages])
+        nb = ctypes.c_size_t()
+        _check(lib().ckks_model_stages_sizes(ctx.h, arr, len(stages), ctypes.byref(nb)), "ckks_model_stages_sizes")
+        self.buf = ctx.torch.empty(max(1, nb.value), dtype=ctx.torch.uint8, device=ctx.device)
+        ac = None if act_coeffs is None else np.ascontiguousarray(act_coeffs, dtype=np.int64)
+        self._keep = (ac, arr)
+        h = ctypes.c_void_p()
+        _check(lib().ckks_model_create_stages(ctx.h, arr, len(stages),
+                                              None if ac is None else ac.ctypes.data_as(ctypes.c_void_p),
+                                              _ptr(self.buf), _stream(stream), ctypes.byref(h)),
+               "ckks_model_create_stages")
+        self.h = h
+        depth = {ACT_NONE: 0, ACT_SQUARE: 1, ACT_CUBIC: 2}
+        self.in_level = stages[0][0].level
+        self.final_level = self.in_level - sum(1 + depth[int(a)] for _, a, _ in stages)
+        return self
 
     def set_hoisting(self, on=True):
         _check(lib().ckks_model_set_hoisting(self.h, 1 if on else 0), "ckks_model_set_hoisting")

@@ -256,18 +256,31 @@ struct ckks_ctx {
     }
 };
 
+// A linear layer  y = sum_k rot_{k g}( sum_j pt_{k,j} o rot_{s_j}(x) ) (+ bias): the BSGS dense
+// (Eq. 1, s_j = j, g = t1), the packed-SISO conv1d (R26) and the average pool (R27).
 struct ckks_layer {
+    int kind = CKKS_LAYER_DENSE;
     uint32_t rows, cols, t, t1, t2, level;
+    std::vector<int32_t> baby;     // t1 baby steps, baby[0] == 0
+    int32_t giant = 0;
+    uint32_t region = 0, items = 1;
     double pt_scale, bias_scale;
-    u64* d_pts;     // [t][level+1][N]
+    u64* d_pts;     // [t2 * t1][level+1][N]
     u64* d_bias;    // [level][N] or null
+};
+
+struct Stage {
+    const ckks_layer* layer;
+    int activation;       // after the layer: 0 none, 1 square, 2 cubic
+    uint32_t replicate_t; // before the layer: y + rot_{-t}(y) when != 0
 };
 
 struct ckks_model {
     std::vector<const ckks_layer*> layers;
+    std::vector<Stage> stages;
+    std::vector<u64*> d_act_stage;   // per stage: masked c0 plaintext of a cubic activation (or null)
     int activation;
     int hoisted = 0;        // baby-step rotations hoisted (NEXT f-1)
-    u64* d_act = nullptr;   // cubic: masked constant-term plaintexts [n_layers-1][L][N] (R23)
 };
 
 namespace {
@@ -868,6 +881,8 @@ ckks_status ckks_add(ckks_ctx* c, const ckks_ct* a, const ckks_ct* b, ckks_ct* o
 }
 
 // ------------------------------------------------------------------------------------ layers
+static size_t layer_dev_bytes(const ckks_ctx* c, size_t count, uint32_t level);
+
 ckks_status ckks_layer_sizes(const ckks_ctx* c, uint32_t rows, uint32_t cols, uint32_t level, size_t* bytes)
 {
     CK_TRY({
@@ -875,37 +890,48 @@ ckks_status ckks_layer_sizes(const ckks_ctx* c, uint32_t rows, uint32_t cols, ui
         if (level < 1 || (int)level >= c->L) throw CkksError(CKKS_E_LEVEL, "layer level must be in [1, L-1]");
         uint32_t t, t1, t2;
         bsgs_split(rows, cols, t, t1, t2);
-        *bytes = align256((size_t)t * (level + 1) * c->n * 8) + align256((size_t)level * c->n * 8) +
-                 align256((size_t)(t > 1 ? t : 1) * c->n * 8);   // staging for the int64 coefficients
+        *bytes = layer_dev_bytes(c, t, level);
         return CKKS_OK;
     })
 }
 
-static ckks_status layer_from_coeffs(ckks_ctx* c, const int64_t* diag, const int64_t* bias, uint32_t rows,
-                                     uint32_t cols, uint32_t level, double pt_scale, double bias_scale, void* dev_buf,
-                                     void* stream, ckks_layer** out)
+static size_t layer_dev_bytes(const ckks_ctx* c, size_t count, uint32_t level)
 {
-    uint32_t t, t1, t2;
-    bsgs_split(rows, cols, t, t1, t2);
-    if (2 * t > (uint32_t)c->n / 2) throw CkksError(CKKS_E_PARAM, "2t exceeds the slot count");
-    if (t1 > 32 || t2 > 32) throw CkksError(CKKS_E_PARAM, "t1, t2 <= 32 supported (t <= 1024)");
+    return align256(count * (level + 1) * c->n * 8) + align256((size_t)level * c->n * 8) +
+           align256((count > 1 ? count : 1) * c->n * 8);   // + staging for the int64 coefficients
+}
+
+static ckks_status layer_general(ckks_ctx* c, const ckks_layer_desc* d, const int64_t* pts, const int64_t* bias,
+                                 void* dev_buf, void* stream, ckks_layer** out)
+{
+    if (d->n_baby < 1 || !d->baby_steps || d->baby_steps[0] != 0 || d->t2 < 1)
+        throw CkksError(CKKS_E_PARAM, "layer: need n_baby >= 1 with baby_steps[0] == 0 and t2 >= 1");
+    if (d->n_baby > 32) throw CkksError(CKKS_E_PARAM, "layer: at most 32 baby steps");
+    if (d->level < 1 || (int)d->level >= c->L) throw CkksError(CKKS_E_LEVEL, "layer level must be in [1, L-1]");
+    const size_t count = (size_t)d->n_baby * d->t2;
     auto* ly = new ckks_layer();
-    ly->rows = rows;
-    ly->cols = cols;
-    ly->t = t;
-    ly->t1 = t1;
-    ly->t2 = t2;
-    ly->level = level;
-    ly->pt_scale = pt_scale;
-    ly->bias_scale = bias_scale;
+    ly->kind = d->kind;
+    ly->rows = d->rows;
+    ly->cols = d->cols;
+    ly->t = d->t;
+    ly->t1 = d->n_baby;
+    ly->t2 = d->t2;
+    ly->baby.assign(d->baby_steps, d->baby_steps + d->n_baby);
+    ly->giant = d->giant;
+    ly->region = d->region;
+    ly->items = d->items ? d->items : 1;
+    ly->level = d->level;
+    ly->pt_scale = d->pt_scale;
+    ly->bias_scale = d->bias_scale;
+    const uint32_t level = d->level;
     char* base = (char*)dev_buf;
     ly->d_pts = (u64*)base;
-    ly->d_bias = bias ? (u64*)(base + align256((size_t)t * (level + 1) * c->n * 8)) : nullptr;
-    int64_t* stage = (int64_t*)(base + align256((size_t)t * (level + 1) * c->n * 8) + align256((size_t)level * c->n * 8));
+    ly->d_bias = bias ? (u64*)(base + align256(count * (level + 1) * c->n * 8)) : nullptr;
+    int64_t* stage = (int64_t*)(base + align256(count * (level + 1) * c->n * 8) + align256((size_t)level * c->n * 8));
     cudaStream_t st = (cudaStream_t)stream;
     auto L = c->launch(stream);
-    cuda_ok(cudaMemcpyAsync(stage, diag, (size_t)t * c->n * 8, cudaMemcpyHostToDevice, st), "upload diag");
-    ck::signed_to_ntt(L, stage, ly->d_pts, (int)t, (int)level + 1);
+    cuda_ok(cudaMemcpyAsync(stage, pts, count * c->n * 8, cudaMemcpyHostToDevice, st), "upload plaintexts");
+    ck::signed_to_ntt(L, stage, ly->d_pts, (int)count, (int)level + 1);
     if (bias) {
         cuda_ok(cudaStreamSynchronize(st), "sync");
         cuda_ok(cudaMemcpyAsync(stage, bias, (size_t)c->n * 8, cudaMemcpyHostToDevice, st), "upload bias");
@@ -914,6 +940,21 @@ static ckks_status layer_from_coeffs(ckks_ctx* c, const int64_t* diag, const int
     cuda_ok(cudaStreamSynchronize(st), "layer upload");
     *out = ly;
     return CKKS_OK;
+}
+
+static ckks_status layer_from_coeffs(ckks_ctx* c, const int64_t* diag, const int64_t* bias, uint32_t rows,
+                                     uint32_t cols, uint32_t level, double pt_scale, double bias_scale, void* dev_buf,
+                                     void* stream, ckks_layer** out, uint32_t region = 0, uint32_t items = 1)
+{
+    uint32_t t, t1, t2;
+    bsgs_split(rows, cols, t, t1, t2);
+    if (2 * t > (uint32_t)c->n / 2) throw CkksError(CKKS_E_PARAM, "2t exceeds the slot count");
+    if (t1 > 32 || t2 > 32) throw CkksError(CKKS_E_PARAM, "t1, t2 <= 32 supported (t <= 1024)");
+    std::vector<int32_t> baby(t1);
+    for (uint32_t j = 0; j < t1; ++j) baby[j] = (int32_t)j;
+    ckks_layer_desc d{CKKS_LAYER_DENSE, rows, cols, t, t2, t1, baby.data(), (int32_t)t1, region, items, level,
+                      pt_scale, bias_scale};
+    return layer_general(c, &d, diag, bias, dev_buf, stream, out);
 }
 
 ckks_status ckks_layer_import(ckks_ctx* c, const int64_t* diag_coeffs, const int64_t* bias_coeffs, uint32_t rows,
@@ -928,8 +969,17 @@ ckks_status ckks_layer_import(ckks_ctx* c, const int64_t* diag_coeffs, const int
     })
 }
 
-ckks_status ckks_layer_create(ckks_ctx* c, const double* W, uint32_t rows, uint32_t cols, const double* bias,
-                              uint32_t level, double in_scale, void* dev_buf, void* stream, ckks_layer** out)
+// library-side encodings of the layer plaintexts (NEXT f-2 packing R25: one copy per item region)
+static void put_regions(std::vector<double>& v, const double* vals, uint32_t len, uint32_t region, uint32_t items,
+                        uint32_t offset)
+{
+    for (uint32_t r = 0; r < items; ++r)
+        for (uint32_t s = 0; s < len; ++s) v[(size_t)r * region + offset + s] = vals[s];
+}
+
+ckks_status ckks_dense_create_packed(ckks_ctx* c, const double* W, uint32_t rows, uint32_t cols, const double* bias,
+                                     uint32_t region, uint32_t items, uint32_t level, double in_scale, void* dev_buf,
+                                     void* stream, ckks_layer** out)
 {
     CK_TRY({
         if (!c || !W || !dev_buf || !out) throw CkksError(CKKS_E_PARAM, "null");
@@ -937,29 +987,119 @@ ckks_status ckks_layer_create(ckks_ctx* c, const double* W, uint32_t rows, uint3
         uint32_t t, t1, t2;
         bsgs_split(rows, cols, t, t1, t2);
         const int n = c->n, slots = n / 2;
-        if (2 * t > (uint32_t)slots) throw CkksError(CKKS_E_PARAM, "2t exceeds the slot count");
+        if (items < 1) items = 1;
+        if (items == 1 && region == 0) region = 2 * t;
+        if (2 * t > region || (size_t)region * items > (size_t)slots)
+            throw CkksError(CKKS_E_PARAM, "regions must hold 2t slots and fit the slot vector");
         const double ptscale = (double)c->primes[level];
         std::vector<int64_t> coeffs((size_t)t * n);
-        std::vector<double> v(slots);
+        std::vector<double> v(slots), dg(t);
         for (uint32_t i = 0; i < t; ++i) {
-            // diag'_i = rot_{-floor(i/t1) t1}(diag_i): slots [k t1, k t1 + t) (R4)
+            // diag'_i = rot_{-floor(i/t1) t1}(diag_i): slots [k t1, k t1 + t) of every item (R4)
             std::fill(v.begin(), v.end(), 0.0);
             const uint32_t k = i / t1;
             for (uint32_t s = 0; s < t; ++s) {
                 const uint32_t col = (s + i) % t;
-                v[k * t1 + s] = (s < rows && col < cols) ? W[(size_t)s * cols + col] : 0.0;
+                dg[s] = (s < rows && col < cols) ? W[(size_t)s * cols + col] : 0.0;
             }
+            put_regions(v, dg.data(), t, region, items, k * t1);
             encode_host(n, v.data(), slots, ptscale, coeffs.data() + (size_t)i * n);
         }
         std::vector<int64_t> bcoef;
         if (bias) {
             std::fill(v.begin(), v.end(), 0.0);
-            for (uint32_t s = 0; s < rows; ++s) v[s] = bias[s];
+            put_regions(v, bias, rows, region, items, 0);
             bcoef.resize(n);
             encode_host(n, v.data(), slots, in_scale, bcoef.data());
         }
         return layer_from_coeffs(c, coeffs.data(), bias ? bcoef.data() : nullptr, rows, cols, level, ptscale,
-                                 in_scale, dev_buf, stream, out);
+                                 in_scale, dev_buf, stream, out, region, items);
+    })
+}
+
+ckks_status ckks_layer_create(ckks_ctx* c, const double* W, uint32_t rows, uint32_t cols, const double* bias,
+                              uint32_t level, double in_scale, void* dev_buf, void* stream, ckks_layer** out)
+{
+    return ckks_dense_create_packed(c, W, rows, cols, bias, 0, 1, level, in_scale, dev_buf, stream, out);
+}
+
+ckks_status ckks_layer_general_sizes(const ckks_ctx* c, uint32_t n_plaintexts, uint32_t level, size_t* bytes)
+{
+    if (!c || !bytes || n_plaintexts == 0) return fail(CKKS_E_PARAM, "null");
+    *bytes = layer_dev_bytes(c, n_plaintexts, level);
+    return CKKS_OK;
+}
+
+ckks_status ckks_layer_import_general(ckks_ctx* c, const ckks_layer_desc* desc, const int64_t* pt_coeffs,
+                                      const int64_t* bias_coeffs, void* dev_buf, void* stream, ckks_layer** out)
+{
+    CK_TRY({
+        if (!c || !desc || !pt_coeffs || !dev_buf || !out) throw CkksError(CKKS_E_PARAM, "null");
+        return layer_general(c, desc, pt_coeffs, bias_coeffs, dev_buf, stream, out);
+    })
+}
+
+// R26: taps ordered centre first (step 0), then i - c for the others; m_i = w_i on every item's [rR, rR + t)
+ckks_status ckks_conv1d_create(ckks_ctx* c, const double* w, uint32_t f, double bias, uint32_t t, uint32_t region,
+                               uint32_t items, uint32_t level, double in_scale, void* dev_buf, void* stream,
+                               ckks_layer** out)
+{
+    CK_TRY({
+        if (!c || !w || !dev_buf || !out || f < 1 || f > 32 || (f & 1) == 0) throw CkksError(CKKS_E_PARAM, "conv1d: odd f in [1, 31]");
+        if (level < 1 || (int)level >= c->L) throw CkksError(CKKS_E_LEVEL, "layer level must be in [1, L-1]");
+        const int n = c->n, slots = n / 2;
+        const uint32_t cc = (f - 1) / 2;
+        if (items < 1) items = 1;
+        if (region == 0) region = 2 * t + cc;
+        if (t + cc > region || (size_t)region * items > (size_t)slots) throw CkksError(CKKS_E_PARAM, "conv1d: regions");
+        const double ptscale = (double)c->primes[level];
+        std::vector<int32_t> steps;
+        std::vector<uint32_t> order;
+        order.push_back(cc);
+        for (uint32_t i = 0; i < f; ++i)
+            if (i != cc) order.push_back(i);
+        std::vector<int64_t> coeffs((size_t)f * n);
+        std::vector<double> v(slots), tap(t);
+        for (uint32_t o = 0; o < f; ++o) {
+            steps.push_back((int32_t)order[o] - (int32_t)cc);
+            std::fill(v.begin(), v.end(), 0.0);
+            std::fill(tap.begin(), tap.end(), w[order[o]]);
+            put_regions(v, tap.data(), t, region, items, 0);
+            encode_host(n, v.data(), slots, ptscale, coeffs.data() + (size_t)o * n);
+        }
+        std::vector<int64_t> bcoef(n);
+        std::fill(v.begin(), v.end(), 0.0);
+        std::fill(tap.begin(), tap.end(), bias);
+        put_regions(v, tap.data(), t, region, items, 0);
+        encode_host(n, v.data(), slots, in_scale, bcoef.data());
+        ckks_layer_desc d{CKKS_LAYER_CONV1D, t, t, t, 1, f, steps.data(), 0, region, items, level, ptscale, in_scale};
+        return layer_general(c, &d, coeffs.data(), bcoef.data(), dev_buf, stream, out);
+    })
+}
+
+// R27: out[k] = (1/f) sum_{i<f} x[k - i] on [f-1, t) of each item; steps 0, -1, .., -(f-1)
+ckks_status ckks_avgpool_create(ckks_ctx* c, uint32_t f, uint32_t t, uint32_t region, uint32_t items, uint32_t level,
+                                void* dev_buf, void* stream, ckks_layer** out)
+{
+    CK_TRY({
+        if (!c || !dev_buf || !out || f < 1 || f > 32 || f > t) throw CkksError(CKKS_E_PARAM, "avgpool: 1 <= f <= min(32, t)");
+        if (level < 1 || (int)level >= c->L) throw CkksError(CKKS_E_LEVEL, "layer level must be in [1, L-1]");
+        const int n = c->n, slots = n / 2;
+        if (items < 1) items = 1;
+        if (region == 0) region = 2 * t;
+        if (t > region || (size_t)region * items > (size_t)slots) throw CkksError(CKKS_E_PARAM, "avgpool: regions");
+        const double ptscale = (double)c->primes[level];
+        std::vector<double> v(slots, 0.0), m(t - (f - 1), 1.0 / f);
+        put_regions(v, m.data(), t - (f - 1), region, items, f - 1);
+        std::vector<int64_t> one(n), coeffs((size_t)f * n);
+        encode_host(n, v.data(), slots, ptscale, one.data());
+        std::vector<int32_t> steps;
+        for (uint32_t i = 0; i < f; ++i) {
+            steps.push_back(-(int32_t)i);
+            std::copy(one.begin(), one.end(), coeffs.begin() + (size_t)i * n);
+        }
+        ckks_layer_desc d{CKKS_LAYER_AVGPOOL, t, t, t, 1, f, steps.data(), 0, region, items, level, ptscale, 0.0};
+        return layer_general(c, &d, coeffs.data(), nullptr, dev_buf, stream, out);
     })
 }
 
@@ -992,17 +1132,19 @@ static void matvec_chunk(ckks_ctx* c, const ckks_layer* ly, const u64* in, size_
         std::vector<int64_t> steps;
         std::vector<u64*> outs;
         for (uint32_t j = 1; j < ly->t1; ++j) {
-            steps.push_back((int64_t)j);
+            steps.push_back((int64_t)ly->baby[j]);
             outs.push_back(baby + (size_t)(j - 1) * B * ctw);
         }
-        rotate_hoisted_impl(c, in, in_stride, nl, B, steps.data(), (int)steps.size(), outs.data(), ctw, stream);
+        if (!steps.empty())
+            rotate_hoisted_impl(c, in, in_stride, nl, B, steps.data(), (int)steps.size(), outs.data(), ctw, stream);
     } else {
         for (uint32_t j = 1; j < ly->t1; ++j)
-            rotate_impl(c, in, in_stride, nl, B, (int64_t)j, baby + (size_t)(j - 1) * B * ctw, ctw, false, stream);
+            rotate_impl(c, in, in_stride, nl, B, (int64_t)ly->baby[j], baby + (size_t)(j - 1) * B * ctw, ctw, false,
+                        stream);
     }
     ck::bsgs_mac(L, ly->d_pts, in, in_stride, baby, Wk, (int)ly->t1, (int)ly->t2, B, nl);
     for (uint32_t k = 1; k < ly->t2; ++k)
-        rotate_impl(c, Wk + (size_t)k * B * ctw, ctw, nl, B, (int64_t)k * ly->t1, Wk, ctw, true, stream);
+        rotate_impl(c, Wk + (size_t)k * B * ctw, ctw, nl, B, (int64_t)k * ly->giant, Wk, ctw, true, stream);
     rescale_impl(c, Wk, ctw, 2, nl, B, out, out_stride, ly->d_bias, stream);
 }
 
@@ -1028,15 +1170,75 @@ ckks_status ckks_matvec_diag(ckks_ctx* c, const ckks_layer* ly, const ckks_ct* i
 }
 
 // ------------------------------------------------------------------------------------ model
-static size_t model_dev_words(const ckks_ctx* c, uint32_t n_layers, int32_t activation)
+static size_t stages_dev_words(const ckks_ctx* c, const ckks_stage* st, uint32_t n)
 {
-    return activation == 2 && n_layers > 1 ? (size_t)(n_layers - 1) * c->L * c->n + c->n : 0;
+    size_t cub = 0;
+    for (uint32_t i = 0; i < n; ++i) cub += st[i].activation == 2 ? 1 : 0;
+    return cub ? cub * c->L * c->n + c->n : 0;
+}
+
+static int stage_level_drop(int act) { return act == 1 ? 1 : act == 2 ? 2 : 0; }
+
+static ckks_model* build_model(ckks_ctx* c, const ckks_stage* st, uint32_t n, const int64_t* act_coeffs, void* dev_buf,
+                               void* stream)
+{
+    if (!st || n == 0) throw CkksError(CKKS_E_PARAM, "empty model");
+    int lvl = (int)st[0].layer->level;
+    for (uint32_t i = 0; i < n; ++i) {
+        if (!st[i].layer) throw CkksError(CKKS_E_PARAM, "null layer");
+        if (st[i].activation < 0 || st[i].activation > 2) throw CkksError(CKKS_E_PARAM, "activation 0|1|2");
+        if ((int)st[i].layer->level != lvl)
+            throw CkksError(CKKS_E_LEVEL, "stage " + std::to_string(i) + " encoded for the wrong level");
+        lvl -= 1 + stage_level_drop(st[i].activation);
+    }
+    if (lvl < 0) throw CkksError(CKKS_E_LEVEL, "model deeper than the chain");
+    const size_t dw = stages_dev_words(c, st, n);
+    if (dw && !dev_buf) throw CkksError(CKKS_E_PARAM, "cubic activation needs the model device buffer");
+    auto* m = new ckks_model();
+    m->activation = st[0].activation;
+    u64* next = (u64*)dev_buf;
+    int64_t* stage_buf = dw ? (int64_t*)((u64*)dev_buf + dw - c->n) : nullptr;
+    auto L = c->launch(stream);
+    cudaStream_t cs = (cudaStream_t)stream;
+    std::vector<int64_t> coef(c->n);
+    std::vector<double> v(c->n / 2);
+    for (uint32_t i = 0; i < n; ++i) {
+        m->layers.push_back(st[i].layer);
+        m->stages.push_back(Stage{st[i].layer, st[i].activation, st[i].replicate_t});
+        u64* dact = nullptr;
+        if (st[i].activation == 2) {
+            const ckks_layer* ly = st[i].layer;
+            const int l = (int)ly->level - 1;   // activation input level
+            if (l < 2) throw CkksError(CKKS_E_LEVEL, "cubic activation needs two more levels");
+            const double S = ly->bias_scale, ql = (double)c->primes[l], ql1 = (double)c->primes[l - 1];
+            const double S3 = (S * S / ql) * S / ql1;
+            const int64_t* src = act_coeffs ? act_coeffs + (size_t)i * c->n : nullptr;
+            if (!src) {
+                // c0 of Eq. 2 on the layer's valid output slots [rR, rR + rows) of every item (R23, R25)
+                std::fill(v.begin(), v.end(), 0.0);
+                const uint32_t R = ly->region ? ly->region : 2 * ly->t;
+                for (uint32_t r = 0; r < ly->items; ++r)
+                    for (uint32_t s = 0; s < ly->rows; ++s) v[(size_t)r * R + s] = 0.49383;
+                encode_host(c->n, v.data(), v.size(), S3, coef.data());
+                src = coef.data();
+            }
+            dact = next;
+            next += (size_t)c->L * c->n;
+            cuda_ok(cudaMemcpyAsync(stage_buf, src, (size_t)c->n * 8, cudaMemcpyHostToDevice, cs), "act upload");
+            ck::signed_to_ntt(L, stage_buf, dact, 1, l - 1);
+            cuda_ok(cudaStreamSynchronize(cs), "act upload");
+        }
+        m->d_act_stage.push_back(dact);
+    }
+    return m;
 }
 
 ckks_status ckks_model_sizes(const ckks_ctx* c, uint32_t n_layers, int32_t activation, size_t* bytes)
 {
     if (!c || !bytes) return fail(CKKS_E_PARAM, "null");
-    *bytes = align256(model_dev_words(c, n_layers, activation) * 8);
+    std::vector<ckks_stage> st(n_layers ? n_layers : 1);
+    for (uint32_t i = 0; i < n_layers; ++i) st[i].activation = (i + 1 < n_layers) ? activation : 0;
+    *bytes = align256(stages_dev_words(c, st.data(), n_layers) * 8);
     return CKKS_OK;
 }
 
@@ -1046,46 +1248,32 @@ ckks_status ckks_model_create(ckks_ctx* c, const ckks_layer* const* layers, uint
     CK_TRY({
         if (!c || !layers || !out || n_layers == 0) throw CkksError(CKKS_E_PARAM, "null/empty model");
         if (activation < 0 || activation > 2) throw CkksError(CKKS_E_PARAM, "activation 0|1|2");
-        int lvl = (int)layers[0]->level;
+        // dense_1 -> act -> replicate -> dense_2 -> ... (PAPER.md L118 shape, BASELINE cfg4)
+        std::vector<ckks_stage> st(n_layers);
         for (uint32_t i = 0; i < n_layers; ++i) {
-            if ((int)layers[i]->level != lvl)
-                throw CkksError(CKKS_E_LEVEL, "layer " + std::to_string(i) + " encoded for the wrong level");
-            lvl -= 1;
-            if (i + 1 < n_layers) lvl -= (activation == 1 ? 1 : activation == 2 ? 2 : 0);
+            st[i].layer = layers[i];
+            st[i].activation = (i + 1 < n_layers) ? activation : 0;
+            st[i].replicate_t = i > 0 ? layers[i]->t : 0;
         }
-        if (lvl < 0) throw CkksError(CKKS_E_LEVEL, "model deeper than the chain");
-        auto* m = new ckks_model();
-        m->activation = activation;
-        for (uint32_t i = 0; i < n_layers; ++i) m->layers.push_back(layers[i]);
-        if (model_dev_words(c, n_layers, activation)) {
-            if (!dev_buf) {
-                delete m;
-                throw CkksError(CKKS_E_PARAM, "cubic activation needs the model device buffer");
-            }
-            m->d_act = (u64*)dev_buf;
-            int64_t* stage = (int64_t*)(m->d_act + (size_t)(n_layers - 1) * c->L * c->n);
-            auto L = c->launch(stream);
-            cudaStream_t st = (cudaStream_t)stream;
-            std::vector<int64_t> coef(c->n);
-            std::vector<double> v(c->n / 2);
-            for (uint32_t i = 0; i + 1 < n_layers; ++i) {
-                const ckks_layer* ly = layers[i];
-                const int l = (int)ly->level - 1;   // activation input level
-                const double S = ly->bias_scale, ql = (double)c->primes[l], ql1 = (double)c->primes[l - 1];
-                const double S3 = (S * S / ql) * S / ql1;
-                const int64_t* src = act_coeffs ? act_coeffs + (size_t)i * c->n : nullptr;
-                if (!src) {
-                    std::fill(v.begin(), v.end(), 0.0);
-                    for (uint32_t r = 0; r < ly->rows; ++r) v[r] = 0.49383;   // c0 of Eq. 2 on valid slots
-                    encode_host(c->n, v.data(), v.size(), S3, coef.data());
-                    src = coef.data();
-                }
-                cuda_ok(cudaMemcpyAsync(stage, src, (size_t)c->n * 8, cudaMemcpyHostToDevice, st), "act upload");
-                ck::signed_to_ntt(L, stage, m->d_act + (size_t)i * c->L * c->n, 1, l - 1);
-                cuda_ok(cudaStreamSynchronize(st), "act upload");
-            }
-        }
-        *out = m;
+        *out = build_model(c, st.data(), n_layers, act_coeffs, dev_buf, stream);
+        (*out)->activation = activation;
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_model_stages_sizes(const ckks_ctx* c, const ckks_stage* stages, uint32_t n, size_t* bytes)
+{
+    if (!c || !stages || !bytes) return fail(CKKS_E_PARAM, "null");
+    *bytes = align256(stages_dev_words(c, stages, n) * 8);
+    return CKKS_OK;
+}
+
+ckks_status ckks_model_create_stages(ckks_ctx* c, const ckks_stage* stages, uint32_t n, const int64_t* act_coeffs,
+                                     void* dev_buf, void* stream, ckks_model** out)
+{
+    CK_TRY({
+        if (!c || !stages || !out || n == 0) throw CkksError(CKKS_E_PARAM, "null/empty model");
+        *out = build_model(c, stages, n, act_coeffs, dev_buf, stream);
         return CKKS_OK;
     })
 }
@@ -1172,7 +1360,7 @@ static void const_residues(ckks_ctx* c, int64_t m0, int nl, std::vector<u64>& ou
 
 static int64_t round_away(double x) { return (int64_t)((x < 0 ? -1.0 : 1.0) * std::floor(std::fabs(x) + 0.5)); }
 
-// One chunk of B ciphertexts through the model.  in: [B][2][l0+1][N]; out: final level.
+// One chunk of B ciphertexts through the model's stages.  in: [B][2][l0+1][N]; out: final level.
 static void forward_chunk(ckks_ctx* c, const ckks_model* m, const u64* in, size_t in_stride, int B, double in_scale,
                           u64* out, size_t out_stride, u64* work, void* stream, int* out_level, double* out_scale)
 {
@@ -1188,45 +1376,47 @@ static void forward_chunk(ckks_ctx* c, const ckks_model* m, const u64* in, size_
     const u64* cur = in;
     size_t cur_stride = in_stride;
     double scale = in_scale;
-    int level = (int)m->layers[0]->level;
-    const int nlay = (int)m->layers.size();
-    for (int li = 0; li < nlay; ++li) {
-        const ckks_layer* ly = m->layers[li];
+    int level = (int)m->stages[0].layer->level;
+    const int nst = (int)m->stages.size();
+    for (int si = 0; si < nst; ++si) {
+        const Stage& sg = m->stages[si];
+        const ckks_layer* ly = sg.layer;
         int nl = level + 1;
-        if (li > 0) {
+        if (sg.replicate_t) {
             // replicate: y + rot_{-t}(y)  (P:L116 duplicated layout)
             const size_t ctw = c->ct_words(nl);
             u64* rep = (cur == bufA) ? bufB : bufA;
             cuda_ok(cudaMemcpy2DAsync(rep, ctw * 8, cur, cur_stride * 8, ctw * 8, B, cudaMemcpyDeviceToDevice,
                                       (cudaStream_t)stream), "replicate copy");
-            rotate_impl(c, cur, cur_stride, nl, B, -(int64_t)ly->t, rep, ctw, true, stream);
+            rotate_impl(c, cur, cur_stride, nl, B, -(int64_t)sg.replicate_t, rep, ctw, true, stream);
             cur = rep;
             cur_stride = ctw;
         }
-        const bool last = (li == nlay - 1);
-        u64* dst = last ? out : ((cur == bufA) ? bufB : bufA);
-        const size_t dst_stride = last ? out_stride : c->ct_words(nl - 1);
+        const bool last = (si == nst - 1);
+        const bool to_out = last && sg.activation == 0;
+        u64* dst = to_out ? out : ((cur == bufA) ? bufB : bufA);
+        const size_t dst_stride = to_out ? out_stride : c->ct_words(nl - 1);
         matvec_chunk(c, ly, cur, cur_stride, B, dst, dst_stride, lwork, stream, m->hoisted != 0);
         scale = scale * ly->pt_scale / (double)c->primes[level];
         level -= 1;
         nl -= 1;
         cur = dst;
         cur_stride = dst_stride;
-        if (last) break;
-        if (m->activation == 1) {
+        if (sg.activation == 1) {
             // square: rescale(relin(z (x) z))
             const size_t w3 = c->ct_words(nl, 3), w2 = c->ct_words(nl);
             ck::tensor(L, cur, cur, cur_stride, bufC, w3, B, nl);
             relin_impl(c, bufC, w3, nl, B, bufD, w2, stream);
-            u64* nxt = (cur == bufA) ? bufB : bufA;
-            rescale_impl(c, bufD, w2, 2, nl, B, nxt, c->ct_words(nl - 1), nullptr, stream);
+            u64* nxt = last ? out : ((cur == bufA) ? bufB : bufA);
+            const size_t ns = last ? out_stride : c->ct_words(nl - 1);
+            rescale_impl(c, bufD, w2, 2, nl, B, nxt, ns, nullptr, stream);
             scale = scale * scale / (double)c->primes[level];
             level -= 1;
             cur = nxt;
-            cur_stride = c->ct_words(nl - 1);
-        } else if (m->activation == 2) {
+            cur_stride = ns;
+        } else if (sg.activation == 2) {
             // Eq. 2 cubic, schedule R23
-            const double c3 = -0.0061728, c2 = 0.092593, c1 = 0.59259, c0 = 0.49383;
+            const double c3 = -0.0061728, c2 = 0.092593, c1 = 0.59259;
             const double S = scale, ql = (double)c->primes[level], ql1 = (double)c->primes[level - 1];
             const size_t w3 = c->ct_words(nl, 3), w2 = c->ct_words(nl), w2m = c->ct_words(nl - 1),
                          w2mm = c->ct_words(nl - 2);
@@ -1247,8 +1437,7 @@ static void forward_chunk(ckks_ctx* c, const ckks_model* m, const u64* in, size_
             const_residues(c, round_away(c2 * S), nl - 1, res);
             cuda_ok(cudaMemcpyAsync(dres, res.data(), (nl - 1) * 8, cudaMemcpyHostToDevice, (cudaStream_t)stream), "c2");
             ck::add_scalar(L, bufD, w2m, dres, B, nl - 1);
-            // h = rescale(relin(z2 (x) a)) -> bufC region reused: tensor into bufC, relin into
-            // a scratch after the tensor, rescale into `h` (level l-2)
+            // h = rescale(relin(z2 (x) a)) (level l-2)
             ck::tensor(L, z2, bufD, w2m, bufC, c->ct_words(nl - 1, 3), B, nl - 1);
             u64* rl = other;   // z2 is dead after the tensor
             relin_impl(c, bufC, c->ct_words(nl - 1, 3), nl - 1, B, rl, w2m, stream);
@@ -1261,20 +1450,20 @@ static void forward_chunk(ckks_ctx* c, const ckks_model* m, const u64* in, size_
             ck::mul_scalar(L, z, cur_stride, bufC, w2, dres + 64, B, 2, nl);
             u64* g = other;   // z2 no longer needed
             rescale_impl(c, bufC, w2, 2, nl, B, g, w2m, nullptr, stream);
-            (void)c0;
             // h += drop(g): add the first nl-2 limbs of each component of g
             ck::add(L, h, w2mm, g, w2m, h, w2mm, B, 1, nl - 2);
             ck::add(L, h + (size_t)(nl - 2) * c->n, w2mm, g + (size_t)(nl - 1) * c->n, w2m, h + (size_t)(nl - 2) * c->n,
                     w2mm, B, 1, nl - 2);
             // + c0 on the valid slots (model plaintext, R23)
-            ck::add(L, h, w2mm, m->d_act + (size_t)li * c->L * c->n, 0, h, w2mm, B, 1, nl - 2);
-            // move h to bufA/bufB for the next layer
-            u64* nxt = (cur == bufA) ? bufB : bufA;
-            cuda_ok(cudaMemcpyAsync(nxt, h, (size_t)B * w2mm * 8, cudaMemcpyDeviceToDevice, (cudaStream_t)stream), "mv");
+            ck::add(L, h, w2mm, m->d_act_stage[si], 0, h, w2mm, B, 1, nl - 2);
+            u64* nxt = last ? out : ((cur == bufA) ? bufB : bufA);
+            const size_t ns = last ? out_stride : w2mm;
+            cuda_ok(cudaMemcpy2DAsync(nxt, ns * 8, h, w2mm * 8, w2mm * 8, B, cudaMemcpyDeviceToDevice,
+                                      (cudaStream_t)stream), "mv");
             scale = S3;
             level -= 2;
             cur = nxt;
-            cur_stride = w2mm;
+            cur_stride = ns;
         }
     }
     *out_level = level;
@@ -1283,11 +1472,8 @@ static void forward_chunk(ckks_ctx* c, const ckks_model* m, const u64* in, size_
 
 static int model_out_level(const ckks_model* m)
 {
-    int lvl = (int)m->layers[0]->level;
-    for (size_t i = 0; i < m->layers.size(); ++i) {
-        lvl -= 1;
-        if (i + 1 < m->layers.size()) lvl -= (m->activation == 1 ? 1 : m->activation == 2 ? 2 : 0);
-    }
+    int lvl = (int)m->stages[0].layer->level;
+    for (const auto& s : m->stages) lvl -= 1 + stage_level_drop(s.activation);
     return lvl;
 }
 
@@ -1297,7 +1483,7 @@ ckks_status ckks_encrypted_forward(ckks_ctx* c, const ckks_model* m, const ckks_
     CK_TRY({
         if (!c || !m || !out || !out->data || !work) throw CkksError(CKKS_E_PARAM, "null");
         check_ct(c, in);
-        if (in->level != m->layers[0]->level) throw CkksError(CKKS_E_SHAPE, "input level != first layer level");
+        if (in->level != m->stages[0].layer->level) throw CkksError(CKKS_E_SHAPE, "input level != first layer level");
         const int nl_in = (int)in->level + 1, ol = model_out_level(m);
         int lvl = 0;
         double sc = 0;
@@ -1321,7 +1507,7 @@ ckks_status ckks_encrypted_forward_host(ckks_ctx* c, const ckks_model* m, const 
 {
     CK_TRY({
         if (!c || !m || !h_in || !h_out || !work) throw CkksError(CKKS_E_PARAM, "null");
-        if (in_level != m->layers[0]->level) throw CkksError(CKKS_E_SHAPE, "input level != first layer level");
+        if (in_level != m->stages[0].layer->level) throw CkksError(CKKS_E_SHAPE, "input level != first layer level");
         const int nl_in = (int)in_level + 1, ol = model_out_level(m);
         const int Bmax = (int)c->max_batch;
         // device staging after the model workspace: [Bmax] input cts + [Bmax] output cts
