@@ -99,3 +99,30 @@ def uniform_residues(seed: int, moduli, shape_prefix, n: int, tag: int = 0) -> n
     for i, q in enumerate(moduli):
         out[..., i, :] = g.integers(0, q, size=tuple(shape_prefix) + (n,), dtype=np.uint64)
     return out
+
+
+# NEXT f-2: the paper's frozen stack at its Table 2 presets.  Synthetic weights
+# (the trained CryptoTL weights are not available); shapes are the paper's.
+P2_STACK = Config(
+    name="paper_p2_frozen_stack", log_n=14, data_bits=(60,) + (50,) * 6, special_bits=(60,), log2_scale=50,
+    batch=128, in_dim=768,
+    note="conv1d f=9 -> dense 768 + ReLU_approx -> avgpool 3 -> dense 766; N=16384, log q = 420, "
+         "log Delta = 50, p = 5 items per ciphertext (Table 2 p2)")
+P1_STACK = Config(
+    name="paper_p1_frozen_stack", log_n=13, data_bits=(40,) + (22,) * 6, special_bits=(46,), log2_scale=22,
+    batch=128, in_dim=768,
+    note="Table 2 p1 chain [40, 22x6 | 46] (log q = 218), N=8192, p = 2")
+
+
+def frozen_stack_weights(t: int = 768, seed: int = 0x5EED0004, f_conv: int = 9, f_pool: int = 3):
+    """conv w ~ N(0, 0.3^2), W1 ~ N(0, 1/t), W2 ~ N(0, 1/(t - f_pool + 1)), biases U[-0.1, 0.1]."""
+    tp = t - f_pool + 1
+    return {"conv_w": _rng(seed, "w", 10).normal(0, 0.3, f_conv), "conv_b": 0.01,
+            "W1": _rng(seed, "w", 11).normal(0, 1 / np.sqrt(t), (t, t)),
+            "b1": _rng(seed, "b", 11).uniform(-0.1, 0.1, t),
+            "W2": _rng(seed, "w", 12).normal(0, 1 / np.sqrt(tp), (tp, tp)),
+            "b2": _rng(seed, "b", 12).uniform(-0.1, 0.1, tp), "f_pool": f_pool}
+
+
+def frozen_stack_items(count: int, t: int = 768, seed: int = 0x5EED0005) -> np.ndarray:
+    return _rng(seed, "x", 20).uniform(-1.0, 1.0, size=(count, t))
