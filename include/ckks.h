@@ -132,6 +132,7 @@ ckks_status ckks_probe_read_all(ckks_ctx* ctx, char* json, size_t cap);
 /* In place over d = device [batch][limbs][N]; limb i is reduced modulo prime i.  Forward maps
  * coefficients (any residues in [0, q_i)) to NTT(a)[k] = sum_j a_j psi^{(2 brev(k)+1) j}
  * (bit-reversed order, R2); inverse is its exact inverse.  limbs <= n_data + n_special. */
+/* batch == 0 is a no-op (d may be NULL); limbs must be in [1, number of primes] else CKKS_E_SHAPE. */
 ckks_status ckks_ntt_fwd(ckks_ctx* ctx, uint64_t* d, uint32_t batch, uint32_t limbs, void* stream);
 ckks_status ckks_ntt_inv(ckks_ctx* ctx, uint64_t* d, uint32_t batch, uint32_t limbs, void* stream);
 

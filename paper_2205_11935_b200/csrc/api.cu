@@ -730,9 +730,10 @@ uint64_t ckks_galois_elt(const ckks_ctx* c, int32_t step) { return c ? c->galois
 static ckks_status ntt_impl(ckks_ctx* c, uint64_t* d, uint32_t batch, uint32_t limbs, void* stream, bool inv)
 {
     CK_TRY({
-        if (!c || !d) throw CkksError(CKKS_E_PARAM, "null");
+        if (!c) throw CkksError(CKKS_E_PARAM, "null context");
         if (limbs == 0 || (int)limbs > c->np) throw CkksError(CKKS_E_SHAPE, "limbs > number of primes");
-        if (batch == 0) return CKKS_OK;
+        if (batch == 0) return CKKS_OK;   // empty batch: no-op, d may be NULL
+        if (!d) throw CkksError(CKKS_E_PARAM, "null data");
         auto L = c->launch(stream);
         // grid.y is limited to 65535 CTAs: chunk the batch
         for (uint32_t b0 = 0; b0 < batch; b0 += 65535) {

@@ -1,0 +1,89 @@
+"""GPU edge cases: empty batch, degenerate layer shapes (t = 1, non-square, t = 1024 = max t1 x t2),
+the smallest ring (N = 1024), level-1 layers ending at level 0, the maximum limb count (16 primes)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+import oracle  # noqa: E402
+from oracle import circuits as OC  # noqa: E402
+from oracle import encoding as OE  # noqa: E402
+import synthetic as S  # noqa: E402
+from paper_2205_11935_b200 import ckks as G  # noqa: E402
+
+
+def u64(t):
+    return t.detach().cpu().numpy().view(np.uint64)
+
+
+def test_empty_batch_is_rejected():
+    g = G.Context(10, (40, 40), (45,), key_seed=1, rot_steps=(1,), max_batch=2)
+    empty = G.Ciphertext(torch.empty((0, 2, 2, g.n), dtype=torch.int64, device="cuda"), 1, 2.0 ** 30)
+    with pytest.raises(G.CkksError) as e:
+        g.rotate(empty, 1, out=g.empty_ct(1, 1))
+    assert e.value.status in (G.E_PARAM, G.E_SHAPE)   # rejected before any launch
+    t = torch.empty((0, 2, g.n), dtype=torch.int64, device="cuda")
+    g.ntt_fwd(t)   # an empty NTT batch is a no-op
+
+
+def test_max_limbs_ntt():
+    bits = (50,) * 15 + (60,)
+    g = G.Context(12, bits, (), want_relin=False, max_batch=1)
+    o = oracle.Context(12, bits, ())
+    x = S.uniform_residues(5, g.primes, (2,), g.n)
+    t = torch.from_numpy(x.view(np.int64)).cuda()
+    g.ntt_fwd(t)
+    got = u64(t)
+    for l in (0, 7, 15):
+        assert np.array_equal(got[1, l], o.ntt(x[1, l], l))
+    g.ntt_inv(t)
+    assert np.array_equal(u64(t), x)
+
+
+@pytest.mark.parametrize("shape,log_n", [((1, 1), 10), ((5, 3), 10), ((3, 17), 11), ((1024, 1024), 12)])
+def test_degenerate_and_max_layer_shapes(shape, log_n):
+    """t = 1 (no rotation at all), non-square, t = 1024 (t1 = t2 = 32, the largest tile)."""
+    rows, cols = shape
+    steps = OC.rotation_steps_for([shape])
+    bits = (50, 40, 40)
+    o = oracle.Context(log_n, bits, (50,))
+    o.keygen(9, steps)
+    g = G.Context(log_n, bits, (50,), key_seed=9, rot_steps=steps, max_batch=2)
+    rng = np.random.default_rng(rows * 31 + cols)
+    W = rng.normal(0, 1 / np.sqrt(cols), (rows, cols))
+    b = rng.uniform(-0.1, 0.1, rows)
+    lay = OC.encode_layer(o, W, b, o.top_level, 2.0 ** 30)
+    gl = G.Layer(g, rows, cols, lay.level, diag_coeffs=lay.diag_coeffs, bias_coeffs=lay.bias_coeffs,
+                 pt_scale=lay.pt_scale, bias_scale=lay.bias_scale)
+    x = rng.uniform(-1, 1, cols)
+    m = OE.encode(OC.pack_input(x, lay.t, o.n // 2), 2.0 ** 30, o.n)
+    ct = g.encrypt(np.stack([m, m]), 4, 0, 2.0 ** 30)
+    out = gl.matvec(ct)
+    for bb in range(2):
+        ref = OC.matvec(o, OC.Ct(o.encrypt(m, 4, bb), 2.0 ** 30), lay)
+        assert np.array_equal(u64(out.data)[bb], ref.data)
+    y = OE.decode(o.decrypt(u64(out.data)[0]), o.primes, out.scale, o.n)
+    assert np.max(np.abs(y[:rows] - (W @ x + b))) < 1e-3
+
+
+def test_smallest_ring_forward_to_level0():
+    """N = 1024, two layers with the square activation consuming the whole chain (ends at level 0)."""
+    cfg = S.Config(name="tiny", log_n=10, data_bits=(50, 40, 40, 40), special_bits=(50,), log2_scale=30,
+                   layers=((8, 16), (4, 8)), activation="square", in_dim=16, weight_std=(0.25, 0.35))
+    steps = OC.rotation_steps_for(cfg.layers)
+    o = oracle.Context(cfg.log_n, cfg.data_bits, cfg.special_bits)
+    o.keygen(cfg.key_seed, steps)
+    g = G.Context(cfg.log_n, cfg.data_bits, cfg.special_bits, key_seed=cfg.key_seed, rot_steps=steps, max_batch=1)
+    prob = S.dense_problem(cfg, batch=1)
+    D = 2.0 ** 30
+    layers = OC.encode_model(o, prob["W"], prob["b"], o.top_level, D, "square")
+    gl = [G.Layer(g, l.rows, l.cols, l.level, diag_coeffs=l.diag_coeffs, bias_coeffs=l.bias_coeffs,
+                  pt_scale=l.pt_scale, bias_scale=l.bias_scale) for l in layers]
+    model = G.Model(g, gl, G.ACT_SQUARE)
+    m = OE.encode(OC.pack_input(prob["x"][0], layers[0].t, o.n // 2), D, o.n)
+    out = model.forward(g.encrypt(m, 2, 0, D))
+    assert out.level == 0
+    ref = OC.forward(o, OC.Ct(o.encrypt(m, 2, 0), D), layers, "square")
+    assert np.array_equal(u64(out.data)[0], ref.data)
