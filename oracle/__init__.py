@@ -91,6 +91,13 @@ def _declare(L):
         "or_relinearize": (INT, [vp, u64p, INT, u64p]),
         "or_rotate": (INT, [vp, u64p, INT, I64, u64p]),
         "or_rotate_hoisted": (INT, [vp, u64p, INT, I64, u64p]),
+        "or_rotate_hoisted_qp": (INT, [vp, u64p, INT, I64, u64p]),
+        "or_rotate_qp": (INT, [vp, u64p, INT, I64, u64p]),
+        "or_moddown": (None, [vp, u64p, INT, INT, u64p]),
+        "or_lift_qp": (None, [vp, u64p, INT, INT, u64p]),
+        "or_plain_qp": (None, [vp, i64p, INT, u64p]),
+        "or_mul_plain_qp": (None, [vp, u64p, u64p, INT, u64p]),
+        "or_add_qp": (None, [vp, u64p, u64p, INT, INT, u64p]),
         "or_rescale": (INT, [vp, u64p, INT, INT, u64p]),
         "or_drop_level": (None, [vp, u64p, INT, INT, INT, u64p]),
     }
@@ -295,6 +302,58 @@ class Context:
         ct = np.ascontiguousarray(ct, dtype=np.uint64)
         out = np.empty_like(ct)
         _check(lib().or_rotate_hoisted(self._c, _p(ct), ct.shape[1] - 1, step, _p(out)), f"rotate_hoisted({step})")
+        return out
+
+    # ---- QP basis (double hoisting, R11c): [ncomp][l+2][N], last limb mod P
+    def rotate_hoisted_qp(self, ct, step):
+        """Baby step of R11c: hoisted rotation of a Q_l ciphertext left in the Q_l P basis."""
+        ct = np.ascontiguousarray(ct, dtype=np.uint64)
+        nl = ct.shape[1]
+        out = np.empty((2, nl + 1, self.n), dtype=np.uint64)
+        _check(lib().or_rotate_hoisted_qp(self._c, _p(ct), nl - 1, step, _p(out)), f"rotate_hoisted_qp({step})")
+        return out
+
+    def rotate_qp(self, w, step):
+        """Giant step of R11c: rotation of a Q_l P ciphertext, result in Q_l P."""
+        w = np.ascontiguousarray(w, dtype=np.uint64)
+        out = np.empty_like(w)
+        _check(lib().or_rotate_qp(self._c, _p(w), w.shape[1] - 2, step, _p(out)), f"rotate_qp({step})")
+        return out
+
+    def moddown(self, x):
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        ncomp, ne = x.shape[0], x.shape[1]
+        out = np.empty((ncomp, ne - 1, self.n), dtype=np.uint64)
+        lib().or_moddown(self._c, _p(x), ne - 2, ncomp, _p(out))
+        return out
+
+    def lift_qp(self, ct):
+        ct = np.ascontiguousarray(ct, dtype=np.uint64)
+        ncomp, nl = ct.shape[0], ct.shape[1]
+        out = np.empty((ncomp, nl + 1, self.n), dtype=np.uint64)
+        lib().or_lift_qp(self._c, _p(ct), nl - 1, ncomp, _p(out))
+        return out
+
+    def plain_qp(self, coeffs, level):
+        m = np.ascontiguousarray(coeffs, dtype=np.int64)
+        out = np.empty((level + 2, self.n), dtype=np.uint64)
+        lib().or_plain_qp(self._c, _p(m, i64p), level, _p(out))
+        return out
+
+    def mul_plain_qp(self, ct, pt):
+        ct = np.ascontiguousarray(ct, dtype=np.uint64)
+        pt = np.ascontiguousarray(pt, dtype=np.uint64)
+        assert pt.shape[0] == ct.shape[1]
+        out = np.empty_like(ct)
+        lib().or_mul_plain_qp(self._c, _p(ct), _p(pt), ct.shape[1] - 2, _p(out))
+        return out
+
+    def add_qp(self, a, b):
+        a = np.ascontiguousarray(a, dtype=np.uint64)
+        b = np.ascontiguousarray(b, dtype=np.uint64)
+        assert a.shape == b.shape
+        out = np.empty_like(a)
+        lib().or_add_qp(self._c, _p(a), _p(b), a.shape[1] - 2, a.shape[0], _p(out))
         return out
 
     def rescale(self, ct):

@@ -111,29 +111,43 @@ class OpCount:
         self.add = 0
 
 
-def matvec(ctx, ct: Ct, layer: EncodedLayer, ops: OpCount | None = None, hoisted: bool = False) -> Ct:
-    """Eq. 1 then one rescale (R7) then + bias (R-bias).  t1+t2-2 rotations, t pt-ct mults.
-    hoisted=True: the t1-1 baby-step rotations are hoisted (NEXT f-1, R11b)."""
-    l = ct.level
-    assert layer.level == l, "layer encoded for another level"
-    pts = [ctx.plain(layer.diag_coeffs[i], l) for i in range(layer.t)]
-    rot = ctx.rotate_hoisted if hoisted else ctx.rotate
-    baby = [ct.data] + [rot(ct.data, j) for j in range(1, layer.t1)]
+def _bsgs_sum(ctx, ct_data, level, t1, t2, giant, baby_steps, pt_coeffs, hoisted, ops):
+    """sum_k rot_{k giant}(sum_j pt_{k t1 + j} o rot_{baby_j}(x))  (Eq. 1), in the order of Eq. 1.
+    hoisted = 0: every rotation non-hoisted (R11); 1: baby steps hoisted (R11b); 2: double hoisting
+    (R11c) -- baby steps, inner sums and giant steps in the Q_l P basis, one ModDown at the end."""
+    l = level
+    if hoisted == 2:
+        baby = [ctx.lift_qp(ct_data) if s == 0 else ctx.rotate_hoisted_qp(ct_data, s) for s in baby_steps]
+        plain, mul, add, rot = ctx.plain_qp, ctx.mul_plain_qp, ctx.add_qp, ctx.rotate_qp
+    else:
+        r = ctx.rotate_hoisted if hoisted else ctx.rotate
+        baby = [ct_data if s == 0 else r(ct_data, s) for s in baby_steps]
+        plain, mul, add, rot = ctx.plain, ctx.mul_plain, ctx.add, ctx.rotate
     if ops:
-        ops.rot += layer.t1 - 1
+        ops.rot += sum(1 for s in baby_steps if s != 0)
     y = None
-    for k in range(layer.t2):
+    for k in range(t2):
         w = None
-        for j in range(layer.t1):
-            term = ctx.mul_plain(baby[j], pts[k * layer.t1 + j])
-            w = term if w is None else ctx.add(w, term)
+        for j in range(t1):
+            term = mul(baby[j], plain(pt_coeffs[k * t1 + j], l))
+            w = term if w is None else add(w, term)
             if ops:
                 ops.mul_plain += 1
         if k > 0:
-            w = ctx.rotate(w, k * layer.t1)
+            w = rot(w, k * giant)
             if ops:
                 ops.rot += 1
-        y = w if y is None else ctx.add(y, w)
+        y = w if y is None else add(y, w)
+    return ctx.moddown(y) if hoisted == 2 else y
+
+
+def matvec(ctx, ct: Ct, layer: EncodedLayer, ops: OpCount | None = None, hoisted: int = 0) -> Ct:
+    """Eq. 1 then one rescale (R7) then + bias (R-bias).  t1+t2-2 rotations, t pt-ct mults.
+    hoisted=1: the t1-1 baby-step rotations are hoisted (NEXT f-1, R11b); 2: double hoisting (R11c)."""
+    l = ct.level
+    assert layer.level == l, "layer encoded for another level"
+    y = _bsgs_sum(ctx, ct.data, l, layer.t1, layer.t2, layer.t1, list(range(layer.t1)), layer.diag_coeffs,
+                  int(hoisted), ops)
     y = ctx.rescale(y)
     out_scale = ct.scale * layer.pt_scale / float(ctx.primes[l])
     y = ctx.add_plain(y, ctx.plain(layer.bias_coeffs, l - 1))
@@ -355,27 +369,11 @@ def encode_pool(ctx, f, t, level, region, items) -> HoistedLayer:
     return HoistedLayer("pool", t, 1, [-i for i in range(f)], 0, level, q_l, 0.0, np.stack([m] * f), None, t, t)
 
 
-def apply_layer(ctx, ct: Ct, lay: HoistedLayer, hoisted: bool = True, ops: OpCount | None = None) -> Ct:
+def apply_layer(ctx, ct: Ct, lay: HoistedLayer, hoisted: int = 1, ops: OpCount | None = None) -> Ct:
     """y = sum_k rot_{k g}(sum_j pt_{k,j} o rot_{s_j}(x)), one rescale, + bias (Eq. 1 / R26 / R27)."""
     l = ct.level
     assert lay.level == l
-    rot = ctx.rotate_hoisted if hoisted else ctx.rotate
-    baby = [ct.data if s == 0 else rot(ct.data, s) for s in lay.baby_steps]
-    if ops:
-        ops.rot += sum(1 for s in lay.baby_steps if s != 0)
-    y = None
-    for k in range(lay.t2):
-        w = None
-        for j in range(lay.t1):
-            term = ctx.mul_plain(baby[j], ctx.plain(lay.pt_coeffs[k * lay.t1 + j], l))
-            w = term if w is None else ctx.add(w, term)
-            if ops:
-                ops.mul_plain += 1
-        if k > 0:
-            w = ctx.rotate(w, k * lay.giant)
-            if ops:
-                ops.rot += 1
-        y = w if y is None else ctx.add(y, w)
+    y = _bsgs_sum(ctx, ct.data, l, lay.t1, lay.t2, lay.giant, lay.baby_steps, lay.pt_coeffs, int(hoisted), ops)
     y = ctx.rescale(y)
     if lay.bias_coeffs is not None:
         y = ctx.add_plain(y, ctx.plain(lay.bias_coeffs, l - 1))

@@ -646,17 +646,16 @@ static u64 centered_mod(u64 r, u64 m, u64 q)
  *   3. inner product  u~_c[p] = sum_{j<=l} D_{j,p} key_j.c[p]   mod p
  *   4. ModDown: r = centered(iNTT_P(u~_c[P])),  u_c[i] = (u~_c[i] - NTT_{q_i}(r mod q_i)) P^{-1} mod q_i
  */
-static int ks_from_digits(const or_ctx* c, const int64_t* digit, int level, int64_t key_id, u64* out)
+/* steps 2-3 into the extended basis: out_qp [2][l+2][N], limb l+1 = P  (no ModDown) */
+static void ks_ip_qp(const or_ctx* c, const int64_t* digit, int level, int kidx, u64* acc)
 {
-    int kidx = find_key(c, key_id);
-    if (kidx < 0) return -3;
     int n = c->n, L = c->n_data, nl = level + 1, np_key = L + 1;
     const u64* key = c->key[kidx];
     int ext[OR_MAXP];
     for (int i = 0; i < nl; i++) ext[i] = i;
     ext[nl] = L;
     int ne = nl + 1;
-    u64* acc = (u64*)calloc((size_t)2 * ne * n, sizeof(u64));
+    memset(acc, 0, sizeof(u64) * (size_t)2 * ne * n);
     u64* D = (u64*)malloc(sizeof(u64) * n);
     for (int j = 0; j < nl; j++) {
         for (int e = 0; e < ne; e++) {
@@ -671,23 +670,40 @@ static int ks_from_digits(const or_ctx* c, const int64_t* digit, int level, int6
             }
         }
     }
+    free(D);
+}
+
+/* step 4 on one component: in [l+2][N] (QP basis) -> out [l+1][N] */
+static void moddown_comp(const or_ctx* c, const u64* in, int level, u64* out)
+{
+    int n = c->n, L = c->n_data, nl = level + 1;
     u64 P = c->q[L];
     u64* r = (u64*)malloc(sizeof(u64) * n);
     u64* t = (u64*)malloc(sizeof(u64) * n);
-    for (int comp = 0; comp < 2; comp++) {
-        memcpy(r, acc + ((size_t)comp * ne + nl) * n, sizeof(u64) * n);
-        or_intt(c, L, r);
-        for (int i = 0; i < nl; i++) {
-            u64 q = c->q[i];
-            u64 pinv = invmod(P % q, q);
-            for (int k = 0; k < n; k++) t[k] = centered_mod(r[k], P, q);
-            or_ntt(c, i, t);
-            const u64* a = acc + ((size_t)comp * ne + i) * n;
-            u64* o = out + ((size_t)comp * nl + i) * n;
-            for (int k = 0; k < n; k++) o[k] = mulmod(submod(a[k], t[k], q), pinv, q);
-        }
+    memcpy(r, in + (size_t)nl * n, sizeof(u64) * n);
+    or_intt(c, L, r);
+    for (int i = 0; i < nl; i++) {
+        u64 q = c->q[i];
+        u64 pinv = invmod(P % q, q);
+        for (int k = 0; k < n; k++) t[k] = centered_mod(r[k], P, q);
+        or_ntt(c, i, t);
+        const u64* a = in + (size_t)i * n;
+        u64* o = out + (size_t)i * n;
+        for (int k = 0; k < n; k++) o[k] = mulmod(submod(a[k], t[k], q), pinv, q);
     }
-    free(acc); free(D); free(r); free(t);
+    free(r); free(t);
+}
+
+static int ks_from_digits(const or_ctx* c, const int64_t* digit, int level, int64_t key_id, u64* out)
+{
+    int kidx = find_key(c, key_id);
+    if (kidx < 0) return -3;
+    int n = c->n, nl = level + 1, ne = nl + 1;
+    u64* acc = (u64*)malloc(sizeof(u64) * (size_t)2 * ne * n);
+    ks_ip_qp(c, digit, level, kidx, acc);
+    for (int comp = 0; comp < 2; comp++)
+        moddown_comp(c, acc + (size_t)comp * ne * n, level, out + (size_t)comp * nl * n);
+    free(acc);
     return 0;
 }
 
@@ -776,7 +792,7 @@ int or_rotate_hoisted(const or_ctx* c, const u64* ct, int level, int64_t step, u
     if (g == 1) { memcpy(out, ct, sizeof(u64) * 2 * h); return 0; }
     if (find_key(c, (int64_t)g) < 0) return -3;
     int64_t* digit = digits_of(c, ct + h, level);
-    int64_t* sd = (int64_t*)malloc(sizeof(int64_t) * (size_t)nl * n);
+    int64_t* sd = (int64_t*)calloc((size_t)nl * n, sizeof(int64_t));   /* sigma_g is a bijection */
     u64 two_n = 2ULL * (u64)n;
     for (int j = 0; j < nl; j++)
         for (u64 i = 0; i < (u64)n; i++) {
@@ -800,6 +816,138 @@ int or_rotate_hoisted(const or_ctx* c, const u64* ct, int level, int64_t step, u
     }
     free(digit); free(sd); free(u);
     return st;
+}
+
+/* ------------------------------------------------------------------ QP-basis (double hoisting, R11c) */
+/*
+ * NEXT f-1 second stage (R11c, "double hoisting"): the BSGS baby-step rotations are left in
+ * the extended basis Q_l P (no ModDown), the inner sums and the giant-step rotations are accumulated
+ * there, and ONE ModDown per layer brings the sum back to Q_l.  A QP ciphertext at level l has l+2
+ * limbs per component: q_0..q_l, then P.
+ */
+static u64 ext_q(const or_ctx* c, int level, int e) { return e <= level ? c->q[e] : c->q[c->n_data]; }
+
+/* step 4 (ModDown) on ncomp components: in [ncomp][l+2][N] -> out [ncomp][l+1][N] */
+void or_moddown(const or_ctx* c, const u64* in_qp, int level, int ncomp, u64* out)
+{
+    int n = c->n, nl = level + 1;
+    for (int comp = 0; comp < ncomp; comp++)
+        moddown_comp(c, in_qp + (size_t)comp * (nl + 1) * n, level, out + (size_t)comp * nl * n);
+}
+
+/* P * ct in the QP basis: residues P c mod q_i on the data limbs, 0 mod P */
+void or_lift_qp(const or_ctx* c, const u64* ct, int level, int ncomp, u64* out)
+{
+    int n = c->n, nl = level + 1;
+    u64 P = c->q[c->n_data];
+    for (int comp = 0; comp < ncomp; comp++) {
+        for (int i = 0; i < nl; i++)
+            for (int k = 0; k < n; k++)
+                out[((size_t)comp * (nl + 1) + i) * n + k] = mulmod(ct[((size_t)comp * nl + i) * n + k], P % c->q[i], c->q[i]);
+        memset(out + ((size_t)comp * (nl + 1) + nl) * n, 0, sizeof(u64) * n);
+    }
+}
+
+/* plaintext of integer coefficients m over q_0..q_l, P (NTT form) */
+void or_plain_qp(const or_ctx* c, const int64_t* m, int level, u64* out)
+{
+    int n = c->n, nl = level + 1;
+    for (int e = 0; e <= nl; e++) {
+        int p = e < nl ? e : c->n_data;
+        u64* o = out + (size_t)e * n;
+        for (int k = 0; k < n; k++) o[k] = from_signed(m[k], c->q[p]);
+        or_ntt(c, p, o);
+    }
+}
+
+void or_mul_plain_qp(const or_ctx* c, const u64* ct, const u64* pt, int level, u64* out)
+{
+    int n = c->n, ne = level + 2;
+    for (int comp = 0; comp < 2; comp++)
+        for (int e = 0; e < ne; e++) {
+            u64 q = ext_q(c, level, e);
+            for (int k = 0; k < n; k++) {
+                size_t idx = ((size_t)comp * ne + e) * n + k;
+                out[idx] = mulmod(ct[idx], pt[(size_t)e * n + k], q);
+            }
+        }
+}
+
+void or_add_qp(const or_ctx* c, const u64* a, const u64* b, int level, int ncomp, u64* out)
+{
+    int n = c->n, ne = level + 2;
+    for (int comp = 0; comp < ncomp; comp++)
+        for (int e = 0; e < ne; e++) {
+            u64 q = ext_q(c, level, e);
+            for (int k = 0; k < n; k++) {
+                size_t idx = ((size_t)comp * ne + e) * n + k;
+                out[idx] = addmod(a[idx], b[idx], q);
+            }
+        }
+}
+
+/* Baby step (R11c): the hoisted rotation of R11b without its ModDown,
+ *   (P sigma_g(c0) + sum_j ModUp(d'_j) gk_j.c0,  sum_j ModUp(d'_j) gk_j.c1)  over Q_l P,
+ * d'_j = sigma_g(d_j) as signed integers, d_j = iNTT_{q_j}(c1[j]).  step 0: P ct. */
+int or_rotate_hoisted_qp(const or_ctx* c, const u64* ct, int level, int64_t step, u64* out)
+{
+    int n = c->n, nl = level + 1, ne = nl + 1;
+    size_t h = (size_t)nl * n;
+    u64 g = or_galois_elt(c, step);
+    if (g == 1) { or_lift_qp(c, ct, level, 2, out); return 0; }
+    int kidx = find_key(c, (int64_t)g);
+    if (kidx < 0) return -3;
+    int64_t* digit = digits_of(c, ct + h, level);
+    int64_t* sd = (int64_t*)calloc((size_t)nl * n, sizeof(int64_t));   /* sigma_g is a bijection */
+    u64 two_n = 2ULL * (u64)n;
+    for (int j = 0; j < nl; j++)
+        for (u64 i = 0; i < (u64)n; i++) {
+            u64 e = (i * g) % two_n;
+            int64_t v = digit[(size_t)j * n + i];
+            if (e < (u64)n) sd[(size_t)j * n + e] = v;
+            else sd[(size_t)j * n + (e - n)] = -v;
+        }
+    ks_ip_qp(c, sd, level, kidx, out);
+    u64 P = c->q[c->n_data];
+    u64* rc0 = (u64*)malloc(sizeof(u64) * n);
+    for (int p = 0; p < nl; p++) {
+        u64 q = c->q[p];
+        or_automorphism_ntt(c, p, ct + (size_t)p * n, g, rc0);
+        u64* o = out + (size_t)p * n;                       /* component 0, limb p */
+        for (int k = 0; k < n; k++) o[k] = addmod(o[k], mulmod(rc0[k], P % q, q), q);
+    }
+    (void)ne;
+    free(rc0); free(digit); free(sd);
+    return 0;
+}
+
+/* Giant step (R11c) on a QP ciphertext w:
+ *   c1' = ModDown(w.c1),  digits d_j = iNTT_{q_j}(sigma_g(c1')[j])  (unsigned, as R9),
+ *   (sigma_g(w.c0) + sum_j ModUp(d_j) gk_j.c0,  sum_j ModUp(d_j) gk_j.c1)  over Q_l P.  step 0: w. */
+int or_rotate_qp(const or_ctx* c, const u64* w, int level, int64_t step, u64* out)
+{
+    int n = c->n, nl = level + 1, ne = nl + 1;
+    size_t hq = (size_t)ne * n, h = (size_t)nl * n;
+    u64 g = or_galois_elt(c, step);
+    if (g == 1) { memcpy(out, w, sizeof(u64) * 2 * hq); return 0; }
+    int kidx = find_key(c, (int64_t)g);
+    if (kidx < 0) return -3;
+    u64* c1 = (u64*)malloc(sizeof(u64) * h);
+    moddown_comp(c, w + hq, level, c1);
+    u64* rc1 = (u64*)malloc(sizeof(u64) * h);
+    for (int p = 0; p < nl; p++) or_automorphism_ntt(c, p, c1 + (size_t)p * n, g, rc1 + (size_t)p * n);
+    int64_t* digit = digits_of(c, rc1, level);
+    ks_ip_qp(c, digit, level, kidx, out);
+    u64* r0 = (u64*)malloc(sizeof(u64) * n);
+    for (int e = 0; e < ne; e++) {
+        int p = e < nl ? e : c->n_data;
+        u64 q = c->q[p];
+        or_automorphism_ntt(c, p, w + (size_t)e * n, g, r0);
+        u64* o = out + (size_t)e * n;
+        for (int k = 0; k < n; k++) o[k] = addmod(o[k], r0[k], q);
+    }
+    free(c1); free(rc1); free(digit); free(r0);
+    return 0;
 }
 
 /* Rescale (R10, "rescaling ... equivalent to rounding"):
