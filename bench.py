@@ -42,7 +42,10 @@ def parse():
     p.add_argument("--no-extras", action="store_true", help="skip the cfg2/cfg3 sub-benchmarks")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--no-hoist", action="store_true", help="non-hoisted baby steps (SEAL semantics, R11)")
+    p.add_argument("--hoisting", type=int, default=2, choices=(0, 1, 2),
+                   help="rotation schedule: 0 non-hoisted (SEAL semantics, R11), 1 hoisted baby steps (R11b), "
+                        "2 double hoisting (R11c, default)")
+    p.add_argument("--no-hoist", action="store_true", help="same as --hoisting 0")
     return p.parse_args()
 
 
@@ -199,7 +202,8 @@ def run_ours(args):
     device = torch.device("cuda", local)
     cfg = S.CFG5
     B = args.batch or cfg.batch
-    ctx, model, ct, prob = build_forward(G, cfg, B, args.max_batch, device, hoisted=not args.no_hoist)
+    hoisting = 0 if args.no_hoist else args.hoisting
+    ctx, model, ct, prob = build_forward(G, cfg, B, args.max_batch, device, hoisted=hoisting)
     out = ctx.empty_ct(B, model.final_level)
     work = torch.empty(model.work_bytes(B), dtype=torch.uint8, device=device)
     stream = torch.cuda.current_stream()
@@ -264,7 +268,8 @@ def run_ours(args):
               "config": {"workload": cfg.name, "batch_per_gpu": B, "N": ctx.n, "limbs": ctx.n_data,
                          "special_primes": ctx.n_special, "dnum": ctx.n_data, "layers": [list(s) for s in cfg.layers],
                          "activation": "square", "max_batch": args.max_batch,
-                         "baby_steps": "non-hoisted (R11)" if args.no_hoist else "hoisted (NEXT f-1, R11b)",
+                         "baby_steps": {0: "non-hoisted (R11)", 1: "hoisted (NEXT f-1, R11b)",
+                                        2: "double hoisting (NEXT f-1, R11c)"}[hoisting],
                          "l2": "inputs (2 GiB of ciphertexts) larger than L2; no flush",
                          "parallelism": f"replicas x{world}"},
               "gpu_launches": launches, "roofline": roofline,
@@ -321,7 +326,7 @@ def run_ours(args):
 def bench_frozen_stack(G, S, device, args):
     """NEXT f-2: the paper's frozen stack (conv 9 -> dense 768 + ReLU_approx -> pool 3 -> dense 766,
     depth 6) at the Table 2 p2 preset (N=16384, log q=420, log Delta=50, p=5 items per ciphertext),
-    library encoders, hoisted baby steps.  Paper context: 2.56 s per forward (5 items) single-thread
+    library encoders, the main line's rotation schedule.  Paper context: 2.56 s per forward (5 items) single-thread
     SEAL+HEXL."""
     import torch
     cfg = S.P2_STACK
@@ -348,7 +353,7 @@ def bench_frozen_stack(G, S, device, args):
     W2[:, f_pool - 1:] = wts["W2"]
     d2 = G.GeneralLayer.dense(ctx, W2, wts["b2"], R, p, l0 - 5, S3)
     model = G.Model.from_stages(ctx, [(conv, 0, 0), (d1, 2, t), (pool, 0, 0), (d2, 0, t)])
-    model.set_hoisting(True)
+    model.set_hoisting(0 if args.no_hoist else args.hoisting)
     xs = S.frozen_stack_items(B * p, t)
     ms = np.empty((B, ctx.n), dtype=np.int64)
     for b in range(B):

@@ -192,6 +192,12 @@ ckks_status ckks_layer_import_general(ckks_ctx* ctx, const ckks_layer_desc* desc
                                       const int64_t* bias_coeffs, void* dev_buf, void* stream, ckks_layer** out);
 /* Workspace (device bytes) ckks_matvec_diag / ckks_encrypted_forward need for `batch` cts. */
 ckks_status ckks_layer_work_sizes(const ckks_ctx* ctx, const ckks_layer* layer, uint32_t batch, size_t* bytes);
+/* Rotation schedule ckks_matvec_diag uses for this layer: 0 = every rotation
+ * non-hoisted (R11, default); 1 = baby steps hoisted (R11b); 2 = double hoisting (R11c): baby steps,
+ * inner sums and giant steps stay in the Q_l P basis and one ModDown per layer returns to Q_l.  The three
+ * give different residues (different rounding points) that decrypt to the same slots.  CKKS_E_PARAM
+ * for any other mode. */
+ckks_status ckks_layer_set_hoisting(ckks_layer* layer, int32_t mode);
 /* y = sum_k rot_{k t1}(sum_j diag'_{k t1+j} o rot_j(x)) (Eq. 1), one rescale (R7), + bias.
  * in at the layer's level; out at level-1, scale = in scale.  work: ckks_layer_work_sizes bytes. */
 ckks_status ckks_matvec_diag(ckks_ctx* ctx, const ckks_layer* layer, const ckks_ct* in, ckks_ct* out, void* work,
@@ -213,7 +219,8 @@ ckks_status ckks_model_stages_sizes(const ckks_ctx* ctx, const ckks_stage* stage
 ckks_status ckks_model_create_stages(ckks_ctx* ctx, const ckks_stage* stages, uint32_t n, const int64_t* act_coeffs,
                                      void* dev_buf, void* stream, ckks_model** out);
 void ckks_model_destroy(ckks_model* model);
-/* on != 0: the baby-step rotations of every dense layer are hoisted (ckks_rotate_hoisted semantics). */
+/* Rotation schedule of every layer of the model, as ckks_layer_set_hoisting: 0 none, 1 hoisted baby
+ * steps (ckks_rotate_hoisted semantics), 2 double hoisting (R11c).  CKKS_E_PARAM for other values. */
 ckks_status ckks_model_set_hoisting(ckks_model* model, int32_t on);
 /* BSGS split of a rows x cols layer: t = max(rows, cols) padded to a multiple of
  * t1 = 2^ceil(ceil(log2 t)/2), t2 = t / t1 (R5). */

@@ -83,6 +83,7 @@ SIGNATURES = {
     "ckks_model_stages_sizes": (_I, [_VP, ctypes.POINTER(ckks_stage), _U32, _PSZ]),
     "ckks_model_create_stages": (_I, [_VP, ctypes.POINTER(ckks_stage), _U32, _VP, _VP, _VP, ctypes.POINTER(_VP)]),
     "ckks_model_set_hoisting": (_I, [_VP, _I]),
+    "ckks_layer_set_hoisting": (_I, [_VP, _I]),
     "ckks_relinearize": (_I, [_VP, _PCT, _PCT, _VP]),
     "ckks_rescale": (_I, [_VP, _PCT, _PCT, _VP]),
     "ckks_add": (_I, [_VP, _PCT, _PCT, _PCT, _VP]),
@@ -406,6 +407,11 @@ class Layer:
         _check(lib().ckks_layer_work_sizes(self.ctx.h, self.h, batch, ctypes.byref(nb)), "ckks_layer_work_sizes")
         return nb.value
 
+    def set_hoisting(self, mode=1):
+        """Rotation schedule of matvec: 0 none, 1 hoisted baby steps (R11b), 2 double hoisting (R11c)."""
+        _check(lib().ckks_layer_set_hoisting(self.h, int(mode)), "ckks_layer_set_hoisting")
+        return self
+
     def matvec(self, ct, out=None, work=None, stream=None):
         ctx = self.ctx
         out = out or ctx.empty_ct(ct.batch, ct.level - 1)
@@ -536,9 +542,11 @@ class Model:
         self.final_level = self.in_level - sum(1 + depth[int(a)] for _, a, _ in stages)
         return self
 
-    def set_hoisting(self, on=True):
-        _check(lib().ckks_model_set_hoisting(self.h, 1 if on else 0), "ckks_model_set_hoisting")
-        self.hoisted = bool(on)
+    def set_hoisting(self, mode=1):
+        """0 none, 1 (or True) hoisted baby steps (R11b), 2 double hoisting (R11c)."""
+        mode = int(mode)
+        _check(lib().ckks_model_set_hoisting(self.h, mode), "ckks_model_set_hoisting")
+        self.hoisted = mode
 
     def work_bytes(self, batch):
         nb = ctypes.c_size_t()

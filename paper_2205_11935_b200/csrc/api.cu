@@ -265,7 +265,8 @@ struct ckks_layer {
     int32_t giant = 0;
     uint32_t region = 0, items = 1;
     double pt_scale, bias_scale;
-    u64* d_pts;     // [t2 * t1][level+1][N]
+    u64* d_pts;     // [t2 * t1][level+2][N]  (limb level+1: mod P, for the double-hoisted Q_l P MAC)
+    int hoisting = 0;   // ckks_matvec_diag: 0 plain, 1 hoisted baby steps, 2 double hoisting
     u64* d_bias;    // [level][N] or null
 };
 
@@ -280,7 +281,7 @@ struct ckks_model {
     std::vector<Stage> stages;
     std::vector<u64*> d_act_stage;   // per stage: masked c0 plaintext of a cubic activation (or null)
     int activation;
-    int hoisted = 0;        // baby-step rotations hoisted (NEXT f-1)
+    int hoisted = 0;        // 0 none, 1 hoisted baby steps (R11b), 2 double hoisting (R11c)  (NEXT f-1)
 };
 
 namespace {
@@ -382,6 +383,68 @@ void rotate_hoisted_impl(ckks_ctx* c, const u64* in, size_t in_stride, int nl, i
         }
         flush();
     }
+}
+
+// Double hoisting (R11c) baby steps: hoisted rotations of a Q_l input left in the Q_l P basis,
+// out_s = sigma_g(P c0 + sum_j D_j key'_j) over nl+1 limbs; batch <= max_batch.
+void rotate_hoisted_qp_impl(ckks_ctx* c, const u64* in, size_t in_stride, int nl, int B, const int64_t* steps,
+                            int n_steps, u64* const* outs, size_t out_stride, void* stream)
+{
+    auto L = c->launch(stream);
+    for (int s = 0; s < n_steps; ++s) {
+        const uint32_t g = c->galois(steps[s]);
+        if (g != 1 && !c->key_perm((int64_t)g))
+            throw CkksError(CKKS_E_NOKEY, "no Galois key for step " + std::to_string(steps[s]));
+    }
+    ck::KsIn ki{in, in_stride, (size_t)nl * c->n, 0};
+    auto w = c->ks_work(B);
+    bool have_modup = false;
+    ck::KsGroup grp{};
+    grp.G = 0;
+    auto flush = [&]() {
+        if (!grp.G) return;
+        ck::KsOut ko{nullptr, out_stride, in, in_stride, 0, 0, 0};
+        ck::keyswitch_finish_qp(L, ki, grp, B, nl, w, ko, true);
+        grp.G = 0;
+    };
+    for (int s = 0; s < n_steps; ++s) {
+        const uint32_t g = c->galois(steps[s]);
+        if (g == 1) {
+            ck::lift_qp(L, in, in_stride, outs[s], out_stride, B, nl);
+            continue;
+        }
+        if (!have_modup) {
+            ck::keyswitch_modup(L, ki, B, nl, w, false);
+            have_modup = true;
+        }
+        grp.key[grp.G] = c->key_perm((int64_t)g);
+        grp.out[grp.G] = outs[s];
+        grp.scatter[grp.G] = g;
+        grp.ginv[grp.G] = c->galois_inv(g);
+        if (++grp.G == KS_GMAX) flush();
+    }
+    flush();
+}
+
+// Double hoisting (R11c) giant step: acc += (sigma_g(w.c0), 0) + KS_QP(sigma_g(ModDown(w.c1))), all in Q_l P.
+void rotate_qp_impl(ckks_ctx* c, const u64* wq, size_t w_stride, int nl, int B, int64_t step, u64* acc,
+                    size_t acc_stride, void* stream)
+{
+    auto L = c->launch(stream);
+    const uint32_t g = c->galois(step);
+    if (g == 1) throw CkksError(CKKS_E_PARAM, "giant step congruent to 0 mod N/2");
+    const u64* key = c->key((int64_t)g);
+    if (!key) throw CkksError(CKKS_E_NOKEY, "no Galois key for step " + std::to_string(step));
+    auto w = c->ks_work(B);
+    ck::KsIn ki{wq, w_stride, (size_t)(nl + 1) * c->n, g};
+    ck::keyswitch_modup(L, ki, B, nl, w, true);
+    ck::KsGroup grp{};
+    grp.key[0] = key;
+    grp.out[0] = acc;
+    grp.scatter[0] = 0;
+    grp.G = 1;
+    ck::KsOut ko{acc, acc_stride, wq, w_stride, g, 0, 1};
+    ck::keyswitch_finish_qp(L, ki, grp, B, nl, w, ko, false);
 }
 
 void relin_impl(ckks_ctx* c, const u64* in3, size_t in_stride, int nl, int batch, u64* out, size_t out_stride,
@@ -546,6 +609,7 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
             }
             for (int b = 0; b < np; ++b) {
                 h.qmod[i][b] = q % primes[b];
+                h.qmod_sh[i][b] = h_shoup(h.qmod[i][b], primes[b]);
                 if (b != i) {
                     h.qinv[i][b] = h_pow(q % primes[b], primes[b] - 2, primes[b]);
                     h.qinv_sh[i][b] = h_shoup(h.qinv[i][b], primes[b]);
@@ -796,7 +860,16 @@ ckks_status ckks_rotate_hoisted(ckks_ctx* c, const ckks_ct* in, const int32_t* s
 ckks_status ckks_model_set_hoisting(ckks_model* m, int32_t on)
 {
     if (!m) return fail(CKKS_E_PARAM, "null");
-    m->hoisted = on ? 1 : 0;
+    if (on < 0 || on > 2) return fail(CKKS_E_PARAM, "hoisting mode must be 0, 1 or 2");
+    m->hoisted = on;
+    return CKKS_OK;
+}
+
+ckks_status ckks_layer_set_hoisting(ckks_layer* l, int32_t mode)
+{
+    if (!l) return fail(CKKS_E_PARAM, "null");
+    if (mode < 0 || mode > 2) return fail(CKKS_E_PARAM, "hoisting mode must be 0, 1 or 2");
+    l->hoisting = mode;
     return CKKS_OK;
 }
 
@@ -898,7 +971,7 @@ ckks_status ckks_layer_sizes(const ckks_ctx* c, uint32_t rows, uint32_t cols, ui
 
 static size_t layer_dev_bytes(const ckks_ctx* c, size_t count, uint32_t level)
 {
-    return align256(count * (level + 1) * c->n * 8) + align256((size_t)level * c->n * 8) +
+    return align256(count * (level + 2) * c->n * 8) + align256((size_t)level * c->n * 8) +
            align256((count > 1 ? count : 1) * c->n * 8);   // + staging for the int64 coefficients
 }
 
@@ -927,12 +1000,12 @@ static ckks_status layer_general(ckks_ctx* c, const ckks_layer_desc* d, const in
     const uint32_t level = d->level;
     char* base = (char*)dev_buf;
     ly->d_pts = (u64*)base;
-    ly->d_bias = bias ? (u64*)(base + align256(count * (level + 1) * c->n * 8)) : nullptr;
-    int64_t* stage = (int64_t*)(base + align256(count * (level + 1) * c->n * 8) + align256((size_t)level * c->n * 8));
+    ly->d_bias = bias ? (u64*)(base + align256(count * (level + 2) * c->n * 8)) : nullptr;
+    int64_t* stage = (int64_t*)(base + align256(count * (level + 2) * c->n * 8) + align256((size_t)level * c->n * 8));
     cudaStream_t st = (cudaStream_t)stream;
     auto L = c->launch(stream);
     cuda_ok(cudaMemcpyAsync(stage, pts, count * c->n * 8, cudaMemcpyHostToDevice, st), "upload plaintexts");
-    ck::signed_to_ntt(L, stage, ly->d_pts, (int)count, (int)level + 1);
+    ck::signed_to_ntt(L, stage, ly->d_pts, (int)count, (int)level + 1, true);
     if (bias) {
         cuda_ok(cudaStreamSynchronize(st), "sync");
         cuda_ok(cudaMemcpyAsync(stage, bias, (size_t)c->n * 8, cudaMemcpyHostToDevice, st), "upload bias");
@@ -1106,10 +1179,12 @@ ckks_status ckks_avgpool_create(ckks_ctx* c, uint32_t f, uint32_t t, uint32_t re
 
 void ckks_layer_destroy(ckks_layer* l) { delete l; }
 
+// baby [t1-1] + inner sums [t2] ciphertexts in the Q_l P basis (the largest of the three modes) + one
+// Q_l ciphertext for the double-hoisted ModDown output
 static size_t layer_work_words(const ckks_ctx* c, const ckks_layer* l, int B)
 {
-    const size_t ctw = c->ct_words((int)l->level + 1);
-    return ((size_t)(l->t1 - 1) + l->t2) * B * ctw;
+    const size_t ctq = c->ct_words((int)l->level + 2);
+    return ((size_t)(l->t1 - 1) + l->t2 + 1) * B * ctq;
 }
 
 ckks_status ckks_layer_work_sizes(const ckks_ctx* c, const ckks_layer* l, uint32_t batch, size_t* bytes)
@@ -1121,15 +1196,36 @@ ckks_status ckks_layer_work_sizes(const ckks_ctx* c, const ckks_layer* l, uint32
 }
 
 // matvec on B ciphertexts (B <= max_batch): in -> out (level-1), work holds baby + W.
+// hoisting 0: every rotation non-hoisted (R11); 1: baby steps hoisted (R11b); 2: double hoisting (R11c)
 static void matvec_chunk(ckks_ctx* c, const ckks_layer* ly, const u64* in, size_t in_stride, int B, u64* out,
-                         size_t out_stride, u64* work, void* stream, bool hoisted = false)
+                         size_t out_stride, u64* work, void* stream, int hoisting = 0)
 {
     const int nl = (int)ly->level + 1;
-    const size_t ctw = c->ct_words(nl);
     auto L = c->launch(stream);
+    if (hoisting == 2) {
+        const size_t ctq = c->ct_words(nl + 1), ctw = c->ct_words(nl);
+        u64* baby = work;                                   // [t1-1][B][2][nl+1][N]
+        u64* Wk = work + (size_t)(ly->t1 - 1) * B * ctq;    // [t2][B][2][nl+1][N]
+        u64* md = Wk + (size_t)ly->t2 * B * ctq;            // [B][2][nl][N]
+        std::vector<int64_t> steps;
+        std::vector<u64*> outs;
+        for (uint32_t j = 1; j < ly->t1; ++j) {
+            steps.push_back((int64_t)ly->baby[j]);
+            outs.push_back(baby + (size_t)(j - 1) * B * ctq);
+        }
+        if (!steps.empty())
+            rotate_hoisted_qp_impl(c, in, in_stride, nl, B, steps.data(), (int)steps.size(), outs.data(), ctq, stream);
+        ck::bsgs_mac(L, ly->d_pts, nl + 1, in, in_stride, baby, Wk, (int)ly->t1, (int)ly->t2, B, nl, true);
+        for (uint32_t k = 1; k < ly->t2; ++k)
+            rotate_qp_impl(c, Wk + (size_t)k * B * ctq, ctq, nl, B, (int64_t)k * ly->giant, Wk, ctq, stream);
+        ck::moddown_qp(L, Wk, ctq, B, nl, c->ks_work(B), md, ctw);
+        rescale_impl(c, md, ctw, 2, nl, B, out, out_stride, ly->d_bias, stream);
+        return;
+    }
+    const size_t ctw = c->ct_words(nl);
     u64* baby = work;                                   // [t1-1][B][2][nl][N]
     u64* Wk = work + (size_t)(ly->t1 - 1) * B * ctw;    // [t2][B][2][nl][N]
-    if (hoisted) {
+    if (hoisting == 1) {
         std::vector<int64_t> steps;
         std::vector<u64*> outs;
         for (uint32_t j = 1; j < ly->t1; ++j) {
@@ -1143,7 +1239,7 @@ static void matvec_chunk(ckks_ctx* c, const ckks_layer* ly, const u64* in, size_
             rotate_impl(c, in, in_stride, nl, B, (int64_t)ly->baby[j], baby + (size_t)(j - 1) * B * ctw, ctw, false,
                         stream);
     }
-    ck::bsgs_mac(L, ly->d_pts, in, in_stride, baby, Wk, (int)ly->t1, (int)ly->t2, B, nl);
+    ck::bsgs_mac(L, ly->d_pts, nl + 1, in, in_stride, baby, Wk, (int)ly->t1, (int)ly->t2, B, nl, false);
     for (uint32_t k = 1; k < ly->t2; ++k)
         rotate_impl(c, Wk + (size_t)k * B * ctw, ctw, nl, B, (int64_t)k * ly->giant, Wk, ctw, true, stream);
     rescale_impl(c, Wk, ctw, 2, nl, B, out, out_stride, ly->d_bias, stream);
@@ -1160,7 +1256,8 @@ ckks_status ckks_matvec_diag(ckks_ctx* c, const ckks_layer* ly, const ckks_ct* i
         for (uint32_t b0 = 0; b0 < in->batch; b0 += c->max_batch) {
             const int B = (int)std::min<uint32_t>(c->max_batch, in->batch - b0);
             matvec_chunk(c, ly, in->data + (size_t)b0 * c->ct_words(nl), c->ct_words(nl), B,
-                         out->data + (size_t)b0 * c->ct_words(nl - 1), c->ct_words(nl - 1), (u64*)work, stream);
+                         out->data + (size_t)b0 * c->ct_words(nl - 1), c->ct_words(nl - 1), (u64*)work, stream,
+                         ly->hoisting);
         }
         out->batch = in->batch;
         out->n_comp = 2;
@@ -1397,7 +1494,7 @@ static void forward_chunk(ckks_ctx* c, const ckks_model* m, const u64* in, size_
         const bool to_out = last && sg.activation == 0;
         u64* dst = to_out ? out : ((cur == bufA) ? bufB : bufA);
         const size_t dst_stride = to_out ? out_stride : c->ct_words(nl - 1);
-        matvec_chunk(c, ly, cur, cur_stride, B, dst, dst_stride, lwork, stream, m->hoisted != 0);
+        matvec_chunk(c, ly, cur, cur_stride, B, dst, dst_stride, lwork, stream, m->hoisted);
         scale = scale * ly->pt_scale / (double)c->primes[level];
         level -= 1;
         nl -= 1;

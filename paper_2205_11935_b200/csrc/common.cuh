@@ -28,6 +28,7 @@ struct DCtx {
     u64 qmod[CKKS_MAXP][CKKS_MAXP];     // q_a mod q_b
     u64 qinv[CKKS_MAXP][CKKS_MAXP];     // q_a^{-1} mod q_b   (a != b)
     u64 qinv_sh[CKKS_MAXP][CKKS_MAXP];
+    u64 qmod_sh[CKKS_MAXP][CKKS_MAXP];  // Shoup constants of qmod
     const u64* tw;                      // [n_primes][4][N]: W, W', IW, IW'  (bit-reversed psi powers)
     u64 cdt[40];                        // discrete Gaussian CDT thresholds (R13)
     int cdt_bound;

@@ -136,10 +136,13 @@ void ntt_batch(const Launch& L, uint64_t* data, int batch, int limbs, int prime0
 
 // ------------------------------------------------------------------------------------ key switch
 // (1) digits: d_j = iNTT_{q_j}(sigma_g(d)[j])  -> [B][nl][N] in [0, q_j)                  (R9)
+//     QP input (double hoisting, R11c, rem != null): d is a Q_l P component and the digits are those of
+//     ModDown(d): d_j = (iNTT_{q_j}(sigma_g(d)[j]) - [r]_{q_j}) P^{-1} with r = centred iNTT_P(sigma_g(d)[P])
+//     (rem[b], from k_ks_qp_rem; sigma_g commutes with the centred lift, so r is gathered once).
 template <int LOGN, int NTH>
 __global__ void __launch_bounds__(NTH)
 k_ks_digits(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t ct_stride, size_t comp_off,
-            u32 galois, u64* __restrict__ digits, int nl)
+            u32 galois, u64* __restrict__ digits, int nl, const u64* __restrict__ rem, int special)
 {
     extern __shared__ u64 sm[];
     using T = NttCta<LOGN, NTH>;
@@ -148,20 +151,57 @@ k_ks_digits(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t ct_s
     u64* dst = digits + ((size_t)b * nl + j) * T::N;
     const DPrime Pr = dc->p[j];
     auto ld = [&](int i) { return galois ? src[galois_src(i, galois, LOGN)] : src[i]; };
-    auto st = [&](int i, u64 v) { dst[i] = v; };
-    ntt_inverse<T>(sm, Pr, twp(dc, j), ld, st);
+    if (rem) {
+        const u64* r = rem + (size_t)b * T::N;
+        const u64 Pbig = dc->p[special].q, Pmod = dc->qmod[special][j];
+        const u64 Pinv = dc->qinv[special][j], Pinv_sh = dc->qinv_sh[special][j];
+        auto st = [&](int i, u64 v) {
+            const u64 x = v + Pr.q - centered_to(r[i], Pbig, Pmod, Pr);
+            dst[i] = csub(shoup_mul(x, Pinv, Pinv_sh, Pr.q), Pr.q);
+        };
+        ntt_inverse<T>(sm, Pr, twp(dc, j), ld, st);
+    } else {
+        auto st = [&](int i, u64 v) { dst[i] = v; };
+        ntt_inverse<T>(sm, Pr, twp(dc, j), ld, st);
+    }
 }
 
-// (2) ModUp: D_{j,e} = NTT_{p_e}(d_j mod p_e) for e != j, e in [0, nl] (nl = special)
+// (1') QP remainder: rem[b][c] = iNTT_P(sigma_g(x_b.c)[P]) for the P limb of QP components
+//      (giant-step digits: one component; the layer's final ModDown: both).  grid (ncomp, B)
 template <int LOGN, int NTH>
 __global__ void __launch_bounds__(NTH)
-k_ks_modup(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* __restrict__ modup, int nl, int special)
+k_ks_qp_rem(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t ct_stride, size_t comp_off,
+            size_t comp_step, u32 galois, int nl, int special, u64* __restrict__ rem)
 {
     extern __shared__ u64 sm[];
     using T = NttCta<LOGN, NTH>;
-    const int j = blockIdx.x / nl;
-    int e = blockIdx.x % nl;
-    if (e >= j) ++e;
+    const int c = blockIdx.x, b = blockIdx.y;
+    const u64* src = in + (size_t)b * ct_stride + comp_off + (size_t)c * comp_step + (size_t)nl * T::N;
+    u64* dst = rem + ((size_t)b * gridDim.x + c) * T::N;
+    const DPrime Pr = dc->p[special];
+    auto ld = [&](int i) { return galois ? src[galois_src(i, galois, LOGN)] : src[i]; };
+    auto st = [&](int i, u64 v) { dst[i] = v; };
+    ntt_inverse<T>(sm, Pr, twp(dc, special), ld, st);
+}
+
+// (2) ModUp: D_{j,e} = NTT_{p_e}(d_j mod p_e) for e != j, e in [0, nl] (nl = special); all_e: e == j too
+//     (QP digits are not the input limbs, so the inner product cannot read D_{j,j} from the input)
+template <int LOGN, int NTH>
+__global__ void __launch_bounds__(NTH)
+k_ks_modup(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* __restrict__ modup, int nl, int special,
+           int all_e)
+{
+    extern __shared__ u64 sm[];
+    using T = NttCta<LOGN, NTH>;
+    int j, e;
+    if (all_e) {
+        j = blockIdx.x / (nl + 1);
+        e = blockIdx.x % (nl + 1);
+    } else {
+        j = blockIdx.x / nl;
+        e = blockIdx.x % nl;
+        if (e >= j) ++e;
+    }
     const int b = blockIdx.y;
     const int p = (e == nl) ? special : e;
     const DPrime Pr = dc->p[p];
@@ -297,11 +337,99 @@ k_ks_ip_out(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u6
     }
 }
 
-void keyswitch_modup(const Launch& L, const KsIn& in, int batch, int nl, const KsWork& w)
+// (5') inner product into the Q_l P basis (double hoisting, R11c) for every key switch g of the group,
+//      one CTA per (ciphertext, row i in [0, nl], SOURCE block); row nl is the special prime P:
+//        u_g,c[i][k] = sum_j D_{j,i}[k] key_g,j.c[p_i][k]
+//        y_g,0 = u_g,0 + addend,  y_g,1 = u_g,1;   out_g,c[i][k'] (+)= y_g,c[src_g(k')]
+//      baby step (scatter g, add_mulP): addend = P c0 (0 on the P row), out = sigma_g(y) with sigma_{g^-1}
+//      permuted keys; giant step (no scatter): addend = sigma_g(w.c0) gathered from the QP input.
+//      D_{j,j} comes from the Q input limb (in != null, baby) or from the ModUp buffer (all_e ModUp).
+template <int NL>
+__global__ void __launch_bounds__(IPO_BLK)
+k_ks_ip_qp(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ in, size_t ct_stride,
+           size_t comp_off, const KsGroup grp, int L, int special, size_t out_stride, const u64* __restrict__ add,
+           size_t add_stride, int add_nl, u32 add_galois, int add_mulP, int accumulate, int B)
+{
+    __shared__ u64 ys[2][IPO_BLK];
+    constexpr int nl = NL;
+    const int n = dc->n, logn = dc->log_n;
+    const int b = blockIdx.x, i = blockIdx.y, blk = blockIdx.z;
+    const int t = threadIdx.x;
+    const int k = blk * IPO_BLK + t;
+    const bool prow = (i == nl);
+    const int p = prow ? special : i;
+    const int krow = prow ? L : i;
+    const DPrime Pr = dc->p[p];
+    u64 dv[NL];
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+        if (j == i && in) dv[j] = in[(size_t)b * ct_stride + comp_off + (size_t)j * n + k];
+        else dv[j] = modup[(((size_t)b * nl + j) * (nl + 1) + i) * n + k];
+    }
+    u64 ad = 0;
+    if (add) {
+        if (add_mulP) {
+            if (!prow)
+                ad = csub(shoup_mul(add[(size_t)b * add_stride + (size_t)i * n + k], dc->qmod[special][i],
+                                    dc->qmod_sh[special][i], Pr.q), Pr.q);
+        } else {
+            const u64* a = add + (size_t)b * add_stride + (size_t)i * n;
+            (void)add_nl;
+            ad = add_galois ? a[galois_src(k, add_galois, logn)] : a[k];
+        }
+    }
+    for (int g = 0; g < grp.G; ++g) {
+        const u64* __restrict__ key = grp.key[g] + (size_t)krow * n + k;
+        const size_t kstride = (size_t)(L + 1) * n;
+        Acc128 a0, a1;
+        a0.zero();
+        a1.zero();
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            a0.mac(dv[j], key[(size_t)(2 * j + 0) * kstride]);
+            a1.mac(dv[j], key[(size_t)(2 * j + 1) * kstride]);
+        }
+        ys[0][t] = addmod(a0.reduce(Pr), ad, Pr.q);
+        ys[1][t] = a1.reduce(Pr);
+        __syncthreads();
+        const u32 gp = grp.scatter[g];
+        int dblk = blk, sidx = t;
+        if (gp) {
+            dblk = galois_src(blk * IPO_BLK, grp.ginv[g], logn) / IPO_BLK;
+            sidx = galois_src(dblk * IPO_BLK + t, gp, logn) - blk * IPO_BLK;
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            u64& o = grp.out[g][(size_t)b * out_stride + ((size_t)c * (nl + 1) + i) * n + (size_t)dblk * IPO_BLK + t];
+            u64 v = ys[c][sidx];
+            if (accumulate) v = addmod(v, o, Pr.q);
+            o = v;
+        }
+        __syncthreads();
+    }
+}
+
+// layer-final ModDown of QP ciphertexts: out[b][c][i] = (y[b][c][i] - x[b][c][i]) P^{-1} mod q_i
+__global__ void __launch_bounds__(256)
+k_moddown_combine(const DCtx* __restrict__ dc, const u64* __restrict__ y, size_t y_stride, const u64* __restrict__ xo,
+                  u64* __restrict__ out, size_t out_stride, int nl, int special)
+{
+    const int n = dc->n;
+    const int k = blockIdx.x * 256 + threadIdx.x;
+    const int i = blockIdx.y, c = blockIdx.z % 2, b = blockIdx.z / 2;
+    const DPrime Pr = dc->p[i];
+    const u64 yv = y[(size_t)b * y_stride + ((size_t)c * (nl + 1) + i) * n + k];
+    const u64 xv = xo[(((size_t)b * 2 + c) * (nl + 1) + i) * n + k];
+    out[(size_t)b * out_stride + ((size_t)c * nl + i) * n + k] =
+        csub(shoup_mul(yv + Pr.q - xv, dc->qinv[special][i], dc->qinv_sh[special][i], Pr.q), Pr.q);
+}
+
+void keyswitch_modup(const Launch& L, const KsIn& in, int batch, int nl, const KsWork& w, bool qp_in)
 {
     if (batch <= 0) return;
     const int special = L.n_data;   // special prime is stored after the data primes
     const size_t smem = sizeof(u64) << L.log_n;
+    const int ne = qp_in ? nl + 1 : nl;   // ModUp targets per digit
     NTT_DISPATCH(L.log_n, {
         constexpr int NT = NttThreads<LG>::value;
         constexpr int NW = NttThreadsWide<LG>::value;
@@ -313,30 +441,116 @@ void keyswitch_modup(const Launch& L, const KsIn& in, int batch, int nl, const K
         const bool pm = L.probe && L.probe->on(PROBE_MODUP);
         if (L.probe && L.probe->on(PROBE_ALL)) {
             L.probe->bytes_by_kernel["k_ks_modup"] +=
-                ((double)batch * nl + (double)batch * nl * nl) * (double)(8 << L.log_n);
-            // butterflies per limb NTT: (N/2) log2 N; targets of digit j: every prime but q_j
+                ((double)batch * nl + (double)batch * nl * ne) * (double)(8 << L.log_n);
+            // butterflies per limb NTT: (N/2) log2 N; targets of digit j: every prime but q_j (QP: all)
             const double bf = (double)(1 << (L.log_n - 1)) * L.log_n * batch;
             for (int j = 0; j < nl; ++j)
                 for (int e = 0; e <= nl; ++e) {
-                    if (e == j) continue;
+                    if (e == j && !qp_in) continue;
                     const int p = (e == nl) ? L.n_data : e;
                     if (L.pclass && L.pclass[p] == PC_FP) L.probe->bfly_fp += bf;
                     else L.probe->bfly_int += bf;
                 }
         }
+        if (qp_in) {
+            auto kr = (wm & 1) ? k_ks_qp_rem<LG, NW> : k_ks_qp_rem<LG, NT>;
+            allow_smem(kr, smem);
+            ProbeScope ps_(L.probe, L.st, "k_ks_qp_rem");
+            kr<<<dim3(1, batch), (wm & 1) ? NW : NT, smem, L.st>>>(L.dc, in.base, in.ct_stride, in.comp_off, 0, in.galois,
+                                                                    nl, special, w.rem);
+        }
         { ProbeScope ps_(L.probe, L.st, "k_ks_digits"); kd<<<dim3(nl, batch), (wm & 1) ? NW : NT, smem, L.st>>>(L.dc, in.base, in.ct_stride, in.comp_off, in.galois,
-                                                              w.digits, nl); }
+                                                              w.digits, nl, qp_in ? w.rem : nullptr, special); }
         if (pm) {
             L.probe->mark(L.st);
-            // digits read once, nl x nl ModUp limbs written
-            L.probe->alg_bytes += ((double)batch * nl + (double)batch * nl * nl) * (double)(8 << L.log_n);
+            // digits read once, nl x ne ModUp limbs written
+            L.probe->alg_bytes += ((double)batch * nl + (double)batch * nl * ne) * (double)(8 << L.log_n);
         }
-        { ProbeScope ps_(L.probe, L.st, "k_ks_modup"); km<<<dim3(nl * nl, batch), (wm & 2) ? NW : NT, smem, L.st>>>(L.dc, w.digits, w.modup, nl,
-                                                                                        special); }
+        { ProbeScope ps_(L.probe, L.st, "k_ks_modup"); km<<<dim3(nl * ne, batch), (wm & 2) ? NW : NT, smem, L.st>>>(L.dc, w.digits, w.modup, nl,
+                                                                                        special, qp_in ? 1 : 0); }
         if (pm) L.probe->mark(L.st);
     });
     check_launch("keyswitch_modup");
-    if (L.counter) *L.counter += 2;
+    if (L.counter) *L.counter += qp_in ? 3 : 2;
+}
+
+// QP-basis finish (R11c): inner product over all nl+1 rows, no ModDown.  in (baby: the Q_l input whose
+// limb j is D_{j,j}) or null (giant: all_e ModUp); addend per KsOut (add_mulP / add_galois)
+void keyswitch_finish_qp(const Launch& L, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
+                         const KsOut& out, bool baby)
+{
+    if (batch <= 0 || grp.G <= 0) return;
+    if (grp.G > KS_GMAX || nl > KS_LMAX) throw std::runtime_error("keyswitch_finish_qp: group/limb limits");
+    const int n = 1 << L.log_n;
+    if (n < IPO_BLK) throw std::runtime_error("N >= 1024 required");
+    const dim3 grid(batch, nl + 1, n / IPO_BLK);
+    const u64* ib = baby ? in.base : nullptr;
+#define IPQ_CASE(V)                                                                                                  \
+    case V: {                                                                                                         \
+        ProbeScope ps_(L.probe, L.st, "k_ks_ip_qp");                                                                  \
+        k_ks_ip_qp<V><<<grid, IPO_BLK, 0, L.st>>>(L.dc, w.modup, ib, in.ct_stride, in.comp_off, grp, L.n_data,         \
+                                                  L.n_data, out.ct_stride, out.add, out.add_stride, nl + 1,           \
+                                                  out.add_galois, baby ? 1 : 0, out.accumulate, batch);               \
+    } break;
+    switch (nl) {
+        IPQ_CASE(1) IPQ_CASE(2) IPQ_CASE(3) IPQ_CASE(4) IPQ_CASE(5) IPQ_CASE(6) IPQ_CASE(7) IPQ_CASE(8)
+        IPQ_CASE(9) IPQ_CASE(10) IPQ_CASE(11) IPQ_CASE(12) IPQ_CASE(13) IPQ_CASE(14) IPQ_CASE(15) IPQ_CASE(16)
+    default: throw std::runtime_error("nl > 16");
+    }
+#undef IPQ_CASE
+    check_launch("keyswitch_finish_qp");
+    if (L.counter) *L.counter += 1;
+}
+
+// layer-final ModDown of B QP ciphertexts y (stride y_stride) into Q_l ciphertexts out
+void moddown_qp(const Launch& L, const uint64_t* y, size_t y_stride, int batch, int nl, const KsWork& w, uint64_t* out,
+                size_t out_stride)
+{
+    if (batch <= 0) return;
+    const int special = L.n_data;
+    const int n = 1 << L.log_n;
+    const size_t smem = sizeof(u64) << L.log_n;
+    NTT_DISPATCH(L.log_n, {
+        constexpr int NT = NttThreads<LG>::value;
+        allow_smem(k_ks_qp_rem<LG, NT>, smem);
+        allow_smem(k_ks_moddown_ntt<LG, NT>, smem);
+        { ProbeScope ps_(L.probe, L.st, "k_ks_qp_rem");
+          k_ks_qp_rem<LG, NT><<<dim3(2, batch), NT, smem, L.st>>>(L.dc, y, y_stride, 0, (size_t)(nl + 1) * n, 0, nl,
+                                                                 special, w.rem); }
+        { ProbeScope ps_(L.probe, L.st, "k_ks_moddown_ntt");
+          k_ks_moddown_ntt<LG, NT><<<dim3(nl, 2, batch), NT, smem, L.st>>>(L.dc, w.rem, nl, special, w.acc); }
+    });
+    { ProbeScope ps_(L.probe, L.st, "k_moddown_combine");
+      k_moddown_combine<<<dim3(n / 256, nl, 2 * batch), 256, 0, L.st>>>(L.dc, y, y_stride, w.acc, out, out_stride, nl,
+                                                                         special); }
+    check_launch("moddown_qp");
+    if (L.counter) *L.counter += 3;
+}
+
+// P ct -> QP basis (a hoisted baby step with g == 1): out[c][i] = P in[c][i], out[c][nl] = 0
+__global__ void __launch_bounds__(256)
+k_lift_qp(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t in_stride, u64* __restrict__ out,
+          size_t out_stride, int nl, int special)
+{
+    const int n = dc->n;
+    const int k = blockIdx.x * 256 + threadIdx.x;
+    const int i = blockIdx.y, c = blockIdx.z % 2, b = blockIdx.z / 2;
+    u64 v = 0;
+    if (i < nl) {
+        const DPrime Pr = dc->p[i];
+        v = csub(shoup_mul(in[(size_t)b * in_stride + ((size_t)c * nl + i) * n + k], dc->qmod[special][i],
+                           dc->qmod_sh[special][i], Pr.q), Pr.q);
+    }
+    out[(size_t)b * out_stride + ((size_t)c * (nl + 1) + i) * n + k] = v;
+}
+
+void lift_qp(const Launch& L, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, int batch, int nl)
+{
+    if (batch <= 0) return;
+    const int n = 1 << L.log_n;
+    k_lift_qp<<<dim3(n / 256, nl + 1, 2 * batch), 256, 0, L.st>>>(L.dc, in, in_stride, out, out_stride, nl, L.n_data);
+    check_launch("lift_qp");
+    if (L.counter) ++*L.counter;
 }
 
 static void launch_ks_ip_out(const Launch& L, const KsWork& w, const KsIn& in, const KsGroup& grp, int batch, int nl,
@@ -393,7 +607,7 @@ void keyswitch(const Launch& L, const KsIn& in, const uint64_t* key, int batch, 
         // switched component + addend in, 2 components out, key rows used once per launch
         L.probe->alg_bytes += (4.0 * batch * nl + 2.0 * nl * (nl + 1)) * (double)(8 << L.log_n);
     }
-    keyswitch_modup(L, in, batch, nl, w);
+    keyswitch_modup(L, in, batch, nl, w, false);
     KsGroup grp{};
     grp.key[0] = key;
     grp.out[0] = out.base;
@@ -550,20 +764,23 @@ void add(const Launch& L, const uint64_t* a, size_t sa, const uint64_t* b, size_
 #define MACF_BL 32
 #define MACF_KH 8
 __global__ void __launch_bounds__(MACF_XT * MACF_BL, 2)
-k_bsgs_mac_fp(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u64* __restrict__ v0, size_t v0_stride,
-              const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl)
+k_bsgs_mac_fp(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_nl, const u64* __restrict__ v0,
+              size_t v0_stride, const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl,
+              int qp)
 {
     extern __shared__ double2 A2[];
     const int n = dc->n;
-    const int l = blockIdx.y;
-    const DPrime Pr = dc->p[l];
+    const int l = blockIdx.y;                      // limb; QP: limb nl is the special prime
+    const int nlx = nl + qp;
+    const int pidx = l < nl ? l : dc->n_data;
+    const DPrime Pr = dc->p[pidx];
     if (prime_class(Pr.q) != PC_FP) return;
     const int tx = threadIdx.x % MACF_XT, ty = threadIdx.x / MACF_XT;
     const int x0 = blockIdx.x * MACF_XT, x = x0 + tx;
     const int t = t1 * t2;
     const u64 mask23 = (1ULL << 23) - 1;
     for (int i = threadIdx.x; i < t * MACF_XT; i += blockDim.x) {
-        const u64 a = pts[((size_t)(i / MACF_XT) * nl + l) * n + x0 + (i % MACF_XT)];
+        const u64 a = pts[((size_t)(i / MACF_XT) * pt_nl + l) * n + x0 + (i % MACF_XT)];
         A2[i] = make_double2(u2d(a >> 23), u2d(a & mask23));
     }
     __syncthreads();
@@ -571,10 +788,12 @@ k_bsgs_mac_fp(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u6
     const double two23 = 8388608.0, two46 = 70368744177664.0;
     const double w46 = two46 - floor(two46 * qinv) * q;                        // 2^46 mod q (exact)
     const double w46q = w46 / q, w23q = two23 / q;
-    const size_t ctw = (size_t)2 * nl * n;
+    const size_t ctw = (size_t)2 * nlx * n;
+    const u64 Pm = qp ? dc->qmod[dc->n_data][l < nl ? l : 0] : 0, Pm_sh = qp ? dc->qmod_sh[dc->n_data][l < nl ? l : 0] : 0;
     for (int b = ty; b < batch; b += MACF_BL) {
         for (int c = 0; c < 2; ++c) {
-            const size_t off = ((size_t)c * nl + l) * n + x;
+            const size_t off = ((size_t)c * nlx + l) * n + x;
+            const size_t off0 = ((size_t)c * nl + l) * n + x;
             for (int k0 = 0; k0 < t2; k0 += MACF_KH) {
                 double sA[MACF_KH], sB[MACF_KH], sC[MACF_KH];
 #pragma unroll
@@ -585,9 +804,11 @@ k_bsgs_mac_fp(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u6
                     for (int u = 0; u < 8; ++u) {
                         const int j = j0 + u;
                         u64 y = 0;
-                        if (j < t1) {
-                            const u64* v = (j == 0) ? v0 + (size_t)b * v0_stride : vb + ((size_t)(j - 1) * batch + b) * ctw;
-                            y = v[off];
+                        if (j == 0) {
+                            if (!qp) y = v0[(size_t)b * v0_stride + off0];
+                            else if (l < nl) y = csub(shoup_mul(v0[(size_t)b * v0_stride + off0], Pm, Pm_sh, Pr.q), Pr.q);
+                        } else if (j < t1) {
+                            y = vb[((size_t)(j - 1) * batch + b) * ctw + off];
                         }
                         y1[u] = u2d(y >> 23);
                         y0[u] = u2d(y & mask23);
@@ -624,24 +845,29 @@ k_bsgs_mac_fp(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u6
 
 // BIG-class limbs (60-bit primes): same tiling as k_bsgs_mac_fp with 128-bit integer accumulators.
 __global__ void __launch_bounds__(MACF_XT * MACF_BL, 2)
-k_bsgs_mac_int(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u64* __restrict__ v0, size_t v0_stride,
-               const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl)
+k_bsgs_mac_int(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_nl, const u64* __restrict__ v0,
+               size_t v0_stride, const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl,
+               int qp)
 {
     extern __shared__ u64 Ai[];
     const int n = dc->n;
     const int l = blockIdx.y;
-    const DPrime Pr = dc->p[l];
+    const int nlx = nl + qp;
+    const int pidx = l < nl ? l : dc->n_data;
+    const DPrime Pr = dc->p[pidx];
     if (prime_class(Pr.q) == PC_FP) return;
     const int tx = threadIdx.x % MACF_XT, ty = threadIdx.x / MACF_XT;
     const int x0 = blockIdx.x * MACF_XT, x = x0 + tx;
     const int t = t1 * t2;
     for (int i = threadIdx.x; i < t * MACF_XT; i += blockDim.x)
-        Ai[i] = pts[((size_t)(i / MACF_XT) * nl + l) * n + x0 + (i % MACF_XT)];
+        Ai[i] = pts[((size_t)(i / MACF_XT) * pt_nl + l) * n + x0 + (i % MACF_XT)];
     __syncthreads();
-    const size_t ctw = (size_t)2 * nl * n;
+    const size_t ctw = (size_t)2 * nlx * n;
+    const u64 Pm = qp ? dc->qmod[dc->n_data][l < nl ? l : 0] : 0, Pm_sh = qp ? dc->qmod_sh[dc->n_data][l < nl ? l : 0] : 0;
     for (int b = ty; b < batch; b += MACF_BL) {
         for (int c = 0; c < 2; ++c) {
-            const size_t off = ((size_t)c * nl + l) * n + x;
+            const size_t off = ((size_t)c * nlx + l) * n + x;
+            const size_t off0 = ((size_t)c * nl + l) * n + x;
             for (int k0 = 0; k0 < t2; k0 += MACF_KH) {
                 Acc128 s[MACF_KH];
 #pragma unroll
@@ -652,9 +878,11 @@ k_bsgs_mac_int(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u
                     for (int u = 0; u < 8; ++u) {
                         const int j = j0 + u;
                         y[u] = 0;
-                        if (j < t1) {
-                            const u64* v = (j == 0) ? v0 + (size_t)b * v0_stride : vb + ((size_t)(j - 1) * batch + b) * ctw;
-                            y[u] = v[off];
+                        if (j == 0) {
+                            if (!qp) y[u] = v0[(size_t)b * v0_stride + off0];
+                            else if (l < nl) y[u] = csub(shoup_mul(v0[(size_t)b * v0_stride + off0], Pm, Pm_sh, Pr.q), Pr.q);
+                        } else if (j < t1) {
+                            y[u] = vb[((size_t)(j - 1) * batch + b) * ctw + off];
                         }
                     }
 #pragma unroll
@@ -674,19 +902,20 @@ k_bsgs_mac_int(const DCtx* __restrict__ dc, const u64* __restrict__ pts, const u
     }
 }
 
-void bsgs_mac(const Launch& L, const uint64_t* pts, const uint64_t* v0, size_t v0_stride, const uint64_t* vbaby,
-              uint64_t* wout, int t1, int t2, int batch, int nl)
+void bsgs_mac(const Launch& L, const uint64_t* pts, int pt_nl, const uint64_t* v0, size_t v0_stride,
+              const uint64_t* vbaby, uint64_t* wout, int t1, int t2, int batch, int nl, bool qp)
 {
+    const int nlx = nl + (qp ? 1 : 0);
     if (batch <= 0) return;
     const int n = 1 << L.log_n;
     if ((size_t)t1 * t2 * MACF_XT * sizeof(double2) > 200 * 1024)
         throw std::runtime_error("bsgs_mac: plaintext tile too large (t <= 1600)");
     const size_t smem_int = (size_t)t1 * t2 * MACF_XT * sizeof(u64);
     allow_smem(k_bsgs_mac_int, smem_int);
-    { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_int"); k_bsgs_mac_int<<<dim3(n / MACF_XT, nl), MACF_XT * MACF_BL, smem_int, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl); }
+    { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_int"); k_bsgs_mac_int<<<dim3(n / MACF_XT, nlx), MACF_XT * MACF_BL, smem_int, L.st>>>(L.dc, pts, pt_nl, v0, v0_stride, vbaby, wout, t1, t2, batch, nl, qp ? 1 : 0); }
     const size_t smem_fp = (size_t)t1 * t2 * MACF_XT * sizeof(double2);
     allow_smem(k_bsgs_mac_fp, smem_fp);
-    { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_fp"); k_bsgs_mac_fp<<<dim3(n / MACF_XT, nl), MACF_XT * MACF_BL, smem_fp, L.st>>>(L.dc, pts, v0, v0_stride, vbaby, wout, t1, t2, batch, nl); }
+    { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_fp"); k_bsgs_mac_fp<<<dim3(n / MACF_XT, nlx), MACF_XT * MACF_BL, smem_fp, L.st>>>(L.dc, pts, pt_nl, v0, v0_stride, vbaby, wout, t1, t2, batch, nl, qp ? 1 : 0); }
     check_launch("bsgs_mac");
     if (L.counter) *L.counter += 2;
 }
@@ -727,27 +956,30 @@ void decrypt(const Launch& L, const uint64_t* ct, size_t ct_stride, const uint64
 // ------------------------------------------------------------------------------------ signed -> NTT
 template <int LOGN>
 __global__ void __launch_bounds__(NttThreads<LOGN>::value)
-k_signed_to_ntt(const DCtx* __restrict__ dc, const long long* __restrict__ coeffs, u64* __restrict__ out, int nl)
+k_signed_to_ntt(const DCtx* __restrict__ dc, const long long* __restrict__ coeffs, u64* __restrict__ out, int nl,
+                int nlimbs)
 {
     extern __shared__ u64 sm[];
     using T = NttCta<LOGN, NttThreads<LOGN>::value>;
     const int l = blockIdx.x, y = blockIdx.y;
-    const DPrime Pr = dc->p[l];
+    const int p = l < nl ? l : dc->n_data;   // limb nl (if present): the special prime
+    const DPrime Pr = dc->p[p];
     const long long* src = coeffs + (size_t)y * T::N;
-    u64* o = out + ((size_t)y * nl + l) * T::N;
+    u64* o = out + ((size_t)y * nlimbs + l) * T::N;
     auto ld = [&](int i) { return signed_to_res(src[i], Pr); };
     auto st = [&](int i, u64 v) { o[i] = v; };
-    ntt_forward<T>(sm, Pr, twp(dc, l), ld, st);
+    ntt_forward<T>(sm, Pr, twp(dc, p), ld, st);
 }
 
-void signed_to_ntt(const Launch& L, const int64_t* coeffs, uint64_t* out, int count, int nl)
+void signed_to_ntt(const Launch& L, const int64_t* coeffs, uint64_t* out, int count, int nl, bool with_special)
 {
+    const int nlimbs = nl + (with_special ? 1 : 0);
     if (count <= 0) return;
     const size_t smem = sizeof(u64) << L.log_n;
     NTT_DISPATCH(L.log_n, {
         constexpr int NT = NttThreads<LG>::value;
         allow_smem(k_signed_to_ntt<LG>, smem);
-        k_signed_to_ntt<LG><<<dim3(nl, count), NT, smem, L.st>>>(L.dc, (const long long*)coeffs, out, nl);
+        k_signed_to_ntt<LG><<<dim3(nlimbs, count), NT, smem, L.st>>>(L.dc, (const long long*)coeffs, out, nl, nlimbs);
     });
     check_launch("signed_to_ntt");
     if (L.counter) ++*L.counter;

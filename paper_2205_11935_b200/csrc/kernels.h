@@ -101,7 +101,16 @@ void keyswitch(const Launch&, const KsIn& in, const uint64_t* key, int batch, in
 // the two halves of a key switch: ModUp of `in` into w (digits, modup), and the inner product +
 // ModDown from w.modup.  scatter_g != 0 writes the result permuted by sigma_{g} where the caller
 // passes g^{-1} (hoisted rotation: out = sigma_g(c0 + ModDown(sum_j D_j key'_j))).
-void keyswitch_modup(const Launch&, const KsIn& in, int batch, int nl, const KsWork& w);
+void keyswitch_modup(const Launch&, const KsIn& in, int batch, int nl, const KsWork& w, bool qp_in = false);
+// double hoisting (R11c): qp_in = the switched component is a Q_l P component (digits of its ModDown,
+// ModUp to every prime); keyswitch_finish_qp leaves the result in Q_l P (baby: addend P c0 from `in`,
+// output sigma_g-scattered; giant: addend = out.add gathered by out.add_galois, accumulated)
+void keyswitch_finish_qp(const Launch&, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
+                         const KsOut& out, bool baby);
+// y [B][2][nl+1][N] (QP, stride y_stride) -> out [B][2][nl][N]: (y - [y_P]) / P  (one ModDown per layer)
+void moddown_qp(const Launch&, const uint64_t* y, size_t y_stride, int batch, int nl, const KsWork& w, uint64_t* out,
+                size_t out_stride);
+void lift_qp(const Launch&, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, int batch, int nl);
 void keyswitch_finish(const Launch&, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
                       const KsOut& out);
 // out limbs[c][N] = in limbs[c][galois_src(k, g)] for `limbs` consecutive limbs (key pre-permutation)
@@ -116,12 +125,13 @@ void tensor(const Launch&, const uint64_t* a, const uint64_t* b, size_t stride, 
             int batch, int nl);
 void add(const Launch&, const uint64_t* a, size_t sa, const uint64_t* b, size_t sb, uint64_t* out, size_t so,
          int batch, int ncomp, int nl);
-void bsgs_mac(const Launch&, const uint64_t* pts, const uint64_t* v0, size_t v0_stride, const uint64_t* vbaby,
-              uint64_t* wout, int t1, int t2, int batch, int nl);
+// pts [t][pt_nl][N]; qp: v/w in the Q_l P basis (nl+1 limbs, the last mod P), v0 (Q_l) lifted by P on load
+void bsgs_mac(const Launch&, const uint64_t* pts, int pt_nl, const uint64_t* v0, size_t v0_stride,
+              const uint64_t* vbaby, uint64_t* wout, int t1, int t2, int batch, int nl, bool qp);
 void decrypt(const Launch&, const uint64_t* ct, size_t ct_stride, const uint64_t* s_ntt, uint64_t* out, int batch, int nl);
 
-// signed int64 coefficients [count][N] -> NTT residues out[count][nl][N] over primes 0..nl-1
-void signed_to_ntt(const Launch&, const int64_t* coeffs, uint64_t* out, int count, int nl);
+// signed int64 coefficients [count][N] -> NTT residues out[count][nl(+1)][N] over primes 0..nl-1 (and P)
+void signed_to_ntt(const Launch&, const int64_t* coeffs, uint64_t* out, int count, int nl, bool with_special = false);
 
 // ---- keygen / encryption samplers (R13-R15; streams as in DESIGN.md)
 // out[y][limb][N] = NTT_{p(limb)}(sample_kind(seed, stream(purpose, id0 + y*id_step, digit0 + y*digit_step, 0), i))

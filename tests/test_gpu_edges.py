@@ -42,8 +42,9 @@ def test_max_limbs_ntt():
     assert np.array_equal(u64(t), x)
 
 
+@pytest.mark.parametrize("mode", [0, 2])
 @pytest.mark.parametrize("shape,log_n", [((1, 1), 10), ((5, 3), 10), ((3, 17), 11), ((1024, 1024), 12)])
-def test_degenerate_and_max_layer_shapes(shape, log_n):
+def test_degenerate_and_max_layer_shapes(shape, log_n, mode):
     """t = 1 (no rotation at all), non-square, t = 1024 (t1 = t2 = 32, the largest tile)."""
     rows, cols = shape
     steps = OC.rotation_steps_for([shape])
@@ -56,13 +57,13 @@ def test_degenerate_and_max_layer_shapes(shape, log_n):
     b = rng.uniform(-0.1, 0.1, rows)
     lay = OC.encode_layer(o, W, b, o.top_level, 2.0 ** 30)
     gl = G.Layer(g, rows, cols, lay.level, diag_coeffs=lay.diag_coeffs, bias_coeffs=lay.bias_coeffs,
-                 pt_scale=lay.pt_scale, bias_scale=lay.bias_scale)
+                 pt_scale=lay.pt_scale, bias_scale=lay.bias_scale).set_hoisting(mode)
     x = rng.uniform(-1, 1, cols)
     m = OE.encode(OC.pack_input(x, lay.t, o.n // 2), 2.0 ** 30, o.n)
     ct = g.encrypt(np.stack([m, m]), 4, 0, 2.0 ** 30)
     out = gl.matvec(ct)
     for bb in range(2):
-        ref = OC.matvec(o, OC.Ct(o.encrypt(m, 4, bb), 2.0 ** 30), lay)
+        ref = OC.matvec(o, OC.Ct(o.encrypt(m, 4, bb), 2.0 ** 30), lay, hoisted=mode)
         assert np.array_equal(u64(out.data)[bb], ref.data)
     y = OE.decode(o.decrypt(u64(out.data)[0]), o.primes, out.scale, o.n)
     assert np.max(np.abs(y[:rows] - (W @ x + b))) < 1e-3

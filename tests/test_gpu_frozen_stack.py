@@ -41,7 +41,7 @@ def weights(t, rng):
             "b2": rng.uniform(-0.1, 0.1, tp), "f_pool": 3}
 
 
-@pytest.mark.parametrize("hoisted", [True, False])
+@pytest.mark.parametrize("hoisted", [0, 1, 2])
 def test_conv_and_pool_layers(hoisted):
     t, n = 64, 2048
     p, R = OC.packing(n // 2, t, 4)
@@ -62,7 +62,8 @@ def test_conv_and_pool_layers(hoisted):
             assert np.array_equal(u64(out.data)[b], ref.data), (lay.kind, b)
 
 
-def test_frozen_stack_small_ring_parity():
+@pytest.mark.parametrize("mode", [1, 2])
+def test_frozen_stack_small_ring_parity(mode):
     """Depth-6 stack on N=4096, t=64, 15 items per ciphertext, ragged batch over max_batch."""
     t, n = 64, 4096
     p, R = OC.packing(n // 2, t, 4)
@@ -81,14 +82,14 @@ def test_frozen_stack_small_ring_parity():
             S3 = (S * S / o.primes[l]) * S / o.primes[l - 1]
             acts[i] = OC.cubic_masked_coeffs(o, lay.rows, lay.t, R, p, S3)
     model = G.Model.from_stages(g, gstages, act_coeffs=acts)
-    model.set_hoisting(True)
+    model.set_hoisting(mode)
     B = 3
     items = [[rng.uniform(-1, 1, t) for _ in range(p)] for _ in range(B)]
     ms = np.stack([OE.encode(OC.pack_items(it, t, R, n // 2), Delta, n) for it in items])
     out = model.forward(g.encrypt(ms, 11, 0, Delta))
     assert out.level == o.top_level - 6
     for b in range(B):
-        ref = OC.forward_stages(o, OC.Ct(o.encrypt(ms[b], 11, b), Delta), stages, R, p, hoisted=True)
+        ref = OC.forward_stages(o, OC.Ct(o.encrypt(ms[b], 11, b), Delta), stages, R, p, hoisted=mode)
         assert np.array_equal(u64(out.data)[b], ref.data), b
         y = OE.decode(o.decrypt(ref.data), o.primes, ref.scale, o.n)
         for r in range(p):
@@ -124,7 +125,8 @@ def test_frozen_stack_library_encoders():
         assert np.max(np.abs(y[r * R: r * R + ref_f.size] - ref_f)) < 1e-3
 
 
-def test_paper_stack_t768_parity():
+@pytest.mark.parametrize("mode", [1, 2])
+def test_paper_stack_t768_parity(mode):
     """The paper's shapes: t = 768, conv f=9, dense 768 + ReLU_approx, pool 3, dense 766, p = 5
     items at N=16384 (Table 2 p column), depth 6 on the [60, 40x7 | 60] chain; bit-exact vs the oracle."""
     t, n = 768, 16384
@@ -144,11 +146,11 @@ def test_paper_stack_t768_parity():
             l = lay.level - 1
             acts[i] = OC.cubic_masked_coeffs(o, lay.rows, lay.t, R, p, (S * S / o.primes[l]) * S / o.primes[l - 1])
     model = G.Model.from_stages(g, gst, act_coeffs=acts)
-    model.set_hoisting(True)
+    model.set_hoisting(mode)
     items = [rng.uniform(-1, 1, t) for _ in range(p)]
     m = OE.encode(OC.pack_items(items, t, R, n // 2), Delta, n)
     out = model.forward(g.encrypt(m, 13, 0, Delta))
-    ref = OC.forward_stages(o, OC.Ct(o.encrypt(m, 13, 0), Delta), stages, R, p, hoisted=True)
+    ref = OC.forward_stages(o, OC.Ct(o.encrypt(m, 13, 0), Delta), stages, R, p, hoisted=mode)
     assert np.array_equal(u64(out.data)[0], ref.data)
     y = OE.decode(o.decrypt(ref.data), o.primes, ref.scale, o.n)
     for r in range(p):

@@ -240,7 +240,7 @@ def _model_case(cfg, activation, B, max_batch, data_bits=None, log_n=None, seed_
     model = G.Model(g, glayers, {"none": 0, "square": 1, "cubic": 2}[activation],
                     act_coeffs=OC.activation_plaintexts(o, layers, activation))
     if hoisted:
-        model.set_hoisting(True)
+        model.set_hoisting(hoisted)
     ms = np.stack([OE.encode(OC.pack_input(prob["x"][b], layers[0].t, o.n // 2), Delta, o.n) for b in range(B)])
     ct = g.encrypt(ms, cfg.enc_seed, 0, Delta)
     out = model.forward(ct)
@@ -282,26 +282,28 @@ def test_forward_cfg4_parity_and_accuracy():
     assert np.max(np.abs(gy - y)) < 1e-3
 
 
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("activation", ["square", "cubic"])
-def test_forward_small_ring_hoisted_parity(activation):
+def test_forward_small_ring_hoisted_parity(activation, mode):
     o, g, prob, layers, ms, ct, out = _model_case(
         S.Config(name="small", log_n=12, data_bits=(60,) + (40,) * 5, special_bits=(60,), log2_scale=40,
                  layers=((64, 128), (32, 64)), activation=activation, in_dim=128,
-                 weight_std=(1 / np.sqrt(128), 1 / np.sqrt(64))), activation, B=3, max_batch=2, hoisted=True)
+                 weight_std=(1 / np.sqrt(128), 1 / np.sqrt(64))), activation, B=3, max_batch=2, hoisted=mode)
     got = u64(out.data)
     for b in range(3):
-        ref = OC.forward(o, OC.Ct(o.encrypt(ms[b], S.CFG4.enc_seed, b), 2.0 ** 40), layers, activation, hoisted=True)
+        ref = OC.forward(o, OC.Ct(o.encrypt(ms[b], S.CFG4.enc_seed, b), 2.0 ** 40), layers, activation, hoisted=mode)
         assert np.array_equal(got[b], ref.data), b
         y = OC.plain_forward(prob["x"][b], prob["W"], prob["b"], activation)
         dec = OE.decode(o.decrypt(ref.data), o.primes, ref.scale, o.n)
         assert np.max(np.abs(dec[: y.size] - y)) < 1e-3
 
 
-def test_forward_cfg4_hoisted_parity_and_accuracy():
+@pytest.mark.parametrize("mode", [1, 2])
+def test_forward_cfg4_hoisted_parity_and_accuracy(mode):
     cfg = S.CFG4
-    o, g, prob, layers, ms, ct, out = _model_case(cfg, "square", B=2, max_batch=2, hoisted=True)
+    o, g, prob, layers, ms, ct, out = _model_case(cfg, "square", B=2, max_batch=2, hoisted=mode)
     for b in range(2):
-        ref = OC.forward(o, OC.Ct(o.encrypt(ms[b], cfg.enc_seed, b), 2.0 ** 40), layers, "square", hoisted=True)
+        ref = OC.forward(o, OC.Ct(o.encrypt(ms[b], cfg.enc_seed, b), 2.0 ** 40), layers, "square", hoisted=mode)
         assert np.array_equal(u64(out.data)[b], ref.data)
         y = OC.plain_forward(prob["x"][b], prob["W"], prob["b"], "square")
         assert np.max(np.abs(OE.decode(o.decrypt(ref.data), o.primes, ref.scale, o.n)[:128] - y)) < 1e-3
