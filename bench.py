@@ -46,6 +46,8 @@ def parse():
                    help="rotation schedule: 0 non-hoisted (SEAL semantics, R11), 1 hoisted baby steps (R11b), "
                         "2 double hoisting (R11c, default)")
     p.add_argument("--no-hoist", action="store_true", help="same as --hoisting 0")
+    p.add_argument("--bsgs-x", type=int, default=None,
+                   help="extra baby-step doublings of the BSGS split (R5b); default 1 with --hoisting 2, else 0")
     return p.parse_args()
 
 
@@ -163,13 +165,16 @@ def profiled_traffic(kernel):
         return None
 
 
-def build_forward(G, cfg, B, max_batch, device, hoisted=True):
-    """Product path only: library encoder, device keygen/encryption."""
+def build_forward(G, cfg, B, max_batch, device, hoisted=True, bsgs_x=None):
+    """Product path only: library encoder, device keygen/encryption.  bsgs_x: extra baby-step
+    doublings (R5b); default 1 under double hoisting (hoisted == 2), else 0 (R5)."""
     import synthetic as S
     shapes = list(cfg.layers)
-    steps = G.model_steps(shapes)
+    if bsgs_x is None:
+        bsgs_x = 1 if int(hoisted) == 2 else 0
+    steps = G.model_steps(shapes, bsgs_x)
     ctx = G.Context(cfg.log_n, cfg.data_bits, cfg.special_bits, key_seed=cfg.key_seed, rot_steps=steps,
-                    max_batch=max_batch, device=device)
+                    max_batch=max_batch, device=device, bsgs_baby_extra=bsgs_x)
     Delta = 2.0 ** cfg.log2_scale
     levels, scales, _ = ctx.model_plan(shapes, G.ACT_SQUARE, ctx.top_level, Delta)
     prob = S.dense_problem(cfg, batch=B)
@@ -177,7 +182,7 @@ def build_forward(G, cfg, B, max_batch, device, hoisted=True):
               for i, (r, c) in enumerate(shapes)]
     model = G.Model(ctx, layers, G.ACT_SQUARE)
     model.set_hoisting(hoisted)
-    t0 = G.bsgs_plan(*shapes[0])[0]
+    t0 = G.bsgs_plan(*shapes[0], bsgs_x)[0]
     slots = ctx.n // 2
     ms = np.empty((B, ctx.n), dtype=np.int64)
     v = np.zeros(slots)
@@ -203,7 +208,7 @@ def run_ours(args):
     cfg = S.CFG5
     B = args.batch or cfg.batch
     hoisting = 0 if args.no_hoist else args.hoisting
-    ctx, model, ct, prob = build_forward(G, cfg, B, args.max_batch, device, hoisted=hoisting)
+    ctx, model, ct, prob = build_forward(G, cfg, B, args.max_batch, device, hoisted=hoisting, bsgs_x=args.bsgs_x)
     out = ctx.empty_ct(B, model.final_level)
     work = torch.empty(model.work_bytes(B), dtype=torch.uint8, device=device)
     stream = torch.cuda.current_stream()
@@ -270,6 +275,7 @@ def run_ours(args):
                          "activation": "square", "max_batch": args.max_batch,
                          "baby_steps": {0: "non-hoisted (R11)", 1: "hoisted (NEXT f-1, R11b)",
                                         2: "double hoisting (NEXT f-1, R11c)"}[hoisting],
+                         "bsgs_t1_t2": [list(G.bsgs_plan(r, c, ctx.bsgs_baby_extra)[1:]) for r, c in cfg.layers],
                          "l2": "inputs (2 GiB of ciphertexts) larger than L2; no flush",
                          "parallelism": f"replicas x{world}"},
               "gpu_launches": launches, "roofline": roofline,

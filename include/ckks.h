@@ -59,6 +59,9 @@ typedef struct {
     uint32_t n_rot_steps;
     int32_t want_relin;         /* generate the relinearisation key (s^2 -> s)                     */
     uint32_t max_batch;         /* ciphertexts per internal launch sequence (workspace sizing)     */
+    uint32_t bsgs_baby_extra;   /* dense layers of this context use t1 = 2^(ceil(log2 t / 2) + x)   */
+                                /* baby steps (x = this, 0..4; R5 is x = 0, see ckks_bsgs_plan_x);  */
+                                /* rot_steps must cover the resulting baby/giant steps               */
 } ckks_params;
 
 /* Host-readable context description. */
@@ -225,6 +228,10 @@ ckks_status ckks_model_set_hoisting(ckks_model* model, int32_t on);
 /* BSGS split of a rows x cols layer: t = max(rows, cols) padded to a multiple of
  * t1 = 2^ceil(ceil(log2 t)/2), t2 = t / t1 (R5). */
 ckks_status ckks_bsgs_plan(uint32_t rows, uint32_t cols, uint32_t* t, uint32_t* t1, uint32_t* t2);
+/* Same with x extra doublings of the baby-step count: t1 = min(2^(ceil(lg/2) + x), 2^lg), lg =
+ * ceil(log2 t) (R5b: under double hoisting a baby step costs ~1/6 of a giant step, so x = 1 is
+ * cheaper; every split computes the same Eq. 1 product).  CKKS_E_PARAM for x > 4. */
+ckks_status ckks_bsgs_plan_x(uint32_t rows, uint32_t cols, uint32_t x, uint32_t* t, uint32_t* t1, uint32_t* t2);
 /* Level/scale schedule of a forward (R8): for each layer the level and scale its input has, and
  * the sorted set of rotation steps the forward needs (baby 1..t1-1, giant k t1, replicate -t).
  * steps may be NULL to query the count; *n_steps is its capacity on input, the count on output. */

@@ -33,28 +33,29 @@ class Ct:
         return self.data.shape[1] - 1
 
 
-def bsgs_split(rows: int, cols: int):
-    """t = max(rows, cols) (P:L96 zero padding); t1 = 2^ceil(ceil(log2 t)/2); t padded to t1 | t (R5)."""
+def bsgs_split(rows: int, cols: int, x: int = 0):
+    """t = max(rows, cols) (P:L96 zero padding); t1 = 2^ceil(ceil(log2 t)/2); t padded to t1 | t (R5).
+    x > 0: t1 = 2^min(lg, ceil(lg/2) + x) (R5b, more baby steps; the same Eq. 1 product)."""
     t = max(rows, cols)
     lg = max(0, math.ceil(math.log2(t)))
-    t1 = 1 << math.ceil(lg / 2)
+    t1 = 1 << min(lg, math.ceil(lg / 2) + x)
     t = -(-t // t1) * t1
     return t, t1, t // t1
 
 
-def diagonals(W: np.ndarray):
+def diagonals(W: np.ndarray, x: int = 0):
     """diag_i(M)[s] = Mpad[s][(s + i) mod t]  for i < t."""
     rows, cols = W.shape
-    t, t1, t2 = bsgs_split(rows, cols)
+    t, t1, t2 = bsgs_split(rows, cols, x)
     Mp = np.zeros((t, t))
     Mp[:rows, :cols] = W
     s = np.arange(t)
     return np.stack([Mp[s, (s + i) % t] for i in range(t)]), (t, t1, t2)
 
 
-def diag_prime_slots(W: np.ndarray, n_slots: int):
+def diag_prime_slots(W: np.ndarray, n_slots: int, x: int = 0):
     """diag'_{k t1 + j} = rot_{-k t1}(diag_{k t1 + j}) as full slot vectors (zero-filled, R4)."""
-    D, (t, t1, t2) = diagonals(W)
+    D, (t, t1, t2) = diagonals(W, x)
     if 2 * t > n_slots:
         raise ValueError("2t exceeds the slot count")
     out = np.zeros((t, n_slots))
@@ -79,10 +80,10 @@ class EncodedLayer:
     bias_coeffs: np.ndarray     # [N] int64
 
 
-def encode_layer(ctx, W, b, level: int, in_scale: float) -> EncodedLayer:
+def encode_layer(ctx, W, b, level: int, in_scale: float, x: int = 0) -> EncodedLayer:
     W = np.asarray(W, dtype=np.float64)
     rows, cols = W.shape
-    slots, (t, t1, t2) = diag_prime_slots(W, ctx.n // 2)
+    slots, (t, t1, t2) = diag_prime_slots(W, ctx.n // 2, x)
     q_l = float(ctx.primes[level])
     coeffs = np.stack([encoding.encode(slots[i], q_l, ctx.n) for i in range(t)])
     bias = np.zeros(ctx.n // 2)
@@ -92,11 +93,11 @@ def encode_layer(ctx, W, b, level: int, in_scale: float) -> EncodedLayer:
     return EncodedLayer(rows, cols, t, t1, t2, level, q_l, in_scale, coeffs, bcoef)
 
 
-def rotation_steps_for(layers_shapes):
+def rotation_steps_for(layers_shapes, x: int = 0):
     """Every Galois step the forward needs: baby 1..t1-1, giant k t1, replicate -t (R5)."""
     steps = set()
     for li, (rows, cols) in enumerate(layers_shapes):
-        t, t1, t2 = bsgs_split(rows, cols)
+        t, t1, t2 = bsgs_split(rows, cols, x)
         steps.update(range(1, t1))
         steps.update(k * t1 for k in range(1, t2))
         if li > 0:
@@ -230,13 +231,13 @@ def forward(ctx, ct: Ct, layers, activation: str = "square", ops: OpCount | None
     return ct
 
 
-def encode_model(ctx, Ws, bs, level: int, scale: float, activation: str):
+def encode_model(ctx, Ws, bs, level: int, scale: float, activation: str, x: int = 0):
     """Encode every layer at the level/scale its input will have (R8 scale bookkeeping)."""
     layers = []
     s = scale
     l = level
     for li, (W, b) in enumerate(zip(Ws, bs)):
-        lay = encode_layer(ctx, W, b, l, s)
+        lay = encode_layer(ctx, W, b, l, s, x)
         layers.append(lay)
         l -= 1                                   # one rescale in the dense layer; scale unchanged
         if li < len(Ws) - 1:

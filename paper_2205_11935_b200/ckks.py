@@ -30,7 +30,8 @@ class ckks_params(ctypes.Structure):
     _fields_ = [("log_n", ctypes.c_uint32), ("n_data", ctypes.c_uint32), ("n_special", ctypes.c_uint32),
                 ("prime_bits", ctypes.POINTER(ctypes.c_uint32)), ("sigma", ctypes.c_double),
                 ("key_seed", ctypes.c_uint64), ("rot_steps", ctypes.POINTER(ctypes.c_int32)),
-                ("n_rot_steps", ctypes.c_uint32), ("want_relin", ctypes.c_int32), ("max_batch", ctypes.c_uint32)]
+                ("n_rot_steps", ctypes.c_uint32), ("want_relin", ctypes.c_int32), ("max_batch", ctypes.c_uint32),
+                ("bsgs_baby_extra", ctypes.c_uint32)]
 
 
 class ckks_info(ctypes.Structure):
@@ -110,6 +111,7 @@ SIGNATURES = {
     "ckks_probe_read": (_I, [_VP, ctypes.POINTER(_D), ctypes.POINTER(_U64), ctypes.POINTER(_D)]),
     "ckks_probe_read_all": (_I, [_VP, ctypes.c_char_p, _SZ]),
     "ckks_bsgs_plan": (_I, [_U32, _U32, ctypes.POINTER(_U32), ctypes.POINTER(_U32), ctypes.POINTER(_U32)]),
+    "ckks_bsgs_plan_x": (_I, [_U32, _U32, _U32, ctypes.POINTER(_U32), ctypes.POINTER(_U32), ctypes.POINTER(_U32)]),
     "ckks_model_plan": (_I, [_VP, _U32, ctypes.POINTER(_U32), ctypes.POINTER(_U32), _I, _U32, _D,
                              ctypes.POINTER(_U32), ctypes.POINTER(_D), ctypes.POINTER(_I), ctypes.POINTER(_U32)]),
 }
@@ -181,7 +183,7 @@ class Context:
     """Owns (as torch tensors) the table/key/workspace buffers that the C context borrows."""
 
     def __init__(self, log_n, data_bits, special_bits=(), key_seed=1, rot_steps=(), want_relin=True,
-                 max_batch=1, sigma=3.2, device="cuda", stream=None):
+                 max_batch=1, sigma=3.2, device="cuda", stream=None, bsgs_baby_extra=0):
         import torch
         self.torch = torch
         self.device = torch.device(device)
@@ -190,7 +192,9 @@ class Context:
         steps = [int(s) for s in rot_steps]
         self._steps = (ctypes.c_int32 * max(1, len(steps)))(*steps) if steps else (ctypes.c_int32 * 1)()
         self.params = ckks_params(int(log_n), len(data_bits), len(special_bits), self._bits, float(sigma),
-                                  int(key_seed), self._steps, len(steps), 1 if want_relin else 0, int(max_batch))
+                                  int(key_seed), self._steps, len(steps), 1 if want_relin else 0, int(max_batch),
+                                  int(bsgs_baby_extra))
+        self.bsgs_baby_extra = int(bsgs_baby_extra)
         tb, kb, wb = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
         _check(lib().ckks_ctx_sizes(ctypes.byref(self.params), ctypes.byref(tb), ctypes.byref(kb),
                                     ctypes.byref(wb)), "ckks_ctx_sizes")
@@ -445,7 +449,7 @@ class GeneralLayer(Layer):
     def dense(cls, ctx, W, bias, region, items, level, in_scale, stream=None):
         Wn = np.ascontiguousarray(W, dtype=np.float64)
         rows, cols = Wn.shape
-        t = bsgs_plan(rows, cols)[0]
+        t = bsgs_plan(rows, cols, ctx.bsgs_baby_extra)[0]
         bn = None if bias is None else np.ascontiguousarray(bias, dtype=np.float64)
 
         def build(self, h):
@@ -574,18 +578,19 @@ class Model:
         return ol.value, osc.value
 
 
-def bsgs_plan(rows, cols):
+def bsgs_plan(rows, cols, x=0):
+    """(t, t1, t2) of a rows x cols dense layer; x extra baby-step doublings (R5 / R5b)."""
     t, t1, t2 = _U32(), _U32(), _U32()
-    _check(lib().ckks_bsgs_plan(int(rows), int(cols), ctypes.byref(t), ctypes.byref(t1), ctypes.byref(t2)),
-           "ckks_bsgs_plan")
+    _check(lib().ckks_bsgs_plan_x(int(rows), int(cols), int(x), ctypes.byref(t), ctypes.byref(t1),
+                                  ctypes.byref(t2)), "ckks_bsgs_plan_x")
     return t.value, t1.value, t2.value
 
 
-def model_steps(shapes):
-    """Rotation steps a forward over these layer shapes needs (host planner of the library, R5)."""
+def model_steps(shapes, x=0):
+    """Rotation steps a forward over these layer shapes needs (host planner of the library, R5/R5b)."""
     steps = set()
     for i, (r, c) in enumerate(shapes):
-        t, t1, t2 = bsgs_plan(r, c)
+        t, t1, t2 = bsgs_plan(r, c, x)
         steps.update(range(1, t1))
         steps.update(k * t1 for k in range(1, t2))
         if i > 0:

@@ -190,6 +190,7 @@ struct ckks_ctx {
     int log_n = 0, n = 0, L = 0, ns = 0, np = 0;
     double sigma = 3.2;
     uint32_t max_batch = 1;
+    uint32_t bsgs_bx = 0;         // extra baby-step doublings of this context's dense layers (R5b)
     std::vector<u64> primes, psi;
     DCtx host_dc{};
     DCtx* d_dc = nullptr;
@@ -301,12 +302,13 @@ void check_ct(const ckks_ctx* c, const ckks_ct* x, int ncomp_expect = 2)
     if (x->batch == 0) throw CkksError(CKKS_E_SHAPE, "empty batch");
 }
 
-void bsgs_split(uint32_t rows, uint32_t cols, uint32_t& t, uint32_t& t1, uint32_t& t2)
+// R5 (x = 0) / R5b: t1 = min(2^(ceil(lg/2) + x), 2^lg)
+void bsgs_split(uint32_t rows, uint32_t cols, uint32_t& t, uint32_t& t1, uint32_t& t2, uint32_t x = 0)
 {
     t = std::max(rows, cols);
     int lg = 0;
     while ((1u << lg) < t) ++lg;
-    t1 = 1u << ((lg + 1) / 2);
+    t1 = 1u << std::min<int>(lg, (lg + 1) / 2 + (int)x);
     t = (t + t1 - 1) / t1 * t1;
     t2 = t / t1;
 }
@@ -549,6 +551,8 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
         c->np = c->L + c->ns;
         c->sigma = p->sigma > 0 ? p->sigma : 3.2;
         c->max_batch = p->max_batch;
+        if (p->bsgs_baby_extra > 4) throw CkksError(CKKS_E_PARAM, "bsgs_baby_extra must be <= 4");
+        c->bsgs_bx = p->bsgs_baby_extra;
         c->primes = primes;
         for (u64 q : primes) c->pclass.push_back(prime_class(q));
         const int n = c->n, np = c->np, L = c->L;
@@ -963,7 +967,7 @@ ckks_status ckks_layer_sizes(const ckks_ctx* c, uint32_t rows, uint32_t cols, ui
         if (!c || !bytes || rows == 0 || cols == 0) throw CkksError(CKKS_E_PARAM, "bad layer shape");
         if (level < 1 || (int)level >= c->L) throw CkksError(CKKS_E_LEVEL, "layer level must be in [1, L-1]");
         uint32_t t, t1, t2;
-        bsgs_split(rows, cols, t, t1, t2);
+        bsgs_split(rows, cols, t, t1, t2, c->bsgs_bx);
         *bytes = layer_dev_bytes(c, t, level);
         return CKKS_OK;
     })
@@ -980,7 +984,7 @@ static ckks_status layer_general(ckks_ctx* c, const ckks_layer_desc* d, const in
 {
     if (d->n_baby < 1 || !d->baby_steps || d->baby_steps[0] != 0 || d->t2 < 1)
         throw CkksError(CKKS_E_PARAM, "layer: need n_baby >= 1 with baby_steps[0] == 0 and t2 >= 1");
-    if (d->n_baby > 32) throw CkksError(CKKS_E_PARAM, "layer: at most 32 baby steps");
+    if (d->n_baby > 64) throw CkksError(CKKS_E_PARAM, "layer: at most 64 baby steps");
     if (d->level < 1 || (int)d->level >= c->L) throw CkksError(CKKS_E_LEVEL, "layer level must be in [1, L-1]");
     const size_t count = (size_t)d->n_baby * d->t2;
     auto* ly = new ckks_layer();
@@ -1021,9 +1025,9 @@ static ckks_status layer_from_coeffs(ckks_ctx* c, const int64_t* diag, const int
                                      void* stream, ckks_layer** out, uint32_t region = 0, uint32_t items = 1)
 {
     uint32_t t, t1, t2;
-    bsgs_split(rows, cols, t, t1, t2);
+    bsgs_split(rows, cols, t, t1, t2, c->bsgs_bx);
     if (2 * t > (uint32_t)c->n / 2) throw CkksError(CKKS_E_PARAM, "2t exceeds the slot count");
-    if (t1 > 32 || t2 > 32) throw CkksError(CKKS_E_PARAM, "t1, t2 <= 32 supported (t <= 1024)");
+    if (t1 > 64 || t2 > 64) throw CkksError(CKKS_E_PARAM, "t1, t2 <= 64 supported");
     std::vector<int32_t> baby(t1);
     for (uint32_t j = 0; j < t1; ++j) baby[j] = (int32_t)j;
     ckks_layer_desc d{CKKS_LAYER_DENSE, rows, cols, t, t2, t1, baby.data(), (int32_t)t1, region, items, level,
@@ -1059,7 +1063,7 @@ ckks_status ckks_dense_create_packed(ckks_ctx* c, const double* W, uint32_t rows
         if (!c || !W || !dev_buf || !out) throw CkksError(CKKS_E_PARAM, "null");
         if (level < 1 || (int)level >= c->L) throw CkksError(CKKS_E_LEVEL, "layer level must be in [1, L-1]");
         uint32_t t, t1, t2;
-        bsgs_split(rows, cols, t, t1, t2);
+        bsgs_split(rows, cols, t, t1, t2, c->bsgs_bx);
         const int n = c->n, slots = n / 2;
         if (items < 1) items = 1;
         if (items == 1 && region == 0) region = 2 * t;
@@ -1380,8 +1384,14 @@ void ckks_model_destroy(ckks_model* m) { delete m; }
 
 ckks_status ckks_bsgs_plan(uint32_t rows, uint32_t cols, uint32_t* t, uint32_t* t1, uint32_t* t2)
 {
+    return ckks_bsgs_plan_x(rows, cols, 0, t, t1, t2);
+}
+
+ckks_status ckks_bsgs_plan_x(uint32_t rows, uint32_t cols, uint32_t x, uint32_t* t, uint32_t* t1, uint32_t* t2)
+{
     if (!rows || !cols || !t || !t1 || !t2) return fail(CKKS_E_PARAM, "bad shape");
-    bsgs_split(rows, cols, *t, *t1, *t2);
+    if (x > 4) return fail(CKKS_E_PARAM, "x must be <= 4");
+    bsgs_split(rows, cols, *t, *t1, *t2, x);
     return CKKS_OK;
 }
 
@@ -1397,7 +1407,7 @@ ckks_status ckks_model_plan(const ckks_ctx* c, uint32_t n_layers, const uint32_t
         double s = in_scale;
         for (uint32_t i = 0; i < n_layers; ++i) {
             uint32_t t, t1, t2;
-            bsgs_split(rows[i], cols[i], t, t1, t2);
+            bsgs_split(rows[i], cols[i], t, t1, t2, c->bsgs_bx);
             if (lvl < 1) throw CkksError(CKKS_E_LEVEL, "model deeper than the chain");
             layer_level[i] = (uint32_t)lvl;
             layer_in_scale[i] = s;

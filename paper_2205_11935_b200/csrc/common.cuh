@@ -77,6 +77,32 @@ struct Acc128 {
     __device__ __forceinline__ u64 reduce(const DPrime& P) const { return reduce128(hi, lo, P); }
 };
 
+// Split accumulator for operands < 2^42 (primes q < 2^42): a = a1 2^21 + a0, b = b1 2^21 + b0 with all
+// parts < 2^21, so every partial product is a 32x32->64 IMAD.WIDE.U32 (with accumulate) below 2^42 and
+// up to 2^20 terms sum without overflow; value = s11 2^42 + s01 2^21 + s00 (< 2^128 always).
+#define SPLIT21_MAXQ (1ULL << 42)
+struct Acc3 {
+    u64 s00, s01, s11;
+    __device__ __forceinline__ void zero() { s00 = s01 = s11 = 0; }
+    __device__ __forceinline__ void mac(u32 a1, u32 a0, u64 b)
+    {
+        const u32 b1 = (u32)(b >> 21), b0 = (u32)b & 0x1FFFFFu;
+        s00 += (u64)a0 * b0;
+        s01 += (u64)a0 * b1;
+        s01 += (u64)a1 * b0;
+        s11 += (u64)a1 * b1;
+    }
+    __device__ __forceinline__ u64 reduce(const DPrime& P) const
+    {
+        const u64 mlo = s01 << 21, mhi = s01 >> 43;
+        const u64 slo = s11 << 42, shi = s11 >> 22;
+        const u64 l1 = s00 + mlo;
+        const u64 l2 = l1 + slo;
+        const u64 hi = mhi + shi + (l1 < s00 ? 1 : 0) + (l2 < l1 ? 1 : 0);
+        return reduce128(hi, l2, P);
+    }
+};
+
 __device__ __forceinline__ u64 addmod(u64 a, u64 b, u64 q) { return csub(a + b, q); }
 __device__ __forceinline__ u64 submod(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
 

@@ -344,53 +344,102 @@ k_ks_ip_out(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u6
 //      baby step (scatter g, add_mulP): addend = P c0 (0 on the P row), out = sigma_g(y) with sigma_{g^-1}
 //      permuted keys; giant step (no scatter): addend = sigma_g(w.c0) gathered from the QP input.
 //      D_{j,j} comes from the Q input limb (in != null, baby) or from the ModUp buffer (all_e ModUp).
-template <int NL>
+//      Each thread handles IPQ_BB ciphertexts of the same coefficient so every key word is read once
+//      per IPQ_BB ciphertexts (the inner product is otherwise L2-bandwidth bound on the key reads).
+template <int NL, bool SPLIT, int IPQ_BB>
+__device__ __forceinline__ void ipqp_dot(const u64 (&dv)[IPQ_BB][NL], const u64* __restrict__ key, size_t kstride,
+                                         const DPrime& Pr, int nb, u64 (&u)[IPQ_BB][2])
+{
+    if constexpr (SPLIT) {
+        Acc3 a[IPQ_BB][2];
+#pragma unroll
+        for (int bb = 0; bb < IPQ_BB; ++bb) a[bb][0].zero(), a[bb][1].zero();
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            const u64 k0 = key[(size_t)(2 * j + 0) * kstride], k1 = key[(size_t)(2 * j + 1) * kstride];
+#pragma unroll
+            for (int bb = 0; bb < IPQ_BB; ++bb) {
+                const u32 x1 = (u32)(dv[bb][j] >> 21), x0 = (u32)dv[bb][j] & 0x1FFFFFu;
+                a[bb][0].mac(x1, x0, k0);
+                a[bb][1].mac(x1, x0, k1);
+            }
+        }
+#pragma unroll
+        for (int bb = 0; bb < IPQ_BB; ++bb)
+            if (bb < nb) u[bb][0] = a[bb][0].reduce(Pr), u[bb][1] = a[bb][1].reduce(Pr);
+    } else {
+        Acc128 a[IPQ_BB][2];
+#pragma unroll
+        for (int bb = 0; bb < IPQ_BB; ++bb) a[bb][0].zero(), a[bb][1].zero();
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            const u64 k0 = key[(size_t)(2 * j + 0) * kstride], k1 = key[(size_t)(2 * j + 1) * kstride];
+#pragma unroll
+            for (int bb = 0; bb < IPQ_BB; ++bb) {
+                a[bb][0].mac(dv[bb][j], k0);
+                a[bb][1].mac(dv[bb][j], k1);
+            }
+        }
+#pragma unroll
+        for (int bb = 0; bb < IPQ_BB; ++bb)
+            if (bb < nb) u[bb][0] = a[bb][0].reduce(Pr), u[bb][1] = a[bb][1].reduce(Pr);
+    }
+}
+
+template <int NL, int IPQ_BB>
 __global__ void __launch_bounds__(IPO_BLK)
 k_ks_ip_qp(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ in, size_t ct_stride,
            size_t comp_off, const KsGroup grp, int L, int special, size_t out_stride, const u64* __restrict__ add,
-           size_t add_stride, int add_nl, u32 add_galois, int add_mulP, int accumulate, int B)
+           size_t add_stride, int add_nl, u32 add_galois, int add_mulP, int accumulate, int B, int allow_split)
 {
-    __shared__ u64 ys[2][IPO_BLK];
+    __shared__ u64 ys[IPQ_BB][2][IPO_BLK];
     constexpr int nl = NL;
     const int n = dc->n, logn = dc->log_n;
-    const int b = blockIdx.x, i = blockIdx.y, blk = blockIdx.z;
+    const int b0 = blockIdx.x * IPQ_BB, i = blockIdx.y, blk = blockIdx.z;
+    const int nb = min(IPQ_BB, B - b0);
     const int t = threadIdx.x;
     const int k = blk * IPO_BLK + t;
     const bool prow = (i == nl);
     const int p = prow ? special : i;
     const int krow = prow ? L : i;
     const DPrime Pr = dc->p[p];
-    u64 dv[NL];
+    (void)add_nl;
+    u64 dv[IPQ_BB][NL];
+    u64 ad[IPQ_BB];
 #pragma unroll
-    for (int j = 0; j < NL; ++j) {
-        if (j == i && in) dv[j] = in[(size_t)b * ct_stride + comp_off + (size_t)j * n + k];
-        else dv[j] = modup[(((size_t)b * nl + j) * (nl + 1) + i) * n + k];
-    }
-    u64 ad = 0;
-    if (add) {
-        if (add_mulP) {
-            if (!prow)
-                ad = csub(shoup_mul(add[(size_t)b * add_stride + (size_t)i * n + k], dc->qmod[special][i],
-                                    dc->qmod_sh[special][i], Pr.q), Pr.q);
-        } else {
-            const u64* a = add + (size_t)b * add_stride + (size_t)i * n;
-            (void)add_nl;
-            ad = add_galois ? a[galois_src(k, add_galois, logn)] : a[k];
-        }
-    }
-    for (int g = 0; g < grp.G; ++g) {
-        const u64* __restrict__ key = grp.key[g] + (size_t)krow * n + k;
-        const size_t kstride = (size_t)(L + 1) * n;
-        Acc128 a0, a1;
-        a0.zero();
-        a1.zero();
+    for (int bb = 0; bb < IPQ_BB; ++bb) {
+        const int b = b0 + (bb < nb ? bb : 0);
 #pragma unroll
         for (int j = 0; j < NL; ++j) {
-            a0.mac(dv[j], key[(size_t)(2 * j + 0) * kstride]);
-            a1.mac(dv[j], key[(size_t)(2 * j + 1) * kstride]);
+            if (j == i && in) dv[bb][j] = in[(size_t)b * ct_stride + comp_off + (size_t)j * n + k];
+            else dv[bb][j] = modup[(((size_t)b * nl + j) * (nl + 1) + i) * n + k];
         }
-        ys[0][t] = addmod(a0.reduce(Pr), ad, Pr.q);
-        ys[1][t] = a1.reduce(Pr);
+        ad[bb] = 0;
+        if (add) {
+            if (add_mulP) {
+                if (!prow)
+                    ad[bb] = csub(shoup_mul(add[(size_t)b * add_stride + (size_t)i * n + k], dc->qmod[special][i],
+                                            dc->qmod_sh[special][i], Pr.q), Pr.q);
+            } else {
+                const u64* a = add + (size_t)b * add_stride + (size_t)i * n;
+                ad[bb] = add_galois ? a[galois_src(k, add_galois, logn)] : a[k];
+            }
+        }
+    }
+    // rows of primes < 2^42: split 21-bit IMAD.WIDE products (Acc3); 60-bit rows: 128-bit products
+    const bool split = allow_split && Pr.q < SPLIT21_MAXQ;
+    const size_t kstride = (size_t)(L + 1) * n;
+    for (int g = 0; g < grp.G; ++g) {
+        const u64* __restrict__ key = grp.key[g] + (size_t)krow * n + k;
+        u64 u[IPQ_BB][2];
+        if (split) ipqp_dot<NL, true, IPQ_BB>(dv, key, kstride, Pr, nb, u);
+        else ipqp_dot<NL, false, IPQ_BB>(dv, key, kstride, Pr, nb, u);
+#pragma unroll
+        for (int bb = 0; bb < IPQ_BB; ++bb)
+            if (bb < nb) {
+                ys[bb][0][t] = addmod(u[bb][0], ad[bb], Pr.q);
+                ys[bb][1][t] = u[bb][1];
+            }
         __syncthreads();
         const u32 gp = grp.scatter[g];
         int dblk = blk, sidx = t;
@@ -399,11 +448,16 @@ k_ks_ip_qp(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64
             sidx = galois_src(dblk * IPO_BLK + t, gp, logn) - blk * IPO_BLK;
         }
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            u64& o = grp.out[g][(size_t)b * out_stride + ((size_t)c * (nl + 1) + i) * n + (size_t)dblk * IPO_BLK + t];
-            u64 v = ys[c][sidx];
-            if (accumulate) v = addmod(v, o, Pr.q);
-            o = v;
+        for (int bb = 0; bb < IPQ_BB; ++bb) {
+            if (bb >= nb) break;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                u64& o = grp.out[g][(size_t)(b0 + bb) * out_stride + ((size_t)c * (nl + 1) + i) * n +
+                                    (size_t)dblk * IPO_BLK + t];
+                u64 v = ys[bb][c][sidx];
+                if (accumulate) v = addmod(v, o, Pr.q);
+                o = v;
+            }
         }
         __syncthreads();
     }
@@ -474,6 +528,180 @@ void keyswitch_modup(const Launch& L, const KsIn& in, int batch, int nl, const K
     if (L.counter) *L.counter += qp_in ? 3 : 2;
 }
 
+// (5'') the baby-step QP inner product on the FP64 tensor cores (DMMA).  For one row i and one
+//      coefficient k the group's inner products are a small matrix product
+//        U[b][(g, c)] = sum_j D_{b,j}[k] key_g,j.c[k]       (16 ciphertexts x 2G columns x K = nl)
+//      computed EXACTLY with mma.sync m16n8k4 f64 on operands split into 23-bit (q < 2^45) or 20-bit
+//      (60-bit primes) parts: every partial product is an integer < 2^46 and every sum < 2^53, so the
+//      tensor-core FP64 accumulation is exact.  The split sums are recombined mod q per output.
+//      CTA = 16 ciphertexts x IPM_KT coefficients of one row; operands staged through shared memory
+//      (XOR-swizzled), results staged per (g, c, b) row and written through the sigma_g block permutation
+//      (aligned IPM_KT-blocks map onto aligned blocks, as for IPO_BLK).  Output as k_ks_ip_qp (baby mode).
+#define IPM_KT 16
+#define IPM_BT 16
+#define IPM_THREADS 128
+__device__ __forceinline__ void dmma16884(double (&c)[4], double a0, double a1, double b0)
+{
+    asm("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+        : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+        : "d"(a0), "d"(a1), "d"(b0));
+}
+
+template <int NL, bool INT>
+__global__ void __launch_bounds__(IPM_THREADS)
+k_ks_ip_mma(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ in, size_t ct_stride,
+            size_t comp_off, const KsGroup grp, int L, int special, size_t out_stride, int B)
+{
+    constexpr int nl = NL;
+    constexpr int NLP = (NL + 3) & ~3;               // K padded to the MMA k-step
+    constexpr int JS = IPM_KT * 16 + 4;              // j stride (words) of the swizzled operand tiles
+    extern __shared__ u64 sm[];
+    u64* Ds = sm;                                    // [NLP][KT][16 b]  (b ^ kk swizzle)
+    u64* Ks = Ds + NLP * JS;                         // [NLP][KT][16 n]  n = 2 g + c
+    u64* As = Ks + NLP * JS;                         // [KT][16 b]      addend P c0
+    u64* Os = As + IPM_KT * 16;                      // [8 g][2 c][16 b][KT]
+    const int n = dc->n, logn = dc->log_n;
+    const int b0 = blockIdx.x * IPM_BT, i = blockIdx.y, k0 = blockIdx.z * IPM_KT;
+    const bool prow = (i == nl);
+    const int p = prow ? special : i;
+    const int krow = prow ? L : i;
+    const DPrime Pr = dc->p[p];
+    if ((prime_class(Pr.q) != PC_FP) != INT) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = grp.G;
+    // ---- stage D, keys, addend (coalesced along k); all loads of a thread issued before the stores
+    constexpr int NIT = NLP * 16 * IPM_KT / IPM_THREADS;
+    {
+        u64 dvals[NIT], kvals[NIT];
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+            const int e = tid + it * IPM_THREADS;
+            const int kk = e % IPM_KT, r = (e / IPM_KT) % 16, j = e / (16 * IPM_KT);
+            const int b = b0 + r;
+            dvals[it] = 0;
+            kvals[it] = 0;
+            if (j < NL) {
+                if (b < B)
+                    dvals[it] = (j == i) ? in[(size_t)b * ct_stride + comp_off + (size_t)j * n + k0 + kk]
+                                         : modup[(((size_t)b * nl + j) * (nl + 1) + i) * n + k0 + kk];
+                const int g = r >> 1, c = r & 1;
+                if (g < G) kvals[it] = grp.key[g][((size_t)(j * 2 + c) * (L + 1) + krow) * n + k0 + kk];
+            }
+        }
+        u64 avals[16 * IPM_KT / IPM_THREADS];
+#pragma unroll
+        for (int it = 0; it < 16 * IPM_KT / IPM_THREADS; ++it) {
+            const int e = tid + it * IPM_THREADS;
+            const int kk = e % IPM_KT, r = e / IPM_KT, b = b0 + r;
+            avals[it] = (!prow && b < B) ? in[(size_t)b * ct_stride + (size_t)i * n + k0 + kk] : 0;
+        }
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+            const int e = tid + it * IPM_THREADS;
+            const int kk = e % IPM_KT, r = (e / IPM_KT) % 16, j = e / (16 * IPM_KT);
+            Ds[j * JS + kk * 16 + (r ^ kk)] = dvals[it];
+            Ks[j * JS + kk * 16 + (r ^ kk)] = kvals[it];
+        }
+#pragma unroll
+        for (int it = 0; it < 16 * IPM_KT / IPM_THREADS; ++it) {
+            const int e = tid + it * IPM_THREADS;
+            const int kk = e % IPM_KT, r = e / IPM_KT;
+            As[kk * 16 + r] = prow ? 0 : csub(shoup_mul(avals[it], dc->qmod[special][i], dc->qmod_sh[special][i], Pr.q), Pr.q);
+        }
+    }
+    __syncthreads();
+    // ---- per coefficient: split-operand DMMA over j, recombination mod q
+    const int gid = lane >> 2, tig = lane & 3;
+    constexpr int KPW = IPM_KT / (IPM_THREADS / 32);
+    for (int kq = 0; kq < KPW; ++kq) {
+        const int kk = warp * KPW + kq;
+        constexpr int NS = INT ? 5 : 3;
+        double S[NS][2][4];
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+#pragma unroll
+            for (int t = 0; t < 2; ++t)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) S[s][t][e] = 0.0;
+#pragma unroll
+        for (int kb = 0; kb < NLP; kb += 4) {
+            const int j = kb + tig;
+            const u64 a0 = Ds[j * JS + kk * 16 + (gid ^ kk)], a1 = Ds[j * JS + kk * 16 + ((gid + 8) ^ kk)];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const u64 bv = Ks[j * JS + kk * 16 + ((t * 8 + gid) ^ kk)];
+                if constexpr (!INT) {
+                    const u64 m = (1ULL << 23) - 1;
+                    const double a0h = u2d(a0 >> 23), a0l = u2d(a0 & m), a1h = u2d(a1 >> 23), a1l = u2d(a1 & m);
+                    const double bh = u2d(bv >> 23), bl = u2d(bv & m);
+                    dmma16884(S[2][t], a0h, a1h, bh);
+                    dmma16884(S[1][t], a0h, a1h, bl);
+                    dmma16884(S[1][t], a0l, a1l, bh);
+                    dmma16884(S[0][t], a0l, a1l, bl);
+                } else {
+                    const u64 m = (1ULL << 20) - 1;
+                    const double x0[3] = {u2d(a0 & m), u2d((a0 >> 20) & m), u2d(a0 >> 40)};
+                    const double x1[3] = {u2d(a1 & m), u2d((a1 >> 20) & m), u2d(a1 >> 40)};
+                    const double y[3] = {u2d(bv & m), u2d((bv >> 20) & m), u2d(bv >> 40)};
+#pragma unroll
+                    for (int sa = 0; sa < 3; ++sa)
+#pragma unroll
+                        for (int sb = 0; sb < 3; ++sb) dmma16884(S[sa + sb][t], x0[sa], x1[sa], y[sb]);
+                }
+            }
+        }
+        // outputs of this thread: (b = gid + 8 (e >> 1), n = 8 t + 2 tig + (e & 1)) -> g = 4 t + tig, c = e & 1
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int bl = gid + 8 * (e >> 1), g = 4 * t + tig, c = e & 1;
+                u64 u;
+                if constexpr (!INT) {
+                    // v = s0 + s1 2^23 + s2 2^46 on the integer pipes (each s < 2^51)
+                    const u64 s0 = d2u(S[0][t][e]), s1 = d2u(S[1][t][e]), s2 = d2u(S[2][t][e]);
+                    u64 lo = s0, hi = 0, add;
+                    add = s1 << 23; lo += add; hi += (lo < add) + (s1 >> 41);
+                    add = s2 << 46; lo += add; hi += (lo < add) + (s2 >> 18);
+                    u = reduce128(hi, lo, Pr);
+                } else {
+                    const u64 s0 = d2u(S[0][t][e]), s1 = d2u(S[1][t][e]), s2 = d2u(S[2][t][e]), s3 = d2u(S[3][t][e]),
+                              s4 = d2u(S[4][t][e]);
+                    // v = s0 + s1 2^20 + s2 2^40 + s3 2^60 + s4 2^80   (each s < 2^48)
+                    u64 lo = s0, hi = 0, add;
+                    add = s1 << 20; lo += add; hi += (lo < add) + (s1 >> 44);
+                    add = s2 << 40; lo += add; hi += (lo < add) + (s2 >> 24);
+                    add = s3 << 60; lo += add; hi += (lo < add) + (s3 >> 4);
+                    hi += s4 << 16;
+                    u = reduce128(hi, lo, Pr);
+                }
+                if (c == 0) u = addmod(u, As[kk * 16 + bl], Pr.q);
+                if (g < G) Os[((g * 2 + c) * 16 + bl) * IPM_KT + (kk ^ ((bl + 4 * g) & 15))] = u;
+            }
+    }
+    __syncthreads();
+    // ---- permuted, coalesced write: row (g, c, b) of IPM_KT destination words per 16 lanes
+    for (int r = tid / IPM_KT; r < G * 2 * 16; r += IPM_THREADS / IPM_KT) {
+        const int t = tid % IPM_KT;
+        const int g = r / 32, c = (r / 16) & 1, bl = r & 15, b = b0 + bl;
+        if (b >= B) continue;
+        const u32 gp = grp.scatter[g];
+        int dblk = blockIdx.z, sidx = t;
+        if (gp) {
+            dblk = galois_src(k0, grp.ginv[g], logn) / IPM_KT;
+            sidx = galois_src(dblk * IPM_KT + t, gp, logn) - k0;
+        }
+        grp.out[g][(size_t)b * out_stride + ((size_t)c * (nl + 1) + i) * n + (size_t)dblk * IPM_KT + t] =
+            Os[((g * 2 + c) * 16 + bl) * IPM_KT + (sidx ^ ((bl + 4 * g) & 15))];
+    }
+}
+
+static size_t ip_mma_smem(int nl)
+{
+    const int NLP = (nl + 3) & ~3, JS = IPM_KT * 16 + 4;
+    return sizeof(u64) * ((size_t)2 * NLP * JS + IPM_KT * 16 + 8 * 2 * 16 * IPM_KT);
+}
+
 // QP-basis finish (R11c): inner product over all nl+1 rows, no ModDown.  in (baby: the Q_l input whose
 // limb j is D_{j,j}) or null (giant: all_e ModUp); addend per KsOut (add_mulP / add_galois)
 void keyswitch_finish_qp(const Launch& L, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
@@ -483,14 +711,57 @@ void keyswitch_finish_qp(const Launch& L, const KsIn& in, const KsGroup& grp, in
     if (grp.G > KS_GMAX || nl > KS_LMAX) throw std::runtime_error("keyswitch_finish_qp: group/limb limits");
     const int n = 1 << L.log_n;
     if (n < IPO_BLK) throw std::runtime_error("N >= 1024 required");
-    const dim3 grid(batch, nl + 1, n / IPO_BLK);
+    static const int bbv = [] {
+        const char* e = getenv("CKKS_IPQ_BB");
+        return e ? atoi(e) : 2;
+    }();
+    static const int spl = [] {
+        const char* e = getenv("CKKS_IP_SPLIT");
+        return e ? atoi(e) : 1;
+    }();
     const u64* ib = baby ? in.base : nullptr;
+    static const int use_mma = [] {
+        const char* e = getenv("CKKS_IP_MMA");
+        return e ? atoi(e) : 0;
+    }();
+    if (baby && use_mma && grp.G >= 2 && out.add == in.base && !out.accumulate) {
+        const size_t smem = ip_mma_smem(nl);
+        const dim3 grid((batch + IPM_BT - 1) / IPM_BT, nl + 1, n / IPM_KT);
+#define IPM_CASE(V)                                                                                                  \
+    case V: {                                                                                                         \
+        allow_smem(k_ks_ip_mma<V, false>, smem);                                                                      \
+        allow_smem(k_ks_ip_mma<V, true>, smem);                                                                       \
+        ProbeScope ps_(L.probe, L.st, "k_ks_ip_mma");                                                                 \
+        k_ks_ip_mma<V, false><<<grid, IPM_THREADS, smem, L.st>>>(L.dc, w.modup, in.base, in.ct_stride, in.comp_off,  \
+                                                               grp, L.n_data, L.n_data, out.ct_stride, batch);        \
+        k_ks_ip_mma<V, true><<<grid, IPM_THREADS, smem, L.st>>>(L.dc, w.modup, in.base, in.ct_stride, in.comp_off,   \
+                                                              grp, L.n_data, L.n_data, out.ct_stride, batch);         \
+    } break;
+        switch (nl) {
+            IPM_CASE(1) IPM_CASE(2) IPM_CASE(3) IPM_CASE(4) IPM_CASE(5) IPM_CASE(6) IPM_CASE(7) IPM_CASE(8)
+            IPM_CASE(9) IPM_CASE(10) IPM_CASE(11) IPM_CASE(12) IPM_CASE(13) IPM_CASE(14) IPM_CASE(15) IPM_CASE(16)
+        default: throw std::runtime_error("nl > 16");
+        }
+#undef IPM_CASE
+        check_launch("keyswitch_finish_qp(mma)");
+        if (L.counter) *L.counter += 2;
+        return;
+    }
 #define IPQ_CASE(V)                                                                                                  \
     case V: {                                                                                                         \
         ProbeScope ps_(L.probe, L.st, "k_ks_ip_qp");                                                                  \
-        k_ks_ip_qp<V><<<grid, IPO_BLK, 0, L.st>>>(L.dc, w.modup, ib, in.ct_stride, in.comp_off, grp, L.n_data,         \
-                                                  L.n_data, out.ct_stride, out.add, out.add_stride, nl + 1,           \
-                                                  out.add_galois, baby ? 1 : 0, out.accumulate, batch);               \
+        if (bbv == 4)                                                                                                 \
+            k_ks_ip_qp<V, 4><<<dim3((batch + 3) / 4, nl + 1, n / IPO_BLK), IPO_BLK, 0, L.st>>>(                      \
+                L.dc, w.modup, ib, in.ct_stride, in.comp_off, grp, L.n_data, L.n_data, out.ct_stride, out.add,         \
+                out.add_stride, nl + 1, out.add_galois, baby ? 1 : 0, out.accumulate, batch, spl);                     \
+        else if (bbv == 1)                                                                                            \
+            k_ks_ip_qp<V, 1><<<dim3(batch, nl + 1, n / IPO_BLK), IPO_BLK, 0, L.st>>>(                                \
+                L.dc, w.modup, ib, in.ct_stride, in.comp_off, grp, L.n_data, L.n_data, out.ct_stride, out.add,         \
+                out.add_stride, nl + 1, out.add_galois, baby ? 1 : 0, out.accumulate, batch, spl);                     \
+        else                                                                                                          \
+            k_ks_ip_qp<V, 2><<<dim3((batch + 1) / 2, nl + 1, n / IPO_BLK), IPO_BLK, 0, L.st>>>(                      \
+                L.dc, w.modup, ib, in.ct_stride, in.comp_off, grp, L.n_data, L.n_data, out.ct_stride, out.add,         \
+                out.add_stride, nl + 1, out.add_galois, baby ? 1 : 0, out.accumulate, batch, spl);                     \
     } break;
     switch (nl) {
         IPQ_CASE(1) IPQ_CASE(2) IPQ_CASE(3) IPQ_CASE(4) IPQ_CASE(5) IPQ_CASE(6) IPQ_CASE(7) IPQ_CASE(8)

@@ -225,16 +225,17 @@ def test_library_encoder_vs_oracle_encoder(c1):
 
 
 # ------------------------------------------------------------------------------------------ forward
-def _model_case(cfg, activation, B, max_batch, data_bits=None, log_n=None, seed_batch=None, hoisted=False):
+def _model_case(cfg, activation, B, max_batch, data_bits=None, log_n=None, seed_batch=None, hoisted=False, x=0):
     log_n = log_n or cfg.log_n
     data_bits = data_bits or cfg.data_bits
-    steps = OC.rotation_steps_for(cfg.layers)
+    steps = OC.rotation_steps_for(cfg.layers, x)
     o = oracle.Context(log_n, data_bits, cfg.special_bits)
     o.keygen(cfg.key_seed, steps)
-    g = G.Context(log_n, data_bits, cfg.special_bits, key_seed=cfg.key_seed, rot_steps=steps, max_batch=max_batch)
+    g = G.Context(log_n, data_bits, cfg.special_bits, key_seed=cfg.key_seed, rot_steps=steps, max_batch=max_batch,
+                  bsgs_baby_extra=x)
     prob = S.dense_problem(cfg, batch=B)
     Delta = 2.0 ** cfg.log2_scale
-    layers = OC.encode_model(o, prob["W"], prob["b"], o.top_level, Delta, activation)
+    layers = OC.encode_model(o, prob["W"], prob["b"], o.top_level, Delta, activation, x)
     glayers = [G.Layer(g, l.rows, l.cols, l.level, diag_coeffs=l.diag_coeffs, bias_coeffs=l.bias_coeffs,
                        pt_scale=l.pt_scale, bias_scale=l.bias_scale) for l in layers]
     model = G.Model(g, glayers, {"none": 0, "square": 1, "cubic": 2}[activation],
@@ -282,13 +283,13 @@ def test_forward_cfg4_parity_and_accuracy():
     assert np.max(np.abs(gy - y)) < 1e-3
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode,x", [(1, 0), (2, 0), (2, 1), (0, 2)])
 @pytest.mark.parametrize("activation", ["square", "cubic"])
-def test_forward_small_ring_hoisted_parity(activation, mode):
+def test_forward_small_ring_hoisted_parity(activation, mode, x):
     o, g, prob, layers, ms, ct, out = _model_case(
         S.Config(name="small", log_n=12, data_bits=(60,) + (40,) * 5, special_bits=(60,), log2_scale=40,
                  layers=((64, 128), (32, 64)), activation=activation, in_dim=128,
-                 weight_std=(1 / np.sqrt(128), 1 / np.sqrt(64))), activation, B=3, max_batch=2, hoisted=mode)
+                 weight_std=(1 / np.sqrt(128), 1 / np.sqrt(64))), activation, B=3, max_batch=2, hoisted=mode, x=x)
     got = u64(out.data)
     for b in range(3):
         ref = OC.forward(o, OC.Ct(o.encrypt(ms[b], S.CFG4.enc_seed, b), 2.0 ** 40), layers, activation, hoisted=mode)
@@ -298,10 +299,11 @@ def test_forward_small_ring_hoisted_parity(activation, mode):
         assert np.max(np.abs(dec[: y.size] - y)) < 1e-3
 
 
-@pytest.mark.parametrize("mode", [1, 2])
-def test_forward_cfg4_hoisted_parity_and_accuracy(mode):
+@pytest.mark.parametrize("mode,x", [(1, 0), (2, 0), (2, 1)])
+def test_forward_cfg4_hoisted_parity_and_accuracy(mode, x):
+    """cfg4 at full size (x = 1, mode 2 is the bench's schedule: t1 = 64 / 32, double hoisting)."""
     cfg = S.CFG4
-    o, g, prob, layers, ms, ct, out = _model_case(cfg, "square", B=2, max_batch=2, hoisted=mode)
+    o, g, prob, layers, ms, ct, out = _model_case(cfg, "square", B=2, max_batch=2, hoisted=mode, x=x)
     for b in range(2):
         ref = OC.forward(o, OC.Ct(o.encrypt(ms[b], cfg.enc_seed, b), 2.0 ** 40), layers, "square", hoisted=mode)
         assert np.array_equal(u64(out.data)[b], ref.data)

@@ -184,3 +184,34 @@ def test_double_hoisted_matvec_vs_float64():
     d = dec_vec(ctx, y2)
     assert np.max(np.abs(d[:16] - (W @ x + b))) < 1e-6
     assert np.max(np.abs(d[16:])) < 1e-6
+
+
+def test_bsgs_split_extra_baby_steps():
+    """R5b: x extra doublings of t1 (capped at 2^ceil(log2 t)); t1 t2 = t padded to t1 | t."""
+    assert C.bsgs_split(256, 512) == (512, 32, 16)
+    assert C.bsgs_split(256, 512, 1) == (512, 64, 8)
+    assert C.bsgs_split(128, 256, 1) == (256, 32, 8)
+    assert C.bsgs_split(766, 766, 1) == (768, 64, 12)
+    assert C.bsgs_split(16, 64, 4) == (64, 64, 1)
+    assert C.bsgs_split(1, 1, 1) == (1, 1, 1)
+    steps = C.rotation_steps_for([(256, 512), (128, 256)], 1)
+    assert steps == sorted(set(range(1, 64)) | {64 * k for k in range(1, 8)} | set(range(1, 32))
+                           | {32 * k for k in range(1, 8)} | {-256})
+
+
+@pytest.mark.parametrize("hoisted", [0, 2])
+def test_matvec_more_baby_steps_vs_float64(hoisted):
+    """Any BSGS split computes the same Eq. 1 product: x = 1 decrypts to W x + b; op counts t1-1 + t2-1."""
+    ctx = small_ctx(log_n=10, steps=C.rotation_steps_for([(16, 64)], 1))
+    rng = np.random.default_rng(12)
+    W = rng.normal(0, 0.1, (16, 64))
+    b = rng.uniform(-0.1, 0.1, 16)
+    x = rng.uniform(-1, 1, 64)
+    lay = C.encode_layer(ctx, W, b, ctx.top_level, 2.0 ** 40, x=1)
+    assert (lay.t1, lay.t2) == (16, 4)
+    ct = enc_vec(ctx, C.pack_input(x, lay.t, ctx.n // 2), 2.0 ** 40)
+    ops = C.OpCount()
+    y = C.matvec(ctx, ct, lay, ops, hoisted=hoisted)
+    assert ops.rot == 15 + 3 and ops.mul_plain == 64
+    d = dec_vec(ctx, y)
+    assert np.max(np.abs(d[:16] - (W @ x + b))) < 1e-6

@@ -63,6 +63,25 @@ __global__ void k_butterfly(uint64_t* out, uint64_t q, uint64_t w, uint64_t ws)
     if (s == 12345) out[0] = s;
 }
 
+// FP64 tensor-core MMA (DMMA) throughput: m16n8k4 f64 (512 FMA per warp instruction)
+__global__ void k_dmma(double* out, double a, double b)
+{
+    double acc[CHAINS / 4][4];
+    for (int c = 0; c < CHAINS / 4; ++c)
+        for (int i = 0; i < 4; ++i) acc[c][i] = threadIdx.x + i;
+    const double a0 = a + threadIdx.x, a1 = a - threadIdx.x, b0 = b + threadIdx.x;
+    for (int it = 0; it < ITERS / 4; ++it)
+#pragma unroll
+        for (int c = 0; c < CHAINS / 4; ++c)
+            asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                         : "+d"(acc[c][0]), "+d"(acc[c][1]), "+d"(acc[c][2]), "+d"(acc[c][3])
+                         : "d"(a0), "d"(a1), "d"(b0));
+    double s = 0;
+    for (int c = 0; c < CHAINS / 4; ++c)
+        for (int i = 0; i < 4; ++i) s += acc[c][i];
+    if (s == 1.2345) out[0] = s;
+}
+
 int main()
 {
     int dev = 0, sms = 0, clk = 0;
@@ -92,6 +111,9 @@ int main()
     run("imad_wide", [&] { k_imad_wide<<<blocks, threads>>>((uint64_t*)buf, 2654435761u); }, (double)ITERS * CHAINS,
         "IMAD.WIDE(+IADD)/s");
     run("iadd3", [&] { k_iadd3<<<blocks, threads>>>((uint32_t*)buf, 3, 5); }, (double)ITERS * CHAINS, "IADD3/s");
+    // per thread: (ITERS/4) x (CHAINS/4) mma, each 512 FMA per warp = 16 per thread
+    run("dmma_m16n8k4", [&] { k_dmma<<<blocks, threads>>>((double*)buf, 1.0000001, 1e-9); },
+        (double)(ITERS / 4) * (CHAINS / 4) * 16.0, "FP64 tensor FMA/s");
     const uint64_t q = 1099510054913ULL, w = 123456789ULL;
     const uint64_t ws = (uint64_t)(((unsigned __int128)w << 64) / q);
     run("shoup_butterfly_64", [&] { k_butterfly<<<blocks, threads>>>((uint64_t*)buf, q, w, ws); },

@@ -25,10 +25,11 @@ def main():
     p.add_argument("--batch", type=int, default=256)
     p.add_argument("--max-batch", type=int, default=256)
     p.add_argument("--no-hoist", action="store_true")
+    p.add_argument("--hoisting", type=int, default=2)
     a = p.parse_args()
     dev = torch.device("cuda", 0)
     if a.mode == "forward":
-        ctx, model, ct, _ = bench.build_forward(G, S.CFG5, a.batch, a.max_batch, dev, hoisted=not a.no_hoist)
+        ctx, model, ct, _ = bench.build_forward(G, S.CFG5, a.batch, a.max_batch, dev, hoisted=0 if a.no_hoist else a.hoisting)
         out = ctx.empty_ct(a.batch, model.final_level)
         work = torch.empty(model.work_bytes(a.batch), dtype=torch.uint8, device=dev)
         model.forward(ct, out, work)
