@@ -569,53 +569,54 @@ k_ks_ip_mma(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u6
     if ((prime_class(Pr.q) != PC_FP) != INT) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = grp.G;
-    // ---- stage D, keys, addend (coalesced along k); all loads of a thread issued before the stores
-    constexpr int NIT = NLP * 16 * IPM_KT / IPM_THREADS;
+    // ---- stage D, keys, addend (coalesced along k); all loads of a thread issued before the stores.
+    //      Thread: coefficient kk = tid % KT, rows r0 = tid / KT and r0 + 8 (b for D, n = 2g + c for keys)
     {
-        u64 dvals[NIT], kvals[NIT];
+        const int kk = tid % IPM_KT, r0 = tid / IPM_KT;
+        u64 dvals[NLP][2], kvals[NLP][2];
+        const size_t jstride_d = (size_t)(nl + 1) * n, jstride_k = (size_t)2 * (L + 1) * n;
 #pragma unroll
-        for (int it = 0; it < NIT; ++it) {
-            const int e = tid + it * IPM_THREADS;
-            const int kk = e % IPM_KT, r = (e / IPM_KT) % 16, j = e / (16 * IPM_KT);
-            const int b = b0 + r;
-            dvals[it] = 0;
-            kvals[it] = 0;
-            if (j < NL) {
-                if (b < B)
-                    dvals[it] = (j == i) ? in[(size_t)b * ct_stride + comp_off + (size_t)j * n + k0 + kk]
-                                         : modup[(((size_t)b * nl + j) * (nl + 1) + i) * n + k0 + kk];
-                const int g = r >> 1, c = r & 1;
-                if (g < G) kvals[it] = grp.key[g][((size_t)(j * 2 + c) * (L + 1) + krow) * n + k0 + kk];
+        for (int h = 0; h < 2; ++h) {
+            const int r = r0 + 8 * h, b = b0 + r, g = r >> 1, c = r & 1;
+            const u64* dsrc = modup + (((size_t)b * nl) * (nl + 1) + i) * n + k0 + kk;
+            const u64* isrc = in + (size_t)b * ct_stride + comp_off + (size_t)i * n + k0 + kk;
+            const u64* ksrc = g < G ? grp.key[g] + ((size_t)c * (L + 1) + krow) * n + k0 + kk : nullptr;
+#pragma unroll
+            for (int j = 0; j < NLP; ++j) {
+                dvals[j][h] = (j < NL && b < B) ? ((j == i) ? *isrc : dsrc[(size_t)j * jstride_d]) : 0;
+                kvals[j][h] = (j < NL && ksrc) ? ksrc[(size_t)j * jstride_k] : 0;
             }
         }
-        u64 avals[16 * IPM_KT / IPM_THREADS];
+        u64 avals[2];
 #pragma unroll
-        for (int it = 0; it < 16 * IPM_KT / IPM_THREADS; ++it) {
-            const int e = tid + it * IPM_THREADS;
-            const int kk = e % IPM_KT, r = e / IPM_KT, b = b0 + r;
-            avals[it] = (!prow && b < B) ? in[(size_t)b * ct_stride + (size_t)i * n + k0 + kk] : 0;
+        for (int h = 0; h < 2; ++h) {
+            const int r = r0 + 8 * h, b = b0 + r;
+            avals[h] = (!prow && b < B) ? in[(size_t)b * ct_stride + (size_t)i * n + k0 + kk] : 0;
         }
 #pragma unroll
-        for (int it = 0; it < NIT; ++it) {
-            const int e = tid + it * IPM_THREADS;
-            const int kk = e % IPM_KT, r = (e / IPM_KT) % 16, j = e / (16 * IPM_KT);
-            Ds[j * JS + kk * 16 + (r ^ kk)] = dvals[it];
-            Ks[j * JS + kk * 16 + (r ^ kk)] = kvals[it];
-        }
+        for (int h = 0; h < 2; ++h) {
+            const int r = r0 + 8 * h;
 #pragma unroll
-        for (int it = 0; it < 16 * IPM_KT / IPM_THREADS; ++it) {
-            const int e = tid + it * IPM_THREADS;
-            const int kk = e % IPM_KT, r = e / IPM_KT;
-            As[kk * 16 + r] = prow ? 0 : csub(shoup_mul(avals[it], dc->qmod[special][i], dc->qmod_sh[special][i], Pr.q), Pr.q);
+            for (int j = 0; j < NLP; ++j) {
+                Ds[j * JS + kk * 16 + (r ^ kk)] = dvals[j][h];
+                Ks[j * JS + kk * 16 + (r ^ kk)] = kvals[j][h];
+            }
+            As[kk * 16 + r] =
+                prow ? 0 : csub(shoup_mul(avals[h], dc->qmod[special][i], dc->qmod_sh[special][i], Pr.q), Pr.q);
         }
     }
     __syncthreads();
     // ---- per coefficient: split-operand DMMA over j, recombination mod q
     const int gid = lane >> 2, tig = lane & 3;
     constexpr int KPW = IPM_KT / (IPM_THREADS / 32);
+    const double q = (double)Pr.q, qinv = 1.0 / q;
+    const double two46 = 70368744177664.0;
+    const double w46 = two46 - floor(two46 * qinv) * q, w46q = w46 / q, c23q = 8388608.0 / q;
+    (void)w46q; (void)c23q;
     for (int kq = 0; kq < KPW; ++kq) {
         const int kk = warp * KPW + kq;
-        constexpr int NS = INT ? 5 : 3;
+        // Karatsuba on the split parts: FP 3 products (hi hi, lo lo, (hi+lo)(hi+lo)), INT 6 (three-part)
+        constexpr int NS = INT ? 6 : 3;
         double S[NS][2][4];
 #pragma unroll
         for (int s = 0; s < NS; ++s)
@@ -627,26 +628,32 @@ k_ks_ip_mma(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u6
         for (int kb = 0; kb < NLP; kb += 4) {
             const int j = kb + tig;
             const u64 a0 = Ds[j * JS + kk * 16 + (gid ^ kk)], a1 = Ds[j * JS + kk * 16 + ((gid + 8) ^ kk)];
+            if constexpr (!INT) {
+                const u64 m = (1ULL << 23) - 1;
+                const double a0h = u2d(a0 >> 23), a0l = u2d(a0 & m), a1h = u2d(a1 >> 23), a1l = u2d(a1 & m);
+                const double a0s = a0h + a0l, a1s = a1h + a1l;
 #pragma unroll
-            for (int t = 0; t < 2; ++t) {
-                const u64 bv = Ks[j * JS + kk * 16 + ((t * 8 + gid) ^ kk)];
-                if constexpr (!INT) {
-                    const u64 m = (1ULL << 23) - 1;
-                    const double a0h = u2d(a0 >> 23), a0l = u2d(a0 & m), a1h = u2d(a1 >> 23), a1l = u2d(a1 & m);
+                for (int t = 0; t < 2; ++t) {
+                    const u64 bv = Ks[j * JS + kk * 16 + ((t * 8 + gid) ^ kk)];
                     const double bh = u2d(bv >> 23), bl = u2d(bv & m);
                     dmma16884(S[2][t], a0h, a1h, bh);
-                    dmma16884(S[1][t], a0h, a1h, bl);
-                    dmma16884(S[1][t], a0l, a1l, bh);
                     dmma16884(S[0][t], a0l, a1l, bl);
-                } else {
-                    const u64 m = (1ULL << 20) - 1;
-                    const double x0[3] = {u2d(a0 & m), u2d((a0 >> 20) & m), u2d(a0 >> 40)};
-                    const double x1[3] = {u2d(a1 & m), u2d((a1 >> 20) & m), u2d(a1 >> 40)};
+                    dmma16884(S[1][t], a0s, a1s, bh + bl);
+                }
+            } else {
+                const u64 m = (1ULL << 20) - 1;
+                const double x0[3] = {u2d(a0 & m), u2d((a0 >> 20) & m), u2d(a0 >> 40)};
+                const double x1[3] = {u2d(a1 & m), u2d((a1 >> 20) & m), u2d(a1 >> 40)};
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    const u64 bv = Ks[j * JS + kk * 16 + ((t * 8 + gid) ^ kk)];
                     const double y[3] = {u2d(bv & m), u2d((bv >> 20) & m), u2d(bv >> 40)};
-#pragma unroll
-                    for (int sa = 0; sa < 3; ++sa)
-#pragma unroll
-                        for (int sb = 0; sb < 3; ++sb) dmma16884(S[sa + sb][t], x0[sa], x1[sa], y[sb]);
+                    dmma16884(S[0][t], x0[0], x1[0], y[0]);
+                    dmma16884(S[1][t], x0[1], x1[1], y[1]);
+                    dmma16884(S[2][t], x0[2], x1[2], y[2]);
+                    dmma16884(S[3][t], x0[0] + x0[1], x1[0] + x1[1], y[0] + y[1]);
+                    dmma16884(S[4][t], x0[1] + x0[2], x1[1] + x1[2], y[1] + y[2]);
+                    dmma16884(S[5][t], x0[0] + x0[2], x1[0] + x1[2], y[0] + y[2]);
                 }
             }
         }
@@ -658,15 +665,19 @@ k_ks_ip_mma(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u6
                 const int bl = gid + 8 * (e >> 1), g = 4 * t + tig, c = e & 1;
                 u64 u;
                 if constexpr (!INT) {
-                    // v = s0 + s1 2^23 + s2 2^46 on the integer pipes (each s < 2^51)
-                    const u64 s0 = d2u(S[0][t][e]), s1 = d2u(S[1][t][e]), s2 = d2u(S[2][t][e]);
-                    u64 lo = s0, hi = 0, add;
-                    add = s1 << 23; lo += add; hi += (lo < add) + (s1 >> 41);
-                    add = s2 << 46; lo += add; hi += (lo < add) + (s2 >> 18);
-                    u = reduce128(hi, lo, Pr);
+                    // v = s0 + s1 2^23 + s2 2^46 mod q on the (otherwise idle) FP64 pipe: each part reduced to
+                    // [-q/2, q/2] (exact), r1 2^23 is an exact scaling, r2 2^46 an exact-product fmodmul
+                    const double s0 = S[0][t][e], s2 = S[2][t][e], s1 = S[1][t][e] - s2 - s0;   // Karatsuba middle
+                    const double r0 = freduce(s0, q, qinv), r1 = freduce(s1, q, qinv), r2 = freduce(s2, q, qinv);
+                    const double k1 = __fma_rn(r1, c23q, CK_RND_MAGIC) - CK_RND_MAGIC;
+                    const double t1 = __fma_rn(-k1, q, r1 * 8388608.0);
+                    const double t2 = fmodmul(r2, w46, w46q, q);
+                    u = fcanon(t2 + t1 + r0, q, qinv);
                 } else {
-                    const u64 s0 = d2u(S[0][t][e]), s1 = d2u(S[1][t][e]), s2 = d2u(S[2][t][e]), s3 = d2u(S[3][t][e]),
-                              s4 = d2u(S[4][t][e]);
+                    // P0 = S0, P1 = S1, P2 = S2, P01 = S3, P12 = S4, P02 = S5 (all exact integers < 2^53)
+                    const double P0 = S[0][t][e], P1 = S[1][t][e], P2 = S[2][t][e];
+                    const u64 s0 = d2u(P0), s1 = d2u(S[3][t][e] - P0 - P1), s2 = d2u(S[5][t][e] - P0 - P2 + P1),
+                              s3 = d2u(S[4][t][e] - P1 - P2), s4 = d2u(P2);
                     // v = s0 + s1 2^20 + s2 2^40 + s3 2^60 + s4 2^80   (each s < 2^48)
                     u64 lo = s0, hi = 0, add;
                     add = s1 << 20; lo += add; hi += (lo < add) + (s1 >> 44);
@@ -680,19 +691,27 @@ k_ks_ip_mma(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u6
             }
     }
     __syncthreads();
-    // ---- permuted, coalesced write: row (g, c, b) of IPM_KT destination words per 16 lanes
-    for (int r = tid / IPM_KT; r < G * 2 * 16; r += IPM_THREADS / IPM_KT) {
-        const int t = tid % IPM_KT;
-        const int g = r / 32, c = (r / 16) & 1, bl = r & 15, b = b0 + bl;
-        if (b >= B) continue;
-        const u32 gp = grp.scatter[g];
-        int dblk = blockIdx.z, sidx = t;
-        if (gp) {
-            dblk = galois_src(k0, grp.ginv[g], logn) / IPM_KT;
-            sidx = galois_src(dblk * IPM_KT + t, gp, logn) - k0;
+    // ---- permuted, coalesced write: row (g, c, b) of IPM_KT destination words per 16 lanes; the
+    //      destination block and source index of this lane are computed once per g
+    {
+        const int t = tid % IPM_KT, r0 = tid / IPM_KT;   // r0 in [0, 8): rows r0, r0 + 8, ...
+        for (int g = 0; g < G; ++g) {
+            const u32 gp = grp.scatter[g];
+            int dblk = blockIdx.z, sidx = t;
+            if (gp) {
+                dblk = galois_src(k0, grp.ginv[g], logn) / IPM_KT;
+                sidx = galois_src(dblk * IPM_KT + t, gp, logn) - k0;
+            }
+            u64* og = grp.out[g] + (size_t)i * n + (size_t)dblk * IPM_KT + t;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int rr = r0 + 8 * h;             // rr = c * 16 + bl
+                const int c = rr >> 4, bl = rr & 15, b = b0 + bl;
+                if (b < B)
+                    og[(size_t)b * out_stride + (size_t)c * (nl + 1) * n] =
+                        Os[((g * 2 + c) * 16 + bl) * IPM_KT + (sidx ^ ((bl + 4 * g) & 15))];
+            }
         }
-        grp.out[g][(size_t)b * out_stride + ((size_t)c * (nl + 1) + i) * n + (size_t)dblk * IPM_KT + t] =
-            Os[((g * 2 + c) * 16 + bl) * IPM_KT + (sidx ^ ((bl + 4 * g) & 15))];
     }
 }
 
@@ -722,7 +741,7 @@ void keyswitch_finish_qp(const Launch& L, const KsIn& in, const KsGroup& grp, in
     const u64* ib = baby ? in.base : nullptr;
     static const int use_mma = [] {
         const char* e = getenv("CKKS_IP_MMA");
-        return e ? atoi(e) : 0;
+        return e ? atoi(e) : 1;
     }();
     if (baby && use_mma && grp.G >= 2 && out.add == in.base && !out.accumulate) {
         const size_t smem = ip_mma_smem(nl);

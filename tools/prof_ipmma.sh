@@ -1,0 +1,11 @@
+export CKKS_IP_MMA=1
+python tools/profile_forward.py --mode forward --batch 256 > gpurun_out/pf.log 2>&1 || exit 1
+for spec in "ip_mma<.int.8, .bool.0:ipmma_fp" "ip_mma<.int.8, .bool.1:ipmma_int"; do
+  re=${spec%%:*}; tag=${spec##*:}
+  rx="$re"
+  ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$rx" -c 1 -o gpurun_out/prof_$tag python tools/profile_forward.py --mode forward --batch 256 > gpurun_out/ncu_$tag.log 2>&1
+  ncu -i gpurun_out/prof_$tag.ncu-rep --page raw --csv > gpurun_out/prof_${tag}_raw.csv 2>&1
+  ncu -i gpurun_out/prof_$tag.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_${tag}_source.csv 2>&1
+  gzip -f gpurun_out/prof_${tag}_source.csv
+  rm -f gpurun_out/prof_$tag.ncu-rep
+done
