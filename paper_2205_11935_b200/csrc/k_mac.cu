@@ -1,0 +1,405 @@
+// k_mac.cu -- sm_100a kernels of the CKKS encrypted-dense-layer hot path.
+//
+// Every operation of SURVEY 8(a) rows a2-a12 is one of these kernels; the host side (api.cu)
+// only sequences launches and tracks level/scale.  Modular arithmetic runs on the integer pipes
+// (64-bit Shoup/Barrett), on the FP64 pipe (exact error-free products for q < 2^45), and -- for the
+// two small modular contractions (key-switch inner product, BSGS inner sums) -- on the FP64 tensor
+// cores with exactly split operands.  Layouts:
+//   ciphertext  [batch][comp][limb][N]  u64, NTT domain, canonical residues in [0, q)
+//   key         [digit j][comp][prime 0..L][N]  (prime L = special P)
+//   plaintexts  [t][limb][N]
+// This unit: BSGS plaintext-ciphertext MAC (Eq. 1 inner sums).
+#include "kinternal.cuh"
+
+namespace ck {
+
+// BSGS inner sums (Eq. 1 inner parenthesis), weights-stationary:
+//   w_k[b] = sum_{j<t1} pt_{k t1 + j} o v_j[b],   v_0 = input ct, v_j = rot_j(input).
+// Thread (coefficient x, giant index k) keeps its t1 plaintext words in registers and loops over the
+// batch, so every plaintext word is read once per launch; v words are shared through L1 by the t2
+// threads of the same coefficient.
+// FP-class limbs (q < 2^45): split-operand FP64 MAC.  Plaintext words a and ciphertext words y are
+// split at 2^23 (a = a1 2^23 + a0, y = y1 2^23 + y0, all parts < 2^23), so every partial product
+// is < 2^46 and the three sums  A = sum a1 y1,  B = sum (a1 y0 + a0 y1),  C = sum a0 y0  over t1 <= 32
+// terms stay below 2^51: exact in FP64 with one DFMA per partial product (4 per MAC, no per-term
+// reduction, accumulator-only dependency chains).  w_k = A 2^46 + B 2^23 + C  mod q at the end.
+// CTA = 8 coefficients x 32 ciphertext lanes; the split plaintext tile [t][8] (double2) is staged once.
+#define MACF_XT 8
+#define MACF_BL 32
+#define MACF_KH 8
+__global__ void __launch_bounds__(MACF_XT * MACF_BL, 2)
+k_bsgs_mac_fp(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_nl, const u64* __restrict__ v0,
+              size_t v0_stride, const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl,
+              int qp)
+{
+    extern __shared__ double2 A2[];
+    const int n = dc->n;
+    const int l = blockIdx.y;                      // limb; QP: limb nl is the special prime
+    const int nlx = nl + qp;
+    const int pidx = l < nl ? l : dc->n_data;
+    const DPrime Pr = dc->p[pidx];
+    if (prime_class(Pr.q) != PC_FP) return;
+    const int tx = threadIdx.x % MACF_XT, ty = threadIdx.x / MACF_XT;
+    const int x0 = blockIdx.x * MACF_XT, x = x0 + tx;
+    const int t = t1 * t2;
+    const u64 mask23 = (1ULL << 23) - 1;
+    for (int i = threadIdx.x; i < t * MACF_XT; i += blockDim.x) {
+        const u64 a = pts[((size_t)(i / MACF_XT) * pt_nl + l) * n + x0 + (i % MACF_XT)];
+        A2[i] = make_double2(u2d(a >> 23), u2d(a & mask23));
+    }
+    __syncthreads();
+    const double q = (double)Pr.q, qinv = 1.0 / q;
+    const double two23 = 8388608.0, two46 = 70368744177664.0;
+    const double w46 = two46 - floor(two46 * qinv) * q;                        // 2^46 mod q (exact)
+    const double w46q = w46 / q, w23q = two23 / q;
+    const size_t ctw = (size_t)2 * nlx * n;
+    const u64 Pm = qp ? dc->qmod[dc->n_data][l < nl ? l : 0] : 0, Pm_sh = qp ? dc->qmod_sh[dc->n_data][l < nl ? l : 0] : 0;
+    for (int b = ty; b < batch; b += MACF_BL) {
+        for (int c = 0; c < 2; ++c) {
+            const size_t off = ((size_t)c * nlx + l) * n + x;
+            const size_t off0 = ((size_t)c * nl + l) * n + x;
+            for (int k0 = 0; k0 < t2; k0 += MACF_KH) {
+                double sA[MACF_KH], sB[MACF_KH], sC[MACF_KH];
+#pragma unroll
+                for (int z = 0; z < MACF_KH; ++z) sA[z] = sB[z] = sC[z] = 0.0;
+                for (int j0 = 0; j0 < t1; j0 += 8) {
+                    double y1[8], y0[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int j = j0 + u;
+                        u64 y = 0;
+                        if (j == 0) {
+                            if (!qp) y = v0[(size_t)b * v0_stride + off0];
+                            else if (l < nl) y = csub(shoup_mul(v0[(size_t)b * v0_stride + off0], Pm, Pm_sh, Pr.q), Pr.q);
+                        } else if (j < t1) {
+                            y = vb[((size_t)(j - 1) * batch + b) * ctw + off];
+                        }
+                        y1[u] = u2d(y >> 23);
+                        y0[u] = u2d(y & mask23);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int j = j0 + u;
+                        if (j < t1) {
+#pragma unroll
+                            for (int z = 0; z < MACF_KH; ++z) {
+                                if (k0 + z < t2) {
+                                    const double2 a = A2[((k0 + z) * t1 + j) * MACF_XT + tx];
+                                    sA[z] = __fma_rn(a.x, y1[u], sA[z]);
+                                    sB[z] = __fma_rn(a.x, y0[u], sB[z]);
+                                    sB[z] = __fma_rn(a.y, y1[u], sB[z]);
+                                    sC[z] = __fma_rn(a.y, y0[u], sC[z]);
+                                }
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int z = 0; z < MACF_KH; ++z) {
+                    if (k0 + z < t2) {
+                        const double r = fmodmul(freduce(sA[z], q, qinv), w46, w46q, q) +
+                                         fmodmul(freduce(sB[z], q, qinv), two23, w23q, q) + freduce(sC[z], q, qinv);
+                        wout[((size_t)(k0 + z) * batch + b) * ctw + off] = fcanon(r, q, qinv);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// BIG-class limbs (60-bit primes): same tiling as k_bsgs_mac_fp with 128-bit integer accumulators.
+__global__ void __launch_bounds__(MACF_XT * MACF_BL, 2)
+k_bsgs_mac_int(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_nl, const u64* __restrict__ v0,
+               size_t v0_stride, const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl,
+               int qp)
+{
+    extern __shared__ u64 Ai[];
+    const int n = dc->n;
+    const int l = blockIdx.y;
+    const int nlx = nl + qp;
+    const int pidx = l < nl ? l : dc->n_data;
+    const DPrime Pr = dc->p[pidx];
+    if (prime_class(Pr.q) == PC_FP) return;
+    const int tx = threadIdx.x % MACF_XT, ty = threadIdx.x / MACF_XT;
+    const int x0 = blockIdx.x * MACF_XT, x = x0 + tx;
+    const int t = t1 * t2;
+    for (int i = threadIdx.x; i < t * MACF_XT; i += blockDim.x)
+        Ai[i] = pts[((size_t)(i / MACF_XT) * pt_nl + l) * n + x0 + (i % MACF_XT)];
+    __syncthreads();
+    const size_t ctw = (size_t)2 * nlx * n;
+    const u64 Pm = qp ? dc->qmod[dc->n_data][l < nl ? l : 0] : 0, Pm_sh = qp ? dc->qmod_sh[dc->n_data][l < nl ? l : 0] : 0;
+    for (int b = ty; b < batch; b += MACF_BL) {
+        for (int c = 0; c < 2; ++c) {
+            const size_t off = ((size_t)c * nlx + l) * n + x;
+            const size_t off0 = ((size_t)c * nl + l) * n + x;
+            for (int k0 = 0; k0 < t2; k0 += MACF_KH) {
+                Acc128 s[MACF_KH];
+#pragma unroll
+                for (int z = 0; z < MACF_KH; ++z) s[z].zero();
+                for (int j0 = 0; j0 < t1; j0 += 8) {
+                    u64 y[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int j = j0 + u;
+                        y[u] = 0;
+                        if (j == 0) {
+                            if (!qp) y[u] = v0[(size_t)b * v0_stride + off0];
+                            else if (l < nl) y[u] = csub(shoup_mul(v0[(size_t)b * v0_stride + off0], Pm, Pm_sh, Pr.q), Pr.q);
+                        } else if (j < t1) {
+                            y[u] = vb[((size_t)(j - 1) * batch + b) * ctw + off];
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        if (j0 + u < t1) {
+#pragma unroll
+                            for (int z = 0; z < MACF_KH; ++z)
+                                if (k0 + z < t2) s[z].mac(Ai[((k0 + z) * t1 + j0 + u) * MACF_XT + tx], y[u]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int z = 0; z < MACF_KH; ++z)
+                    if (k0 + z < t2) wout[((size_t)(k0 + z) * batch + b) * ctw + off] = s[z].reduce(Pr);
+            }
+        }
+    }
+}
+
+// BSGS inner sums on the FP64 tensor cores (DMMA).  For one limb and one coefficient x the inner
+// sums are a small matrix product over the baby-step index j:
+//     W[b][k] = sum_{j<t1} V_j[b] pt_{k t1 + j}        (rows b = ciphertexts, columns k = giant index)
+// computed EXACTLY with mma.sync m16n8k4 f64 on split operands (as k_ks_ip_mma): FP class (q < 2^45)
+// two 23-bit parts and Karatsuba (3 products; every product < 2^47.2, folded mod q every 32 terms so
+// all sums stay < 2^53), BIG/MID class (q < 2^61) three 20-bit parts and 6 Karatsuba products (every
+// sum < 2^50 for t1 <= 256).  CTA = MACM_XT coefficients (one per warp) of one limb and one 8-wide
+// giant-index tile; it streams all ciphertexts in tiles of 16 through a cp.async pipeline of
+// MACM_JC-baby-step stages (each [MACM_JC][2 c][16 b][MACM_XT] words, XOR-swizzled so every fragment
+// load is bank-conflict free), keeps its plaintext tile [t2p][t1][MACM_XT] resident (read once per
+// launch), and writes W through a shared-memory tile as coalesced 64-byte rows.
+#define MACM_XT 8
+#define MACM_JC 4
+#define MACM_ST 4
+#define MACM_THREADS (32 * MACM_XT)
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+// swizzled word index of V element (jj, c, bb, x) in a stage and of pt element (k, j, x) in the tile
+__device__ __forceinline__ int macm_vidx(int jj, int c, int bb, int x)
+{
+    return ((jj * 2 + c) * 16 + bb) * MACM_XT + (x ^ (((jj & 3) << 1) | ((bb >> 1) & 1)));
+}
+__device__ __forceinline__ int macm_pidx(int k, int j, int t1, int x)
+{
+    return (k * t1 + j) * MACM_XT + (x ^ (((k & 3) << 1) | ((j >> 1) & 1)));
+}
+
+template <bool INT>
+__global__ void __launch_bounds__(MACM_THREADS, INT ? 1 : 2)
+k_bsgs_mac_mma(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_nl, const u64* __restrict__ v0,
+               size_t v0_stride, const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl,
+               int qp)
+{
+    constexpr int SV = MACM_JC * 2 * 16 * MACM_XT;          // words per stage
+    extern __shared__ u64 msm[];
+    const int n = dc->n;
+    const int l = blockIdx.y;
+    const int nlx = nl + qp;
+    const int pidx = l < nl ? l : dc->n_data;
+    const DPrime Pr = dc->p[pidx];
+    if ((prime_class(Pr.q) != PC_FP) != INT) return;
+    const int x0 = blockIdx.x * MACM_XT, k0 = blockIdx.z * 8;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int t1p = (t1 + MACM_JC - 1) / MACM_JC * MACM_JC;
+    u64* Ps = msm;                                           // [8][t1p][XT] (k relative to k0)
+    u64* Vs = Ps + 8 * t1p * MACM_XT;                        // [ST][SV]
+    u64* Os = Vs + MACM_ST * SV;                             // [8 k][2 c][16 b][XT]
+    // ---- plaintext tile (zero beyond t1 / t2)
+    for (int i = tid; i < 8 * t1p * MACM_XT; i += MACM_THREADS) {
+        const int x = i % MACM_XT, j = (i / MACM_XT) % t1p, k = i / (MACM_XT * t1p);
+        u64 a = 0;
+        if (j < t1 && k0 + k < t2) a = pts[((size_t)((k0 + k) * t1 + j) * pt_nl + l) * n + x0 + x];
+        Ps[macm_pidx(k, j, t1p, x)] = a;
+    }
+    const size_t ctw = (size_t)2 * nlx * n;
+    const u64 Pm = qp ? dc->qmod[dc->n_data][l < nl ? l : 0] : 0, Pm_sh = qp ? dc->qmod_sh[dc->n_data][l < nl ? l : 0] : 0;
+    const int nbt = (batch + 15) / 16, njc = t1p / MACM_JC, iters = nbt * njc;
+    // stage fill: 4 words per thread; j = 0 comes from the input (times P mod q in the QP basis)
+    auto fill = [&](int it) {
+        u64* S = Vs + (it % MACM_ST) * SV;
+        const int bt = it / njc, jc = it % njc;
+#pragma unroll
+        for (int h = 0; h < SV / MACM_THREADS; ++h) {
+            const int e = tid + h * MACM_THREADS;
+            const int x = e % MACM_XT, row = e / MACM_XT;
+            const int bb = row % 16, c = (row / 16) % 2, jj = row / 32;
+            const int j = jc * MACM_JC + jj, b = bt * 16 + bb;
+            u64* dst = S + macm_vidx(jj, c, bb, x);
+            if (b >= batch || j >= t1) {
+                *dst = 0;
+            } else if (j == 0) {
+                u64 y = 0;
+                if (!qp) y = v0[(size_t)b * v0_stride + ((size_t)c * nl + l) * n + x0 + x];
+                else if (l < nl)
+                    y = csub(shoup_mul(v0[(size_t)b * v0_stride + ((size_t)c * nl + l) * n + x0 + x], Pm, Pm_sh, Pr.q), Pr.q);
+                *dst = y;
+            } else {
+                cp_async8(dst, vb + ((size_t)(j - 1) * batch + b) * ctw + ((size_t)c * nlx + l) * n + x0 + x);
+            }
+        }
+    };
+#pragma unroll
+    for (int s = 0; s < MACM_ST - 1; ++s) {
+        if (s < iters) fill(s);
+        cp_async_commit();
+    }
+    const double q = (double)Pr.q, qinv = 1.0 / q;
+    constexpr int NS = INT ? 6 : 3;
+    double S[NS][2][4];
+    const int x = warp;
+    for (int it = 0; it < iters; ++it) {
+        const int bt = it / njc, jc = it % njc;
+        if (jc == 0) {
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) S[s][c][e] = 0.0;
+        }
+        cp_async_wait<MACM_ST - 2>();
+        __syncthreads();
+        if (it + MACM_ST - 1 < iters) fill(it + MACM_ST - 1);
+        cp_async_commit();
+        const u64* Sv = Vs + (it % MACM_ST) * SV;
+        const int j = jc * MACM_JC + tig;
+        const u64 bv = Ps[macm_pidx(gid, j, t1p, x)];
+        if constexpr (!INT) {
+            const u64 m = (1ULL << 23) - 1;
+            const double bh = u2d(bv >> 23), bl = u2d(bv & m), bs = bh + bl;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const u64 a0 = Sv[macm_vidx(tig, c, gid, x)], a1 = Sv[macm_vidx(tig, c, gid + 8, x)];
+                const double a0h = u2d(a0 >> 23), a0l = u2d(a0 & m), a1h = u2d(a1 >> 23), a1l = u2d(a1 & m);
+                dmma16884(S[2][c], a0h, a1h, bh);
+                dmma16884(S[0][c], a0l, a1l, bl);
+                dmma16884(S[1][c], a0h + a0l, a1h + a1l, bs);
+            }
+            if ((jc & 7) == 7) {                              // fold every 32 terms (exactness, see above)
+#pragma unroll
+                for (int s = 0; s < 3; ++s)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) S[s][c][e] = freduce(S[s][c][e], q, qinv);
+            }
+        } else {
+            const u64 m = (1ULL << 20) - 1;
+            const double y[3] = {u2d(bv & m), u2d((bv >> 20) & m), u2d(bv >> 40)};
+            const double y01 = y[0] + y[1], y12 = y[1] + y[2], y02 = y[0] + y[2];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const u64 a0 = Sv[macm_vidx(tig, c, gid, x)], a1 = Sv[macm_vidx(tig, c, gid + 8, x)];
+                const double p[3] = {u2d(a0 & m), u2d((a0 >> 20) & m), u2d(a0 >> 40)};
+                const double r[3] = {u2d(a1 & m), u2d((a1 >> 20) & m), u2d(a1 >> 40)};
+                dmma16884(S[0][c], p[0], r[0], y[0]);
+                dmma16884(S[1][c], p[1], r[1], y[1]);
+                dmma16884(S[2][c], p[2], r[2], y[2]);
+                dmma16884(S[3][c], p[0] + p[1], r[0] + r[1], y01);
+                dmma16884(S[4][c], p[1] + p[2], r[1] + r[2], y12);
+                dmma16884(S[5][c], p[0] + p[2], r[0] + r[2], y02);
+            }
+        }
+        if (jc == njc - 1) {
+            // recombine mod q: thread holds (b = gid + 8 (e >> 1), k = 2 tig + (e & 1)) for c = 0, 1
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    u64 u;
+                    if constexpr (!INT) {
+                        const double s0 = S[0][c][e], s2 = S[2][c][e], s1 = S[1][c][e] - s2 - s0;
+                        const double r0 = freduce(s0, q, qinv), r1 = freduce(s1, q, qinv), r2 = freduce(s2, q, qinv);
+                        const double two46 = 70368744177664.0;
+                        const double w46 = two46 - floor(two46 * qinv) * q, w46q = w46 / q, c23q = 8388608.0 / q;
+                        const double k1 = __fma_rn(r1, c23q, CK_RND_MAGIC) - CK_RND_MAGIC;
+                        const double tt1 = __fma_rn(-k1, q, r1 * 8388608.0);
+                        const double tt2 = fmodmul(r2, w46, w46q, q);
+                        u = fcanon(tt2 + tt1 + r0, q, qinv);
+                    } else {
+                        const double P0 = S[0][c][e], P1 = S[1][c][e], P2 = S[2][c][e];
+                        const u64 s0 = d2u(P0), s1 = d2u(S[3][c][e] - P0 - P1), s2 = d2u(S[5][c][e] - P0 - P2 + P1),
+                                  s3 = d2u(S[4][c][e] - P1 - P2), s4 = d2u(P2);
+                        u64 lo = s0, hi = 0, add;
+                        add = s1 << 20; lo += add; hi += (lo < add) + (s1 >> 44);
+                        add = s2 << 40; lo += add; hi += (lo < add) + (s2 >> 24);
+                        add = s3 << 60; lo += add; hi += (lo < add) + (s3 >> 4);
+                        hi += s4 << 16;
+                        u = reduce128(hi, lo, Pr);
+                    }
+                    const int bb = gid + 8 * (e >> 1), k = 2 * tig + (e & 1);
+                    const int row = (k * 2 + c) * 16 + bb;
+                    Os[row * MACM_XT + (x ^ ((((row >> 6) & 3) << 1) | ((row >> 1) & 1)))] = u;
+                }
+            __syncthreads();
+            // coalesced write: row (k, c, bb) of MACM_XT words
+            for (int i = tid; i < 8 * 2 * 16 * MACM_XT; i += MACM_THREADS) {
+                const int xx = i % MACM_XT, row = i / MACM_XT;
+                const int bb = row % 16, c = (row / 16) % 2, k = row / 32, b = bt * 16 + bb;
+                if (b < batch && k0 + k < t2)
+                    wout[((size_t)(k0 + k) * batch + b) * ctw + ((size_t)c * nlx + l) * n + x0 + xx] =
+                        Os[row * MACM_XT + (xx ^ ((((row >> 6) & 3) << 1) | ((row >> 1) & 1)))];
+            }
+        }
+    }
+    cp_async_wait<0>();
+}
+
+static size_t mac_mma_smem(int t1)
+{
+    const int t1p = (t1 + MACM_JC - 1) / MACM_JC * MACM_JC;
+    return sizeof(u64) * ((size_t)8 * t1p * MACM_XT + (size_t)MACM_ST * MACM_JC * 2 * 16 * MACM_XT + 8 * 2 * 16 * MACM_XT);
+}
+
+void bsgs_mac(const Launch& L, const uint64_t* pts, int pt_nl, const uint64_t* v0, size_t v0_stride,
+              const uint64_t* vbaby, uint64_t* wout, int t1, int t2, int batch, int nl, bool qp)
+{
+    const int nlx = nl + (qp ? 1 : 0);
+    if (batch <= 0) return;
+    const int n = 1 << L.log_n;
+    static const int use_mma = [] {
+        const char* e = getenv("CKKS_MAC_MMA");
+        return e ? atoi(e) : 1;
+    }();
+    if (use_mma && t1 <= 256 && n >= MACM_XT) {
+        const size_t smem = mac_mma_smem(t1);
+        allow_smem(k_bsgs_mac_mma<true>, smem);
+        allow_smem(k_bsgs_mac_mma<false>, smem);
+        const dim3 grid(n / MACM_XT, nlx, (t2 + 7) / 8);
+        { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_mma_int"); k_bsgs_mac_mma<true><<<grid, MACM_THREADS, smem, L.st>>>(L.dc, pts, pt_nl, v0, v0_stride, vbaby, wout, t1, t2, batch, nl, qp ? 1 : 0); }
+        { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_mma_fp"); k_bsgs_mac_mma<false><<<grid, MACM_THREADS, smem, L.st>>>(L.dc, pts, pt_nl, v0, v0_stride, vbaby, wout, t1, t2, batch, nl, qp ? 1 : 0); }
+        check_launch("bsgs_mac_mma");
+        if (L.counter) *L.counter += 2;
+        return;
+    }
+    if ((size_t)t1 * t2 * MACF_XT * sizeof(double2) > 200 * 1024)
+        throw std::runtime_error("bsgs_mac: plaintext tile too large (t <= 1600)");
+    const size_t smem_int = (size_t)t1 * t2 * MACF_XT * sizeof(u64);
+    allow_smem(k_bsgs_mac_int, smem_int);
+    { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_int"); k_bsgs_mac_int<<<dim3(n / MACF_XT, nlx), MACF_XT * MACF_BL, smem_int, L.st>>>(L.dc, pts, pt_nl, v0, v0_stride, vbaby, wout, t1, t2, batch, nl, qp ? 1 : 0); }
+    const size_t smem_fp = (size_t)t1 * t2 * MACF_XT * sizeof(double2);
+    allow_smem(k_bsgs_mac_fp, smem_fp);
+    { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_fp"); k_bsgs_mac_fp<<<dim3(n / MACF_XT, nlx), MACF_XT * MACF_BL, smem_fp, L.st>>>(L.dc, pts, pt_nl, v0, v0_stride, vbaby, wout, t1, t2, batch, nl, qp ? 1 : 0); }
+    check_launch("bsgs_mac");
+    if (L.counter) *L.counter += 2;
+}
+
+}  // namespace ck

@@ -1,0 +1,100 @@
+// kinternal.cuh -- helpers shared by the kernel translation units (internal).
+#pragma once
+#include "common.cuh"
+#include "ntt.cuh"
+#include "kernels.h"
+#include <algorithm>
+#include <cstdlib>
+#include <stdexcept>
+#include <string>
+
+namespace ck {
+
+// ------------------------------------------------------------------------------------ helpers
+__device__ __forceinline__ const u64* twp(const DCtx* dc, int p) { return dc->tw + (size_t)p * 8 * dc->n; }
+
+// NTT-domain automorphism (R3): out[k] = in[src(k)] with 2 brev(src)+1 = g (2 brev(k)+1) mod 2N
+__device__ __forceinline__ int galois_src(int k, u32 g, int logn)
+{
+    const u32 e = 2u * brev32((u32)k, logn) + 1u;
+    const u32 eg = (e * g) & ((2u << logn) - 1u);
+    return (int)brev32((eg - 1u) >> 1, logn);
+}
+
+static void check_launch(const char* what)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class K>
+static void allow_smem(K kernel, size_t bytes)
+{
+    if (bytes > 48 * 1024) {
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    }
+}
+
+// Threads per CTA of the key-switch NTT kernels: bit set = 32 residues per thread (N/32 threads),
+// clear = 16 (N/16 threads).  bits: 1 digits, 2 ModUp, 4 ModDown iNTT, 8 ModDown NTT.  Default 2;
+// CKKS_NTT_WIDE overrides it (tuning experiments only).
+static int ntt_wide_mask()
+{
+    static int mask = [] {
+        const char* e = getenv("CKKS_NTT_WIDE");
+        return e ? atoi(e) : 2;
+    }();
+    return mask;
+}
+
+#define NTT_DISPATCH(LOGN_VAR, ...)                                                     \
+    switch (LOGN_VAR) {                                                                  \
+    case 10: { constexpr int LG = 10; __VA_ARGS__; } break;                                     \
+    case 11: { constexpr int LG = 11; __VA_ARGS__; } break;                                     \
+    case 12: { constexpr int LG = 12; __VA_ARGS__; } break;                                     \
+    case 13: { constexpr int LG = 13; __VA_ARGS__; } break;                                     \
+    case 14: { constexpr int LG = 14; __VA_ARGS__; } break;                                     \
+    default: throw std::runtime_error("unsupported log_n");                              \
+    }
+
+// ------------------------------------------------------------------------------------ PRNG (R15)
+__device__ __forceinline__ u64 mix64(u64 z)
+{
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ u64 prng(u64 seed, u64 stream, u64 i)
+{
+    const u64 k = mix64(seed ^ mix64(stream));
+    return mix64(k + (i + 1) * 0x9E3779B97F4A7C15ULL);
+}
+__device__ __forceinline__ u64 stream_tag(u64 purpose, u64 id, u64 digit, u64 prime)
+{
+    return (purpose << 56) | ((id & 0xFFFFFFFFFULL) << 20) | ((digit & 0x3FF) << 10) | (prime & 0x3FF);
+}
+__device__ __forceinline__ long long sample_small(const DCtx* dc, int kind, u64 seed, u64 stream, u64 i)
+{
+    const u64 r = prng(seed, stream, i);
+    if (kind == 0) return (long long)(((r >> 32) * 3ULL) >> 32) - 1;   // ternary (R14)
+    const int B = dc->cdt_bound;                                         // CDT Gaussian (R13)
+    long long v = -B;
+    for (int k = 0; k < 2 * B; ++k) v += (r >= dc->cdt[k]) ? 1 : 0;
+    return v;
+}
+__device__ __forceinline__ u64 signed_to_res(long long x, const DPrime& P)
+{
+    if (x >= 0) return reduce64((u64)x, P);
+    const u64 m = reduce64((u64)(-(x + 1)) + 1ULL, P);
+    return m ? P.q - m : 0;
+}
+
+// FP64 tensor-core MMA m16n8k4 (exact for the split-operand products used here)
+__device__ __forceinline__ void dmma16884(double (&c)[4], double a0, double a1, double b0)
+{
+    asm("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+        : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+        : "d"(a0), "d"(a1), "d"(b0));
+}
+
+}  // namespace ck
