@@ -38,13 +38,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
     objs, procs = [], []
+    headers = [d for d in _deps() if not d.endswith(".cu")]
     for src in _sources():
         obj = os.path.join(OUT_DIR, os.path.basename(src) + ".o")
+        objs.append(obj)
+        if not force and os.path.exists(obj) and \
+                all(os.path.getmtime(d) <= os.path.getmtime(obj) for d in headers + [src]):
+            continue                                   # object up to date (incremental rebuild)
         cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT), src))
-        objs.append(obj)
     for p, src in procs:
         out, _ = p.communicate()
         if p.returncode != 0:

@@ -166,20 +166,22 @@ k_bsgs_mac_int(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_
     }
 }
 
-// BSGS inner sums on the FP64 tensor cores (DMMA).  For one limb and one coefficient x the inner
-// sums are a small matrix product over the baby-step index j:
+// BSGS inner sums on the FP64 tensor cores (DMMA).  For one limb, one component c and one
+// coefficient x the inner sums are a small matrix product over the baby-step index j:
 //     W[b][k] = sum_{j<t1} V_j[b] pt_{k t1 + j}        (rows b = ciphertexts, columns k = giant index)
-// computed EXACTLY with mma.sync m16n8k4 f64 on split operands (as k_ks_ip_mma): FP class (q < 2^45)
-// two 23-bit parts and Karatsuba (3 products; every product < 2^47.2, folded mod q every 32 terms so
-// all sums stay < 2^53), BIG/MID class (q < 2^61) three 20-bit parts and 6 Karatsuba products (every
-// sum < 2^50 for t1 <= 256).  CTA = MACM_XT coefficients (one per warp) of one limb and one 8-wide
-// giant-index tile; it streams all ciphertexts in tiles of 16 through a cp.async pipeline of
-// MACM_JC-baby-step stages (each [MACM_JC][2 c][16 b][MACM_XT] words, XOR-swizzled so every fragment
-// load is bank-conflict free), keeps its plaintext tile [t2p][t1][MACM_XT] resident (read once per
-// launch), and writes W through a shared-memory tile as coalesced 64-byte rows.
+// computed EXACTLY with mma.sync m16n8k4 f64 on split operands (as k_ks_ip_mma).  FP class (q < 2^45):
+// two parts at 2^23 and Karatsuba (3 products); every product of part sums is < 2^47.2 (< 2^46.1 for
+// q < 2^41), and the accumulators are folded mod q every 32 (64) terms, so every sum is an exact
+// integer < 2^53.  BIG/MID class (q < 2^61): three 20-bit parts, 6 Karatsuba products, every sum
+// < 2^50 for t1 <= 256.  CTA = MACM_XT coefficients (one per warp) x one limb x one component x one
+// 8-wide giant-index tile; it streams all ciphertexts in tiles of 16 through a cp.async pipeline of
+// MACM_JC-baby-step stages ([MACM_JC][16 b][MACM_XT] words, XOR-swizzled so every fragment load is
+// bank-conflict free), keeps its plaintext tile [8][t1][MACM_XT] resident (read once per launch), and
+// writes W through shared memory as coalesced 64-byte rows.  Each thread copies the same (b, x) for
+// MACM_JC consecutive baby steps, so fill addresses are one pointer plus a constant stride.
 #define MACM_XT 8
-#define MACM_JC 4
-#define MACM_ST 4
+#define MACM_JC 16
+#define MACM_ST 3
 #define MACM_THREADS (32 * MACM_XT)
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem)
@@ -191,10 +193,10 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
-// swizzled word index of V element (jj, c, bb, x) in a stage and of pt element (k, j, x) in the tile
-__device__ __forceinline__ int macm_vidx(int jj, int c, int bb, int x)
+// swizzled word index of V element (jj, bb, x) in a stage and of pt element (k, j, x) in the tile
+__device__ __forceinline__ int macm_vidx(int jj, int bb, int x)
 {
-    return ((jj * 2 + c) * 16 + bb) * MACM_XT + (x ^ (((jj & 3) << 1) | ((bb >> 1) & 1)));
+    return (jj * 16 + bb) * MACM_XT + (x ^ (((jj & 3) << 1) | ((bb >> 1) & 1)));
 }
 __device__ __forceinline__ int macm_pidx(int k, int j, int t1, int x)
 {
@@ -202,12 +204,14 @@ __device__ __forceinline__ int macm_pidx(int k, int j, int t1, int x)
 }
 
 template <bool INT>
-__global__ void __launch_bounds__(MACM_THREADS, INT ? 1 : 2)
+__global__ void __launch_bounds__(MACM_THREADS, 2)
 k_bsgs_mac_mma(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_nl, const u64* __restrict__ v0,
                size_t v0_stride, const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl,
                int qp)
 {
-    constexpr int SV = MACM_JC * 2 * 16 * MACM_XT;          // words per stage
+    constexpr int SV = MACM_JC * 16 * MACM_XT;               // words per stage
+    constexpr int EPT = SV / MACM_THREADS;                   // words per thread per stage (= MACM_JC / 2)
+    static_assert(MACM_THREADS / MACM_XT == 32 && EPT * 2 == MACM_JC, "fill mapping");
     extern __shared__ u64 msm[];
     const int n = dc->n;
     const int l = blockIdx.y;
@@ -215,13 +219,13 @@ k_bsgs_mac_mma(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_
     const int pidx = l < nl ? l : dc->n_data;
     const DPrime Pr = dc->p[pidx];
     if ((prime_class(Pr.q) != PC_FP) != INT) return;
-    const int x0 = blockIdx.x * MACM_XT, k0 = blockIdx.z * 8;
+    const int x0 = blockIdx.x * MACM_XT, c = blockIdx.z & 1, k0 = (blockIdx.z >> 1) * 8;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gid = lane >> 2, tig = lane & 3;
     const int t1p = (t1 + MACM_JC - 1) / MACM_JC * MACM_JC;
     u64* Ps = msm;                                           // [8][t1p][XT] (k relative to k0)
     u64* Vs = Ps + 8 * t1p * MACM_XT;                        // [ST][SV]
-    u64* Os = Vs + MACM_ST * SV;                             // [8 k][2 c][16 b][XT]
+    u64* Os = Vs + MACM_ST * SV;                             // [8 k][16 b][XT]
     // ---- plaintext tile (zero beyond t1 / t2)
     for (int i = tid; i < 8 * t1p * MACM_XT; i += MACM_THREADS) {
         const int x = i % MACM_XT, j = (i / MACM_XT) % t1p, k = i / (MACM_XT * t1p);
@@ -229,30 +233,38 @@ k_bsgs_mac_mma(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_
         if (j < t1 && k0 + k < t2) a = pts[((size_t)((k0 + k) * t1 + j) * pt_nl + l) * n + x0 + x];
         Ps[macm_pidx(k, j, t1p, x)] = a;
     }
-    const size_t ctw = (size_t)2 * nlx * n;
+    const size_t ctw = (size_t)2 * nlx * n, jstride = (size_t)batch * ctw;
     const u64 Pm = qp ? dc->qmod[dc->n_data][l < nl ? l : 0] : 0, Pm_sh = qp ? dc->qmod_sh[dc->n_data][l < nl ? l : 0] : 0;
     const int nbt = (batch + 15) / 16, njc = t1p / MACM_JC, iters = nbt * njc;
-    // stage fill: 4 words per thread; j = 0 comes from the input (times P mod q in the QP basis)
+    // fill mapping: thread -> (x, bb, half) copies baby steps jj = half * EPT + h, h < EPT
+    const int fx = tid % MACM_XT, fbb = (tid / MACM_XT) % 16, fhalf = tid / (MACM_XT * 16);
+    const size_t foff = ((size_t)c * nlx + l) * n + x0 + fx;
     auto fill = [&](int it) {
         u64* S = Vs + (it % MACM_ST) * SV;
-        const int bt = it / njc, jc = it % njc;
+        const int bt = it / njc, jc = it - bt * njc;
+        const int b = bt * 16 + fbb, jb = jc * MACM_JC + fhalf * EPT;
+        const bool fast = b < batch && jb >= 1 && jb + EPT <= t1;
+        if (fast) {
+            const u64* src = vb + ((size_t)(jb - 1) * batch + b) * ctw + foff;
 #pragma unroll
-        for (int h = 0; h < SV / MACM_THREADS; ++h) {
-            const int e = tid + h * MACM_THREADS;
-            const int x = e % MACM_XT, row = e / MACM_XT;
-            const int bb = row % 16, c = (row / 16) % 2, jj = row / 32;
-            const int j = jc * MACM_JC + jj, b = bt * 16 + bb;
-            u64* dst = S + macm_vidx(jj, c, bb, x);
-            if (b >= batch || j >= t1) {
-                *dst = 0;
-            } else if (j == 0) {
-                u64 y = 0;
-                if (!qp) y = v0[(size_t)b * v0_stride + ((size_t)c * nl + l) * n + x0 + x];
-                else if (l < nl)
-                    y = csub(shoup_mul(v0[(size_t)b * v0_stride + ((size_t)c * nl + l) * n + x0 + x], Pm, Pm_sh, Pr.q), Pr.q);
-                *dst = y;
-            } else {
-                cp_async8(dst, vb + ((size_t)(j - 1) * batch + b) * ctw + ((size_t)c * nlx + l) * n + x0 + x);
+            for (int h = 0; h < EPT; ++h) cp_async8(S + macm_vidx(fhalf * EPT + h, fbb, fx), src + h * jstride);
+        } else {
+#pragma unroll
+            for (int h = 0; h < EPT; ++h) {
+                const int j = jb + h;
+                u64* dst = S + macm_vidx(fhalf * EPT + h, fbb, fx);
+                if (b >= batch || j >= t1) {
+                    *dst = 0;
+                } else if (j == 0) {
+                    u64 y = 0;
+                    if (!qp) y = v0[(size_t)b * v0_stride + ((size_t)c * nl + l) * n + x0 + fx];
+                    else if (l < nl)
+                        y = csub(shoup_mul(v0[(size_t)b * v0_stride + ((size_t)c * nl + l) * n + x0 + fx], Pm, Pm_sh, Pr.q),
+                                 Pr.q);
+                    *dst = y;
+                } else {
+                    cp_async8(dst, vb + ((size_t)(j - 1) * batch + b) * ctw + foff);
+                }
             }
         }
     };
@@ -262,102 +274,97 @@ k_bsgs_mac_mma(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_
         cp_async_commit();
     }
     const double q = (double)Pr.q, qinv = 1.0 / q;
+    // fold interval in k-steps of 4 terms (FP class only): 64 terms for q < 2^41, else 32
+    const int fold_ks = Pr.q < (1ULL << 41) ? 16 : 8;
     constexpr int NS = INT ? 6 : 3;
-    double S[NS][2][4];
+    constexpr int KS = MACM_JC / 4;                          // k-steps per stage
+    double S[NS][4];
     const int x = warp;
-    for (int it = 0; it < iters; ++it) {
-        const int bt = it / njc, jc = it % njc;
-        if (jc == 0) {
+    const int xsw = x ^ (((gid & 3) << 1) | ((tig >> 1) & 1));   // pt swizzle (j >> 1 & 1 == tig >> 1 & 1)
+    const u64* Pw = Ps + (size_t)gid * t1p * MACM_XT + xsw;
+    int it = 0;
+    for (int bt = 0; bt < nbt; ++bt) {
 #pragma unroll
-            for (int s = 0; s < NS; ++s)
+        for (int s = 0; s < NS; ++s)
 #pragma unroll
-                for (int c = 0; c < 2; ++c)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) S[s][c][e] = 0.0;
-        }
-        cp_async_wait<MACM_ST - 2>();
-        __syncthreads();
-        if (it + MACM_ST - 1 < iters) fill(it + MACM_ST - 1);
-        cp_async_commit();
-        const u64* Sv = Vs + (it % MACM_ST) * SV;
-        const int j = jc * MACM_JC + tig;
-        const u64 bv = Ps[macm_pidx(gid, j, t1p, x)];
-        if constexpr (!INT) {
-            const u64 m = (1ULL << 23) - 1;
-            const double bh = u2d(bv >> 23), bl = u2d(bv & m), bs = bh + bl;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const u64 a0 = Sv[macm_vidx(tig, c, gid, x)], a1 = Sv[macm_vidx(tig, c, gid + 8, x)];
-                const double a0h = u2d(a0 >> 23), a0l = u2d(a0 & m), a1h = u2d(a1 >> 23), a1l = u2d(a1 & m);
-                dmma16884(S[2][c], a0h, a1h, bh);
-                dmma16884(S[0][c], a0l, a1l, bl);
-                dmma16884(S[1][c], a0h + a0l, a1h + a1l, bs);
-            }
-            if ((jc & 7) == 7) {                              // fold every 32 terms (exactness, see above)
-#pragma unroll
-                for (int s = 0; s < 3; ++s)
-#pragma unroll
-                    for (int c = 0; c < 2; ++c)
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) S[s][c][e] = freduce(S[s][c][e], q, qinv);
-            }
-        } else {
-            const u64 m = (1ULL << 20) - 1;
-            const double y[3] = {u2d(bv & m), u2d((bv >> 20) & m), u2d(bv >> 40)};
-            const double y01 = y[0] + y[1], y12 = y[1] + y[2], y02 = y[0] + y[2];
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const u64 a0 = Sv[macm_vidx(tig, c, gid, x)], a1 = Sv[macm_vidx(tig, c, gid + 8, x)];
-                const double p[3] = {u2d(a0 & m), u2d((a0 >> 20) & m), u2d(a0 >> 40)};
-                const double r[3] = {u2d(a1 & m), u2d((a1 >> 20) & m), u2d(a1 >> 40)};
-                dmma16884(S[0][c], p[0], r[0], y[0]);
-                dmma16884(S[1][c], p[1], r[1], y[1]);
-                dmma16884(S[2][c], p[2], r[2], y[2]);
-                dmma16884(S[3][c], p[0] + p[1], r[0] + r[1], y01);
-                dmma16884(S[4][c], p[1] + p[2], r[1] + r[2], y12);
-                dmma16884(S[5][c], p[0] + p[2], r[0] + r[2], y02);
-            }
-        }
-        if (jc == njc - 1) {
-            // recombine mod q: thread holds (b = gid + 8 (e >> 1), k = 2 tig + (e & 1)) for c = 0, 1
-#pragma unroll
-            for (int c = 0; c < 2; ++c)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    u64 u;
-                    if constexpr (!INT) {
-                        const double s0 = S[0][c][e], s2 = S[2][c][e], s1 = S[1][c][e] - s2 - s0;
-                        const double r0 = freduce(s0, q, qinv), r1 = freduce(s1, q, qinv), r2 = freduce(s2, q, qinv);
-                        const double two46 = 70368744177664.0;
-                        const double w46 = two46 - floor(two46 * qinv) * q, w46q = w46 / q, c23q = 8388608.0 / q;
-                        const double k1 = __fma_rn(r1, c23q, CK_RND_MAGIC) - CK_RND_MAGIC;
-                        const double tt1 = __fma_rn(-k1, q, r1 * 8388608.0);
-                        const double tt2 = fmodmul(r2, w46, w46q, q);
-                        u = fcanon(tt2 + tt1 + r0, q, qinv);
-                    } else {
-                        const double P0 = S[0][c][e], P1 = S[1][c][e], P2 = S[2][c][e];
-                        const u64 s0 = d2u(P0), s1 = d2u(S[3][c][e] - P0 - P1), s2 = d2u(S[5][c][e] - P0 - P2 + P1),
-                                  s3 = d2u(S[4][c][e] - P1 - P2), s4 = d2u(P2);
-                        u64 lo = s0, hi = 0, add;
-                        add = s1 << 20; lo += add; hi += (lo < add) + (s1 >> 44);
-                        add = s2 << 40; lo += add; hi += (lo < add) + (s2 >> 24);
-                        add = s3 << 60; lo += add; hi += (lo < add) + (s3 >> 4);
-                        hi += s4 << 16;
-                        u = reduce128(hi, lo, Pr);
-                    }
-                    const int bb = gid + 8 * (e >> 1), k = 2 * tig + (e & 1);
-                    const int row = (k * 2 + c) * 16 + bb;
-                    Os[row * MACM_XT + (x ^ ((((row >> 6) & 3) << 1) | ((row >> 1) & 1)))] = u;
-                }
+            for (int e = 0; e < 4; ++e) S[s][e] = 0.0;
+        for (int jc = 0; jc < njc; ++jc, ++it) {
+            cp_async_wait<MACM_ST - 2>();
             __syncthreads();
-            // coalesced write: row (k, c, bb) of MACM_XT words
-            for (int i = tid; i < 8 * 2 * 16 * MACM_XT; i += MACM_THREADS) {
-                const int xx = i % MACM_XT, row = i / MACM_XT;
-                const int bb = row % 16, c = (row / 16) % 2, k = row / 32, b = bt * 16 + bb;
-                if (b < batch && k0 + k < t2)
-                    wout[((size_t)(k0 + k) * batch + b) * ctw + ((size_t)c * nlx + l) * n + x0 + xx] =
-                        Os[row * MACM_XT + (xx ^ ((((row >> 6) & 3) << 1) | ((row >> 1) & 1)))];
+            if (it + MACM_ST - 1 < iters) fill(it + MACM_ST - 1);
+            cp_async_commit();
+            const u64* Sv = Vs + (it % MACM_ST) * SV;
+#pragma unroll
+            for (int kq = 0; kq < KS; ++kq) {
+                const int jj = kq * 4 + tig;
+                const u64 bv = Pw[(size_t)(jc * MACM_JC + jj) * MACM_XT];
+                const u64 a0 = Sv[macm_vidx(jj, gid, x)], a1 = Sv[macm_vidx(jj, gid + 8, x)];
+                if constexpr (!INT) {
+                    const u64 m = (1ULL << 23) - 1;
+                    const double bh = u2d(bv >> 23), bl = u2d(bv & m);
+                    const double a0h = u2d(a0 >> 23), a0l = u2d(a0 & m), a1h = u2d(a1 >> 23), a1l = u2d(a1 & m);
+                    dmma16884(S[2], a0h, a1h, bh);
+                    dmma16884(S[0], a0l, a1l, bl);
+                    dmma16884(S[1], a0h + a0l, a1h + a1l, bh + bl);
+                } else {
+                    const u64 m = (1ULL << 20) - 1;
+                    const double y[3] = {u2d(bv & m), u2d((bv >> 20) & m), u2d(bv >> 40)};
+                    const double p[3] = {u2d(a0 & m), u2d((a0 >> 20) & m), u2d(a0 >> 40)};
+                    const double r[3] = {u2d(a1 & m), u2d((a1 >> 20) & m), u2d(a1 >> 40)};
+                    dmma16884(S[0], p[0], r[0], y[0]);
+                    dmma16884(S[1], p[1], r[1], y[1]);
+                    dmma16884(S[2], p[2], r[2], y[2]);
+                    dmma16884(S[3], p[0] + p[1], r[0] + r[1], y[0] + y[1]);
+                    dmma16884(S[4], p[1] + p[2], r[1] + r[2], y[1] + y[2]);
+                    dmma16884(S[5], p[0] + p[2], r[0] + r[2], y[0] + y[2]);
+                }
+                if constexpr (!INT) {
+                    const int ks = jc * KS + kq + 1;              // k-steps accumulated so far
+                    if (ks % fold_ks == 0 && ks * 4 < t1p) {      // fold (exactness, see above)
+#pragma unroll
+                        for (int s = 0; s < 3; ++s)
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) S[s][e] = freduce(S[s][e], q, qinv);
+                    }
+                }
             }
+        }
+        // recombine mod q: thread holds (b = gid + 8 (e >> 1), k = 2 tig + (e & 1))
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            u64 u;
+            if constexpr (!INT) {
+                const double s0 = S[0][e], s2 = S[2][e], s1 = S[1][e] - s2 - s0;
+                const double r0 = freduce(s0, q, qinv), r1 = freduce(s1, q, qinv), r2 = freduce(s2, q, qinv);
+                const double two46 = 70368744177664.0;
+                const double w46 = two46 - floor(two46 * qinv) * q, w46q = w46 / q, c23q = 8388608.0 / q;
+                const double k1 = __fma_rn(r1, c23q, CK_RND_MAGIC) - CK_RND_MAGIC;
+                const double tt1 = __fma_rn(-k1, q, r1 * 8388608.0);
+                const double tt2 = fmodmul(r2, w46, w46q, q);
+                u = fcanon(tt2 + tt1 + r0, q, qinv);
+            } else {
+                const double P0 = S[0][e], P1 = S[1][e], P2 = S[2][e];
+                const u64 s0 = d2u(P0), s1 = d2u(S[3][e] - P0 - P1), s2 = d2u(S[5][e] - P0 - P2 + P1),
+                          s3 = d2u(S[4][e] - P1 - P2), s4 = d2u(P2);
+                u64 lo = s0, hi = 0, add;
+                add = s1 << 20; lo += add; hi += (lo < add) + (s1 >> 44);
+                add = s2 << 40; lo += add; hi += (lo < add) + (s2 >> 24);
+                add = s3 << 60; lo += add; hi += (lo < add) + (s3 >> 4);
+                hi += s4 << 16;
+                u = reduce128(hi, lo, Pr);
+            }
+            const int bb = gid + 8 * (e >> 1), k = 2 * tig + (e & 1);
+            const int row = k * 16 + bb;
+            Os[row * MACM_XT + (x ^ ((((row >> 5) & 3) << 1) | ((row >> 1) & 1)))] = u;
+        }
+        __syncthreads();
+        // coalesced write: row (k, bb) of MACM_XT words
+        for (int i = tid; i < 8 * 16 * MACM_XT; i += MACM_THREADS) {
+            const int xx = i % MACM_XT, row = i / MACM_XT;
+            const int bb = row % 16, k = row / 16, b = bt * 16 + bb;
+            if (b < batch && k0 + k < t2)
+                wout[((size_t)(k0 + k) * batch + b) * ctw + ((size_t)c * nlx + l) * n + x0 + xx] =
+                    Os[row * MACM_XT + (xx ^ ((((row >> 5) & 3) << 1) | ((row >> 1) & 1)))];
         }
     }
     cp_async_wait<0>();
@@ -366,7 +373,7 @@ k_bsgs_mac_mma(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_
 static size_t mac_mma_smem(int t1)
 {
     const int t1p = (t1 + MACM_JC - 1) / MACM_JC * MACM_JC;
-    return sizeof(u64) * ((size_t)8 * t1p * MACM_XT + (size_t)MACM_ST * MACM_JC * 2 * 16 * MACM_XT + 8 * 2 * 16 * MACM_XT);
+    return sizeof(u64) * ((size_t)8 * t1p * MACM_XT + (size_t)MACM_ST * MACM_JC * 16 * MACM_XT + 8 * 16 * MACM_XT);
 }
 
 void bsgs_mac(const Launch& L, const uint64_t* pts, int pt_nl, const uint64_t* v0, size_t v0_stride,
@@ -383,7 +390,7 @@ void bsgs_mac(const Launch& L, const uint64_t* pts, int pt_nl, const uint64_t* v
         const size_t smem = mac_mma_smem(t1);
         allow_smem(k_bsgs_mac_mma<true>, smem);
         allow_smem(k_bsgs_mac_mma<false>, smem);
-        const dim3 grid(n / MACM_XT, nlx, (t2 + 7) / 8);
+        const dim3 grid(n / MACM_XT, nlx, 2 * ((t2 + 7) / 8));
         { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_mma_int"); k_bsgs_mac_mma<true><<<grid, MACM_THREADS, smem, L.st>>>(L.dc, pts, pt_nl, v0, v0_stride, vbaby, wout, t1, t2, batch, nl, qp ? 1 : 0); }
         { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_mma_fp"); k_bsgs_mac_mma<false><<<grid, MACM_THREADS, smem, L.st>>>(L.dc, pts, pt_nl, v0, v0_stride, vbaby, wout, t1, t2, batch, nl, qp ? 1 : 0); }
         check_launch("bsgs_mac_mma");

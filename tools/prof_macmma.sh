@@ -1,7 +1,7 @@
 # ncu --set full of the DMMA BSGS MAC kernels (fp and int class), one launch each
 P="python tools/profile_forward.py --mode forward --batch 256"
 $P > gpurun_out/pf.log 2>&1 || exit 1
-for spec in "k_bsgs_mac_mma<false>:macmma_fp" "k_bsgs_mac_mma<true>:macmma_int"; do
+for spec in "k_bsgs_mac_mma<.bool.0:macmma_fp" "k_bsgs_mac_mma<.bool.1:macmma_int"; do
   re=${spec%%:*}; tag=${spec##*:}
   ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$re" -c 1 -o gpurun_out/prof_$tag $P > gpurun_out/ncu_$tag.log 2>&1
   ncu -i gpurun_out/prof_$tag.ncu-rep --page raw --csv > gpurun_out/prof_${tag}_raw.csv 2>&1
