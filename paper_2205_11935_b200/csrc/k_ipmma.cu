@@ -1,0 +1,268 @@
+// k_ipmma.cu -- sm_100a kernel of the CKKS encrypted-dense-layer hot path: the hoisted baby-step
+// key-switch inner product in the Q_l P basis (double hoisting, R11c) on the FP64 tensor
+// cores.  Layouts:
+//   ModUp output  [b][digit j][row 0..nl][N]   (row nl = special prime P)
+//   key           [digit j][comp][prime 0..L][N]  (pre-permuted by sigma_g^{-1})
+//   baby output   [b][comp][row 0..nl][N]   (Q_l P basis, sigma_g-permuted)
+#include "kinternal.cuh"
+
+namespace ck {
+
+// For one row i (prime) and one coefficient k the group's inner products are a small matrix product
+//     U[b][(g, c)] = sum_{j < nl} D_{b,j}[k] key_{g,j,c}[k]     (16 ciphertexts x 2G columns x K = nl)
+// computed EXACTLY with mma.sync m16n8k4 f64 on split operands: q < 2^45 two 23-bit parts and
+// Karatsuba (3 products, every sum < 2^53 for nl <= 16), 60-bit primes three 20-bit parts and 6
+// products.  The split sums are recombined mod q per output, the addend P c0 is added, and the
+// result is written through the sigma_g block permutation (aligned IP2_KT-blocks of NTT indices map
+// onto aligned blocks).
+//
+// Pipelined form: one CTA owns one row and IP2_KT coefficients and streams every ciphertext of the
+// batch in tiles of 16 through a cp.async pipeline (D tile + raw c0 addend per stage), so its key
+// tile (all digits, all G rotations, both components) is read once per launch and, for the FP class,
+// split once into registers; loads of the next tile overlap the DMMA work and the permuted stores
+// of the current one.
+#define IP2_KT 16
+#define IP2_THREADS 256
+#define IP2_ST 3
+
+__device__ __forceinline__ void ip2_cp8(void* smem, const void* gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void ip2_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void ip2_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+template <int NL>
+struct Ip2Shape {
+    static constexpr int NLP = (NL + 3) & ~3;              // K padded to the MMA k-step
+    static constexpr int JS = IP2_KT * 16 + 4;             // j stride (words) of the swizzled tiles
+    static constexpr int SD = NLP * JS + IP2_KT * 16;      // words per stage: D tile + c0 addend
+    static constexpr size_t smem = sizeof(u64) * ((size_t)NLP * JS + (size_t)IP2_ST * SD + 8 * 2 * 16 * IP2_KT);
+};
+
+template <int NL, bool INT>
+__global__ void __launch_bounds__(IP2_THREADS, 2)
+k_ks_ip_mma2(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ in, size_t ct_stride,
+             size_t comp_off, const KsGroup grp, int L, int special, size_t out_stride, int B)
+{
+    constexpr int nl = NL;
+    constexpr int NLP = Ip2Shape<NL>::NLP, JS = Ip2Shape<NL>::JS, SD = Ip2Shape<NL>::SD;
+    constexpr int KPW = IP2_KT / (IP2_THREADS / 32);       // coefficients per warp
+    constexpr bool CACHE = !INT && NLP <= 8;               // FP class: split key fragments held in registers
+    extern __shared__ u64 sm[];
+    u64* Ks = sm;                                          // [NLP][KT][16 n]  n = 2 g + c  (n ^ kk swizzle)
+    u64* Dst = Ks + NLP * JS;                              // [ST][ D [NLP][KT][16 b] | c0 [KT][16 b] ]
+    u64* Os = Dst + IP2_ST * SD;                           // [8 g][2 c][16 b][KT]
+    const int n = dc->n, logn = dc->log_n;
+    const int i = blockIdx.y, k0 = blockIdx.x * IP2_KT;
+    const bool prow = (i == nl);
+    const int p = prow ? special : i;
+    const int krow = prow ? L : i;
+    const DPrime Pr = dc->p[p];
+    if ((prime_class(Pr.q) != PC_FP) != INT) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int G = grp.G;
+    const int nbt = (B + 15) / 16;
+    // ---- stage fill: thread = (coefficient fk, ciphertext row fr); digits j stride (nl+1) N
+    const int fk = tid % IP2_KT, fr = tid / IP2_KT;
+    auto fill = [&](int bt) {
+        u64* S = Dst + (bt % IP2_ST) * SD;
+        const int b = bt * 16 + fr;
+        if (b < B) {
+            const u64* dsrc = modup + (((size_t)b * nl) * (nl + 1) + i) * n + k0 + fk;
+            const u64* isrc = in + (size_t)b * ct_stride + (size_t)i * n + k0 + fk;
+#pragma unroll
+            for (int j = 0; j < NL; ++j)
+                ip2_cp8(S + j * JS + fk * 16 + (fr ^ fk), (j == i) ? isrc + comp_off : dsrc + (size_t)j * (nl + 1) * n);
+            if (!prow) ip2_cp8(S + NLP * JS + fk * 16 + fr, isrc);
+            else S[NLP * JS + fk * 16 + fr] = 0;
+        } else {
+#pragma unroll
+            for (int j = 0; j < NL; ++j) S[j * JS + fk * 16 + (fr ^ fk)] = 0;
+            S[NLP * JS + fk * 16 + fr] = 0;
+        }
+#pragma unroll
+        for (int j = NL; j < NLP; ++j) S[j * JS + fk * 16 + (fr ^ fk)] = 0;
+    };
+#pragma unroll
+    for (int s = 0; s < IP2_ST - 1; ++s) {
+        if (s < nbt) fill(s);
+        ip2_commit();
+    }
+    // ---- key tile (once): rows n = 2 g + c
+    for (int e = tid; e < NLP * IP2_KT * 16; e += IP2_THREADS) {
+        const int j = e / (IP2_KT * 16), rem = e % (IP2_KT * 16), kk = rem % IP2_KT, r = rem / IP2_KT;
+        const int g = r >> 1, c = r & 1;
+        u64 v = 0;
+        if (j < NL && g < G) v = grp.key[g][((size_t)j * 2 * (L + 1) + (size_t)c * (L + 1) + krow) * n + k0 + kk];
+        Ks[j * JS + kk * 16 + (r ^ kk)] = v;
+    }
+    __syncthreads();
+    const double q = (double)Pr.q, qinv = 1.0 / q;
+    const double two46 = 70368744177664.0;
+    const double w46 = two46 - floor(two46 * qinv) * q, w46q = w46 / q, c23q = 8388608.0 / q;
+    const u64 Pm = prow ? 0 : dc->qmod[special][i], Pm_sh = prow ? 0 : dc->qmod_sh[special][i];
+    const u64 m23 = (1ULL << 23) - 1;
+    // FP class: split key fragments [kq][kb][t] -> (hi, lo, hi + lo), loaded once
+    double kf[CACHE ? KPW : 1][CACHE ? NLP / 4 : 1][2][3];
+    if constexpr (CACHE) {
+#pragma unroll
+        for (int kq = 0; kq < KPW; ++kq) {
+            const int kk = warp * KPW + kq;
+#pragma unroll
+            for (int kb = 0; kb < NLP / 4; ++kb)
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    const u64 bv = Ks[(kb * 4 + tig) * JS + kk * 16 + ((t * 8 + gid) ^ kk)];
+                    const double bh = u2d(bv >> 23), bl = u2d(bv & m23);
+                    kf[kq][kb][t][0] = bh;
+                    kf[kq][kb][t][1] = bl;
+                    kf[kq][kb][t][2] = bh + bl;
+                }
+        }
+    }
+    for (int bt = 0; bt < nbt; ++bt) {
+        ip2_wait<IP2_ST - 2>();
+        __syncthreads();
+        if (bt + IP2_ST - 1 < nbt) fill(bt + IP2_ST - 1);
+        ip2_commit();
+        const u64* Ds = Dst + (bt % IP2_ST) * SD;
+        const u64* As = Ds + NLP * JS;
+#pragma unroll
+        for (int kq = 0; kq < KPW; ++kq) {
+            const int kk = warp * KPW + kq;
+            constexpr int NS = INT ? 6 : 3;
+            double S[NS][2][4];
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+#pragma unroll
+                for (int t = 0; t < 2; ++t)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) S[s][t][e] = 0.0;
+#pragma unroll
+            for (int kb = 0; kb < NLP / 4; ++kb) {
+                const int j = kb * 4 + tig;
+                const u64 a0 = Ds[j * JS + kk * 16 + (gid ^ kk)], a1 = Ds[j * JS + kk * 16 + ((gid + 8) ^ kk)];
+                if constexpr (!INT) {
+                    const double a0h = u2d(a0 >> 23), a0l = u2d(a0 & m23), a1h = u2d(a1 >> 23), a1l = u2d(a1 & m23);
+                    const double a0s = a0h + a0l, a1s = a1h + a1l;
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        double bh, bl, bs;
+                        if constexpr (CACHE) {
+                            bh = kf[kq][kb][t][0];
+                            bl = kf[kq][kb][t][1];
+                            bs = kf[kq][kb][t][2];
+                        } else {
+                            const u64 bv = Ks[j * JS + kk * 16 + ((t * 8 + gid) ^ kk)];
+                            bh = u2d(bv >> 23);
+                            bl = u2d(bv & m23);
+                            bs = bh + bl;
+                        }
+                        dmma16884(S[2][t], a0h, a1h, bh);
+                        dmma16884(S[0][t], a0l, a1l, bl);
+                        dmma16884(S[1][t], a0s, a1s, bs);
+                    }
+                } else {
+                    const u64 m = (1ULL << 20) - 1;
+                    const double x0[3] = {u2d(a0 & m), u2d((a0 >> 20) & m), u2d(a0 >> 40)};
+                    const double x1[3] = {u2d(a1 & m), u2d((a1 >> 20) & m), u2d(a1 >> 40)};
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        const u64 bv = Ks[j * JS + kk * 16 + ((t * 8 + gid) ^ kk)];
+                        const double y[3] = {u2d(bv & m), u2d((bv >> 20) & m), u2d(bv >> 40)};
+                        dmma16884(S[0][t], x0[0], x1[0], y[0]);
+                        dmma16884(S[1][t], x0[1], x1[1], y[1]);
+                        dmma16884(S[2][t], x0[2], x1[2], y[2]);
+                        dmma16884(S[3][t], x0[0] + x0[1], x1[0] + x1[1], y[0] + y[1]);
+                        dmma16884(S[4][t], x0[1] + x0[2], x1[1] + x1[2], y[1] + y[2]);
+                        dmma16884(S[5][t], x0[0] + x0[2], x1[0] + x1[2], y[0] + y[2]);
+                    }
+                }
+            }
+            // outputs of this thread: (b = gid + 8 (e >> 1), n = 8 t + 2 tig + (e & 1)) -> g = 4 t + tig, c = e & 1
+#pragma unroll
+            for (int t = 0; t < 2; ++t)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int bl = gid + 8 * (e >> 1), g = 4 * t + tig, c = e & 1;
+                    u64 u;
+                    if constexpr (!INT) {
+                        const double s0 = S[0][t][e], s2 = S[2][t][e], s1 = S[1][t][e] - s2 - s0;   // Karatsuba middle
+                        const double r0 = freduce(s0, q, qinv), r1 = freduce(s1, q, qinv), r2 = freduce(s2, q, qinv);
+                        const double k1 = __fma_rn(r1, c23q, CK_RND_MAGIC) - CK_RND_MAGIC;
+                        const double t1 = __fma_rn(-k1, q, r1 * 8388608.0);
+                        const double t2 = fmodmul(r2, w46, w46q, q);
+                        u = fcanon(t2 + t1 + r0, q, qinv);
+                    } else {
+                        const double P0 = S[0][t][e], P1 = S[1][t][e], P2 = S[2][t][e];
+                        const u64 s0 = d2u(P0), s1 = d2u(S[3][t][e] - P0 - P1), s2 = d2u(S[5][t][e] - P0 - P2 + P1),
+                                  s3 = d2u(S[4][t][e] - P1 - P2), s4 = d2u(P2);
+                        u64 lo = s0, hi = 0, add;
+                        add = s1 << 20; lo += add; hi += (lo < add) + (s1 >> 44);
+                        add = s2 << 40; lo += add; hi += (lo < add) + (s2 >> 24);
+                        add = s3 << 60; lo += add; hi += (lo < add) + (s3 >> 4);
+                        hi += s4 << 16;
+                        u = reduce128(hi, lo, Pr);
+                    }
+                    if (c == 0 && !prow) u = addmod(u, csub(shoup_mul(As[kk * 16 + bl], Pm, Pm_sh, Pr.q), Pr.q), Pr.q);
+                    if (g < G) Os[((g * 2 + c) * 16 + bl) * IP2_KT + (kk ^ ((bl + 4 * g) & 15))] = u;
+                }
+        }
+        __syncthreads();
+        // ---- permuted, coalesced write: row (g, c, b) of IP2_KT destination words per 16 lanes
+        {
+            const int t = tid % IP2_KT, r0 = tid / IP2_KT;   // r0 in [0, 16): rows r0, r0 + 16
+            for (int g = 0; g < G; ++g) {
+                const u32 gp = grp.scatter[g];
+                int dblk = blockIdx.x, sidx = t;
+                if (gp) {
+                    dblk = galois_src(k0, grp.ginv[g], logn) / IP2_KT;
+                    sidx = galois_src(dblk * IP2_KT + t, gp, logn) - k0;
+                }
+                u64* og = grp.out[g] + (size_t)i * n + (size_t)dblk * IP2_KT + t;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int rr = r0 + 16 * h;            // rr = c * 16 + bl
+                    const int c = rr >> 4, bl = rr & 15, b = bt * 16 + bl;
+                    if (b < B)
+                        og[(size_t)b * out_stride + (size_t)c * (nl + 1) * n] =
+                            Os[((g * 2 + c) * 16 + bl) * IP2_KT + (sidx ^ ((bl + 4 * g) & 15))];
+                }
+            }
+        }
+    }
+    ip2_wait<0>();
+}
+
+// host launcher: both prime classes of a baby-step group (scatter outputs, addend P c0, no accumulation)
+void ip_mma_pipelined(const Launch& L, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
+                      size_t out_stride)
+{
+    const int n = 1 << L.log_n;
+    const dim3 grid(n / IP2_KT, nl + 1);
+#define IP2_CASE(V)                                                                                                  \
+    case V: {                                                                                                         \
+        const size_t smem = Ip2Shape<V>::smem;                                                                        \
+        allow_smem(k_ks_ip_mma2<V, false>, smem);                                                                     \
+        allow_smem(k_ks_ip_mma2<V, true>, smem);                                                                      \
+        ProbeScope ps_(L.probe, L.st, "k_ks_ip_mma");                                                                 \
+        k_ks_ip_mma2<V, true><<<grid, IP2_THREADS, smem, L.st>>>(L.dc, w.modup, in.base, in.ct_stride, in.comp_off,  \
+                                                               grp, L.n_data, L.n_data, out_stride, batch);           \
+        k_ks_ip_mma2<V, false><<<grid, IP2_THREADS, smem, L.st>>>(L.dc, w.modup, in.base, in.ct_stride, in.comp_off, \
+                                                                grp, L.n_data, L.n_data, out_stride, batch);          \
+    } break;
+    switch (nl) {
+        IP2_CASE(1) IP2_CASE(2) IP2_CASE(3) IP2_CASE(4) IP2_CASE(5) IP2_CASE(6) IP2_CASE(7) IP2_CASE(8)
+        IP2_CASE(9) IP2_CASE(10) IP2_CASE(11) IP2_CASE(12) IP2_CASE(13) IP2_CASE(14) IP2_CASE(15) IP2_CASE(16)
+    default: throw std::runtime_error("nl > 16");
+    }
+#undef IP2_CASE
+    check_launch("ip_mma_pipelined");
+    if (L.counter) *L.counter += 2;
+}
+
+}  // namespace ck

@@ -614,8 +614,12 @@ void keyswitch_finish_qp(const Launch& L, const KsIn& in, const KsGroup& grp, in
     const u64* ib = baby ? in.base : nullptr;
     static const int use_mma = [] {
         const char* e = getenv("CKKS_IP_MMA");
-        return e ? atoi(e) : 1;
+        return e ? atoi(e) : 2;
     }();
+    if (baby && use_mma == 2 && grp.G >= 2 && out.add == in.base && !out.accumulate) {
+        ip_mma_pipelined(L, in, grp, batch, nl, w, out.ct_stride);
+        return;
+    }
     if (baby && use_mma && grp.G >= 2 && out.add == in.base && !out.accumulate) {
         const size_t smem = ip_mma_smem(nl);
         const dim3 grid((batch + IPM_BT - 1) / IPM_BT, nl + 1, n / IPM_KT);

@@ -107,6 +107,10 @@ void keyswitch_modup(const Launch&, const KsIn& in, int batch, int nl, const KsW
 // output sigma_g-scattered; giant: addend = out.add gathered by out.add_galois, accumulated)
 void keyswitch_finish_qp(const Launch&, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
                          const KsOut& out, bool baby);
+// the baby-step (scatter, addend P c0) QP inner product of a group on the FP64 tensor cores, pipelined
+// over the batch (k_ipmma.cu); CKKS_IP_MMA=1 selects the unpipelined k_ks_ip_mma, 0 the IMAD kernel
+void ip_mma_pipelined(const Launch&, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
+                      size_t out_stride);
 // y [B][2][nl+1][N] (QP, stride y_stride) -> out [B][2][nl][N]: (y - [y_P]) / P  (one ModDown per layer)
 void moddown_qp(const Launch&, const uint64_t* y, size_t y_stride, int batch, int nl, const KsWork& w, uint64_t* out,
                 size_t out_stride);
