@@ -709,6 +709,7 @@ ckks_status ckks_probe_enable(ckks_ctx* c, int32_t kind)
         c->probe.alg_bytes = 0;
         c->probe.names.clear();
         c->probe.bytes_by_kernel.clear();
+        c->probe.flops_by_kernel.clear();
         c->probe.bfly_fp = c->probe.bfly_int = 0;
         while (kind && c->probe.ev.size() < 4096) {
             cudaEvent_t e;
@@ -736,11 +737,14 @@ ckks_status ckks_probe_read_all(ckks_ctx* c, char* json, size_t cap)
         std::string s = "{";
         for (auto& kv : per) {
             if (s.size() > 1) s += ", ";
-            char buf[256];
+            char buf[320];
             const auto it = c->probe.bytes_by_kernel.find(kv.first);
-            std::snprintf(buf, sizeof(buf), "\"%s\": {\"ms\": %.6f, \"launches\": %llu, \"alg_bytes\": %.1f}",
+            const auto fl = c->probe.flops_by_kernel.find(kv.first);
+            std::snprintf(buf, sizeof(buf),
+                          "\"%s\": {\"ms\": %.6f, \"launches\": %llu, \"alg_bytes\": %.1f, \"tensor_flops\": %.1f}",
                           kv.first.c_str(), kv.second.first, (unsigned long long)kv.second.second,
-                          it == c->probe.bytes_by_kernel.end() ? 0.0 : it->second);
+                          it == c->probe.bytes_by_kernel.end() ? 0.0 : it->second,
+                          fl == c->probe.flops_by_kernel.end() ? 0.0 : fl->second);
             s += buf;
         }
         {

@@ -244,6 +244,20 @@ void ip_mma_pipelined(const Launch& L, const KsIn& in, const KsGroup& grp, int b
 {
     const int n = 1 << L.log_n;
     const dim3 grid(n / IP2_KT, nl + 1);
+    if (L.probe && L.probe->kind == PROBE_ALL) {
+        // exact split products per modular MAC: 3 (FP class rows), 6 (60-bit rows); MACs per row:
+        // B x G x 2 components x nl digits x N.  Bytes: ModUp words and input limbs read, c0 addend,
+        // the group's keys, the G rotated outputs written.
+        double fl = 0;
+        for (int i = 0; i <= nl; ++i) {
+            const int p = i == nl ? L.n_data : i;
+            fl += 2.0 * ((L.pclass && L.pclass[p] == PC_FP) ? 3 : 6) * batch * grp.G * 2.0 * nl * n;
+        }
+        L.probe->flops_by_kernel["k_ks_ip_mma"] += fl;
+        L.probe->bytes_by_kernel["k_ks_ip_mma"] +=
+            ((double)batch * nl * (nl + 1) + (double)batch * nl + (double)grp.G * nl * 2 * (nl + 1) +
+             (double)grp.G * batch * 2 * (nl + 1)) * n * 8.0;
+    }
 #define IP2_CASE(V)                                                                                                  \
     case V: {                                                                                                         \
         const size_t smem = Ip2Shape<V>::smem;                                                                        \

@@ -387,6 +387,18 @@ void bsgs_mac(const Launch& L, const uint64_t* pts, int pt_nl, const uint64_t* v
         return e ? atoi(e) : 1;
     }();
     if (use_mma && t1 <= 256 && n >= MACM_XT) {
+        if (L.probe && L.probe->kind == PROBE_ALL) {
+            // per row: B x 2 components x t1 x t2 x N modular MACs, 3 (FP class) or 6 (60-bit) exact
+            // split products each; bytes: baby steps + input read, plaintexts read, W written
+            for (int l = 0; l < nlx; ++l) {
+                const int p = l < nl ? l : L.n_data;
+                const bool fp = L.pclass && L.pclass[p] == PC_FP;
+                const char* nm = fp ? "k_bsgs_mac_mma_fp" : "k_bsgs_mac_mma_int";
+                L.probe->flops_by_kernel[nm] += 2.0 * (fp ? 3 : 6) * batch * 2.0 * t1 * t2 * n;
+                L.probe->bytes_by_kernel[nm] +=
+                    ((double)t1 * batch * 2 + (double)t1 * t2 + (double)t2 * batch * 2) * n * 8.0;
+            }
+        }
         const size_t smem = mac_mma_smem(t1);
         allow_smem(k_bsgs_mac_mma<true>, smem);
         allow_smem(k_bsgs_mac_mma<false>, smem);

@@ -20,6 +20,8 @@ struct Probe {
     size_t used = 0;
     double alg_bytes = 0;   // algorithmic bytes of the probed launches
     std::map<std::string, double> bytes_by_kernel;   // PROBE_ALL: algorithmic bytes per kernel name
+    std::map<std::string, double> flops_by_kernel;   // PROBE_ALL: FP64 tensor-core FLOPs (2 per FMA) the exact
+                                                     // split products need, per kernel name
     double bfly_fp = 0, bfly_int = 0;                // ModUp butterflies on FP64-class / integer-class primes
     void mark(cudaStream_t s)
     {
