@@ -43,15 +43,14 @@ struct Ip2Shape {
 };
 
 template <int NL, bool INT>
-__global__ void __launch_bounds__(IP2_THREADS, 2)
-k_ks_ip_mma2(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ in, size_t ct_stride,
-             size_t comp_off, const KsGroup grp, int L, int special, size_t out_stride, int B)
+__device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64* __restrict__ modup,
+                                         const u64* __restrict__ in, size_t ct_stride, size_t comp_off,
+                                         const KsGroup& grp, int L, int special, size_t out_stride, int B, u64* sm)
 {
     constexpr int nl = NL;
     constexpr int NLP = Ip2Shape<NL>::NLP, JS = Ip2Shape<NL>::JS, SD = Ip2Shape<NL>::SD;
     constexpr int KPW = IP2_KT / (IP2_THREADS / 32);       // coefficients per warp
     constexpr bool CACHE = !INT && NLP <= 8;               // FP class: split key fragments held in registers
-    extern __shared__ u64 sm[];
     u64* Ks = sm;                                          // [NLP][KT][16 n]  n = 2 g + c  (n ^ kk swizzle)
     u64* Dst = Ks + NLP * JS;                              // [ST][ D [NLP][KT][16 b] | c0 [KT][16 b] ]
     u64* Os = Dst + IP2_ST * SD;                           // [8 g][2 c][16 b][KT]
@@ -61,7 +60,6 @@ k_ks_ip_mma2(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u
     const int p = prow ? special : i;
     const int krow = prow ? L : i;
     const DPrime Pr = dc->p[p];
-    if ((prime_class(Pr.q) != PC_FP) != INT) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gid = lane >> 2, tig = lane & 3;
     const int G = grp.G;
@@ -190,25 +188,29 @@ k_ks_ip_mma2(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u
                 for (int e = 0; e < 4; ++e) {
                     const int bl = gid + 8 * (e >> 1), g = 4 * t + tig, c = e & 1;
                     u64 u;
+                    const u64 add = (c == 0 && !prow) ? csub(shoup_mul(As[kk * 16 + bl], Pm, Pm_sh, Pr.q), Pr.q) : 0;
                     if constexpr (!INT) {
-                        const double s0 = S[0][t][e], s2 = S[2][t][e], s1 = S[1][t][e] - s2 - s0;   // Karatsuba middle
-                        const double r0 = freduce(s0, q, qinv), r1 = freduce(s1, q, qinv), r2 = freduce(s2, q, qinv);
-                        const double k1 = __fma_rn(r1, c23q, CK_RND_MAGIC) - CK_RND_MAGIC;
-                        const double t1 = __fma_rn(-k1, q, r1 * 8388608.0);
-                        const double t2 = fmodmul(r2, w46, w46q, q);
-                        u = fcanon(t2 + t1 + r0, q, qinv);
+                        // v = s_hh 2^46 + (s_mid - s_hh - s_ll) 2^23 + s_ll mod q on the FP64 pipe, without
+                        // pre-reductions: s_hh < 2^48 goes straight into the exact fmodmul by 2^46 mod q;
+                        // mid < 2^51: k1 = rint(mid 2^23 / q), mid 2^23 - k1 q is exact in one FMA (the
+                        // scaling by 2^23 is exact and the true remainder is < 1.5 q); s_ll < 2^51; the
+                        // signed sum stays < 2^52 for fcanon.
+                        const double s0 = S[0][t][e], s2 = S[2][t][e], mid = S[1][t][e] - s2 - s0;
+                        const double k1 = __fma_rn(mid, c23q, CK_RND_MAGIC) - CK_RND_MAGIC;
+                        const double t1 = __fma_rn(-k1, q, mid * 8388608.0);
+                        const double t2 = fmodmul(s2, w46, w46q, q);
+                        u = addmod(fcanon(t2 + t1 + s0, q, qinv), add, Pr.q);
                     } else {
                         const double P0 = S[0][t][e], P1 = S[1][t][e], P2 = S[2][t][e];
                         const u64 s0 = d2u(P0), s1 = d2u(S[3][t][e] - P0 - P1), s2 = d2u(S[5][t][e] - P0 - P2 + P1),
                                   s3 = d2u(S[4][t][e] - P1 - P2), s4 = d2u(P2);
-                        u64 lo = s0, hi = 0, add;
-                        add = s1 << 20; lo += add; hi += (lo < add) + (s1 >> 44);
-                        add = s2 << 40; lo += add; hi += (lo < add) + (s2 >> 24);
-                        add = s3 << 60; lo += add; hi += (lo < add) + (s3 >> 4);
+                        u64 lo = s0, hi = 0, a2;
+                        a2 = s1 << 20; lo += a2; hi += (lo < a2) + (s1 >> 44);
+                        a2 = s2 << 40; lo += a2; hi += (lo < a2) + (s2 >> 24);
+                        a2 = s3 << 60; lo += a2; hi += (lo < a2) + (s3 >> 4);
                         hi += s4 << 16;
-                        u = reduce128(hi, lo, Pr);
+                        u = addmod(reduce128(hi, lo, Pr), add, Pr.q);
                     }
-                    if (c == 0 && !prow) u = addmod(u, csub(shoup_mul(As[kk * 16 + bl], Pm, Pm_sh, Pr.q), Pr.q), Pr.q);
                     if (g < G) Os[((g * 2 + c) * 16 + bl) * IP2_KT + (kk ^ ((bl + 4 * g) & 15))] = u;
                 }
         }
@@ -238,6 +240,20 @@ k_ks_ip_mma2(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u
     ip2_wait<0>();
 }
 
+// one launch for both prime classes (rows of either class run side by side, so the FP64-heavy and
+// the integer-heavy epilogues share the SMs)
+template <int NL>
+__global__ void __launch_bounds__(IP2_THREADS, 2)
+k_ks_ip_mma2(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ in, size_t ct_stride,
+             size_t comp_off, const KsGroup grp, int L, int special, size_t out_stride, int B)
+{
+    extern __shared__ u64 sm[];
+    const int i = blockIdx.y;
+    const u64 q = dc->p[i == NL ? special : i].q;
+    if (prime_class(q) == PC_FP) ip2_body<NL, false>(dc, modup, in, ct_stride, comp_off, grp, L, special, out_stride, B, sm);
+    else ip2_body<NL, true>(dc, modup, in, ct_stride, comp_off, grp, L, special, out_stride, B, sm);
+}
+
 // host launcher: both prime classes of a baby-step group (scatter outputs, addend P c0, no accumulation)
 void ip_mma_pipelined(const Launch& L, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
                       size_t out_stride)
@@ -261,13 +277,10 @@ void ip_mma_pipelined(const Launch& L, const KsIn& in, const KsGroup& grp, int b
 #define IP2_CASE(V)                                                                                                  \
     case V: {                                                                                                         \
         const size_t smem = Ip2Shape<V>::smem;                                                                        \
-        allow_smem(k_ks_ip_mma2<V, false>, smem);                                                                     \
-        allow_smem(k_ks_ip_mma2<V, true>, smem);                                                                      \
+        allow_smem(k_ks_ip_mma2<V>, smem);                                                                            \
         ProbeScope ps_(L.probe, L.st, "k_ks_ip_mma");                                                                 \
-        k_ks_ip_mma2<V, true><<<grid, IP2_THREADS, smem, L.st>>>(L.dc, w.modup, in.base, in.ct_stride, in.comp_off,  \
-                                                               grp, L.n_data, L.n_data, out_stride, batch);           \
-        k_ks_ip_mma2<V, false><<<grid, IP2_THREADS, smem, L.st>>>(L.dc, w.modup, in.base, in.ct_stride, in.comp_off, \
-                                                                grp, L.n_data, L.n_data, out_stride, batch);          \
+        k_ks_ip_mma2<V><<<grid, IP2_THREADS, smem, L.st>>>(L.dc, w.modup, in.base, in.ct_stride, in.comp_off, grp,   \
+                                                         L.n_data, L.n_data, out_stride, batch);                      \
     } break;
     switch (nl) {
         IP2_CASE(1) IP2_CASE(2) IP2_CASE(3) IP2_CASE(4) IP2_CASE(5) IP2_CASE(6) IP2_CASE(7) IP2_CASE(8)
@@ -276,7 +289,7 @@ void ip_mma_pipelined(const Launch& L, const KsIn& in, const KsGroup& grp, int b
     }
 #undef IP2_CASE
     check_launch("ip_mma_pipelined");
-    if (L.counter) *L.counter += 2;
+    if (L.counter) *L.counter += 1;
 }
 
 }  // namespace ck

@@ -1,9 +1,5 @@
-# full bench line + launch list + ncu captures of the dominant DMMA kernels
-timeout 900 python bench.py > gpurun_out/bench_full.log 2>&1
-tail -c 1500 gpurun_out/bench_full.log
 P="python tools/profile_forward.py --mode forward --batch 256"
 $P > gpurun_out/pf.log 2>&1 || exit 1
-ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_forward_b256.csv $P > gpurun_out/ncu1.log 2>&1
 for spec in "k_ks_ip_mma2<.int.8, .bool.0:ipmma2_fp" "k_ks_ip_mma2<.int.8, .bool.1:ipmma2_int"; do
   re=${spec%%:*}; tag=${spec##*:}
   ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$re" -c 1 -o gpurun_out/prof_$tag $P > gpurun_out/ncu_$tag.log 2>&1
