@@ -35,12 +35,16 @@ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x >> 1); }
 //   PC_FP     q < 2^45: residues held as exact integers in FP64 registers; butterflies on the
 //                       FP64 pipe (8 DFMA-class ops: error-free product + rint quotient), signed
 //                       representatives; forward needs no reduction, inverse reduces per pass
+//   PC_FPR    q < 2^50: FP64 pipe as PC_FP, one reduction per butterfly (11 FP64 ops): forward
+//                       reduces the X input to [-q/2, q/2] (every value stays < 1.5 q), inverse
+//                       reduces the sum output (every value < q) -- all products exact, |y w/q| < 2^51
 //   PC_MID    q < 2^52: 64-bit integer Shoup, forward without reductions, inverse Harvey-lazy
 //   PC_BIG    q < 2^61: 64-bit integer Shoup, Harvey-lazy both ways ([0,4q) fwd, [0,2q) inv)
-enum { PC_FP = 0, PC_MID = 1, PC_BIG = 2, PC_SMALL = 3 };
+// (key-switch inner products and BSGS sums treat every class but PC_FP as 60-bit: three-part splits)
+enum { PC_FP = 0, PC_MID = 1, PC_BIG = 2, PC_SMALL = 3, PC_FPR = 4 };
 __host__ __device__ __forceinline__ int prime_class(u64 q)
 {
-    return q < (1ULL << 45) ? PC_FP : (q < (1ULL << 52) ? PC_MID : PC_BIG);
+    return q < (1ULL << 45) ? PC_FP : q < (1ULL << 50) ? PC_FPR : (q < (1ULL << 52) ? PC_MID : PC_BIG);
 }
 
 // ---- FP64 modular arithmetic on exact integers (|values| < 2^51)
@@ -173,9 +177,9 @@ struct NttCta {
     }
 
     // ---- FP64 variants (PC_FP): x holds exact signed integers
-    template <int P>
+    template <int P, bool R>
     __device__ __forceinline__ static void fwd_compute_fp(double (&x)[E], int tid, const double* __restrict__ Wd,
-                                                          const double* __restrict__ Wq, double q)
+                                                          const double* __restrict__ Wq, double q, double qinv)
     {
         using G_ = Pass<P>;
         constexpr int K = G_::K;
@@ -192,8 +196,8 @@ struct NttCta {
                     const double w = __ldg(Wd + m), wq = __ldg(Wq + m);
                     double& X = x[g * (1 << K) + i];
                     double& Y = x[g * (1 << K) + i + half];
-                    const double t = fmodmul(Y, w, wq, q);   // |t| < 0.51 q
-                    const double xx = X;
+                    const double t = fmodmul(Y, w, wq, q);   // |t| < 0.51 q  (FPR: |Y| < 2 q, |t| <= q)
+                    const double xx = R ? freduce(X, q, qinv) : X;
                     X = xx + t;                              // |.| grows by < 0.51 q per stage
                     Y = xx - t;
                 }
@@ -201,14 +205,15 @@ struct NttCta {
         }
     }
 
-    template <int P>
+    template <int P, bool R>
     __device__ __forceinline__ static void inv_compute_fp(double (&x)[E], int tid, const double* __restrict__ IWd,
                                                           const double* __restrict__ IWq, double q, double qinv)
     {
         using G_ = Pass<P>;
         constexpr int K = G_::K;
-        // pass entry: bring every value back to [-q/2, q/2] (the X lineage doubles per stage)
-        if constexpr (P != NPASS - 1) {
+        // pass entry: bring every value back to [-q/2, q/2] (the X lineage doubles per stage);
+        // FPR reduces every sum instead
+        if constexpr (P != NPASS - 1 && !R) {
 #pragma unroll
             for (int i = 0; i < E; ++i) x[i] = freduce(x[i], q, qinv);
         }
@@ -226,14 +231,14 @@ struct NttCta {
                     double& X = x[g * (1 << K) + i];
                     double& Y = x[g * (1 << K) + i + half];
                     const double u = X, v = Y;
-                    X = u + v;
+                    X = R ? freduce(u + v, q, qinv) : u + v;
                     Y = fmodmul(u - v, w, wq, q);
                 }
             }
         }
     }
 
-    template <class Load, class Store>
+    template <bool R = false, class Load, class Store>
     __device__ __forceinline__ static void forward_fp(u64* sm, const DPrime& Pr, const u64* __restrict__ tw,
                                                       Load&& ld, Store&& st)
     {
@@ -255,7 +260,7 @@ struct NttCta {
                     if constexpr (P == 0) x[g * (1 << K) + i] = u2d(ld(idx));
                     else x[g * (1 << K) + i] = smd[swz(idx)];
                 }
-            fwd_compute_fp<P>(x, tid, Wd, Wq, q);
+            fwd_compute_fp<P, R>(x, tid, Wd, Wq, q, qinv);
 #pragma unroll
             for (int g = 0; g < G_::G; ++g)
 #pragma unroll
@@ -270,7 +275,7 @@ struct NttCta {
         __syncthreads();
     }
 
-    template <class Load, class Store>
+    template <bool R = false, class Load, class Store>
     __device__ __forceinline__ static void inverse_fp(u64* sm, const DPrime& Pr, const u64* __restrict__ tw,
                                                       Load&& ld, Store&& st)
     {
@@ -284,7 +289,7 @@ struct NttCta {
 #pragma unroll 4
         for (int c = 0; c < E; ++c) {
             const int idx = c * NT + tid;
-            smd[swz(idx)] = u2d(ld(idx));
+            smd[swz(idx)] = R ? freduce(u2d(ld(idx)), q, qinv) : u2d(ld(idx));
         }
         __syncthreads();
         static_for<0, NPASS>([&](auto pc) {
@@ -295,7 +300,7 @@ struct NttCta {
             for (int g = 0; g < G_::G; ++g)
 #pragma unroll
                 for (int i = 0; i < (1 << K); ++i) x[g * (1 << K) + i] = smd[swz(index<P>(tid, g, i))];
-            inv_compute_fp<P>(x, tid, IWd, IWq, q, qinv);
+            inv_compute_fp<P, R>(x, tid, IWd, IWq, q, qinv);
 #pragma unroll
             for (int g = 0; g < G_::G; ++g)
 #pragma unroll
@@ -425,6 +430,7 @@ __device__ __forceinline__ void ntt_forward(u64* sm, const DPrime& Pr, const u64
 {
     switch (prime_class(Pr.q)) {
     case PC_FP: T::forward_fp(sm, Pr, tw, ld, st); break;
+    case PC_FPR: T::template forward_fp<true>(sm, Pr, tw, ld, st); break;
     case PC_MID: T::template forward<PC_MID>(sm, Pr, tw, ld, st); break;
     default: T::template forward<PC_BIG>(sm, Pr, tw, ld, st); break;
     }
@@ -432,7 +438,9 @@ __device__ __forceinline__ void ntt_forward(u64* sm, const DPrime& Pr, const u64
 template <class T, class Load, class Store>
 __device__ __forceinline__ void ntt_inverse(u64* sm, const DPrime& Pr, const u64* tw, Load&& ld, Store&& st)
 {
-    if (prime_class(Pr.q) == PC_FP) T::inverse_fp(sm, Pr, tw, ld, st);
+    const int pc = prime_class(Pr.q);
+    if (pc == PC_FP) T::inverse_fp(sm, Pr, tw, ld, st);
+    else if (pc == PC_FPR) T::template inverse_fp<true>(sm, Pr, tw, ld, st);
     else T::template inverse<PC_BIG>(sm, Pr, tw, ld, st);
 }
 

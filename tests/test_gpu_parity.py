@@ -325,3 +325,35 @@ def test_rotation_batch_cfg3_sampled():
         got = out.data
         for b in rng.integers(0, cfg.batch, 1):
             assert np.array_equal(u64(got[b]), o.rotate(x[b], step)), (step, b)
+
+
+@pytest.mark.parametrize("bits", [(40,) * 2, (45,) * 2, (50,) * 2, (60,) * 2])
+def test_ntt_extreme_residues(bits):
+    """Worst cases of the lazy/exactness bounds of every prime class (FP64 q < 2^45, FP64 with
+    per-butterfly reduction q < 2^50, 64-bit Shoup above): all-(q-1), alternating 0/(q-1) and
+    random limbs at N=16384, forward and inverse vs the oracle, and the round trip."""
+    log_n = 14
+    g = G.Context(log_n, bits, (), max_batch=1, want_relin=False)
+    o = oracle.Context(log_n, bits, ())
+    n = g.n
+    rng = np.random.default_rng(5)
+    rows = []
+    for q in g.primes:
+        rows.append([np.full(n, q - 1, dtype=np.uint64),
+                     np.where(np.arange(n) % 2 == 0, 0, q - 1).astype(np.uint64),
+                     rng.integers(0, q, n, dtype=np.uint64)])
+    x = np.stack([np.stack([rows[l][k] for l in range(len(bits))]) for k in range(3)])   # [3][limbs][N]
+    t = torch.from_numpy(x.view(np.int64)).cuda()
+    g.ntt_fwd(t)
+    got = u64(t)
+    for b in range(3):
+        for l in range(len(bits)):
+            assert np.array_equal(got[b, l], o.ntt(x[b, l], l)), (bits, b, l)
+    g.ntt_inv(t)
+    assert np.array_equal(u64(t), x)
+    t2 = torch.from_numpy(x.view(np.int64)).cuda()
+    g.ntt_inv(t2)
+    inv = u64(t2)
+    for b in range(3):
+        for l in range(len(bits)):
+            assert np.array_equal(inv[b, l], o.intt(x[b, l], l)), (bits, b, l)
