@@ -88,3 +88,33 @@ def test_smallest_ring_forward_to_level0():
     assert out.level == 0
     ref = OC.forward(o, OC.Ct(o.encrypt(m, 2, 0), D), layers, "square")
     assert np.array_equal(u64(out.data)[0], ref.data)
+
+
+@pytest.mark.parametrize("data_bits", [(60, 44, 44), (60, 40, 40)])
+def test_bsgs_mac_worst_case_residues(data_bits):
+    """Exactness bounds of the tensor-core BSGS inner sums and baby-step inner products: every
+    ciphertext residue q-1 and every diagonal the constant -1 (all NTT values q-1), so every split
+    partial sum is at its maximum.  t = 512 with one extra baby-step doubling (t1 = 64, t2 = 8): for
+    44-bit primes the q < 2^45 accumulators fold mod q every 32 terms, for 40-bit every 64; double
+    hoisting, bit-exact vs the oracle (the inputs are not encryptions; only residues are compared)."""
+    log_n, special = 12, (60,)
+    t, x = 512, 1
+    steps = OC.rotation_steps_for([(t, t)], x)
+    o = oracle.Context(log_n, data_bits, special)
+    o.keygen(7, steps)
+    g = G.Context(log_n, data_bits, special, key_seed=7, rot_steps=steps, max_batch=2, bsgs_baby_extra=x)
+    n, level = g.n, len(data_bits) - 1
+    diag = np.zeros((t, n), dtype=np.int64)
+    diag[:, 0] = -1
+    lay = OC.EncodedLayer(t, t, t, 64, 8, level, float(o.primes[level]), 2.0 ** 30, diag, np.zeros(n, dtype=np.int64))
+    gl = G.Layer(g, t, t, level, diag_coeffs=lay.diag_coeffs, bias_coeffs=lay.bias_coeffs, pt_scale=lay.pt_scale,
+                 bias_scale=lay.bias_scale).set_hoisting(2)
+    data = np.empty((2, 2, level + 1, n), dtype=np.uint64)
+    for i in range(level + 1):
+        data[:, :, i, :] = np.uint64(o.primes[i] - 1)
+    data[1, 1, :, ::3] = 0                                          # second ciphertext: a mix with zeros
+    ct = G.Ciphertext(torch.from_numpy(data.view(np.int64)).cuda(), level, 2.0 ** 30)
+    out = gl.matvec(ct)
+    for b in range(2):
+        ref = OC.matvec(o, OC.Ct(data[b].copy(), 2.0 ** 30), lay, hoisted=2)
+        assert np.array_equal(u64(out.data)[b], ref.data), (data_bits, b)
