@@ -187,6 +187,21 @@ void encode_host(int n, const double* values, size_t count, double scale, int64_
 
 // ================================================================================== structures
 struct ckks_ctx {
+    // host-buffer forward: copy streams (H2D, D2H) and the events that order staging-buffer reuse
+    cudaStream_t h2d_st = nullptr, d2h_st = nullptr;
+    cudaEvent_t ev_h2d[2] = {}, ev_done[2] = {}, ev_d2h[2] = {}, ev_ready = nullptr;
+    void ensure_copy_streams()
+    {
+        if (h2d_st) return;
+        cuda_ok(cudaStreamCreateWithFlags(&h2d_st, cudaStreamNonBlocking), "copy stream");
+        cuda_ok(cudaStreamCreateWithFlags(&d2h_st, cudaStreamNonBlocking), "copy stream");
+        for (int k = 0; k < 2; ++k) {
+            cuda_ok(cudaEventCreateWithFlags(&ev_h2d[k], cudaEventDisableTiming), "event");
+            cuda_ok(cudaEventCreateWithFlags(&ev_done[k], cudaEventDisableTiming), "event");
+            cuda_ok(cudaEventCreateWithFlags(&ev_d2h[k], cudaEventDisableTiming), "event");
+        }
+        cuda_ok(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming), "event");
+    }
     int log_n = 0, n = 0, L = 0, ns = 0, np = 0;
     double sigma = 3.2;
     uint32_t max_batch = 1;
@@ -695,8 +710,19 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
 
 void ckks_ctx_destroy(ckks_ctx* ctx)
 {
-    if (ctx)
+    if (ctx) {
         for (auto e : ctx->probe.ev) cudaEventDestroy(e);
+        if (ctx->h2d_st) {
+            cudaStreamDestroy(ctx->h2d_st);
+            cudaStreamDestroy(ctx->d2h_st);
+            for (int k = 0; k < 2; ++k) {
+                cudaEventDestroy(ctx->ev_h2d[k]);
+                cudaEventDestroy(ctx->ev_done[k]);
+                cudaEventDestroy(ctx->ev_d2h[k]);
+            }
+            cudaEventDestroy(ctx->ev_ready);
+        }
+    }
     delete ctx;
 }
 
@@ -1450,7 +1476,8 @@ static size_t model_work_words(const ckks_ctx* c, const ckks_model* m, int B)
     return lw + 4 * big;
 }
 // + host-path staging: one chunk of input and one of output ciphertexts
-static size_t host_stage_words(const ckks_ctx* c, int B) { return (size_t)B * 2 * c->ct_words(c->L); }
+// host-buffer forward staging: two input and two output chunk buffers (double buffering)
+static size_t host_stage_words(const ckks_ctx* c, int B) { return (size_t)2 * B * 2 * c->ct_words(c->L); }
 
 ckks_status ckks_model_work_sizes(const ckks_ctx* c, const ckks_model* m, uint32_t batch, size_t* bytes)
 {
@@ -1622,22 +1649,39 @@ ckks_status ckks_encrypted_forward_host(ckks_ctx* c, const ckks_model* m, const 
         if (in_level != m->stages[0].layer->level) throw CkksError(CKKS_E_SHAPE, "input level != first layer level");
         const int nl_in = (int)in_level + 1, ol = model_out_level(m);
         const int Bmax = (int)c->max_batch;
-        // device staging after the model workspace: [Bmax] input cts + [Bmax] output cts
+        // device staging after the model workspace: 2 x [Bmax] input cts + 2 x [Bmax] output cts.  Chunk c
+        // uses buffer c % 2; H2D of chunk c+1 and D2H of chunk c-1 run on their own streams (separate
+        // copy engines, PCIe full duplex) while chunk c is evaluated on `stream`; events order the reuse.
         const size_t mw = model_work_words(c, m, Bmax);
-        u64* d_in = (u64*)work + mw;
-        u64* d_out = d_in + (size_t)Bmax * c->ct_words(nl_in);
+        const size_t in_w = (size_t)Bmax * c->ct_words(nl_in), out_w = (size_t)Bmax * c->ct_words(ol + 1);
+        u64* d_in[2] = {(u64*)work + mw, (u64*)work + mw + in_w};
+        u64* d_out[2] = {(u64*)work + mw + 2 * in_w, (u64*)work + mw + 2 * in_w + out_w};
         cudaStream_t st = (cudaStream_t)stream;
+        c->ensure_copy_streams();
+        cudaStream_t sh = c->h2d_st, sd = c->d2h_st;
         int lvl = 0;
         double sc = 0;
-        for (uint32_t b0 = 0; b0 < batch; b0 += Bmax) {
-            const int B = (int)std::min<uint32_t>(Bmax, batch - b0);
-            cuda_ok(cudaMemcpyAsync(d_in, h_in + (size_t)b0 * c->ct_words(nl_in), (size_t)B * c->ct_words(nl_in) * 8,
-                                    cudaMemcpyHostToDevice, st), "h2d");
-            forward_chunk(c, m, d_in, c->ct_words(nl_in), B, in_scale, d_out, c->ct_words(ol + 1), (u64*)work, stream,
-                          &lvl, &sc);
-            cuda_ok(cudaMemcpyAsync(h_out + (size_t)b0 * c->ct_words(ol + 1), d_out, (size_t)B * c->ct_words(ol + 1) * 8,
-                                    cudaMemcpyDeviceToHost, st), "d2h");
+        cuda_ok(cudaEventRecord(c->ev_ready, st), "event");          // work/staging free w.r.t. earlier calls
+        cuda_ok(cudaStreamWaitEvent(sh, c->ev_ready, 0), "wait");
+        int ci = 0;
+        for (uint32_t b0 = 0; b0 < batch; b0 += Bmax, ++ci) {
+            const int B = (int)std::min<uint32_t>(Bmax, batch - b0), k = ci & 1;
+            if (ci >= 2) cuda_ok(cudaStreamWaitEvent(sh, c->ev_done[k], 0), "wait");          // forward(ci-2) read d_in[k]
+            cuda_ok(cudaMemcpyAsync(d_in[k], h_in + (size_t)b0 * c->ct_words(nl_in), (size_t)B * c->ct_words(nl_in) * 8,
+                                    cudaMemcpyHostToDevice, sh), "h2d");
+            cuda_ok(cudaEventRecord(c->ev_h2d[k], sh), "event");
+            cuda_ok(cudaStreamWaitEvent(st, c->ev_h2d[k], 0), "wait");
+            if (ci >= 2) cuda_ok(cudaStreamWaitEvent(st, c->ev_d2h[k], 0), "wait");          // D2H(ci-2) read d_out[k]
+            forward_chunk(c, m, d_in[k], c->ct_words(nl_in), B, in_scale, d_out[k], c->ct_words(ol + 1), (u64*)work,
+                          stream, &lvl, &sc);
+            cuda_ok(cudaEventRecord(c->ev_done[k], st), "event");
+            cuda_ok(cudaStreamWaitEvent(sd, c->ev_done[k], 0), "wait");
+            cuda_ok(cudaMemcpyAsync(h_out + (size_t)b0 * c->ct_words(ol + 1), d_out[k],
+                                    (size_t)B * c->ct_words(ol + 1) * 8, cudaMemcpyDeviceToHost, sd), "d2h");
+            cuda_ok(cudaEventRecord(c->ev_d2h[k], sd), "event");
         }
+        cuda_ok(cudaEventRecord(c->ev_ready, sd), "event");
+        cuda_ok(cudaStreamWaitEvent(st, c->ev_ready, 0), "wait");    // the caller's stream sees every copy
         cuda_ok(cudaStreamSynchronize(st), "forward_host");
         if (out_level) *out_level = (uint32_t)lvl;
         if (out_scale) *out_scale = sc;

@@ -357,3 +357,39 @@ def test_ntt_extreme_residues(bits):
     for b in range(3):
         for l in range(len(bits)):
             assert np.array_equal(inv[b, l], o.intt(x[b, l], l)), (bits, b, l)
+
+
+def test_forward_host_buffers_chunked():
+    """ckks_encrypted_forward_host (H2D / compute / D2H overlapped on three streams, double-buffered
+    staging) on 5 ciphertexts in chunks of 2 (ragged last chunk), twice in a row (staging reuse across
+    calls): bit-identical to the device-resident forward and to the oracle."""
+    cfg = S.Config(name="small", log_n=12, data_bits=(60,) + (40,) * 5, special_bits=(60,), log2_scale=40,
+                   layers=((64, 128), (32, 64)), activation="square", in_dim=128,
+                   weight_std=(1 / np.sqrt(128), 1 / np.sqrt(64)))
+    steps = OC.rotation_steps_for(cfg.layers, 1)
+    o = oracle.Context(cfg.log_n, cfg.data_bits, cfg.special_bits)
+    o.keygen(cfg.key_seed, steps)
+    g = G.Context(cfg.log_n, cfg.data_bits, cfg.special_bits, key_seed=cfg.key_seed, rot_steps=steps, max_batch=2,
+                  bsgs_baby_extra=1)
+    B = 5
+    prob = S.dense_problem(cfg, batch=B)
+    D = 2.0 ** 40
+    layers = OC.encode_model(o, prob["W"], prob["b"], o.top_level, D, "square", 1)
+    gl = [G.Layer(g, l.rows, l.cols, l.level, diag_coeffs=l.diag_coeffs, bias_coeffs=l.bias_coeffs,
+                  pt_scale=l.pt_scale, bias_scale=l.bias_scale) for l in layers]
+    model = G.Model(g, gl, G.ACT_SQUARE)
+    model.set_hoisting(2)
+    ms = np.stack([OE.encode(OC.pack_input(prob["x"][b], layers[0].t, o.n // 2), D, o.n) for b in range(B)])
+    ct = g.encrypt(ms, cfg.enc_seed, 0, D)
+    work = torch.empty(model.work_bytes(B), dtype=torch.uint8, device="cuda")
+    out = model.forward(ct, work=work)
+    h_in = torch.empty(tuple(ct.data.shape), dtype=torch.int64, pin_memory=True)
+    h_in.copy_(ct.data)
+    h_out = torch.empty(tuple(out.data.shape), dtype=torch.int64, pin_memory=True)
+    for _ in range(2):
+        h_out.zero_()
+        lvl, sc = model.forward_host(h_in, ct.level, ct.scale, h_out, work)
+        assert lvl == out.level and sc == out.scale
+        assert torch.equal(h_out, out.data.cpu())
+    ref = OC.forward(o, OC.Ct(o.encrypt(ms[4], cfg.enc_seed, 4), D), layers, "square", hoisted=2)
+    assert np.array_equal(h_out.numpy().view(np.uint64)[4], ref.data)
