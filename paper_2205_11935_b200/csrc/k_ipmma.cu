@@ -194,12 +194,15 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
                         // pre-reductions: s_hh < 2^48 goes straight into the exact fmodmul by 2^46 mod q;
                         // mid < 2^51: k1 = rint(mid 2^23 / q), mid 2^23 - k1 q is exact in one FMA (the
                         // scaling by 2^23 is exact and the true remainder is < 1.5 q); s_ll < 2^51; the
-                        // signed sum stays < 2^52 for fcanon.
+                        // signed sum (with the addend) stays < 2^52.  FP-class baby-step outputs are
+                        // stored as SIGNED representatives in [-q/2, q/2] (two's complement words): their
+                        // only consumer, the BSGS MAC, splits them with an arithmetic shift, which saves the
+                        // canonicalisation here.
                         const double s0 = S[0][t][e], s2 = S[2][t][e], mid = S[1][t][e] - s2 - s0;
                         const double k1 = __fma_rn(mid, c23q, CK_RND_MAGIC) - CK_RND_MAGIC;
                         const double t1 = __fma_rn(-k1, q, mid * 8388608.0);
                         const double t2 = fmodmul(s2, w46, w46q, q);
-                        u = addmod(fcanon(t2 + t1 + s0, q, qinv), add, Pr.q);
+                        u = d2s(freduce(t2 + t1 + (s0 + (double)add), q, qinv));
                     } else {
                         const double P0 = S[0][t][e], P1 = S[1][t][e], P2 = S[2][t][e];
                         const u64 s0 = d2u(P0), s1 = d2u(S[3][t][e] - P0 - P1), s2 = d2u(S[5][t][e] - P0 - P2 + P1),

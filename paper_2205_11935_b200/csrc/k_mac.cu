@@ -74,7 +74,7 @@ k_bsgs_mac_fp(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_n
                         } else if (j < t1) {
                             y = vb[((size_t)(j - 1) * batch + b) * ctw + off];
                         }
-                        y1[u] = u2d(y >> 23);
+                        y1[u] = s2d((u64)((long long)y >> 23));   // signed or canonical words
                         y0[u] = u2d(y & mask23);
                     }
 #pragma unroll
@@ -302,7 +302,9 @@ k_bsgs_mac_mma(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_
                 if constexpr (!INT) {
                     const u64 m = (1ULL << 23) - 1;
                     const double bh = u2d(bv >> 23), bl = u2d(bv & m);
-                    const double a0h = u2d(a0 >> 23), a0l = u2d(a0 & m), a1h = u2d(a1 >> 23), a1l = u2d(a1 & m);
+                    // V words: canonical, or signed [-q/2, q/2] from the tensor-core IP (arithmetic shift)
+                    const double a0h = s2d((u64)((long long)a0 >> 23)), a0l = u2d(a0 & m),
+                                 a1h = s2d((u64)((long long)a1 >> 23)), a1l = u2d(a1 & m);
                     dmma16884(S[2], a0h, a1h, bh);
                     dmma16884(S[0], a0l, a1l, bl);
                     dmma16884(S[1], a0h + a0l, a1h + a1l, bh + bl);

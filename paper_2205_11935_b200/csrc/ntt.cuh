@@ -67,6 +67,12 @@ __device__ __forceinline__ double freduce(double v, double q, double qinv)
 __device__ __forceinline__ double u2d(u64 a) { return __longlong_as_double((long long)(a | 0x4330000000000000ULL)) - CK_TWO52; }
 // v in [0, 2^52) exact integer -> u64
 __device__ __forceinline__ u64 d2u(double v) { return (u64)__double_as_longlong(v + CK_TWO52) & 0xFFFFFFFFFFFFFULL; }
+// signed integers |x| < 2^51 <-> double (two's complement int64 in a u64 word)
+__device__ __forceinline__ double s2d(u64 a)
+{
+    return __longlong_as_double((long long)(a + 0x4338000000000000ULL)) - CK_RND_MAGIC;
+}
+__device__ __forceinline__ u64 d2s(double v) { return (u64)__double_as_longlong(v + CK_RND_MAGIC) - 0x4338000000000000ULL; }
 // signed representative with |v| < 2^51 -> canonical [0, q)
 __device__ __forceinline__ u64 fcanon(double v, double q, double qinv)
 {
