@@ -616,6 +616,14 @@ void keyswitch_finish_qp(const Launch& L, const KsIn& in, const KsGroup& grp, in
         const char* e = getenv("CKKS_IP_MMA");
         return e ? atoi(e) : 2;
     }();
+    static const int use_giant = [] {
+        const char* e = getenv("CKKS_IP_GIANT");
+        return e ? atoi(e) : 1;
+    }();
+    if (!baby && use_giant && grp.G == 1 && out.accumulate && out.add && !grp.scatter[0] && out.base == grp.out[0]) {
+        ip_giant(L, grp.key[0], batch, nl, w, out.base, out.ct_stride, out.add, out.add_stride, out.add_galois);
+        return;
+    }
     if (baby && use_mma == 2 && grp.G >= 2 && out.add == in.base && !out.accumulate) {
         ip_mma_pipelined(L, in, grp, batch, nl, w, out.ct_stride);
         return;

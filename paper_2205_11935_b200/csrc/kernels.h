@@ -113,6 +113,10 @@ void keyswitch_finish_qp(const Launch&, const KsIn& in, const KsGroup& grp, int 
 // over the batch (k_ipmma.cu); CKKS_IP_MMA=1 selects the unpipelined k_ks_ip_mma, 0 the IMAD kernel
 void ip_mma_pipelined(const Launch&, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
                       size_t out_stride);
+// the giant-step (G = 1, accumulate, addend sigma_g(w.c0)) QP inner product, key-stationary over the
+// batch (k_ipgiant.cu); CKKS_IP_GIANT=0 selects the per-ciphertext-pair kernel k_ks_ip_qp
+void ip_giant(const Launch&, const uint64_t* key, int batch, int nl, const KsWork& w, uint64_t* acc,
+              size_t acc_stride, const uint64_t* add, size_t add_stride, uint32_t add_galois);
 // y [B][2][nl+1][N] (QP, stride y_stride) -> out [B][2][nl][N]: (y - [y_P]) / P  (one ModDown per layer)
 void moddown_qp(const Launch&, const uint64_t* y, size_t y_stride, int batch, int nl, const KsWork& w, uint64_t* out,
                 size_t out_stride);
