@@ -85,19 +85,21 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
 #pragma unroll
         for (int j = NL; j < NLP; ++j) S[j * JS + fk * 16 + (fr ^ fk)] = 0;
     };
+    // ---- key tile (once, asynchronously, its own commit group ahead of the first D stages): rows n = 2 g + c
+    for (int e = tid; e < NLP * IP2_KT * 16; e += IP2_THREADS) {
+        const int j = e / (IP2_KT * 16), rem = e % (IP2_KT * 16), kk = rem % IP2_KT, r = rem / IP2_KT;
+        const int g = r >> 1, c = r & 1;
+        u64* dst = Ks + j * JS + kk * 16 + (r ^ kk);
+        if (j < NL && g < G) ip2_cp8(dst, grp.key[g] + ((size_t)j * 2 * (L + 1) + (size_t)c * (L + 1) + krow) * n + k0 + kk);
+        else *dst = 0;
+    }
+    ip2_commit();
 #pragma unroll
     for (int s = 0; s < IP2_ST - 1; ++s) {
         if (s < nbt) fill(s);
         ip2_commit();
     }
-    // ---- key tile (once): rows n = 2 g + c
-    for (int e = tid; e < NLP * IP2_KT * 16; e += IP2_THREADS) {
-        const int j = e / (IP2_KT * 16), rem = e % (IP2_KT * 16), kk = rem % IP2_KT, r = rem / IP2_KT;
-        const int g = r >> 1, c = r & 1;
-        u64 v = 0;
-        if (j < NL && g < G) v = grp.key[g][((size_t)j * 2 * (L + 1) + (size_t)c * (L + 1) + krow) * n + k0 + kk];
-        Ks[j * JS + kk * 16 + (r ^ kk)] = v;
-    }
+    ip2_wait<IP2_ST - 1>();                                // the key group (the D stages may still fly)
     __syncthreads();
     const double q = (double)Pr.q, qinv = 1.0 / q;
     const double two46 = 70368744177664.0;

@@ -227,11 +227,25 @@ k_bsgs_mac_mma(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_
     u64* Vs = Ps + 8 * t1p * MACM_XT;                        // [ST][SV]
     u64* Os = Vs + MACM_ST * SV;                             // [8 k][16 b][XT]
     // ---- plaintext tile (zero beyond t1 / t2)
-    for (int i = tid; i < 8 * t1p * MACM_XT; i += MACM_THREADS) {
-        const int x = i % MACM_XT, j = (i / MACM_XT) % t1p, k = i / (MACM_XT * t1p);
-        u64 a = 0;
-        if (j < t1 && k0 + k < t2) a = pts[((size_t)((k0 + k) * t1 + j) * pt_nl + l) * n + x0 + x];
-        Ps[macm_pidx(k, j, t1p, x)] = a;
+    // (8 tile loads in flight per thread before their stores: the tile is latency-, not bandwidth-bound,
+    //  and it precedes the pipeline)
+    for (int i0 = tid; i0 < 8 * t1p * MACM_XT; i0 += 8 * MACM_THREADS) {
+        u64 a[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+            const int i = i0 + h * MACM_THREADS;
+            const int x = i % MACM_XT, j = (i / MACM_XT) % t1p, k = i / (MACM_XT * t1p);
+            a[h] = 0;
+            if (i < 8 * t1p * MACM_XT && j < t1 && k0 + k < t2)
+                a[h] = pts[((size_t)((k0 + k) * t1 + j) * pt_nl + l) * n + x0 + x];
+        }
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+            const int i = i0 + h * MACM_THREADS;
+            if (i >= 8 * t1p * MACM_XT) break;
+            const int x = i % MACM_XT, j = (i / MACM_XT) % t1p, k = i / (MACM_XT * t1p);
+            Ps[macm_pidx(k, j, t1p, x)] = a[h];
+        }
     }
     const size_t ctw = (size_t)2 * nlx * n, jstride = (size_t)batch * ctw;
     const u64 Pm = qp ? dc->qmod[dc->n_data][l < nl ? l : 0] : 0, Pm_sh = qp ? dc->qmod_sh[dc->n_data][l < nl ? l : 0] : 0;
