@@ -168,8 +168,8 @@ def profiled_traffic(kernel):
 
 KERNEL_DESC = {
     "k_ks_ip_mma": "baby-step QP key-switch inner product (FP64 tensor cores, exact split operands)",
-    "k_bsgs_mac_mma_fp": "BSGS inner sums, q < 2^45 limbs (FP64 tensor cores)",
-    "k_bsgs_mac_mma_int": "BSGS inner sums, 60-bit limbs (FP64 tensor cores)",
+    "k_bsgs_mac_mma": "BSGS inner sums (FP64 tensor cores, exact split operands)",
+    "k_ks_ip_giant": "giant-step QP key-switch inner product (key-stationary IMAD)",
     "k_ks_modup": "key-switch ModUp NTT",
 }
 

@@ -204,21 +204,18 @@ __device__ __forceinline__ int macm_pidx(int k, int j, int t1, int x)
 }
 
 template <bool INT>
-__global__ void __launch_bounds__(MACM_THREADS, 2)
-k_bsgs_mac_mma(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_nl, const u64* __restrict__ v0,
-               size_t v0_stride, const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl,
-               int qp)
+__device__ __forceinline__ void macm_body(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_nl,
+                                          const u64* __restrict__ v0, size_t v0_stride, const u64* __restrict__ vb,
+                                          u64* __restrict__ wout, int t1, int t2, int batch, int nl, int qp, u64* msm)
 {
     constexpr int SV = MACM_JC * 16 * MACM_XT;               // words per stage
     constexpr int EPT = SV / MACM_THREADS;                   // words per thread per stage (= MACM_JC / 2)
     static_assert(MACM_THREADS / MACM_XT == 32 && EPT * 2 == MACM_JC, "fill mapping");
-    extern __shared__ u64 msm[];
     const int n = dc->n;
     const int l = blockIdx.y;
     const int nlx = nl + qp;
     const int pidx = l < nl ? l : dc->n_data;
     const DPrime Pr = dc->p[pidx];
-    if ((prime_class(Pr.q) != PC_FP) != INT) return;
     const int x0 = blockIdx.x * MACM_XT, c = blockIdx.z & 1, k0 = (blockIdx.z >> 1) * 8;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gid = lane >> 2, tig = lane & 3;
@@ -386,6 +383,19 @@ k_bsgs_mac_mma(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_
     cp_async_wait<0>();
 }
 
+// one launch for both limb classes (the 3-product FP rows and the 6-product 60-bit rows share the SMs)
+__global__ void __launch_bounds__(MACM_THREADS, 2)
+k_bsgs_mac_mma(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_nl, const u64* __restrict__ v0,
+               size_t v0_stride, const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl,
+               int qp)
+{
+    extern __shared__ u64 msm[];
+    const int l = blockIdx.y;
+    const u64 q = dc->p[l < nl ? l : dc->n_data].q;
+    if (prime_class(q) == PC_FP) macm_body<false>(dc, pts, pt_nl, v0, v0_stride, vb, wout, t1, t2, batch, nl, qp, msm);
+    else macm_body<true>(dc, pts, pt_nl, v0, v0_stride, vb, wout, t1, t2, batch, nl, qp, msm);
+}
+
 static size_t mac_mma_smem(int t1)
 {
     const int t1p = (t1 + MACM_JC - 1) / MACM_JC * MACM_JC;
@@ -409,20 +419,18 @@ void bsgs_mac(const Launch& L, const uint64_t* pts, int pt_nl, const uint64_t* v
             for (int l = 0; l < nlx; ++l) {
                 const int p = l < nl ? l : L.n_data;
                 const bool fp = L.pclass && L.pclass[p] == PC_FP;
-                const char* nm = fp ? "k_bsgs_mac_mma_fp" : "k_bsgs_mac_mma_int";
+                const char* nm = "k_bsgs_mac_mma";
                 L.probe->flops_by_kernel[nm] += 2.0 * (fp ? 3 : 6) * batch * 2.0 * t1 * t2 * n;
                 L.probe->bytes_by_kernel[nm] +=
                     ((double)t1 * batch * 2 + (double)t1 * t2 + (double)t2 * batch * 2) * n * 8.0;
             }
         }
         const size_t smem = mac_mma_smem(t1);
-        allow_smem(k_bsgs_mac_mma<true>, smem);
-        allow_smem(k_bsgs_mac_mma<false>, smem);
+        allow_smem(k_bsgs_mac_mma, smem);
         const dim3 grid(n / MACM_XT, nlx, 2 * ((t2 + 7) / 8));
-        { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_mma_int"); k_bsgs_mac_mma<true><<<grid, MACM_THREADS, smem, L.st>>>(L.dc, pts, pt_nl, v0, v0_stride, vbaby, wout, t1, t2, batch, nl, qp ? 1 : 0); }
-        { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_mma_fp"); k_bsgs_mac_mma<false><<<grid, MACM_THREADS, smem, L.st>>>(L.dc, pts, pt_nl, v0, v0_stride, vbaby, wout, t1, t2, batch, nl, qp ? 1 : 0); }
+        { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_mma"); k_bsgs_mac_mma<<<grid, MACM_THREADS, smem, L.st>>>(L.dc, pts, pt_nl, v0, v0_stride, vbaby, wout, t1, t2, batch, nl, qp ? 1 : 0); }
         check_launch("bsgs_mac_mma");
-        if (L.counter) *L.counter += 2;
+        if (L.counter) *L.counter += 1;
         return;
     }
     if ((size_t)t1 * t2 * MACF_XT * sizeof(double2) > 200 * 1024)

@@ -1,4 +1,4 @@
-# parity subset + bench with the async IP key tile and batched MAC tile prologue
+# parity subset + bench with the merged MAC launch (both limb classes)
 (timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_frozen_stack.py tests/test_gpu_edges.py -x -q -k "hoist or stack or forward or edge or level or worst or host or matvec" 2>&1 | tail -3) > gpurun_out/pytest_gpu.log 2>&1
 tail -2 gpurun_out/pytest_gpu.log
 timeout 600 python bench.py --no-cpu-baseline --no-extras --no-e2e > gpurun_out/bench_ps.log 2>&1
