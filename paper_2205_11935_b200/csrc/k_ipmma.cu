@@ -24,6 +24,11 @@ namespace ck {
 #define IP2_KT 16
 #define IP2_THREADS 256
 #define IP2_ST 3
+// 60-bit rows: 128-bit IMAD products (1; measured slower: 188 vs 168 ms per step) or the 6-product
+// DMMA split (0, default)
+#ifndef IP2_INT_IMAD
+#define IP2_INT_IMAD 0
+#endif
 
 __device__ __forceinline__ void ip2_cp8(void* smem, const void* gmem)
 {
@@ -106,6 +111,13 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
     const double w46 = two46 - floor(two46 * qinv) * q, w46q = w46 / q, c23q = 8388608.0 / q;
     const u64 Pm = prow ? 0 : dc->qmod[special][i], Pm_sh = prow ? 0 : dc->qmod_sh[special][i];
     const u64 m23 = (1ULL << 23) - 1;
+    // 60-bit rows on IMAD: this thread's 2g + c key column of coefficient ik, in registers
+    const int ik = tid % IP2_KT, in_ = tid / IP2_KT;
+    u64 kreg[(INT && IP2_INT_IMAD) ? NL : 1];
+    if constexpr (INT && IP2_INT_IMAD) {
+#pragma unroll
+        for (int j = 0; j < NL; ++j) kreg[j] = Ks[j * JS + ik * 16 + (in_ ^ ik)];
+    }
     // FP class: split key fragments [kq][kb][t] -> (hi, lo, hi + lo), loaded once
     double kf[CACHE ? KPW : 1][CACHE ? NLP / 4 : 1][2][3];
     if constexpr (CACHE) {
@@ -131,6 +143,22 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
         ip2_commit();
         const u64* Ds = Dst + (bt % IP2_ST) * SD;
         const u64* As = Ds + NLP * JS;
+        if constexpr (INT && IP2_INT_IMAD) {
+            // 60-bit rows on the integer pipe (128-bit products): thread = (coefficient ik, column in = 2g + c),
+            // key words stationary in registers, 16 ciphertexts of the tile in turn.  These CTAs share SMs with
+            // the tensor-core CTAs of the FP rows, so the two pipes overlap.
+            const int g = in_ >> 1, c = in_ & 1;
+#pragma unroll 2
+            for (int bl = 0; bl < 16; ++bl) {
+                Acc128 a;
+                a.zero();
+#pragma unroll
+                for (int j = 0; j < NL; ++j) a.mac(Ds[j * JS + ik * 16 + (bl ^ ik)], kreg[j]);
+                u64 u = a.reduce(Pr);
+                if (c == 0 && !prow) u = addmod(u, csub(shoup_mul(As[ik * 16 + bl], Pm, Pm_sh, Pr.q), Pr.q), Pr.q);
+                if (g < G) Os[((g * 2 + c) * 16 + bl) * IP2_KT + (ik ^ ((bl + 4 * g) & 15))] = u;
+            }
+        } else
 #pragma unroll
         for (int kq = 0; kq < KPW; ++kq) {
             const int kk = warp * KPW + kq;

@@ -14,12 +14,12 @@
 namespace ck {
 
 // ------------------------------------------------------------------------------------ NTT batch
-template <int LOGN, bool INV>
-__global__ void __launch_bounds__(NttThreads<LOGN>::value)
+template <int LOGN, bool INV, int NTH>
+__global__ void __launch_bounds__(NTH)
 k_ntt_batch(const DCtx* __restrict__ dc, u64* __restrict__ data, int limbs, int prime0)
 {
     extern __shared__ u64 sm[];
-    using T = NttCta<LOGN, NttThreads<LOGN>::value>;
+    using T = NttCta<LOGN, NTH>;
     const int l = blockIdx.x, b = blockIdx.y, p = prime0 + l;
     u64* a = data + ((size_t)b * limbs + l) * T::N;
     const DPrime Pr = dc->p[p];
@@ -34,8 +34,13 @@ void ntt_batch(const Launch& L, uint64_t* data, int batch, int limbs, int prime0
     if (batch <= 0 || limbs <= 0) return;
     const size_t smem = sizeof(u64) << L.log_n;
     NTT_DISPATCH(L.log_n, {
-        constexpr int NT = NttThreads<LG>::value;
-        auto k = inverse ? k_ntt_batch<LG, true> : k_ntt_batch<LG, false>;
+        // threads per CTA: 16 residues per thread (NT), or 32 (NW): CKKS_NTT_WIDE bit 16 (forward, default
+        // on: cfg2 1.10 -> 1.04 ms) and bit 32 (inverse, default off: 1.27 vs 1.39 ms)
+        constexpr int NT0 = NttThreads<LG>::value, NW = NttThreadsWide<LG>::value;
+        const bool wide = (ntt_wide_mask() & (inverse ? 32 : 16)) != 0;
+        const int NT = wide ? NW : NT0;
+        auto k = wide ? (inverse ? k_ntt_batch<LG, true, NW> : k_ntt_batch<LG, false, NW>)
+                      : (inverse ? k_ntt_batch<LG, true, NT0> : k_ntt_batch<LG, false, NT0>);
         allow_smem(k, smem);
         const bool pr = L.probe && L.probe->on(PROBE_NTT);
         if (L.probe && L.probe->on(PROBE_ALL))

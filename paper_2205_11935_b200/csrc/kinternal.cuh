@@ -36,13 +36,14 @@ static void allow_smem(K kernel, size_t bytes)
 }
 
 // Threads per CTA of the key-switch NTT kernels: bit set = 32 residues per thread (N/32 threads),
-// clear = 16 (N/16 threads).  bits: 1 digits, 2 ModUp, 4 ModDown iNTT, 8 ModDown NTT.  Default 2;
+// clear = 16 (N/16 threads).  bits: 1 digits, 2 ModUp, 4 ModDown iNTT, 8 ModDown NTT, 16 batched forward
+// NTT, 32 batched inverse NTT.  Default 2 | 16 (measured, tools/sweep_wide2.sh, tools/ab_nttbatch.sh);
 // CKKS_NTT_WIDE overrides it (tuning experiments only).
 static int ntt_wide_mask()
 {
     static int mask = [] {
         const char* e = getenv("CKKS_NTT_WIDE");
-        return e ? atoi(e) : 2;
+        return e ? atoi(e) : 2 | 16;
     }();
     return mask;
 }
