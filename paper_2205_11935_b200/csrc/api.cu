@@ -1664,8 +1664,11 @@ ckks_status ckks_encrypted_forward_host(ckks_ctx* c, const ckks_model* m, const 
         cuda_ok(cudaEventRecord(c->ev_ready, st), "event");          // work/staging free w.r.t. earlier calls
         cuda_ok(cudaStreamWaitEvent(sh, c->ev_ready, 0), "wait");
         int ci = 0;
-        for (uint32_t b0 = 0; b0 < batch; b0 += Bmax, ++ci) {
-            const int B = (int)std::min<uint32_t>(Bmax, batch - b0), k = ci & 1;
+        // the first chunk is a quarter chunk, so the exposed H2D before the first evaluation (and, through
+        // the shifted boundaries, the D2H after the last) is short; all later chunks are Bmax
+        const uint32_t first = batch > (uint32_t)Bmax ? std::max<uint32_t>(1, (uint32_t)Bmax / 4) : (uint32_t)Bmax;
+        for (uint32_t b0 = 0; b0 < batch; b0 += (ci == 0 ? first : (uint32_t)Bmax), ++ci) {
+            const int B = (int)std::min<uint32_t>(ci == 0 ? first : (uint32_t)Bmax, batch - b0), k = ci & 1;
             if (ci >= 2) cuda_ok(cudaStreamWaitEvent(sh, c->ev_done[k], 0), "wait");          // forward(ci-2) read d_in[k]
             cuda_ok(cudaMemcpyAsync(d_in[k], h_in + (size_t)b0 * c->ct_words(nl_in), (size_t)B * c->ct_words(nl_in) * 8,
                                     cudaMemcpyHostToDevice, sh), "h2d");

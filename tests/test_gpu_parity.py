@@ -325,6 +325,11 @@ def test_rotation_batch_cfg3_sampled():
         got = out.data
         for b in rng.integers(0, cfg.batch, 1):
             assert np.array_equal(u64(got[b]), o.rotate(x[b], step)), (step, b)
+    # the hoisted form the bench also times (one ModUp per ciphertext for all 9 steps, R11b)
+    outs = g.rotate_hoisted(ct, cfg.rot_steps)
+    for step, out in zip(cfg.rot_steps, outs):
+        b = int(rng.integers(0, cfg.batch))
+        assert np.array_equal(u64(out.data[b]), o.rotate_hoisted(x[b], step)), (step, b)
 
 
 @pytest.mark.parametrize("bits", [(40,) * 2, (45,) * 2, (50,) * 2, (60,) * 2])
