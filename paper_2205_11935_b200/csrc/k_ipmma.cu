@@ -175,7 +175,7 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
                 const int j = kb * 4 + tig;
                 const u64 a0 = Ds[j * JS + kk * 16 + (gid ^ kk)], a1 = Ds[j * JS + kk * 16 + ((gid + 8) ^ kk)];
                 if constexpr (!INT) {
-                    const double a0h = u2d(a0 >> 23), a0l = u2d(a0 & m23), a1h = u2d(a1 >> 23), a1l = u2d(a1 & m23);
+                    const double a0h = p2d(a0 >> 23), a0l = p2d(a0 & m23), a1h = p2d(a1 >> 23), a1l = p2d(a1 & m23);
                     const double a0s = a0h + a0l, a1s = a1h + a1l;
 #pragma unroll
                     for (int t = 0; t < 2; ++t) {
@@ -196,12 +196,12 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
                     }
                 } else {
                     const u64 m = (1ULL << 20) - 1;
-                    const double x0[3] = {u2d(a0 & m), u2d((a0 >> 20) & m), u2d(a0 >> 40)};
-                    const double x1[3] = {u2d(a1 & m), u2d((a1 >> 20) & m), u2d(a1 >> 40)};
+                    const double x0[3] = {p2d(a0 & m), p2d((a0 >> 20) & m), p2d(a0 >> 40)};
+                    const double x1[3] = {p2d(a1 & m), p2d((a1 >> 20) & m), p2d(a1 >> 40)};
 #pragma unroll
                     for (int t = 0; t < 2; ++t) {
                         const u64 bv = Ks[j * JS + kk * 16 + ((t * 8 + gid) ^ kk)];
-                        const double y[3] = {u2d(bv & m), u2d((bv >> 20) & m), u2d(bv >> 40)};
+                        const double y[3] = {p2d(bv & m), p2d((bv >> 20) & m), p2d(bv >> 40)};
                         dmma16884(S[0][t], x0[0], x1[0], y[0]);
                         dmma16884(S[1][t], x0[1], x1[1], y[1]);
                         dmma16884(S[2][t], x0[2], x1[2], y[2]);

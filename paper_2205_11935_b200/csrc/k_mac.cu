@@ -312,18 +312,18 @@ __device__ __forceinline__ void macm_body(const DCtx* __restrict__ dc, const u64
                 const u64 a0 = Sv[macm_vidx(jj, gid, x)], a1 = Sv[macm_vidx(jj, gid + 8, x)];
                 if constexpr (!INT) {
                     const u64 m = (1ULL << 23) - 1;
-                    const double bh = u2d(bv >> 23), bl = u2d(bv & m);
+                    const double bh = p2d(bv >> 23), bl = p2d(bv & m);
                     // V words: canonical, or signed [-q/2, q/2] from the tensor-core IP (arithmetic shift)
-                    const double a0h = s2d((u64)((long long)a0 >> 23)), a0l = u2d(a0 & m),
-                                 a1h = s2d((u64)((long long)a1 >> 23)), a1l = u2d(a1 & m);
+                    const double a0h = sp2d((long long)a0 >> 23), a0l = p2d(a0 & m),
+                                 a1h = sp2d((long long)a1 >> 23), a1l = p2d(a1 & m);
                     dmma16884(S[2], a0h, a1h, bh);
                     dmma16884(S[0], a0l, a1l, bl);
                     dmma16884(S[1], a0h + a0l, a1h + a1l, bh + bl);
                 } else {
                     const u64 m = (1ULL << 20) - 1;
-                    const double y[3] = {u2d(bv & m), u2d((bv >> 20) & m), u2d(bv >> 40)};
-                    const double p[3] = {u2d(a0 & m), u2d((a0 >> 20) & m), u2d(a0 >> 40)};
-                    const double r[3] = {u2d(a1 & m), u2d((a1 >> 20) & m), u2d(a1 >> 40)};
+                    const double y[3] = {p2d(bv & m), p2d((bv >> 20) & m), p2d(bv >> 40)};
+                    const double p[3] = {p2d(a0 & m), p2d((a0 >> 20) & m), p2d(a0 >> 40)};
+                    const double r[3] = {p2d(a1 & m), p2d((a1 >> 20) & m), p2d(a1 >> 40)};
                     dmma16884(S[0], p[0], r[0], y[0]);
                     dmma16884(S[1], p[1], r[1], y[1]);
                     dmma16884(S[2], p[2], r[2], y[2]);

@@ -67,6 +67,10 @@ __device__ __forceinline__ double freduce(double v, double q, double qinv)
 __device__ __forceinline__ double u2d(u64 a) { return __longlong_as_double((long long)(a | 0x4330000000000000ULL)) - CK_TWO52; }
 // v in [0, 2^52) exact integer -> u64
 __device__ __forceinline__ u64 d2u(double v) { return (u64)__double_as_longlong(v + CK_TWO52) & 0xFFFFFFFFFFFFFULL; }
+// 32-bit parts -> double by the conversion instruction (I2F.F64), not the FP64 add of u2d: the split
+// operands of the tensor-core kernels are converted off the FP64 datapath that DMMA shares
+__device__ __forceinline__ double p2d(u64 part) { return __uint2double_rn((unsigned)part); }
+__device__ __forceinline__ double sp2d(long long part) { return __int2double_rn((int)part); }
 // signed integers |x| < 2^51 <-> double (two's complement int64 in a u64 word)
 __device__ __forceinline__ double s2d(u64 a)
 {
