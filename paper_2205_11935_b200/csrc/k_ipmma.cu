@@ -176,7 +176,7 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
                 const u64 a0 = Ds[j * JS + kk * 16 + (gid ^ kk)], a1 = Ds[j * JS + kk * 16 + ((gid + 8) ^ kk)];
                 if constexpr (!INT) {
                     const double a0h = p2d(a0 >> 23), a0l = p2d(a0 & m23), a1h = p2d(a1 >> 23), a1l = p2d(a1 & m23);
-                    const double a0s = a0h + a0l, a1s = a1h + a1l;
+                    const double a0s = p2d((a0 >> 23) + (a0 & m23)), a1s = p2d((a1 >> 23) + (a1 & m23));
 #pragma unroll
                     for (int t = 0; t < 2; ++t) {
                         double bh, bl, bs;

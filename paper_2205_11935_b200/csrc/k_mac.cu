@@ -318,7 +318,9 @@ __device__ __forceinline__ void macm_body(const DCtx* __restrict__ dc, const u64
                                  a1h = sp2d((long long)a1 >> 23), a1l = p2d(a1 & m);
                     dmma16884(S[2], a0h, a1h, bh);
                     dmma16884(S[0], a0l, a1l, bl);
-                    dmma16884(S[1], a0h + a0l, a1h + a1l, bh + bl);
+                    // part sums in the integer domain (IADD + I2F instead of a DADD on the shared datapath)
+                    dmma16884(S[1], sp2d(((long long)a0 >> 23) + (long long)(a0 & m)),
+                              sp2d(((long long)a1 >> 23) + (long long)(a1 & m)), p2d((bv >> 23) + (bv & m)));
                 } else {
                     const u64 m = (1ULL << 20) - 1;
                     const double y[3] = {p2d(bv & m), p2d((bv >> 20) & m), p2d(bv >> 40)};
