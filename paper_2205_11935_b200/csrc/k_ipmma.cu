@@ -26,6 +26,10 @@ namespace ck {
 #define IP2_ST 3
 // 60-bit rows: 128-bit IMAD products (1; measured slower: 188 vs 168 ms per step) or the 6-product
 // DMMA split (0, default)
+// FP rows: all coefficients' DMMAs before their epilogues (1), or coefficient by coefficient (0)
+#ifndef IP2_FP_BATCH
+#define IP2_FP_BATCH 1
+#endif
 #ifndef IP2_INT_IMAD
 #define IP2_INT_IMAD 0
 #endif
@@ -55,7 +59,7 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
     constexpr int nl = NL;
     constexpr int NLP = Ip2Shape<NL>::NLP, JS = Ip2Shape<NL>::JS, SD = Ip2Shape<NL>::SD;
     constexpr int KPW = IP2_KT / (IP2_THREADS / 32);       // coefficients per warp
-    constexpr bool CACHE = !INT && NLP <= 8;               // FP class: split key fragments held in registers
+    constexpr bool CACHE = !INT && NLP <= 8 && !IP2_FP_BATCH;   // FP class: split key fragments in registers
     u64* Ks = sm;                                          // [NLP][KT][16 n]  n = 2 g + c  (n ^ kk swizzle)
     u64* Dst = Ks + NLP * JS;                              // [ST][ D [NLP][KT][16 b] | c0 [KT][16 b] ]
     u64* Os = Dst + IP2_ST * SD;                           // [8 g][2 c][16 b][KT]
@@ -157,6 +161,53 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
                 u64 u = a.reduce(Pr);
                 if (c == 0 && !prow) u = addmod(u, csub(shoup_mul(As[ik * 16 + bl], Pm, Pm_sh, Pr.q), Pr.q), Pr.q);
                 if (g < G) Os[((g * 2 + c) * 16 + bl) * IP2_KT + (ik ^ ((bl + 4 * g) & 15))] = u;
+            }
+        } else if constexpr (!INT && IP2_FP_BATCH) {
+            // FP rows: the DMMAs of all KPW coefficients of the warp first (independent accumulator sets, so
+            // the tensor latency of one overlaps the conversions of the next), then all epilogues
+            double S[KPW][3][2][4];
+#pragma unroll
+            for (int kq = 0; kq < KPW; ++kq)
+#pragma unroll
+                for (int s3 = 0; s3 < 3; ++s3)
+#pragma unroll
+                    for (int t = 0; t < 2; ++t)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) S[kq][s3][t][e] = 0.0;
+#pragma unroll
+            for (int kb = 0; kb < NLP / 4; ++kb) {
+                const int j = kb * 4 + tig;
+#pragma unroll
+                for (int kq = 0; kq < KPW; ++kq) {
+                    const int kk = warp * KPW + kq;
+                    const u64 a0 = Ds[j * JS + kk * 16 + (gid ^ kk)], a1 = Ds[j * JS + kk * 16 + ((gid + 8) ^ kk)];
+                    const double a0h = p2d(a0 >> 23), a0l = p2d(a0 & m23), a1h = p2d(a1 >> 23), a1l = p2d(a1 & m23);
+                    const double a0s = p2d((a0 >> 23) + (a0 & m23)), a1s = p2d((a1 >> 23) + (a1 & m23));
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        const u64 bv = Ks[j * JS + kk * 16 + ((t * 8 + gid) ^ kk)];
+                        dmma16884(S[kq][2][t], a0h, a1h, p2d(bv >> 23));
+                        dmma16884(S[kq][0][t], a0l, a1l, p2d(bv & m23));
+                        dmma16884(S[kq][1][t], a0s, a1s, p2d((bv >> 23) + (bv & m23)));
+                    }
+                }
+            }
+#pragma unroll
+            for (int kq = 0; kq < KPW; ++kq) {
+                const int kk = warp * KPW + kq;
+#pragma unroll
+                for (int t = 0; t < 2; ++t)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int bl = gid + 8 * (e >> 1), g = 4 * t + tig, c = e & 1;
+                        const u64 add = (c == 0 && !prow) ? csub(shoup_mul(As[kk * 16 + bl], Pm, Pm_sh, Pr.q), Pr.q) : 0;
+                        const double s0 = S[kq][0][t][e], s2 = S[kq][2][t][e], mid = S[kq][1][t][e] - s2 - s0;
+                        const double k1 = __fma_rn(mid, c23q, CK_RND_MAGIC) - CK_RND_MAGIC;
+                        const double t1 = __fma_rn(-k1, q, mid * 8388608.0);
+                        const double t2 = fmodmul(s2, w46, w46q, q);
+                        const u64 u = d2s(freduce(t2 + t1 + (s0 + (double)add), q, qinv));
+                        if (g < G) Os[((g * 2 + c) * 16 + bl) * IP2_KT + (kk ^ ((bl + 4 * g) & 15))] = u;
+                    }
             }
         } else
 #pragma unroll
