@@ -156,6 +156,28 @@ def pipe_peaks():
         return {"fp64_butterfly_peak": 2.285e12, "int_butterfly_peak": 8.661e11, "dmma_fma_rate": 1.85e13}
 
 
+def profiled_pipes(kernel):
+    """Pipe utilisation of `kernel` from its committed ncu --set full capture (profiles/r01/ncu_final)."""
+    import csv
+    tag = {"k_ks_ip_mma": "ipmma2", "k_bsgs_mac_mma": "macmma", "k_ks_modup": "modup",
+           "k_ks_ip_giant": "ipgiant"}.get(kernel)
+    path = os.path.join(ROOT, "profiles", "r01", "ncu_final", f"prof_{tag}_raw.csv")
+    try:
+        rows = list(csv.reader(open(path)))
+        d = dict(zip(rows[0], rows[2]))
+        keys = {"tensor_dmma_pct": "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+                "fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+                "alu_pipe_pct": "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+                "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+                "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
+                "dram_pct": "dram__throughput.avg.pct_of_peak_sustained_elapsed"}
+        out = {k: round(float(d[v]), 1) for k, v in keys.items() if v in d}
+        out["source"] = os.path.relpath(path, ROOT) + " (one launch, ncu --set full)"
+        return out
+    except Exception:
+        return None
+
+
 def profiled_traffic(kernel):
     """dram bytes per launch of `kernel` from the committed ncu summary (profiles/), else None."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
@@ -194,7 +216,8 @@ def tensor_roofline(name, per_kernel, ms_local, steps, pb, hbm_peak, hbm_src, br
               "peak_source": "measured FP64 tensor (DMMA m16n8k4) FMA rate x 2, profiles/r01/pipe_bench.json "
                              "(the guide's nominal bf16:fp64 ratio applied to MEASURED_PEAKS bf16 gives a lower peak)",
               "flops_def": "2 x (3 split products per MAC for q < 2^45 rows, 6 for 60-bit rows) x modular MACs",
-              "traffic": profiled_traffic(name), "kernel_ms_total": round(k["ms"], 3),
+              "traffic": profiled_traffic(name), "ncu_pipes": profiled_pipes(name),
+              "kernel_ms_total": round(k["ms"], 3),
               "tensor_flops_per_launch": round(k["tensor_flops"] / max(1, k["launches"]), 1)})
     r["hbm"].update({"peak_source": hbm_src, "alg_bytes_per_launch": round(k["alg_bytes"] / max(1, k["launches"]), 1)})
     return r
