@@ -216,7 +216,8 @@ def tensor_roofline(name, per_kernel, ms_local, steps, pb, hbm_peak, hbm_src, br
               "peak_source": "measured FP64 tensor (DMMA m16n8k4) FMA rate x 2, profiles/r01/pipe_bench.json "
                              "(the guide's nominal bf16:fp64 ratio applied to MEASURED_PEAKS bf16 gives a lower peak)",
               "flops_def": "2 x (3 split products per MAC for q < 2^45 rows, 6 for 60-bit rows) x modular MACs",
-              "traffic": profiled_traffic(name), "ncu_pipes": profiled_pipes(name),
+              "traffic": (profiled_traffic(name) or {}).get("dram_bytes_per_launch"),
+              "traffic_detail": profiled_traffic(name), "ncu_pipes": profiled_pipes(name),
               "kernel_ms_total": round(k["ms"], 3),
               "tensor_flops_per_launch": round(k["tensor_flops"] / max(1, k["launches"]), 1)})
     r["hbm"].update({"peak_source": hbm_src, "alg_bytes_per_launch": round(k["alg_bytes"] / max(1, k["launches"]), 1)})
@@ -245,7 +246,8 @@ def modup_roofline(per_kernel, bfly, ms_local, pb, hbm_peak, hbm_src, brief=Fals
               "peak_source": "measured pipe peaks (profiles/r01/pipe_bench.json: FP64 DFMA/8 per butterfly, "
                              "64-bit Shoup butterfly) weighted by the kernel's FP64/int prime mix "
                              f"({bfly['fp64'] / bf_total:.3f} FP64)" if bf_total else "n/a",
-              "traffic": profiled_traffic("k_ks_modup"), "kernel_ms_total": round(mod_ms, 3)})
+              "traffic": (profiled_traffic("k_ks_modup") or {}).get("dram_bytes_per_launch"),
+              "traffic_detail": profiled_traffic("k_ks_modup"), "kernel_ms_total": round(mod_ms, 3)})
     r["hbm"].update({"peak_source": hbm_src, "vs_8TBs": round(hbm_achieved / 8000.0, 4),
                      "alg_bytes_def": "(B*nl + B*nl^2) * N * 8 per launch"})
     return r
