@@ -48,13 +48,14 @@ struct Ip2Shape {
     static constexpr int NLP = (NL + 3) & ~3;              // K padded to the MMA k-step
     static constexpr int JS = IP2_KT * 16 + 4;             // j stride (words) of the swizzled tiles
     static constexpr int SD = NLP * JS + IP2_KT * 16;      // words per stage: D tile + c0 addend
-    static constexpr size_t smem = sizeof(u64) * ((size_t)NLP * JS + (size_t)IP2_ST * SD + 8 * 2 * 16 * IP2_KT);
+    static constexpr size_t smem = sizeof(u64) * ((size_t)NLP * JS + (size_t)IP2_ST * SD + 8 * 2 * 16 * IP2_KT + 8);
 };
 
 template <int NL, bool INT>
 __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64* __restrict__ modup,
                                          const u64* __restrict__ in, size_t ct_stride, size_t comp_off,
-                                         const KsGroup& grp, int L, int special, size_t out_stride, int B, u64* sm)
+                                         const KsGroup& grp, int L, int special, size_t out_stride, int B, u64* sm,
+                                         int i, int cblk)
 {
     constexpr int nl = NL;
     constexpr int NLP = Ip2Shape<NL>::NLP, JS = Ip2Shape<NL>::JS, SD = Ip2Shape<NL>::SD;
@@ -63,8 +64,9 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
     u64* Ks = sm;                                          // [NLP][KT][16 n]  n = 2 g + c  (n ^ kk swizzle)
     u64* Dst = Ks + NLP * JS;                              // [ST][ D [NLP][KT][16 b] | c0 [KT][16 b] ]
     u64* Os = Dst + IP2_ST * SD;                           // [8 g][2 c][16 b][KT]
+    u64** Ob = reinterpret_cast<u64**>(Os + 8 * 2 * 16 * IP2_KT);   // [8 g] destination block of rotation g
     const int n = dc->n, logn = dc->log_n;
-    const int i = blockIdx.y, k0 = blockIdx.x * IP2_KT;
+    const int k0 = cblk * IP2_KT;
     const bool prow = (i == nl);
     const int p = prow ? special : i;
     const int krow = prow ? L : i;
@@ -103,6 +105,21 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
         else *dst = 0;
     }
     ip2_commit();
+    // sigma_g store addressing, fixed for the whole launch: the destination block of rotation g (shared by
+    // the CTA) and this thread's source index within it (4 bits per g, packed)
+    const int wt = tid % IP2_KT, wr = tid / IP2_KT;        // write phase: word wt of rows wr, wr + 16
+    u32 spk = 0;
+    for (int g = 0; g < G; ++g) {
+        const u32 gp = grp.scatter[g];
+        int dblk = cblk, sidx = wt;
+        if (gp) {
+            dblk = galois_src(k0, grp.ginv[g], logn) / IP2_KT;
+            sidx = galois_src(dblk * IP2_KT + wt, gp, logn) - k0;
+        }
+        spk |= (u32)sidx << (4 * g);
+        if (tid == 0) Ob[g] = grp.out[g] + (size_t)i * n + (size_t)dblk * IP2_KT;
+    }
+    const size_t wlimb = (size_t)(nl + 1) * n;             // component stride of an output ciphertext
 #pragma unroll
     for (int s = 0; s < IP2_ST - 1; ++s) {
         if (s < nbt) fill(s);
@@ -299,24 +316,19 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
                 }
         }
         __syncthreads();
-        // ---- permuted, coalesced write: row (g, c, b) of IP2_KT destination words per 16 lanes
+        // ---- permuted, coalesced write: row (g, c = h, b = wr) of IP2_KT destination words per 16 lanes
         {
-            const int t = tid % IP2_KT, r0 = tid / IP2_KT;   // r0 in [0, 16): rows r0, r0 + 16
-            for (int g = 0; g < G; ++g) {
-                const u32 gp = grp.scatter[g];
-                int dblk = blockIdx.x, sidx = t;
-                if (gp) {
-                    dblk = galois_src(k0, grp.ginv[g], logn) / IP2_KT;
-                    sidx = galois_src(dblk * IP2_KT + t, gp, logn) - k0;
-                }
-                u64* og = grp.out[g] + (size_t)i * n + (size_t)dblk * IP2_KT + t;
+            const int b = bt * 16 + wr;
+            if (b < B) {
+                const size_t boff = (size_t)b * out_stride + wt;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int rr = r0 + 16 * h;            // rr = c * 16 + bl
-                    const int c = rr >> 4, bl = rr & 15, b = bt * 16 + bl;
-                    if (b < B)
-                        og[(size_t)b * out_stride + (size_t)c * (nl + 1) * n] =
-                            Os[((g * 2 + c) * 16 + bl) * IP2_KT + (sidx ^ ((bl + 4 * g) & 15))];
+                for (int g = 0; g < 8; ++g) {
+                    if (g < G) {
+                        u64* og = Ob[g] + boff;
+                        const int sx = ((spk >> (4 * g)) & 15) ^ ((wr + 4 * g) & 15);
+                        og[0] = Os[((g * 2 + 0) * 16 + wr) * IP2_KT + sx];
+                        og[wlimb] = Os[((g * 2 + 1) * 16 + wr) * IP2_KT + sx];
+                    }
                 }
             }
         }
@@ -332,10 +344,12 @@ k_ks_ip_mma2(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u
              size_t comp_off, const KsGroup grp, int L, int special, size_t out_stride, int B)
 {
     extern __shared__ u64 sm[];
-    const int i = blockIdx.y;
+    // (tried: rows fastest, so CTAs of both classes share an SM at the same time -- 150 vs 147.5 ms per step)
+    const int i = blockIdx.y, cblk = blockIdx.x;
     const u64 q = dc->p[i == NL ? special : i].q;
-    if (prime_class(q) == PC_FP) ip2_body<NL, false>(dc, modup, in, ct_stride, comp_off, grp, L, special, out_stride, B, sm);
-    else ip2_body<NL, true>(dc, modup, in, ct_stride, comp_off, grp, L, special, out_stride, B, sm);
+    if (prime_class(q) == PC_FP)
+        ip2_body<NL, false>(dc, modup, in, ct_stride, comp_off, grp, L, special, out_stride, B, sm, i, cblk);
+    else ip2_body<NL, true>(dc, modup, in, ct_stride, comp_off, grp, L, special, out_stride, B, sm, i, cblk);
 }
 
 // host launcher: both prime classes of a baby-step group (scatter outputs, addend P c0, no accumulation)

@@ -250,9 +250,15 @@ __device__ __forceinline__ void macm_body(const DCtx* __restrict__ dc, const u64
     // fill mapping: thread -> (x, bb, half) copies baby steps jj = half * EPT + h, h < EPT
     const int fx = tid % MACM_XT, fbb = (tid / MACM_XT) % 16, fhalf = tid / (MACM_XT * 16);
     const size_t foff = ((size_t)c * nlx + l) * n + x0 + fx;
+    // stage (bt, jc) of the fill sequence tracked by counters (no runtime division per stage)
+    int fbt = 0, fjc = 0;
     auto fill = [&](int it) {
         u64* S = Vs + (it % MACM_ST) * SV;
-        const int bt = it / njc, jc = it - bt * njc;
+        const int bt = fbt, jc = fjc;
+        if (++fjc == njc) {
+            fjc = 0;
+            ++fbt;
+        }
         const int b = bt * 16 + fbb, jb = jc * MACM_JC + fhalf * EPT;
         const bool fast = b < batch && jb >= 1 && jb + EPT <= t1;
         if (fast) {
