@@ -16,6 +16,13 @@ namespace ck {
 // Rows of primes < 2^42: 21-bit split products on IMAD.WIDE.U32 (< 2^42 each, exact 64-bit sums);
 // 60-bit rows: 128-bit products.
 #define IPG_BLK 128
+#ifndef IPG_UNROLL
+#define IPG_UNROLL 4
+#endif
+constexpr int kIpgUnroll = IPG_UNROLL;   // ciphertexts per unrolled batch step
+#ifndef IPG_MINB
+#define IPG_MINB 4
+#endif
 
 template <int NL, bool SPLIT>
 __device__ __forceinline__ void ipg_row(const DCtx* __restrict__ dc, const u64* __restrict__ modup,
@@ -41,7 +48,7 @@ __device__ __forceinline__ void ipg_row(const DCtx* __restrict__ dc, const u64* 
     const int src = add_galois ? galois_src(k, add_galois, logn) : k;
     const size_t dstride = (size_t)(nl + 1) * n;
     const u64* dbase = modup + (size_t)i * n + k;
-#pragma unroll 2
+#pragma unroll kIpgUnroll
     for (int b = 0; b < B; ++b) {
         const u64* d = dbase + (size_t)b * nl * dstride;
         u64 dv[NL];
@@ -95,7 +102,7 @@ __device__ __forceinline__ void ipg_row(const DCtx* __restrict__ dc, const u64* 
 }
 
 template <int NL>
-__global__ void __launch_bounds__(IPG_BLK)
+__global__ void __launch_bounds__(IPG_BLK, IPG_MINB)
 k_ks_ip_giant(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ key, int L,
               int special, u64* __restrict__ acc, size_t acc_stride, const u64* __restrict__ add, size_t add_stride,
               u32 add_galois, int B)
