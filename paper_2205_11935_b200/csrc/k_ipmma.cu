@@ -27,6 +27,9 @@ namespace ck {
 // 60-bit rows: 128-bit IMAD products (1; measured slower: 188 vs 168 ms per step) or the 6-product
 // DMMA split (0, default)
 // FP rows: all coefficients' DMMAs before their epilogues (1), or coefficient by coefficient (0)
+#ifndef CK_STREAM_STORES
+#define CK_STREAM_STORES 0
+#endif
 #ifndef IP2_FP_BATCH
 #define IP2_FP_BATCH 1
 #endif
@@ -326,8 +329,13 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
                     if (g < G) {
                         u64* og = Ob[g] + boff;
                         const int sx = ((spk >> (4 * g)) & 15) ^ ((wr + 4 * g) & 15);
+#if CK_STREAM_STORES
+                        __stcs(og, Os[((g * 2 + 0) * 16 + wr) * IP2_KT + sx]);
+                        __stcs(og + wlimb, Os[((g * 2 + 1) * 16 + wr) * IP2_KT + sx]);
+#else
                         og[0] = Os[((g * 2 + 0) * 16 + wr) * IP2_KT + sx];
                         og[wlimb] = Os[((g * 2 + 1) * 16 + wr) * IP2_KT + sx];
+#endif
                     }
                 }
             }

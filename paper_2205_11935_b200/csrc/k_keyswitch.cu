@@ -10,6 +10,9 @@
 //   plaintexts  [t][limb][N]
 // This unit: key switching (digits, ModUp, inner products, ModDown), Galois gathers.
 #include "kinternal.cuh"
+#ifndef CK_STREAM_STORES
+#define CK_STREAM_STORES 0
+#endif
 
 namespace ck {
 
@@ -87,7 +90,11 @@ k_ks_modup(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* __r
     const u64* src = digits + ((size_t)b * nl + j) * T::N;
     u64* dst = modup + (((size_t)b * nl + j) * (nl + 1) + e) * T::N;
     auto ld = [&](int i) { return reduce64_lazy(src[i], Pr); };
+#if CK_STREAM_STORES
+    auto st = [&](int i, u64 v) { __stcs(dst + i, v); };   // ModUp words: read once, by the next kernel
+#else
     auto st = [&](int i, u64 v) { dst[i] = v; };
+#endif
     ntt_forward<T>(sm, Pr, twp(dc, p), ld, st);
 }
 
