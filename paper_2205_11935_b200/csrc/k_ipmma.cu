@@ -215,17 +215,22 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
 #pragma unroll
             for (int kq = 0; kq < KPW; ++kq) {
                 const int kk = warp * KPW + kq;
+                // addend P c0 of this thread's two ciphertexts (the same for every rotation g)
+                double addd[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    addd[h] = prow ? 0.0 : (double)csub(shoup_mul(As[kk * 16 + gid + 8 * h], Pm, Pm_sh, Pr.q), Pr.q);
 #pragma unroll
                 for (int t = 0; t < 2; ++t)
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int bl = gid + 8 * (e >> 1), g = 4 * t + tig, c = e & 1;
-                        const u64 add = (c == 0 && !prow) ? csub(shoup_mul(As[kk * 16 + bl], Pm, Pm_sh, Pr.q), Pr.q) : 0;
+                        const double add = (c == 0) ? addd[e >> 1] : 0.0;
                         const double s0 = S[kq][0][t][e], s2 = S[kq][2][t][e], mid = S[kq][1][t][e] - s2 - s0;
                         const double k1 = __fma_rn(mid, c23q, CK_RND_MAGIC) - CK_RND_MAGIC;
                         const double t1 = __fma_rn(-k1, q, mid * 8388608.0);
                         const double t2 = fmodmul(s2, w46, w46q, q);
-                        const u64 u = d2s(freduce(t2 + t1 + (s0 + (double)add), q, qinv));
+                        const u64 u = d2s(freduce(t2 + t1 + (s0 + add), q, qinv));
                         if (g < G) Os[((g * 2 + c) * 16 + bl) * IP2_KT + (kk ^ ((bl + 4 * g) & 15))] = u;
                     }
             }
@@ -283,13 +288,17 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
                 }
             }
             // outputs of this thread: (b = gid + 8 (e >> 1), n = 8 t + 2 tig + (e & 1)) -> g = 4 t + tig, c = e & 1
+            u64 addw[2];                                   // addend P c0 of the thread's two ciphertexts
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                addw[h] = prow ? 0 : csub(shoup_mul(As[kk * 16 + gid + 8 * h], Pm, Pm_sh, Pr.q), Pr.q);
 #pragma unroll
             for (int t = 0; t < 2; ++t)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int bl = gid + 8 * (e >> 1), g = 4 * t + tig, c = e & 1;
                     u64 u;
-                    const u64 add = (c == 0 && !prow) ? csub(shoup_mul(As[kk * 16 + bl], Pm, Pm_sh, Pr.q), Pr.q) : 0;
+                    const u64 add = (c == 0) ? addw[e >> 1] : 0;
                     if constexpr (!INT) {
                         // v = s_hh 2^46 + (s_mid - s_hh - s_ll) 2^23 + s_ll mod q on the FP64 pipe, without
                         // pre-reductions: s_hh < 2^48 goes straight into the exact fmodmul by 2^46 mod q;
