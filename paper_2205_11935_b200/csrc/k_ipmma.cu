@@ -23,8 +23,10 @@ namespace ck {
 // of the current one.
 #define IP2_KT 16
 #define IP2_THREADS 256
+#ifndef IP2_ST
 #define IP2_ST 3
-// 60-bit rows: 128-bit IMAD products (1; measured slower: 188 vs 168 ms per step) or the 6-product
+#endif
+// 60-bit rows: 128-bit IMAD products (1; measured slower: 188 vs 168, and at round end 162 vs 140 ms per step) or the 6-product
 // DMMA split (0, default)
 // FP rows: all coefficients' DMMAs before their epilogues (1), or coefficient by coefficient (0)
 #ifndef CK_STREAM_STORES
