@@ -16,6 +16,12 @@
  *     n_comp is 2 (or 3 between ckks_mul and ckks_relinearize).
  *   - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).
  *     Preconditions (level, scale, key presence, shapes) are checked on the host before launch.
+ *   - Calls on one ckks_ctx must be stream-ordered (one stream, or events inserted by the caller):
+ *     key switching, hoisted rotations and rescale use scratch space inside the context's workspace
+ *     buffer, so two calls on the same context running concurrently on different streams would race.
+ *   - SECURITY: keys and encryption randomness come from a seeded counter-based generator (SplitMix64,
+ *     reading R15 of DESIGN.md) so that the CPU oracle can reproduce them bit for bit.  It is NOT a
+ *     CSPRNG: anyone who knows the 64-bit seed recovers the secret key.  TEST/BENCHMARK USE ONLY.
  *   - Return value: CKKS_OK (0) or a negative ckks_status; ckks_last_error() gives a message
  *     (thread-local).  On error nothing has been launched.
  *   - There is no CPU fallback: without a CUDA device every compute call returns CKKS_E_CUDA.
@@ -238,6 +244,13 @@ ckks_status ckks_bsgs_plan_x(uint32_t rows, uint32_t cols, uint32_t x, uint32_t*
 ckks_status ckks_model_plan(const ckks_ctx* ctx, uint32_t n_layers, const uint32_t* rows, const uint32_t* cols,
                             int32_t activation, uint32_t in_level, double in_scale, uint32_t* layer_level,
                             double* layer_in_scale, int32_t* steps, uint32_t* n_steps);
+/* The rotation steps ckks_model_plan lists, without a context (needed to choose the Galois keys of the
+ * context itself): rows x cols dense layers with x extra baby-step doublings (R5b).  steps may be NULL
+ * to query the count; *n_steps is its capacity on input, the count on output (CKKS_E_SIZE if short). */
+ckks_status ckks_model_steps(uint32_t n_layers, const uint32_t* rows, const uint32_t* cols, uint32_t x, int32_t* steps,
+                             uint32_t* n_steps);
+/* Input level of the model's first stage and the level its output ends at. */
+ckks_status ckks_model_levels(const ckks_model* model, uint32_t* in_level, uint32_t* out_level);
 /* Device workspace bytes for a forward over `batch` ciphertexts (chunked at max_batch). */
 ckks_status ckks_model_work_sizes(const ckks_ctx* ctx, const ckks_model* model, uint32_t batch, size_t* bytes);
 /* dense_1 -> act -> replicate -> dense_2 -> ... on a batch of independent
@@ -250,6 +263,18 @@ ckks_status ckks_encrypted_forward(ckks_ctx* ctx, const ckks_model* model, const
 ckks_status ckks_encrypted_forward_host(ckks_ctx* ctx, const ckks_model* model, const uint64_t* h_in,
                                         uint32_t batch, uint32_t in_level, double in_scale, uint64_t* h_out,
                                         uint32_t* out_level, double* out_scale, void* work, void* stream);
+
+/* ---- CUDA graph of a forward (launch overhead) -------------------------- */
+/* Captures the whole launch sequence of ckks_encrypted_forward(in -> out, work) for in->batch <=
+ * max_batch ciphertexts into a CUDA graph (on a context-owned capture stream ordered after `stream`).
+ * The graph binds in->data, out->data and work: ckks_graph_launch replays the forward on `stream`
+ * over whatever those buffers hold, with one launch.  Sets out->level/scale.  CKKS_E_SIZE if
+ * in->batch > max_batch; key/scale/level errors as ckks_encrypted_forward (nothing captured). */
+typedef struct ckks_graph ckks_graph;
+ckks_status ckks_forward_graph_create(ckks_ctx* ctx, const ckks_model* model, const ckks_ct* in, ckks_ct* out,
+                                      void* work, void* stream, ckks_graph** graph);
+ckks_status ckks_graph_launch(ckks_graph* graph, void* stream);
+void ckks_graph_destroy(ckks_graph* graph);
 
 /* ---- client-side helpers (off the hot path) ------------------------------------------------ */
 /* values (count <= N/2 reals) -> int64 coefficients m[N] = round(scale * inverse embedding) (R4). */

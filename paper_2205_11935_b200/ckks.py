@@ -98,6 +98,12 @@ SIGNATURES = {
     "ckks_model_create": (_I, [_VP, ctypes.POINTER(_VP), _U32, _I, _VP, _VP, _VP, ctypes.POINTER(_VP)]),
     "ckks_model_destroy": (None, [_VP]),
     "ckks_model_work_sizes": (_I, [_VP, _VP, _U32, _PSZ]),
+    "ckks_model_steps": (_I, [_U32, ctypes.POINTER(_U32), ctypes.POINTER(_U32), _U32, ctypes.POINTER(_I),
+                              ctypes.POINTER(_U32)]),
+    "ckks_model_levels": (_I, [_VP, ctypes.POINTER(_U32), ctypes.POINTER(_U32)]),
+    "ckks_forward_graph_create": (_I, [_VP, _VP, _PCT, _PCT, _VP, _VP, ctypes.POINTER(_VP)]),
+    "ckks_graph_launch": (_I, [_VP, _VP]),
+    "ckks_graph_destroy": (None, [_VP]),
     "ckks_encrypted_forward": (_I, [_VP, _VP, _PCT, _PCT, _VP, _VP]),
     "ckks_encrypted_forward_host": (_I, [_VP, _VP, _VP, _U32, _U32, _D, _VP, ctypes.POINTER(_U32),
                                          ctypes.POINTER(_D), _VP, _VP]),
@@ -511,9 +517,12 @@ class Model:
                                        None if ac is None else ac.ctypes.data_as(ctypes.c_void_p), _ptr(self.buf),
                                        _stream(stream), ctypes.byref(h)), "ckks_model_create")
         self.h = h
-        depth = {ACT_NONE: 0, ACT_SQUARE: 1, ACT_CUBIC: 2}[int(activation)]
-        self.in_level = self.layers[0].level
-        self.final_level = self.in_level - len(self.layers) - (len(self.layers) - 1) * depth
+        self._levels()
+
+    def _levels(self):
+        il, ol = _U32(), _U32()
+        _check(lib().ckks_model_levels(self.h, ctypes.byref(il), ctypes.byref(ol)), "ckks_model_levels")
+        self.in_level, self.final_level = il.value, ol.value
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -541,9 +550,7 @@ class Model:
                                               _ptr(self.buf), _stream(stream), ctypes.byref(h)),
                "ckks_model_create_stages")
         self.h = h
-        depth = {ACT_NONE: 0, ACT_SQUARE: 1, ACT_CUBIC: 2}
-        self.in_level = stages[0][0].level
-        self.final_level = self.in_level - sum(1 + depth[int(a)] for _, a, _ in stages)
+        self._levels()
         return self
 
     def set_hoisting(self, mode=1):
@@ -569,6 +576,10 @@ class Model:
         out.level, out.scale = o.level, o.scale
         return out
 
+    def graph(self, ct, out=None, work=None, stream=None):
+        """CUDA graph of the forward ct -> out (buffers bound at capture); replay with .launch()."""
+        return ForwardGraph(self, ct, out, work, stream)
+
     def forward_host(self, h_in, in_level, in_scale, h_out, work, stream=None):
         """h_in / h_out: pinned torch int64 CPU tensors.  Returns (out_level, out_scale)."""
         ol, osc = ctypes.c_uint32(), ctypes.c_double()
@@ -576,6 +587,35 @@ class Model:
                                                  float(in_scale), _ptr(h_out), ctypes.byref(ol), ctypes.byref(osc),
                                                  _ptr(work), _stream(stream)), "ckks_encrypted_forward_host")
         return ol.value, osc.value
+
+
+class ForwardGraph:
+    """ckks_forward_graph_create / ckks_graph_launch: the forward's launch sequence as one CUDA graph."""
+
+    def __init__(self, model, ct, out=None, work=None, stream=None):
+        ctx = model.ctx
+        self.model, self.ct = model, ct
+        self.out = out if out is not None else ctx.empty_ct(ct.batch, model.final_level)
+        self.work = work if work is not None else ctx.torch.empty(model.work_bytes(ct.batch),
+                                                                  dtype=ctx.torch.uint8, device=ctx.device)
+        i, o = ct.c(), self.out.c()
+        h = ctypes.c_void_p()
+        _check(lib().ckks_forward_graph_create(ctx.h, model.h, ctypes.byref(i), ctypes.byref(o), _ptr(self.work),
+                                               _stream(stream), ctypes.byref(h)), "ckks_forward_graph_create")
+        self.h = h
+        self.out.level, self.out.scale = o.level, o.scale
+
+    def launch(self, stream=None):
+        _check(lib().ckks_graph_launch(self.h, _stream(stream)), "ckks_graph_launch")
+        return self.out
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                lib().ckks_graph_destroy(self.h)
+            except Exception:
+                pass
+            self.h = None
 
 
 def bsgs_plan(rows, cols, x=0):
@@ -587,15 +627,15 @@ def bsgs_plan(rows, cols, x=0):
 
 
 def model_steps(shapes, x=0):
-    """Rotation steps a forward over these layer shapes needs (host planner of the library, R5/R5b)."""
-    steps = set()
-    for i, (r, c) in enumerate(shapes):
-        t, t1, t2 = bsgs_plan(r, c, x)
-        steps.update(range(1, t1))
-        steps.update(k * t1 for k in range(1, t2))
-        if i > 0:
-            steps.add(-t)
-    return sorted(steps)
+    """Rotation steps a forward over these layer shapes needs (ckks_model_steps, R5/R5b)."""
+    k = len(shapes)
+    rows = (_U32 * k)(*[int(r) for r, _ in shapes])
+    cols = (_U32 * k)(*[int(c) for _, c in shapes])
+    ns = _U32(0)
+    _check(lib().ckks_model_steps(k, rows, cols, int(x), None, ctypes.byref(ns)), "ckks_model_steps")
+    st = (_I * max(1, ns.value))()
+    _check(lib().ckks_model_steps(k, rows, cols, int(x), st, ctypes.byref(ns)), "ckks_model_steps")
+    return list(st[: ns.value])
 
 
 # C-ABI names re-exported for symmetry with include/ckks.h

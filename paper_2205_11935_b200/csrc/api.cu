@@ -296,6 +296,8 @@ struct ckks_model {
     std::vector<const ckks_layer*> layers;
     std::vector<Stage> stages;
     std::vector<u64*> d_act_stage;   // per stage: masked c0 plaintext of a cubic activation (or null)
+    std::vector<u64*> d_act_const;   // per stage: residues [3][CKKS_MAXP] of the Eq. 2 constants c3, c2, c1
+    std::vector<double> act_scale;   // per stage: the activation input scale the constants were encoded for
     int activation;
     int hoisted = 0;        // 0 none, 1 hoisted baby steps (R11b), 2 double hoisting (R11c)  (NEXT f-1)
 };
@@ -483,7 +485,9 @@ void rescale_impl(ckks_ctx* c, const u64* in, size_t in_stride, int ncomp, int n
 {
     if (nl < 2) throw CkksError(CKKS_E_LEVEL, "rescale at level 0 (depth exhausted)");
     auto L = c->launch(stream);
-    u64* rem = c->ks_work(c->max_batch).rem;   // [B][<=3][N]
+    // [B][<=3][N] remainder scratch: the key-switch region's remainders, or (a context without a special
+    // prime has no key-switch region) the start of the workspace, which is at least 3 max_batch N words
+    u64* rem = c->ns ? c->ks_work(c->max_batch).rem : c->d_work;
     for (int b0 = 0; b0 < batch; b0 += (int)c->max_batch) {
         const int B = std::min((int)c->max_batch, batch - b0);
         ck::rescale(L, in + (size_t)b0 * in_stride, in_stride, out + (size_t)b0 * out_stride, out_stride, B, ncomp,
@@ -534,6 +538,7 @@ static void sizes_impl(const ckks_params* p, size_t* tb, size_t* kb, size_t* wb,
     *kb = align256((size_t)np * n * 8) + align256((size_t)2 * L * n * 8) + 2 * ids.size() * key_words * 8;
     const int B = (int)p->max_batch;
     size_t w = std::max(enc_work_words(L, n, B), p->n_special ? ks_work_words(L, n, B) : (size_t)0);
+    w = std::max(w, (size_t)3 * B * n);   // rescale remainders (rescale_impl)
     // keygen scratch: e_ntt [L][L+1][N] + s' [np][N]
     w = std::max(w, (size_t)L * (L + 1) * n + (size_t)np * n);
     *wb = align256(w * 8);
@@ -1229,6 +1234,52 @@ ckks_status ckks_layer_work_sizes(const ckks_ctx* c, const ckks_layer* l, uint32
     return CKKS_OK;
 }
 
+// Every Galois / relinearisation key a layer or a model needs, checked before anything is launched
+// (ckks.h: "on error nothing has been launched").
+static void require_step_key(const ckks_ctx* c, int64_t step)
+{
+    const uint32_t g = c->galois(step);
+    if (g != 1 && !c->key((int64_t)g)) throw CkksError(CKKS_E_NOKEY, "no Galois key for step " + std::to_string(step));
+}
+static void check_layer_keys(const ckks_ctx* c, const ckks_layer* ly, int hoisting)
+{
+    for (uint32_t j = 1; j < ly->t1; ++j) require_step_key(c, ly->baby[j]);
+    for (uint32_t k = 1; k < ly->t2; ++k) {
+        const int64_t step = (int64_t)k * ly->giant;
+        if (hoisting == 2 && c->galois(step) == 1) throw CkksError(CKKS_E_PARAM, "giant step congruent to 0 mod N/2");
+        require_step_key(c, step);
+    }
+}
+// the scales a forward from in_scale produces must be the ones the cubic constants were encoded for
+static void check_model_scales(const ckks_ctx* c, const ckks_model* m, double scale)
+{
+    int level = (int)m->stages[0].layer->level;
+    for (size_t si = 0; si < m->stages.size(); ++si) {
+        const auto& sg = m->stages[si];
+        scale = scale * sg.layer->pt_scale / (double)c->primes[level];
+        level -= 1;
+        if (sg.activation == 1) {
+            scale = scale * scale / (double)c->primes[level];
+            level -= 1;
+        } else if (sg.activation == 2) {
+            const double S = m->act_scale[si];
+            if (std::fabs(scale - S) > std::ldexp(S, -40))
+                throw CkksError(CKKS_E_SCALE, "cubic activation input scale differs from the model's encoding");
+            scale = (S * S / (double)c->primes[level]) * S / (double)c->primes[level - 1];
+            level -= 2;
+        }
+    }
+}
+
+static void check_model_keys(const ckks_ctx* c, const ckks_model* m)
+{
+    for (const auto& sg : m->stages) {
+        if (sg.replicate_t) require_step_key(c, -(int64_t)sg.replicate_t);
+        check_layer_keys(c, sg.layer, m->hoisted);
+        if (sg.activation && !c->key(0)) throw CkksError(CKKS_E_NOKEY, "no relinearisation key");
+    }
+}
+
 // matvec on B ciphertexts (B <= max_batch): in -> out (level-1), work holds baby + W.
 // hoisting 0: every rotation non-hoisted (R11); 1: baby steps hoisted (R11b); 2: double hoisting (R11c)
 static void matvec_chunk(ckks_ctx* c, const ckks_layer* ly, const u64* in, size_t in_stride, int B, u64* out,
@@ -1286,6 +1337,7 @@ ckks_status ckks_matvec_diag(ckks_ctx* c, const ckks_layer* ly, const ckks_ct* i
         if (!c || !ly || !out || !out->data || !work) throw CkksError(CKKS_E_PARAM, "null");
         check_ct(c, in);
         if (in->level != ly->level) throw CkksError(CKKS_E_SHAPE, "input level != layer level");
+        check_layer_keys(c, ly, ly->hoisting);
         const int nl = (int)in->level + 1;
         for (uint32_t b0 = 0; b0 < in->batch; b0 += c->max_batch) {
             const int B = (int)std::min<uint32_t>(c->max_batch, in->batch - b0);
@@ -1302,11 +1354,26 @@ ckks_status ckks_matvec_diag(ckks_ctx* c, const ckks_layer* ly, const ckks_ct* i
 }
 
 // ------------------------------------------------------------------------------------ model
+// residues of a signed integer constant m0 modulo q_0..q_{nl-1} (a constant plaintext at coefficient 0 has
+// the NTT value m0 mod q_i in every slot, R23)
+static void const_residues(const ckks_ctx* c, int64_t m0, int nl, u64* out)
+{
+    for (int i = 0; i < nl; ++i) {
+        const u64 q = c->primes[i];
+        out[i] = m0 >= 0 ? (u64)m0 % q : (q - ((u64)(-(m0 + 1)) + 1) % q) % q;
+    }
+}
+
+static int64_t round_away(double x) { return (int64_t)((x < 0 ? -1.0 : 1.0) * std::floor(std::fabs(x) + 0.5)); }
+
+// per cubic stage: the masked c0 plaintext [L][N] and the constant residues [3][CKKS_MAXP] of c3, c2, c1
+// (computed once at model creation, so the forward issues no host->device copy); + one N-word staging row
+#define ACT_CONST_WORDS (3 * CKKS_MAXP)
 static size_t stages_dev_words(const ckks_ctx* c, const ckks_stage* st, uint32_t n)
 {
     size_t cub = 0;
     for (uint32_t i = 0; i < n; ++i) cub += st[i].activation == 2 ? 1 : 0;
-    return cub ? cub * c->L * c->n + c->n : 0;
+    return cub ? cub * ((size_t)c->L * c->n + ACT_CONST_WORDS) + c->n : 0;
 }
 
 static int stage_level_drop(int act) { return act == 1 ? 1 : act == 2 ? 2 : 0; }
@@ -1356,11 +1423,27 @@ static ckks_model* build_model(ckks_ctx* c, const ckks_stage* st, uint32_t n, co
             }
             dact = next;
             next += (size_t)c->L * c->n;
+            // Eq. 2 constants of the R23 schedule: c3 at scale q_l (l + 1 limbs), c2 at S (l limbs), c1 at
+            // S3 q_l / S (l + 1 limbs)
+            const double c3 = -0.0061728, c2 = 0.092593, c1 = 0.59259;
+            u64 cres[ACT_CONST_WORDS] = {};
+            const_residues(c, round_away(c3 * ql), l + 1, cres);
+            const_residues(c, round_away(c2 * S), l, cres + CKKS_MAXP);
+            const_residues(c, round_away(c1 * (S3 * ql / S)), l + 1, cres + 2 * CKKS_MAXP);
+            u64* dconst = next;
+            next += ACT_CONST_WORDS;
             cuda_ok(cudaMemcpyAsync(stage_buf, src, (size_t)c->n * 8, cudaMemcpyHostToDevice, cs), "act upload");
             ck::signed_to_ntt(L, stage_buf, dact, 1, l - 1);
+            cuda_ok(cudaMemcpyAsync(dconst, cres, sizeof(cres), cudaMemcpyHostToDevice, cs), "act upload");
             cuda_ok(cudaStreamSynchronize(cs), "act upload");
+            m->d_act_const.push_back(dconst);
+            m->act_scale.push_back(S);
         }
         m->d_act_stage.push_back(dact);
+        if (!dact) {
+            m->d_act_const.push_back(nullptr);
+            m->act_scale.push_back(0.0);
+        }
     }
     return m;
 }
@@ -1425,6 +1508,31 @@ ckks_status ckks_bsgs_plan_x(uint32_t rows, uint32_t cols, uint32_t x, uint32_t*
     return CKKS_OK;
 }
 
+ckks_status ckks_model_steps(uint32_t n_layers, const uint32_t* rows, const uint32_t* cols, uint32_t x, int32_t* steps,
+                             uint32_t* n_steps)
+{
+    CK_TRY({
+        if (!rows || !cols || !n_steps || n_layers == 0) throw CkksError(CKKS_E_PARAM, "null");
+        if (x > 4) throw CkksError(CKKS_E_PARAM, "x must be <= 4");
+        std::vector<int32_t> st;
+        for (uint32_t i = 0; i < n_layers; ++i) {
+            uint32_t t, t1, t2;
+            bsgs_split(rows[i], cols[i], t, t1, t2, x);
+            for (uint32_t j = 1; j < t1; ++j) st.push_back((int32_t)j);
+            for (uint32_t k = 1; k < t2; ++k) st.push_back((int32_t)(k * t1));
+            if (i > 0) st.push_back(-(int32_t)t);
+        }
+        std::sort(st.begin(), st.end());
+        st.erase(std::unique(st.begin(), st.end()), st.end());
+        if (steps) {
+            if (st.size() > *n_steps) throw CkksError(CKKS_E_SIZE, "steps buffer too small");
+            std::copy(st.begin(), st.end(), steps);
+        }
+        *n_steps = (uint32_t)st.size();
+        return CKKS_OK;
+    })
+}
+
 ckks_status ckks_model_plan(const ckks_ctx* c, uint32_t n_layers, const uint32_t* rows, const uint32_t* cols,
                             int32_t activation, uint32_t in_level, double in_scale, uint32_t* layer_level,
                             double* layer_in_scale, int32_t* steps, uint32_t* n_steps)
@@ -1487,17 +1595,6 @@ ckks_status ckks_model_work_sizes(const ckks_ctx* c, const ckks_model* m, uint32
     return CKKS_OK;
 }
 
-// residues of a signed integer constant (host) -> device array [nl] in `dst` (small upload)
-static void const_residues(ckks_ctx* c, int64_t m0, int nl, std::vector<u64>& out)
-{
-    out.resize(nl);
-    for (int i = 0; i < nl; ++i) {
-        const u64 q = c->primes[i];
-        out[i] = m0 >= 0 ? (u64)m0 % q : (q - ((u64)(-(m0 + 1)) + 1) % q) % q;
-    }
-}
-
-static int64_t round_away(double x) { return (int64_t)((x < 0 ? -1.0 : 1.0) * std::floor(std::fabs(x) + 0.5)); }
 
 // One chunk of B ciphertexts through the model's stages.  in: [B][2][l0+1][N]; out: final level.
 static void forward_chunk(ckks_ctx* c, const ckks_model* m, const u64* in, size_t in_stride, int B, double in_scale,
@@ -1555,7 +1652,6 @@ static void forward_chunk(ckks_ctx* c, const ckks_model* m, const u64* in, size_
             cur_stride = ns;
         } else if (sg.activation == 2) {
             // Eq. 2 cubic, schedule R23
-            const double c3 = -0.0061728, c2 = 0.092593, c1 = 0.59259;
             const double S = scale, ql = (double)c->primes[level], ql1 = (double)c->primes[level - 1];
             const size_t w3 = c->ct_words(nl, 3), w2 = c->ct_words(nl), w2m = c->ct_words(nl - 1),
                          w2mm = c->ct_words(nl - 2);
@@ -1566,16 +1662,11 @@ static void forward_chunk(ckks_ctx* c, const ckks_model* m, const u64* in, size_
             relin_impl(c, bufC, w3, nl, B, bufD, w2, stream);
             rescale_impl(c, bufD, w2, 2, nl, B, other, w2m, nullptr, stream);
             u64* z2 = other;
-            // a = rescale(z o [c3]_{ql}) + [c2]_S  -> bufD (level l-1)
-            std::vector<u64> res;
-            u64* dres = bufD + (size_t)B * w2m;   // small scratch after a
-            const_residues(c, round_away(c3 * ql), nl, res);
-            cuda_ok(cudaMemcpyAsync(dres, res.data(), nl * 8, cudaMemcpyHostToDevice, (cudaStream_t)stream), "c3");
+            // a = rescale(z o [c3]_{ql}) + [c2]_S  -> bufD (level l-1); constants precomputed at model creation
+            const u64* dres = m->d_act_const[si];
             ck::mul_scalar(L, z, cur_stride, bufC, w2, dres, B, 2, nl);
             rescale_impl(c, bufC, w2, 2, nl, B, bufD, w2m, nullptr, stream);
-            const_residues(c, round_away(c2 * S), nl - 1, res);
-            cuda_ok(cudaMemcpyAsync(dres, res.data(), (nl - 1) * 8, cudaMemcpyHostToDevice, (cudaStream_t)stream), "c2");
-            ck::add_scalar(L, bufD, w2m, dres, B, nl - 1);
+            ck::add_scalar(L, bufD, w2m, dres + CKKS_MAXP, B, nl - 1);
             // h = rescale(relin(z2 (x) a)) (level l-2)
             ck::tensor(L, z2, bufD, w2m, bufC, c->ct_words(nl - 1, 3), B, nl - 1);
             u64* rl = other;   // z2 is dead after the tensor
@@ -1584,9 +1675,7 @@ static void forward_chunk(ckks_ctx* c, const ckks_model* m, const u64* in, size_
             rescale_impl(c, rl, w2m, 2, nl - 1, B, h, w2mm, nullptr, stream);
             const double S3 = (S * S / ql) * S / ql1;
             // g = drop(rescale(z o [c1]_{S3 ql / S})) + [c0]_{S3} -> accumulate into h
-            const_residues(c, round_away(c1 * (S3 * ql / S)), nl, res);
-            cuda_ok(cudaMemcpyAsync(dres + 64, res.data(), nl * 8, cudaMemcpyHostToDevice, (cudaStream_t)stream), "c1");
-            ck::mul_scalar(L, z, cur_stride, bufC, w2, dres + 64, B, 2, nl);
+            ck::mul_scalar(L, z, cur_stride, bufC, w2, dres + 2 * CKKS_MAXP, B, 2, nl);
             u64* g = other;   // z2 no longer needed
             rescale_impl(c, bufC, w2, 2, nl, B, g, w2m, nullptr, stream);
             // h += drop(g): add the first nl-2 limbs of each component of g
@@ -1616,6 +1705,14 @@ static int model_out_level(const ckks_model* m)
     return lvl;
 }
 
+ckks_status ckks_model_levels(const ckks_model* m, uint32_t* in_level, uint32_t* out_level)
+{
+    if (!m || !in_level || !out_level) return fail(CKKS_E_PARAM, "null");
+    *in_level = m->stages[0].layer->level;
+    *out_level = (uint32_t)model_out_level(m);
+    return CKKS_OK;
+}
+
 ckks_status ckks_encrypted_forward(ckks_ctx* c, const ckks_model* m, const ckks_ct* in, ckks_ct* out, void* work,
                                    void* stream)
 {
@@ -1623,6 +1720,8 @@ ckks_status ckks_encrypted_forward(ckks_ctx* c, const ckks_model* m, const ckks_
         if (!c || !m || !out || !out->data || !work) throw CkksError(CKKS_E_PARAM, "null");
         check_ct(c, in);
         if (in->level != m->stages[0].layer->level) throw CkksError(CKKS_E_SHAPE, "input level != first layer level");
+        check_model_keys(c, m);
+        check_model_scales(c, m, in->scale);
         const int nl_in = (int)in->level + 1, ol = model_out_level(m);
         int lvl = 0;
         double sc = 0;
@@ -1647,8 +1746,13 @@ ckks_status ckks_encrypted_forward_host(ckks_ctx* c, const ckks_model* m, const 
     CK_TRY({
         if (!c || !m || !h_in || !h_out || !work) throw CkksError(CKKS_E_PARAM, "null");
         if (in_level != m->stages[0].layer->level) throw CkksError(CKKS_E_SHAPE, "input level != first layer level");
+        check_model_keys(c, m);
+        check_model_scales(c, m, in_scale);
         const int nl_in = (int)in_level + 1, ol = model_out_level(m);
-        const int Bmax = (int)c->max_batch;
+        if (batch == 0) throw CkksError(CKKS_E_SHAPE, "empty batch");
+        // chunks never exceed Bw = min(batch, max_batch): the workspace ckks_model_work_sizes(batch) returns
+        // is laid out for Bw ciphertexts (model work, then the staging buffers below)
+        const int Bmax = (int)std::min<uint32_t>(batch, c->max_batch);
         // device staging after the model workspace: 2 x [Bmax] input cts + 2 x [Bmax] output cts.  Chunk c
         // uses buffer c % 2; H2D of chunk c+1 and D2H of chunk c-1 run on their own streams (separate
         // copy engines, PCIe full duplex) while chunk c is evaluated on `stream`; events order the reuse.
@@ -1690,6 +1794,93 @@ ckks_status ckks_encrypted_forward_host(ckks_ctx* c, const ckks_model* m, const 
         if (out_scale) *out_scale = sc;
         return CKKS_OK;
     })
+}
+
+// ------------------------------------------------------------------------------------ CUDA graphs
+// The launch sequence of one forward (SURVEY 3 stack 4, 8(a) row a12 "launch overhead (CUDA graph)") is
+// captured once on a context-owned capture stream and replayed with one cudaGraphLaunch: for a single
+// ciphertext (cfg1, cfg4 latency) the ~100-300 kernels are each a few microseconds, so the host launch
+// cost would otherwise dominate.  The graph binds the buffers it was captured with.
+struct ckks_graph {
+    ckks_ctx* ctx = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    unsigned long long kernels = 0;   // kernels per replay (bench gpu_launches)
+};
+
+ckks_status ckks_forward_graph_create(ckks_ctx* c, const ckks_model* m, const ckks_ct* in, ckks_ct* out, void* work,
+                                      void* stream, ckks_graph** out_graph)
+{
+    CK_TRY({
+        if (!c || !m || !in || !out || !out->data || !work || !out_graph) throw CkksError(CKKS_E_PARAM, "null");
+        check_ct(c, in);
+        if (in->level != m->stages[0].layer->level) throw CkksError(CKKS_E_SHAPE, "input level != first layer level");
+        if (in->batch > c->max_batch) throw CkksError(CKKS_E_SIZE, "graph forward: batch above max_batch");
+        check_model_keys(c, m);
+        check_model_scales(c, m, in->scale);
+        cudaStream_t cap;
+        cuda_ok(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "capture stream");
+        // the capture stream starts after everything already queued on the caller's stream
+        cudaEvent_t ev;
+        cuda_ok(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+        cuda_ok(cudaEventRecord(ev, (cudaStream_t)stream), "event");
+        cuda_ok(cudaStreamWaitEvent(cap, ev, 0), "wait");
+        cuda_ok(cudaStreamSynchronize(cap), "sync");
+        cudaEventDestroy(ev);
+        const int probe_kind = c->probe.kind;
+        c->probe.kind = ck::PROBE_OFF;   // no event records inside the graph
+        const unsigned long long l0 = c->launches;
+        int lvl = 0;
+        double sc = 0;
+        auto* gph = new ckks_graph();
+        gph->ctx = c;
+        cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+        try {
+            if (e != cudaSuccess) throw CkksError(CKKS_E_CUDA, std::string("begin capture: ") + cudaGetErrorString(e));
+            const int nl_in = (int)in->level + 1, ol = model_out_level(m);
+            forward_chunk(c, m, in->data, c->ct_words(nl_in), (int)in->batch, in->scale, out->data,
+                          c->ct_words(ol + 1), (u64*)work, cap, &lvl, &sc);
+            cuda_ok(cudaStreamEndCapture(cap, &gph->graph), "end capture");
+            cuda_ok(cudaGraphInstantiate(&gph->exec, gph->graph, 0), "instantiate");
+        } catch (...) {
+            cudaGraph_t g = nullptr;
+            cudaStreamEndCapture(cap, &g);
+            if (g) cudaGraphDestroy(g);
+            c->probe.kind = probe_kind;
+            c->launches = l0;
+            cudaStreamDestroy(cap);
+            delete gph;
+            throw;
+        }
+        c->probe.kind = probe_kind;
+        gph->kernels = c->launches - l0;
+        c->launches = l0;
+        cudaStreamDestroy(cap);
+        out->batch = in->batch;
+        out->n_comp = 2;
+        out->level = (uint32_t)lvl;
+        out->scale = sc;
+        *out_graph = gph;
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_graph_launch(ckks_graph* g, void* stream)
+{
+    CK_TRY({
+        if (!g || !g->exec) throw CkksError(CKKS_E_PARAM, "null graph");
+        cuda_ok(cudaGraphLaunch(g->exec, (cudaStream_t)stream), "graph launch");
+        g->ctx->launches += g->kernels;
+        return CKKS_OK;
+    })
+}
+
+void ckks_graph_destroy(ckks_graph* g)
+{
+    if (!g) return;
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
 }
 
 // ------------------------------------------------------------------------------------ client side

@@ -118,3 +118,93 @@ def test_bsgs_mac_worst_case_residues(data_bits):
     for b in range(2):
         ref = OC.matvec(o, OC.Ct(data[b].copy(), 2.0 ** 30), lay, hoisted=2)
         assert np.array_equal(u64(out.data)[b], ref.data), (data_bits, b)
+
+
+def _small_dense_model(max_batch, activation="cubic", steps_drop=()):
+    cfg = S.Config(name="small", log_n=12, data_bits=(60,) + (40,) * 5, special_bits=(60,), log2_scale=40,
+                   layers=((64, 128), (32, 64)), activation=activation, in_dim=128,
+                   weight_std=(1 / np.sqrt(128), 1 / np.sqrt(64)))
+    steps = [s for s in OC.rotation_steps_for(cfg.layers, 1) if s not in steps_drop]
+    o = oracle.Context(cfg.log_n, cfg.data_bits, cfg.special_bits)
+    g = G.Context(cfg.log_n, cfg.data_bits, cfg.special_bits, key_seed=cfg.key_seed, rot_steps=steps,
+                  max_batch=max_batch, bsgs_baby_extra=1)
+    D = 2.0 ** 40
+    prob = S.dense_problem(cfg, batch=4)
+    layers = OC.encode_model(o, prob["W"], prob["b"], o.top_level, D, activation, 1)
+    gl = [G.Layer(g, l.rows, l.cols, l.level, diag_coeffs=l.diag_coeffs, bias_coeffs=l.bias_coeffs,
+                  pt_scale=l.pt_scale, bias_scale=l.bias_scale) for l in layers]
+    model = G.Model(g, gl, {"square": 1, "cubic": 2}[activation],
+                    act_coeffs=OC.activation_plaintexts(o, layers, activation))
+    model.set_hoisting(2)
+    ms = np.stack([OE.encode(OC.pack_input(prob["x"][b], layers[0].t, o.n // 2), D, o.n) for b in range(4)])
+    return g, model, ms, D
+
+
+@pytest.mark.parametrize("activation", ["square", "cubic"])
+def test_forward_graph_matches_stream_forward(activation):
+    """ckks_forward_graph_create / ckks_graph_launch (the forward as one CUDA graph) gives the same bits
+    as the stream forward, replayed twice over new inputs copied into the bound buffer."""
+    g, model, ms, D = _small_dense_model(4, activation)
+    ct = g.encrypt(ms[:3], 11, 0, D)
+    ref = model.forward(ct)
+    inp = g.encrypt(ms[:3], 12, 0, D)                    # another encryption in the bound input buffer
+    graph = model.graph(inp)
+    l0 = g.launches()
+    inp.data.copy_(ct.data)
+    out = graph.launch()
+    torch.cuda.synchronize()
+    assert out.level == ref.level and out.scale == ref.scale
+    assert torch.equal(out.data, ref.data)
+    assert g.launches() - l0 == graph_kernels(g, graph, l0)
+    out.data.zero_()
+    graph.launch()
+    torch.cuda.synchronize()
+    assert torch.equal(out.data, ref.data)
+
+
+def graph_kernels(g, graph, l0):
+    return g.launches() - l0
+
+
+def test_forward_host_small_batch_tight_workspace():
+    """a host-buffer forward with batch < max_batch and a workspace sized for that batch
+    (ckks_model_work_sizes(batch)) stays inside the workspace and matches the device forward."""
+    g, model, ms, D = _small_dense_model(8, "square")
+    ct = g.encrypt(ms[:3], 11, 0, D)
+    ref = model.forward(ct)
+    nb = model.work_bytes(3)
+    work = torch.zeros(nb + 4096, dtype=torch.uint8, device="cuda")
+    work[nb:] = 0xA5                                     # guard band after the sized workspace
+    h_in = torch.empty(tuple(ct.data.shape), dtype=torch.int64, pin_memory=True)
+    h_in.copy_(ct.data)
+    h_out = torch.empty(tuple(ref.data.shape), dtype=torch.int64, pin_memory=True)
+    lvl, sc = model.forward_host(h_in, ct.level, ct.scale, h_out, work[:nb])
+    assert lvl == ref.level and sc == ref.scale
+    assert torch.equal(h_out, ref.data.cpu())
+    assert bool((work[nb:] == 0xA5).all()), "host forward wrote past its workspace"
+
+
+def test_rescale_without_special_prime():
+    """a context with no special prime (no key switching) still rescales inside its own
+    workspace, bit-exact vs the oracle."""
+    bits = (50, 40, 40)
+    o = oracle.Context(11, bits, ())
+    g = G.Context(11, bits, (), want_relin=False, max_batch=2)
+    x = S.uniform_residues(9, g.primes, (2, 2), g.n)     # [2 cts][2 comps][3 limbs][N]
+    ct = g.from_numpy(x, scale=2.0 ** 40)
+    out = g.rescale(ct)
+    for b in range(2):
+        assert np.array_equal(u64(out.data)[b], o.rescale(x[b]))
+
+
+def test_missing_key_rejected_before_any_launch():
+    """ckks.h: on error nothing has been launched -- a model whose giant-step key is missing fails in
+    the up-front key check (CKKS_E_NOKEY) without launching a kernel."""
+    g, model, ms, D = _small_dense_model(4, "square", steps_drop=(64,))
+    ct = g.encrypt(ms[:2], 11, 0, D)
+    torch.cuda.synchronize()
+    l0 = g.launches()
+    with pytest.raises(G.CkksError) as e:
+        model.forward(ct)
+    assert e.value.status == G.E_NOKEY
+    assert g.launches() == l0

@@ -1,0 +1,158 @@
+"""GPU parity of the launch shapes the bench times (VERDICT r01 "What's weak" 1).
+
+bench.py runs 256 ciphertexts per launch sequence (max_batch = 256) with double hoisting (R11c) and
+t1 = 64 / 32 (R5b, x = 1).  At that shape every batch-tiled kernel runs several batch tiles per CTA:
+  * k_bsgs_mac_mma   -- batch tiles bt >= 1 of 16 ciphertexts (cp.async ring over baby-step stages),
+  * k_ks_ip_mma2     -- the 3-stage cp.async ring over >= 2 tiles of 16 ciphertexts,
+  * k_ks_ip_giant    -- the 4-ciphertext unrolled batch loop plus its remainder,
+and the forward is chunked at max_batch with a ragged last chunk.  These tests compare EVERY output
+ciphertext (small ring) or a sample spanning first/middle/last tiles and chunks (full cfg4 size) with
+the CPU oracle, bit-exactly (north_star: bit-exact ciphertexts vs the oracle), and the decryptions with
+the float64 forward within 1e-3 (Eq. 1; SURVEY 8(d) "parity for every measured run").
+The oracle references come from a spawn process pool (tests/oracle_pool.py).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+from oracle import circuits as OC  # noqa: E402
+import synthetic as S  # noqa: E402
+from paper_2205_11935_b200 import ckks as G  # noqa: E402
+import oracle_pool as OP  # noqa: E402
+
+SMALL = S.Config(name="small_ring", log_n=12, data_bits=(60,) + (40,) * 5, special_bits=(60,), log2_scale=40,
+                 layers=((64, 128), (32, 64)), activation="square", in_dim=128,
+                 weight_std=(1 / np.sqrt(128), 1 / np.sqrt(64)))
+
+
+def u64(t):
+    return t.detach().cpu().numpy().view(np.uint64)
+
+
+def gpu_forward(spec, B, max_batch):
+    """The library forward over B ciphertexts in launch sequences of max_batch, with the oracle's
+    encodings (shared plaintexts) and the library's device encryption."""
+    cfg, x, act = spec["cfg"], spec.get("x", 0), spec["activation"]
+    s, ms = OP.batch_messages(spec, B)
+    g = G.Context(cfg.log_n, cfg.data_bits, cfg.special_bits, key_seed=cfg.key_seed,
+                  rot_steps=OC.rotation_steps_for(cfg.layers, x), max_batch=max_batch, bsgs_baby_extra=x)
+    gl = [G.Layer(g, l.rows, l.cols, l.level, diag_coeffs=l.diag_coeffs, bias_coeffs=l.bias_coeffs,
+                  pt_scale=l.pt_scale, bias_scale=l.bias_scale) for l in s["layers"]]
+    model = G.Model(g, gl, {"none": 0, "square": 1, "cubic": 2}[act],
+                    act_coeffs=OC.activation_plaintexts(s["o"], s["layers"], act))
+    model.set_hoisting(spec.get("hoisting", 0))
+    D = 2.0 ** cfg.log2_scale
+    out = model.forward(g.encrypt(ms, cfg.enc_seed, 0, D))
+    torch.cuda.synchronize()
+    return s, u64(out.data), out
+
+
+def check(got, out, refs):
+    for b, (ref, scale, err) in refs.items():
+        assert out.level == ref.shape[1] - 1 and abs(out.scale - scale) <= 1e-9 * scale
+        assert np.array_equal(got[b], ref), f"ciphertext {b} differs from the oracle"
+        assert err < 1e-3, (b, err)
+
+
+@pytest.mark.parametrize("activation", ["square", "cubic"])
+def test_bench_shape_small_ring_every_ciphertext(activation):
+    """Double hoisting, x = 1, max_batch = 50, B = 105 (chunks 50, 50, 5): MAC/IP batch tiles 0..3 with a
+    ragged fourth tile (50 = 3 x 16 + 2), a ragged one-tile chunk, the giant-step unroll-4 body and its
+    remainders (50 % 4 = 2, 5 % 4 = 1).  Every one of the 105 output ciphertexts vs the oracle."""
+    B, mb = 105, 50
+    spec = {"kind": "dense", "cfg": SMALL, "batch": B, "activation": activation, "hoisting": 2, "x": 1}
+    _, got, out = gpu_forward(spec, B, mb)
+    refs = OP.oracle_forwards(spec, range(B))
+    check(got, out, refs)
+
+
+@pytest.mark.parametrize("mode,x", [(0, 0), (1, 0), (2, 0)])
+def test_large_batch_other_schedules_small_ring(mode, x):
+    """The other rotation schedules (non-hoisted R11, hoisted R11b, double hoisting with t1 = 2^ceil(lg/2))
+    at 2 full batch tiles + a ragged one (max_batch = 40, B = 45): every ciphertext vs the oracle."""
+    B, mb = 45, 40
+    spec = {"kind": "dense", "cfg": SMALL, "batch": B, "activation": "square", "hoisting": mode, "x": x}
+    _, got, out = gpu_forward(spec, B, mb)
+    refs = OP.oracle_forwards(spec, range(B))
+    check(got, out, refs)
+
+
+def test_bench_shape_cfg4_full_size_sampled():
+    """BASELINE cfg4 network at full size in the bench's exact launch configuration: max_batch = 256,
+    double hoisting, t1 = 64 / 32; B = 300 (a full 256 chunk and a ragged 44 chunk).  Sampled ciphertexts
+    b in {0, 15, 16, 17, 100, 255} (first/second batch tile boundaries, middle, last of the full chunk)
+    and {256, 299} (the ragged chunk) vs the oracle, bit-exactly."""
+    B, mb = 300, 256
+    spec = {"kind": "dense", "cfg": S.CFG4, "batch": B, "activation": "square", "hoisting": 2, "x": 1}
+    _, got, out = gpu_forward(spec, B, mb)
+    refs = OP.oracle_forwards(spec, [0, 15, 16, 17, 100, 255, 256, 299])
+    check(got, out, refs)
+
+
+def test_paper_p2_stack_batch_sampled():
+    """NEXT f-2 at the Table 2 p2 preset (N=16384, log q = 420 = [60, 50x6 | 60],
+    log Delta = 50, p = 5 items) in the bench's launch shape (128 ciphertexts per launch sequence, the
+    hoisted schedule) on B = 20 ciphertexts with max_batch = 20: sampled b in {0, 16, 17, 19} (second
+    batch tile, ragged tile) bit-exact vs the oracle, items decrypted within 1e-3 of the float64 stack."""
+    cfg = S.P2_STACK
+    t, B = 768, 20
+    spec = {"kind": "stack", "cfg": cfg, "t": t, "batch": B, "hoisting": 2}
+    s, ms = OP.batch_messages(spec, B)
+    steps = OC.frozen_stack_steps(t, [(t, t), (t - 2, t)], 9, 3)
+    g = G.Context(cfg.log_n, cfg.data_bits, cfg.special_bits, key_seed=cfg.key_seed, rot_steps=steps, max_batch=B)
+    R, p = s["R"], s["p"]
+    kinds = {"dense": G.LAYER_DENSE, "conv": G.LAYER_CONV1D, "pool": G.LAYER_AVGPOOL}
+    gst, acts = [], np.zeros((len(s["stages"]), g.n), dtype=np.int64)
+    o = s["o"]
+    for i, (lay, act, rep) in enumerate(s["stages"]):
+        gl = G.GeneralLayer.imported(g, kinds[lay.kind], lay.rows, lay.cols, lay.t, lay.t2, lay.baby_steps, lay.giant,
+                                     R, p, lay.level, lay.pt_scale, lay.bias_scale, lay.pt_coeffs, lay.bias_coeffs)
+        gst.append((gl, {"none": 0, "cubic": 2}[act], rep))
+        if act == "cubic":
+            S_ = lay.bias_scale
+            lv = lay.level - 1
+            acts[i] = OC.cubic_masked_coeffs(o, lay.rows, lay.t, R, p, (S_ * S_ / o.primes[lv]) * S_ / o.primes[lv - 1])
+    model = G.Model.from_stages(g, gst, act_coeffs=acts)
+    model.set_hoisting(2)
+    D = 2.0 ** cfg.log2_scale
+    out = model.forward(g.encrypt(ms, cfg.enc_seed, 0, D))
+    got = u64(out.data)
+    check(got, out, OP.oracle_forwards(spec, [0, 16, 17, 19]))
+
+
+def test_guard_bands_and_repeatability_bench_shape():
+    """Stand-in for compute-sanitizer memcheck/racecheck (closed on this GPU pool): the bench-shaped forward
+    (double hoisting, x = 1, B = 33 in one launch sequence: tiles 16 + 16 + 1 in every batch-tiled kernel)
+    with 1 MiB guard bands around the workspace and the output, repeated 3 times: the guard bands are
+    untouched (no out-of-bounds write), and every repetition gives the same bits (a shared-memory race
+    in a cp.async ring or an epilogue would show up as run-to-run differences), which are the oracle's."""
+    B = 33
+    spec = {"kind": "dense", "cfg": SMALL, "batch": B, "activation": "square", "hoisting": 2, "x": 1}
+    cfg = SMALL
+    s, ms = OP.batch_messages(spec, B)
+    g = G.Context(cfg.log_n, cfg.data_bits, cfg.special_bits, key_seed=cfg.key_seed,
+                  rot_steps=OC.rotation_steps_for(cfg.layers, 1), max_batch=B, bsgs_baby_extra=1)
+    gl = [G.Layer(g, l.rows, l.cols, l.level, diag_coeffs=l.diag_coeffs, bias_coeffs=l.bias_coeffs,
+                  pt_scale=l.pt_scale, bias_scale=l.bias_scale) for l in s["layers"]]
+    model = G.Model(g, gl, G.ACT_SQUARE)
+    model.set_hoisting(2)
+    ct = g.encrypt(ms, cfg.enc_seed, 0, 2.0 ** 40)
+    guard = 1 << 17                                            # words (1 MiB)
+    nw = model.work_bytes(B) // 8
+    wbuf = torch.full((nw + 2 * guard,), 0x5A5A5A5A5A5A5A5A, dtype=torch.int64, device="cuda")
+    work = wbuf[guard: guard + nw].view(torch.uint8)
+    no = B * 2 * (model.final_level + 1) * g.n
+    obuf = torch.full((no + 2 * guard,), -1, dtype=torch.int64, device="cuda")
+    out = G.Ciphertext(obuf[guard: guard + no].view(B, 2, model.final_level + 1, g.n), model.final_level, 1.0)
+    runs = []
+    for _ in range(3):
+        model.forward(ct, out, work)
+        torch.cuda.synchronize()
+        runs.append(u64(out.data).copy())
+        assert bool((wbuf[:guard] == 0x5A5A5A5A5A5A5A5A).all()) and bool((wbuf[guard + nw:] == 0x5A5A5A5A5A5A5A5A).all())
+        assert bool((obuf[:guard] == -1).all()) and bool((obuf[guard + no:] == -1).all())
+    assert all(np.array_equal(runs[0], r) for r in runs[1:])
+    check(runs[0], out, OP.oracle_forwards(spec, [0, 15, 16, 31, 32]))
