@@ -708,10 +708,9 @@ def cpu_baseline_and_parity(G, S, device, B, max_batch, hoisting, bsgs_x):
     import torch
     from oracle import circuits as OC
     OP = _oracle_pool_mod()
-    sample = [0, B - 1]
-    workers = oracle_workers(max(len(sample), 16))
-    while len(sample) < workers:
-        sample.append(1 + (len(sample) * 997) % (B - 2))
+    workers = oracle_workers(16)
+    # first and last ciphertext of the batch (first and last launch chunk), the rest spread over it
+    sample = sorted(set([0, B - 1] + [int(v) for v in np.linspace(0, B - 1, max(2, workers))]))[:max(2, workers)]
     pool = OraclePool(S, B, workers)
     try:
         wall, refs, busy = pool.forwards(sample)

@@ -59,6 +59,9 @@ def _declare(L):
         "or_ctx_new": (vp, [INT, INT, INT, ctypes.POINTER(ctypes.c_int), DBL]),
         "or_ctx_new_primes": (vp, [INT, INT, INT, u64p, DBL]),
         "or_ctx_free": (None, [vp]),
+        "or_set_digits": (INT, [vp, ctypes.POINTER(ctypes.c_int), INT]),
+        "or_n_digits": (INT, [vp]),
+        "or_n_special": (INT, [vp]),
         "or_n": (INT, [vp]),
         "or_n_data": (INT, [vp]),
         "or_prime": (U64, [vp, INT]),
@@ -124,7 +127,8 @@ def _check(st, what):
 class Context:
     """Oracle CKKS context: prime chain, tables, and (after keygen) the seeded keys."""
 
-    def __init__(self, log_n, data_bits, special_bits=(), sigma=3.2, primes=None):
+    def __init__(self, log_n, data_bits, special_bits=(), sigma=3.2, primes=None, digits=None):
+        """digits: sizes of the key-switching digits (consecutive data primes, R9b), default one per prime."""
         L = lib()
         self.log_n = int(log_n)
         self.n = 1 << self.log_n
@@ -139,6 +143,11 @@ class Context:
             self._c = L.or_ctx_new_primes(self.log_n, self.n_data, self.n_special, _p(arr), sigma)
         if not self._c:
             raise OracleError("or_ctx_new failed (bad parameters)")
+        if digits is not None:
+            arr = (ctypes.c_int * len(digits))(*[int(d) for d in digits])
+            _check(L.or_set_digits(self._c, arr, len(digits)), "set_digits")
+        self.n_digits = int(L.or_n_digits(self._c))
+        self.digits = list(digits) if digits is not None else [1] * self.n_data
         self.primes = [int(L.or_prime(self._c, i)) for i in range(self.n_data + self.n_special)]
         self.psi = [int(L.or_psi(self._c, i)) for i in range(self.n_data + self.n_special)]
         self.keys = set()
@@ -152,6 +161,13 @@ class Context:
     @property
     def special(self):
         return self.primes[self.n_data] if self.n_special else None
+
+    @property
+    def special_product(self):
+        P = 1
+        for q in self.primes[self.n_data:]:
+            P *= q
+        return P
 
     @property
     def top_level(self):
@@ -210,7 +226,7 @@ class Context:
 
     def export_key(self, key_id):
         L = self.n_data
-        out = np.empty((L, 2, L + 1, self.n), dtype=np.uint64)
+        out = np.empty((self.n_digits, 2, L + self.n_special, self.n), dtype=np.uint64)
         _check(lib().or_export_key(self._c, key_id, _p(out)), "export_key")
         return out
 
@@ -304,12 +320,12 @@ class Context:
         _check(lib().or_rotate_hoisted(self._c, _p(ct), ct.shape[1] - 1, step, _p(out)), f"rotate_hoisted({step})")
         return out
 
-    # ---- QP basis (double hoisting, R11c): [ncomp][l+2][N], last limb mod P
+    # ---- QP basis (double hoisting, R11c): [ncomp][l+1+K][N], the last K limbs mod P_0..P_{K-1}
     def rotate_hoisted_qp(self, ct, step):
         """Baby step of R11c: hoisted rotation of a Q_l ciphertext left in the Q_l P basis."""
         ct = np.ascontiguousarray(ct, dtype=np.uint64)
         nl = ct.shape[1]
-        out = np.empty((2, nl + 1, self.n), dtype=np.uint64)
+        out = np.empty((2, nl + self.n_special, self.n), dtype=np.uint64)
         _check(lib().or_rotate_hoisted_qp(self._c, _p(ct), nl - 1, step, _p(out)), f"rotate_hoisted_qp({step})")
         return out
 
@@ -317,26 +333,27 @@ class Context:
         """Giant step of R11c: rotation of a Q_l P ciphertext, result in Q_l P."""
         w = np.ascontiguousarray(w, dtype=np.uint64)
         out = np.empty_like(w)
-        _check(lib().or_rotate_qp(self._c, _p(w), w.shape[1] - 2, step, _p(out)), f"rotate_qp({step})")
+        _check(lib().or_rotate_qp(self._c, _p(w), w.shape[1] - 1 - self.n_special, step, _p(out)),
+               f"rotate_qp({step})")
         return out
 
     def moddown(self, x):
         x = np.ascontiguousarray(x, dtype=np.uint64)
         ncomp, ne = x.shape[0], x.shape[1]
-        out = np.empty((ncomp, ne - 1, self.n), dtype=np.uint64)
-        lib().or_moddown(self._c, _p(x), ne - 2, ncomp, _p(out))
+        out = np.empty((ncomp, ne - self.n_special, self.n), dtype=np.uint64)
+        lib().or_moddown(self._c, _p(x), ne - 1 - self.n_special, ncomp, _p(out))
         return out
 
     def lift_qp(self, ct):
         ct = np.ascontiguousarray(ct, dtype=np.uint64)
         ncomp, nl = ct.shape[0], ct.shape[1]
-        out = np.empty((ncomp, nl + 1, self.n), dtype=np.uint64)
+        out = np.empty((ncomp, nl + self.n_special, self.n), dtype=np.uint64)
         lib().or_lift_qp(self._c, _p(ct), nl - 1, ncomp, _p(out))
         return out
 
     def plain_qp(self, coeffs, level):
         m = np.ascontiguousarray(coeffs, dtype=np.int64)
-        out = np.empty((level + 2, self.n), dtype=np.uint64)
+        out = np.empty((level + 1 + self.n_special, self.n), dtype=np.uint64)
         lib().or_plain_qp(self._c, _p(m, i64p), level, _p(out))
         return out
 
@@ -345,7 +362,7 @@ class Context:
         pt = np.ascontiguousarray(pt, dtype=np.uint64)
         assert pt.shape[0] == ct.shape[1]
         out = np.empty_like(ct)
-        lib().or_mul_plain_qp(self._c, _p(ct), _p(pt), ct.shape[1] - 2, _p(out))
+        lib().or_mul_plain_qp(self._c, _p(ct), _p(pt), ct.shape[1] - 1 - self.n_special, _p(out))
         return out
 
     def add_qp(self, a, b):
@@ -353,7 +370,7 @@ class Context:
         b = np.ascontiguousarray(b, dtype=np.uint64)
         assert a.shape == b.shape
         out = np.empty_like(a)
-        lib().or_add_qp(self._c, _p(a), _p(b), a.shape[1] - 2, a.shape[0], _p(out))
+        lib().or_add_qp(self._c, _p(a), _p(b), a.shape[1] - 1 - self.n_special, a.shape[0], _p(out))
         return out
 
     def rescale(self, ct):

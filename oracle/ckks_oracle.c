@@ -20,6 +20,11 @@
  * and against schoolbook negacyclic convolution.
  *
  * All residues handed in or out are canonical, in [0, q).
+ *
+ * Key switching generalises to the hybrid form of SURVEY 8(f) row f-3 (readings R9b, R17b,
+ * R10b): the data primes are partitioned into dnum digits of consecutive primes (default: one digit per
+ * prime) and there are K >= 1 special primes with P = their product.  Digit values are integers
+ * (CRT lifts, up to 2^126) held in `__int128`.
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -31,6 +36,9 @@ typedef unsigned __int128 u128;
 
 #define OR_MAXP 64
 #define OR_MAXKEYS 512
+#define OR_MAXSP 4
+
+typedef __int128 i128;
 
 /* ------------------------------------------------------------------ scalar modular arithmetic */
 
@@ -142,6 +150,9 @@ typedef struct or_ctx {
     u64 n_inv[OR_MAXP];
     u64 cdt[64];            /* discrete-Gaussian CDT thresholds (R13) */
     int cdt_bound;          /* support [-bound, bound]                */
+    /* key-switching digits (R9b): digit j = data primes dig_start[j] .. dig_start[j] + dig_len[j] - 1 */
+    int n_digits;
+    int dig_start[OR_MAXP], dig_len[OR_MAXP];
     /* keys */
     int have_sk;
     int8_t* s;              /* secret coefficients                      */
@@ -149,8 +160,36 @@ typedef struct or_ctx {
     u64* pk;                /* [2][n_data][N] NTT form, top level        */
     int n_keys;
     int64_t key_id[OR_MAXKEYS];
-    u64* key[OR_MAXKEYS];   /* [n_data digits][2][n_data + 1][N] NTT form */
+    u64* key[OR_MAXKEYS];   /* [n_digits][2][n_data + n_special][N] NTT form */
 } or_ctx;
+
+static void default_digits(or_ctx* c)
+{
+    c->n_digits = c->n_data;
+    for (int j = 0; j < c->n_data; j++) { c->dig_start[j] = j; c->dig_len[j] = 1; }
+}
+
+/* Digit partition (R9b): sizes[0..count-1] consecutive data primes per digit, summing to n_data.  Must be
+ * called before any switching key is generated.  Returns -1 on a bad partition. */
+int or_set_digits(or_ctx* c, const int* sizes, int count)
+{
+    if (c->n_keys || count < 1 || count > c->n_data) return -1;
+    int start = 0;
+    for (int j = 0; j < count; j++) {
+        if (sizes[j] < 1) return -1;
+        double bits = 0;
+        for (int k = 0; k < sizes[j] && start + k < c->n_data; k++) bits += log2((double)c->q[start + k]);
+        if (bits > 125.0) return -1;       /* digit values must fit a signed 128-bit integer */
+        c->dig_start[j] = start;
+        c->dig_len[j] = sizes[j];
+        start += sizes[j];
+    }
+    if (start != c->n_data) return -1;
+    c->n_digits = count;
+    return 0;
+}
+int or_n_digits(const or_ctx* c) { return c->n_digits; }
+int or_n_special(const or_ctx* c) { return c->n_special; }
 
 int or_n(const or_ctx* c) { return c->n; }
 int or_n_data(const or_ctx* c) { return c->n_data; }
@@ -236,7 +275,7 @@ int or_cdt_bound(const or_ctx* c) { return c->cdt_bound; }
 
 or_ctx* or_ctx_new(int log_n, int n_data, int n_special, const int* bits, double sigma)
 {
-    if (log_n < 1 || log_n > 17 || n_data < 1 || n_special < 0 || n_special > 1 ||
+    if (log_n < 1 || log_n > 17 || n_data < 1 || n_special < 0 || n_special > OR_MAXSP ||
         n_data + n_special > OR_MAXP)
         return NULL;
     or_ctx* c = (or_ctx*)calloc(1, sizeof(or_ctx));
@@ -245,8 +284,14 @@ or_ctx* or_ctx_new(int log_n, int n_data, int n_special, const int* bits, double
     c->n_data = n_data;
     c->n_special = n_special;
     c->sigma = sigma;
+    default_digits(c);
     int np = n_data + n_special;
     if (gen_chain(c, bits, np) != 0) { free(c); return NULL; }
+    {
+        double pbits = 0;   /* P = product of the special primes must fit a signed 128-bit integer */
+        for (int k = 0; k < n_special; k++) pbits += log2((double)c->q[n_data + k]);
+        if (pbits > 125.0) { free(c); return NULL; }
+    }
     for (int i = 0; i < np; i++) {
         u64 q = c->q[i];
         c->psi[i] = min_primitive_2n_root(q, c->n);
@@ -270,7 +315,7 @@ or_ctx* or_ctx_new(int log_n, int n_data, int n_special, const int* bits, double
 /* Test-only constructor with an explicit prime list (for the N=8, q=17 worked example). */
 or_ctx* or_ctx_new_primes(int log_n, int n_data, int n_special, const u64* primes, double sigma)
 {
-    if (log_n < 1 || log_n > 17 || n_data < 1 || n_special < 0 || n_special > 1 ||
+    if (log_n < 1 || log_n > 17 || n_data < 1 || n_special < 0 || n_special > OR_MAXSP ||
         n_data + n_special > OR_MAXP)
         return NULL;
     or_ctx* c = (or_ctx*)calloc(1, sizeof(or_ctx));
@@ -279,6 +324,7 @@ or_ctx* or_ctx_new_primes(int log_n, int n_data, int n_special, const u64* prime
     c->n_data = n_data;
     c->n_special = n_special;
     c->sigma = sigma;
+    default_digits(c);
     for (int i = 0; i < n_data + n_special; i++) {
         u64 q = primes[i];
         if (!is_prime_u64(q) || (q - 1) % (2ULL * (u64)c->n) != 0) { free(c); return NULL; }
@@ -437,20 +483,30 @@ static int find_key(const or_ctx* c, int64_t id)
     return -1;
 }
 
+/* P = product of the special primes, reduced mod q (R17b) */
+static u64 special_product_mod(const or_ctx* c, u64 q)
+{
+    u64 r = 1 % q;
+    for (int k = 0; k < c->n_special; k++) r = mulmod(r, c->q[c->n_data + k] % q, q);
+    return r;
+}
+
 /*
- * Key-switching key from s' to s (R5): for every digit j < n_data (one digit per data prime,
- * S:L214) and every prime p in {q_0..q_{L-1}, P}:
- *     b_j[p] = -a_j[p] s[p] + e_j[p] + [p == j] (P mod q_j) s'[p],      a_j[p] uniform (NTT form).
+ * Key-switching key from s' to s (R5, R17b): for every digit j < n_digits (one digit per data prime by
+ * default; groups of consecutive primes in the hybrid form, R9b) and every prime p in
+ * {q_0..q_{L-1}, P_0..P_{K-1}}:
+ *     b_j[p] = -a_j[p] s[p] + e_j[p] + [p in digit j] (P mod p) s'[p],      a_j[p] uniform (NTT form),
+ * P = P_0 ... P_{K-1}: the gadget is P times the CRT idempotent of digit j (1 mod the digit's primes,
+ * 0 mod every other prime), so sum_j d_j g_j = P d mod Q for digits d_j = d mod Q_j.
  * id 0 -> s' = s^2 (relinearisation key); id = g (odd) -> s' = sigma_g(s) (Galois key).
- * Layout: [digit j][component c][prime p = 0..L][N], special prime last.
+ * Layout: [digit j][component c][prime p = 0..L+K-1][N], special primes last.
  */
 int or_gen_switch_key(or_ctx* c, u64 seed, int64_t id)
 {
-    if (!c->have_sk || c->n_special != 1) return -1;
+    if (!c->have_sk || c->n_special < 1) return -1;
     if (find_key(c, id) >= 0) return 0;
     if (c->n_keys >= OR_MAXKEYS) return -1;
-    int n = c->n, L = c->n_data, np = L + 1;
-    u64 P = c->q[L];
+    int n = c->n, L = c->n_data, np = L + c->n_special, D = c->n_digits;
     /* s' in NTT form over all primes */
     u64* sprime = (u64*)malloc(sizeof(u64) * (size_t)np * n);
     if (id == 0) {
@@ -469,10 +525,10 @@ int or_gen_switch_key(or_ctx* c, u64 seed, int64_t id)
         }
         free(coef);
     }
-    u64* key = (u64*)malloc(sizeof(u64) * (size_t)L * 2 * np * n);
+    u64* key = (u64*)malloc(sizeof(u64) * (size_t)D * 2 * np * n);
     int64_t* ecoef = (int64_t*)malloc(sizeof(int64_t) * n);
     u64* e = (u64*)malloc(sizeof(u64) * n);
-    for (int j = 0; j < L; j++) {
+    for (int j = 0; j < D; j++) {
         or_sample_gaussian(c, seed, or_stream(TAG_KS_E, (u64)id, (u64)j, 0), ecoef, n);
         for (int p = 0; p < np; p++) {
             u64 q = c->q[p];
@@ -481,7 +537,8 @@ int or_gen_switch_key(or_ctx* c, u64 seed, int64_t id)
             or_sample_uniform(seed, or_stream(TAG_KS_A, (u64)id, (u64)j, (u64)p), q, a, n);
             small_to_ntt(c, p, ecoef, e);
             const u64* s = sp(c, c->s_ntt, p);
-            u64 gadget = (p == j) ? (P % q) : 0;
+            int in_digit = p < L && p >= c->dig_start[j] && p < c->dig_start[j] + c->dig_len[j];
+            u64 gadget = in_digit ? special_product_mod(c, q) : 0;
             for (int k = 0; k < n; k++) {
                 u64 v = addmod(negmod(mulmod(a[k], s[k], q), q), e[k], q);
                 if (gadget) v = addmod(v, mulmod(gadget, sp(c, sprime, p)[k], q), q);
@@ -502,8 +559,8 @@ int or_export_key(const or_ctx* c, int64_t id, u64* out)
 {
     int k = find_key(c, id);
     if (k < 0) return -3;
-    size_t np = (size_t)c->n_data + 1;
-    memcpy(out, c->key[k], sizeof(u64) * (size_t)c->n_data * 2 * np * c->n);
+    size_t np = (size_t)c->n_data + c->n_special;
+    memcpy(out, c->key[k], sizeof(u64) * (size_t)c->n_digits * 2 * np * c->n);
     return 0;
 }
 int or_export_secret(const or_ctx* c, int8_t* out)
@@ -639,29 +696,67 @@ static u64 centered_mod(u64 r, u64 m, u64 q)
 }
 
 /* ------------------------------------------------------------------ key switching (R5, R9-R12) */
-/*
- * Key switch from explicit digit polynomials (signed integer coefficients, one digit per data
- * prime j <= l), R-KS steps 2-4:
- *   2. ModUp: D_{j,p} = NTT_p(digit_j mod p) for every p in {q_0..q_l, P}
- *   3. inner product  u~_c[p] = sum_{j<=l} D_{j,p} key_j.c[p]   mod p
- *   4. ModDown: r = centered(iNTT_P(u~_c[P])),  u_c[i] = (u~_c[i] - NTT_{q_i}(r mod q_i)) P^{-1} mod q_i
- */
-/* steps 2-3 into the extended basis: out_qp [2][l+2][N], limb l+1 = P  (no ModDown) */
-static void ks_ip_qp(const or_ctx* c, const int64_t* digit, int level, int kidx, u64* acc)
+/* signed 128-bit integer -> residue mod q */
+static u64 from_i128(i128 x, u64 q)
 {
-    int n = c->n, L = c->n_data, nl = level + 1, np_key = L + 1;
+    i128 r = x % (i128)q;
+    return (u64)(r < 0 ? r + (i128)q : r);
+}
+/* CRT lift (Garner, R9b) of residues r[0..k-1] modulo m[0..k-1] (distinct primes) to the unique integer
+ * in [0, m_0 ... m_{k-1}); the product must stay below 2^127. */
+static i128 crt_lift(const u64* r, const u64* m, int k)
+{
+    unsigned __int128 x = r[0], M = m[0];
+    for (int i = 1; i < k; i++) {
+        u64 xm = (u64)(x % m[i]);
+        u64 t = mulmod(submod(r[i], xm, m[i]), invmod((u64)(M % m[i]), m[i]), m[i]);
+        x += M * t;
+        M *= m[i];
+    }
+    return (i128)x;
+}
+static unsigned __int128 special_product(const or_ctx* c)
+{
+    unsigned __int128 P = 1;
+    for (int k = 0; k < c->n_special; k++) P *= c->q[c->n_data + k];
+    return P;
+}
+/* prime index of limb e of a Q_l P (extended-basis) polynomial: data primes 0..l, then P_0..P_{K-1} */
+static int ext_prime(const or_ctx* c, int level, int e) { return e <= level ? e : c->n_data + (e - level - 1); }
+/* number of active digits at level l and the active primes of digit j (a digit is cut at the level) */
+static int active_digits(const or_ctx* c, int level)
+{
+    int d = 0;
+    while (d < c->n_digits && c->dig_start[d] <= level) d++;
+    return d;
+}
+static int digit_len_at(const or_ctx* c, int j, int level)
+{
+    int end = c->dig_start[j] + c->dig_len[j];
+    if (end > level + 1) end = level + 1;
+    return end - c->dig_start[j];
+}
+
+/*
+ * Key switch from explicit digit polynomials (signed integer coefficients, one per active digit j),
+ * R-KS steps 2-4:
+ *   2. ModUp: D_{j,p} = NTT_p(digit_j mod p) for every p in {q_0..q_l, P_0..P_{K-1}}
+ *   3. inner product  u~_c[p] = sum_j D_{j,p} key_j.c[p]   mod p
+ *   4. ModDown: r = centered(CRT_P(iNTT(u~_c[P_k]))),  u_c[i] = (u~_c[i] - NTT_{q_i}(r mod q_i)) P^{-1} mod q_i
+ */
+/* steps 2-3 into the extended basis: acc [2][l+1+K][N]  (no ModDown) */
+static void ks_ip_qp(const or_ctx* c, const i128* digit, int level, int kidx, u64* acc)
+{
+    int n = c->n, L = c->n_data, nl = level + 1, np_key = L + c->n_special;
     const u64* key = c->key[kidx];
-    int ext[OR_MAXP];
-    for (int i = 0; i < nl; i++) ext[i] = i;
-    ext[nl] = L;
-    int ne = nl + 1;
+    int ne = nl + c->n_special, nd = active_digits(c, level);
     memset(acc, 0, sizeof(u64) * (size_t)2 * ne * n);
     u64* D = (u64*)malloc(sizeof(u64) * n);
-    for (int j = 0; j < nl; j++) {
+    for (int j = 0; j < nd; j++) {
         for (int e = 0; e < ne; e++) {
-            int p = ext[e];
+            int p = ext_prime(c, level, e);
             u64 q = c->q[p];
-            for (int k = 0; k < n; k++) D[k] = from_signed(digit[(size_t)j * n + k], q);
+            for (int k = 0; k < n; k++) D[k] = from_i128(digit[(size_t)j * n + k], q);
             or_ntt(c, p, D);
             for (int comp = 0; comp < 2; comp++) {
                 const u64* kv = key + (((size_t)j * 2 + comp) * np_key + p) * n;
@@ -673,32 +768,44 @@ static void ks_ip_qp(const or_ctx* c, const int64_t* digit, int level, int kidx,
     free(D);
 }
 
-/* step 4 on one component: in [l+2][N] (QP basis) -> out [l+1][N] */
+/* step 4 on one component: in [l+1+K][N] (QP basis) -> out [l+1][N] */
 static void moddown_comp(const or_ctx* c, const u64* in, int level, u64* out)
 {
-    int n = c->n, L = c->n_data, nl = level + 1;
-    u64 P = c->q[L];
-    u64* r = (u64*)malloc(sizeof(u64) * n);
+    int n = c->n, L = c->n_data, nl = level + 1, K = c->n_special;
+    unsigned __int128 P = special_product(c);
+    u64* rs = (u64*)malloc(sizeof(u64) * (size_t)K * n);   /* coefficient residues mod P_k */
+    u64 pm[OR_MAXSP];
+    for (int k = 0; k < K; k++) {
+        memcpy(rs + (size_t)k * n, in + (size_t)(nl + k) * n, sizeof(u64) * n);
+        or_intt(c, L + k, rs + (size_t)k * n);
+        pm[k] = c->q[L + k];
+    }
+    /* r = the centred representative of the CRT of the special residues, (-P/2, P/2) (R10b) */
+    i128* r = (i128*)malloc(sizeof(i128) * n);
+    for (int k = 0; k < n; k++) {
+        u64 v[OR_MAXSP];
+        for (int m = 0; m < K; m++) v[m] = rs[(size_t)m * n + k];
+        unsigned __int128 x = (unsigned __int128)crt_lift(v, pm, K);
+        r[k] = x <= (P - 1) / 2 ? (i128)x : -(i128)(P - x);
+    }
     u64* t = (u64*)malloc(sizeof(u64) * n);
-    memcpy(r, in + (size_t)nl * n, sizeof(u64) * n);
-    or_intt(c, L, r);
     for (int i = 0; i < nl; i++) {
         u64 q = c->q[i];
-        u64 pinv = invmod(P % q, q);
-        for (int k = 0; k < n; k++) t[k] = centered_mod(r[k], P, q);
+        u64 pinv = invmod(special_product_mod(c, q), q);
+        for (int k = 0; k < n; k++) t[k] = from_i128(r[k], q);
         or_ntt(c, i, t);
         const u64* a = in + (size_t)i * n;
         u64* o = out + (size_t)i * n;
         for (int k = 0; k < n; k++) o[k] = mulmod(submod(a[k], t[k], q), pinv, q);
     }
-    free(r); free(t);
+    free(rs); free(r); free(t);
 }
 
-static int ks_from_digits(const or_ctx* c, const int64_t* digit, int level, int64_t key_id, u64* out)
+static int ks_from_digits(const or_ctx* c, const i128* digit, int level, int64_t key_id, u64* out)
 {
     int kidx = find_key(c, key_id);
     if (kidx < 0) return -3;
-    int n = c->n, nl = level + 1, ne = nl + 1;
+    int n = c->n, nl = level + 1, ne = nl + c->n_special;
     u64* acc = (u64*)malloc(sizeof(u64) * (size_t)2 * ne * n);
     ks_ip_qp(c, digit, level, kidx, acc);
     for (int comp = 0; comp < 2; comp++)
@@ -707,19 +814,42 @@ static int ks_from_digits(const or_ctx* c, const int64_t* digit, int level, int6
     return 0;
 }
 
-/* digits of d (NTT form): d_j = iNTT_{q_j}(d[j]) as integers in [0, q_j)  (R9, unsigned lift) */
-static int64_t* digits_of(const or_ctx* c, const u64* d, int level)
+/* digits of d (NTT form, l+1 limbs) (R9, R9b): d_j = the CRT lift of iNTT_{q}(d[q]) over the active
+ * primes q of digit j, an integer in [0, prod q) (unsigned lift); [n_active_digits][N] */
+static i128* digits_of(const or_ctx* c, const u64* d, int level)
 {
-    int n = c->n, nl = level + 1;
-    int64_t* digit = (int64_t*)malloc(sizeof(int64_t) * (size_t)nl * n);
-    u64* tmp = (u64*)malloc(sizeof(u64) * n);
-    for (int j = 0; j < nl; j++) {
-        memcpy(tmp, d + (size_t)j * n, sizeof(u64) * n);
-        or_intt(c, j, tmp);
-        for (int k = 0; k < n; k++) digit[(size_t)j * n + k] = (int64_t)tmp[k];
+    int n = c->n, nd = active_digits(c, level);
+    i128* digit = (i128*)malloc(sizeof(i128) * (size_t)nd * n);
+    u64* tmp = (u64*)malloc(sizeof(u64) * (size_t)(level + 1) * n);
+    for (int i = 0; i <= level; i++) {
+        memcpy(tmp + (size_t)i * n, d + (size_t)i * n, sizeof(u64) * n);
+        or_intt(c, i, tmp + (size_t)i * n);
+    }
+    for (int j = 0; j < nd; j++) {
+        int s0 = c->dig_start[j], len = digit_len_at(c, j, level);
+        for (int k = 0; k < n; k++) {
+            u64 r[OR_MAXP], m[OR_MAXP];
+            for (int i = 0; i < len; i++) { r[i] = tmp[(size_t)(s0 + i) * n + k]; m[i] = c->q[s0 + i]; }
+            digit[(size_t)j * n + k] = crt_lift(r, m, len);
+        }
     }
     free(tmp);
     return digit;
+}
+/* sigma_g on signed integer digit polynomials (coefficient i -> i g mod 2N, negated if >= N) */
+static i128* sigma_digits(const or_ctx* c, const i128* digit, int nd, u64 g)
+{
+    int n = c->n;
+    i128* sd = (i128*)calloc((size_t)nd * n, sizeof(i128));   /* sigma_g is a bijection */
+    u64 two_n = 2ULL * (u64)n;
+    for (int j = 0; j < nd; j++)
+        for (u64 i = 0; i < (u64)n; i++) {
+            u64 e = (i * g) % two_n;
+            i128 v = digit[(size_t)j * n + i];
+            if (e < (u64)n) sd[(size_t)j * n + e] = v;
+            else sd[(size_t)j * n + (e - n)] = -v;
+        }
+    return sd;
 }
 
 /* KS(d; key) at level l with the unsigned digits of d (R-KS step 1 + ks_from_digits). */
@@ -727,7 +857,7 @@ int or_keyswitch(const or_ctx* c, const u64* d, int level, int64_t key_id, u64* 
 {
     if (find_key(c, key_id) < 0) return -3;
     if (level < 0 || level >= c->n_data) return -2;
-    int64_t* digit = digits_of(c, d, level);
+    i128* digit = digits_of(c, d, level);
     int st = ks_from_digits(c, digit, level, key_id, out);
     free(digit);
     return st;
@@ -777,8 +907,8 @@ int or_rotate(const or_ctx* c, const u64* ct, int level, int64_t step, u64* out)
 /*
  * Hoisted rotation (NEXT f-1; reading R11b): the digits are taken from the UNROTATED c1 and the
  * automorphism is applied to them as signed integer polynomials,
- *     d_j = iNTT_{q_j}(c1[j]) in [0, q_j),   d'_j = sigma_g(d_j)  (coefficient i -> i g mod 2N, negated
- *     if >= N, as a signed integer: -d, not q_j - d),
+ *     d_j = digits of c1 (R9 / R9b, unsigned lift),   d'_j = sigma_g(d_j)  (coefficient i -> i g mod 2N,
+ *     negated if >= N, as a signed integer: -d, not Q_j - d),
  *     (sigma_g(c0), 0) + ModDown(sum_j ModUp(d'_j) key_j).
  * All rotations of one ciphertext can then share ModUp(d_j) (sigma_g commutes with NTT_p).  The
  * result differs from the non-hoisted one by an encryption of a small value (different rounding
@@ -791,16 +921,8 @@ int or_rotate_hoisted(const or_ctx* c, const u64* ct, int level, int64_t step, u
     u64 g = or_galois_elt(c, step);
     if (g == 1) { memcpy(out, ct, sizeof(u64) * 2 * h); return 0; }
     if (find_key(c, (int64_t)g) < 0) return -3;
-    int64_t* digit = digits_of(c, ct + h, level);
-    int64_t* sd = (int64_t*)calloc((size_t)nl * n, sizeof(int64_t));   /* sigma_g is a bijection */
-    u64 two_n = 2ULL * (u64)n;
-    for (int j = 0; j < nl; j++)
-        for (u64 i = 0; i < (u64)n; i++) {
-            u64 e = (i * g) % two_n;
-            int64_t v = digit[(size_t)j * n + i];
-            if (e < (u64)n) sd[(size_t)j * n + e] = v;
-            else sd[(size_t)j * n + (e - n)] = -v;
-        }
+    i128* digit = digits_of(c, ct + h, level);
+    i128* sd = sigma_digits(c, digit, active_digits(c, level), g);
     u64* u = (u64*)malloc(sizeof(u64) * 2 * h);
     int st = ks_from_digits(c, sd, level, (int64_t)g, u);
     if (st == 0) {
@@ -822,38 +944,39 @@ int or_rotate_hoisted(const or_ctx* c, const u64* ct, int level, int64_t step, u
 /*
  * NEXT f-1 second stage (R11c, "double hoisting"): the BSGS baby-step rotations are left in
  * the extended basis Q_l P (no ModDown), the inner sums and the giant-step rotations are accumulated
- * there, and ONE ModDown per layer brings the sum back to Q_l.  A QP ciphertext at level l has l+2
- * limbs per component: q_0..q_l, then P.
+ * there, and ONE ModDown per layer brings the sum back to Q_l.  A QP ciphertext at level l has l+1+K
+ * limbs per component: q_0..q_l, then P_0..P_{K-1}.
  */
-static u64 ext_q(const or_ctx* c, int level, int e) { return e <= level ? c->q[e] : c->q[c->n_data]; }
+static u64 ext_q(const or_ctx* c, int level, int e) { return c->q[ext_prime(c, level, e)]; }
 
-/* step 4 (ModDown) on ncomp components: in [ncomp][l+2][N] -> out [ncomp][l+1][N] */
+/* step 4 (ModDown) on ncomp components: in [ncomp][l+1+K][N] -> out [ncomp][l+1][N] */
 void or_moddown(const or_ctx* c, const u64* in_qp, int level, int ncomp, u64* out)
 {
-    int n = c->n, nl = level + 1;
+    int n = c->n, nl = level + 1, ne = nl + c->n_special;
     for (int comp = 0; comp < ncomp; comp++)
-        moddown_comp(c, in_qp + (size_t)comp * (nl + 1) * n, level, out + (size_t)comp * nl * n);
+        moddown_comp(c, in_qp + (size_t)comp * ne * n, level, out + (size_t)comp * nl * n);
 }
 
-/* P * ct in the QP basis: residues P c mod q_i on the data limbs, 0 mod P */
+/* P * ct in the QP basis: residues P c mod q_i on the data limbs, 0 mod every P_k */
 void or_lift_qp(const or_ctx* c, const u64* ct, int level, int ncomp, u64* out)
 {
-    int n = c->n, nl = level + 1;
-    u64 P = c->q[c->n_data];
+    int n = c->n, nl = level + 1, ne = nl + c->n_special;
     for (int comp = 0; comp < ncomp; comp++) {
-        for (int i = 0; i < nl; i++)
+        for (int i = 0; i < nl; i++) {
+            u64 pm = special_product_mod(c, c->q[i]);
             for (int k = 0; k < n; k++)
-                out[((size_t)comp * (nl + 1) + i) * n + k] = mulmod(ct[((size_t)comp * nl + i) * n + k], P % c->q[i], c->q[i]);
-        memset(out + ((size_t)comp * (nl + 1) + nl) * n, 0, sizeof(u64) * n);
+                out[((size_t)comp * ne + i) * n + k] = mulmod(ct[((size_t)comp * nl + i) * n + k], pm, c->q[i]);
+        }
+        memset(out + ((size_t)comp * ne + nl) * n, 0, sizeof(u64) * (size_t)c->n_special * n);
     }
 }
 
-/* plaintext of integer coefficients m over q_0..q_l, P (NTT form) */
+/* plaintext of integer coefficients m over q_0..q_l, P_0..P_{K-1} (NTT form) */
 void or_plain_qp(const or_ctx* c, const int64_t* m, int level, u64* out)
 {
-    int n = c->n, nl = level + 1;
-    for (int e = 0; e <= nl; e++) {
-        int p = e < nl ? e : c->n_data;
+    int n = c->n, ne = level + 1 + c->n_special;
+    for (int e = 0; e < ne; e++) {
+        int p = ext_prime(c, level, e);
         u64* o = out + (size_t)e * n;
         for (int k = 0; k < n; k++) o[k] = from_signed(m[k], c->q[p]);
         or_ntt(c, p, o);
@@ -862,7 +985,7 @@ void or_plain_qp(const or_ctx* c, const int64_t* m, int level, u64* out)
 
 void or_mul_plain_qp(const or_ctx* c, const u64* ct, const u64* pt, int level, u64* out)
 {
-    int n = c->n, ne = level + 2;
+    int n = c->n, ne = level + 1 + c->n_special;
     for (int comp = 0; comp < 2; comp++)
         for (int e = 0; e < ne; e++) {
             u64 q = ext_q(c, level, e);
@@ -875,7 +998,7 @@ void or_mul_plain_qp(const or_ctx* c, const u64* ct, const u64* pt, int level, u
 
 void or_add_qp(const or_ctx* c, const u64* a, const u64* b, int level, int ncomp, u64* out)
 {
-    int n = c->n, ne = level + 2;
+    int n = c->n, ne = level + 1 + c->n_special;
     for (int comp = 0; comp < ncomp; comp++)
         for (int e = 0; e < ne; e++) {
             u64 q = ext_q(c, level, e);
@@ -888,45 +1011,36 @@ void or_add_qp(const or_ctx* c, const u64* a, const u64* b, int level, int ncomp
 
 /* Baby step (R11c): the hoisted rotation of R11b without its ModDown,
  *   (P sigma_g(c0) + sum_j ModUp(d'_j) gk_j.c0,  sum_j ModUp(d'_j) gk_j.c1)  over Q_l P,
- * d'_j = sigma_g(d_j) as signed integers, d_j = iNTT_{q_j}(c1[j]).  step 0: P ct. */
+ * d'_j = sigma_g(d_j) as signed integers, d_j the digits of c1.  step 0: P ct. */
 int or_rotate_hoisted_qp(const or_ctx* c, const u64* ct, int level, int64_t step, u64* out)
 {
-    int n = c->n, nl = level + 1, ne = nl + 1;
+    int n = c->n, nl = level + 1;
     size_t h = (size_t)nl * n;
     u64 g = or_galois_elt(c, step);
     if (g == 1) { or_lift_qp(c, ct, level, 2, out); return 0; }
     int kidx = find_key(c, (int64_t)g);
     if (kidx < 0) return -3;
-    int64_t* digit = digits_of(c, ct + h, level);
-    int64_t* sd = (int64_t*)calloc((size_t)nl * n, sizeof(int64_t));   /* sigma_g is a bijection */
-    u64 two_n = 2ULL * (u64)n;
-    for (int j = 0; j < nl; j++)
-        for (u64 i = 0; i < (u64)n; i++) {
-            u64 e = (i * g) % two_n;
-            int64_t v = digit[(size_t)j * n + i];
-            if (e < (u64)n) sd[(size_t)j * n + e] = v;
-            else sd[(size_t)j * n + (e - n)] = -v;
-        }
+    i128* digit = digits_of(c, ct + h, level);
+    i128* sd = sigma_digits(c, digit, active_digits(c, level), g);
     ks_ip_qp(c, sd, level, kidx, out);
-    u64 P = c->q[c->n_data];
     u64* rc0 = (u64*)malloc(sizeof(u64) * n);
     for (int p = 0; p < nl; p++) {
         u64 q = c->q[p];
+        u64 pm = special_product_mod(c, q);
         or_automorphism_ntt(c, p, ct + (size_t)p * n, g, rc0);
         u64* o = out + (size_t)p * n;                       /* component 0, limb p */
-        for (int k = 0; k < n; k++) o[k] = addmod(o[k], mulmod(rc0[k], P % q, q), q);
+        for (int k = 0; k < n; k++) o[k] = addmod(o[k], mulmod(rc0[k], pm, q), q);
     }
-    (void)ne;
     free(rc0); free(digit); free(sd);
     return 0;
 }
 
 /* Giant step (R11c) on a QP ciphertext w:
- *   c1' = ModDown(w.c1),  digits d_j = iNTT_{q_j}(sigma_g(c1')[j])  (unsigned, as R9),
+ *   c1' = ModDown(w.c1),  digits d_j of sigma_g(c1') (unsigned, as R9 / R9b),
  *   (sigma_g(w.c0) + sum_j ModUp(d_j) gk_j.c0,  sum_j ModUp(d_j) gk_j.c1)  over Q_l P.  step 0: w. */
 int or_rotate_qp(const or_ctx* c, const u64* w, int level, int64_t step, u64* out)
 {
-    int n = c->n, nl = level + 1, ne = nl + 1;
+    int n = c->n, nl = level + 1, ne = nl + c->n_special;
     size_t hq = (size_t)ne * n, h = (size_t)nl * n;
     u64 g = or_galois_elt(c, step);
     if (g == 1) { memcpy(out, w, sizeof(u64) * 2 * hq); return 0; }
@@ -936,11 +1050,11 @@ int or_rotate_qp(const or_ctx* c, const u64* w, int level, int64_t step, u64* ou
     moddown_comp(c, w + hq, level, c1);
     u64* rc1 = (u64*)malloc(sizeof(u64) * h);
     for (int p = 0; p < nl; p++) or_automorphism_ntt(c, p, c1 + (size_t)p * n, g, rc1 + (size_t)p * n);
-    int64_t* digit = digits_of(c, rc1, level);
+    i128* digit = digits_of(c, rc1, level);
     ks_ip_qp(c, digit, level, kidx, out);
     u64* r0 = (u64*)malloc(sizeof(u64) * n);
     for (int e = 0; e < ne; e++) {
-        int p = e < nl ? e : c->n_data;
+        int p = ext_prime(c, level, e);
         u64 q = c->q[p];
         or_automorphism_ntt(c, p, w + (size_t)e * n, g, r0);
         u64* o = out + (size_t)e * n;
