@@ -53,11 +53,16 @@ typedef struct ckks_model ckks_model;
 
 /* Scheme parameters (R1, R13-R15).  Primes: for each entry of prime_bits in order, the largest
  * unused prime q < 2^bits with q = 1 mod 2N; the first n_data are q_0..q_{L-1}, then the special
- * prime P (n_special = 1) used by key switching.  Keys are generated on the device from key_seed. */
+ * primes P_0..P_{K-1} (K = n_special) used by key switching, P = P_0 ... P_{K-1}.  Keys are generated
+ * on the device from key_seed.
+ * Key switching (readings R9b/R10b/R17b): the data primes are split into dnum
+ * digits of consecutive primes (digit_sizes, each 1 or 2; NULL = one digit per prime);
+ * K = 2 special primes with 2-prime digits is the hybrid form (fewer ModUp NTTs: dnum digits instead
+ * of L, each lifted by an exact 2-prime CRT).  Switching keys are [dnum][2][L+K][N]. */
 typedef struct {
     uint32_t log_n;             /* 10..14 (N = 1024 .. 16384; one limb must fit shared memory)     */
     uint32_t n_data;            /* L >= 1 data primes                                              */
-    uint32_t n_special;         /* 0 (NTT-only context) or 1                                       */
+    uint32_t n_special;         /* 0 (NTT-only context), 1 or 2 special primes                     */
     const uint32_t* prime_bits; /* n_data + n_special entries, each in [log_n + 2, 61]             */
     double sigma;               /* discrete Gaussian error parameter, 3.2 (R13)                    */
     uint64_t key_seed;          /* seed of the counter-based PRNG for s, pk, relin and Galois keys */
@@ -68,13 +73,17 @@ typedef struct {
     uint32_t bsgs_baby_extra;   /* dense layers of this context use t1 = 2^(ceil(log2 t / 2) + x)   */
                                 /* baby steps (x = this, 0..4; R5 is x = 0, see ckks_bsgs_plan_x);  */
                                 /* rot_steps must cover the resulting baby/giant steps               */
+    const uint32_t* digit_sizes; /* n_digits entries in {1, 2} summing to n_data, or NULL (all 1)     */
+    uint32_t n_digits;
 } ckks_params;
 
 /* Host-readable context description. */
 typedef struct {
     uint32_t log_n, n, n_data, n_special, n_keys;
-    uint64_t primes[16];        /* q_0..q_{L-1}, then P                                            */
+    uint64_t primes[16];        /* q_0..q_{L-1}, then P_0..P_{K-1}                                 */
     uint64_t psi[16];           /* minimal primitive 2N-th root used by the NTT (R2)               */
+    uint32_t n_digits;          /* key-switching digits dnum                                       */
+    uint32_t digit_sizes[16];
 } ckks_info;
 
 /* Layer kinds (the paper's frozen stack).  Every layer is evaluated as
@@ -290,7 +299,7 @@ ckks_status ckks_decrypt(ckks_ctx* ctx, const ckks_ct* in, uint64_t* d_out, void
 ckks_status ckks_decode(const ckks_ctx* ctx, const uint64_t* h_residues, uint32_t level, double scale, double* values,
                         uint32_t count);
 /* Export key material to host memory (synchronises `stream`):
- *   key_id 0 = relinearisation key, key_id = g (odd) = Galois key: [L][2][L+1][N] NTT form;
+ *   key_id 0 = relinearisation key, key_id = g (odd) = Galois key: [dnum][2][L+K][N] NTT form;
  *   key_id -1 = secret s in NTT form over all primes [L + n_special][N];
  *   key_id -2 = public key [2][L][N] NTT form.  (Test/parity use only.) */
 ckks_status ckks_export_key(ckks_ctx* ctx, int64_t key_id, uint64_t* h_out, void* stream);

@@ -31,13 +31,15 @@ class ckks_params(ctypes.Structure):
                 ("prime_bits", ctypes.POINTER(ctypes.c_uint32)), ("sigma", ctypes.c_double),
                 ("key_seed", ctypes.c_uint64), ("rot_steps", ctypes.POINTER(ctypes.c_int32)),
                 ("n_rot_steps", ctypes.c_uint32), ("want_relin", ctypes.c_int32), ("max_batch", ctypes.c_uint32),
-                ("bsgs_baby_extra", ctypes.c_uint32)]
+                ("bsgs_baby_extra", ctypes.c_uint32), ("digit_sizes", ctypes.POINTER(ctypes.c_uint32)),
+                ("n_digits", ctypes.c_uint32)]
 
 
 class ckks_info(ctypes.Structure):
     _fields_ = [("log_n", ctypes.c_uint32), ("n", ctypes.c_uint32), ("n_data", ctypes.c_uint32),
                 ("n_special", ctypes.c_uint32), ("n_keys", ctypes.c_uint32),
-                ("primes", ctypes.c_uint64 * 16), ("psi", ctypes.c_uint64 * 16)]
+                ("primes", ctypes.c_uint64 * 16), ("psi", ctypes.c_uint64 * 16), ("n_digits", ctypes.c_uint32),
+                ("digit_sizes", ctypes.c_uint32 * 16)]
 
 
 class ckks_ct(ctypes.Structure):
@@ -189,7 +191,8 @@ class Context:
     """Owns (as torch tensors) the table/key/workspace buffers that the C context borrows."""
 
     def __init__(self, log_n, data_bits, special_bits=(), key_seed=1, rot_steps=(), want_relin=True,
-                 max_batch=1, sigma=3.2, device="cuda", stream=None, bsgs_baby_extra=0):
+                 max_batch=1, sigma=3.2, device="cuda", stream=None, bsgs_baby_extra=0, digits=None):
+        """digits: key-switching digit sizes (1 or 2 consecutive data primes each, R9b); None = one per prime."""
         import torch
         self.torch = torch
         self.device = torch.device(device)
@@ -197,9 +200,10 @@ class Context:
         self._bits = (ctypes.c_uint32 * len(bits))(*bits)
         steps = [int(s) for s in rot_steps]
         self._steps = (ctypes.c_int32 * max(1, len(steps)))(*steps) if steps else (ctypes.c_int32 * 1)()
+        self._digits = (ctypes.c_uint32 * len(digits))(*[int(d) for d in digits]) if digits else None
         self.params = ckks_params(int(log_n), len(data_bits), len(special_bits), self._bits, float(sigma),
                                   int(key_seed), self._steps, len(steps), 1 if want_relin else 0, int(max_batch),
-                                  int(bsgs_baby_extra))
+                                  int(bsgs_baby_extra), self._digits, len(digits) if digits else 0)
         self.bsgs_baby_extra = int(bsgs_baby_extra)
         tb, kb, wb = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
         _check(lib().ckks_ctx_sizes(ctypes.byref(self.params), ctypes.byref(tb), ctypes.byref(kb),
@@ -219,6 +223,8 @@ class Context:
         self.psi = [int(info.psi[i]) for i in range(self.n_data + self.n_special)]
         self.n_keys = info.n_keys
         self.max_batch = int(max_batch)
+        self.n_digits = info.n_digits
+        self.digits = [int(info.digit_sizes[j]) for j in range(self.n_digits)]
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -367,7 +373,7 @@ class Context:
         elif key_id == -2:
             shape = (2, L, self.n)
         else:
-            shape = (L, 2, L + 1, self.n)
+            shape = (self.n_digits, 2, L + self.n_special, self.n)
         out = np.empty(shape, dtype=np.uint64)
         _check(lib().ckks_export_key(self.h, int(key_id), out.ctypes.data_as(ctypes.c_void_p), _stream(stream)),
                "ckks_export_key")

@@ -203,6 +203,15 @@ struct ckks_ctx {
         cuda_ok(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming), "event");
     }
     int log_n = 0, n = 0, L = 0, ns = 0, np = 0;
+    int nd = 0;                                    // key-switching digits (R9b)
+    std::vector<int> dig_start, dig_len;
+    // digits with at least one active prime at nl limbs (the last may be cut at the level)
+    int active_digits(int nl) const
+    {
+        int d = 0;
+        while (d < nd && dig_start[d] < nl) ++d;
+        return d;
+    }
     double sigma = 3.2;
     uint32_t max_batch = 1;
     uint32_t bsgs_bx = 0;         // extra baby-step doublings of this context's dense layers (R5b)
@@ -234,6 +243,9 @@ struct ckks_ctx {
         l.counter = &launches;
         l.probe = &probe;
         l.pclass = pclass.data();
+        l.n_digits = nd;
+        l.dig_start = dig_start.data();
+        l.dig_len = dig_len.data();
         return l;
     }
     size_t ct_words(int nl, int ncomp = 2) const { return (size_t)ncomp * nl * n; }
@@ -256,7 +268,8 @@ struct ckks_ctx {
         const int64_t r = ((step % slots) + slots) % slots;
         return (uint32_t)h_pow(5, (u64)r, 2ULL * n);
     }
-    // KS workspace views for `B` ciphertexts (sized for the top level)
+    // KS workspace views for `B` ciphertexts (sized for the top level): digits [B][L][N],
+    // ModUp [B][dnum][L+K][N], ModDown outputs [G][B][2][L+K][N], remainders [G][B][3][K][N]
     ck::KsWork ks_work(int B) const
     {
         ck::KsWork w;
@@ -264,9 +277,9 @@ struct ckks_ctx {
         w.digits = p;
         p += (size_t)B * L * n;
         w.modup = p;
-        p += (size_t)B * L * (L + 1) * n;
+        p += (size_t)B * nd * (L + ns) * n;
         w.acc = p;
-        p += (size_t)KS_GMAX * B * 2 * (L + 1) * n;
+        p += (size_t)KS_GMAX * B * 2 * (L + ns) * n;
         w.rem = p;
         return w;
     }
@@ -281,7 +294,7 @@ struct ckks_layer {
     int32_t giant = 0;
     uint32_t region = 0, items = 1;
     double pt_scale, bias_scale;
-    u64* d_pts;     // [t2 * t1][level+2][N]  (limb level+1: mod P, for the double-hoisted Q_l P MAC)
+    u64* d_pts;     // [t2 * t1][level+1+K][N]  (limbs level+1..: mod P_k, for the double-hoisted Q_l P MAC)
     int hoisting = 0;   // ckks_matvec_diag: 0 plain, 1 hoisted baby steps, 2 double hoisting
     u64* d_bias;    // [level][N] or null
 };
@@ -305,9 +318,9 @@ struct ckks_model {
 namespace {
 
 // digits + modup + KS_GMAX x (ModDown outputs x + remainders)
-size_t ks_work_words(int L, int n, int B)
+size_t ks_work_words(int L, int K, int nd, int n, int B)
 {
-    return (size_t)B * n * ((size_t)L + (size_t)L * (L + 1) + (size_t)KS_GMAX * (2 * (L + 1) + 3));
+    return (size_t)B * n * ((size_t)L + (size_t)nd * (L + K) + (size_t)KS_GMAX * (2 * (L + K) + 3 * K));
 }
 size_t enc_work_words(int L, int n, int B) { return (size_t)B * n * (4 * (size_t)L + 1); }
 
@@ -455,7 +468,7 @@ void rotate_qp_impl(ckks_ctx* c, const u64* wq, size_t w_stride, int nl, int B, 
     const u64* key = c->key((int64_t)g);
     if (!key) throw CkksError(CKKS_E_NOKEY, "no Galois key for step " + std::to_string(step));
     auto w = c->ks_work(B);
-    ck::KsIn ki{wq, w_stride, (size_t)(nl + 1) * c->n, g};
+    ck::KsIn ki{wq, w_stride, (size_t)(nl + c->ns) * c->n, g};
     ck::keyswitch_modup(L, ki, B, nl, w, true);
     ck::KsGroup grp{};
     grp.key[0] = key;
@@ -514,15 +527,27 @@ static void sizes_impl(const ckks_params* p, size_t* tb, size_t* kb, size_t* wb,
 {
     if (!p || !p->prime_bits) throw CkksError(CKKS_E_PARAM, "null params");
     if (p->log_n < 10 || p->log_n > 14) throw CkksError(CKKS_E_PARAM, "log_n must be in [10, 14]");
-    if (p->n_data < 1 || p->n_special > 1 || p->n_data + p->n_special > CKKS_MAXP)
-        throw CkksError(CKKS_E_PARAM, "need 1 <= n_data, n_special <= 1, n_data + n_special <= 16");
+    if (p->n_data < 1 || p->n_special > 2 || p->n_data + p->n_special > CKKS_MAXP)
+        throw CkksError(CKKS_E_PARAM, "need 1 <= n_data, n_special <= 2, n_data + n_special <= 16");
     if (p->n_special == 0 && (p->n_rot_steps || p->want_relin))
         throw CkksError(CKKS_E_PARAM, "key switching needs a special prime");
     if (p->max_batch < 1) throw CkksError(CKKS_E_PARAM, "max_batch >= 1");
-    const int n = 1 << p->log_n, L = (int)p->n_data, np = L + (int)p->n_special;
+    const int n = 1 << p->log_n, L = (int)p->n_data, K = (int)p->n_special, np = L + K;
     std::vector<u32> bits(p->prime_bits, p->prime_bits + np);
     auto primes = prime_chain((int)p->log_n, bits);
     if (primes_out) *primes_out = primes;
+    // digits (R9b): 1 or 2 consecutive data primes each
+    int nd = L;
+    if (p->digit_sizes) {
+        uint32_t sum = 0;
+        for (uint32_t j = 0; j < p->n_digits; ++j) {
+            if (p->digit_sizes[j] < 1 || p->digit_sizes[j] > 2)
+                throw CkksError(CKKS_E_PARAM, "digit sizes must be 1 or 2 primes");
+            sum += p->digit_sizes[j];
+        }
+        if (sum != p->n_data || p->n_digits == 0) throw CkksError(CKKS_E_PARAM, "digit sizes must sum to n_data");
+        nd = (int)p->n_digits;
+    }
     // number of distinct switching keys
     std::vector<int64_t> ids;
     if (p->want_relin) ids.push_back(0);
@@ -532,15 +557,15 @@ static void sizes_impl(const ckks_params* p, size_t* tb, size_t* kb, size_t* wb,
         const int64_t g = (int64_t)h_pow(5, (u64)r, 2ULL * n);
         if (g != 1 && std::find(ids.begin(), ids.end(), g) == ids.end()) ids.push_back(g);
     }
-    const size_t key_words = p->n_special ? (size_t)L * 2 * (L + 1) * n : 0;
+    const size_t key_words = p->n_special ? (size_t)nd * 2 * np * n : 0;
     *tb = align256(sizeof(DCtx)) + align256((size_t)np * 8 * n * 8);
     // every switching key, plus a sigma_{g^-1}-permuted copy per key slot (used by hoisted rotations)
     *kb = align256((size_t)np * n * 8) + align256((size_t)2 * L * n * 8) + 2 * ids.size() * key_words * 8;
     const int B = (int)p->max_batch;
-    size_t w = std::max(enc_work_words(L, n, B), p->n_special ? ks_work_words(L, n, B) : (size_t)0);
+    size_t w = std::max(enc_work_words(L, n, B), p->n_special ? ks_work_words(L, K, nd, n, B) : (size_t)0);
     w = std::max(w, (size_t)3 * B * n);   // rescale remainders (rescale_impl)
-    // keygen scratch: e_ntt [L][L+1][N] + s' [np][N]
-    w = std::max(w, (size_t)L * (L + 1) * n + (size_t)np * n);
+    // keygen scratch: e_ntt [dnum][L+K][N] + s' [np][N]
+    w = std::max(w, (size_t)nd * np * n + (size_t)np * n);
     *wb = align256(w * 8);
 }
 
@@ -575,6 +600,17 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
         c->bsgs_bx = p->bsgs_baby_extra;
         c->primes = primes;
         for (u64 q : primes) c->pclass.push_back(prime_class(q));
+        {
+            int st = 0;
+            const int nd = p->digit_sizes ? (int)p->n_digits : (int)p->n_data;
+            for (int j = 0; j < nd; ++j) {
+                const int len = p->digit_sizes ? (int)p->digit_sizes[j] : 1;
+                c->dig_start.push_back(st);
+                c->dig_len.push_back(len);
+                st += len;
+            }
+            c->nd = nd;
+        }
         const int n = c->n, np = c->np, L = c->L;
         // ---- constants
         DCtx& h = c->host_dc;
@@ -640,6 +676,39 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
                 }
             }
         }
+        // key switching constants (R9b, R10b, R17b): digit table, 2-prime CRT inverses, P = prod P_k
+        h.n_digits = c->nd;
+        for (int j = 0; j < c->nd; ++j) {
+            h.dig_start[j] = c->dig_start[j];
+            h.dig_len[j] = c->dig_len[j];
+            if (c->dig_len[j] == 2) {
+                const int s1 = c->dig_start[j] + 1;
+                h.dig_inv[s1] = h_pow(primes[s1 - 1] % primes[s1], primes[s1] - 2, primes[s1]);
+                h.dig_inv_sh[s1] = h_shoup(h.dig_inv[s1], primes[s1]);
+            }
+        }
+        if (c->ns == 2) {
+            const int s1 = L + 1;
+            h.dig_inv[s1] = h_pow(primes[L] % primes[s1], primes[s1] - 2, primes[s1]);
+            h.dig_inv_sh[s1] = h_shoup(h.dig_inv[s1], primes[s1]);
+        }
+        if (c->ns) {
+            for (int i = 0; i < np; ++i) {
+                u64 pm = 1 % primes[i];
+                for (int k = 0; k < c->ns; ++k) pm = h_mulmod(pm, primes[L + k] % primes[i], primes[i]);
+                h.pmod[i] = i < L ? pm : 0;
+                h.pmod_sh[i] = h_shoup(h.pmod[i], primes[i]);
+                if (i < L) {
+                    h.pinv[i] = h_pow(pm, primes[i] - 2, primes[i]);
+                    h.pinv_sh[i] = h_shoup(h.pinv[i], primes[i]);
+                }
+            }
+            u128 P = 1;
+            for (int k = 0; k < c->ns; ++k) P *= primes[L + k];
+            const u128 half = (P - 1) / 2;
+            h.phalf_lo = (u64)half;
+            h.phalf_hi = (u64)(half >> 64);
+        }
         // R13 CDT, same definition as DESIGN.md (computed here independently)
         {
             const int B = (int)std::floor(6.0 * c->sigma);
@@ -669,7 +738,7 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
         c->d_s = (u64*)kbase;
         c->d_pk = (u64*)(kbase + align256((size_t)np * n * 8));
         c->d_keys = (u64*)(kbase + align256((size_t)np * n * 8) + align256((size_t)2 * L * n * 8));
-        c->key_words = c->ns ? (size_t)L * 2 * (L + 1) * n : 0;
+        c->key_words = c->ns ? (size_t)c->nd * 2 * np * n : 0;
         c->d_work = (u64*)d_work;
         c->work_bytes = wb;
         if (p->want_relin) c->key_ids.push_back(0);
@@ -689,21 +758,22 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
         ck::sample_ntt(Lc, scratch, 1, L, L, 1, seed, 3, 0, 0, 0, 0);                 // pk e (TAG 3)
         ck::pk_combine(Lc, c->d_pk, scratch, c->d_s, L);
         if (c->ns) {
-            u64* e_ntt = scratch;                               // [L][L+1][N]
-            u64* sp = scratch + (size_t)L * (L + 1) * n;        // [np][N]
+            const int nd = c->nd;
+            u64* e_ntt = scratch;                               // [dnum][L+K][N]
+            u64* sp = scratch + (size_t)nd * np * n;            // [np][N]
             for (size_t ki = 0; ki < c->key_ids.size(); ++ki) {
                 const int64_t id = c->key_ids[ki];
                 u64* key = c->d_keys + ki * c->key_words;
                 if (id == 0) ck::square_ntt(Lc, c->d_s, sp, np);
                 else ck::galois_ntt(Lc, c->d_s, sp, np, (uint32_t)id);
-                for (int j = 0; j < L; ++j)
-                    for (int pi = 0; pi <= L; ++pi)
-                        ck::sample_uniform(Lc, key + (((size_t)j * 2 + 1) * (L + 1) + pi) * n, pi, seed, 4, (u64)id,
+                for (int j = 0; j < nd; ++j)
+                    for (int pi = 0; pi < np; ++pi)
+                        ck::sample_uniform(Lc, key + (((size_t)j * 2 + 1) * np + pi) * n, pi, seed, 4, (u64)id,
                                            (u64)j);
-                ck::sample_ntt(Lc, e_ntt, L, L + 1, L, 1, seed, 5, (u64)id, 0, 0, 1);   // e_j (TAG 5)
+                ck::sample_ntt(Lc, e_ntt, nd, np, L, 1, seed, 5, (u64)id, 0, 0, 1);   // e_j (TAG 5)
                 ck::keyswitch_key_combine(Lc, key, e_ntt, c->d_s, sp, L);
                 if (id != 0)   // key'_j = sigma_{g^-1}(gk_j): sum_j sigma_g(D_j) gk_j = sigma_g(sum_j D_j key'_j)
-                    ck::galois_limbs(Lc, key, c->d_keys_perm + ki * c->key_words, (size_t)L * 2 * (L + 1),
+                    ck::galois_limbs(Lc, key, c->d_keys_perm + ki * c->key_words, (size_t)nd * 2 * np,
                                      c->galois_inv((uint32_t)id));
             }
         }
@@ -823,6 +893,8 @@ ckks_status ckks_ctx_info(const ckks_ctx* c, ckks_info* o)
         o->primes[i] = c->primes[i];
         o->psi[i] = c->psi[i];
     }
+    o->n_digits = (uint32_t)c->nd;
+    for (int j = 0; j < c->nd; ++j) o->digit_sizes[j] = (uint32_t)c->dig_len[j];
     return CKKS_OK;
 }
 
@@ -1010,7 +1082,7 @@ ckks_status ckks_layer_sizes(const ckks_ctx* c, uint32_t rows, uint32_t cols, ui
 
 static size_t layer_dev_bytes(const ckks_ctx* c, size_t count, uint32_t level)
 {
-    return align256(count * (level + 2) * c->n * 8) + align256((size_t)level * c->n * 8) +
+    return align256(count * (level + 1 + c->ns) * c->n * 8) + align256((size_t)level * c->n * 8) +
            align256((count > 1 ? count : 1) * c->n * 8);   // + staging for the int64 coefficients
 }
 
@@ -1039,8 +1111,9 @@ static ckks_status layer_general(ckks_ctx* c, const ckks_layer_desc* d, const in
     const uint32_t level = d->level;
     char* base = (char*)dev_buf;
     ly->d_pts = (u64*)base;
-    ly->d_bias = bias ? (u64*)(base + align256(count * (level + 2) * c->n * 8)) : nullptr;
-    int64_t* stage = (int64_t*)(base + align256(count * (level + 2) * c->n * 8) + align256((size_t)level * c->n * 8));
+    ly->d_bias = bias ? (u64*)(base + align256(count * (level + 1 + c->ns) * c->n * 8)) : nullptr;
+    int64_t* stage =
+        (int64_t*)(base + align256(count * (level + 1 + c->ns) * c->n * 8) + align256((size_t)level * c->n * 8));
     cudaStream_t st = (cudaStream_t)stream;
     auto L = c->launch(stream);
     cuda_ok(cudaMemcpyAsync(stage, pts, count * c->n * 8, cudaMemcpyHostToDevice, st), "upload plaintexts");
@@ -1222,7 +1295,7 @@ void ckks_layer_destroy(ckks_layer* l) { delete l; }
 // Q_l ciphertext for the double-hoisted ModDown output
 static size_t layer_work_words(const ckks_ctx* c, const ckks_layer* l, int B)
 {
-    const size_t ctq = c->ct_words((int)l->level + 2);
+    const size_t ctq = c->ct_words((int)l->level + 1 + std::max(c->ns, 1));
     return ((size_t)(l->t1 - 1) + l->t2 + 1) * B * ctq;
 }
 
@@ -1288,7 +1361,7 @@ static void matvec_chunk(ckks_ctx* c, const ckks_layer* ly, const u64* in, size_
     const int nl = (int)ly->level + 1;
     auto L = c->launch(stream);
     if (hoisting == 2) {
-        const size_t ctq = c->ct_words(nl + 1), ctw = c->ct_words(nl);
+        const size_t ctq = c->ct_words(nl + c->ns), ctw = c->ct_words(nl);
         u64* baby = work;                                   // [t1-1][B][2][nl+1][N]
         u64* Wk = work + (size_t)(ly->t1 - 1) * B * ctq;    // [t2][B][2][nl+1][N]
         u64* md = Wk + (size_t)ly->t2 * B * ctq;            // [B][2][nl][N]
@@ -1300,7 +1373,7 @@ static void matvec_chunk(ckks_ctx* c, const ckks_layer* ly, const u64* in, size_
         }
         if (!steps.empty())
             rotate_hoisted_qp_impl(c, in, in_stride, nl, B, steps.data(), (int)steps.size(), outs.data(), ctq, stream);
-        ck::bsgs_mac(L, ly->d_pts, nl + 1, in, in_stride, baby, Wk, (int)ly->t1, (int)ly->t2, B, nl, true);
+        ck::bsgs_mac(L, ly->d_pts, nl + c->ns, in, in_stride, baby, Wk, (int)ly->t1, (int)ly->t2, B, nl, true);
         for (uint32_t k = 1; k < ly->t2; ++k)
             rotate_qp_impl(c, Wk + (size_t)k * B * ctq, ctq, nl, B, (int64_t)k * ly->giant, Wk, ctq, stream);
         ck::moddown_qp(L, Wk, ctq, B, nl, c->ks_work(B), md, ctw);
@@ -1324,7 +1397,7 @@ static void matvec_chunk(ckks_ctx* c, const ckks_layer* ly, const u64* in, size_
             rotate_impl(c, in, in_stride, nl, B, (int64_t)ly->baby[j], baby + (size_t)(j - 1) * B * ctw, ctw, false,
                         stream);
     }
-    ck::bsgs_mac(L, ly->d_pts, nl + 1, in, in_stride, baby, Wk, (int)ly->t1, (int)ly->t2, B, nl, false);
+    ck::bsgs_mac(L, ly->d_pts, nl + c->ns, in, in_stride, baby, Wk, (int)ly->t1, (int)ly->t2, B, nl, false);
     for (uint32_t k = 1; k < ly->t2; ++k)
         rotate_impl(c, Wk + (size_t)k * B * ctw, ctw, nl, B, (int64_t)k * ly->giant, Wk, ctw, true, stream);
     rescale_impl(c, Wk, ctw, 2, nl, B, out, out_stride, ly->d_bias, stream);

@@ -32,6 +32,15 @@ struct DCtx {
     const u64* tw;                      // [n_primes][4][N]: W, W', IW, IW'  (bit-reversed psi powers)
     u64 cdt[40];                        // discrete Gaussian CDT thresholds (R13)
     int cdt_bound;
+    // key switching (R9b, R10b, R17b): dnum digits of 1 or 2 consecutive data primes; P = the product of
+    // the n_special (1 or 2) special primes
+    int n_digits;
+    int dig_start[CKKS_MAXP], dig_len[CKKS_MAXP];
+    u64 dig_inv[CKKS_MAXP], dig_inv_sh[CKKS_MAXP];   // [p]: q_{p-1}^{-1} mod q_p when p is the 2nd prime of
+                                                     // a 2-prime group (a digit, or P_1 of P = P_0 P_1)
+    u64 pmod[CKKS_MAXP], pmod_sh[CKKS_MAXP];         // P mod q_p (0 for the special primes)
+    u64 pinv[CKKS_MAXP], pinv_sh[CKKS_MAXP];         // P^{-1} mod q_i (data primes)
+    u64 phalf_lo, phalf_hi;                          // (P - 1) / 2 as a 128-bit integer
 };
 
 __device__ __forceinline__ u64 csub(u64 a, u64 m) { return a >= m ? a - m : a; }
@@ -116,3 +125,36 @@ __device__ __forceinline__ u64 centered_to(u64 r, u64 m, u64 m_mod_b, const DPri
 }
 
 __device__ __forceinline__ u32 brev32(u32 x, int bits) { return __brev(x) >> (32 - bits); }
+
+// ---- 2-prime CRT groups (hybrid key switching, R9b / R10b).  A group {q_s, q_{s+1}} holds an integer
+// x in [0, q_s q_{s+1}) as (a, t): a = x mod q_s, t = (x - a) / q_s = (x mod q_{s+1} - a) q_s^{-1} mod q_{s+1}
+// (Garner), so x = a + q_s t exactly.
+// t from a (< q_s) and b = x mod q_{s+1} (< q_{s+1}); canonical [0, q_{s+1})
+__device__ __forceinline__ u64 crt2_t(const DCtx* __restrict__ dc, int s, u64 a, u64 b)
+{
+    const DPrime& B = dc->p[s + 1];
+    const u64 am = reduce64(a, B);
+    return csub(shoup_mul(submod(b, am, B.q), dc->dig_inv[s + 1], dc->dig_inv_sh[s + 1], B.q), B.q);
+}
+// x mod q_pb for x = a + q_s t, in [0, 2 q_pb)
+__device__ __forceinline__ u64 crt2_lazy(const DCtx* __restrict__ dc, int s, u64 a, u64 t, const DPrime& B, int pb)
+{
+    const u64 u = shoup_mul(t, dc->qmod[s][pb], dc->qmod_sh[s][pb], B.q);   // [0, 2q)
+    const u64 v = reduce64_lazy(a, B);                                     // [0, 2q)
+    return csub(u + v, B.q2);
+}
+// centred special remainder r (R10 / R10b) reduced mod data prime pb, canonical [0, q_pb):
+//   K = 1: r = rem0 in [0, P);  K = 2: r = rem0 + P_0 rem1 in [0, P_0 P_1) (CRT pair); r > (P-1)/2 -> r - P
+__device__ __forceinline__ u64 special_centered(const DCtx* __restrict__ dc, u64 rem0, u64 rem1, const DPrime& B, int pb)
+{
+    const int L = dc->n_data;
+    if (dc->n_special == 1) return centered_to(rem0, dc->p[L].q, dc->pmod[pb], B);
+    const u64 P0 = dc->p[L].q;
+    const u64 lo0 = P0 * rem1, hi0 = __umul64hi(P0, rem1);
+    const u64 lo = lo0 + rem0, hi = hi0 + (lo < lo0 ? 1 : 0);
+    const bool neg = hi > dc->phalf_hi || (hi == dc->phalf_hi && lo > dc->phalf_lo);
+    const u64 v = csub(crt2_lazy(dc, L, rem0, rem1, B, pb), B.q);
+    return neg ? submod(v, dc->pmod[pb], B.q) : v;
+}
+// prime index of row e of a Q_l P polynomial with nl data rows: q_e, then the special primes
+__host__ __device__ __forceinline__ int ext_prime_of(int e, int nl, int L) { return e < nl ? e : L + (e - nl); }

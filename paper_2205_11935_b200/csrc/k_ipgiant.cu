@@ -1,14 +1,14 @@
 // k_ipgiant.cu -- sm_100a kernel of the CKKS encrypted-dense-layer hot path: the giant-step
 // key-switch inner product of double hoisting (R11c) in the Q_l P basis, accumulated.
 // Layouts:
-//   ModUp output  [b][digit j][row 0..nl][N]   (all_e: every row, row nl = special prime P)
-//   key           [digit j][comp][prime 0..L][N]
-//   accumulator   [b][comp][row 0..nl][N]   (Q_l P), addend w [b][comp][row][N] (Q_l P)
+//   ModUp output  [b][digit j][row 0..nl+K-1][N]   (all_e: every row, rows nl.. = special primes)
+//   key           [digit j][comp][prime 0..L+K-1][N]
+//   accumulator   [b][comp][row 0..nl+K-1][N]   (Q_l P), addend w [b][comp][row][N] (Q_l P)
 #include "kinternal.cuh"
 
 namespace ck {
 
-// Giant step (R11c):  acc[b][c][i][k] += sum_{j<nl} D_{b,j}[i][k] key_{j,c}[i][k] + [c = 0] sigma_g(w.c0)[i][k].
+// Giant step (R11c):  acc[b][c][i][k] += sum_{j<nd} D_{b,j}[i][k] key_{j,c}[i][k] + [c = 0] sigma_g(w.c0)[i][k].
 // Key-stationary form: one thread per (row i, coefficient k) keeps its 2 nl key words in registers
 // (split once into 21-bit halves for q < 2^42 rows) and walks the whole batch, so every key word is read
 // once per launch (the per-ciphertext-pair CTAs of k_ks_ip_qp re-read the group key B/2 times from L2)
@@ -26,37 +26,34 @@ constexpr int kIpgUnroll = IPG_UNROLL;   // ciphertexts per unrolled batch step
 
 template <int NL, bool SPLIT>
 __device__ __forceinline__ void ipg_row(const DCtx* __restrict__ dc, const u64* __restrict__ modup,
-                                        const u64* __restrict__ key, int L, int special, u64* __restrict__ acc,
+                                        const u64* __restrict__ key, int nl, u64* __restrict__ acc,
                                         size_t acc_stride, const u64* __restrict__ add, size_t add_stride,
                                         u32 add_galois, int B)
 {
-    constexpr int nl = NL;
-    const int n = dc->n, logn = dc->log_n;
+    // NL = digits (the contraction length); rows i of Q_l P: q_0..q_{nl-1}, then the special primes
+    const int n = dc->n, logn = dc->log_n, ne = nl + dc->n_special, np = dc->n_data + dc->n_special;
     const int i = blockIdx.y, k = blockIdx.x * IPG_BLK + threadIdx.x;
-    const bool prow = (i == nl);
-    const int p = prow ? special : i;
-    const int krow = prow ? L : i;
+    const int p = ext_prime_of(i, nl, dc->n_data);
+    const int krow = p;
     const DPrime Pr = dc->p[p];
-    const size_t kstride = (size_t)(L + 1) * n;
     u64 kw[2][NL];
 #pragma unroll
     for (int j = 0; j < NL; ++j) {
-        kw[0][j] = key[((size_t)(2 * j) * (L + 1) + krow) * n + k];
-        kw[1][j] = key[((size_t)(2 * j + 1) * (L + 1) + krow) * n + k];
+        kw[0][j] = key[((size_t)(2 * j) * np + krow) * n + k];
+        kw[1][j] = key[((size_t)(2 * j + 1) * np + krow) * n + k];
     }
-    (void)kstride;
     const int src = add_galois ? galois_src(k, add_galois, logn) : k;
-    const size_t dstride = (size_t)(nl + 1) * n;
+    const size_t dstride = (size_t)ne * n;
     const u64* dbase = modup + (size_t)i * n + k;
 #pragma unroll kIpgUnroll
     for (int b = 0; b < B; ++b) {
-        const u64* d = dbase + (size_t)b * nl * dstride;
+        const u64* d = dbase + (size_t)b * NL * dstride;
         u64 dv[NL];
 #pragma unroll
         for (int j = 0; j < NL; ++j) dv[j] = d[(size_t)j * dstride];
         u64* o = acc + (size_t)b * acc_stride + (size_t)i * n + k;
         const u64 a0 = add[(size_t)b * add_stride + (size_t)i * n + src];
-        const u64 o0 = o[0], o1 = o[(size_t)(nl + 1) * n];
+        const u64 o0 = o[0], o1 = o[dstride];
         u64 u0, u1;
         if constexpr (SPLIT) {
             u64 s00[2] = {0, 0}, s01[2] = {0, 0}, s11[2] = {0, 0};
@@ -97,22 +94,22 @@ __device__ __forceinline__ void ipg_row(const DCtx* __restrict__ dc, const u64* 
             u1 = a[1].reduce(Pr);
         }
         o[0] = addmod(addmod(u0, a0, Pr.q), o0, Pr.q);
-        o[(size_t)(nl + 1) * n] = addmod(u1, o1, Pr.q);
+        o[dstride] = addmod(u1, o1, Pr.q);
     }
 }
 
 template <int NL>
 __global__ void __launch_bounds__(IPG_BLK, IPG_MINB)
-k_ks_ip_giant(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ key, int L,
-              int special, u64* __restrict__ acc, size_t acc_stride, const u64* __restrict__ add, size_t add_stride,
+k_ks_ip_giant(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ key, int nl,
+              u64* __restrict__ acc, size_t acc_stride, const u64* __restrict__ add, size_t add_stride,
               u32 add_galois, int B)
 {
     const int i = blockIdx.y;
-    const u64 q = dc->p[i == NL ? special : i].q;
+    const u64 q = dc->p[ext_prime_of(i, nl, dc->n_data)].q;
     if (q < SPLIT21_MAXQ)
-        ipg_row<NL, true>(dc, modup, key, L, special, acc, acc_stride, add, add_stride, add_galois, B);
+        ipg_row<NL, true>(dc, modup, key, nl, acc, acc_stride, add, add_stride, add_galois, B);
     else
-        ipg_row<NL, false>(dc, modup, key, L, special, acc, acc_stride, add, add_stride, add_galois, B);
+        ipg_row<NL, false>(dc, modup, key, nl, acc, acc_stride, add, add_stride, add_galois, B);
 }
 
 void ip_giant(const Launch& L, const uint64_t* key, int batch, int nl, const KsWork& w, uint64_t* acc,
@@ -120,17 +117,17 @@ void ip_giant(const Launch& L, const uint64_t* key, int batch, int nl, const KsW
 {
     const int n = 1 << L.log_n;
     if (n % IPG_BLK) throw std::runtime_error("N >= 128 required");
-    const dim3 grid(n / IPG_BLK, nl + 1);
+    const dim3 grid(n / IPG_BLK, nl + L.n_special);
 #define IPG_CASE(V)                                                                                                  \
     case V: {                                                                                                         \
         ProbeScope ps_(L.probe, L.st, "k_ks_ip_giant");                                                               \
-        k_ks_ip_giant<V><<<grid, IPG_BLK, 0, L.st>>>(L.dc, w.modup, key, L.n_data, L.n_data, acc, acc_stride, add,    \
-                                                     add_stride, add_galois, batch);                                  \
+        k_ks_ip_giant<V><<<grid, IPG_BLK, 0, L.st>>>(L.dc, w.modup, key, nl, acc, acc_stride, add, add_stride,        \
+                                                     add_galois, batch);                                              \
     } break;
-    switch (nl) {
+    switch (L.active_digits(nl)) {
         IPG_CASE(1) IPG_CASE(2) IPG_CASE(3) IPG_CASE(4) IPG_CASE(5) IPG_CASE(6) IPG_CASE(7) IPG_CASE(8)
         IPG_CASE(9) IPG_CASE(10) IPG_CASE(11) IPG_CASE(12) IPG_CASE(13) IPG_CASE(14) IPG_CASE(15) IPG_CASE(16)
-    default: throw std::runtime_error("nl > 16");
+    default: throw std::runtime_error("more than 16 digits");
     }
 #undef IPG_CASE
     check_launch("ip_giant");

@@ -1,15 +1,15 @@
 // k_ipmma.cu -- sm_100a kernel of the CKKS encrypted-dense-layer hot path: the hoisted baby-step
 // key-switch inner product in the Q_l P basis (double hoisting, R11c) on the FP64 tensor
 // cores.  Layouts:
-//   ModUp output  [b][digit j][row 0..nl][N]   (row nl = special prime P)
-//   key           [digit j][comp][prime 0..L][N]  (pre-permuted by sigma_g^{-1})
-//   baby output   [b][comp][row 0..nl][N]   (Q_l P basis, sigma_g-permuted)
+//   ModUp output  [b][digit j][row 0..nl+K-1][N]   (rows nl..: the special primes P_0..P_{K-1})
+//   key           [digit j][comp][prime 0..L+K-1][N]  (pre-permuted by sigma_g^{-1})
+//   baby output   [b][comp][row 0..nl+K-1][N]   (Q_l P basis, sigma_g-permuted)
 #include "kinternal.cuh"
 
 namespace ck {
 
 // For one row i (prime) and one coefficient k the group's inner products are a small matrix product
-//     U[b][(g, c)] = sum_{j < nl} D_{b,j}[k] key_{g,j,c}[k]     (16 ciphertexts x 2G columns x K = nl)
+//     U[b][(g, c)] = sum_{j < nd} D_{b,j}[k] key_{g,j,c}[k]     (16 ciphertexts x 2G columns x K = nd digits)
 // computed EXACTLY with mma.sync m16n8k4 f64 on split operands: q < 2^45 two 23-bit parts and
 // Karatsuba (3 products, every sum < 2^53 for nl <= 16), 60-bit primes three 20-bit parts and 6
 // products.  The split sums are recombined mod q per output, the addend P c0 is added, and the
@@ -49,7 +49,7 @@ template <int N>
 __device__ __forceinline__ void ip2_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
 template <int NL>
-struct Ip2Shape {
+struct Ip2Shape {                                          // NL = digits (the contraction length)
     static constexpr int NLP = (NL + 3) & ~3;              // K padded to the MMA k-step
     static constexpr int JS = IP2_KT * 16 + 4;             // j stride (words) of the swizzled tiles
     static constexpr int SD = NLP * JS + IP2_KT * 16;      // words per stage: D tile + c0 addend
@@ -59,10 +59,9 @@ struct Ip2Shape {
 template <int NL, bool INT>
 __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64* __restrict__ modup,
                                          const u64* __restrict__ in, size_t ct_stride, size_t comp_off,
-                                         const KsGroup& grp, int L, int special, size_t out_stride, int B, u64* sm,
+                                         const KsGroup& grp, int nl, size_t out_stride, int B, u64* sm,
                                          int i, int cblk)
 {
-    constexpr int nl = NL;
     constexpr int NLP = Ip2Shape<NL>::NLP, JS = Ip2Shape<NL>::JS, SD = Ip2Shape<NL>::SD;
     constexpr int KPW = IP2_KT / (IP2_THREADS / 32);       // coefficients per warp
     constexpr bool CACHE = !INT && NLP <= 8 && !IP2_FP_BATCH;   // FP class: split key fragments in registers
@@ -70,27 +69,30 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
     u64* Dst = Ks + NLP * JS;                              // [ST][ D [NLP][KT][16 b] | c0 [KT][16 b] ]
     u64* Os = Dst + IP2_ST * SD;                           // [8 g][2 c][16 b][KT]
     u64** Ob = reinterpret_cast<u64**>(Os + 8 * 2 * 16 * IP2_KT);   // [8 g] destination block of rotation g
-    const int n = dc->n, logn = dc->log_n;
+    const int n = dc->n, logn = dc->log_n, K = dc->n_special, ne = nl + K, np = dc->n_data + K;
     const int k0 = cblk * IP2_KT;
-    const bool prow = (i == nl);
-    const int p = prow ? special : i;
-    const int krow = prow ? L : i;
+    const bool prow = (i >= nl);                           // a special-prime row
+    const int p = ext_prime_of(i, nl, dc->n_data);
+    const int krow = p;
     const DPrime Pr = dc->p[p];
+    int ownj = -1;                                         // the digit whose primes include q_i (D = input limb)
+    for (int j = 0; j < NL; ++j)
+        if (!prow && i >= dc->dig_start[j] && i < dc->dig_start[j] + dc->dig_len[j]) ownj = j;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gid = lane >> 2, tig = lane & 3;
     const int G = grp.G;
     const int nbt = (B + 15) / 16;
-    // ---- stage fill: thread = (coefficient fk, ciphertext row fr); digits j stride (nl+1) N
+    // ---- stage fill: thread = (coefficient fk, ciphertext row fr); digits j stride (nl+K) N
     const int fk = tid % IP2_KT, fr = tid / IP2_KT;
     auto fill = [&](int bt) {
         u64* S = Dst + (bt % IP2_ST) * SD;
         const int b = bt * 16 + fr;
         if (b < B) {
-            const u64* dsrc = modup + (((size_t)b * nl) * (nl + 1) + i) * n + k0 + fk;
+            const u64* dsrc = modup + (((size_t)b * NL) * ne + i) * n + k0 + fk;
             const u64* isrc = in + (size_t)b * ct_stride + (size_t)i * n + k0 + fk;
 #pragma unroll
             for (int j = 0; j < NL; ++j)
-                ip2_cp8(S + j * JS + fk * 16 + (fr ^ fk), (j == i) ? isrc + comp_off : dsrc + (size_t)j * (nl + 1) * n);
+                ip2_cp8(S + j * JS + fk * 16 + (fr ^ fk), (j == ownj) ? isrc + comp_off : dsrc + (size_t)j * ne * n);
             if (!prow) ip2_cp8(S + NLP * JS + fk * 16 + fr, isrc);
             else S[NLP * JS + fk * 16 + fr] = 0;
         } else {
@@ -106,7 +108,7 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
         const int j = e / (IP2_KT * 16), rem = e % (IP2_KT * 16), kk = rem % IP2_KT, r = rem / IP2_KT;
         const int g = r >> 1, c = r & 1;
         u64* dst = Ks + j * JS + kk * 16 + (r ^ kk);
-        if (j < NL && g < G) ip2_cp8(dst, grp.key[g] + ((size_t)j * 2 * (L + 1) + (size_t)c * (L + 1) + krow) * n + k0 + kk);
+        if (j < NL && g < G) ip2_cp8(dst, grp.key[g] + ((size_t)j * 2 * np + (size_t)c * np + krow) * n + k0 + kk);
         else *dst = 0;
     }
     ip2_commit();
@@ -124,7 +126,7 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
         spk |= (u32)sidx << (4 * g);
         if (tid == 0) Ob[g] = grp.out[g] + (size_t)i * n + (size_t)dblk * IP2_KT;
     }
-    const size_t wlimb = (size_t)(nl + 1) * n;             // component stride of an output ciphertext
+    const size_t wlimb = (size_t)ne * n;                   // component stride of an output ciphertext
 #pragma unroll
     for (int s = 0; s < IP2_ST - 1; ++s) {
         if (s < nbt) fill(s);
@@ -135,7 +137,7 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
     const double q = (double)Pr.q, qinv = 1.0 / q;
     const double two46 = 70368744177664.0;
     const double w46 = two46 - floor(two46 * qinv) * q, w46q = w46 / q, c23q = 8388608.0 / q;
-    const u64 Pm = prow ? 0 : dc->qmod[special][i], Pm_sh = prow ? 0 : dc->qmod_sh[special][i];
+    const u64 Pm = prow ? 0 : dc->pmod[i], Pm_sh = prow ? 0 : dc->pmod_sh[i];
     const u64 m23 = (1ULL << 23) - 1;
     // 60-bit rows on IMAD: this thread's 2g + c key column of coefficient ik, in registers
     const int ik = tid % IP2_KT, in_ = tid / IP2_KT;
@@ -360,36 +362,36 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
 template <int NL>
 __global__ void __launch_bounds__(IP2_THREADS, 2)
 k_ks_ip_mma2(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ in, size_t ct_stride,
-             size_t comp_off, const KsGroup grp, int L, int special, size_t out_stride, int B)
+             size_t comp_off, const KsGroup grp, int nl, size_t out_stride, int B)
 {
     extern __shared__ u64 sm[];
     // (tried: rows fastest, so CTAs of both classes share an SM at the same time -- 150 vs 147.5 ms per step)
     const int i = blockIdx.y, cblk = blockIdx.x;
-    const u64 q = dc->p[i == NL ? special : i].q;
+    const u64 q = dc->p[ext_prime_of(i, nl, dc->n_data)].q;
     if (prime_class(q) == PC_FP)
-        ip2_body<NL, false>(dc, modup, in, ct_stride, comp_off, grp, L, special, out_stride, B, sm, i, cblk);
-    else ip2_body<NL, true>(dc, modup, in, ct_stride, comp_off, grp, L, special, out_stride, B, sm, i, cblk);
+        ip2_body<NL, false>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm, i, cblk);
+    else ip2_body<NL, true>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm, i, cblk);
 }
 
 // host launcher: both prime classes of a baby-step group (scatter outputs, addend P c0, no accumulation)
 void ip_mma_pipelined(const Launch& L, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
                       size_t out_stride)
 {
-    const int n = 1 << L.log_n;
-    const dim3 grid(n / IP2_KT, nl + 1);
+    const int n = 1 << L.log_n, ne = nl + L.n_special, nd = L.active_digits(nl);
+    const dim3 grid(n / IP2_KT, ne);
     if (L.probe && L.probe->kind == PROBE_ALL) {
         // exact split products per modular MAC: 3 (FP class rows), 6 (60-bit rows); MACs per row:
-        // B x G x 2 components x nl digits x N.  Bytes: ModUp words and input limbs read, c0 addend,
+        // B x G x 2 components x nd digits x N.  Bytes: ModUp words and input limbs read, c0 addend,
         // the group's keys, the G rotated outputs written.
         double fl = 0;
-        for (int i = 0; i <= nl; ++i) {
-            const int p = i == nl ? L.n_data : i;
-            fl += 2.0 * ((L.pclass && L.pclass[p] == PC_FP) ? 3 : 6) * batch * grp.G * 2.0 * nl * n;
+        for (int i = 0; i < ne; ++i) {
+            const int p = ext_prime_of(i, nl, L.n_data);
+            fl += 2.0 * ((L.pclass && L.pclass[p] == PC_FP) ? 3 : 6) * batch * grp.G * 2.0 * nd * n;
         }
         L.probe->flops_by_kernel["k_ks_ip_mma"] += fl;
         L.probe->bytes_by_kernel["k_ks_ip_mma"] +=
-            ((double)batch * nl * (nl + 1) + (double)batch * nl + (double)grp.G * nl * 2 * (nl + 1) +
-             (double)grp.G * batch * 2 * (nl + 1)) * n * 8.0;
+            ((double)batch * nd * ne + (double)batch * nl + (double)grp.G * nd * 2 * ne + (double)grp.G * batch * 2 * ne) *
+            n * 8.0;
     }
 #define IP2_CASE(V)                                                                                                  \
     case V: {                                                                                                         \
@@ -397,12 +399,12 @@ void ip_mma_pipelined(const Launch& L, const KsIn& in, const KsGroup& grp, int b
         allow_smem(k_ks_ip_mma2<V>, smem);                                                                            \
         ProbeScope ps_(L.probe, L.st, "k_ks_ip_mma");                                                                 \
         k_ks_ip_mma2<V><<<grid, IP2_THREADS, smem, L.st>>>(L.dc, w.modup, in.base, in.ct_stride, in.comp_off, grp,   \
-                                                         L.n_data, L.n_data, out_stride, batch);                      \
+                                                         nl, out_stride, batch);                                      \
     } break;
-    switch (nl) {
+    switch (nd) {
         IP2_CASE(1) IP2_CASE(2) IP2_CASE(3) IP2_CASE(4) IP2_CASE(5) IP2_CASE(6) IP2_CASE(7) IP2_CASE(8)
         IP2_CASE(9) IP2_CASE(10) IP2_CASE(11) IP2_CASE(12) IP2_CASE(13) IP2_CASE(14) IP2_CASE(15) IP2_CASE(16)
-    default: throw std::runtime_error("nl > 16");
+    default: throw std::runtime_error("more than 16 digits");
     }
 #undef IP2_CASE
     check_launch("ip_mma_pipelined");

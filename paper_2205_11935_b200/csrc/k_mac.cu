@@ -6,7 +6,7 @@
 // two small modular contractions (key-switch inner product, BSGS inner sums) -- on the FP64 tensor
 // cores with exactly split operands.  Layouts:
 //   ciphertext  [batch][comp][limb][N]  u64, NTT domain, canonical residues in [0, q)
-//   key         [digit j][comp][prime 0..L][N]  (prime L = special P)
+//   key         [digit j][comp][prime 0..L+K-1][N]  (primes L.. = the special primes P_k)
 //   plaintexts  [t][limb][N]
 // This unit: BSGS plaintext-ciphertext MAC (Eq. 1 inner sums).
 #include "kinternal.cuh"
@@ -34,9 +34,9 @@ k_bsgs_mac_fp(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_n
 {
     extern __shared__ double2 A2[];
     const int n = dc->n;
-    const int l = blockIdx.y;                      // limb; QP: limb nl is the special prime
-    const int nlx = nl + qp;
-    const int pidx = l < nl ? l : dc->n_data;
+    const int l = blockIdx.y;                      // limb; QP: limbs nl.. are the special primes
+    const int nlx = nl + (qp ? dc->n_special : 0);
+    const int pidx = ext_prime_of(l, nl, dc->n_data);
     const DPrime Pr = dc->p[pidx];
     if (prime_class(Pr.q) != PC_FP) return;
     const int tx = threadIdx.x % MACF_XT, ty = threadIdx.x / MACF_XT;
@@ -53,7 +53,7 @@ k_bsgs_mac_fp(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_n
     const double w46 = two46 - floor(two46 * qinv) * q;                        // 2^46 mod q (exact)
     const double w46q = w46 / q, w23q = two23 / q;
     const size_t ctw = (size_t)2 * nlx * n;
-    const u64 Pm = qp ? dc->qmod[dc->n_data][l < nl ? l : 0] : 0, Pm_sh = qp ? dc->qmod_sh[dc->n_data][l < nl ? l : 0] : 0;
+    const u64 Pm = qp ? dc->pmod[l < nl ? l : 0] : 0, Pm_sh = qp ? dc->pmod_sh[l < nl ? l : 0] : 0;
     for (int b = ty; b < batch; b += MACF_BL) {
         for (int c = 0; c < 2; ++c) {
             const size_t off = ((size_t)c * nlx + l) * n + x;
@@ -116,8 +116,8 @@ k_bsgs_mac_int(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_
     extern __shared__ u64 Ai[];
     const int n = dc->n;
     const int l = blockIdx.y;
-    const int nlx = nl + qp;
-    const int pidx = l < nl ? l : dc->n_data;
+    const int nlx = nl + (qp ? dc->n_special : 0);
+    const int pidx = ext_prime_of(l, nl, dc->n_data);
     const DPrime Pr = dc->p[pidx];
     if (prime_class(Pr.q) == PC_FP) return;
     const int tx = threadIdx.x % MACF_XT, ty = threadIdx.x / MACF_XT;
@@ -127,7 +127,7 @@ k_bsgs_mac_int(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_
         Ai[i] = pts[((size_t)(i / MACF_XT) * pt_nl + l) * n + x0 + (i % MACF_XT)];
     __syncthreads();
     const size_t ctw = (size_t)2 * nlx * n;
-    const u64 Pm = qp ? dc->qmod[dc->n_data][l < nl ? l : 0] : 0, Pm_sh = qp ? dc->qmod_sh[dc->n_data][l < nl ? l : 0] : 0;
+    const u64 Pm = qp ? dc->pmod[l < nl ? l : 0] : 0, Pm_sh = qp ? dc->pmod_sh[l < nl ? l : 0] : 0;
     for (int b = ty; b < batch; b += MACF_BL) {
         for (int c = 0; c < 2; ++c) {
             const size_t off = ((size_t)c * nlx + l) * n + x;
@@ -213,8 +213,8 @@ __device__ __forceinline__ void macm_body(const DCtx* __restrict__ dc, const u64
     static_assert(MACM_THREADS / MACM_XT == 32 && EPT * 2 == MACM_JC, "fill mapping");
     const int n = dc->n;
     const int l = blockIdx.y;
-    const int nlx = nl + qp;
-    const int pidx = l < nl ? l : dc->n_data;
+    const int nlx = nl + (qp ? dc->n_special : 0);
+    const int pidx = ext_prime_of(l, nl, dc->n_data);
     const DPrime Pr = dc->p[pidx];
     const int x0 = blockIdx.x * MACM_XT, c = blockIdx.z & 1, k0 = (blockIdx.z >> 1) * 8;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -245,7 +245,7 @@ __device__ __forceinline__ void macm_body(const DCtx* __restrict__ dc, const u64
         }
     }
     const size_t ctw = (size_t)2 * nlx * n, jstride = (size_t)batch * ctw;
-    const u64 Pm = qp ? dc->qmod[dc->n_data][l < nl ? l : 0] : 0, Pm_sh = qp ? dc->qmod_sh[dc->n_data][l < nl ? l : 0] : 0;
+    const u64 Pm = qp ? dc->pmod[l < nl ? l : 0] : 0, Pm_sh = qp ? dc->pmod_sh[l < nl ? l : 0] : 0;
     const int nbt = (batch + 15) / 16, njc = t1p / MACM_JC, iters = nbt * njc;
     // fill mapping: thread -> (x, bb, half) copies baby steps jj = half * EPT + h, h < EPT
     const int fx = tid % MACM_XT, fbb = (tid / MACM_XT) % 16, fhalf = tid / (MACM_XT * 16);
@@ -399,7 +399,7 @@ k_bsgs_mac_mma(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_
 {
     extern __shared__ u64 msm[];
     const int l = blockIdx.y;
-    const u64 q = dc->p[l < nl ? l : dc->n_data].q;
+    const u64 q = dc->p[ext_prime_of(l, nl, dc->n_data)].q;
     if (prime_class(q) == PC_FP) macm_body<false>(dc, pts, pt_nl, v0, v0_stride, vb, wout, t1, t2, batch, nl, qp, msm);
     else macm_body<true>(dc, pts, pt_nl, v0, v0_stride, vb, wout, t1, t2, batch, nl, qp, msm);
 }
@@ -413,7 +413,7 @@ static size_t mac_mma_smem(int t1)
 void bsgs_mac(const Launch& L, const uint64_t* pts, int pt_nl, const uint64_t* v0, size_t v0_stride,
               const uint64_t* vbaby, uint64_t* wout, int t1, int t2, int batch, int nl, bool qp)
 {
-    const int nlx = nl + (qp ? 1 : 0);
+    const int nlx = nl + (qp ? L.n_special : 0);
     if (batch <= 0) return;
     const int n = 1 << L.log_n;
     static const int use_mma = [] {
@@ -425,7 +425,7 @@ void bsgs_mac(const Launch& L, const uint64_t* pts, int pt_nl, const uint64_t* v
             // per row: B x 2 components x t1 x t2 x N modular MACs, 3 (FP class) or 6 (60-bit) exact
             // split products each; bytes: baby steps + input read, plaintexts read, W written
             for (int l = 0; l < nlx; ++l) {
-                const int p = l < nl ? l : L.n_data;
+                const int p = ext_prime_of(l, nl, L.n_data);
                 const bool fp = L.pclass && L.pclass[p] == PC_FP;
                 const char* nm = "k_bsgs_mac_mma";
                 L.probe->flops_by_kernel[nm] += 2.0 * (fp ? 3 : 6) * batch * 2.0 * t1 * t2 * n;

@@ -6,7 +6,7 @@
 // two small modular contractions (key-switch inner product, BSGS inner sums) -- on the FP64 tensor
 // cores with exactly split operands.  Layouts:
 //   ciphertext  [batch][comp][limb][N]  u64, NTT domain, canonical residues in [0, q)
-//   key         [digit j][comp][prime 0..L][N]  (prime L = special P)
+//   key         [digit j][comp][prime 0..L+K-1][N]  (primes L.. = the special primes P_k)
 //   plaintexts  [t][limb][N]
 // This unit: batched NTT, rescale, elementwise ops, decrypt, samplers and keygen.
 #include "kinternal.cuh"
@@ -211,7 +211,7 @@ k_signed_to_ntt(const DCtx* __restrict__ dc, const long long* __restrict__ coeff
     extern __shared__ u64 sm[];
     using T = NttCta<LOGN, NttThreads<LOGN>::value>;
     const int l = blockIdx.x, y = blockIdx.y;
-    const int p = l < nl ? l : dc->n_data;   // limb nl (if present): the special prime
+    const int p = ext_prime_of(l, nl, dc->n_data);   // limbs nl..: the special primes
     const DPrime Pr = dc->p[p];
     const long long* src = coeffs + (size_t)y * T::N;
     u64* o = out + ((size_t)y * nlimbs + l) * T::N;
@@ -222,7 +222,7 @@ k_signed_to_ntt(const DCtx* __restrict__ dc, const long long* __restrict__ coeff
 
 void signed_to_ntt(const Launch& L, const int64_t* coeffs, uint64_t* out, int count, int nl, bool with_special)
 {
-    const int nlimbs = nl + (with_special ? 1 : 0);
+    const int nlimbs = nl + (with_special ? L.n_special : 0);
     if (count <= 0) return;
     const size_t smem = sizeof(u64) << L.log_n;
     NTT_DISPATCH(L.log_n, {
@@ -243,7 +243,7 @@ k_sample_ntt(const DCtx* __restrict__ dc, u64* __restrict__ out, int nlimbs, int
     extern __shared__ u64 sm[];
     using T = NttCta<LOGN, NttThreads<LOGN>::value>;
     const int limb = blockIdx.x, y = blockIdx.y;
-    const int p = (limb < nl_data) ? limb : dc->n_data;
+    const int p = ext_prime_of(limb, nl_data, dc->n_data);
     const DPrime Pr = dc->p[p];
     const u64 stream = stream_tag(purpose, id0 + (u64)y * id_step, digit0 + (u64)y * digit_step, 0);
     u64* o = out + ((size_t)y * nlimbs + limb) * T::N;
@@ -286,23 +286,21 @@ void sample_uniform(const Launch& L, uint64_t* out, int prime, uint64_t seed, ui
     if (L.counter) ++*L.counter;
 }
 
-// key[j][1][p] already holds a_j[p]; e_ntt[j][p][N]; s_ntt[p][N]; sprime[p][N]:
-//   key[j][0][p] = -a s + e + [p == j] (P mod q_j) s'      (R5)
+// key[j][1][p] already holds a_j[p]; e_ntt[j][p][N]; s_ntt[p][N]; sprime[p][N]; np = L + K primes:
+//   key[j][0][p] = -a s + e + [p in digit j] (P mod p) s'      (R5, R17b; P = prod of the special primes)
 __global__ void k_ks_key_combine(const DCtx* __restrict__ dc, u64* __restrict__ key, const u64* __restrict__ e_ntt,
-                                 const u64* __restrict__ s_ntt, const u64* __restrict__ sprime, int L)
+                                 const u64* __restrict__ s_ntt, const u64* __restrict__ sprime, int np)
 {
     const int n = dc->n;
     const int k = blockIdx.x * 256 + threadIdx.x, p = blockIdx.y, j = blockIdx.z;
     const DPrime Pr = dc->p[p];
-    const size_t row1 = (((size_t)j * 2 + 1) * (L + 1) + p) * n + k;
-    const size_t row0 = (((size_t)j * 2 + 0) * (L + 1) + p) * n + k;
+    const size_t row1 = (((size_t)j * 2 + 1) * np + p) * n + k;
+    const size_t row0 = (((size_t)j * 2 + 0) * np + p) * n + k;
     const u64 a = key[row1];
     const u64 s = s_ntt[(size_t)p * n + k];
-    u64 v = submod(e_ntt[((size_t)j * (L + 1) + p) * n + k], mulmod(a, s, Pr), Pr.q);
-    if (p == j) {
-        const u64 gadget = dc->qmod[L][p];   // P mod q_j
-        v = addmod(v, mulmod(gadget, sprime[(size_t)p * n + k], Pr), Pr.q);
-    }
+    u64 v = submod(e_ntt[((size_t)j * np + p) * n + k], mulmod(a, s, Pr), Pr.q);
+    if (p < dc->n_data && p >= dc->dig_start[j] && p < dc->dig_start[j] + dc->dig_len[j])
+        v = addmod(v, mulmod(dc->pmod[p], sprime[(size_t)p * n + k], Pr), Pr.q);   // gadget P mod q_p
     key[row0] = v;
 }
 
@@ -310,7 +308,8 @@ void keyswitch_key_combine(const Launch& L, uint64_t* key, const uint64_t* e_ntt
                            const uint64_t* sprime, int Ld)
 {
     const int n = 1 << L.log_n;
-    k_ks_key_combine<<<dim3(n / 256, Ld + 1, Ld), 256, 0, L.st>>>(L.dc, key, e_ntt, s_ntt, sprime, Ld);
+    const int np = Ld + L.n_special;
+    k_ks_key_combine<<<dim3(n / 256, np, L.n_digits), 256, 0, L.st>>>(L.dc, key, e_ntt, s_ntt, sprime, np);
     check_launch("ks_key_combine");
     if (L.counter) ++*L.counter;
 }

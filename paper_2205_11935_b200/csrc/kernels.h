@@ -61,6 +61,16 @@ struct Launch {
     unsigned long long* counter;   // launches issued (for bench gpu_launches)
     Probe* probe;
     const int* pclass;             // host: prime class (ntt.cuh PC_*) of every prime, for probe accounting
+    int n_digits;                  // key-switching digits (R9b): host copies of the digit table
+    const int* dig_start;
+    const int* dig_len;
+    // digits with at least one prime among the nl active data primes
+    int active_digits(int nl) const
+    {
+        int d = 0;
+        while (d < n_digits && dig_start[d] < nl) ++d;
+        return d;
+    }
 };
 
 // batched in-place NTT over [batch][limbs][N]; limb l uses prime (prime0 + l)
@@ -83,10 +93,10 @@ struct KsOut {
     int accumulate;           // out += result (giant-step accumulation)
 };
 struct KsWork {
-    uint64_t* digits;         // [B][nl][N]
-    uint64_t* modup;          // [B][nl][nl+1][N]
-    uint64_t* acc;            // [G][B][2][nl+1][N]   (ModDown NTT outputs x, one block per rotation)
-    uint64_t* rem;            // [G][B][3][N]
+    uint64_t* digits;         // [B][nl][N]  digit coefficients (2-prime digits: (a, t) CRT pairs, R9b)
+    uint64_t* modup;          // [B][nd][nl+K][N]  (row e: q_e for e < nl, then P_0..P_{K-1})
+    uint64_t* acc;            // [G][B][2][nl+K][N]   (ModDown NTT outputs x, one block per rotation)
+    uint64_t* rem;            // [G][B][3][K][N]  special remainders (K = 2: CRT pairs)
 };
 #define KS_GMAX 8
 #define KS_LMAX 16
@@ -110,7 +120,7 @@ void keyswitch_modup(const Launch&, const KsIn& in, int batch, int nl, const KsW
 void keyswitch_finish_qp(const Launch&, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
                          const KsOut& out, bool baby);
 // the baby-step (scatter, addend P c0) QP inner product of a group on the FP64 tensor cores, pipelined
-// over the batch (k_ipmma.cu); CKKS_IP_MMA=1 selects the unpipelined k_ks_ip_mma, 0 the IMAD kernel
+// over the batch (k_ipmma.cu); CKKS_IP_MMA=0 selects the IMAD kernel k_ks_ip_qp
 void ip_mma_pipelined(const Launch&, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
                       size_t out_stride);
 // the giant-step (G = 1, accumulate, addend sigma_g(w.c0)) QP inner product, key-stationary over the
@@ -123,6 +133,20 @@ void moddown_qp(const Launch&, const uint64_t* y, size_t y_stride, int batch, in
 void lift_qp(const Launch&, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, int batch, int nl);
 void keyswitch_finish(const Launch&, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
                       const KsOut& out);
+// whole-limb NTT kernels of key switching (k_ksdigits.cu, k_ksmodup.cu, k_ksmoddown.cu); wide = 32 residues/thread
+void launch_ks_digits(const Launch&, const KsIn& in, int nd, int batch, int nl, uint64_t* digits, const uint64_t* rem,
+                      bool wide);
+void launch_ks_qp_rem(const Launch&, const uint64_t* in, size_t ct_stride, size_t comp_off, size_t comp_step,
+                      uint32_t galois, int nl, int ncomp, int batch, uint64_t* rem, bool wide);
+void launch_ks_modup(const Launch&, const uint64_t* digits, uint64_t* modup, int nl, int nd, bool all_e, int pairs,
+                     int batch, bool wide);
+void launch_ks_moddown_intt(const Launch&, const uint64_t* modup, const KsGroup& grp, int nl, int nd, int batch,
+                            uint64_t* rem, bool wide);
+void launch_ks_moddown_ntt(const Launch&, const uint64_t* rem, int nl, int gb, uint64_t* xo, bool wide);
+// the IMAD inner products (k_ipqp.cu): data rows + ModDown combine + permutation (ip_out); Q_l P basis (ip_qp)
+void ip_out(const Launch&, const KsWork& w, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsOut& out);
+void ip_qp(const Launch&, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w, const KsOut& out,
+           bool baby, int bbv, int spl);
 // out limbs[c][N] = in limbs[c][galois_src(k, g)] for `limbs` consecutive limbs (key pre-permutation)
 void galois_limbs(const Launch&, const uint64_t* in, uint64_t* out, size_t limbs, uint32_t g);
 

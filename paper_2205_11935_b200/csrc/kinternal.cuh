@@ -90,6 +90,13 @@ __device__ __forceinline__ u64 signed_to_res(long long x, const DPrime& P)
     return m ? P.q - m : 0;
 }
 
+// active primes of key-switching digit j at nl data limbs (R9b: a digit is cut at the level)
+__device__ __forceinline__ int digit_len_at(const DCtx* __restrict__ dc, int j, int nl)
+{
+    const int s0 = dc->dig_start[j];
+    return min(dc->dig_len[j], nl - s0);
+}
+
 // FP64 tensor-core MMA m16n8k4 (exact for the split-operand products used here)
 __device__ __forceinline__ void dmma16884(double (&c)[4], double a0, double a1, double b0)
 {

@@ -37,6 +37,7 @@ class Config:
     note: str = ""
     weight_std: tuple = ()      # per-layer N(0, std^2)
     bias_range: float = 0.1     # U[-bias_range, bias_range]
+    digits: tuple = ()          # key-switching digit sizes (R9b); () = one digit per data prime
 
     @property
     def n(self):
@@ -70,7 +71,21 @@ CFG5 = Config(
     weight_std=(1.0 / np.sqrt(512), 1.0 / np.sqrt(256)),
     note="1024 independent cfg4 inputs, one ciphertext each, one batched launch sequence")
 
-CONFIGS = {c.name: c for c in (CFG1, CFG2, CFG3, CFG4, CFG5)}
+# SURVEY 8(f) row f-3, reading R29: the cfg4/cfg5 network with hybrid key switching -- the same 8 data
+# primes [60, 40x7], two 40-bit special primes (log QP = 420 <= 438 at N = 16384) and dnum = 5 digits
+# {q0}, {q1 q2}, {q3 q4}, {q5 q6}, {q7}
+CFG4_HYBRID = Config(
+    name="cfg4_two_layer_forward_hybrid_ks", log_n=14, data_bits=(60,) + (40,) * 7, special_bits=(40, 40),
+    log2_scale=40, layers=((256, 512), (128, 256)), activation="square", batch=1, in_dim=512,
+    weight_std=(1.0 / np.sqrt(512), 1.0 / np.sqrt(256)), digits=(1, 2, 2, 2, 1),
+    note="cfg4 with hybrid key switching: [60, 40x7 | 40, 40], dnum = 5 (R29)")
+CFG5_HYBRID = Config(
+    name="cfg5_throughput_batch_hybrid_ks", log_n=14, data_bits=(60,) + (40,) * 7, special_bits=(40, 40),
+    log2_scale=40, layers=((256, 512), (128, 256)), activation="square", batch=1024, in_dim=512,
+    weight_std=(1.0 / np.sqrt(512), 1.0 / np.sqrt(256)), digits=(1, 2, 2, 2, 1),
+    note="cfg5 with hybrid key switching: [60, 40x7 | 40, 40], dnum = 5 (R29)")
+
+CONFIGS = {c.name: c for c in (CFG1, CFG2, CFG3, CFG4, CFG5, CFG4_HYBRID, CFG5_HYBRID)}
 
 _PURPOSE = {"x": 1, "w": 2, "b": 3, "residues": 4}
 

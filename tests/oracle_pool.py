@@ -25,7 +25,7 @@ def _dense_setup(spec, keys):
     import synthetic as S
     cfg = spec["cfg"]
     x = spec.get("x", 0)
-    o = oracle.Context(cfg.log_n, cfg.data_bits, cfg.special_bits)
+    o = oracle.Context(cfg.log_n, cfg.data_bits, cfg.special_bits, digits=cfg.digits or None)
     if keys:
         o.keygen(cfg.key_seed, OC.rotation_steps_for(cfg.layers, x))
     prob = S.dense_problem(cfg, batch=spec["batch"])
@@ -56,7 +56,7 @@ def _stack_setup(spec, keys):
     p, R = OC.packing(n // 2, t, 4)
     wts = S.frozen_stack_weights(t)
     steps = OC.frozen_stack_steps(t, [(t, t), (t - 2, t)], 9, 3)
-    o = oracle.Context(cfg.log_n, cfg.data_bits, cfg.special_bits)
+    o = oracle.Context(cfg.log_n, cfg.data_bits, cfg.special_bits, digits=cfg.digits or None)
     if keys:
         o.keygen(cfg.key_seed, steps)
     D = 2.0 ** cfg.log2_scale

@@ -38,7 +38,8 @@ def gpu_forward(spec, B, max_batch):
     cfg, x, act = spec["cfg"], spec.get("x", 0), spec["activation"]
     s, ms = OP.batch_messages(spec, B)
     g = G.Context(cfg.log_n, cfg.data_bits, cfg.special_bits, key_seed=cfg.key_seed,
-                  rot_steps=OC.rotation_steps_for(cfg.layers, x), max_batch=max_batch, bsgs_baby_extra=x)
+                  rot_steps=OC.rotation_steps_for(cfg.layers, x), max_batch=max_batch, bsgs_baby_extra=x,
+                  digits=cfg.digits or None)
     gl = [G.Layer(g, l.rows, l.cols, l.level, diag_coeffs=l.diag_coeffs, bias_coeffs=l.bias_coeffs,
                   pt_scale=l.pt_scale, bias_scale=l.bias_scale) for l in s["layers"]]
     model = G.Model(g, gl, {"none": 0, "square": 1, "cubic": 2}[act],
