@@ -46,6 +46,10 @@ def parse():
                    help="rotation schedule: 0 non-hoisted (SEAL semantics, R11), 1 hoisted baby steps (R11b), "
                         "2 double hoisting (R11c, default)")
     p.add_argument("--no-hoist", action="store_true", help="same as --hoisting 0")
+    p.add_argument("--ks", default="hybrid", choices=("hybrid", "single"),
+                   help="key switching: hybrid (R29: [60, 40x7 | 40, 40], dnum 5, the default) or single "
+                        "(one digit per prime + one 60-bit special prime, dnum 8)")
+    p.add_argument("--no-ks-variant", action="store_true", help="skip timing the other key-switching variant")
     p.add_argument("--bsgs-x", type=int, default=None,
                    help="extra baby-step doublings of the BSGS split (R5b); default 1 with --hoisting 2, else 0")
     return p.parse_args()
@@ -262,7 +266,7 @@ def build_forward(G, cfg, B, max_batch, device, hoisted=True, bsgs_x=None):
         bsgs_x = 1 if int(hoisted) == 2 else 0
     steps = G.model_steps(shapes, bsgs_x)
     ctx = G.Context(cfg.log_n, cfg.data_bits, cfg.special_bits, key_seed=cfg.key_seed, rot_steps=steps,
-                    max_batch=max_batch, device=device, bsgs_baby_extra=bsgs_x)
+                    max_batch=max_batch, device=device, bsgs_baby_extra=bsgs_x, digits=cfg.digits or None)
     Delta = 2.0 ** cfg.log2_scale
     levels, scales, _ = ctx.model_plan(shapes, G.ACT_SQUARE, ctx.top_level, Delta)
     prob = S.dense_problem(cfg, batch=B)
@@ -293,7 +297,7 @@ def run_ours(args):
     rank, local, world = dist_init("nccl")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    cfg = S.CFG5
+    cfg = workload_cfg(S, args.ks)
     B = args.batch or cfg.batch
     hoisting = 0 if args.no_hoist else args.hoisting
     ctx, model, ct, prob = build_forward(G, cfg, B, args.max_batch, device, hoisted=hoisting, bsgs_x=args.bsgs_x)
@@ -348,7 +352,11 @@ def run_ours(args):
               "warmup": max(3, args.warmup), "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
               "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded; shapes of BASELINE cfg5)",
               "config": {"workload": cfg.name, "batch_per_gpu": B, "N": ctx.n, "limbs": ctx.n_data,
-                         "special_primes": ctx.n_special, "dnum": ctx.n_data, "layers": [list(s) for s in cfg.layers],
+                         "special_primes": ctx.n_special, "dnum": ctx.n_digits, "digits": ctx.digits,
+                         "chain_bits": list(cfg.data_bits) + ["|"] + list(cfg.special_bits),
+                         "key_switching": {"hybrid": "hybrid (R29: dnum 5 digits, K = 2 special primes)",
+                                           "single": "one digit per prime, one special prime (R9)"}[args.ks],
+                         "layers": [list(s) for s in cfg.layers],
                          "activation": "square", "max_batch": args.max_batch,
                          "baby_steps": {0: "non-hoisted (R11)", 1: "hoisted (NEXT f-1, R11b)",
                                         2: "double hoisting (NEXT f-1, R11c)"}[hoisting],
@@ -401,13 +409,55 @@ def run_ours(args):
             result[k]["frac_of_measured_hbm"] = round(result[k]["GBps"] / peak, 4)
             result[k]["frac_of_8TBs"] = round(result[k]["GBps"] / 8000.0, 4)
 
+    if not args.no_ks_variant:
+        other = "single" if args.ks == "hybrid" else "hybrid"
+        result["ks_variant"] = bench_ks_variant(G, S, device, args, other, B, hoisting)
+        torch.cuda.empty_cache()
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"], parity = cpu_baseline_and_parity(G, S, device, B, args.max_batch, hoisting, args.bsgs_x)
+        result["cpu_baseline"], parity = cpu_baseline_and_parity(G, S, device, B, args.max_batch, hoisting, args.bsgs_x,
+                                                                 cfg)
         if parity is not None:
             result["parity"] = parity
     if rank == 0:
         print(json.dumps(result), flush=True)
     barrier()
+
+
+def workload_cfg(S, ks):
+    """The headline workload: BASELINE cfg5 with the chosen key switching (R29 hybrid by default)."""
+    return S.CFG5_HYBRID if ks == "hybrid" else S.CFG5
+
+
+def bench_ks_variant(G, S, device, args, ks, B, hoisting):
+    """The same cfg5 step with the other key-switching variant (device-resident, CUDA events)."""
+    import torch
+    cfg = workload_cfg(S, ks)
+    ctx, model, ct, _ = build_forward(G, cfg, B, args.max_batch, device, hoisted=hoisting, bsgs_x=args.bsgs_x)
+    out = ctx.empty_ct(B, model.final_level)
+    work = torch.empty(model.work_bytes(B), dtype=torch.uint8, device=device)
+    for _ in range(2):
+        model.forward(ct, out, work)
+    torch.cuda.synchronize()
+    reps = max(2, args.steps)
+    ctx.probe(G.PROBE_ALL)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        model.forward(ct, out, work)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    per = ctx.probe_read_all()
+    ctx.probe(G.PROBE_OFF)
+    per.pop("_modup_butterflies", None)
+    tot = sum(v["ms"] for v in per.values())
+    shares = {k: round(v["ms"] / tot, 4) for k, v in sorted(per.items(), key=lambda kv: -kv[1]["ms"])[:6]}
+    res = {"workload": cfg.name, "key_switching": ks, "dnum": ctx.n_digits, "special_primes": ctx.n_special,
+           "chain_bits": list(cfg.data_bits) + ["|"] + list(cfg.special_bits), "ms_per_step": round(ms, 3),
+           "forwards_per_s": round(B / (ms / 1e3), 2), "kernel_shares": shares}
+    del out, work, ct, model, ctx
+    return res
 
 
 def bench_frozen_stack(G, S, device, args):
@@ -665,11 +715,11 @@ class OraclePool:
     """Spawn pool of single-threaded oracle processes; every worker builds the oracle context, keys and
     encoded layers once (untimed setup), then times each forward it runs."""
 
-    def __init__(self, S, batch, workers):
+    def __init__(self, cfg, batch, workers):
         import concurrent.futures as cf
         import multiprocessing as mp
         OP = _oracle_pool_mod()
-        self.spec = dict(ORACLE_SPEC_KW, cfg=S.CFG5, batch=batch)
+        self.spec = dict(ORACLE_SPEC_KW, cfg=cfg, batch=batch)
         self.workers = workers
         self.ex = cf.ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("spawn"),
                                          initializer=OP._init, initargs=(self.spec,))
@@ -698,7 +748,7 @@ def _timed_oracle_forward(b):
     return bb, d, sc, e, time.perf_counter() - t0
 
 
-def cpu_baseline_and_parity(G, S, device, B, max_batch, hoisting, bsgs_x):
+def cpu_baseline_and_parity(G, S, device, B, max_batch, hoisting, bsgs_x, cfg):
     """cpu_baseline: the oracle forward over a process pool of the host cores, on a bounded sample of the
     cfg5 workload (one forward per worker; value = forwards / pool wall time).  parity: the library
     forward over the same B ciphertexts in the timed run's launch configuration (max_batch, hoisting,
@@ -711,7 +761,7 @@ def cpu_baseline_and_parity(G, S, device, B, max_batch, hoisting, bsgs_x):
     workers = oracle_workers(16)
     # first and last ciphertext of the batch (first and last launch chunk), the rest spread over it
     sample = sorted(set([0, B - 1] + [int(v) for v in np.linspace(0, B - 1, max(2, workers))]))[:max(2, workers)]
-    pool = OraclePool(S, B, workers)
+    pool = OraclePool(cfg, B, workers)
     try:
         wall, refs, busy = pool.forwards(sample)
     finally:
@@ -723,12 +773,11 @@ def cpu_baseline_and_parity(G, S, device, B, max_batch, hoisting, bsgs_x):
             "host_cores_available": os.cpu_count()}
     parity = None
     if hoisting == 2 and (bsgs_x is None or bsgs_x == 1):
-        spec = dict(ORACLE_SPEC_KW, cfg=S.CFG5, batch=B)
+        spec = dict(ORACLE_SPEC_KW, cfg=cfg, batch=B)
         s, ms = OP.batch_messages(spec, B)
-        cfg = S.CFG5
         ctx = G.Context(cfg.log_n, cfg.data_bits, cfg.special_bits, key_seed=cfg.key_seed,
                         rot_steps=OC.rotation_steps_for(cfg.layers, 1), max_batch=max_batch, device=device,
-                        bsgs_baby_extra=1)
+                        bsgs_baby_extra=1, digits=cfg.digits or None)
         gl = [G.Layer(ctx, l.rows, l.cols, l.level, diag_coeffs=l.diag_coeffs, bias_coeffs=l.bias_coeffs,
                       pt_scale=l.pt_scale, bias_scale=l.bias_scale) for l in s["layers"]]
         model = G.Model(ctx, gl, G.ACT_SQUARE)
@@ -741,9 +790,9 @@ def cpu_baseline_and_parity(G, S, device, B, max_batch, hoisting, bsgs_x):
         parity = {"checked": sorted(exact), "bit_exact": all(exact.values()),
                   "mismatch": sorted(b for b, v in exact.items() if not v),
                   "max_abs_err_vs_float64": max(refs[b][2] for b in refs),
-                  "how": f"library forward of the same {B} ciphertexts, max_batch {max_batch}, double hoisting, "
-                         "t1 64/32 (the timed run's launch sequence) on the oracle's encodings; every sampled "
-                         "ciphertext vs the C oracle"}
+                  "how": f"library forward of the same {B} ciphertexts ({cfg.name}), max_batch {max_batch}, double "
+                         "hoisting, t1 64/32 (the timed run's launch sequence) on the oracle's encodings; every "
+                         "sampled ciphertext vs the C oracle"}
         del out, ct, model, gl, ctx
         torch.cuda.empty_cache()
     return base, parity
@@ -760,9 +809,10 @@ def run_reference(args):
             barrier()
             return
     import synthetic as S
-    B = S.CFG5.batch
+    cfg = workload_cfg(S, args.ks)
+    B = cfg.batch
     workers = oracle_workers(16)
-    pool = OraclePool(S, B, workers)
+    pool = OraclePool(cfg, B, workers)
     try:
         for i in range(max(0, args.warmup)):
             if i >= 1:
@@ -780,7 +830,7 @@ def run_reference(args):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 1),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
            "data": "synthetic (seeded; shapes of BASELINE cfg5)",
-           "config": {"workload": S.CFG5.name, "batch_per_step": workers, "N": S.CFG5.n, "limbs": len(S.CFG5.data_bits),
+           "config": {"workload": cfg.name, "batch_per_step": workers, "N": cfg.n, "limbs": len(cfg.data_bits),
                       "note": f"each step = {workers} ciphertexts of the cfg5 batch (bounded sample) through the "
                               "double-hoisted cfg4 forward of the CPU oracle, one single-threaded process each"},
            "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": workers, "kind": "oracle",

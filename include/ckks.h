@@ -292,6 +292,21 @@ ckks_status ckks_encode(const ckks_ctx* ctx, const double* values, uint32_t coun
  * of ciphertext i comes from (enc_seed, first_index + i).  out->data device [batch][2][L][N]. */
 ckks_status ckks_encrypt(ckks_ctx* ctx, const int64_t* h_coeffs, uint32_t batch, uint64_t enc_seed,
                          uint64_t first_index, double scale, ckks_ct* out, void* stream);
+/* Client side on the device: the same three steps without host round trips.
+ * ckks_encode_device: d_values device [batch][values_stride] doubles (the first `count` <= N/2 of each row)
+ *   -> d_coeffs device [batch][N] int64 = round_half_away(inverse canonical embedding of scale * values) (R4,
+ *   R16), one n-point FFT per vector in FP64 (k_encode.cu); may differ by +-1 from ckks_encode on a
+ *   coefficient lying within rounding error of a half-integer.  Requires |scale * value| small enough that
+ *   every coefficient fits int64 (not checked on the device).
+ * ckks_encrypt_device: as ckks_encrypt, from device coefficients [batch][N]; no host synchronisation.
+ * ckks_decode_device: decrypted residues d_residues device [batch][level+1][N] (ckks_decrypt) -> d_values
+ *   device [batch][count] real slot values / scale (centred CRT lift in FP64, forward FFT). */
+ckks_status ckks_encode_device(ckks_ctx* ctx, const double* d_values, uint32_t count, size_t values_stride,
+                               uint32_t batch, double scale, int64_t* d_coeffs, void* stream);
+ckks_status ckks_encrypt_device(ckks_ctx* ctx, const int64_t* d_coeffs, uint32_t batch, uint64_t enc_seed,
+                                uint64_t first_index, double scale, ckks_ct* out, void* stream);
+ckks_status ckks_decode_device(ckks_ctx* ctx, const uint64_t* d_residues, uint32_t level, uint32_t batch,
+                               double scale, double* d_values, uint32_t count, void* stream);
 /* c0 + c1 s, inverse NTT: d_out device [batch][level+1][N] coefficient residues. */
 ckks_status ckks_decrypt(ckks_ctx* ctx, const ckks_ct* in, uint64_t* d_out, void* stream);
 /* Host decode of one decrypted [level+1][N] residue block: centered CRT lift, canonical

@@ -111,6 +111,9 @@ SIGNATURES = {
                                          ctypes.POINTER(_D), _VP, _VP]),
     "ckks_encode": (_I, [_VP, _VP, _U32, _D, _VP]),
     "ckks_encrypt": (_I, [_VP, _VP, _U32, _U64, _U64, _D, _PCT, _VP]),
+    "ckks_encode_device": (_I, [_VP, _VP, _U32, _SZ, _U32, _D, _VP, _VP]),
+    "ckks_encrypt_device": (_I, [_VP, _VP, _U32, _U64, _U64, _D, _PCT, _VP]),
+    "ckks_decode_device": (_I, [_VP, _VP, _U32, _U32, _D, _VP, _U32, _VP]),
     "ckks_decrypt": (_I, [_VP, _PCT, _VP, _VP]),
     "ckks_decode": (_I, [_VP, _VP, _U32, _D, _VP, _U32]),
     "ckks_export_key": (_I, [_VP, _I64, _VP, _VP]),
@@ -350,6 +353,33 @@ class Context:
         o = out.c()
         _check(lib().ckks_encrypt(self.h, m.ctypes.data_as(ctypes.c_void_p), m.shape[0], int(enc_seed),
                                   int(first_index), float(scale), ctypes.byref(o), _stream(stream)), "ckks_encrypt")
+        return out
+
+    def encode_device(self, values, scale, out=None, stream=None):
+        """values: device float64 tensor [batch][count] -> device int64 coefficients [batch][N] (f-4)."""
+        v = values if values.dim() == 2 else values[None]
+        B, count = int(v.shape[0]), int(v.shape[1])
+        out = out if out is not None else self.torch.empty((B, self.n), dtype=self.torch.int64, device=self.device)
+        _check(lib().ckks_encode_device(self.h, _ptr(v), count, int(v.stride(0)), B, float(scale), _ptr(out),
+                                        _stream(stream)), "ckks_encode_device")
+        return out
+
+    def encrypt_device(self, coeffs, enc_seed, first_index=0, scale=1.0, out=None, stream=None):
+        """device int64 coefficients [batch][N] -> top-level ciphertexts (device encryption, no host copies)."""
+        B = int(coeffs.shape[0])
+        out = out or self.empty_ct(B, self.top_level, scale=scale)
+        o = out.c()
+        _check(lib().ckks_encrypt_device(self.h, _ptr(coeffs), B, int(enc_seed), int(first_index), float(scale),
+                                         ctypes.byref(o), _stream(stream)), "ckks_encrypt_device")
+        out.level, out.scale = o.level, o.scale
+        return out
+
+    def decode_device(self, residues, level, scale, count, out=None, stream=None):
+        """device decrypted residues [batch][level+1][N] -> device float64 slot values [batch][count]."""
+        B = int(residues.shape[0])
+        out = out if out is not None else self.torch.empty((B, count), dtype=self.torch.float64, device=self.device)
+        _check(lib().ckks_decode_device(self.h, _ptr(residues), int(level), B, float(scale), _ptr(out), int(count),
+                                        _stream(stream)), "ckks_decode_device")
         return out
 
     def decrypt(self, ct, stream=None):

@@ -130,6 +130,12 @@ u64 min_root(u64 q, int log_n)
 }
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+// device canonical-embedding tables (k_encode.cu): slot positions [n] u32, zeta^k [n], omega^p [n/2] (n = N/2)
+size_t embed_table_bytes(int N)
+{
+    const size_t n = (size_t)N / 2;
+    return align256(n * 4) + align256(n * 16) + align256(n / 2 * 16);
+}
 
 // ------------------------------------------------------------------------------ FFT (encode/decode)
 void fft(std::vector<std::complex<double>>& a, int sign)
@@ -558,7 +564,7 @@ static void sizes_impl(const ckks_params* p, size_t* tb, size_t* kb, size_t* wb,
         if (g != 1 && std::find(ids.begin(), ids.end(), g) == ids.end()) ids.push_back(g);
     }
     const size_t key_words = p->n_special ? (size_t)nd * 2 * np * n : 0;
-    *tb = align256(sizeof(DCtx)) + align256((size_t)np * 8 * n * 8);
+    *tb = align256(sizeof(DCtx)) + align256((size_t)np * 8 * n * 8) + embed_table_bytes(n);
     // every switching key, plus a sigma_{g^-1}-permuted copy per key slot (used by hoisted rotations)
     *kb = align256((size_t)np * n * 8) + align256((size_t)2 * L * n * 8) + 2 * ids.size() * key_words * 8;
     const int B = (int)p->max_batch;
@@ -732,6 +738,35 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
         h.tw = c->d_tw;
         cudaStream_t st = (cudaStream_t)stream;
         cuda_ok(cudaMemcpyAsync(c->d_tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice, st), "upload tables");
+        // canonical embedding tables (R3): pos(i) = (5^i mod 2N - 1) / 4, zeta^k, omega^p in long double
+        {
+            const int ns = n / 2;
+            char* eb = tbase + align256(sizeof(DCtx)) + align256((size_t)np * 8 * n * 8);
+            std::vector<u32> pos(ns);
+            std::vector<double> zeta(2 * (size_t)ns), omega(ns);
+            u64 e = 1;
+            for (int i = 0; i < ns; ++i) {
+                pos[i] = (u32)((e - 1) / 4);
+                e = e * 5 % (2ULL * n);
+            }
+            const long double pi = 3.141592653589793238462643383279502884L;
+            for (int k = 0; k < ns; ++k) {
+                zeta[2 * k] = (double)cosl(pi * k / n);
+                zeta[2 * k + 1] = (double)sinl(pi * k / n);
+            }
+            for (int q = 0; q < ns / 2; ++q) {
+                omega[2 * q] = (double)cosl(2 * pi * q / ns);
+                omega[2 * q + 1] = (double)sinl(2 * pi * q / ns);
+            }
+            h.slot_pos = (const u32*)eb;
+            h.fft_zeta = (const double2*)(eb + align256((size_t)ns * 4));
+            h.fft_omega = (const double2*)(eb + align256((size_t)ns * 4) + align256((size_t)ns * 16));
+            cuda_ok(cudaMemcpyAsync((void*)h.slot_pos, pos.data(), pos.size() * 4, cudaMemcpyHostToDevice, st), "tables");
+            cuda_ok(cudaMemcpyAsync((void*)h.fft_zeta, zeta.data(), zeta.size() * 8, cudaMemcpyHostToDevice, st), "tables");
+            cuda_ok(cudaMemcpyAsync((void*)h.fft_omega, omega.data(), omega.size() * 8, cudaMemcpyHostToDevice, st),
+                    "tables");
+            cuda_ok(cudaStreamSynchronize(st), "tables");   // host vectors go out of scope
+        }
         cuda_ok(cudaMemcpyAsync(c->d_dc, &h, sizeof(DCtx), cudaMemcpyHostToDevice, st), "upload consts");
         // ---- key buffers
         char* kbase = (char*)d_keys;
@@ -1994,6 +2029,58 @@ ckks_status ckks_encrypt(ckks_ctx* c, const int64_t* h_coeffs, uint32_t batch, u
         out->n_comp = 2;
         out->level = (uint32_t)(L - 1);
         out->scale = scale;
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_encode_device(ckks_ctx* c, const double* d_values, uint32_t count, size_t values_stride,
+                               uint32_t batch, double scale, int64_t* d_coeffs, void* stream)
+{
+    CK_TRY({
+        if (!c || (!d_values && count) || !d_coeffs) throw CkksError(CKKS_E_PARAM, "null");
+        if (count > (uint32_t)c->n / 2) throw CkksError(CKKS_E_PARAM, "more values than slots");
+        if (count > values_stride && batch > 1) throw CkksError(CKKS_E_PARAM, "values_stride < count");
+        if (!(scale > 0) || scale >= std::ldexp(1.0, 62)) throw CkksError(CKKS_E_PARAM, "scale out of range");
+        ck::encode_device(c->launch(stream), d_values, (int)count, values_stride, (int)batch, scale, d_coeffs);
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_encrypt_device(ckks_ctx* c, const int64_t* d_coeffs, uint32_t batch, uint64_t enc_seed,
+                                uint64_t first_index, double scale, ckks_ct* out, void* stream)
+{
+    CK_TRY({
+        if (!c || !d_coeffs || !out || !out->data) throw CkksError(CKKS_E_PARAM, "null");
+        const int L = c->L, n = c->n;
+        auto Lc = c->launch(stream);
+        for (uint32_t b0 = 0; b0 < batch; b0 += c->max_batch) {
+            const int B = (int)std::min<uint32_t>(c->max_batch, batch - b0);
+            u64* u = c->d_work;   // stream-ordered reuse of the workspace across chunks (no host sync)
+            u64* e0 = u + (size_t)B * L * n;
+            u64* e1 = e0 + (size_t)B * L * n;
+            u64* mm = e1 + (size_t)B * L * n;
+            ck::signed_to_ntt(Lc, d_coeffs + (size_t)b0 * n, mm, B, L);
+            ck::sample_ntt(Lc, u, B, L, L, 0, enc_seed, 6, first_index + b0, 1, 0, 0);
+            ck::sample_ntt(Lc, e0, B, L, L, 1, enc_seed, 7, first_index + b0, 1, 0, 0);
+            ck::sample_ntt(Lc, e1, B, L, L, 1, enc_seed, 8, first_index + b0, 1, 0, 0);
+            ck::encrypt_combine(Lc, c->d_pk, u, e0, e1, mm, out->data + (size_t)b0 * c->ct_words(L), B, L);
+        }
+        out->batch = batch;
+        out->n_comp = 2;
+        out->level = (uint32_t)(L - 1);
+        out->scale = scale;
+        return CKKS_OK;
+    })
+}
+
+ckks_status ckks_decode_device(ckks_ctx* c, const uint64_t* d_residues, uint32_t level, uint32_t batch, double scale,
+                               double* d_values, uint32_t count, void* stream)
+{
+    CK_TRY({
+        if (!c || !d_residues || !d_values) throw CkksError(CKKS_E_PARAM, "null");
+        if ((int)level >= c->L) throw CkksError(CKKS_E_SHAPE, "level");
+        if (count > (uint32_t)c->n / 2) throw CkksError(CKKS_E_PARAM, "count > slots");
+        ck::decode_device(c->launch(stream), d_residues, (int)level + 1, (int)batch, scale, d_values, (int)count);
         return CKKS_OK;
     })
 }

@@ -7,6 +7,7 @@
 // Lazy ranges are stated at every use.
 #pragma once
 #include <cstdint>
+#include <vector_types.h>
 
 typedef uint64_t u64;
 typedef uint32_t u32;
@@ -41,6 +42,10 @@ struct DCtx {
     u64 pmod[CKKS_MAXP], pmod_sh[CKKS_MAXP];         // P mod q_p (0 for the special primes)
     u64 pinv[CKKS_MAXP], pinv_sh[CKKS_MAXP];         // P^{-1} mod q_i (data primes)
     u64 phalf_lo, phalf_hi;                          // (P - 1) / 2 as a 128-bit integer
+    // canonical embedding on the device (k_encode.cu, R3/R4): n = N/2 slots
+    const u32* slot_pos;                             // [n] (5^i mod 2N - 1) / 4
+    const double2* fft_zeta;                         // [n] zeta^k = e^{i pi k / N}
+    const double2* fft_omega;                        // [n/2] omega^p = e^{2 pi i p / n}
 };
 
 __device__ __forceinline__ u64 csub(u64 a, u64 m) { return a >= m ? a - m : a; }

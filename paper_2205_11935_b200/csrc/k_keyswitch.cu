@@ -46,35 +46,36 @@ void keyswitch_modup(const Launch& L, const KsIn& in, int batch, int nl, const K
     const int K = L.n_special, ne = nl + K, nd = L.active_digits(nl);
     int pairs = 0;   // (digit, target row) pairs of the ModUp
     for (int j = 0; j < nd; ++j) pairs += qp_in ? ne : ne - std::min(L.dig_len[j], nl - L.dig_start[j]);
-    {
-        const int wm = ntt_wide_mask();
-        const bool pm = L.probe && L.probe->on(PROBE_MODUP);
-        if (L.probe && L.probe->on(PROBE_ALL)) {
-            L.probe->bytes_by_kernel["k_ks_modup"] += ((double)batch * nl + (double)batch * pairs) * (double)(8 << L.log_n);
-            // butterflies per limb NTT: (N/2) log2 N; targets of digit j: every row but its own (QP: all)
-            const double bf = (double)(1 << (L.log_n - 1)) * L.log_n * batch;
-            for (int j = 0; j < nd; ++j) {
-                const int s0 = L.dig_start[j], len = std::min(L.dig_len[j], nl - s0);
-                for (int e = 0; e < ne; ++e) {
-                    if (!qp_in && e >= s0 && e < s0 + len) continue;
-                    const int p = e < nl ? e : L.n_data + (e - nl);
-                    if (L.pclass && L.pclass[p] == PC_FP) L.probe->bfly_fp += bf;
-                    else L.probe->bfly_int += bf;
-                }
+    const bool pm = L.probe && L.probe->on(PROBE_MODUP);
+    if (L.probe && L.probe->on(PROBE_ALL)) {
+        L.probe->bytes_by_kernel["k_ks_modup"] += ((double)batch * nl + (double)batch * pairs) * (double)(8 << L.log_n);
+        // butterflies per limb NTT: (N/2) log2 N; targets of digit j: every row but its own (QP: all)
+        const double bf = (double)(1 << (L.log_n - 1)) * L.log_n * batch;
+        for (int j = 0; j < nd; ++j) {
+            const int s0 = L.dig_start[j], len = std::min(L.dig_len[j], nl - s0);
+            for (int e = 0; e < ne; ++e) {
+                if (!qp_in && e >= s0 && e < s0 + len) continue;
+                const int p = e < nl ? e : L.n_data + (e - nl);
+                if (L.pclass && L.pclass[p] == PC_FP) L.probe->bfly_fp += bf;
+                else L.probe->bfly_int += bf;
             }
         }
-        if (qp_in) launch_ks_qp_rem(L, in.base, in.ct_stride, in.comp_off, 0, in.galois, nl, 1, batch, w.rem, wm & 1);
-        launch_ks_digits(L, in, nd, batch, nl, w.digits, qp_in ? w.rem : nullptr, wm & 1);
-        if (pm) {
-            L.probe->mark(L.st);
-            // digits read once, one ModUp limb written per (digit, target) pair
-            L.probe->alg_bytes += ((double)batch * nl + (double)batch * pairs) * (double)(8 << L.log_n);
-        }
-        launch_ks_modup(L, w.digits, w.modup, nl, nd, qp_in, pairs, batch, wm & 2);
-        if (pm) L.probe->mark(L.st);
     }
+    if (qp_in) launch_ks_qp_rem(L, in.base, in.ct_stride, in.comp_off, 0, in.galois, nl, 1, batch, w.rem);
+    launch_ks_digits(L, in, nl, batch, w.digits, qp_in ? w.rem : nullptr);
+    if (pm) {
+        L.probe->mark(L.st);
+        // digits read once, one ModUp limb written per (digit, target) pair
+        L.probe->alg_bytes += ((double)batch * nl + (double)batch * pairs) * (double)(8 << L.log_n);
+    }
+    launch_ks_modup(L, w.digits, w.modup, nl, qp_in, batch);
+    if (pm) L.probe->mark(L.st);
     check_launch("keyswitch_modup");
-    if (L.counter) *L.counter += qp_in ? 3 : 2;
+    if (L.counter) {   // digits and ModUp: one launch per digit size present
+        DigitSet one, two;
+        digit_sets(L, nl, qp_in, one, two);
+        *L.counter += (qp_in ? 1 : 0) + 2 * ((one.count ? 1 : 0) + (two.count ? 1 : 0));
+    }
 }
 
 // QP-basis finish (R11c): inner product over all nl+K rows, no ModDown.  in (baby: the Q_l input whose
@@ -121,8 +122,8 @@ void moddown_qp(const Launch& L, const uint64_t* y, size_t y_stride, int batch, 
 {
     if (batch <= 0) return;
     const int n = 1 << L.log_n;
-    launch_ks_qp_rem(L, y, y_stride, 0, (size_t)(nl + L.n_special) * n, 0, nl, 2, batch, w.rem, false);
-    launch_ks_moddown_ntt(L, w.rem, nl, batch, w.acc, false);
+    launch_ks_qp_rem(L, y, y_stride, 0, (size_t)(nl + L.n_special) * n, 0, nl, 2, batch, w.rem);
+    launch_ks_moddown_ntt(L, w.rem, nl, batch, w.acc);
     { ProbeScope ps_(L.probe, L.st, "k_moddown_combine");
       k_moddown_combine<<<dim3(n / 256, nl, 2 * batch), 256, 0, L.st>>>(L.dc, y, y_stride, w.acc, out, out_stride, nl); }
     check_launch("moddown_qp");
@@ -161,9 +162,8 @@ void keyswitch_finish(const Launch& L, const KsIn& in, const KsGroup& grp, int b
     if (batch <= 0 || grp.G <= 0) return;
     if (grp.G > KS_GMAX || nl > KS_LMAX) throw std::runtime_error("keyswitch_finish: group/limb limits");
     const int n = 1 << L.log_n, nd = L.active_digits(nl);
-    const int wm = ntt_wide_mask();
-    launch_ks_moddown_intt(L, w.modup, grp, nl, nd, batch, w.rem, wm & 4);
-    launch_ks_moddown_ntt(L, w.rem, nl, batch * grp.G, w.acc, wm & 8);
+    launch_ks_moddown_intt(L, w.modup, grp, nl, nd, batch, w.rem);
+    launch_ks_moddown_ntt(L, w.rem, nl, batch * grp.G, w.acc);
     if (n < 1024) throw std::runtime_error("N >= 1024 required");
     ip_out(L, w, in, grp, batch, nl, out);
     check_launch("keyswitch_finish");

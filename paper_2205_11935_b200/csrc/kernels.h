@@ -133,16 +133,25 @@ void moddown_qp(const Launch&, const uint64_t* y, size_t y_stride, int batch, in
 void lift_qp(const Launch&, const uint64_t* in, size_t in_stride, uint64_t* out, size_t out_stride, int batch, int nl);
 void keyswitch_finish(const Launch&, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
                       const KsOut& out);
-// whole-limb NTT kernels of key switching (k_ksdigits.cu, k_ksmodup.cu, k_ksmoddown.cu); wide = 32 residues/thread
-void launch_ks_digits(const Launch&, const KsIn& in, int nd, int batch, int nl, uint64_t* digits, const uint64_t* rem,
-                      bool wide);
+// The active key-switching digits of one prime-count class (1- or 2-prime digits) at nl data limbs, passed to
+// the digit / ModUp kernels by value (kernel parameter space: no dependent global loads in their prologue).
+struct DigitSet {
+    int count;                 // digits in the set
+    int j[KS_LMAX];            // digit index (its block of the ModUp buffer)
+    int s0[KS_LMAX];           // its first data prime
+    int first[KS_LMAX + 1];    // ModUp: prefix sums of the target rows per digit (blockIdx.x -> digit)
+};
+// whole-limb NTT kernels of key switching (k_ksdigits.cu, k_ksqprem.cu, k_ksmodup.cu, k_ksmoddown.cu), one
+// instantiation per digit size / special-prime count so every loader and storer is branch-free
+void launch_ks_digits(const Launch&, const KsIn& in, int nl, int batch, uint64_t* digits, const uint64_t* rem);
 void launch_ks_qp_rem(const Launch&, const uint64_t* in, size_t ct_stride, size_t comp_off, size_t comp_step,
-                      uint32_t galois, int nl, int ncomp, int batch, uint64_t* rem, bool wide);
-void launch_ks_modup(const Launch&, const uint64_t* digits, uint64_t* modup, int nl, int nd, bool all_e, int pairs,
-                     int batch, bool wide);
+                      uint32_t galois, int nl, int ncomp, int batch, uint64_t* rem);
+void launch_ks_modup(const Launch&, const uint64_t* digits, uint64_t* modup, int nl, bool all_e, int batch);
 void launch_ks_moddown_intt(const Launch&, const uint64_t* modup, const KsGroup& grp, int nl, int nd, int batch,
-                            uint64_t* rem, bool wide);
-void launch_ks_moddown_ntt(const Launch&, const uint64_t* rem, int nl, int gb, uint64_t* xo, bool wide);
+                            uint64_t* rem);
+void launch_ks_moddown_ntt(const Launch&, const uint64_t* rem, int nl, int gb, uint64_t* xo);
+// the two DigitSets (1-prime, 2-prime digits) of the active digits at nl limbs; first[] counts ModUp targets
+void digit_sets(const Launch&, int nl, bool all_e, DigitSet& one, DigitSet& two);
 // the IMAD inner products (k_ipqp.cu): data rows + ModDown combine + permutation (ip_out); Q_l P basis (ip_qp)
 void ip_out(const Launch&, const KsWork& w, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsOut& out);
 void ip_qp(const Launch&, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w, const KsOut& out,
@@ -164,6 +173,11 @@ void bsgs_mac(const Launch&, const uint64_t* pts, int pt_nl, const uint64_t* v0,
               const uint64_t* vbaby, uint64_t* wout, int t1, int t2, int batch, int nl, bool qp);
 void decrypt(const Launch&, const uint64_t* ct, size_t ct_stride, const uint64_t* s_ntt, uint64_t* out, int batch, int nl);
 
+// client side on the device (k_encode.cu, f-4): canonical-embedding encode of values [batch][count] (row stride
+// vstride) at scale -> int64 coefficients [batch][N]; decode of decrypted residues [batch][nl][N] -> [batch][count]
+void encode_device(const Launch&, const double* values, int count, size_t vstride, int batch, double scale,
+                   int64_t* out);
+void decode_device(const Launch&, const uint64_t* res, int nl, int batch, double scale, double* out, int count);
 // signed int64 coefficients [count][N] -> NTT residues out[count][nl(+1)][N] over primes 0..nl-1 (and P)
 void signed_to_ntt(const Launch&, const int64_t* coeffs, uint64_t* out, int count, int nl, bool with_special = false);
 

@@ -35,15 +35,15 @@ static void allow_smem(K kernel, size_t bytes)
     }
 }
 
-// Threads per CTA of the key-switch NTT kernels: bit set = 32 residues per thread (N/32 threads),
-// clear = 16 (N/16 threads).  bits: 1 digits, 2 ModUp, 4 ModDown iNTT, 8 ModDown NTT, 16 batched forward
-// NTT, 32 batched inverse NTT.  Default 2 | 16 (measured, tools/sweep_wide2.sh, tools/ab_nttbatch.sh);
-// CKKS_NTT_WIDE overrides it (tuning experiments only).
+// Threads per CTA of the batched NTT kernel (k_ntt_batch): bit 16 set = 32 residues per thread (N/32 threads)
+// for the forward, bit 32 for the inverse; clear = 16 (N/16 threads).  Default 16 (measured,
+// tools/ab_nttbatch.sh); CKKS_NTT_WIDE overrides it (tuning experiments only).  The key-switching NTT
+// kernels use fixed shapes: ModUp 32 residues per thread (compute-bound), the others 16.
 static int ntt_wide_mask()
 {
     static int mask = [] {
         const char* e = getenv("CKKS_NTT_WIDE");
-        return e ? atoi(e) : 2 | 16;
+        return e ? atoi(e) : 16;
     }();
     return mask;
 }
