@@ -393,6 +393,7 @@ def run_ours(args):
                          "h2d_bytes_per_step": int(h_in.numel() * 8), "d2h_bytes_per_step": int(h_out.numel() * 8),
                          "wall_s": round(time.perf_counter() - t0, 3)}
         del h_in, h_out
+        result["e2e_client_on_gpu"] = bench_e2e_client(G, ctx, model, prob, B, work, args, device)
 
     del work, out, ct, model
     torch.cuda.empty_cache()
@@ -401,7 +402,9 @@ def run_ours(args):
     if not args.no_extras:
         result["latency"] = bench_latency(G, S, device, args)
         torch.cuda.empty_cache()
-        result["frozen_stack_p2"] = bench_frozen_stack(G, S, device, args)
+        result["frozen_stack_p2"] = bench_frozen_stack(G, S, device, args, S.P2_STACK)
+        torch.cuda.empty_cache()
+        result["frozen_stack_p1"] = bench_frozen_stack(G, S, device, args, S.P1_STACK)
         torch.cuda.empty_cache()
         result["ntt_microbench"] = bench_ntt(G, S, device, args)
         result["keyswitch"] = bench_keyswitch(G, S, device, args)
@@ -422,6 +425,57 @@ def run_ours(args):
     if rank == 0:
         print(json.dumps(result), flush=True)
     barrier()
+
+
+def bench_e2e_client(G, ctx, model, prob, B, work, args, device):
+    """NEXT f-4: client and server on one GPU, end to end from host float64 inputs to host float64 outputs
+    through the public API: H2D of the packed inputs [x || x], ckks_encode_device ->
+    ckks_encrypt_device -> ckks_encrypted_forward -> ckks_decrypt -> ckks_decode_device, D2H of the 128
+    output values per input.  Every step's copies and kernels are inside the timed region."""
+    import torch
+    t0 = G.bsgs_plan(*prob["W"][0].shape, ctx.bsgs_baby_extra)[0]
+    d = prob["x"].shape[1]
+    h_x = torch.zeros((B, 2 * t0), dtype=torch.float64, pin_memory=True)
+    h_x[:, :d] = torch.from_numpy(prob["x"])
+    h_x[:, t0:t0 + d] = torch.from_numpy(prob["x"])
+    rows = prob["W"][-1].shape[0]
+    h_y = torch.empty((B, rows), dtype=torch.float64, pin_memory=True)
+    D = 2.0 ** 40
+    d_x = torch.empty((B, 2 * t0), dtype=torch.float64, device=device)
+    coeffs = torch.empty((B, ctx.n), dtype=torch.int64, device=device)
+    ct = ctx.empty_ct(B, ctx.top_level, scale=D)
+    out = ctx.empty_ct(B, model.final_level)
+    dec = torch.empty((B, model.final_level + 1, ctx.n), dtype=torch.int64, device=device)
+    d_y = torch.empty((B, rows), dtype=torch.float64, device=device)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        d_x.copy_(h_x, non_blocking=True)
+        ctx.encode_device(d_x, D, out=coeffs)
+        ctx.encrypt_device(coeffs, 0x5EED0002, 0, D, out=ct)
+        model.forward(ct, out, work)
+        c = out.c()
+        G._check(G.lib().ckks_decrypt(ctx.h, G.ctypes.byref(c), G._ptr(dec), G._stream()), "ckks_decrypt")
+        ctx.decode_device(dec, out.level, out.scale, rows, out=d_y)
+        h_y.copy_(d_y, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    ref = prob["x"] @ prob["W"][0].T + prob["b"][0]
+    ref = (ref * ref) @ prob["W"][1].T + prob["b"][1]
+    err = float(np.max(np.abs(h_y.numpy() - ref)))
+    return {"value": round(B / (ms / 1e3), 3), "unit": UNIT, "ms_per_step": round(ms, 3),
+            "h2d_bytes_per_step": int(h_x.numel() * 8), "d2h_bytes_per_step": int(h_y.numel() * 8),
+            "max_abs_err_vs_float64_all_inputs": err,
+            "how": "host float64 [x||x] -> H2D -> ckks_encode_device -> ckks_encrypt_device -> forward -> "
+                   "ckks_decrypt -> ckks_decode_device -> D2H of the 128 outputs (client and server on the GPU)"}
 
 
 def workload_cfg(S, ks):
@@ -460,13 +514,14 @@ def bench_ks_variant(G, S, device, args, ks, B, hoisting):
     return res
 
 
-def bench_frozen_stack(G, S, device, args):
+def bench_frozen_stack(G, S, device, args, cfg=None):
     """NEXT f-2: the paper's frozen stack (conv 9 -> dense 768 + ReLU_approx -> pool 3 -> dense 766,
-    depth 6) at the Table 2 p2 preset (N=16384, log q=420, log Delta=50, p=5 items per ciphertext),
-    library encoders, the main line's rotation schedule.  Paper context: 2.56 s per forward (5 items) single-thread
-    SEAL+HEXL."""
+    depth 6) at a Table 2 preset: p2 = N=16384, log q=420 = [60, 50x6 | 60], log Delta=50,
+    p=5 items per ciphertext; p1 = N=8192, [40, 22x6 | 46] (log q ~ 217), log Delta=22, p=2 items.
+    Library encoders, the main line's rotation schedule.  Paper context: 2.56 s (p2) / 1.08 s (p1) per
+    forward single-thread SEAL+HEXL."""
     import torch
-    cfg = S.P2_STACK
+    cfg = cfg or S.P2_STACK
     t, f_conv, f_pool = 768, 9, 3
     c = (f_conv - 1) // 2
     n_slots = (1 << cfg.log_n) // 2
@@ -478,7 +533,7 @@ def bench_frozen_stack(G, S, device, args):
         steps |= set(range(1, t1)) | set(k * t1 for k in range(1, t2)) | {-tt}
     B = cfg.batch
     ctx = G.Context(cfg.log_n, cfg.data_bits, cfg.special_bits, key_seed=cfg.key_seed, rot_steps=sorted(steps),
-                    max_batch=B, device=device)
+                    max_batch=B, device=device, digits=cfg.digits or None)
     wts = S.frozen_stack_weights(t)
     D = 2.0 ** cfg.log2_scale
     l0 = ctx.top_level
@@ -511,17 +566,23 @@ def bench_frozen_stack(G, S, device, args):
     e1.record()
     torch.cuda.synchronize()
     ms_fwd = e0.elapsed_time(e1) / reps
-    # accuracy check of one item against the float64 stack (product decode path)
-    y = ctx.decode(u64_np(ctx.decrypt(out))[0], out.level, out.scale, R)
-    ref = _plain_stack(xs[0], wts)
-    err = float(np.max(np.abs(y[: ref.size] - ref)))
+    # accuracy of every item of two ciphertexts against the float64 stack (product decode path)
+    dec = u64_np(ctx.decrypt(out))
+    err = 0.0
+    for b in (0, B - 1):
+        y = ctx.decode(dec[b], out.level, out.scale, n_slots)
+        for r in range(p):
+            ref = _plain_stack(xs[b * p + r], wts)
+            err = max(err, float(np.max(np.abs(y[r * R: r * R + ref.size] - ref))))
     fwd_s = B / (ms_fwd / 1e3)
+    t_paper = {"paper_p2_frozen_stack": 2.56, "paper_p1_frozen_stack": 1.08}[cfg.name]
     return {"workload": cfg.name, "batch_cts": B, "items_per_ct": p, "region": R, "depth": 6,
+            "chain_bits": list(cfg.data_bits) + ["|"] + list(cfg.special_bits), "log2_scale": cfg.log2_scale,
             "ms_per_batch": round(ms_fwd, 2), "forwards_per_s": round(fwd_s, 2), "items_per_s": round(fwd_s * p, 1),
-            "max_abs_err_item0": err,
-            "paper_context": {"t_S_s_per_forward_p2_avx512": 2.56, "items_per_forward": 5,
-                              "source": "PAPER.md L191 (Table 2), single thread i7-1165G7",
-                              "speedup_forwards": round(fwd_s * 2.56, 1)}}
+            "max_abs_err_items": err,
+            "paper_context": {"t_S_s_per_forward_avx512": t_paper, "items_per_forward": p,
+                              "source": "PAPER.md L190-191 (Table 2), single thread i7-1165G7",
+                              "speedup_forwards": round(fwd_s * t_paper, 1)}}
 
 
 def u64_np(t):

@@ -26,10 +26,12 @@ def main():
     p.add_argument("--max-batch", type=int, default=256)
     p.add_argument("--no-hoist", action="store_true")
     p.add_argument("--hoisting", type=int, default=2)
+    p.add_argument("--ks", default="hybrid", choices=("hybrid", "single"))
     a = p.parse_args()
     dev = torch.device("cuda", 0)
     if a.mode == "forward":
-        ctx, model, ct, _ = bench.build_forward(G, S.CFG5, a.batch, a.max_batch, dev, hoisted=0 if a.no_hoist else a.hoisting)
+        ctx, model, ct, _ = bench.build_forward(G, bench.workload_cfg(S, a.ks), a.batch, a.max_batch, dev,
+                                                hoisted=0 if a.no_hoist else a.hoisting)
         out = ctx.empty_ct(a.batch, model.final_level)
         work = torch.empty(model.work_bytes(a.batch), dtype=torch.uint8, device=dev)
         model.forward(ct, out, work)
