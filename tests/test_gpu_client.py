@@ -51,7 +51,7 @@ def test_encrypt_device_bit_exact_and_decode_device():
     for b in range(B):
         ref = OE.decode(o.decrypt(u64(ct.data)[b]), o.primes, 2.0 ** 40, o.n)
         assert np.max(np.abs(y[b] - ref)) < 1e-9
-        assert np.max(np.abs(y[b] - vals[b])) < 2.0 ** -28
+        assert np.max(np.abs(y[b] - vals[b])) < 2.0 ** -20          # fresh-encryption noise over 2^40
 
 
 def test_client_round_trip_through_a_forward_level():
