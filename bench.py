@@ -368,6 +368,10 @@ def run_ours(args):
     if clk:
         result["clocks"] = clk
 
+    # ---- A/B of the BSGS inner sums: FP64 tensor cores (DMMA, the default) vs integer tensor cores (tcgen05 kind::i8)
+    if not args.no_extras:
+        result["mac_tc_ab"] = bench_mac_ab(G, ctx, model, ct, out, work, args, stream)
+
     # ---- e2e through the C-ABI with host buffers (H2D + D2H inside the timed region)
     if not args.no_e2e:
         nl_in = ct.level + 1
@@ -425,6 +429,38 @@ def run_ours(args):
     if rank == 0:
         print(json.dumps(result), flush=True)
     barrier()
+
+
+def bench_mac_ab(G, ctx, model, ct, out, work, args, stream):
+    """The timed step with each BSGS-MAC kernel (ckks_set_option("mac_tc")): same bits (checked), device time."""
+    import torch
+    res = {}
+    ref = None
+    old = G.get_option("mac_tc")
+    try:
+        for name, v in (("fp64_dmma", 0), ("int8_tcgen05", 1)):
+            G.set_option("mac_tc", v)
+            model.forward(ct, out, work)
+            torch.cuda.synchronize()
+            bits = out.data.clone()
+            if ref is None:
+                ref = bits
+            ctx.probe(G.PROBE_ALL)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(max(2, args.steps)):
+                model.forward(ct, out, work)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            per = ctx.probe_read_all()
+            ctx.probe(G.PROBE_OFF)
+            mac = {k: round(w["ms"] / max(2, args.steps), 3) for k, w in per.items() if k.startswith("k_bsgs_mac")}
+            ip = round(per.get("k_ks_ip_mma", {}).get("ms", 0.0) / max(2, args.steps), 3)
+            res[name] = {"ms_per_step": round(e0.elapsed_time(e1) / max(2, args.steps), 3), "mac_ms_per_step": mac,
+                         "baby_ip_ms_per_step": ip, "same_bits": bool(torch.equal(bits, ref))}
+    finally:
+        G.set_option("mac_tc", old)
+    return res
 
 
 def bench_e2e_client(G, ctx, model, prob, B, work, args, device):

@@ -132,6 +132,13 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
                             ckks_ctx** out);
 void ckks_ctx_destroy(ckks_ctx* ctx);
 ckks_status ckks_ctx_info(const ckks_ctx* ctx, ckks_info* out);
+/* Process-wide kernel selection for measured A/B runs (not a precision or semantics switch: every choice gives
+ * the same bits).  "mac_tc": 1 = the BSGS inner sums of double-hoisted layers on the integer tensor cores
+ * (tcgen05.mma kind::i8, TMEM accumulators, TMA operand staging; k_mac_tc.cu), 0 = on the FP64 tensor cores
+ * (DMMA, the default: faster in the measured A/B).  Takes effect for launches issued
+ * after the call.  CKKS_E_PARAM for an unknown name or value. */
+ckks_status ckks_set_option(const char* name, int64_t value);
+ckks_status ckks_get_option(const char* name, int64_t* value);
 /* Number of kernels this context has launched so far (bench accounting). */
 uint64_t ckks_launch_count(const ckks_ctx* ctx);
 /* Measurement probe: from now on record a CUDA event pair, on the launching stream, around every

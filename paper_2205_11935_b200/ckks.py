@@ -73,6 +73,8 @@ SIGNATURES = {
     "ckks_ctx_destroy": (None, [_VP]),
     "ckks_ctx_info": (_I, [_VP, ctypes.POINTER(ckks_info)]),
     "ckks_launch_count": (_U64, [_VP]),
+    "ckks_set_option": (_I, [ctypes.c_char_p, _I64]),
+    "ckks_get_option": (_I, [ctypes.c_char_p, ctypes.POINTER(_I64)]),
     "ckks_ntt_fwd": (_I, [_VP, _VP, _U32, _U32, _VP]),
     "ckks_ntt_inv": (_I, [_VP, _VP, _U32, _U32, _VP]),
     "ckks_rotate": (_I, [_VP, _PCT, _I, _PCT, _VP]),
@@ -652,6 +654,17 @@ class ForwardGraph:
             except Exception:
                 pass
             self.h = None
+
+
+def set_option(name, value):
+    """ckks_set_option: process-wide kernel selection for A/B runs ("mac_tc": integer tensor-core BSGS MAC)."""
+    _check(lib().ckks_set_option(name.encode(), int(value)), "ckks_set_option")
+
+
+def get_option(name):
+    v = _I64()
+    _check(lib().ckks_get_option(name.encode(), ctypes.byref(v)), "ckks_get_option")
+    return v.value
 
 
 def bsgs_plan(rows, cols, x=0):

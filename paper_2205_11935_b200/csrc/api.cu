@@ -426,7 +426,7 @@ void rotate_hoisted_impl(ckks_ctx* c, const u64* in, size_t in_stride, int nl, i
 // Double hoisting (R11c) baby steps: hoisted rotations of a Q_l input left in the Q_l P basis,
 // out_s = sigma_g(P c0 + sum_j D_j key'_j) over nl+1 limbs; batch <= max_batch.
 void rotate_hoisted_qp_impl(ckks_ctx* c, const u64* in, size_t in_stride, int nl, int B, const int64_t* steps,
-                            int n_steps, u64* const* outs, size_t out_stride, void* stream)
+                            int n_steps, u64* const* outs, size_t out_stride, void* stream, bool mac_layout = false)
 {
     auto L = c->launch(stream);
     for (int s = 0; s < n_steps; ++s) {
@@ -442,12 +442,14 @@ void rotate_hoisted_qp_impl(ckks_ctx* c, const u64* in, size_t in_stride, int nl
     auto flush = [&]() {
         if (!grp.G) return;
         ck::KsOut ko{nullptr, out_stride, in, in_stride, 0, 0, 0};
+        ko.mac_layout = mac_layout ? 1 : 0;
         ck::keyswitch_finish_qp(L, ki, grp, B, nl, w, ko, true);
         grp.G = 0;
     };
     for (int s = 0; s < n_steps; ++s) {
         const uint32_t g = c->galois(steps[s]);
         if (g == 1) {
+            if (mac_layout) throw CkksError(CKKS_E_PARAM, "MAC layout with an identity baby step");
             ck::lift_qp(L, in, in_stride, outs[s], out_stride, B, nl);
             continue;
         }
@@ -935,6 +937,27 @@ ckks_status ckks_ctx_info(const ckks_ctx* c, ckks_info* o)
 
 uint64_t ckks_launch_count(const ckks_ctx* c) { return c ? c->launches : 0; }
 
+ckks_status ckks_set_option(const char* name, int64_t value)
+{
+    if (!name) return fail(CKKS_E_PARAM, "null option name");
+    if (std::strcmp(name, "mac_tc") == 0) {
+        if (value != 0 && value != 1) return fail(CKKS_E_PARAM, "mac_tc is 0 or 1");
+        ck::set_mac_tc((int)value);
+        return CKKS_OK;
+    }
+    return fail(CKKS_E_PARAM, std::string("unknown option ") + name);
+}
+
+ckks_status ckks_get_option(const char* name, int64_t* value)
+{
+    if (!name || !value) return fail(CKKS_E_PARAM, "null");
+    if (std::strcmp(name, "mac_tc") == 0) {
+        *value = ck::get_mac_tc();
+        return CKKS_OK;
+    }
+    return fail(CKKS_E_PARAM, std::string("unknown option ") + name);
+}
+
 uint64_t ckks_galois_elt(const ckks_ctx* c, int32_t step) { return c ? c->galois(step) : 0; }
 
 static ckks_status ntt_impl(ckks_ctx* c, uint64_t* d, uint32_t batch, uint32_t limbs, void* stream, bool inv)
@@ -1406,9 +1429,16 @@ static void matvec_chunk(ckks_ctx* c, const ckks_layer* ly, const u64* in, size_
             steps.push_back((int64_t)ly->baby[j]);
             outs.push_back(baby + (size_t)(j - 1) * B * ctq);
         }
+        // the tensor-core MAC reads the baby steps in its own layout, which the tensor-core baby-step inner
+        // product writes: used when every baby-step group of KS_GMAX rotations has >= 2 members and no baby step
+        // is the identity
+        bool mac_layout = ck::bsgs_mac_tc_enabled(L, (int)ly->t1, B) && (steps.size() % KS_GMAX) != 1;
+        for (int64_t st : steps) mac_layout = mac_layout && c->galois(st) != 1;
         if (!steps.empty())
-            rotate_hoisted_qp_impl(c, in, in_stride, nl, B, steps.data(), (int)steps.size(), outs.data(), ctq, stream);
-        ck::bsgs_mac(L, ly->d_pts, nl + c->ns, in, in_stride, baby, Wk, (int)ly->t1, (int)ly->t2, B, nl, true);
+            rotate_hoisted_qp_impl(c, in, in_stride, nl, B, steps.data(), (int)steps.size(), outs.data(), ctq, stream,
+                                   mac_layout);
+        ck::bsgs_mac(L, ly->d_pts, nl + c->ns, in, in_stride, baby, Wk, (int)ly->t1, (int)ly->t2, B, nl, true,
+                     mac_layout);
         for (uint32_t k = 1; k < ly->t2; ++k)
             rotate_qp_impl(c, Wk + (size_t)k * B * ctq, ctq, nl, B, (int64_t)k * ly->giant, Wk, ctq, stream);
         ck::moddown_qp(L, Wk, ctq, B, nl, c->ks_work(B), md, ctw);

@@ -60,7 +60,7 @@ template <int NL, bool INT>
 __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64* __restrict__ modup,
                                          const u64* __restrict__ in, size_t ct_stride, size_t comp_off,
                                          const KsGroup& grp, int nl, size_t out_stride, int B, u64* sm,
-                                         int i, int cblk)
+                                         int i, int cblk, int mac_layout)
 {
     constexpr int NLP = Ip2Shape<NL>::NLP, JS = Ip2Shape<NL>::JS, SD = Ip2Shape<NL>::SD;
     constexpr int KPW = IP2_KT / (IP2_THREADS / 32);       // coefficients per warp
@@ -114,7 +114,10 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
     ip2_commit();
     // sigma_g store addressing, fixed for the whole launch: the destination block of rotation g (shared by
     // the CTA) and this thread's source index within it (4 bits per g, packed)
-    const int wt = tid % IP2_KT, wr = tid / IP2_KT;        // write phase: word wt of rows wr, wr + 16
+    // write phase: word wt of rows wr.  MAC layout (k_mac_tc.cu: per baby step [c][row][x/4][b][x%4]): a warp
+    // writes 4 coefficients x 8 ciphertexts = 256 contiguous bytes; else rows of 16 coefficients
+    const int wt = mac_layout ? ((tid >> 6) << 2) | (tid & 3) : tid % IP2_KT;
+    const int wr = mac_layout ? (tid >> 2) & 15 : tid / IP2_KT;
     u32 spk = 0;
     for (int g = 0; g < G; ++g) {
         const u32 gp = grp.scatter[g];
@@ -124,9 +127,12 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
             sidx = galois_src(dblk * IP2_KT + wt, gp, logn) - k0;
         }
         spk |= (u32)sidx << (4 * g);
-        if (tid == 0) Ob[g] = grp.out[g] + (size_t)i * n + (size_t)dblk * IP2_KT;
+        if (tid == 0)
+            Ob[g] = mac_layout ? grp.out[g] + ((size_t)i * (n / 4) + (size_t)dblk * (IP2_KT / 4)) * (4 * (size_t)B)
+                               : grp.out[g] + (size_t)i * n + (size_t)dblk * IP2_KT;
     }
-    const size_t wlimb = (size_t)ne * n;                   // component stride of an output ciphertext
+    // component stride of an output ciphertext (MAC layout: of the baby step's whole batch)
+    const size_t wlimb = mac_layout ? (size_t)ne * n * B : (size_t)ne * n;
 #pragma unroll
     for (int s = 0; s < IP2_ST - 1; ++s) {
         if (s < nbt) fill(s);
@@ -234,7 +240,9 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
                         const double k1 = __fma_rn(mid, c23q, CK_RND_MAGIC) - CK_RND_MAGIC;
                         const double t1 = __fma_rn(-k1, q, mid * 8388608.0);
                         const double t2 = fmodmul(s2, w46, w46q, q);
-                        const u64 u = d2s(freduce(t2 + t1 + (s0 + add), q, qinv));
+                        double r = freduce(t2 + t1 + (s0 + add), q, qinv);   // [-q/2, q/2]
+                        r = r < 0.0 ? r + q : r;                             // canonical: the byte-plane MAC
+                        const u64 u = d2u(r);
                         if (g < G) Os[((g * 2 + c) * 16 + bl) * IP2_KT + (kk ^ ((bl + 4 * g) & 15))] = u;
                     }
             }
@@ -308,15 +316,13 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
                         // pre-reductions: s_hh < 2^48 goes straight into the exact fmodmul by 2^46 mod q;
                         // mid < 2^51: k1 = rint(mid 2^23 / q), mid 2^23 - k1 q is exact in one FMA (the
                         // scaling by 2^23 is exact and the true remainder is < 1.5 q); s_ll < 2^51; the
-                        // signed sum (with the addend) stays < 2^52.  FP-class baby-step outputs are
-                        // stored as SIGNED representatives in [-q/2, q/2] (two's complement words): their
-                        // only consumer, the BSGS MAC, splits them with an arithmetic shift, which saves the
-                        // canonicalisation here.
+                        // signed sum (with the addend) stays < 2^52.  Outputs are canonical (the byte-plane
+                        // BSGS MAC reads the residue words as unsigned bytes).
                         const double s0 = S[0][t][e], s2 = S[2][t][e], mid = S[1][t][e] - s2 - s0;
                         const double k1 = __fma_rn(mid, c23q, CK_RND_MAGIC) - CK_RND_MAGIC;
                         const double t1 = __fma_rn(-k1, q, mid * 8388608.0);
                         const double t2 = fmodmul(s2, w46, w46q, q);
-                        u = d2s(freduce(t2 + t1 + (s0 + (double)add), q, qinv));
+                        u = fcanon(t2 + t1 + (s0 + (double)add), q, qinv);
                     } else {
                         const double P0 = S[0][t][e], P1 = S[1][t][e], P2 = S[2][t][e];
                         const u64 s0 = d2u(P0), s1 = d2u(S[3][t][e] - P0 - P1), s2 = d2u(S[5][t][e] - P0 - P2 + P1),
@@ -336,7 +342,8 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
         {
             const int b = bt * 16 + wr;
             if (b < B) {
-                const size_t boff = (size_t)b * out_stride + wt;
+                const size_t boff = mac_layout ? (size_t)(wt >> 2) * 4 * B + (size_t)b * 4 + (wt & 3)
+                                               : (size_t)b * out_stride + wt;
 #pragma unroll
                 for (int g = 0; g < 8; ++g) {
                     if (g < G) {
@@ -362,20 +369,20 @@ __device__ __forceinline__ void ip2_body(const DCtx* __restrict__ dc, const u64*
 template <int NL>
 __global__ void __launch_bounds__(IP2_THREADS, 2)
 k_ks_ip_mma2(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u64* __restrict__ in, size_t ct_stride,
-             size_t comp_off, const KsGroup grp, int nl, size_t out_stride, int B)
+             size_t comp_off, const KsGroup grp, int nl, size_t out_stride, int B, int mac_layout)
 {
     extern __shared__ u64 sm[];
     // (tried: rows fastest, so CTAs of both classes share an SM at the same time -- 150 vs 147.5 ms per step)
     const int i = blockIdx.y, cblk = blockIdx.x;
     const u64 q = dc->p[ext_prime_of(i, nl, dc->n_data)].q;
     if (prime_class(q) == PC_FP)
-        ip2_body<NL, false>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm, i, cblk);
-    else ip2_body<NL, true>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm, i, cblk);
+        ip2_body<NL, false>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm, i, cblk, mac_layout);
+    else ip2_body<NL, true>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm, i, cblk, mac_layout);
 }
 
 // host launcher: both prime classes of a baby-step group (scatter outputs, addend P c0, no accumulation)
 void ip_mma_pipelined(const Launch& L, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
-                      size_t out_stride)
+                      size_t out_stride, bool mac_layout)
 {
     const int n = 1 << L.log_n, ne = nl + L.n_special, nd = L.active_digits(nl);
     const dim3 grid(n / IP2_KT, ne);
@@ -399,7 +406,7 @@ void ip_mma_pipelined(const Launch& L, const KsIn& in, const KsGroup& grp, int b
         allow_smem(k_ks_ip_mma2<V>, smem);                                                                            \
         ProbeScope ps_(L.probe, L.st, "k_ks_ip_mma");                                                                 \
         k_ks_ip_mma2<V><<<grid, IP2_THREADS, smem, L.st>>>(L.dc, w.modup, in.base, in.ct_stride, in.comp_off, grp,   \
-                                                         nl, out_stride, batch);                                      \
+                                                         nl, out_stride, batch, mac_layout ? 1 : 0);                  \
     } break;
     switch (nd) {
         IP2_CASE(1) IP2_CASE(2) IP2_CASE(3) IP2_CASE(4) IP2_CASE(5) IP2_CASE(6) IP2_CASE(7) IP2_CASE(8)

@@ -108,9 +108,10 @@ void keyswitch_finish_qp(const Launch& L, const KsIn& in, const KsGroup& grp, in
         return;
     }
     if (baby && use_mma && grp.G >= 2 && out.add == in.base && !out.accumulate) {
-        ip_mma_pipelined(L, in, grp, batch, nl, w, out.ct_stride);
+        ip_mma_pipelined(L, in, grp, batch, nl, w, out.ct_stride, out.mac_layout != 0);
         return;
     }
+    if (out.mac_layout) throw std::runtime_error("keyswitch_finish_qp: MAC layout needs the tensor-core IP path");
     ip_qp(L, in, grp, batch, nl, w, out, baby, bbv, spl);
     check_launch("keyswitch_finish_qp");
     if (L.counter) *L.counter += 1;

@@ -411,8 +411,13 @@ static size_t mac_mma_smem(int t1)
 }
 
 void bsgs_mac(const Launch& L, const uint64_t* pts, int pt_nl, const uint64_t* v0, size_t v0_stride,
-              const uint64_t* vbaby, uint64_t* wout, int t1, int t2, int batch, int nl, bool qp)
+              const uint64_t* vbaby, uint64_t* wout, int t1, int t2, int batch, int nl, bool qp, bool mac_layout)
 {
+    if (mac_layout) {   // double-hoisted baby steps in the tensor-core MAC layout (the producer checked the shape)
+        if (!bsgs_mac_tc(L, pts, pt_nl, v0, v0_stride, vbaby, wout, t1, t2, batch, nl))
+            throw std::runtime_error("bsgs_mac: MAC layout without the tensor-core MAC");
+        return;
+    }
     const int nlx = nl + (qp ? L.n_special : 0);
     if (batch <= 0) return;
     const int n = 1 << L.log_n;
@@ -420,6 +425,7 @@ void bsgs_mac(const Launch& L, const uint64_t* pts, int pt_nl, const uint64_t* v
         const char* e = getenv("CKKS_MAC_MMA");
         return e ? atoi(e) : 1;
     }();
+
     if (use_mma && t1 <= 256 && n >= MACM_XT) {
         if (L.probe && L.probe->kind == PROBE_ALL) {
             // per row: B x 2 components x t1 x t2 x N modular MACs, 3 (FP class) or 6 (60-bit) exact

@@ -91,6 +91,7 @@ struct KsOut {
     uint32_t add_galois;      // apply sigma_g to the addend on load
     int add_comp1;            // add component 1 of the addend as well (relinearize)
     int accumulate;           // out += result (giant-step accumulation)
+    int mac_layout = 0;       // double-hoisted baby steps written in the tensor-core MAC layout (k_mac_tc.cu)
 };
 struct KsWork {
     uint64_t* digits;         // [B][nl][N]  digit coefficients (2-prime digits: (a, t) CRT pairs, R9b)
@@ -122,7 +123,7 @@ void keyswitch_finish_qp(const Launch&, const KsIn& in, const KsGroup& grp, int 
 // the baby-step (scatter, addend P c0) QP inner product of a group on the FP64 tensor cores, pipelined
 // over the batch (k_ipmma.cu); CKKS_IP_MMA=0 selects the IMAD kernel k_ks_ip_qp
 void ip_mma_pipelined(const Launch&, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
-                      size_t out_stride);
+                      size_t out_stride, bool mac_layout = false);
 // the giant-step (G = 1, accumulate, addend sigma_g(w.c0)) QP inner product, key-stationary over the
 // batch (k_ipgiant.cu); CKKS_IP_GIANT=0 selects the per-ciphertext-pair kernel k_ks_ip_qp
 void ip_giant(const Launch&, const uint64_t* key, int batch, int nl, const KsWork& w, uint64_t* acc,
@@ -170,7 +171,16 @@ void add(const Launch&, const uint64_t* a, size_t sa, const uint64_t* b, size_t 
          int batch, int ncomp, int nl);
 // pts [t][pt_nl][N]; qp: v/w in the Q_l P basis (nl+1 limbs, the last mod P), v0 (Q_l) lifted by P on load
 void bsgs_mac(const Launch&, const uint64_t* pts, int pt_nl, const uint64_t* v0, size_t v0_stride,
-              const uint64_t* vbaby, uint64_t* wout, int t1, int t2, int batch, int nl, bool qp);
+              const uint64_t* vbaby, uint64_t* wout, int t1, int t2, int batch, int nl, bool qp, bool mac_layout = false);
+// the same inner sums on the integer tensor cores (tcgen05 kind::i8, k_mac_tc.cu) for double-hoisted baby
+// steps stored in the MAC layout: per baby step j >= 1, words [c][row][x / 4][b][x % 4] (contiguous over the
+// batch, so a TMA box of 4 coefficients x 64 ciphertexts is one 2 KB row); false = shape not supported
+bool bsgs_mac_tc(const Launch&, const uint64_t* pts, int pt_nl, const uint64_t* v0, size_t v0_stride,
+                 const uint64_t* vbaby, uint64_t* wout, int t1, int t2, int batch, int nl);
+// whether the tensor-core MAC (and so the MAC layout of the baby steps) is used for this shape
+bool bsgs_mac_tc_enabled(const Launch&, int t1, int batch);
+void set_mac_tc(int on);
+int get_mac_tc();
 void decrypt(const Launch&, const uint64_t* ct, size_t ct_stride, const uint64_t* s_ntt, uint64_t* out, int batch, int nl);
 
 // client side on the device (k_encode.cu, f-4): canonical-embedding encode of values [batch][count] (row stride

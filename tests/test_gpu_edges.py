@@ -90,8 +90,9 @@ def test_smallest_ring_forward_to_level0():
     assert np.array_equal(u64(out.data)[0], ref.data)
 
 
+@pytest.mark.parametrize("mac_tc", [0, 1])
 @pytest.mark.parametrize("data_bits", [(60, 44, 44), (60, 40, 40)])
-def test_bsgs_mac_worst_case_residues(data_bits):
+def test_bsgs_mac_worst_case_residues(data_bits, mac_tc):
     """Exactness bounds of the tensor-core BSGS inner sums and baby-step inner products: every
     ciphertext residue q-1 and every diagonal the constant -1 (all NTT values q-1), so every split
     partial sum is at its maximum.  t = 512 with one extra baby-step doubling (t1 = 64, t2 = 8): for
@@ -114,7 +115,12 @@ def test_bsgs_mac_worst_case_residues(data_bits):
         data[:, :, i, :] = np.uint64(o.primes[i] - 1)
     data[1, 1, :, ::3] = 0                                          # second ciphertext: a mix with zeros
     ct = G.Ciphertext(torch.from_numpy(data.view(np.int64)).cuda(), level, 2.0 ** 30)
-    out = gl.matvec(ct)
+    old = G.get_option("mac_tc")
+    G.set_option("mac_tc", mac_tc)           # also the integer tensor-core MAC: T_s sums at their bound
+    try:
+        out = gl.matvec(ct)
+    finally:
+        G.set_option("mac_tc", old)
     for b in range(2):
         ref = OC.matvec(o, OC.Ct(data[b].copy(), 2.0 ** 30), lay, hoisted=2)
         assert np.array_equal(u64(out.data)[b], ref.data), (data_bits, b)

@@ -167,3 +167,32 @@ def test_guard_bands_and_repeatability_bench_shape():
         assert bool((obuf[:guard] == -1).all()) and bool((obuf[guard + no:] == -1).all())
     assert all(np.array_equal(runs[0], r) for r in runs[1:])
     check(runs[0], out, OP.oracle_forwards(spec, [0, 15, 16, 31, 32]))
+
+
+@pytest.fixture
+def mac_tc():
+    """The integer tensor-core BSGS MAC (tcgen05 kind::i8, ckks_set_option("mac_tc", 1)) for one test."""
+    old = G.get_option("mac_tc")
+    G.set_option("mac_tc", 1)
+    yield
+    G.set_option("mac_tc", old)
+
+
+@pytest.mark.parametrize("activation", ["square", "cubic"])
+def test_mac_tensor_core_int8_every_ciphertext(mac_tc, activation):
+    """The tcgen05 kind::i8 byte-plane MAC (k_mac_tc.cu) with the baby steps in its layout: max_batch = 130
+    (a full and a ragged 128-row M tile), B = 135, t1 = 64 / 32 (8 / 4 TMA stages), every ciphertext vs the
+    oracle, the same bits as the FP64 tensor-core path."""
+    B, mb = 135, 130
+    spec = {"kind": "dense", "cfg": SMALL, "batch": B, "activation": activation, "hoisting": 2, "x": 1}
+    _, got, out = gpu_forward(spec, B, mb)
+    check(got, out, OP.oracle_forwards(spec, range(B)))
+
+
+def test_mac_tensor_core_int8_cfg4_and_hybrid(mac_tc):
+    """The tcgen05 MAC at full size on the hybrid chain (R29: 60-bit row = 8 bytes / 15 shift classes, 40-bit
+    rows 5 / 9): B = 260 (M tiles 128, 128, 4), sampled ciphertexts vs the oracle."""
+    B, mb = 260, 256
+    spec = {"kind": "dense", "cfg": S.CFG4_HYBRID, "batch": B, "activation": "square", "hoisting": 2, "x": 1}
+    _, got, out = gpu_forward(spec, B, mb)
+    check(got, out, OP.oracle_forwards(spec, [0, 127, 128, 255, 256, 259]))

@@ -204,13 +204,14 @@ int main()
 {
     bool ok = true;
     ok &= check<16, 32>(1);
-    ok &= check<72, 320>(1);
+    ok &= check<80, 320>(1);
     ok &= check<144, 64>(3);
     ok &= check<256, 128>(1);
-    ok &= check<40, 160>(2);
+    ok &= check<48, 160>(2);
     if (!ok) return 1;
     rate<144, 320>(2000);
     rate<256, 128>(4000);
-    rate<72, 320>(4000);
+    rate<80, 320>(4000);
+    rate<128, 512>(2000);
     return 0;
 }
