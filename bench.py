@@ -161,11 +161,14 @@ def pipe_peaks():
 
 
 def profiled_pipes(kernel):
-    """Pipe utilisation of `kernel` from its committed ncu --set full capture (profiles/r01/ncu_final)."""
+    """Pipe utilisation of `kernel` from its committed ncu --set full capture (profiles/r02/ncu_hybrid, the
+    headline hybrid schedule, else profiles/r01/ncu_final)."""
     import csv
     tag = {"k_ks_ip_mma": "ipmma2", "k_bsgs_mac_mma": "macmma", "k_ks_modup": "modup",
            "k_ks_ip_giant": "ipgiant"}.get(kernel)
-    path = os.path.join(ROOT, "profiles", "r01", "ncu_final", f"prof_{tag}_raw.csv")
+    path = os.path.join(ROOT, "profiles", "r02", "ncu_hybrid", f"prof_{tag}_raw.csv")
+    if not os.path.exists(path):
+        path = os.path.join(ROOT, "profiles", "r01", "ncu_final", f"prof_{tag}_raw.csv")
     try:
         rows = list(csv.reader(open(path)))
         d = dict(zip(rows[0], rows[2]))

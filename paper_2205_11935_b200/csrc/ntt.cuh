@@ -6,12 +6,12 @@
 // the inverse runs the stages backwards with IW = psi^{-brev(.)} (Gentleman-Sande) and N^{-1}.
 //
 // B200 mapping.  One CTA owns one limb (N <= 16384 words = 128 KiB of shared memory).  Each of
-// NT threads holds E = N/NT residues in registers; a "pass" performs K = LOGE consecutive stages
-// entirely in registers on groups of 2^K elements (radix-2^K), so the limb crosses shared memory
-// only between passes (3 round trips for N=16384, NT=512).  The first forward pass loads straight
+// NT threads holds E = N/NT residues in registers; a "pass" performs K = LOGK = 4 consecutive stages
+// entirely in registers on groups of 16 elements (radix-16), so the limb crosses shared memory
+// only between passes (4 passes for N=16384).  The first forward pass loads straight
 // from the caller's loader (HBM, coalesced: lane <-> consecutive index), the last pass stores
 // straight through the caller's storer (each thread owns E contiguous words).  The inverse mirrors
-// this.  Shared memory is XOR-swizzled  a ^ ((a >> LOGE) & 15)  -- conflict-free (2 wavefronts per
+// this.  Shared memory is XOR-swizzled  a ^ (((a >> 4) ^ (a >> 5)) & 15)  -- conflict-free (2 wavefronts per
 // 64-bit warp access) for every pass of every supported (LOGN, NT), checked by
 // tests/test_ntt_layout.py.  Butterflies are Harvey-lazy: forward values live in [0, 4q), inverse
 // values in [0, 2q); loaders must supply values < 2q; storers receive canonical values in [0, q).
