@@ -945,6 +945,11 @@ ckks_status ckks_set_option(const char* name, int64_t value)
         ck::set_mac_tc((int)value);
         return CKKS_OK;
     }
+    if (std::strcmp(name, "ip_v3") == 0) {
+        if (value != 0 && value != 1) return fail(CKKS_E_PARAM, "ip_v3 is 0 or 1");
+        ck::set_ip_v3((int)value);
+        return CKKS_OK;
+    }
     return fail(CKKS_E_PARAM, std::string("unknown option ") + name);
 }
 
@@ -953,6 +958,10 @@ ckks_status ckks_get_option(const char* name, int64_t* value)
     if (!name || !value) return fail(CKKS_E_PARAM, "null");
     if (std::strcmp(name, "mac_tc") == 0) {
         *value = ck::get_mac_tc();
+        return CKKS_OK;
+    }
+    if (std::strcmp(name, "ip_v3") == 0) {
+        *value = ck::get_ip_v3();
         return CKKS_OK;
     }
     return fail(CKKS_E_PARAM, std::string("unknown option ") + name);

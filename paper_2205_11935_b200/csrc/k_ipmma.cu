@@ -400,6 +400,11 @@ void ip_mma_pipelined(const Launch& L, const KsIn& in, const KsGroup& grp, int b
             ((double)batch * nd * ne + (double)batch * nl + (double)grp.G * nd * 2 * ne + (double)grp.G * batch * 2 * ne) *
             n * 8.0;
     }
+    if (ip_mma3(L, in, grp, batch, nl, w, out_stride, mac_layout)) {   // k_ipmma3.cu (default for <= 5 digits)
+        check_launch("ip_mma3");
+        if (L.counter) *L.counter += 1;
+        return;
+    }
 #define IP2_CASE(V)                                                                                                  \
     case V: {                                                                                                         \
         const size_t smem = Ip2Shape<V>::smem;                                                                        \

@@ -124,6 +124,13 @@ void keyswitch_finish_qp(const Launch&, const KsIn& in, const KsGroup& grp, int 
 // over the batch (k_ipmma.cu); CKKS_IP_MMA=0 selects the IMAD kernel k_ks_ip_qp
 void ip_mma_pipelined(const Launch&, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
                       size_t out_stride, bool mac_layout = false);
+// the same inner product with the key pre-multiplied by 2^23 (FP rows) / 2^{20u} (60-bit rows): two / three
+// accumulators and one modular fold per output (k_ipmma3.cu); false when not applicable (> 5 digits, or
+// switched off by ckks_set_option("ip_v3", 0)) -- the caller then launches k_ks_ip_mma2
+bool ip_mma3(const Launch&, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
+             size_t out_stride, bool mac_layout);
+void set_ip_v3(int on);
+int get_ip_v3();
 // the giant-step (G = 1, accumulate, addend sigma_g(w.c0)) QP inner product, key-stationary over the
 // batch (k_ipgiant.cu); CKKS_IP_GIANT=0 selects the per-ciphertext-pair kernel k_ks_ip_qp
 void ip_giant(const Launch&, const uint64_t* key, int batch, int nl, const KsWork& w, uint64_t* acc,
