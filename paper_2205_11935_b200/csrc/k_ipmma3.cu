@@ -54,15 +54,25 @@ struct Ip3Shape {                                           // NL = active digit
 
 // word position of (b, k) in a [16 b][16 k] slice: 16-byte chunks (k, k^1) XOR-swizzled by b
 __device__ __forceinline__ int ip3_pos(int b, int k) { return b * 16 + (k ^ ((b & 7) << 1)); }
+// double2 position of (k index kidx, column n) in coefficient kk's block of the FP key tile: blocks of 4 K
+// indices [kb][n 16][kidx % 4] (the last block only KF - 4 kb wide), so the 8 lanes (gid, tig) of a quarter
+// warp read 8 consecutive 16-byte units (conflict-free LDS.128)
+template <int KF>
+__device__ __forceinline__ int ip3_kpos(int kk, int kidx, int n)
+{
+    const int kb = kidx >> 2, w = (KF - 4 * kb) < 4 ? (KF - 4 * kb) : 4;
+    return kk * KF * 16 + kb * 64 + n * w + (kidx & 3);
+}
 // column of B value (k index kidx, n) in the 60-bit key tile (two 8-word halves alternate with kidx)
 __device__ __forceinline__ int ip3_icol(int n, int kidx) { return (n + ((kidx & 1) << 3)) & 15; }
 
-template <int NL, bool INT>
+template <int NL, bool INT, bool MACL>
 __device__ __forceinline__ void ip3_body(const DCtx* __restrict__ dc, const u64* __restrict__ modup,
                                          const u64* __restrict__ in, size_t ct_stride, size_t comp_off,
                                          const KsGroup& grp, int nl, size_t out_stride, int B, u64* sm, int i,
-                                         int cblk, int mac_layout)
+                                         int cblk)
 {
+    constexpr int mac_layout = MACL ? 1 : 0;
     using S = Ip3Shape<NL>;
     constexpr int JS = S::JS, SD = S::SD;
     constexpr int KPW = IP3_KT / (IP3_THREADS / 32);        // coefficients per warp
@@ -116,9 +126,9 @@ __device__ __forceinline__ void ip3_body(const DCtx* __restrict__ dc, const u64*
         const u64 kv = (g < G) ? __ldg(grp.key[g] + ((size_t)j * 2 * np + (size_t)c * np + p) * n + k0 + kk) : 0;
         if constexpr (!INT) {
             const u64 kp = mulmod(kv, (1ULL << 23) % Pr.q, Pr);                 // K' = K 2^23 mod q
-            double2* d = reinterpret_cast<double2*>(Kw) + ((kk * S::KF + 2 * j) * 16 + r);
-            d[0] = make_double2((double)(kp & m23), (double)(kp >> 23));       // kidx 2j   (Dh): K'l, K'h
-            d[16] = make_double2((double)(kv & m23), (double)(kv >> 23));      // kidx 2j+1 (Dl): Kl, Kh
+            double2* d = reinterpret_cast<double2*>(Kw);
+            d[ip3_kpos<S::KF>(kk, 2 * j, r)] = make_double2((double)(kp & m23), (double)(kp >> 23));     // Dh: K'l, K'h
+            d[ip3_kpos<S::KF>(kk, 2 * j + 1, r)] = make_double2((double)(kv & m23), (double)(kv >> 23)); // Dl: Kl, Kh
         } else {
             const u64 w20 = (1ULL << 20) % Pr.q, w40 = mulmod(w20, w20, Pr);
             const u64 ku[3] = {kv, mulmod(kv, w20, Pr), mulmod(kv, w40, Pr)};
@@ -182,20 +192,18 @@ __device__ __forceinline__ void ip3_body(const DCtx* __restrict__ dc, const u64*
                         for (int e = 0; e < 4; ++e) Sa[kq][v][t][e] = 0.0;
 #pragma unroll
             for (int kb = 0; kb < NKB; ++kb) {
-                const int j = kj[kb], sh = ksh[kb];
+                const int sh = ksh[kb];
+                const bool live = kj[kb] >= 0;
+                const int j = live ? kj[kb] : NL;          // dead lanes read the c0 slice, times a zero B value
                 const u64 mk = sh ? ~0ULL : m23;
 #pragma unroll
                 for (int kq = 0; kq < KPW; ++kq) {
                     const int kk = warp * KPW + kq;
-                    u64 a0 = 0, a1 = 0;
-                    double2 b0 = make_double2(0.0, 0.0), b1 = b0;
-                    if (j >= 0) {
-                        a0 = Ds[j * JS + ip3_pos(gid, kk)];
-                        a1 = Ds[j * JS + ip3_pos(gid + 8, kk)];
-                        const int kidx = 4 * kb + tig;
-                        b0 = Kd[(kk * S::KF + kidx) * 16 + gid];
-                        b1 = Kd[(kk * S::KF + kidx) * 16 + 8 + gid];
-                    }
+                    const u64 a0 = Ds[j * JS + ip3_pos(gid, kk)];
+                    const u64 a1 = Ds[j * JS + ip3_pos(gid + 8, kk)];
+                    const int kidx = 4 * kb + tig;          // dead lanes' positions stay inside shared memory
+                    const double2 v0 = Kd[ip3_kpos<S::KF>(kk, kidx, gid)], v1 = Kd[ip3_kpos<S::KF>(kk, kidx, 8 + gid)];
+                    const double2 b0 = live ? v0 : make_double2(0.0, 0.0), b1 = live ? v1 : make_double2(0.0, 0.0);
                     const double x0 = p2d((a0 >> sh) & mk), x1 = p2d((a1 >> sh) & mk);
                     dmma16884(Sa[kq][0][0], x0, x1, b0.x);
                     dmma16884(Sa[kq][1][0], x0, x1, b0.y);
@@ -210,19 +218,25 @@ __device__ __forceinline__ void ip3_body(const DCtx* __restrict__ dc, const u64*
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
                     addd[h] = prow ? 0.0 : (double)csub(shoup_mul(As[ip3_pos(gid + 8 * h, kk)], Pm, Pm_sh, Pr.q), Pr.q);
+                // output (b = gid + 8 h, column 8 t + 2 tig + c) -> Os[(g = 4 t + tig, c)][b][kk ^ ((b + 4 g) & 15)]:
+                // two base addresses per thread (h), the (t, c) offsets are immediates
+                u64* ob[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    ob[h] = Os + (2 * tig * 16 + gid + 8 * h) * IP3_KT + (kk ^ ((gid + 8 * h + 4 * tig) & 15));
 #pragma unroll
                 for (int t = 0; t < 2; ++t)
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const int bl = gid + 8 * (e >> 1), g = 4 * t + tig, c = e & 1;
+                        const int c = e & 1;
                         // U = S0 + 2^23 S1 (+ P c0) mod q: |fmodmul| < 0.51 q, S0 < 2^50.6 -> |v| < 2^51
                         const double hi = fmodmul(Sa[kq][1][t][e], w23, w23q, q);
                         const double v = hi + (Sa[kq][0][t][e] + ((c == 0) ? addd[e >> 1] : 0.0));
                         const double r = freduce(v, q, qinv);                    // [-q/2, q/2]
                         // the DMMA BSGS MAC reads signed words (arithmetic-shift split); the byte-plane
-                        // tensor-core MAC needs canonical ones
-                        const u64 u = mac_layout ? d2u(r < 0.0 ? r + q : r) : d2s(r);
-                        if (g < G) Os[((g * 2 + c) * 16 + bl) * IP3_KT + (kk ^ ((bl + 4 * g) & 15))] = u;
+                        // tensor-core MAC needs canonical ones.  Rows g >= G are staged but never written out.
+                        const u64 u = MACL ? d2u(r < 0.0 ? r + q : r) : d2s(r);
+                        ob[e >> 1][(8 * t + c) * 16 * IP3_KT] = u;
                     }
             }
         } else {
@@ -272,7 +286,7 @@ __device__ __forceinline__ void ip3_body(const DCtx* __restrict__ dc, const u64*
                         lo += a2v;
                         hi += (lo < a2v ? 1 : 0);
                         const u64 u = addmod(reduce128(hi, lo, Pr), (c == 0) ? addw[e >> 1] : 0, Pr.q);
-                        if (g < G) Os[((g * 2 + c) * 16 + bl) * IP3_KT + (kk ^ ((bl + 4 * g) & 15))] = u;
+                        Os[((g * 2 + c) * 16 + bl) * IP3_KT + (kk ^ ((bl + 4 * g) & 15))] = u;
                     }
             }
         }
@@ -306,9 +320,14 @@ k_ks_ip_mma3(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u
     extern __shared__ __align__(16) u64 sm3[];
     const int i = blockIdx.y, cblk = blockIdx.x;
     const u64 q = dc->p[ext_prime_of(i, nl, dc->n_data)].q;
-    if (prime_class(q) == PC_FP)
-        ip3_body<NL, false>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm3, i, cblk, mac_layout);
-    else ip3_body<NL, true>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm3, i, cblk, mac_layout);
+    const bool fp = prime_class(q) == PC_FP;
+    if (mac_layout) {
+        if (fp) ip3_body<NL, false, true>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm3, i, cblk);
+        else ip3_body<NL, true, true>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm3, i, cblk);
+    } else {
+        if (fp) ip3_body<NL, false, false>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm3, i, cblk);
+        else ip3_body<NL, true, false>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm3, i, cblk);
+    }
 }
 
 // process-wide selection (ckks_set_option("ip_v3", ..)): 1 = this kernel for up to IP3_MAXD digits (default),
