@@ -8,6 +8,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "ntt.cuh"
+#include "ntt_c.cuh"
 
 #include <cuda_runtime.h>
 
@@ -566,7 +567,7 @@ static void sizes_impl(const ckks_params* p, size_t* tb, size_t* kb, size_t* wb,
         if (g != 1 && std::find(ids.begin(), ids.end(), g) == ids.end()) ids.push_back(g);
     }
     const size_t key_words = p->n_special ? (size_t)nd * 2 * np * n : 0;
-    *tb = align256(sizeof(DCtx)) + align256((size_t)np * 8 * n * 8) + embed_table_bytes(n);
+    *tb = align256(sizeof(DCtx)) + align256((size_t)np * CK_TW_WORDS * n * 8) + embed_table_bytes(n);
     // every switching key, plus a sigma_{g^-1}-permuted copy per key slot (used by hoisted rotations)
     *kb = align256((size_t)np * n * 8) + align256((size_t)2 * L * n * 8) + 2 * ids.size() * key_words * 8;
     const int B = (int)p->max_batch;
@@ -628,7 +629,7 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
         h.n_data = L;
         h.n_special = c->ns;
         h.n_primes = np;
-        std::vector<u64> tw((size_t)np * 8 * n);
+        std::vector<u64> tw((size_t)np * CK_TW_WORDS * n);
         for (int i = 0; i < np; ++i) {
             const u64 q = primes[i];
             const u64 psi = min_root(q, c->log_n), ipsi = h_pow(psi, q - 2, q);
@@ -643,7 +644,7 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
             P.r64_sh = h_shoup(P.r64, q);
             // W[idx] = psi^{brev(idx)} (stage s = floor(log2 idx), block idx - 2^s), stored at the
             // pass-ordered position ntt_tw_position (ntt.cuh); same for psi^{-1}.
-            u64* W = tw.data() + (size_t)i * 8 * n;
+            u64* W = tw.data() + (size_t)i * CK_TW_WORDS * n;
             std::vector<u64> fw(n), iw(n);
             u64 pw = 1, ipw = 1;
             for (int m = 0; m < n; ++m) {
@@ -674,6 +675,18 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
                 std::memcpy(&W[5 * n + pos], &wq, 8);
                 std::memcpy(&W[6 * n + pos], &iwd, 8);
                 std::memcpy(&W[7 * n + pos], &iwq, 8);
+            }
+            // pair tables of the cluster schedule (ntt_c.cuh): (w, fl(w/q)) at ntt_c_tw_position, forward then inverse
+            for (int idx = 1; idx < n && ntt_c_supported(c->log_n); ++idx) {
+                int s = 0;
+                while ((2 << s) <= idx) ++s;
+                const int pos = ntt_c_tw_position(c->log_n, s, idx - (1 << s));
+                const double wd = (double)fw[idx], iwd = (double)iw[idx];
+                const double wq = wd / (double)q, iwq = iwd / (double)q;
+                std::memcpy(&W[8 * n + 2 * pos], &wd, 8);
+                std::memcpy(&W[8 * n + 2 * pos + 1], &wq, 8);
+                std::memcpy(&W[10 * n + 2 * pos], &iwd, 8);
+                std::memcpy(&W[10 * n + 2 * pos + 1], &iwq, 8);
             }
             for (int b = 0; b < np; ++b) {
                 h.qmod[i][b] = q % primes[b];
@@ -743,7 +756,7 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
         // canonical embedding tables (R3): pos(i) = (5^i mod 2N - 1) / 4, zeta^k, omega^p in long double
         {
             const int ns = n / 2;
-            char* eb = tbase + align256(sizeof(DCtx)) + align256((size_t)np * 8 * n * 8);
+            char* eb = tbase + align256(sizeof(DCtx)) + align256((size_t)np * CK_TW_WORDS * n * 8);
             std::vector<u32> pos(ns);
             std::vector<double> zeta(2 * (size_t)ns), omega(ns);
             u64 e = 1;
@@ -950,6 +963,11 @@ ckks_status ckks_set_option(const char* name, int64_t value)
         ck::set_ip_v3((int)value);
         return CKKS_OK;
     }
+    if (std::strcmp(name, "ntt_q") == 0) {
+        if (value < 0 || value > 255) return fail(CKKS_E_PARAM, "ntt_q is a bit mask 0..255");
+        ck::set_ntt_q((int)value);
+        return CKKS_OK;
+    }
     return fail(CKKS_E_PARAM, std::string("unknown option ") + name);
 }
 
@@ -962,6 +980,10 @@ ckks_status ckks_get_option(const char* name, int64_t* value)
     }
     if (std::strcmp(name, "ip_v3") == 0) {
         *value = ck::get_ip_v3();
+        return CKKS_OK;
+    }
+    if (std::strcmp(name, "ntt_q") == 0) {
+        *value = ck::get_ntt_q();
         return CKKS_OK;
     }
     return fail(CKKS_E_PARAM, std::string("unknown option ") + name);

@@ -13,6 +13,9 @@ typedef uint64_t u64;
 typedef uint32_t u32;
 
 #define CKKS_MAXP 16
+// twiddle words per prime: W, W', IW, IW' (u64), Wd, Wq, IWd, IWq (double), then the pair tables
+// [N] x (w, w/q) of the cluster schedule, forward and inverse (ntt_c.cuh)
+#define CK_TW_WORDS 12
 
 struct DPrime {
     u64 q, q2;
@@ -30,7 +33,7 @@ struct DCtx {
     u64 qinv[CKKS_MAXP][CKKS_MAXP];     // q_a^{-1} mod q_b   (a != b)
     u64 qinv_sh[CKKS_MAXP][CKKS_MAXP];
     u64 qmod_sh[CKKS_MAXP][CKKS_MAXP];  // Shoup constants of qmod
-    const u64* tw;                      // [n_primes][4][N]: W, W', IW, IW'  (bit-reversed psi powers)
+    const u64* tw;                      // [n_primes][CK_TW_WORDS][N]  (bit-reversed psi powers)
     u64 cdt[40];                        // discrete Gaussian CDT thresholds (R13)
     int cdt_bound;
     // key switching (R9b, R10b, R17b): dnum digits of 1 or 2 consecutive data primes; P = the product of

@@ -29,31 +29,101 @@ k_ntt_batch(const DCtx* __restrict__ dc, u64* __restrict__ data, int limbs, int 
     else ntt_forward<T>(sm, Pr, twp(dc, p), ld, st);
 }
 
+// CTA-pair schedule (ntt_c.cuh) for FP64-class limbs: grid (limbs * CL, batch) in clusters of CL CTAs; IO = ST_BULK /
+// LD_BULK (TMA rows) or ST_DIRECT / LD_DIRECT (256-bit accesses)
+template <int LOGN, bool INV, int IO>
+__global__ void __launch_bounds__(NttC<LOGN>::NT, NttC<LOGN>::MINB)
+k_ntt_batch_c(const DCtx* __restrict__ dc, u64* __restrict__ data, int limbs, int prime0)
+{
+    extern __shared__ u64 sm[];
+    using TC = NttC<LOGN>;
+    const int l = blockIdx.x / TC::CL, h = blockIdx.x % TC::CL, b = blockIdx.y, p = prime0 + l;
+    u64* a = data + ((size_t)b * limbs + l) * TC::N;
+    const DPrime Pr = dc->p[p];
+    const bool r = prime_class(Pr.q) == PC_FPR;
+    if constexpr (INV) {
+        auto st = [&](int i, u64 v) { a[i] = v; };
+        if (r) TC::template inverse_fp<true, IO>(sm, h, Pr, twq_inv(dc, p), a, st);
+        else TC::template inverse_fp<false, IO>(sm, h, Pr, twq_inv(dc, p), a, st);
+    } else {
+        auto ld = [&](int i) { return a[i]; };
+        if (r) TC::template forward_fp<true, IO>(sm, h, Pr, twq_fwd(dc, p), ld, a);
+        else TC::template forward_fp<false, IO>(sm, h, Pr, twq_fwd(dc, p), ld, a);
+    }
+}
+
+static int g_ntt_q = [] {
+    const char* e = getenv("CKKS_NTT_Q");
+    return e ? atoi(e) : (int)NTTQ_DEFAULT;
+}();
+void set_ntt_q(int mask) { g_ntt_q = mask; }
+int get_ntt_q() { return g_ntt_q; }
+
+template <int LG, bool INV, int NTH>
+static void ntt_batch_run(const Launch& L, uint64_t* data, int batch, int limbs, int l0, int l1, int prime0, bool fp)
+{
+    // limbs [l0, l1) of every [limbs][N] block: the kernels take the block stride from `limbs`, so the run is
+    // addressed by offsetting the base pointer and prime0 and keeping gridDim.x = l1 - l0
+    uint64_t* base = data + ((size_t)l0 << LG);
+    if constexpr (LG >= 12) {
+        if (fp) {
+            using TC = NttC<LG>;
+            // TMA row copies (UBLKCP) for the forward's outputs at every N and for the inverse's inputs at
+            // N <= 8192 (cfg2 inverse at N = 16384: 1.059 ms with the bulk loads vs 1.028 ms with 256-bit loads;
+            // N = 8192: 0.129 vs 0.134 ms; forward 0.521 vs 0.530 ms at N = 16384, 0.115 vs 0.121 ms at N = 8192)
+            const bool direct = (g_ntt_q & NTTQ_DIRECT_IO) || (INV && LG == 14);
+            auto k = direct ? k_ntt_batch_c<LG, INV, ST_DIRECT> : k_ntt_batch_c<LG, INV, ST_BULK>;
+            allow_smem(k, TC::SMEM_ALL);
+            launch_cluster(k, dim3((l1 - l0) * TC::CL, batch), TC::NT, TC::SMEM_ALL, L.st, TC::CL, L.dc, base, limbs,
+                           prime0 + l0);
+            return;
+        }
+    }
+    auto k = k_ntt_batch<LG, INV, NTH>;
+    allow_smem(k, sizeof(u64) << LG);
+    k<<<dim3(l1 - l0, batch), NTH, sizeof(u64) << LG, L.st>>>(L.dc, base, limbs, prime0 + l0);
+}
+
 void ntt_batch(const Launch& L, uint64_t* data, int batch, int limbs, int prime0, bool inverse)
 {
     if (batch <= 0 || limbs <= 0) return;
-    const size_t smem = sizeof(u64) << L.log_n;
+    const double bytes = 2.0 * batch * limbs * (double)(8 << L.log_n);   // read + write each limb once
+    const bool pr = L.probe && L.probe->on(PROBE_NTT);
+    if (L.probe && L.probe->on(PROBE_ALL)) L.probe->bytes_by_kernel["k_ntt_batch"] += bytes;
+    if (pr) {
+        L.probe->mark(L.st);
+        L.probe->alg_bytes += bytes;
+    }
     NTT_DISPATCH(L.log_n, {
-        // threads per CTA: 16 residues per thread (NT), or 32 (NW): CKKS_NTT_WIDE bit 16 (forward, default
-        // on: cfg2 1.10 -> 1.04 ms) and bit 32 (inverse, default off: 1.27 vs 1.39 ms)
+        ProbeScope ps_(L.probe, L.st, "k_ntt_batch");
+        // threads per CTA of the whole-limb kernel: 16 residues per thread (NT0), or 32 (NW): CKKS_NTT_WIDE bit 16
+        // (forward, default on: cfg2 1.10 -> 1.04 ms) and bit 32 (inverse, default off: 1.27 vs 1.39 ms)
         constexpr int NT0 = NttThreads<LG>::value, NW = NttThreadsWide<LG>::value;
         const bool wide = (ntt_wide_mask() & (inverse ? 32 : 16)) != 0;
-        const int NT = wide ? NW : NT0;
-        auto k = wide ? (inverse ? k_ntt_batch<LG, true, NW> : k_ntt_batch<LG, false, NW>)
-                      : (inverse ? k_ntt_batch<LG, true, NT0> : k_ntt_batch<LG, false, NT0>);
-        allow_smem(k, smem);
-        const bool pr = L.probe && L.probe->on(PROBE_NTT);
-        if (L.probe && L.probe->on(PROBE_ALL))
-            L.probe->bytes_by_kernel["k_ntt_batch"] += 2.0 * batch * limbs * (double)(8 << L.log_n);
-        if (pr) {
-            L.probe->mark(L.st);
-            L.probe->alg_bytes += 2.0 * batch * limbs * (double)(8 << L.log_n);   // read + write each limb once
+        const bool cl = ntt_c_supported(LG) && (g_ntt_q & (inverse ? NTTQ_BATCH_INV : NTTQ_BATCH_FWD)) != 0;
+        // maximal runs of limbs of one kind: FP64-class limbs on the CTA-pair schedule (when selected), the rest
+        // (and everything when it is off) on the whole-limb kernel
+        for (int l0 = 0; l0 < limbs;) {
+            auto is_fp = [&](int l) {
+                const int c = L.pclass[prime0 + l];
+                return cl && (c == PC_FP || c == PC_FPR);
+            };
+            const bool fp = is_fp(l0);
+            int l1 = l0 + 1;
+            while (l1 < limbs && is_fp(l1) == fp) ++l1;
+            if (inverse) {
+                if (wide) ntt_batch_run<LG, true, NW>(L, data, batch, limbs, l0, l1, prime0, fp);
+                else ntt_batch_run<LG, true, NT0>(L, data, batch, limbs, l0, l1, prime0, fp);
+            } else {
+                if (wide) ntt_batch_run<LG, false, NW>(L, data, batch, limbs, l0, l1, prime0, fp);
+                else ntt_batch_run<LG, false, NT0>(L, data, batch, limbs, l0, l1, prime0, fp);
+            }
+            if (L.counter) ++*L.counter;
+            l0 = l1;
         }
-        { ProbeScope ps_(L.probe, L.st, "k_ntt_batch"); k<<<dim3(limbs, batch), NT, smem, L.st>>>(L.dc, data, limbs, prime0); }
-        if (pr) L.probe->mark(L.st);
     });
+    if (pr) L.probe->mark(L.st);
     check_launch("ntt_batch");
-    if (L.counter) ++*L.counter;
 }
 
 // ------------------------------------------------------------------------------------ rescale

@@ -2,6 +2,7 @@
 #pragma once
 #include "common.cuh"
 #include "ntt.cuh"
+#include "ntt_c.cuh"
 #include "kernels.h"
 #include <algorithm>
 #include <cstdlib>
@@ -11,7 +12,10 @@
 namespace ck {
 
 // ------------------------------------------------------------------------------------ helpers
-__device__ __forceinline__ const u64* twp(const DCtx* dc, int p) { return dc->tw + (size_t)p * 8 * dc->n; }
+__device__ __forceinline__ const u64* twp(const DCtx* dc, int p) { return dc->tw + (size_t)p * CK_TW_WORDS * dc->n; }
+// (w, w/q) pair tables of the cluster schedule (ntt_c.cuh): forward, inverse
+__device__ __forceinline__ const double2* twq_fwd(const DCtx* dc, int p) { return reinterpret_cast<const double2*>(twp(dc, p) + 8 * dc->n); }
+__device__ __forceinline__ const double2* twq_inv(const DCtx* dc, int p) { return reinterpret_cast<const double2*>(twp(dc, p) + 10 * dc->n); }
 
 // NTT-domain automorphism (R3): out[k] = in[src(k)] with 2 brev(src)+1 = g (2 brev(k)+1) mod 2N
 __device__ __forceinline__ int galois_src(int k, u32 g, int logn)
@@ -33,6 +37,26 @@ static void allow_smem(K kernel, size_t bytes)
     if (bytes > 48 * 1024) {
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     }
+}
+
+// launch with thread-block clusters of `cl` CTAs along x (grid.x is a multiple of cl)
+template <class... KA, class... A>
+static void launch_cluster(void (*kernel)(KA...), dim3 grid, int threads, size_t smem, cudaStream_t st, int cl, A... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KA>(args)...);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("cluster launch: ") + cudaGetErrorString(e));
 }
 
 // Threads per CTA of the batched NTT kernel (k_ntt_batch): bit 16 set = 32 residues per thread (N/32 threads)
