@@ -164,11 +164,14 @@ def profiled_pipes(kernel):
     """Pipe utilisation of `kernel` from its committed ncu --set full capture (profiles/r02/ncu_hybrid, the
     headline hybrid schedule, else profiles/r01/ncu_final)."""
     import csv
-    tag = {"k_ks_ip_mma": "ipmma2", "k_bsgs_mac_mma": "macmma", "k_ks_modup": "modup",
-           "k_ks_ip_giant": "ipgiant"}.get(kernel)
-    path = os.path.join(ROOT, "profiles", "r02", "ncu_hybrid", f"prof_{tag}_raw.csv")
-    if not os.path.exists(path):
-        path = os.path.join(ROOT, "profiles", "r01", "ncu_final", f"prof_{tag}_raw.csv")
+    tags = {"k_ks_ip_mma": ("ipmma3", "ipmma2"), "k_bsgs_mac_mma": ("macmma",), "k_ks_modup": ("modup2", "modup"),
+            "k_ks_ip_giant": ("ipgiant",)}.get(kernel, ())
+    path = ""
+    for sub in ("r02/final", "r02/s3", "r02/ncu_hybrid", "r01/ncu_final"):   # newest capture first
+        for tag in tags:
+            cand = os.path.join(ROOT, "profiles", *sub.split("/"), f"prof_{tag}_raw.csv")
+            if not path and os.path.exists(cand):
+                path = cand
     try:
         rows = list(csv.reader(open(path)))
         d = dict(zip(rows[0], rows[2]))
@@ -213,15 +216,25 @@ def tensor_roofline(name, per_kernel, ms_local, steps, pb, hbm_peak, hbm_src, br
     achieved = k["tensor_flops"] / sec / 1e12 if sec > 0 else 0.0
     tpeak = 2.0 * pb["dmma_fma_rate"] / 1e12
     hbm = k["alg_bytes"] / sec / 1e9 if sec > 0 else 0.0
-    r = {"bound": "tensor", "achieved": round(achieved, 2), "peak": round(tpeak, 2), "unit": "TFLOP/s",
-         "frac": round(achieved / tpeak, 4),
-         "hbm": {"achieved_GBps": round(hbm, 1), "peak_GBps": hbm_peak, "frac": round(hbm / hbm_peak, 4)},
-         "launches_probed": k["launches"], "share_of_step": round(k["ms"] / ms_local, 4) if ms_local else None}
+    # the binding roof is the one with the larger time floor (flops / tensor peak vs bytes / HBM peak), i.e. the
+    # larger of the two fractions; the other is reported beside it
+    tens = {"achieved_TFLOPs": round(achieved, 2), "peak_TFLOPs": round(tpeak, 2), "frac": round(achieved / tpeak, 4)}
+    hb = {"achieved_GBps": round(hbm, 1), "peak_GBps": hbm_peak, "frac": round(hbm / hbm_peak, 4)}
+    if hb["frac"] > tens["frac"]:
+        r = {"bound": "hbm", "achieved": hb["achieved_GBps"], "peak": hbm_peak, "unit": "GB/s", "frac": hb["frac"]}
+    else:
+        r = {"bound": "tensor", "achieved": tens["achieved_TFLOPs"], "peak": tens["peak_TFLOPs"], "unit": "TFLOP/s",
+             "frac": tens["frac"]}
+    r.update({"tensor": tens, "hbm": hb, "launches_probed": k["launches"],
+              "share_of_step": round(k["ms"] / ms_local, 4) if ms_local else None})
     if brief:
         return r
     r.update({"kernel": f"{name} ({KERNEL_DESC.get(name, '')})",
-              "peak_source": "measured FP64 tensor (DMMA m16n8k4) FMA rate x 2, profiles/r01/pipe_bench.json "
-                             "(the guide's nominal bf16:fp64 ratio applied to MEASURED_PEAKS bf16 gives a lower peak)",
+              "peak_source": (hbm_src if r["bound"] == "hbm" else
+                              "measured FP64 tensor (DMMA m16n8k4) FMA rate x 2, profiles/r01/pipe_bench.json"),
+              "bound_rule": "the roof with the larger time floor: algorithmic bytes / measured HBM rate vs split-product "
+                            "FLOPs / measured FP64 tensor rate (37.0 TFLOP/s, profiles/r01/pipe_bench.json; the guide's "
+                            "nominal bf16:fp64 ratio applied to MEASURED_PEAKS bf16 gives a lower tensor peak)",
               "flops_def": "2 x (3 split products per MAC for q < 2^45 rows, 6 for 60-bit rows) x modular MACs",
               "traffic": (profiled_traffic(name) or {}).get("dram_bytes_per_launch"),
               "traffic_detail": profiled_traffic(name), "ncu_pipes": profiled_pipes(name),

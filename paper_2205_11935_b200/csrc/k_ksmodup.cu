@@ -32,12 +32,18 @@ k_ks_modup(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* __r
         if constexpr (ALPHA == 1) return reduce64_lazy(src[i], Pr);
         else return crt2_lazy(dc, s0, src[i], src[T::N + i], Pr, p);
     };
+    // a < q_s0 < 2 q_p (primes of the same size): a itself is the lazy residue the transform accepts ([0, 2q))
+    auto ld_small = [&](int i) {
+        if constexpr (ALPHA == 1) return src[i];
+        else return csub(shoup_mul(src[T::N + i], dc->qmod[s0][p], dc->qmod_sh[s0][p], Pr.q) + src[i], Pr.q2);
+    };
 #if CK_STREAM_STORES
     auto st = [&](int i, u64 v) { __stcs(dst + i, v); };   // ModUp words: read once, by the next kernel
 #else
     auto st = [&](int i, u64 v) { dst[i] = v; };
 #endif
-    ntt_forward<T>(sm, Pr, twp(dc, p), ld, st);
+    if (dc->p[s0].q < Pr.q2) ntt_forward<T>(sm, Pr, twp(dc, p), ld_small, st);
+    else ntt_forward<T>(sm, Pr, twp(dc, p), ld, st);
 }
 
 // The same ModUp with the FP64-class target rows on the CTA-pair schedule (ntt_c.cuh): grid (CL * targets, B) in
@@ -67,8 +73,18 @@ k_ks_modup_c(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* _
         if constexpr (ALPHA == 1) return reduce64_lazy(src[i], Pr);
         else return crt2_lazy(dc, s0, src[i], src[TC::N + i], Pr, p);
     };
-    if (pc == PC_FP) TC::template forward_fp<false>(sm, h, Pr, twq_fwd(dc, p), ld, dst);
-    else TC::template forward_fp<true>(sm, h, Pr, twq_fwd(dc, p), ld, dst);
+    auto ld_small = [&](int i) {   // q_s0 < 2 q_p: see k_ks_modup
+        if constexpr (ALPHA == 1) return src[i];
+        else return csub(shoup_mul(src[TC::N + i], dc->qmod[s0][p], dc->qmod_sh[s0][p], Pr.q) + src[i], Pr.q2);
+    };
+    const bool small = dc->p[s0].q < Pr.q2;
+    if (pc == PC_FP) {
+        if (small) TC::template forward_fp<false>(sm, h, Pr, twq_fwd(dc, p), ld_small, dst);
+        else TC::template forward_fp<false>(sm, h, Pr, twq_fwd(dc, p), ld, dst);
+    } else {
+        if (small) TC::template forward_fp<true>(sm, h, Pr, twq_fwd(dc, p), ld_small, dst);
+        else TC::template forward_fp<true>(sm, h, Pr, twq_fwd(dc, p), ld, dst);
+    }
 }
 
 // integer-class target rows of a ModUp launch (with k_ks_modup_c): grid (set.count * rows.count, B)
