@@ -71,10 +71,11 @@ void keyswitch_modup(const Launch& L, const KsIn& in, int batch, int nl, const K
     launch_ks_modup(L, w.digits, w.modup, nl, qp_in, batch);
     if (pm) L.probe->mark(L.st);
     check_launch("keyswitch_modup");
-    if (L.counter) {   // digits and ModUp: one launch per digit size present
+    if (L.counter) {
         DigitSet one, two;
         digit_sets(L, nl, qp_in, one, two);
-        *L.counter += (qp_in ? 1 : 0) + 2 * ((one.count ? 1 : 0) + (two.count ? 1 : 0));
+        const int sizes = (one.count ? 1 : 0) + (two.count ? 1 : 0);
+        *L.counter += (qp_in ? 1 : 0) + 1 + sizes;   // digits: one launch (both sizes together), ModUp: one per size
     }
 }
 

@@ -22,8 +22,9 @@ k_ks_digits(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t ct_s
     const u64* r0 = QPK ? rem + (size_t)b * QPK * T::N : nullptr;
     const u64* r1 = QPK ? r0 + (size_t)(QPK - 1) * T::N : nullptr;
     u64* d0 = digits + ((size_t)b * nl + s0) * T::N;
+    const int alpha = ALPHA ? ALPHA : set.first[blockIdx.x];   // ALPHA = 0: digits of both sizes in one launch
 #pragma unroll 1
-    for (int h = 0; h < ALPHA; ++h) {
+    for (int h = 0; h < alpha; ++h) {
         const int pj = s0 + h;
         const u64* src = in + (size_t)b * ct_stride + comp_off + (size_t)pj * T::N;
         u64* dst = d0 + (size_t)h * T::N;
@@ -61,8 +62,28 @@ void launch_ks_digits(const Launch& L, const KsIn& in, int nl, int batch, uint64
     digit_sets(L, nl, false, one, two);
     ProbeScope ps_(L.probe, L.st, "k_ks_digits");
     const int qpk = rem ? L.n_special : 0;
+    // both digit sizes present: one launch (ALPHA = 0, the size per CTA in set.first) -- two launches of 2-5 CTAs
+    // per ciphertext each end in a partial wave (B = 256: 5.2 and 3.5 waves); two-prime digits first in the grid
+    DigitSet mix;
+    mix.count = 0;
+    if (one.count && two.count) {
+        for (int k = 0; k < two.count; ++k, ++mix.count) {
+            mix.j[mix.count] = two.j[k];
+            mix.s0[mix.count] = two.s0[k];
+            mix.first[mix.count] = 2;
+        }
+        for (int k = 0; k < one.count; ++k, ++mix.count) {
+            mix.j[mix.count] = one.j[k];
+            mix.s0[mix.count] = one.s0[k];
+            mix.first[mix.count] = 1;
+        }
+    }
     NTT_DISPATCH(L.log_n, {
-        if (qpk == 0) {
+        if (mix.count) {
+            if (qpk == 0) digits_launch<LG, 0, 0>(L, in, nl, batch, digits, rem, mix);
+            else if (qpk == 1) digits_launch<LG, 0, 1>(L, in, nl, batch, digits, rem, mix);
+            else digits_launch<LG, 0, 2>(L, in, nl, batch, digits, rem, mix);
+        } else if (qpk == 0) {
             digits_launch<LG, 1, 0>(L, in, nl, batch, digits, rem, one);
             digits_launch<LG, 2, 0>(L, in, nl, batch, digits, rem, two);
         } else if (qpk == 1) {
