@@ -667,9 +667,11 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
                 W[2 * n + pos] = iw[idx];
                 W[3 * n + pos] = h_shoup(iw[idx], q);
             }
-            // FP64 copies for PC_FP primes: w and fl(w / q), as raw double bits
+            // FP64 copies for the FP64-pipe classes: the centred representative w in (-q/2, q/2] and fl(w / q), as
+            // raw double bits (|w / q| <= 1/2 doubles the multiplicand range of fmodmul, ntt.cuh)
+            auto centred = [q](u64 w) { return w > q / 2 ? -(double)(q - w) : (double)w; };
             for (int pos = 0; pos < n; ++pos) {
-                const double wd = (double)W[pos], iwd = (double)W[2 * n + pos];
+                const double wd = centred(W[pos]), iwd = centred(W[2 * n + pos]);
                 const double wq = wd / (double)q, iwq = iwd / (double)q;
                 std::memcpy(&W[4 * n + pos], &wd, 8);
                 std::memcpy(&W[5 * n + pos], &wq, 8);
@@ -681,7 +683,7 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
                 int s = 0;
                 while ((2 << s) <= idx) ++s;
                 const int pos = ntt_c_tw_position(c->log_n, s, idx - (1 << s));
-                const double wd = (double)fw[idx], iwd = (double)iw[idx];
+                const double wd = centred(fw[idx]), iwd = centred(iw[idx]);
                 const double wq = wd / (double)q, iwq = iwd / (double)q;
                 std::memcpy(&W[8 * n + 2 * pos], &wd, 8);
                 std::memcpy(&W[8 * n + 2 * pos + 1], &wq, 8);

@@ -35,9 +35,11 @@ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x >> 1); }
 //   PC_FP     q < 2^45: residues held as exact integers in FP64 registers; butterflies on the
 //                       FP64 pipe (8 DFMA-class ops: error-free product + rint quotient), signed
 //                       representatives; forward needs no reduction, inverse reduces per pass
-//   PC_FPR    q < 2^50: FP64 pipe as PC_FP, one reduction per butterfly (11 FP64 ops): forward
-//                       reduces the X input to [-q/2, q/2] (every value stays < 1.5 q), inverse
-//                       reduces the sum output (every value < q) -- all products exact, |y w/q| < 2^51
+//   PC_FPR    q < 2^50: FP64 pipe as PC_FP with a few reductions (twiddles are centred, |w| <= q/2, so
+//                       fmodmul takes |y| < 2^52 ~ 4q): the forward reduces the X input of the first stage
+//                       of every pass (values < 3.7 q inside a pass of <= 5 stages: 8.6-8.75 FP64 ops per
+//                       butterfly), the inverse reduces every other stage's sums (values < 1.2 q, |u - v| <
+//                       2.3 q: 9.5 ops) -- bounds in DESIGN.md section 5
 //   PC_MID    q < 2^52: 64-bit integer Shoup, forward without reductions, inverse Harvey-lazy
 //   PC_BIG    q < 2^61: 64-bit integer Shoup, Harvey-lazy both ways ([0,4q) fwd, [0,2q) inv)
 // (key-switch inner products and BSGS sums treat every class but PC_FP as 60-bit: three-part splits)
@@ -50,7 +52,9 @@ __host__ __device__ __forceinline__ int prime_class(u64 q)
 // ---- FP64 modular arithmetic on exact integers (|values| < 2^51)
 #define CK_RND_MAGIC 6755399441055744.0   /* 1.5 * 2^52: x + M - M = rint(x) for |x| < 2^51 */
 #define CK_TWO52 4503599627370496.0
-// y * w mod q as a signed representative in (-0.51 q, 0.51 q); wq = fl(w / q)
+// y * w mod q as a signed representative; wq = fl(w / q), |w| <= q/2 (centred twiddles), |y| < 2^52:
+// |y wq| < 2^51 so k = rint(y wq) exactly, |y wq - y w / q| <= |y| 2^-54, so |result| <= (1/2 + |y| 2^-54) q
+// (< 0.51 q for |y| < 2^47, < 0.75 q always); ph - k q and the sum with pl are integers < 2^53: exact
 __device__ __forceinline__ double fmodmul(double y, double w, double wq, double q)
 {
     const double ph = y * w;
@@ -206,9 +210,9 @@ struct NttCta {
                     const double w = __ldg(Wd + m), wq = __ldg(Wq + m);
                     double& X = x[g * (1 << K) + i];
                     double& Y = x[g * (1 << K) + i + half];
-                    const double t = fmodmul(Y, w, wq, q);   // |t| < 0.51 q  (FPR: |Y| < 2 q, |t| <= q)
-                    const double xx = R ? freduce(X, q, qinv) : X;
-                    X = xx + t;                              // |.| grows by < 0.51 q per stage
+                    const double t = fmodmul(Y, w, wq, q);   // |t| < 0.51 q  (FPR: < (0.5 + |Y| / 16 q) q)
+                    const double xx = (R && r == 0) ? freduce(X, q, qinv) : X;
+                    X = xx + t;                              // |.| grows by < 0.51 q per stage (FPR: < 0.75 q)
                     Y = xx - t;
                 }
             }
@@ -241,7 +245,8 @@ struct NttCta {
                     double& X = x[g * (1 << K) + i];
                     double& Y = x[g * (1 << K) + i + half];
                     const double u = X, v = Y;
-                    X = R ? freduce(u + v, q, qinv) : u + v;
+                    // FPR: sums reduced at every other stage, counted from the first one executed (LOGN - 1)
+                    X = (R && ((LOGN - 1 - (G_::S0 + r)) & 1)) ? freduce(u + v, q, qinv) : u + v;
                     Y = fmodmul(u - v, w, wq, q);
                 }
             }
@@ -293,7 +298,7 @@ struct NttCta {
         const double q = (double)Pr.q, qinv = 1.0 / q;
         const double* IWd = reinterpret_cast<const double*>(tw + 6 * N);
         const double* IWq = reinterpret_cast<const double*>(tw + 7 * N);
-        const double ninv = (double)Pr.ninv, ninvq = ninv / q;
+        const double ninv = Pr.ninv > Pr.q / 2 ? -(double)(Pr.q - Pr.ninv) : (double)Pr.ninv, ninvq = ninv / q;
         double* smd = reinterpret_cast<double*>(sm);
         double x[E];
 #pragma unroll 4

@@ -139,7 +139,7 @@ struct NttC {
                     double& X = x[g * (1 << K) + i];
                     double& Y = x[g * (1 << K) + i + half];
                     const double tt = fmodmul(Y, w.x, w.y, q);
-                    const double xx = R ? freduce(X, q, qinv) : X;
+                    const double xx = (R && r == 0) ? freduce(X, q, qinv) : X;   // FPR: first stage of a pass
                     X = xx + tt;
                     Y = xx - tt;
                 }
@@ -171,7 +171,7 @@ struct NttC {
                     double& X = x[g * (1 << K) + i];
                     double& Y = x[g * (1 << K) + i + half];
                     const double u = X, v = Y;
-                    X = R ? freduce(u + v, q, qinv) : u + v;
+                    X = (R && ((LOGN - 1 - (S0g + r)) & 1)) ? freduce(u + v, q, qinv) : u + v;   // as ntt.cuh
                     Y = fmodmul(u - v, w.x, w.y, q);
                 }
             }
@@ -311,7 +311,7 @@ struct NttC {
     {
         const int t = threadIdx.x;
         const double q = (double)Pr.q, qinv = 1.0 / q;
-        const double ninv = (double)Pr.ninv, ninvq = ninv / q;
+        const double ninv = Pr.ninv > Pr.q / 2 ? -(double)(Pr.q - Pr.ninv) : (double)Pr.ninv, ninvq = ninv / q;
         double* smd = reinterpret_cast<double*>(sm);
         double x[E];
         if constexpr (LD == LD_BULK) {
