@@ -5,6 +5,7 @@
 //   key           [digit j][comp][prime 0..L+K-1][N]
 //   accumulator   [b][comp][row 0..nl+K-1][N]   (Q_l P), addend w [b][comp][row][N] (Q_l P)
 #include "kinternal.cuh"
+#include <cmath>
 
 namespace ck {
 
@@ -45,8 +46,11 @@ __device__ __forceinline__ void ipg_row(const DCtx* __restrict__ dc, const u64* 
     const int src = add_galois ? galois_src(k, add_galois, logn) : k;
     const size_t dstride = (size_t)ne * n;
     const u64* dbase = modup + (size_t)i * n + k;
+    // blockIdx.z = slice of the batch (the grid alone is 2.2 waves of CTAs at N = 16384, 10 rows)
+    const int bper = (B + gridDim.z - 1) / gridDim.z;
+    const int b_lo = blockIdx.z * bper, b_hi = min(B, b_lo + bper);
 #pragma unroll kIpgUnroll
-    for (int b = 0; b < B; ++b) {
+    for (int b = b_lo; b < b_hi; ++b) {
         const u64* d = dbase + (size_t)b * NL * dstride;
         u64 dv[NL];
 #pragma unroll
@@ -117,7 +121,24 @@ void ip_giant(const Launch& L, const uint64_t* key, int batch, int nl, const KsW
 {
     const int n = 1 << L.log_n;
     if (n % IPG_BLK) throw std::runtime_error("N >= 128 required");
-    const dim3 grid(n / IPG_BLK, nl + L.n_special);
+    // batch slices: the split (1, 2, 4 or 8, at least 16 ciphertexts each) whose CTA count fills its last wave best
+    static const int slots = [] {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return sms * IPG_MINB;
+    }();
+    int split = 1;
+    double best = 0.0;
+    for (int sp = 1; sp <= 8 && batch / sp >= 16; sp *= 2) {
+        const double waves = (double)(n / IPG_BLK) * (nl + L.n_special) * sp / slots;
+        const double eff = waves / std::ceil(waves);
+        if (eff > best + 0.02) {
+            best = eff;
+            split = sp;
+        }
+    }
+    const dim3 grid(n / IPG_BLK, nl + L.n_special, split);
 #define IPG_CASE(V)                                                                                                  \
     case V: {                                                                                                         \
         ProbeScope ps_(L.probe, L.st, "k_ks_ip_giant");                                                               \
