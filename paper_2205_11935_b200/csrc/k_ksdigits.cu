@@ -22,6 +22,7 @@ k_ks_digits(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t ct_s
     const u64* r0 = QPK ? rem + (size_t)b * QPK * T::N : nullptr;
     const u64* r1 = QPK ? r0 + (size_t)(QPK - 1) * T::N : nullptr;
     u64* d0 = digits + ((size_t)b * nl + s0) * T::N;
+    const u32 ginv = galois ? galois_inv(galois, LOGN) : 0;
     const int alpha = ALPHA ? ALPHA : set.first[blockIdx.x];   // ALPHA = 0: digits of both sizes in one launch
 #pragma unroll 1
     for (int h = 0; h < alpha; ++h) {
@@ -29,7 +30,8 @@ k_ks_digits(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t ct_s
         const u64* src = in + (size_t)b * ct_stride + comp_off + (size_t)pj * T::N;
         u64* dst = d0 + (size_t)h * T::N;
         const DPrime Pr = dc->p[pj];
-        auto ld = [&](int i) { return galois ? src[galois_src(i, galois, LOGN)] : src[i]; };
+        auto ld = [&](int i) { return src[i]; };
+        auto place = [&](int i) { return galois ? galois_dst(i, ginv, LOGN) : i; };   // sigma_g in the staging
         auto st = [&](int i, u64 v) {
             if constexpr (QPK > 0) {
                 const u64 r = QPK == 1 ? centered_to(r0[i], dc->p[dc->n_data].q, dc->pmod[pj], Pr)
@@ -39,7 +41,7 @@ k_ks_digits(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t ct_s
             if constexpr (ALPHA == 1) dst[i] = v;
             else dst[i] = (h == 0) ? v : crt2_t(dc, s0, d0[i], v);   // d0 written by this CTA (synchronised)
         };
-        ntt_inverse<T>(sm, Pr, twp(dc, pj), ld, st);
+        ntt_inverse<T>(sm, Pr, twp(dc, pj), ld, st, place);
     }
 }
 

@@ -15,17 +15,19 @@ k_ks_qp_rem(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t ct_s
     using T = NttCta<LOGN, NTH>;
     const int c = blockIdx.x, b = blockIdx.y, L = dc->n_data;
     u64* d0 = rem + ((size_t)b * gridDim.x + c) * K * T::N;
+    const u32 ginv = galois ? galois_inv(galois, LOGN) : 0;
 #pragma unroll 1
     for (int k = 0; k < K; ++k) {
         const u64* src = in + (size_t)b * ct_stride + comp_off + (size_t)c * comp_step + (size_t)(nl + k) * T::N;
         u64* dst = d0 + (size_t)k * T::N;
         const DPrime Pr = dc->p[L + k];
-        auto ld = [&](int i) { return galois ? src[galois_src(i, galois, LOGN)] : src[i]; };
+        auto ld = [&](int i) { return src[i]; };
+        auto place = [&](int i) { return galois ? galois_dst(i, ginv, LOGN) : i; };   // sigma_g in the staging
         auto st = [&](int i, u64 v) {
             if constexpr (K == 1) dst[i] = v;
             else dst[i] = (k == 0) ? v : crt2_t(dc, L, d0[i], v);
         };
-        ntt_inverse<T>(sm, Pr, twp(dc, L + k), ld, st);
+        ntt_inverse<T>(sm, Pr, twp(dc, L + k), ld, st, place);
     }
 }
 

@@ -25,6 +25,19 @@ __device__ __forceinline__ int galois_src(int k, u32 g, int logn)
     return (int)brev32((eg - 1u) >> 1, logn);
 }
 
+// g^{-1} mod 2N for an odd g (Newton: x <- x (2 - g x) doubles the correct low bits; g g = 1 mod 8)
+__device__ __forceinline__ u32 galois_inv(u32 g, int logn)
+{
+    u32 x = g;
+#pragma unroll
+    for (int it = 0; it < 4; ++it) x *= 2u - g * x;
+    return x & ((2u << logn) - 1u);
+}
+// sigma_g of an NTT-domain limb read in ITS OWN order: the value at index i belongs at k with galois_src(k, g) = i,
+// i.e. k = galois_src(i, g^{-1}) -- the staging of the whole-limb inverse NTTs scatters in shared memory instead of
+// gathering 8-byte words from global memory
+__device__ __forceinline__ int galois_dst(int i, u32 ginv, int logn) { return galois_src(i, ginv, logn); }
+
 static void check_launch(const char* what)
 {
     cudaError_t e = cudaGetLastError();

@@ -290,9 +290,17 @@ struct NttCta {
         __syncthreads();
     }
 
+    // place(idx) = the transform index the value ld(idx) belongs to (a permuted input read in its own order, so
+    // the global loads stay coalesced and the permutation happens in the shared-memory staging)
     template <bool R = false, class Load, class Store>
     __device__ __forceinline__ static void inverse_fp(u64* sm, const DPrime& Pr, const u64* __restrict__ tw,
                                                       Load&& ld, Store&& st)
+    {
+        inverse_fp<R>(sm, Pr, tw, ld, st, [](int i) { return i; });
+    }
+    template <bool R = false, class Load, class Store, class Place>
+    __device__ __forceinline__ static void inverse_fp(u64* sm, const DPrime& Pr, const u64* __restrict__ tw,
+                                                      Load&& ld, Store&& st, Place&& place)
     {
         const int tid = threadIdx.x;
         const double q = (double)Pr.q, qinv = 1.0 / q;
@@ -304,7 +312,7 @@ struct NttCta {
 #pragma unroll 4
         for (int c = 0; c < E; ++c) {
             const int idx = c * NT + tid;
-            smd[swz(idx)] = R ? freduce(u2d(ld(idx)), q, qinv) : u2d(ld(idx));
+            smd[swz(place(idx))] = R ? freduce(u2d(ld(idx)), q, qinv) : u2d(ld(idx));
         }
         __syncthreads();
         static_for<0, NPASS>([&](auto pc) {
@@ -397,6 +405,12 @@ struct NttCta {
     __device__ __forceinline__ static void inverse(u64* sm, const DPrime& Pr, const u64* __restrict__ tw,
                                                    Load&& ld, Store&& st)
     {
+        inverse<PC, STAGED>(sm, Pr, tw, ld, st, [](int i) { return i; });
+    }
+    template <int PC = PC_BIG, bool STAGED = true, class Load, class Store, class Place>
+    __device__ __forceinline__ static void inverse(u64* sm, const DPrime& Pr, const u64* __restrict__ tw,
+                                                   Load&& ld, Store&& st, Place&& place)
+    {
         const int tid = threadIdx.x;
         const u64 q = Pr.q, q2 = Pr.q2;
         const u64* IW = tw + 2 * N;
@@ -408,7 +422,7 @@ struct NttCta {
 #pragma unroll 4
             for (int c = 0; c < E; ++c) {
                 const int idx = c * NT + tid;
-                sm[swz(idx)] = ld(idx);
+                sm[swz(place(idx))] = ld(idx);
             }
             __syncthreads();
         }
@@ -450,13 +464,18 @@ __device__ __forceinline__ void ntt_forward(u64* sm, const DPrime& Pr, const u64
     default: T::template forward<PC_BIG>(sm, Pr, tw, ld, st); break;
     }
 }
+template <class T, class Load, class Store, class Place>
+__device__ __forceinline__ void ntt_inverse(u64* sm, const DPrime& Pr, const u64* tw, Load&& ld, Store&& st, Place&& place)
+{
+    const int pc = prime_class(Pr.q);
+    if (pc == PC_FP) T::inverse_fp(sm, Pr, tw, ld, st, place);
+    else if (pc == PC_FPR) T::template inverse_fp<true>(sm, Pr, tw, ld, st, place);
+    else T::template inverse<PC_BIG>(sm, Pr, tw, ld, st, place);
+}
 template <class T, class Load, class Store>
 __device__ __forceinline__ void ntt_inverse(u64* sm, const DPrime& Pr, const u64* tw, Load&& ld, Store&& st)
 {
-    const int pc = prime_class(Pr.q);
-    if (pc == PC_FP) T::inverse_fp(sm, Pr, tw, ld, st);
-    else if (pc == PC_FPR) T::template inverse_fp<true>(sm, Pr, tw, ld, st);
-    else T::template inverse<PC_BIG>(sm, Pr, tw, ld, st);
+    ntt_inverse<T>(sm, Pr, tw, ld, st, [](int i) { return i; });
 }
 
 // Threads per CTA: 16 residues per thread by default (more warps to hide the load latency of
