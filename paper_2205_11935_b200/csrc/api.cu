@@ -642,6 +642,11 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
             P.one_sh = (u64)(((u128)1 << 64) / q);
             P.r64 = (u64)(((u128)1 << 64) % q);
             P.r64_sh = h_shoup(P.r64, q);
+            P.w20 = (1ULL << 20) % q;
+            P.w23 = (1ULL << 23) % q;
+            P.w40 = (1ULL << 40) % q;
+            P.qinv_d = 1.0 / (double)q;
+            P.w23q = (double)P.w23 / (double)q;
             // W[idx] = psi^{brev(idx)} (stage s = floor(log2 idx), block idx - 2^s), stored at the
             // pass-ordered position ntt_tw_position (ntt.cuh); same for psi^{-1}.
             u64* W = tw.data() + (size_t)i * CK_TW_WORDS * n;

@@ -22,6 +22,9 @@ struct DPrime {
     u64 ninv, ninv_sh;   // N^{-1} mod q and its Shoup companion
     u64 one_sh;          // floor(2^64 / q): Shoup companion of 1
     u64 r64, r64_sh;     // 2^64 mod q and companion
+    u64 w20, w23, w40;   // 2^20, 2^23, 2^40 mod q (split-operand recombination, k_ipmma3.cu)
+    double qinv_d;       // fl(1 / q)
+    double w23q;         // fl(w23 / q)
 };
 
 // Per-context constants, resident in device memory (tables buffer).

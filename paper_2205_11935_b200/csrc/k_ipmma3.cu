@@ -66,7 +66,15 @@ __device__ __forceinline__ int ip3_kpos(int kk, int kidx, int n)
 // column of B value (k index kidx, n) in the 60-bit key tile (two 8-word halves alternate with kidx)
 __device__ __forceinline__ int ip3_icol(int n, int kidx) { return (n + ((kidx & 1) << 3)) & 15; }
 
-template <int NL, bool INT, bool MACL>
+// y * w mod q when the product y w is exact in FP64 (w = 2^23 for q > 2^23: a power of two): no low part
+__device__ __forceinline__ double fmodmul_pow2(double y, double w, double wq, double q)
+{
+    const double k = __fma_rn(y, wq, CK_RND_MAGIC) - CK_RND_MAGIC;
+    return __fma_rn(-k, q, y * w);
+}
+
+// BIGQ: q > 2^23, so 2^23 mod q = 2^23 and the fold of S1 is fmodmul_pow2 (4 FP64 operations instead of 6)
+template <int NL, bool INT, bool MACL, bool BIGQ = false>
 __device__ __forceinline__ void ip3_body(const DCtx* __restrict__ dc, const u64* __restrict__ modup,
                                          const u64* __restrict__ in, size_t ct_stride, size_t comp_off,
                                          const KsGroup& grp, int nl, size_t out_stride, int B, u64* sm, int i,
@@ -125,13 +133,12 @@ __device__ __forceinline__ void ip3_body(const DCtx* __restrict__ dc, const u64*
         const int g = r >> 1, c = r & 1;
         const u64 kv = (g < G) ? __ldg(grp.key[g] + ((size_t)j * 2 * np + (size_t)c * np + p) * n + k0 + kk) : 0;
         if constexpr (!INT) {
-            const u64 kp = mulmod(kv, (1ULL << 23) % Pr.q, Pr);                 // K' = K 2^23 mod q
+            const u64 kp = mulmod(kv, Pr.w23, Pr);                              // K' = K 2^23 mod q
             double2* d = reinterpret_cast<double2*>(Kw);
             d[ip3_kpos<S::KF>(kk, 2 * j, r)] = make_double2((double)(kp & m23), (double)(kp >> 23));     // Dh: K'l, K'h
             d[ip3_kpos<S::KF>(kk, 2 * j + 1, r)] = make_double2((double)(kv & m23), (double)(kv >> 23)); // Dl: Kl, Kh
         } else {
-            const u64 w20 = (1ULL << 20) % Pr.q, w40 = mulmod(w20, w20, Pr);
-            const u64 ku[3] = {kv, mulmod(kv, w20, Pr), mulmod(kv, w40, Pr)};
+            const u64 ku[3] = {kv, mulmod(kv, Pr.w20, Pr), mulmod(kv, Pr.w40, Pr)};
 #pragma unroll
             for (int u = 0; u < 3; ++u) {
                 const int kidx = 3 * j + u;
@@ -159,8 +166,8 @@ __device__ __forceinline__ void ip3_body(const DCtx* __restrict__ dc, const u64*
                                : grp.out[g] + (size_t)i * n + (size_t)dblk * IP3_KT;
     }
     const size_t wlimb = mac_layout ? (size_t)ne * n * B : (size_t)ne * n;
-    const double q = (double)Pr.q, qinv = 1.0 / q;
-    const double w23 = (double)((1ULL << 23) % Pr.q), w23q = w23 / q;
+    const double q = (double)Pr.q, qinv = Pr.qinv_d;      // host-computed: no 64-bit division per CTA
+    const double w23 = (double)Pr.w23, w23q = Pr.w23q;
     const u64 Pm = prow ? 0 : dc->pmod[i], Pm_sh = prow ? 0 : dc->pmod_sh[i];
     // this lane's K index per k-step: FP (j, part) = (kidx >> 1, kidx & 1); INT (j, u) = (kidx / 3, kidx % 3)
     int kj[NKB], ksh[NKB];
@@ -230,7 +237,8 @@ __device__ __forceinline__ void ip3_body(const DCtx* __restrict__ dc, const u64*
                     for (int e = 0; e < 4; ++e) {
                         const int c = e & 1;
                         // U = S0 + 2^23 S1 (+ P c0) mod q: |fmodmul| < 0.51 q, S0 < 2^50.6 -> |v| < 2^51
-                        const double hi = fmodmul(Sa[kq][1][t][e], w23, w23q, q);
+                        const double hi = BIGQ ? fmodmul_pow2(Sa[kq][1][t][e], w23, w23q, q)
+                                               : fmodmul(Sa[kq][1][t][e], w23, w23q, q);
                         const double v = hi + (Sa[kq][0][t][e] + ((c == 0) ? addd[e >> 1] : 0.0));
                         const double r = freduce(v, q, qinv);                    // [-q/2, q/2]
                         // the DMMA BSGS MAC reads signed words (arithmetic-shift split); the byte-plane
@@ -321,11 +329,13 @@ k_ks_ip_mma3(const DCtx* __restrict__ dc, const u64* __restrict__ modup, const u
     const int i = blockIdx.y, cblk = blockIdx.x;
     const u64 q = dc->p[ext_prime_of(i, nl, dc->n_data)].q;
     const bool fp = prime_class(q) == PC_FP;
+    const bool bigq = q > (1ULL << 23);
     if (mac_layout) {
         if (fp) ip3_body<NL, false, true>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm3, i, cblk);
         else ip3_body<NL, true, true>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm3, i, cblk);
     } else {
-        if (fp) ip3_body<NL, false, false>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm3, i, cblk);
+        if (fp && bigq) ip3_body<NL, false, false, true>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm3, i, cblk);
+        else if (fp) ip3_body<NL, false, false>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm3, i, cblk);
         else ip3_body<NL, true, false>(dc, modup, in, ct_stride, comp_off, grp, nl, out_stride, B, sm3, i, cblk);
     }
 }
