@@ -736,6 +736,8 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
             const u128 half = (P - 1) / 2;
             h.phalf_lo = (u64)half;
             h.phalf_hi = (u64)(half >> 64);
+            h.phalf_a = c->ns == 2 ? (u64)(half % primes[L]) : (u64)half;
+            h.phalf_t = c->ns == 2 ? (u64)(half / primes[L]) : 0;
         }
         // R13 CDT, same definition as DESIGN.md (computed here independently)
         {

@@ -48,6 +48,8 @@ struct DCtx {
     u64 pmod[CKKS_MAXP], pmod_sh[CKKS_MAXP];         // P mod q_p (0 for the special primes)
     u64 pinv[CKKS_MAXP], pinv_sh[CKKS_MAXP];         // P^{-1} mod q_i (data primes)
     u64 phalf_lo, phalf_hi;                          // (P - 1) / 2 as a 128-bit integer
+    u64 phalf_a, phalf_t;                            // K = 2: (P - 1) / 2 = phalf_a + P_0 phalf_t (mixed radix, as the
+                                                     // remainder pairs: comparing (t, a) lexicographically is exact)
     // canonical embedding on the device (k_encode.cu, R3/R4): n = N/2 slots
     const u32* slot_pos;                             // [n] (5^i mod 2N - 1) / 4
     const double2* fft_zeta;                         // [n] zeta^k = e^{i pi k / N}

@@ -41,7 +41,43 @@ k_ks_digits(const DCtx* __restrict__ dc, const u64* __restrict__ in, size_t ct_s
             if constexpr (ALPHA == 1) dst[i] = v;
             else dst[i] = (h == 0) ? v : crt2_t(dc, s0, d0[i], v);   // d0 written by this CTA (synchronised)
         };
-        ntt_inverse<T>(sm, Pr, twp(dc, pj), ld, st, place);
+        // QP input with K = 2 special primes, everything below 2^45: the fused ModDown goes on in FP64 from the
+        // transform's signed output x (|x| < 0.51 q) -- the integer form (special_centered + two Shoup products,
+        // ~55 integer-pipe instructions per coefficient) was 40 % of this kernel's issue slots (ncu source page)
+        bool fpe = false;
+        if constexpr (QPK == 2) {
+            const u64 lim = 1ULL << 45;
+            fpe = Pr.q < lim && dc->p[dc->n_data].q < lim && dc->p[dc->n_data + 1].q < lim && (h == 0 || dc->p[s0].q < lim);
+        }
+        if (fpe) {
+            if constexpr (QPK == 2) {
+                const double q = (double)Pr.q, qi = Pr.qinv_d;
+                auto cen = [&](u64 w) { return w > Pr.q / 2 ? -(double)(Pr.q - w) : (double)w; };
+                const double p0 = cen(dc->qmod[dc->n_data][pj]), p0q = p0 * qi;     // P_0 mod q (centred), / q
+                const double pm = (double)dc->pmod[pj];                              // P mod q
+                const double pv = cen(dc->pinv[pj]), pvq = pv * qi;                  // P^{-1} mod q
+                const double dv = h ? cen(dc->dig_inv[pj]) : 0.0, dvq = dv * qi;     // q_s0^{-1} mod q (2nd prime)
+                const u64 ha = dc->phalf_a, ht = dc->phalf_t;
+                auto stf = [&](int i, double x) {
+                    const u64 a = r0[i], t = r1[i];
+                    const bool neg = t > ht || (t == ht && a > ha);                  // a + P_0 t > (P - 1) / 2, exactly
+                    const double y = fmodmul(u2d(t), p0, p0q, q);                    // P_0 t mod q, |y| < 0.51 q
+                    const double z = ((x - u2d(a)) - y) + (neg ? pm : 0.0);          // x - [r]_q, |z| < 2^47
+                    double o = fmodmul(z, pv, pvq, q);
+                    if (h == 0) {
+                        o = o < 0.0 ? o + q : o;
+                        dst[i] = d2u(o);
+                    } else {                                                         // Garner: (o - d_0) q_s0^{-1} mod q
+                        double g = fmodmul(o - u2d(d0[i]), dv, dvq, q);
+                        g = g < 0.0 ? g + q : g;
+                        dst[i] = d2u(g);
+                    }
+                };
+                T::template inverse_fp<false, true>(sm, Pr, twp(dc, pj), ld, stf, place);
+            }
+        } else {
+            ntt_inverse<T>(sm, Pr, twp(dc, pj), ld, st, place);
+        }
     }
 }
 

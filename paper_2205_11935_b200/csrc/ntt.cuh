@@ -296,9 +296,11 @@ struct NttCta {
     __device__ __forceinline__ static void inverse_fp(u64* sm, const DPrime& Pr, const u64* __restrict__ tw,
                                                       Load&& ld, Store&& st)
     {
-        inverse_fp<R>(sm, Pr, tw, ld, st, [](int i) { return i; });
+        inverse_fp<R, false>(sm, Pr, tw, ld, st, [](int i) { return i; });
     }
-    template <bool R = false, class Load, class Store, class Place>
+    // SIGNED_ST: st(idx, double) receives the signed representative (|v| < 0.66 q) instead of the canonical word
+    // (for epilogues that go on in FP64, k_ksdigits.cu)
+    template <bool R = false, bool SIGNED_ST = false, class Load, class Store, class Place>
     __device__ __forceinline__ static void inverse_fp(u64* sm, const DPrime& Pr, const u64* __restrict__ tw,
                                                       Load&& ld, Store&& st, Place&& place)
     {
@@ -331,9 +333,13 @@ struct NttCta {
                     const int idx = index<P>(tid, g, i);
                     const double v = x[g * (1 << K) + i];
                     if constexpr (P == 0) {
-                        double r = fmodmul(v, ninv, ninvq, q);   // (-0.51 q, 0.51 q)
-                        r = r < 0.0 ? r + q : r;
-                        st(idx, d2u(r));
+                        double r = fmodmul(v, ninv, ninvq, q);   // (-0.51 q, 0.51 q); FPR: (-0.66 q, 0.66 q)
+                        if constexpr (SIGNED_ST) {
+                            st(idx, r);
+                        } else {
+                            r = r < 0.0 ? r + q : r;
+                            st(idx, d2u(r));
+                        }
                     } else {
                         smd[swz(idx)] = v;
                     }

@@ -1,1 +1,2 @@
-timeout 600 python tools/ab_option.py ntt_q 7 > gpurun_out/ab_quick.log 2>&1
+timeout 900 python bench.py --max-batch 512 --no-extras --no-cpu-baseline --no-e2e --no-ks-variant > gpurun_out/bench_mb512.log 2>&1
+timeout 900 python bench.py --max-batch 256 --no-extras --no-cpu-baseline --no-e2e --no-ks-variant > gpurun_out/bench_mb256.log 2>&1
