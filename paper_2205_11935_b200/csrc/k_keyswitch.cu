@@ -25,21 +25,6 @@ namespace ck {
 // reduces it mod any target prime with one Shoup product.  K special primes P_0..P_{K-1}, P = their
 // product (R17b); rows of a Q_l P polynomial: q_0..q_{nl-1}, then P_0..P_{K-1}.
 
-// layer-final ModDown of QP ciphertexts: out[b][c][i] = (y[b][c][i] - x[b][c][i]) P^{-1} mod q_i
-__global__ void __launch_bounds__(256)
-k_moddown_combine(const DCtx* __restrict__ dc, const u64* __restrict__ y, size_t y_stride, const u64* __restrict__ xo,
-                  u64* __restrict__ out, size_t out_stride, int nl)
-{
-    const int n = dc->n, ne = nl + dc->n_special;
-    const int k = blockIdx.x * 256 + threadIdx.x;
-    const int i = blockIdx.y, c = blockIdx.z % 2, b = blockIdx.z / 2;
-    const DPrime Pr = dc->p[i];
-    const u64 yv = y[(size_t)b * y_stride + ((size_t)c * ne + i) * n + k];
-    const u64 xv = xo[(((size_t)b * 2 + c) * ne + i) * n + k];
-    out[(size_t)b * out_stride + ((size_t)c * nl + i) * n + k] =
-        csub(shoup_mul(yv + Pr.q - xv, dc->pinv[i], dc->pinv_sh[i], Pr.q), Pr.q);
-}
-
 void keyswitch_modup(const Launch& L, const KsIn& in, int batch, int nl, const KsWork& w, bool qp_in)
 {
     if (batch <= 0) return;
@@ -125,11 +110,9 @@ void moddown_qp(const Launch& L, const uint64_t* y, size_t y_stride, int batch, 
     if (batch <= 0) return;
     const int n = 1 << L.log_n;
     launch_ks_qp_rem(L, y, y_stride, 0, (size_t)(nl + L.n_special) * n, 0, nl, 2, batch, w.rem);
-    launch_ks_moddown_ntt(L, w.rem, nl, batch, w.acc);
-    { ProbeScope ps_(L.probe, L.st, "k_moddown_combine");
-      k_moddown_combine<<<dim3(n / 256, nl, 2 * batch), 256, 0, L.st>>>(L.dc, y, y_stride, w.acc, out, out_stride, nl); }
+    launch_ks_moddown_ntt_fused(L, w.rem, nl, batch, y, y_stride, out, out_stride);   // (y - x) P^{-1} in the storer
     check_launch("moddown_qp");
-    if (L.counter) *L.counter += 3;
+    if (L.counter) *L.counter += 2;
 }
 
 // P ct -> QP basis (a hoisted baby step with g == 1): out[c][i] = P in[c][i], out[c][special rows] = 0

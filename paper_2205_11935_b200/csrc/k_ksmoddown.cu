@@ -39,22 +39,33 @@ k_ks_moddown_intt(const DCtx* __restrict__ dc, const u64* __restrict__ modup, co
 }
 
 // ModDown, data rows: x_g,c[i] = NTT_{q_i}(centred(r_g,c) mod q_i) (R10, R10b).  grid (nl, 2, B*G)
-template <int LOGN, int NTH, int K>
+// FUSE (the layer-final ModDown of Q_l P ciphertexts y, G = 1): the storer finishes the ModDown,
+// out[b][c][i] = (y[b][c][i] - x) P^{-1} mod q_i, instead of writing x for a combine kernel.
+template <int LOGN, int NTH, int K, bool FUSE>
 __global__ void __launch_bounds__(NTH)
-k_ks_moddown_ntt(const DCtx* __restrict__ dc, const u64* __restrict__ rem, int nl, u64* __restrict__ xo)
+k_ks_moddown_ntt(const DCtx* __restrict__ dc, const u64* __restrict__ rem, int nl, u64* __restrict__ xo,
+                 const u64* __restrict__ y, size_t y_stride, u64* __restrict__ out, size_t out_stride)
 {
     extern __shared__ u64 sm[];
     using T = NttCta<LOGN, NTH>;
     const int i = blockIdx.x, c = blockIdx.y, gb = blockIdx.z;   // gb = g * B + b
     const DPrime Pr = dc->p[i];
     const u64* r0 = rem + ((size_t)gb * 2 + c) * K * T::N;
-    u64* o = xo + (((size_t)gb * 2 + c) * (nl + K) + i) * T::N;
     auto ld = [&](int k) {
         if constexpr (K == 1) return centered_to(r0[k], dc->p[dc->n_data].q, dc->pmod[i], Pr);
         else return special_centered(dc, r0[k], r0[T::N + k], Pr, i);
     };
-    auto st = [&](int k, u64 v) { o[k] = v; };
-    ntt_forward<T>(sm, Pr, twp(dc, i), ld, st);
+    if constexpr (FUSE) {
+        const u64* yy = y + (size_t)gb * y_stride + ((size_t)c * (nl + K) + i) * T::N;
+        u64* oo = out + (size_t)gb * out_stride + ((size_t)c * nl + i) * T::N;
+        const u64 pinv = dc->pinv[i], pinv_sh = dc->pinv_sh[i];
+        auto st = [&](int k, u64 v) { oo[k] = csub(shoup_mul(yy[k] + Pr.q - v, pinv, pinv_sh, Pr.q), Pr.q); };
+        ntt_forward<T>(sm, Pr, twp(dc, i), ld, st);
+    } else {
+        u64* o = xo + (((size_t)gb * 2 + c) * (nl + K) + i) * T::N;
+        auto st = [&](int k, u64 v) { o[k] = v; };
+        ntt_forward<T>(sm, Pr, twp(dc, i), ld, st);
+    }
 }
 
 void launch_ks_moddown_intt(const Launch& L, const uint64_t* modup, const KsGroup& grp, int nl, int nd, int batch,
@@ -77,11 +88,25 @@ void launch_ks_moddown_ntt(const Launch& L, const uint64_t* rem, int nl, int gb,
     ProbeScope ps_(L.probe, L.st, "k_ks_moddown_ntt");
     NTT_DISPATCH(L.log_n, {
         constexpr int NT = NttThreads<LG>::value;
-        auto kn = L.n_special == 2 ? k_ks_moddown_ntt<LG, NT, 2> : k_ks_moddown_ntt<LG, NT, 1>;
+        auto kn = L.n_special == 2 ? k_ks_moddown_ntt<LG, NT, 2, false> : k_ks_moddown_ntt<LG, NT, 1, false>;
         allow_smem(kn, smem);
-        kn<<<dim3(nl, 2, gb), NT, smem, L.st>>>(L.dc, rem, nl, xo);
+        kn<<<dim3(nl, 2, gb), NT, smem, L.st>>>(L.dc, rem, nl, xo, nullptr, 0, nullptr, 0);
     });
     check_launch("ks_moddown_ntt");
+}
+
+void launch_ks_moddown_ntt_fused(const Launch& L, const uint64_t* rem, int nl, int batch, const uint64_t* y,
+                                 size_t y_stride, uint64_t* out, size_t out_stride)
+{
+    const size_t smem = sizeof(u64) << L.log_n;
+    ProbeScope ps_(L.probe, L.st, "k_ks_moddown_ntt");
+    NTT_DISPATCH(L.log_n, {
+        constexpr int NT = NttThreads<LG>::value;
+        auto kn = L.n_special == 2 ? k_ks_moddown_ntt<LG, NT, 2, true> : k_ks_moddown_ntt<LG, NT, 1, true>;
+        allow_smem(kn, smem);
+        kn<<<dim3(nl, 2, batch), NT, smem, L.st>>>(L.dc, rem, nl, nullptr, y, y_stride, out, out_stride);
+    });
+    check_launch("ks_moddown_ntt_fused");
 }
 
 }  // namespace ck

@@ -167,6 +167,9 @@ void launch_ks_modup(const Launch&, const uint64_t* digits, uint64_t* modup, int
 void launch_ks_moddown_intt(const Launch&, const uint64_t* modup, const KsGroup& grp, int nl, int nd, int batch,
                             uint64_t* rem);
 void launch_ks_moddown_ntt(const Launch&, const uint64_t* rem, int nl, int gb, uint64_t* xo);
+// the same transform with the layer-final ModDown finished in its storer: out = (y - x) P^{-1}
+void launch_ks_moddown_ntt_fused(const Launch&, const uint64_t* rem, int nl, int batch, const uint64_t* y,
+                                 size_t y_stride, uint64_t* out, size_t out_stride);
 // the two DigitSets (1-prime, 2-prime digits) of the active digits at nl limbs; first[] counts ModUp targets
 void digit_sets(const Launch&, int nl, bool all_e, DigitSet& one, DigitSet& two);
 // the IMAD inner products (k_ipqp.cu): data rows + ModDown combine + permutation (ip_out); Q_l P basis (ip_qp)
