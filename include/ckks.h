@@ -135,8 +135,13 @@ ckks_status ckks_ctx_info(const ckks_ctx* ctx, ckks_info* out);
 /* Process-wide kernel selection for measured A/B runs (not a precision or semantics switch: every choice gives
  * the same bits).  "mac_tc": 1 = the BSGS inner sums of double-hoisted layers on the integer tensor cores
  * (tcgen05.mma kind::i8, TMEM accumulators, TMA operand staging; k_mac_tc.cu), 0 = on the FP64 tensor cores
- * (DMMA, the default: faster in the measured A/B).  Takes effect for launches issued
- * after the call.  CKKS_E_PARAM for an unknown name or value. */
+ * (DMMA, the default: faster in the measured A/B).  "ip_v3": 1 (default) = the baby-step
+ * key-switch inner product with the pre-multiplied key (k_ipmma3.cu), 0 = the Karatsuba form (k_ipmma.cu).
+ * "ntt_q": bit mask selecting the CTA-pair FP64 NTT schedule (ntt_c.cuh: thread-block clusters, TMA row copies):
+ * 1 batch NTT forward, 2 batch NTT inverse, 4 key-switch ModUp at N <= 8192, 8 ModUp at N = 16384, 64 plain 256-bit
+ * accesses instead of the TMA copies; default 7.  "nvtx": 1 = an NVTX range around every hot-path launch site
+ * (named by kernel class), default 0 (env CKKS_NVTX).  Takes effect for launches issued after the call.
+ * CKKS_E_PARAM for an unknown name or value. */
 ckks_status ckks_set_option(const char* name, int64_t value);
 ckks_status ckks_get_option(const char* name, int64_t* value);
 /* Number of kernels this context has launched so far (bench accounting). */

@@ -977,6 +977,11 @@ ckks_status ckks_set_option(const char* name, int64_t value)
         ck::set_ntt_q((int)value);
         return CKKS_OK;
     }
+    if (std::strcmp(name, "nvtx") == 0) {
+        if (value != 0 && value != 1) return fail(CKKS_E_PARAM, "nvtx is 0 or 1");
+        ck::set_nvtx((int)value);
+        return CKKS_OK;
+    }
     return fail(CKKS_E_PARAM, std::string("unknown option ") + name);
 }
 
@@ -993,6 +998,10 @@ ckks_status ckks_get_option(const char* name, int64_t* value)
     }
     if (std::strcmp(name, "ntt_q") == 0) {
         *value = ck::get_ntt_q();
+        return CKKS_OK;
+    }
+    if (std::strcmp(name, "nvtx") == 0) {
+        *value = ck::nvtx_on();
         return CKKS_OK;
     }
     return fail(CKKS_E_PARAM, std::string("unknown option ") + name);

@@ -52,6 +52,13 @@ k_ntt_batch_c(const DCtx* __restrict__ dc, u64* __restrict__ data, int limbs, in
     }
 }
 
+static int g_nvtx = [] {
+    const char* e = getenv("CKKS_NVTX");
+    return e ? atoi(e) : 0;
+}();
+int nvtx_on() { return g_nvtx; }
+void set_nvtx(int on) { g_nvtx = on; }
+
 static int g_ntt_q = [] {
     const char* e = getenv("CKKS_NTT_Q");
     return e ? atoi(e) : (int)NTTQ_DEFAULT;

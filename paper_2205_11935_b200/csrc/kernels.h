@@ -3,6 +3,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <map>
 #include <string>
 #include <vector>
@@ -36,12 +37,19 @@ struct Probe {
 };
 
 struct Launch;
-// PROBE_ALL: event pair around one launch site, tagged with the kernel name
+// NVTX ranges around every hot-path launch site (ckks_set_option("nvtx", 1) / env CKKS_NVTX=1): names the
+// launches of a timeline capture by kernel class; off by default (two host calls per launch site)
+int nvtx_on();
+void set_nvtx(int on);
+// PROBE_ALL: event pair around one launch site, tagged with the kernel name (+ the NVTX range when enabled)
 struct ProbeScope {
     Probe* p;
     cudaStream_t st;
-    ProbeScope(Probe* probe, cudaStream_t s, const char* name) : p(probe && probe->kind == PROBE_ALL ? probe : nullptr), st(s)
+    bool nv;
+    ProbeScope(Probe* probe, cudaStream_t s, const char* name)
+        : p(probe && probe->kind == PROBE_ALL ? probe : nullptr), st(s), nv(nvtx_on() != 0)
     {
+        if (nv) nvtxRangePushA(name);
         if (p) {
             p->names.push_back(name);
             p->mark(st);
@@ -50,6 +58,7 @@ struct ProbeScope {
     ~ProbeScope()
     {
         if (p) p->mark(st);
+        if (nv) nvtxRangePop();
     }
 };
 
