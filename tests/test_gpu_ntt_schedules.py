@@ -82,3 +82,16 @@ def test_modup_cluster_cfg4_hybrid_sampled(ntt_q):
     spec = {"kind": "dense", "cfg": S.CFG4_HYBRID, "batch": B, "activation": "square", "hoisting": 2, "x": 1}
     _, got, out = gpu_forward(spec, B, B)
     check(got, out, OP.oracle_forwards(spec, [0, 17, 39]))
+
+
+def test_nvtx_ranges_do_not_change_results():
+    """ckks_set_option("nvtx", 1): NVTX ranges around every launch site (host-side only); same bits as the oracle."""
+    old = G.get_option("nvtx")
+    G.set_option("nvtx", 1)
+    try:
+        B = 5
+        spec = {"kind": "dense", "cfg": SMALL, "batch": B, "activation": "square", "hoisting": 2, "x": 1}
+        _, got, out = gpu_forward(spec, B, 4)
+        check(got, out, OP.oracle_forwards(spec, range(B)))
+    finally:
+        G.set_option("nvtx", old)
