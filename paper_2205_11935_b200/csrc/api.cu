@@ -694,6 +694,8 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
                 std::memcpy(&W[8 * n + 2 * pos + 1], &wq, 8);
                 std::memcpy(&W[10 * n + 2 * pos], &iwd, 8);
                 std::memcpy(&W[10 * n + 2 * pos + 1], &iwq, 8);
+                W[12 * n + 2 * pos] = fw[idx];                      // integer pairs (w, w') for ArInt
+                W[12 * n + 2 * pos + 1] = h_shoup(fw[idx], q);
             }
             for (int b = 0; b < np; ++b) {
                 h.qmod[i][b] = q % primes[b];

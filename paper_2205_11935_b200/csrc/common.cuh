@@ -13,9 +13,9 @@ typedef uint64_t u64;
 typedef uint32_t u32;
 
 #define CKKS_MAXP 16
-// twiddle words per prime: W, W', IW, IW' (u64), Wd, Wq, IWd, IWq (double), then the pair tables
-// [N] x (w, w/q) of the cluster schedule, forward and inverse (ntt_c.cuh)
-#define CK_TW_WORDS 12
+// twiddle words per prime: W, W', IW, IW' (u64), Wd, Wq, IWd, IWq (double), then the pair tables of the cluster
+// schedule (ntt_c.cuh): [N] x (w, w/q) forward and inverse (FP64), [N] x (w, w') forward (integer Shoup)
+#define CK_TW_WORDS 14
 
 struct DPrime {
     u64 q, q2;

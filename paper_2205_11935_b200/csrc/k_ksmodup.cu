@@ -46,9 +46,9 @@ k_ks_modup(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* __r
     else ntt_forward<T>(sm, Pr, twp(dc, p), ld, st);
 }
 
-// The same ModUp with the FP64-class target rows on the CTA-pair schedule (ntt_c.cuh): grid (CL * targets, B) in
-// clusters of CL CTAs; clusters whose target is an integer-class prime exit at once (both CTAs: same target) and
-// k_ks_modup_rows transforms those rows.
+// The same ModUp on the CTA-pair schedule (ntt_c.cuh): grid (CL * targets, B) in clusters of CL CTAs; FP64-class
+// targets on the FP64 pipe, integer-class targets (q_0, 60-bit special primes) on the integer pipe in the same
+// launch and CTA shape, so CTAs of both kinds share an SM.
 template <int LOGN, int ALPHA>
 __global__ void __launch_bounds__(NttC<LOGN>::NT, NttC<LOGN>::MINB)
 k_ks_modup_c(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* __restrict__ modup, int nl, int nd,
@@ -66,7 +66,6 @@ k_ks_modup_c(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* _
     const int p = ext_prime_of(e, nl, dc->n_data);
     const DPrime Pr = dc->p[p];
     const int pc = prime_class(Pr.q);
-    if (pc != PC_FP && pc != PC_FPR) return;
     const u64* src = digits + ((size_t)b * nl + s0) * TC::N;
     u64* dst = modup + (((size_t)b * nd + j) * ne + e) * TC::N;
     auto ld = [&](int i) {
@@ -81,40 +80,12 @@ k_ks_modup_c(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* _
     if (pc == PC_FP) {
         if (small) TC::template forward_fp<false>(sm, h, Pr, twq_fwd(dc, p), ld_small, dst);
         else TC::template forward_fp<false>(sm, h, Pr, twq_fwd(dc, p), ld, dst);
-    } else {
+    } else if (pc == PC_FPR) {
         if (small) TC::template forward_fp<true>(sm, h, Pr, twq_fwd(dc, p), ld_small, dst);
         else TC::template forward_fp<true>(sm, h, Pr, twq_fwd(dc, p), ld, dst);
+    } else {
+        TC::forward_int(sm, h, Pr, twq_fwd_int(dc, p), ld, dst);
     }
-}
-
-// integer-class target rows of a ModUp launch (with k_ks_modup_c): grid (set.count * rows.count, B)
-struct RowSet {
-    int count;
-    int e[CKKS_MAXP];
-};
-template <int LOGN, int NTH, int ALPHA>
-__global__ void __launch_bounds__(NTH)
-k_ks_modup_rows(const DCtx* __restrict__ dc, const u64* __restrict__ digits, u64* __restrict__ modup, int nl, int nd,
-                int all_e, const DigitSet set, const RowSet rows)
-{
-    extern __shared__ u64 sm[];
-    using T = NttCta<LOGN, NTH>;
-    const int ne = nl + dc->n_special;
-    const int t = blockIdx.x / rows.count, e = rows.e[blockIdx.x % rows.count];
-    const int s0 = set.s0[t], j = set.j[t];
-    if (!all_e && e >= s0 && e < s0 + ALPHA) return;   // a row of the digit itself: read from the input
-    const int b = blockIdx.y;
-    const int p = ext_prime_of(e, nl, dc->n_data);
-    const DPrime Pr = dc->p[p];
-    const u64* src = digits + ((size_t)b * nl + s0) * T::N;
-    u64* dst = modup + (((size_t)b * nd + j) * ne + e) * T::N;
-    auto ld = [&](int i) {
-        if constexpr (ALPHA == 1) return reduce64_lazy(src[i], Pr);
-        else return crt2_lazy(dc, s0, src[i], src[T::N + i], Pr, p);
-    };
-    auto st = [&](int i, u64 v) { dst[i] = v; };
-    if (prime_class(Pr.q) == PC_MID) T::template forward<PC_MID>(sm, Pr, twp(dc, p), ld, st);
-    else T::template forward<PC_BIG>(sm, Pr, twp(dc, p), ld, st);
 }
 
 template <int LG>
@@ -123,39 +94,16 @@ static bool launch_ks_modup_c(const Launch& L, const uint64_t* digits, uint64_t*
 {
     if constexpr (ntt_c_supported(LG)) {
         if (!(get_ntt_q() & (LG == 14 ? NTTQ_MODUP_14 : NTTQ_MODUP))) return false;
-        // small launches are latency-bound: the separate launch for the integer-class rows would double their
-        // critical path (cfg1 at batch 1: 800 -> 894 us per forward), so they keep the single whole-limb kernel
-        if ((long)batch * (one.first[one.count] + two.first[two.count]) < 4 * 148) return false;
         using TC = NttC<LG>;
-        constexpr int NW = NttThreadsWide<LG>::value;
-        RowSet rows;
-        rows.count = 0;
-        for (int e = 0; e < nl + L.n_special; ++e) {
-            const int c = L.pclass[e < nl ? e : L.n_data + (e - nl)];
-            if (c != PC_FP && c != PC_FPR) rows.e[rows.count++] = e;
-        }
-        const size_t smem = sizeof(u64) << LG;
-        // the integer-class rows are one more launch per digit size (the caller counts one each)
-        if (L.counter && rows.count) *L.counter += (one.count ? 1 : 0) + (two.count ? 1 : 0);
         if (one.count) {
             allow_smem(k_ks_modup_c<LG, 1>, TC::SMEM_ALL);
             launch_cluster(k_ks_modup_c<LG, 1>, dim3(one.first[one.count] * TC::CL, batch), TC::NT, TC::SMEM_ALL, L.st,
                            TC::CL, L.dc, digits, modup, nl, nd, all_e ? 1 : 0, one);
-            if (rows.count) {
-                allow_smem(k_ks_modup_rows<LG, NW, 1>, smem);
-                k_ks_modup_rows<LG, NW, 1><<<dim3(one.count * rows.count, batch), NW, smem, L.st>>>(
-                    L.dc, digits, modup, nl, nd, all_e ? 1 : 0, one, rows);
-            }
         }
         if (two.count) {
             allow_smem(k_ks_modup_c<LG, 2>, TC::SMEM_ALL);
             launch_cluster(k_ks_modup_c<LG, 2>, dim3(two.first[two.count] * TC::CL, batch), TC::NT, TC::SMEM_ALL, L.st,
                            TC::CL, L.dc, digits, modup, nl, nd, all_e ? 1 : 0, two);
-            if (rows.count) {
-                allow_smem(k_ks_modup_rows<LG, NW, 2>, smem);
-                k_ks_modup_rows<LG, NW, 2><<<dim3(two.count * rows.count, batch), NW, smem, L.st>>>(
-                    L.dc, digits, modup, nl, nd, all_e ? 1 : 0, two, rows);
-            }
         }
         return true;
     } else {

@@ -40,7 +40,8 @@ k_ntt_batch_c(const DCtx* __restrict__ dc, u64* __restrict__ data, int limbs, in
     const int l = blockIdx.x / TC::CL, h = blockIdx.x % TC::CL, b = blockIdx.y, p = prime0 + l;
     u64* a = data + ((size_t)b * limbs + l) * TC::N;
     const DPrime Pr = dc->p[p];
-    const bool r = prime_class(Pr.q) == PC_FPR;
+    const int pc = prime_class(Pr.q);
+    const bool r = pc == PC_FPR;
     if constexpr (INV) {
         auto st = [&](int i, u64 v) { a[i] = v; };
         if (r) TC::template inverse_fp<true, IO>(sm, h, Pr, twq_inv(dc, p), a, st);
@@ -48,7 +49,8 @@ k_ntt_batch_c(const DCtx* __restrict__ dc, u64* __restrict__ data, int limbs, in
     } else {
         auto ld = [&](int i) { return a[i]; };
         if (r) TC::template forward_fp<true, IO>(sm, h, Pr, twq_fwd(dc, p), ld, a);
-        else TC::template forward_fp<false, IO>(sm, h, Pr, twq_fwd(dc, p), ld, a);
+        else if (pc == PC_FP) TC::template forward_fp<false, IO>(sm, h, Pr, twq_fwd(dc, p), ld, a);
+        else TC::template forward_int<IO>(sm, h, Pr, twq_fwd_int(dc, p), ld, a);   // integer-class limb, same launch
     }
 }
 
@@ -111,9 +113,10 @@ void ntt_batch(const Launch& L, uint64_t* data, int batch, int limbs, int prime0
         // maximal runs of limbs of one kind: FP64-class limbs on the CTA-pair schedule (when selected), the rest
         // (and everything when it is off) on the whole-limb kernel
         for (int l0 = 0; l0 < limbs;) {
+            // (the forward handles every class on the cluster schedule; the inverse only the FP64 classes)
             auto is_fp = [&](int l) {
                 const int c = L.pclass[prime0 + l];
-                return cl && (c == PC_FP || c == PC_FPR);
+                return cl && (!inverse || c == PC_FP || c == PC_FPR);
             };
             const bool fp = is_fp(l0);
             int l1 = l0 + 1;

@@ -139,13 +139,13 @@ void ip_mma_pipelined(const Launch&, const KsIn& in, const KsGroup& grp, int bat
 bool ip_mma3(const Launch&, const KsIn& in, const KsGroup& grp, int batch, int nl, const KsWork& w,
              size_t out_stride, bool mac_layout);
 void set_ip_v3(int on);
-// CTA-pair (cluster) FP64 NTT schedule (ntt_c.cuh), bit mask: 1 batch NTT forward, 2 batch NTT inverse, 4 ModUp at
-// N <= 8192, 8 ModUp at N = 16384 (measured slower there: 27.3 vs 25.7 ms per B = 256 chunk, the integer-class rows
-// need their own launch),
+// CTA-pair (cluster) NTT schedule (ntt_c.cuh), bit mask: 1 batch NTT forward, 2 batch NTT inverse, 4 ModUp at
+// N <= 8192, 8 ModUp at N = 16384 (24.2 -> 23.4 ms per B = 256 chunk once the integer-class target rows ran in the
+// same launch on the integer pipe; with a launch of their own it was slower, 25.7 ms),
 // 64 plain 256-bit global accesses instead of the TMA row copies (A/B)  (ckks_set_option("ntt_q", mask); env
 // CKKS_NTT_Q; default NTTQ_DEFAULT)
 enum { NTTQ_BATCH_FWD = 1, NTTQ_BATCH_INV = 2, NTTQ_MODUP = 4, NTTQ_MODUP_14 = 8, NTTQ_DIRECT_IO = 64,
-       NTTQ_DEFAULT = NTTQ_BATCH_FWD | NTTQ_BATCH_INV | NTTQ_MODUP };
+       NTTQ_DEFAULT = NTTQ_BATCH_FWD | NTTQ_BATCH_INV | NTTQ_MODUP | NTTQ_MODUP_14 };
 void set_ntt_q(int mask);
 int get_ntt_q();
 int get_ip_v3();

@@ -15,6 +15,7 @@ namespace ck {
 __device__ __forceinline__ const u64* twp(const DCtx* dc, int p) { return dc->tw + (size_t)p * CK_TW_WORDS * dc->n; }
 // (w, w/q) pair tables of the cluster schedule (ntt_c.cuh): forward, inverse
 __device__ __forceinline__ const double2* twq_fwd(const DCtx* dc, int p) { return reinterpret_cast<const double2*>(twp(dc, p) + 8 * dc->n); }
+__device__ __forceinline__ const ulonglong2* twq_fwd_int(const DCtx* dc, int p) { return reinterpret_cast<const ulonglong2*>(twp(dc, p) + 12 * dc->n); }
 __device__ __forceinline__ const double2* twq_inv(const DCtx* dc, int p) { return reinterpret_cast<const double2*>(twp(dc, p) + 10 * dc->n); }
 
 // NTT-domain automorphism (R3): out[k] = in[src(k)] with 2 brev(src)+1 = g (2 brev(k)+1) mod 2N

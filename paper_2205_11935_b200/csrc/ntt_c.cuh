@@ -67,6 +67,46 @@ enum { LD_DIRECT = 0, LD_BULK = 2 };
 #define NTTC_ST_DEFAULT ST_BULK
 #endif
 
+// Arithmetic of the forward transform.  ArFp<R>: the FP64 classes of ntt.cuh (exact signed integers in doubles;
+// R = PC_FPR, the X input reduced in the first stage of a pass).  ArInt: 64-bit Harvey-lazy Shoup butterflies
+// ([0, 4q) values, any q < 2^61) on the integer pipe -- so integer-class limbs run in the same launch and the same
+// CTA shape as FP64-class ones, and CTAs of both kinds share an SM (different pipes).
+template <bool R>
+struct ArFp {
+    using V = double;
+    using TW = double2;
+    double q, qinv;
+    __device__ __forceinline__ explicit ArFp(const DPrime& P) : q((double)P.q), qinv(1.0 / (double)P.q) {}
+    __device__ __forceinline__ V in(u64 a) const { return u2d(a); }
+    template <bool FIRST>
+    __device__ __forceinline__ void bfly(V& X, V& Y, const TW& w) const
+    {
+        const double tt = fmodmul(Y, w.x, w.y, q);
+        const double xx = (R && FIRST) ? freduce(X, q, qinv) : X;
+        X = xx + tt;
+        Y = xx - tt;
+    }
+    __device__ __forceinline__ u64 out(V v) const { return fcanon(v, q, qinv); }
+};
+struct ArInt {
+    using V = u64;
+    using TW = ulonglong2;   // (w, floor(w 2^64 / q))
+    u64 q, q2;
+    __device__ __forceinline__ explicit ArInt(const DPrime& P) : q(P.q), q2(P.q2) {}
+    __device__ __forceinline__ V in(u64 a) const { return a; }
+    template <bool FIRST>
+    __device__ __forceinline__ void bfly(V& X, V& Y, const TW& w) const
+    {
+        const u64 xx = csub(X, q2);                     // [0, 2q)
+        const u64 tt = shoup_mul(Y, w.x, w.y, q);       // [0, 2q) for any Y < 2^64
+        X = xx + tt;                                    // [0, 4q)
+        Y = xx - tt + q2;
+    }
+    __device__ __forceinline__ u64 out(V v) const { return csub(csub(v, q2), q); }
+};
+__device__ __forceinline__ ulonglong2 ldg_pair(const ulonglong2* p) { return __ldg(p); }
+__device__ __forceinline__ double2 ldg_pair(const double2* p) { return __ldg(p); }
+
 template <int LOGN_>
 struct NttC {
     static constexpr int LOGN = LOGN_;
@@ -116,34 +156,31 @@ struct NttC {
         return (h << G_::S0) + ((g * NT + t) >> G_::SH);
     }
 
-    template <int P, bool R>
-    __device__ __forceinline__ static void fwd_pass(double (&x)[E], int h, int t, const double2* __restrict__ TW,
-                                                    double q, double qinv)
+    template <int P, class AR>
+    __device__ __forceinline__ static void fwd_pass(typename AR::V (&x)[E], int h, int t,
+                                                    const typename AR::TW* __restrict__ TW, const AR& ar)
     {
         using G_ = Pass<P>;
         constexpr int K = G_::K, S0g = SB + G_::S0;
 #pragma unroll
         for (int g = 0; g < G_::G; ++g) {
             const int b0 = tw_base<P>(h, t, g);
-#pragma unroll
-            for (int r = 0; r < K; ++r) {
-                const int half = 1 << (K - 1 - r);
+            static_for<0, K>([&](auto rc) {
+                constexpr int r = decltype(rc)::value;
+                constexpr int half = 1 << (K - 1 - r);
 #pragma unroll
                 for (int i = 0; i < (1 << K); ++i) {
                     if (i & half) continue;
 #ifdef KNOCK_TW   /* tools/lab timing experiment only */
-                    const double2 w = make_double2(12345.0 + r + b0, 1e-8);
+                    typename AR::TW w;
+                    w.x = (decltype(w.x))(12345 + r + b0);
+                    w.y = (decltype(w.y))1;
 #else
-                    const double2 w = __ldg(TW + ((1 << (S0g + r)) + ((i >> (K - r)) << S0g) + b0));
+                    const typename AR::TW w = ldg_pair(TW + ((1 << (S0g + r)) + ((i >> (K - r)) << S0g) + b0));
 #endif
-                    double& X = x[g * (1 << K) + i];
-                    double& Y = x[g * (1 << K) + i + half];
-                    const double tt = fmodmul(Y, w.x, w.y, q);
-                    const double xx = (R && r == 0) ? freduce(X, q, qinv) : X;   // FPR: first stage of a pass
-                    X = xx + tt;
-                    Y = xx - tt;
+                    ar.template bfly<r == 0>(x[g * (1 << K) + i], x[g * (1 << K) + i + half], w);
                 }
-            }
+            });
         }
     }
 
@@ -186,19 +223,32 @@ struct NttC {
     __device__ __forceinline__ static void forward_fp(u64* sm, int h, const DPrime& Pr, const double2* __restrict__ TW,
                                                       Load&& ld, u64* __restrict__ dst)
     {
+        forward<ArFp<R>, ST>(sm, h, ArFp<R>(Pr), TW, ld, dst);
+    }
+    // the same transform on the integer pipe (any q < 2^61); TW = the (w, w') pair table
+    template <int ST = NTTC_ST_DEFAULT, class Load>
+    __device__ __forceinline__ static void forward_int(u64* sm, int h, const DPrime& Pr,
+                                                       const ulonglong2* __restrict__ TW, Load&& ld,
+                                                       u64* __restrict__ dst)
+    {
+        forward<ArInt, ST>(sm, h, ArInt(Pr), TW, ld, dst);
+    }
+    template <class AR, int ST, class Load>
+    __device__ __forceinline__ static void forward(u64* sm, int h, const AR ar, const typename AR::TW* __restrict__ TW,
+                                                   Load&& ld, u64* __restrict__ dst)
+    {
+        using V = typename AR::V;
         const int t = threadIdx.x;
-        const double q = (double)Pr.q, qinv = 1.0 / q;
-        double* smd = reinterpret_cast<double*>(sm);
-        double x[E];
+        V* smd = reinterpret_cast<V*>(sm);
+        V x[E];
 #ifdef NTTC_DUP   /* tools/lab experiment: no cluster, each CTA loads both halves and does all of stage 0 for its own */
         if constexpr (CL == 2) {
-            const double2 w = __ldg(TW + 1);
+            const typename AR::TW w = ldg_pair(TW + 1);
 #pragma unroll
             for (int i = 0; i < E; ++i) {
-                const double X = u2d(ld(t + NT * i)), Y = u2d(ld(t + NT * i + M));
-                const double tt = fmodmul(Y, w.x, w.y, q);
-                const double xx = R ? freduce(X, q, qinv) : X;
-                x[i] = h ? xx - tt : xx + tt;
+                V X = ar.in(ld(t + NT * i)), Y = ar.in(ld(t + NT * i + M));
+                ar.template bfly<true>(X, Y, w);
+                x[i] = h ? Y : X;
             }
         } else
 #endif
@@ -207,37 +257,36 @@ struct NttC {
             // to rank 0, Y' to rank 1 -- at register i of thread t either way
             cluster_arrive();   // the partner must be running before its shared memory is written
             const int i0 = 16 * h;
-            double keep[16], send[16];
-            const double2 w = __ldg(TW + 1);
+            V keep[16], send[16];
+            const typename AR::TW w = ldg_pair(TW + 1);
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
-                keep[k] = u2d(ld(t + NT * (i0 + k)));
-                send[k] = u2d(ld(t + NT * (i0 + k) + M));
+                keep[k] = ar.in(ld(t + NT * (i0 + k)));
+                send[k] = ar.in(ld(t + NT * (i0 + k) + M));
             }
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
-                const double tt = fmodmul(send[k], w.x, w.y, q);
-                const double xx = R ? freduce(keep[k], q, qinv) : keep[k];
-                const double xo = xx + tt, yo = xx - tt;
+                V xo = keep[k], yo = send[k];
+                ar.template bfly<true>(xo, yo, w);
                 keep[k] = h ? yo : xo;
                 send[k] = h ? xo : yo;
             }
             cluster_wait();
-            double* remote = cooperative_groups::this_cluster().map_shared_rank(smd, h ^ 1);
+            V* remote = cooperative_groups::this_cluster().map_shared_rank(smd, h ^ 1);
 #pragma unroll
             for (int k = 0; k < 16; ++k) remote[k * NT + t] = send[k];
             cluster_arrive();
             cluster_wait();
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
-                const double got = smd[k * NT + t];
+                const V got = smd[k * NT + t];
                 x[k] = h ? got : keep[k];
                 x[16 + k] = h ? keep[k] : got;
             }
             __syncthreads();   // the receive buffer aliases the exchange region
         } else {
 #pragma unroll
-            for (int i = 0; i < E; ++i) x[i] = u2d(ld(t + pos0(i)));
+            for (int i = 0; i < E; ++i) x[i] = ar.in(ld(t + pos0(i)));
         }
         static_for<0, 3>([&](auto pc) {
             constexpr int P = decltype(pc)::value;
@@ -253,7 +302,7 @@ struct NttC {
                 }
             }
 #ifndef KNOCK_FP   /* tools/lab timing experiment only */
-            fwd_pass<P, R>(x, h, t, TW, q, qinv);
+            fwd_pass<P, AR>(x, h, t, TW, ar);
 #endif
             if constexpr (P != 2) {
 #pragma unroll
@@ -268,9 +317,9 @@ struct NttC {
                     const int base = h * M + ((g * NT + t) << K);
 #pragma unroll
                     for (int i = 0; i < (1 << K); i += 4)
-                        st_global_v4(dst + base + i, fcanon(x[g * (1 << K) + i], q, qinv),
-                                     fcanon(x[g * (1 << K) + i + 1], q, qinv), fcanon(x[g * (1 << K) + i + 2], q, qinv),
-                                     fcanon(x[g * (1 << K) + i + 3], q, qinv));
+                        st_global_v4(dst + base + i, ar.out(x[g * (1 << K) + i]),
+                                     ar.out(x[g * (1 << K) + i + 1]), ar.out(x[g * (1 << K) + i + 2]),
+                                     ar.out(x[g * (1 << K) + i + 3]));
                 }
             } else {
                 // ST_BULK: each thread writes its 128-byte output rows into shared memory and hands them to the
@@ -284,7 +333,7 @@ struct NttC {
 #pragma unroll
                     for (int i = 0; i < (1 << K); i += 2)
                         *reinterpret_cast<ulonglong2*>(row + i) =
-                            make_ulonglong2(fcanon(x[g * (1 << K) + i], q, qinv), fcanon(x[g * (1 << K) + i + 1], q, qinv));
+                            make_ulonglong2(ar.out(x[g * (1 << K) + i]), ar.out(x[g * (1 << K) + i + 1]));
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #pragma unroll

@@ -97,7 +97,7 @@ def test_kernel_options_round_trip():
     """ckks_set_option / ckks_get_option (host-side state, no launch): every documented option reads back what
     was set, defaults are the documented ones, unknown names and out-of-range values are CKKS_E_PARAM."""
     from paper_2205_11935_b200 import ckks as G
-    defaults = {"mac_tc": 0, "ip_v3": 1, "ntt_q": 7, "nvtx": 0}
+    defaults = {"mac_tc": 0, "ip_v3": 1, "ntt_q": 15, "nvtx": 0}
     env = {"mac_tc": "CKKS_MAC_TC", "ip_v3": "CKKS_IP_V3", "ntt_q": "CKKS_NTT_Q", "nvtx": "CKKS_NVTX"}
     for name, d in defaults.items():
         if env[name] not in os.environ:                         # an env override changes the default
