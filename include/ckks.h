@@ -139,7 +139,8 @@ ckks_status ckks_ctx_info(const ckks_ctx* ctx, ckks_info* out);
  * key-switch inner product with the pre-multiplied key (k_ipmma3.cu), 0 = the Karatsuba form (k_ipmma.cu).
  * "ntt_q": bit mask selecting the CTA-pair FP64 NTT schedule (ntt_c.cuh: thread-block clusters, TMA row copies):
  * 1 batch NTT forward, 2 batch NTT inverse, 4 key-switch ModUp at N <= 8192, 8 ModUp at N = 16384, 64 plain 256-bit
- * accesses instead of the TMA copies; default 15.  "nvtx": 1 = an NVTX range around every hot-path launch site
+ * accesses instead of the TMA copies; default 15.  "giant_multi": 1 (default) = all giant steps of a double-hoisted layer accumulated in one
+ * pass (k_ks_ip_giant_multi), 0 = one accumulator pass per step.  "nvtx": 1 = an NVTX range around every hot-path launch site
  * (named by kernel class), default 0 (env CKKS_NVTX).  Takes effect for launches issued after the call.
  * CKKS_E_PARAM for an unknown name or value. */
 ckks_status ckks_set_option(const char* name, int64_t value);

@@ -979,6 +979,11 @@ ckks_status ckks_set_option(const char* name, int64_t value)
         ck::set_ntt_q((int)value);
         return CKKS_OK;
     }
+    if (std::strcmp(name, "giant_multi") == 0) {
+        if (value != 0 && value != 1) return fail(CKKS_E_PARAM, "giant_multi is 0 or 1");
+        ck::set_giant_multi((int)value);
+        return CKKS_OK;
+    }
     if (std::strcmp(name, "nvtx") == 0) {
         if (value != 0 && value != 1) return fail(CKKS_E_PARAM, "nvtx is 0 or 1");
         ck::set_nvtx((int)value);
@@ -1000,6 +1005,10 @@ ckks_status ckks_get_option(const char* name, int64_t* value)
     }
     if (std::strcmp(name, "ntt_q") == 0) {
         *value = ck::get_ntt_q();
+        return CKKS_OK;
+    }
+    if (std::strcmp(name, "giant_multi") == 0) {
+        *value = ck::get_giant_multi();
         return CKKS_OK;
     }
     if (std::strcmp(name, "nvtx") == 0) {
@@ -1490,8 +1499,45 @@ static void matvec_chunk(ckks_ctx* c, const ckks_layer* ly, const u64* in, size_
                                    mac_layout);
         ck::bsgs_mac(L, ly->d_pts, nl + c->ns, in, in_stride, baby, Wk, (int)ly->t1, (int)ly->t2, B, nl, true,
                      mac_layout);
-        for (uint32_t k = 1; k < ly->t2; ++k)
-            rotate_qp_impl(c, Wk + (size_t)k * B * ctq, ctq, nl, B, (int64_t)k * ly->giant, Wk, ctq, stream);
+        // giant steps: every step's digits / ModUp first (each into its own scratch, carved from the baby-step
+        // buffer, which is dead after the inner sums), then ONE pass over the accumulator for up to KS_GMAX steps
+        // (k_ks_ip_giant_multi); the per-step form (one accumulator pass per step) when the scratch does not fit
+        const int G = (int)ly->t2 - 1, nd = L.active_digits(nl), ne = nl + c->ns;
+        const size_t step_words = (size_t)B * c->n * ((size_t)nl + (size_t)nd * ne + (size_t)c->ns);
+        const bool multi = ck::get_giant_multi() && G >= 1 && nd <= 5 &&
+                           (size_t)std::min(G, IPGM_GMAX) * step_words <= (size_t)(ly->t1 - 1) * B * ctq;
+        if (multi) {
+            for (int g0 = 0; g0 < G; g0 += IPGM_GMAX) {
+                const int gn = std::min(IPGM_GMAX, G - g0);
+                const u64 *modup[KS_GMAX], *keys[KS_GMAX], *adds[KS_GMAX];
+                uint32_t gal[KS_GMAX];
+                for (int gi = 0; gi < gn; ++gi) {
+                    const uint32_t k = (uint32_t)(g0 + gi + 1);
+                    const int64_t step = (int64_t)k * ly->giant;
+                    const uint32_t g = c->galois(step);
+                    if (g == 1) throw CkksError(CKKS_E_PARAM, "giant step congruent to 0 mod N/2");
+                    const u64* key = c->key((int64_t)g);
+                    if (!key) throw CkksError(CKKS_E_NOKEY, "no Galois key for step " + std::to_string(step));
+                    ck::KsWork w{};
+                    u64* p = baby + (size_t)gi * step_words;
+                    w.digits = p;
+                    w.modup = p + (size_t)B * nl * c->n;
+                    w.rem = w.modup + (size_t)B * nd * ne * c->n;
+                    const u64* wk = Wk + (size_t)k * B * ctq;
+                    ck::KsIn ki{wk, ctq, (size_t)ne * c->n, g};
+                    ck::keyswitch_modup(L, ki, B, nl, w, true);
+                    modup[gi] = w.modup;
+                    keys[gi] = key;
+                    adds[gi] = wk;
+                    gal[gi] = g;
+                }
+                if (!ck::ip_giant_multi(L, gn, modup, keys, adds, gal, B, nl, Wk, ctq, ctq))
+                    throw CkksError(CKKS_E_PARAM, "ip_giant_multi not applicable");
+            }
+        } else {
+            for (uint32_t k = 1; k < ly->t2; ++k)
+                rotate_qp_impl(c, Wk + (size_t)k * B * ctq, ctq, nl, B, (int64_t)k * ly->giant, Wk, ctq, stream);
+        }
         ck::moddown_qp(L, Wk, ctq, B, nl, c->ks_work(B), md, ctw);
         rescale_impl(c, md, ctw, 2, nl, B, out, out_stride, ly->d_bias, stream);
         return;

@@ -151,6 +151,16 @@ int get_ntt_q();
 int get_ip_v3();
 // the giant-step (G = 1, accumulate, addend sigma_g(w.c0)) QP inner product, key-stationary over the
 // batch (k_ipgiant.cu); CKKS_IP_GIANT=0 selects the per-ciphertext-pair kernel k_ks_ip_qp
+// all G <= KS_GMAX giant steps of a layer in one pass over the accumulator: step g has its own ModUp words, key,
+// addend ciphertexts (stride add_stride, sigma_g gathered) and Galois element; false when not applicable (> 5 digits)
+bool ip_giant_multi(const Launch&, int G, const uint64_t* const* modup, const uint64_t* const* key,
+                    const uint64_t* const* add, const uint32_t* galois, int batch, int nl, uint64_t* acc,
+                    size_t acc_stride, size_t add_stride);
+#ifndef IPGM_GMAX
+#define IPGM_GMAX 4   // giant steps per accumulator pass (shared memory: IPGM_GMAX x 2 nd x 1 KiB of key words per CTA)
+#endif
+void set_giant_multi(int on);
+int get_giant_multi();
 void ip_giant(const Launch&, const uint64_t* key, int batch, int nl, const KsWork& w, uint64_t* acc,
               size_t acc_stride, const uint64_t* add, size_t add_stride, uint32_t add_galois);
 // y [B][2][nl+1][N] (QP, stride y_stride) -> out [B][2][nl][N]: (y - [y_P]) / P  (one ModDown per layer)

@@ -97,16 +97,17 @@ def test_kernel_options_round_trip():
     """ckks_set_option / ckks_get_option (host-side state, no launch): every documented option reads back what
     was set, defaults are the documented ones, unknown names and out-of-range values are CKKS_E_PARAM."""
     from paper_2205_11935_b200 import ckks as G
-    defaults = {"mac_tc": 0, "ip_v3": 1, "ntt_q": 15, "nvtx": 0}
-    env = {"mac_tc": "CKKS_MAC_TC", "ip_v3": "CKKS_IP_V3", "ntt_q": "CKKS_NTT_Q", "nvtx": "CKKS_NVTX"}
+    defaults = {"mac_tc": 0, "ip_v3": 1, "ntt_q": 15, "nvtx": 0, "giant_multi": 1}
+    env = {"mac_tc": "CKKS_MAC_TC", "ip_v3": "CKKS_IP_V3", "ntt_q": "CKKS_NTT_Q", "nvtx": "CKKS_NVTX",
+           "giant_multi": "CKKS_GIANT_MULTI"}
     for name, d in defaults.items():
         if env[name] not in os.environ:                         # an env override changes the default
             assert G.get_option(name) == d, name
-    for name, vals in {"mac_tc": (1, 0), "ip_v3": (0, 1), "ntt_q": (0, 15, 79, 7), "nvtx": (1, 0)}.items():
+    for name, vals in {"mac_tc": (1, 0), "ip_v3": (0, 1), "ntt_q": (0, 15, 79, 7), "nvtx": (1, 0), "giant_multi": (0, 1)}.items():
         for v in vals:
             G.set_option(name, v)
             assert G.get_option(name) == v
-    for name, bad in (("mac_tc", 2), ("ip_v3", -1), ("ntt_q", 256), ("nvtx", 5), ("no_such_option", 0)):
+    for name, bad in (("mac_tc", 2), ("ip_v3", -1), ("ntt_q", 256), ("nvtx", 5), ("giant_multi", 2), ("no_such_option", 0)):
         with pytest.raises(Exception):
             G.set_option(name, bad)
     with pytest.raises(Exception):
