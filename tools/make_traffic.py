@@ -46,9 +46,10 @@ out = {
     # Eq. 1 sums of dense1: baby steps + input (t1 x B x 2) and plaintexts (t1 x t2) read, t2 x B x 2 written, per row
     "k_bsgs_mac_mma": entry("macmma", (64 * B * 2 + 64 * 8 + 8 * B * 2) * ne * N8,
                             "dense1 chunk, B = 256, t1 = 64, t2 = 8, all 10 QP rows (one launch)"),
-    # giant-step IP: ModUp words (nd x ne), key, accumulator read + written (2 x ne), sigma_g(w.c0) addend (ne)
-    "k_ks_ip_giant": entry("ipgiant", (B * nd * ne + nd * 2 * ne + 2 * 2 * B * ne + B * ne) * N8,
-                           "B = 256, nl = 8 (10 QP rows), one giant step of dense1, 4 batch slices"),
+    # giant-step IP, 4 steps in one accumulator pass: per step ModUp words (nd x ne), key and the sigma_g(w.c0)
+    # addend (ne); the accumulator read + written once (2 x 2 x ne)
+    "k_ks_ip_giant": entry("ipgiant", (4 * (B * nd * ne + nd * 2 * ne + B * ne) + 2 * 2 * B * ne) * N8,
+                           "B = 256, nl = 8 (10 QP rows), giant steps 1-4 of dense1 in one pass"),
     # digits of a giant step: the 8 data limbs + 2 remainder words read per ciphertext, 8 digit words written
     "k_ks_digits": entry("digits", (B * nl + B * K + B * nl) * N8,
                          "giant-step digits (both sizes in one launch, QP input: fused ModDown), B = 256"),

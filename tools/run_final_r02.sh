@@ -11,7 +11,7 @@ timeout 900 python bench.py --impl reference --steps 1 --warmup 0 > $O/bench_ref
 P="python tools/profile_forward.py --mode forward --batch 256"
 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_forward_b256.csv $P > $O/ncu_launches.log 2>&1
 # name:tag:launch-skip (function base names; skip picks the dense1 instance of each)
-for spec in "k_ks_ip_mma3:ipmma3:0" "k_ks_modup:modup2:3" "k_bsgs_mac_mma:macmma:0" "k_ks_digits:digits:1" "k_ks_ip_giant:ipgiant:0"; do
+for spec in "k_ks_ip_mma3:ipmma3:0" "k_ks_modup_c:modup2:3" "k_bsgs_mac_mma:macmma:0" "k_ks_digits:digits:1" "k_ks_ip_giant_multi:ipgiant:0"; do
   IFS=: read k tag skip <<< "$spec"
   ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base function -k "$k" --launch-skip $skip -c 1 -o $O/prof_$tag $P > $O/ncu_$tag.log 2>&1
   ncu -i $O/prof_$tag.ncu-rep --page raw --csv > $O/prof_${tag}_raw.csv 2>&1

@@ -1,6 +1,10 @@
+O=gpurun_out/final
 P="python tools/profile_forward.py --mode forward --batch 256"
-ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base function -k k_ks_ip_giant_multi -c 1 -o gpurun_out/prof_ipgm $P > gpurun_out/ncu_ipgm.log 2>&1
-ncu -i gpurun_out/prof_ipgm.ncu-rep --page raw --csv > gpurun_out/prof_ipgm_raw.csv 2>&1
-ncu -i gpurun_out/prof_ipgm.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_ipgm_source.csv 2>&1
-gzip -f gpurun_out/prof_ipgm_source.csv
-rm -f gpurun_out/prof_ipgm.ncu-rep
+for spec in "k_ks_modup_c:modup2:3" "k_ks_ip_giant_multi:ipgiant:0"; do
+  IFS=: read k tag skip <<< "$spec"
+  ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base function -k "$k" --launch-skip $skip -c 1 -o $O/prof_$tag $P > $O/ncu_$tag.log 2>&1
+  ncu -i $O/prof_$tag.ncu-rep --page raw --csv > $O/prof_${tag}_raw.csv 2>&1
+  ncu -i $O/prof_$tag.ncu-rep --page source --csv --print-source sass > $O/prof_${tag}_source.csv 2>&1
+  gzip -f $O/prof_${tag}_source.csv
+  rm -f $O/prof_$tag.ncu-rep
+done
