@@ -179,9 +179,14 @@ k_bsgs_mac_int(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_
 // bank-conflict free), keeps its plaintext tile [8][t1][MACM_XT] resident (read once per launch), and
 // writes W through shared memory as coalesced 64-byte rows.  Each thread copies the same (b, x) for
 // MACM_JC consecutive baby steps, so fill addresses are one pointer plus a constant stride.
-#define MACM_XT 8
+#ifndef MACM_XT
+#define MACM_XT 16   // coefficients per CTA: 16 = 128-byte rows per (baby step, ciphertext) from HBM, 512 threads, one CTA
+                     // per SM; 8 = 64-byte rows, 256 threads, two CTAs per SM (A/B in DESIGN.md section 5)
+#endif
 #define MACM_JC 16
-#define MACM_ST 3
+#ifndef MACM_ST
+#define MACM_ST 3   // 4 stages (208 KiB): 26.2 vs 23.0 ms per chunk
+#endif
 #define MACM_THREADS (32 * MACM_XT)
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem)
@@ -196,11 +201,29 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // swizzled word index of V element (jj, bb, x) in a stage and of pt element (k, j, x) in the tile
 __device__ __forceinline__ int macm_vidx(int jj, int bb, int x)
 {
+#if MACM_XT == 8
     return (jj * 16 + bb) * MACM_XT + (x ^ (((jj & 3) << 1) | ((bb >> 1) & 1)));
+#else   // rows of 16 words = all 16 banks: the 16 (tig, gid & 3) lanes of a half-warp need 16 different columns
+    return (jj * 16 + bb) * MACM_XT + (x ^ (((jj & 3) << 2) | (bb & 3)));
+#endif
 }
 __device__ __forceinline__ int macm_pidx(int k, int j, int t1, int x)
 {
+#if MACM_XT == 8
     return (k * t1 + j) * MACM_XT + (x ^ (((k & 3) << 1) | ((j >> 1) & 1)));
+#else
+    return (k * t1 + j) * MACM_XT + (x ^ (((k & 3) << 2) | (j & 3)));
+#endif
+}
+
+// column swizzle of output row (k, bb) in the staging tile
+__device__ __forceinline__ int macm_osw(int row)
+{
+#if MACM_XT == 8
+    return (((row >> 5) & 3) << 1) | ((row >> 1) & 1);
+#else
+    return (((row >> 5) & 3) << 2) | (row & 3);
+#endif
 }
 
 template <bool INT>
@@ -297,7 +320,11 @@ __device__ __forceinline__ void macm_body(const DCtx* __restrict__ dc, const u64
     constexpr int KS = MACM_JC / 4;                          // k-steps per stage
     double S[NS][4];
     const int x = warp;
+#if MACM_XT == 8
     const int xsw = x ^ (((gid & 3) << 1) | ((tig >> 1) & 1));   // pt swizzle (j >> 1 & 1 == tig >> 1 & 1)
+#else
+    const int xsw = x ^ (((gid & 3) << 2) | tig);                // pt swizzle (j & 3 == tig)
+#endif
     const u64* Pw = Ps + (size_t)gid * t1p * MACM_XT + xsw;
     int it = 0;
     for (int bt = 0; bt < nbt; ++bt) {
@@ -376,7 +403,7 @@ __device__ __forceinline__ void macm_body(const DCtx* __restrict__ dc, const u64
             }
             const int bb = gid + 8 * (e >> 1), k = 2 * tig + (e & 1);
             const int row = k * 16 + bb;
-            Os[row * MACM_XT + (x ^ ((((row >> 5) & 3) << 1) | ((row >> 1) & 1)))] = u;
+            Os[row * MACM_XT + (x ^ macm_osw(row))] = u;
         }
         __syncthreads();
         // coalesced write: row (k, bb) of MACM_XT words
@@ -385,14 +412,14 @@ __device__ __forceinline__ void macm_body(const DCtx* __restrict__ dc, const u64
             const int bb = row % 16, k = row / 16, b = bt * 16 + bb;
             if (b < batch && k0 + k < t2)
                 wout[((size_t)(k0 + k) * batch + b) * ctw + ((size_t)c * nlx + l) * n + x0 + xx] =
-                    Os[row * MACM_XT + (xx ^ ((((row >> 5) & 3) << 1) | ((row >> 1) & 1)))];
+                    Os[row * MACM_XT + (xx ^ macm_osw(row))];
         }
     }
     cp_async_wait<0>();
 }
 
 // one launch for both limb classes (the 3-product FP rows and the 6-product 60-bit rows share the SMs)
-__global__ void __launch_bounds__(MACM_THREADS, 2)
+__global__ void __launch_bounds__(MACM_THREADS, MACM_XT == 8 ? 2 : 1)
 k_bsgs_mac_mma(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_nl, const u64* __restrict__ v0,
                size_t v0_stride, const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl,
                int qp)
