@@ -86,6 +86,10 @@ __device__ __forceinline__ void ip3_body(const DCtx* __restrict__ dc, const u64*
     constexpr int KPW = IP3_KT / (IP3_THREADS / 32);        // coefficients per warp
     constexpr int KX = INT ? S::KI : S::KF;                 // contraction length
     constexpr int NKB = (KX + 3) / 4;                       // MMA k-steps
+    // FP rows with two spare K slots (nd = 1, 3, 5): the addend P c0 rides in them as one more "digit" -- A = the
+    // staged c0 slice (what the dead lanes read anyway), B = (P mod q) pre-multiplied like a key word, columns
+    // c = 0 only -- instead of a Shoup product per (ciphertext, coefficient) in the epilogue
+    constexpr bool ADDK = !INT && (4 * NKB - KX) >= 2;
     u64* Kw = sm;                                           // key tile (FP: double2 [k][kidx][n]; INT: u64)
     u64* Dst = Kw + S::KEYW;
     u64* Os = Dst + IP3_ST * SD;
@@ -178,6 +182,17 @@ __device__ __forceinline__ void ip3_body(const DCtx* __restrict__ dc, const u64*
         ksh[kb] = INT ? 20 * (kidx % 3) : ((kidx & 1) ? 0 : 23);
     }
     const double2* Kd = reinterpret_cast<const double2*>(Kw);
+    // ADDK: the B values of this lane's spare K slot (last k-step, K index KX + part) for columns gid and 8 + gid
+    double2 addb0 = make_double2(0.0, 0.0), addb1 = make_double2(0.0, 0.0);
+    if constexpr (ADDK) {
+        const int part = 4 * (NKB - 1) + tig - KX;             // 0: pairs with the high part of c0, 1: with the low part
+        if (part >= 0 && part < 2 && !prow) {
+            const u64 pm = dc->pmod[i], w = part == 0 ? mulmod(pm, Pr.w23, Pr) : pm;
+            const double2 val = make_double2((double)(w & m23), (double)(w >> 23));
+            if ((gid & 1) == 0 && (gid >> 1) < G) addb0 = val;             // column n = (g, c) = (n >> 1, n & 1)
+            if ((gid & 1) == 0 && ((8 + gid) >> 1) < G) addb1 = val;
+        }
+    }
     for (int bt = 0; bt < nbt; ++bt) {
         ip3_wait<IP3_ST - 2>();
         __syncthreads();                                   // stage bt landed (and the key tile, at bt = 0)
@@ -210,7 +225,8 @@ __device__ __forceinline__ void ip3_body(const DCtx* __restrict__ dc, const u64*
                     const u64 a1 = Ds[j * JS + ip3_pos(gid + 8, kk)];
                     const int kidx = 4 * kb + tig;          // dead lanes' positions stay inside shared memory
                     const double2 v0 = Kd[ip3_kpos<S::KF>(kk, kidx, gid)], v1 = Kd[ip3_kpos<S::KF>(kk, kidx, 8 + gid)];
-                    const double2 b0 = live ? v0 : make_double2(0.0, 0.0), b1 = live ? v1 : make_double2(0.0, 0.0);
+                    const double2 b0 = live ? v0 : ((ADDK && kb == NKB - 1) ? addb0 : make_double2(0.0, 0.0)),
+                                  b1 = live ? v1 : ((ADDK && kb == NKB - 1) ? addb1 : make_double2(0.0, 0.0));
                     const double x0 = p2d((a0 >> sh) & mk), x1 = p2d((a1 >> sh) & mk);
                     dmma16884(Sa[kq][0][0], x0, x1, b0.x);
                     dmma16884(Sa[kq][1][0], x0, x1, b0.y);
@@ -221,10 +237,11 @@ __device__ __forceinline__ void ip3_body(const DCtx* __restrict__ dc, const u64*
 #pragma unroll
             for (int kq = 0; kq < KPW; ++kq) {
                 const int kk = warp * KPW + kq;
-                double addd[2];                            // P c0 of this thread's two ciphertexts
+                double addd[2];                            // P c0 of this thread's two ciphertexts (ADDK: in S0, S1)
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
-                    addd[h] = prow ? 0.0 : (double)csub(shoup_mul(As[ip3_pos(gid + 8 * h, kk)], Pm, Pm_sh, Pr.q), Pr.q);
+                    addd[h] = (ADDK || prow) ? 0.0
+                                             : (double)csub(shoup_mul(As[ip3_pos(gid + 8 * h, kk)], Pm, Pm_sh, Pr.q), Pr.q);
                 // output (b = gid + 8 h, column 8 t + 2 tig + c) -> Os[(g = 4 t + tig, c)][b][kk ^ ((b + 4 g) & 15)]:
                 // two base addresses per thread (h), the (t, c) offsets are immediates
                 u64* ob[2];

@@ -179,15 +179,13 @@ k_bsgs_mac_int(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_
 // bank-conflict free), keeps its plaintext tile [8][t1][MACM_XT] resident (read once per launch), and
 // writes W through shared memory as coalesced 64-byte rows.  Each thread copies the same (b, x) for
 // MACM_JC consecutive baby steps, so fill addresses are one pointer plus a constant stride.
-#ifndef MACM_XT
-#define MACM_XT 16   // coefficients per CTA: 16 = 128-byte rows per (baby step, ciphertext) from HBM, 512 threads, one CTA
-                     // per SM; 8 = 64-byte rows, 256 threads, two CTAs per SM (A/B in DESIGN.md section 5)
-#endif
+// XT = coefficients per CTA (template parameter): 16 = 128-byte rows per (baby step, ciphertext) from HBM, 512 threads,
+// one CTA per SM -- faster for the large batched launches (B = 256: 23.7 -> 23.0 ms per chunk); 8 = 64-byte rows,
+// 256 threads, two CTAs per SM -- faster for small batches (B = 128 stacks +3 %, single-ciphertext latency +5 %)
 #define MACM_JC 16
 #ifndef MACM_ST
 #define MACM_ST 3   // 4 stages (208 KiB): 26.2 vs 23.0 ms per chunk
 #endif
-#define MACM_THREADS (32 * MACM_XT)
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem)
 {
@@ -199,38 +197,34 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
 // swizzled word index of V element (jj, bb, x) in a stage and of pt element (k, j, x) in the tile
+template <int XT>
 __device__ __forceinline__ int macm_vidx(int jj, int bb, int x)
 {
-#if MACM_XT == 8
-    return (jj * 16 + bb) * MACM_XT + (x ^ (((jj & 3) << 1) | ((bb >> 1) & 1)));
-#else   // rows of 16 words = all 16 banks: the 16 (tig, gid & 3) lanes of a half-warp need 16 different columns
-    return (jj * 16 + bb) * MACM_XT + (x ^ (((jj & 3) << 2) | (bb & 3)));
-#endif
+    if constexpr (XT == 8) return (jj * 16 + bb) * XT + (x ^ (((jj & 3) << 1) | ((bb >> 1) & 1)));
+    // rows of 16 words = all 16 banks: the 16 (tig, gid & 3) lanes of a half-warp need 16 different columns
+    else return (jj * 16 + bb) * XT + (x ^ (((jj & 3) << 2) | (bb & 3)));
 }
+template <int XT>
 __device__ __forceinline__ int macm_pidx(int k, int j, int t1, int x)
 {
-#if MACM_XT == 8
-    return (k * t1 + j) * MACM_XT + (x ^ (((k & 3) << 1) | ((j >> 1) & 1)));
-#else
-    return (k * t1 + j) * MACM_XT + (x ^ (((k & 3) << 2) | (j & 3)));
-#endif
+    if constexpr (XT == 8) return (k * t1 + j) * XT + (x ^ (((k & 3) << 1) | ((j >> 1) & 1)));
+    else return (k * t1 + j) * XT + (x ^ (((k & 3) << 2) | (j & 3)));
 }
 
 // column swizzle of output row (k, bb) in the staging tile
+template <int XT>
 __device__ __forceinline__ int macm_osw(int row)
 {
-#if MACM_XT == 8
-    return (((row >> 5) & 3) << 1) | ((row >> 1) & 1);
-#else
-    return (((row >> 5) & 3) << 2) | (row & 3);
-#endif
+    if constexpr (XT == 8) return (((row >> 5) & 3) << 1) | ((row >> 1) & 1);
+    else return (((row >> 5) & 3) << 2) | (row & 3);
 }
 
-template <bool INT>
+template <bool INT, int MACM_XT>
 __device__ __forceinline__ void macm_body(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_nl,
                                           const u64* __restrict__ v0, size_t v0_stride, const u64* __restrict__ vb,
                                           u64* __restrict__ wout, int t1, int t2, int batch, int nl, int qp, u64* msm)
 {
+    constexpr int MACM_THREADS = 32 * MACM_XT;
     constexpr int SV = MACM_JC * 16 * MACM_XT;               // words per stage
     constexpr int EPT = SV / MACM_THREADS;                   // words per thread per stage (= MACM_JC / 2)
     static_assert(MACM_THREADS / MACM_XT == 32 && EPT * 2 == MACM_JC, "fill mapping");
@@ -264,7 +258,7 @@ __device__ __forceinline__ void macm_body(const DCtx* __restrict__ dc, const u64
             const int i = i0 + h * MACM_THREADS;
             if (i >= 8 * t1p * MACM_XT) break;
             const int x = i % MACM_XT, j = (i / MACM_XT) % t1p, k = i / (MACM_XT * t1p);
-            Ps[macm_pidx(k, j, t1p, x)] = a[h];
+            Ps[macm_pidx<MACM_XT>(k, j, t1p, x)] = a[h];
         }
     }
     const size_t ctw = (size_t)2 * nlx * n, jstride = (size_t)batch * ctw;
@@ -287,12 +281,12 @@ __device__ __forceinline__ void macm_body(const DCtx* __restrict__ dc, const u64
         if (fast) {
             const u64* src = vb + ((size_t)(jb - 1) * batch + b) * ctw + foff;
 #pragma unroll
-            for (int h = 0; h < EPT; ++h) cp_async8(S + macm_vidx(fhalf * EPT + h, fbb, fx), src + h * jstride);
+            for (int h = 0; h < EPT; ++h) cp_async8(S + macm_vidx<MACM_XT>(fhalf * EPT + h, fbb, fx), src + h * jstride);
         } else {
 #pragma unroll
             for (int h = 0; h < EPT; ++h) {
                 const int j = jb + h;
-                u64* dst = S + macm_vidx(fhalf * EPT + h, fbb, fx);
+                u64* dst = S + macm_vidx<MACM_XT>(fhalf * EPT + h, fbb, fx);
                 if (b >= batch || j >= t1) {
                     *dst = 0;
                 } else if (j == 0) {
@@ -320,11 +314,8 @@ __device__ __forceinline__ void macm_body(const DCtx* __restrict__ dc, const u64
     constexpr int KS = MACM_JC / 4;                          // k-steps per stage
     double S[NS][4];
     const int x = warp;
-#if MACM_XT == 8
-    const int xsw = x ^ (((gid & 3) << 1) | ((tig >> 1) & 1));   // pt swizzle (j >> 1 & 1 == tig >> 1 & 1)
-#else
-    const int xsw = x ^ (((gid & 3) << 2) | tig);                // pt swizzle (j & 3 == tig)
-#endif
+    // pt swizzle: XT = 8: (j >> 1 & 1 == tig >> 1 & 1); XT = 16: (j & 3 == tig)
+    const int xsw = MACM_XT == 8 ? (x ^ (((gid & 3) << 1) | ((tig >> 1) & 1))) : (x ^ (((gid & 3) << 2) | tig));
     const u64* Pw = Ps + (size_t)gid * t1p * MACM_XT + xsw;
     int it = 0;
     for (int bt = 0; bt < nbt; ++bt) {
@@ -342,7 +333,7 @@ __device__ __forceinline__ void macm_body(const DCtx* __restrict__ dc, const u64
             for (int kq = 0; kq < KS; ++kq) {
                 const int jj = kq * 4 + tig;
                 const u64 bv = Pw[(size_t)(jc * MACM_JC + jj) * MACM_XT];
-                const u64 a0 = Sv[macm_vidx(jj, gid, x)], a1 = Sv[macm_vidx(jj, gid + 8, x)];
+                const u64 a0 = Sv[macm_vidx<MACM_XT>(jj, gid, x)], a1 = Sv[macm_vidx<MACM_XT>(jj, gid + 8, x)];
                 if constexpr (!INT) {
                     const u64 m = (1ULL << 23) - 1;
                     const double bh = p2d(bv >> 23), bl = p2d(bv & m);
@@ -403,7 +394,7 @@ __device__ __forceinline__ void macm_body(const DCtx* __restrict__ dc, const u64
             }
             const int bb = gid + 8 * (e >> 1), k = 2 * tig + (e & 1);
             const int row = k * 16 + bb;
-            Os[row * MACM_XT + (x ^ macm_osw(row))] = u;
+            Os[row * MACM_XT + (x ^ macm_osw<MACM_XT>(row))] = u;
         }
         __syncthreads();
         // coalesced write: row (k, bb) of MACM_XT words
@@ -412,14 +403,15 @@ __device__ __forceinline__ void macm_body(const DCtx* __restrict__ dc, const u64
             const int bb = row % 16, k = row / 16, b = bt * 16 + bb;
             if (b < batch && k0 + k < t2)
                 wout[((size_t)(k0 + k) * batch + b) * ctw + ((size_t)c * nlx + l) * n + x0 + xx] =
-                    Os[row * MACM_XT + (xx ^ macm_osw(row))];
+                    Os[row * MACM_XT + (xx ^ macm_osw<MACM_XT>(row))];
         }
     }
     cp_async_wait<0>();
 }
 
 // one launch for both limb classes (the 3-product FP rows and the 6-product 60-bit rows share the SMs)
-__global__ void __launch_bounds__(MACM_THREADS, MACM_XT == 8 ? 2 : 1)
+template <int XT>
+__global__ void __launch_bounds__(32 * XT, XT == 8 ? 2 : 1)
 k_bsgs_mac_mma(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_nl, const u64* __restrict__ v0,
                size_t v0_stride, const u64* __restrict__ vb, u64* __restrict__ wout, int t1, int t2, int batch, int nl,
                int qp)
@@ -427,14 +419,14 @@ k_bsgs_mac_mma(const DCtx* __restrict__ dc, const u64* __restrict__ pts, int pt_
     extern __shared__ u64 msm[];
     const int l = blockIdx.y;
     const u64 q = dc->p[ext_prime_of(l, nl, dc->n_data)].q;
-    if (prime_class(q) == PC_FP) macm_body<false>(dc, pts, pt_nl, v0, v0_stride, vb, wout, t1, t2, batch, nl, qp, msm);
-    else macm_body<true>(dc, pts, pt_nl, v0, v0_stride, vb, wout, t1, t2, batch, nl, qp, msm);
+    if (prime_class(q) == PC_FP) macm_body<false, XT>(dc, pts, pt_nl, v0, v0_stride, vb, wout, t1, t2, batch, nl, qp, msm);
+    else macm_body<true, XT>(dc, pts, pt_nl, v0, v0_stride, vb, wout, t1, t2, batch, nl, qp, msm);
 }
 
-static size_t mac_mma_smem(int t1)
+static size_t mac_mma_smem(int t1, int xt)
 {
     const int t1p = (t1 + MACM_JC - 1) / MACM_JC * MACM_JC;
-    return sizeof(u64) * ((size_t)8 * t1p * MACM_XT + (size_t)MACM_ST * MACM_JC * 16 * MACM_XT + 8 * 16 * MACM_XT);
+    return sizeof(u64) * ((size_t)8 * t1p * xt + (size_t)MACM_ST * MACM_JC * 16 * xt + 8 * 16 * xt);
 }
 
 void bsgs_mac(const Launch& L, const uint64_t* pts, int pt_nl, const uint64_t* v0, size_t v0_stride,
@@ -453,7 +445,7 @@ void bsgs_mac(const Launch& L, const uint64_t* pts, int pt_nl, const uint64_t* v
         return e ? atoi(e) : 1;
     }();
 
-    if (use_mma && t1 <= 256 && n >= MACM_XT) {
+    if (use_mma && t1 <= 256 && n >= 16) {
         if (L.probe && L.probe->kind == PROBE_ALL) {
             // per row: B x 2 components x t1 x t2 x N modular MACs, 3 (FP class) or 6 (60-bit) exact
             // split products each; bytes: baby steps + input read, plaintexts read, W written
@@ -466,10 +458,23 @@ void bsgs_mac(const Launch& L, const uint64_t* pts, int pt_nl, const uint64_t* v
                     ((double)t1 * batch * 2 + (double)t1 * t2 + (double)t2 * batch * 2) * n * 8.0;
             }
         }
-        const size_t smem = mac_mma_smem(t1);
-        allow_smem(k_bsgs_mac_mma, smem);
-        const dim3 grid(n / MACM_XT, nlx, 2 * ((t2 + 7) / 8));
-        { ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_mma"); k_bsgs_mac_mma<<<grid, MACM_THREADS, smem, L.st>>>(L.dc, pts, pt_nl, v0, v0_stride, vbaby, wout, t1, t2, batch, nl, qp ? 1 : 0); }
+        // 16 coefficients per CTA for the large batched launches, 8 below (see the XT note above)
+        static const int xt_batch = [] {
+            const char* e = getenv("CKKS_MAC_XT16_BATCH");
+            return e ? atoi(e) : 192;
+        }();
+        ProbeScope ps_(L.probe, L.st, "k_bsgs_mac_mma");
+        if (batch >= xt_batch && mac_mma_smem(t1, 16) <= 227 * 1024) {   // (t1 <= 112 fits the 227 KiB)
+            const size_t smem = mac_mma_smem(t1, 16);
+            allow_smem(k_bsgs_mac_mma<16>, smem);
+            k_bsgs_mac_mma<16><<<dim3(n / 16, nlx, 2 * ((t2 + 7) / 8)), 512, smem, L.st>>>(
+                L.dc, pts, pt_nl, v0, v0_stride, vbaby, wout, t1, t2, batch, nl, qp ? 1 : 0);
+        } else {
+            const size_t smem = mac_mma_smem(t1, 8);
+            allow_smem(k_bsgs_mac_mma<8>, smem);
+            k_bsgs_mac_mma<8><<<dim3(n / 8, nlx, 2 * ((t2 + 7) / 8)), 256, smem, L.st>>>(
+                L.dc, pts, pt_nl, v0, v0_stride, vbaby, wout, t1, t2, batch, nl, qp ? 1 : 0);
+        }
         check_launch("bsgs_mac_mma");
         if (L.counter) *L.counter += 1;
         return;
