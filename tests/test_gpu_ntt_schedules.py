@@ -95,3 +95,20 @@ def test_nvtx_ranges_do_not_change_results():
         check(got, out, OP.oracle_forwards(spec, range(B)))
     finally:
         G.set_option("nvtx", old)
+
+
+@pytest.mark.parametrize("giant_multi", [0, 1])
+def test_giant_step_accumulation_forms(giant_multi):
+    """Double-hoisted forward with the giant steps accumulated per step (k_ks_ip_giant, option giant_multi = 0) and in
+    one pass per 4 steps (k_ks_ip_giant_multi, the default: Karatsuba split products summed over the steps, one
+    reduction per ciphertext): t2 = 8 giant tiles (7 steps = passes of 4 + 3) on the small ring, B = 37 in chunks of
+    20 (ragged batch slices), every ciphertext vs the oracle."""
+    old = G.get_option("giant_multi")
+    G.set_option("giant_multi", giant_multi)
+    try:
+        B, mb = 37, 20
+        spec = {"kind": "dense", "cfg": SMALL, "batch": B, "activation": "square", "hoisting": 2, "x": 0}
+        _, got, out = gpu_forward(spec, B, mb)
+        check(got, out, OP.oracle_forwards(spec, range(B)))
+    finally:
+        G.set_option("giant_multi", old)
