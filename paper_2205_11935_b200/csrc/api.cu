@@ -645,6 +645,7 @@ ckks_status ckks_ctx_create(const ckks_params* p, void* d_tables, void* d_keys, 
             P.w20 = (1ULL << 20) % q;
             P.w23 = (1ULL << 23) % q;
             P.w40 = (1ULL << 40) % q;
+            P.mu90 = q >= (1ULL << 59) ? (u64)((((u128)1) << 90) / q) : 0;
             P.qinv_d = 1.0 / (double)q;
             P.w23q = (double)P.w23 / (double)q;
             // W[idx] = psi^{brev(idx)} (stage s = floor(log2 idx), block idx - 2^s), stored at the

@@ -23,6 +23,7 @@ struct DPrime {
     u64 one_sh;          // floor(2^64 / q): Shoup companion of 1
     u64 r64, r64_sh;     // 2^64 mod q and companion
     u64 w20, w23, w40;   // 2^20, 2^23, 2^40 mod q (split-operand recombination, k_ipmma3.cu)
+    u64 mu90;            // floor(2^90 / q) for q >= 2^59 (< 2^32: one-word Barrett of values < 2^89), else 0
     double qinv_d;       // fl(1 / q)
     double w23q;         // fl(w23 / q)
 };
@@ -79,6 +80,16 @@ __device__ __forceinline__ u64 reduce128(u64 hi, u64 lo, const DPrime& P)
     u64 s = a + b;                                 // [0, 4q) < 2^63
     s = csub(s, P.q2);
     return csub(s, P.q);
+}
+
+// (hi, lo) < 2^89 -> [0, q) for q in [2^59, 2^61): one-word Barrett.  Th = T >> 58 < 2^31, qe = (Th mu90) >> 32 is
+// within 3 of floor(T / q) from below, so T - qe q (mod 2^64) is in [0, 4q)
+__device__ __forceinline__ u64 reduce89(u64 hi, u64 lo, const DPrime& P)
+{
+    const u32 th = (u32)((hi << 6) | (lo >> 58));
+    const u32 qe = (u32)(((u64)th * (u32)P.mu90) >> 32);
+    const u64 r = lo - (u64)qe * P.q;
+    return csub(csub(r, P.q2), P.q);
 }
 
 __device__ __forceinline__ u64 mulmod(u64 a, u64 b, const DPrime& P)

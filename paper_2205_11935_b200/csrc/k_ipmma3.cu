@@ -310,7 +310,8 @@ __device__ __forceinline__ void ip3_body(const DCtx* __restrict__ dc, const u64*
                         u64 lo = s0 + a1v, hi = (s1 >> 44) + (s2 >> 24) + (lo < a1v ? 1 : 0);
                         lo += a2v;
                         hi += (lo < a2v ? 1 : 0);
-                        const u64 u = addmod(reduce128(hi, lo, Pr), (c == 0) ? addw[e >> 1] : 0, Pr.q);
+                        const u64 red = Pr.mu90 ? reduce89(hi, lo, Pr) : reduce128(hi, lo, Pr);   // uniform per CTA
+                        const u64 u = addmod(red, (c == 0) ? addw[e >> 1] : 0, Pr.q);
                         Os[((g * 2 + c) * 16 + bl) * IP3_KT + (kk ^ ((bl + 4 * g) & 15))] = u;
                     }
             }
