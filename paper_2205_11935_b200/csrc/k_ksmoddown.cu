@@ -55,16 +55,35 @@ k_ks_moddown_ntt(const DCtx* __restrict__ dc, const u64* __restrict__ rem, int n
         if constexpr (K == 1) return centered_to(r0[k], dc->p[dc->n_data].q, dc->pmod[i], Pr);
         else return special_centered(dc, r0[k], r0[T::N + k], Pr, i);
     };
+    // K = 2 with every prime below 2^45: the centred remainder mod q_i in FP64 (as the digits' epilogue,
+    // k_ksdigits.cu): sign by the exact mixed-radix test, r = a + fmodmul(t, P_0) - [neg] (P mod q), |r| < 2 q
+    bool fpl = false;
+    if constexpr (K == 2) {
+        const u64 lim = 1ULL << 45;
+        fpl = Pr.q < lim && dc->p[dc->n_data].q < lim && dc->p[dc->n_data + 1].q < lim;
+    }
+    const double qd = (double)Pr.q;
+    const double p0 = dc->qmod[dc->n_data][i] > Pr.q / 2 ? -(double)(Pr.q - dc->qmod[dc->n_data][i])
+                                                         : (double)dc->qmod[dc->n_data][i];
+    const double p0q = p0 * Pr.qinv_d, pmd = (double)dc->pmod[i];
+    const u64 ha = dc->phalf_a, ht = dc->phalf_t;
+    auto ldf = [&](int k) {
+        const u64 a = r0[k], t = r0[T::N + k];
+        const bool neg = t > ht || (t == ht && a > ha);
+        return (u2d(a) + fmodmul(u2d(t), p0, p0q, qd)) - (neg ? pmd : 0.0);
+    };
     if constexpr (FUSE) {
         const u64* yy = y + (size_t)gb * y_stride + ((size_t)c * (nl + K) + i) * T::N;
         u64* oo = out + (size_t)gb * out_stride + ((size_t)c * nl + i) * T::N;
         const u64 pinv = dc->pinv[i], pinv_sh = dc->pinv_sh[i];
         auto st = [&](int k, u64 v) { oo[k] = csub(shoup_mul(yy[k] + Pr.q - v, pinv, pinv_sh, Pr.q), Pr.q); };
-        ntt_forward<T>(sm, Pr, twp(dc, i), ld, st);
+        if (fpl) T::forward_fp(sm, Pr, twp(dc, i), ldf, st);
+        else ntt_forward<T>(sm, Pr, twp(dc, i), ld, st);
     } else {
         u64* o = xo + (((size_t)gb * 2 + c) * (nl + K) + i) * T::N;
         auto st = [&](int k, u64 v) { o[k] = v; };
-        ntt_forward<T>(sm, Pr, twp(dc, i), ld, st);
+        if (fpl) T::forward_fp(sm, Pr, twp(dc, i), ldf, st);
+        else ntt_forward<T>(sm, Pr, twp(dc, i), ld, st);
     }
 }
 

@@ -89,6 +89,10 @@ __device__ __forceinline__ u64 fcanon(double v, double q, double qinv)
     return d2u(r);
 }
 
+// forward loaders may return the value as an exact signed double (|v| < 2 q) instead of a word in [0, 2q)
+__device__ __forceinline__ double ld_to_fp(u64 a) { return u2d(a); }
+__device__ __forceinline__ double ld_to_fp(double v) { return v; }
+
 template <int LOGN_, int NT_>
 struct NttCta {
     static constexpr int LOGN = LOGN_;
@@ -272,7 +276,7 @@ struct NttCta {
 #pragma unroll
                 for (int i = 0; i < (1 << K); ++i) {
                     const int idx = index<P>(tid, g, i);
-                    if constexpr (P == 0) x[g * (1 << K) + i] = u2d(ld(idx));
+                    if constexpr (P == 0) x[g * (1 << K) + i] = ld_to_fp(ld(idx));   // u64 in [0, 2q) or a signed double
                     else x[g * (1 << K) + i] = smd[swz(idx)];
                 }
             fwd_compute_fp<P, R>(x, tid, Wd, Wq, q, qinv);
