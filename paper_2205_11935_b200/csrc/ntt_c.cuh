@@ -78,6 +78,7 @@ struct ArFp {
     double q, qinv;
     __device__ __forceinline__ explicit ArFp(const DPrime& P) : q((double)P.q), qinv(1.0 / (double)P.q) {}
     __device__ __forceinline__ V in(u64 a) const { return u2d(a); }
+    __device__ __forceinline__ V in(double v) const { return v; }   // loaders may hand over a signed double
     template <bool FIRST>
     __device__ __forceinline__ void bfly(V& X, V& Y, const TW& w) const
     {
